@@ -1,0 +1,507 @@
+"""oracle -- CPU checkers for the QUOTA hot path (TEST INFRASTRUCTURE ONLY).
+
+Two checkers, both plain fp64 C++ behind ctypes:
+
+* ``Ref``    -- oracle/_ref/libquota_ref.so: the UNMODIFIED reference library
+  (/root/reference/proj/src/*.cpp compiled where it lies by oracle/Makefile)
+  plus the marshalling shim oracle/ref_capi.cpp.  This is R0.
+* ``Port``   -- oracle/_build/libquota_oracle.so: the restatement
+  oracle/quota_oracle.cpp (R1) with the north_star switches (per-token
+  activation scales, per-output-channel weights, SwiGLU, GQA).  Pinned to R0
+  bit-for-bit by tests/test_oracle_pin.py.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+``--impl reference`` leg may import this package.  The product
+(paper_2604_17320_b200) never does.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REF_SO = os.path.join(HERE, "_ref", "libquota_ref.so")
+PORT_SO = os.path.join(HERE, "_build", "libquota_oracle.so")
+
+_dp = C.POINTER(C.c_double)
+_ip = C.POINTER(C.c_int)
+_i8p = C.POINTER(C.c_int8)
+
+
+def _d(a):
+    return a.ctypes.data_as(_dp)
+
+
+def _i(a):
+    return a.ctypes.data_as(_ip)
+
+
+def _b(a):
+    return a.ctypes.data_as(_i8p)
+
+
+def f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+class OracleError(RuntimeError):
+    pass
+
+
+_ref_lib = None
+_port_lib = None
+
+
+def ref_lib():
+    global _ref_lib
+    if _ref_lib is None:
+        if not os.path.exists(REF_SO):
+            raise OracleError(f"{REF_SO} missing: run `make -C oracle ref`")
+        lib = C.CDLL(REF_SO)
+        lib.qref_last_error.restype = C.c_char_p
+        lib.qref_round_half_even.restype = C.c_double
+        lib.qref_round_half_even.argtypes = [C.c_double]
+        lib.qref_silu.restype = C.c_double
+        lib.qref_model_create.restype = C.c_void_p
+        lib.qref_model_create.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64]
+        lib.qref_model_free.argtypes = [C.c_void_p]
+        lib.qref_model_weight_checksum.restype = C.c_uint64
+        lib.qref_model_weight_checksum.argtypes = [C.c_void_p]
+        lib.qref_model_get_weight.argtypes = [C.c_void_p, C.c_int, C.c_int, _dp, C.c_int64]
+        lib.qref_model_set_weight.argtypes = [C.c_void_p, C.c_int, C.c_int, _dp, C.c_int64]
+        lib.qref_model_prepare_quant.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, _dp]
+        lib.qref_model_weight_codes.argtypes = [C.c_void_p, C.c_int, C.c_int, _i8p, _dp]
+        lib.qref_fit_act_scales.argtypes = [C.c_void_p, C.c_int, C.POINTER(_dp), _ip, _ip, C.c_int, _dp]
+        lib.qref_prefill.restype = C.c_void_p
+        lib.qref_prefill.argtypes = [C.c_void_p, C.c_int, _dp, C.c_int, C.c_int, _ip, C.c_char_p, _dp, C.c_int]
+        for n in ("qref_run_free", "qref_run_logits_rows", "qref_run_n_prunes"):
+            getattr(lib, n).argtypes = [C.c_void_p]
+        lib.qref_run_logits.argtypes = [C.c_void_p, _dp]
+        lib.qref_run_layout.argtypes = [C.c_void_p, _ip, _ip, _ip, C.c_int]
+        lib.qref_run_prune.argtypes = [C.c_void_p, C.c_int, _ip, _ip, _ip, C.c_int, _ip]
+        lib.qref_run_block_output.argtypes = [C.c_void_p, C.c_int, _dp, _ip]
+        lib.qref_run_kv.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, _i8p, _dp, _ip, _ip]
+        lib.qref_decode.argtypes = [C.c_void_p, _dp, _dp]
+        lib.qref_fnv1a64.restype = C.c_uint64
+        lib.qref_fnv1a64.argtypes = [_dp, C.c_int64]
+        lib.qref_layer_cost.restype = C.c_double
+        lib.qref_layer_cost.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int]
+        lib.qref_percentile.argtypes = [_dp, C.c_int, C.c_double, _dp]
+        _ref_lib = lib
+    return _ref_lib
+
+
+def port_lib():
+    global _port_lib
+    if _port_lib is None:
+        if not os.path.exists(PORT_SO):
+            raise OracleError(f"{PORT_SO} missing: run `make -C oracle port`")
+        lib = C.CDLL(PORT_SO)
+        lib.qo_last_error.restype = C.c_char_p
+        lib.qo_model_create.restype = C.c_void_p
+        lib.qo_model_create.argtypes = [_ip]
+        lib.qo_model_free.argtypes = [C.c_void_p]
+        lib.qo_model_set_weight.argtypes = [C.c_void_p, C.c_int, C.c_int, _dp, C.c_int64]
+        lib.qo_model_prepare.argtypes = [C.c_void_p, _dp]
+        lib.qo_model_weight_codes.argtypes = [C.c_void_p, C.c_int, C.c_int, _i8p, _dp]
+        lib.qo_prefill.restype = C.c_void_p
+        lib.qo_prefill.argtypes = [C.c_void_p, C.c_int, _dp, C.c_int, C.c_int, _ip, C.c_int, _ip, _dp, _dp,
+                                   C.c_int, C.c_int]
+        for n in ("qo_run_free", "qo_run_logits_rows", "qo_run_n_prunes"):
+            getattr(lib, n).argtypes = [C.c_void_p]
+        lib.qo_run_logits.argtypes = [C.c_void_p, _dp]
+        lib.qo_run_layout.argtypes = [C.c_void_p, _ip, _ip, _ip]
+        lib.qo_run_prune.argtypes = [C.c_void_p, C.c_int, _ip, _ip, _ip, _ip]
+        lib.qo_run_last_scores.argtypes = [C.c_void_p, _dp, _dp, _ip]
+        lib.qo_run_block_output.argtypes = [C.c_void_p, C.c_int, _dp, _ip]
+        lib.qo_run_kv.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, _i8p, _dp, _ip, _ip]
+        lib.qo_decode.argtypes = [C.c_void_p, _dp, _dp]
+        lib.qo_run_batch.argtypes = [C.c_void_p, C.c_int, C.c_int, C.POINTER(_dp), _ip, _ip, C.c_int, _ip, _dp,
+                                     _dp, _ip, C.c_int, C.c_int, C.POINTER(_dp), C.c_int, _dp]
+        _port_lib = lib
+    return _port_lib
+
+
+def _check(rc, lib, prefix):
+    if rc != 0:
+        msg = getattr(lib, prefix + "_last_error")().decode()
+        raise OracleError(msg)
+
+
+# ---------------------------------------------------------------- configs
+
+
+@dataclass
+class ModelCfg:
+    """Shape + semantic switches.  Defaults = reference R0."""
+
+    n_layers: int = 4
+    d_model: int = 256
+    n_heads: int = 4
+    n_kv_heads: int = 4
+    d_head: int = 64
+    d_ff: int = 1024
+    mlp: int = 0          # 0 SiLU (reference), 1 SwiGLU
+    act_mode: int = 0     # 0 static per-tensor (reference), 1 dynamic per-token
+    weight_axis: int = 2  # 1 PerRow (reference prepare_quant_env), 2 PerColumn
+    act_bits: int = 4
+    weight_bits: int = 4
+    kv_bits: int = 4
+
+    def as_array(self):
+        return np.array([self.n_layers, self.d_model, self.n_heads, self.n_kv_heads, self.d_head, self.d_ff,
+                         self.mlp, self.act_mode, self.weight_axis, self.act_bits, self.weight_bits,
+                         self.kv_bits], dtype=np.int32)
+
+    def is_reference_expressible(self):
+        return (self.mlp == 0 and self.n_kv_heads == self.n_heads and self.d_ff == 4 * self.d_model
+                and self.act_mode == 0)
+
+
+@dataclass
+class Recipe:
+    candidate_layers: list
+    keep_ratios: list
+    weights: tuple = (0.25, 0.45, 0.10, 0.20)  # recipe.hpp:10-14
+    v0: int = 144
+    quant_digest: str = "w4a4kv4-sym-rne"
+
+    def to_json(self):
+        import json
+        return json.dumps({"schema_version": 1, "candidate_layers": list(self.candidate_layers),
+                           "keep_ratios": list(self.keep_ratios),
+                           "metric_weights": {"mag": self.weights[0], "inter": self.weights[1],
+                                              "intra": self.weights[2], "quant": self.weights[3]},
+                           "v0": self.v0, "quant_digest": self.quant_digest})
+
+
+@dataclass
+class Weights:
+    """fp64 weights, reference orientation W[d_in x d_out] (y = x W)."""
+
+    layers: list = field(default_factory=list)  # dict(wq, wk, wv, wo, w1, w2, w3?, g1, g2)
+    head: np.ndarray = None
+    gf: np.ndarray = None
+
+
+@dataclass
+class RunResult:
+    logits: np.ndarray
+    visual: int
+    text: int
+    positions: np.ndarray
+    trace: list  # [(layer, budget, positions ndarray)]
+
+
+# ---------------------------------------------------------------- R0 (reference)
+
+
+class Ref:
+    """The unmodified reference (R0) through oracle/_ref/libquota_ref.so."""
+
+    def __init__(self, cfg: ModelCfg, seed: int = 1):
+        assert cfg.mlp == 0 and cfg.n_kv_heads == cfg.n_heads and cfg.d_ff == 4 * cfg.d_model
+        self.lib = ref_lib()
+        self.cfg = cfg
+        self.h = self.lib.qref_model_create(cfg.n_layers, cfg.n_heads, cfg.d_model, cfg.d_head, seed)
+        if not self.h:
+            raise OracleError(self.lib.qref_last_error().decode())
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.lib.qref_model_free(self.h)
+            self.h = None
+
+    def get(self, layer, which, shape):
+        out = np.empty(int(np.prod(shape)), dtype=np.float64)
+        _check(self.lib.qref_model_get_weight(self.h, layer, which, _d(out), out.size), self.lib, "qref")
+        return out.reshape(shape)
+
+    def weights(self) -> Weights:
+        c = self.cfg
+        d, f = c.d_model, c.d_ff
+        w = Weights()
+        for l in range(c.n_layers):
+            w.layers.append(dict(wq=self.get(l, 0, (d, d)), wk=self.get(l, 1, (d, d)), wv=self.get(l, 2, (d, d)),
+                                 wo=self.get(l, 3, (d, d)), w1=self.get(l, 4, (d, f)), w2=self.get(l, 5, (f, d)),
+                                 g1=self.get(l, 6, (d,)), g2=self.get(l, 7, (d,))))
+        w.head = self.get(-1, 0, (d, d))
+        w.gf = self.get(-1, 6, (d,))
+        return w
+
+    def set_weights(self, w: Weights):
+        names = ["wq", "wk", "wv", "wo", "w1", "w2", "g1", "g2"]
+        for l, lw in enumerate(w.layers):
+            for i, n in enumerate(names):
+                a = f64(lw[n]).ravel()
+                _check(self.lib.qref_model_set_weight(self.h, l, i, _d(a), a.size), self.lib, "qref")
+        a = f64(w.head).ravel()
+        _check(self.lib.qref_model_set_weight(self.h, -1, 0, _d(a), a.size), self.lib, "qref")
+        a = f64(w.gf).ravel()
+        _check(self.lib.qref_model_set_weight(self.h, -1, 6, _d(a), a.size), self.lib, "qref")
+
+    def checksum(self):
+        return self.lib.qref_model_weight_checksum(self.h)
+
+    def fit_act_scales(self, samples):
+        """fit_act_scales (calibrator.cpp:237-249); samples = [(emb, visual, text)]."""
+        embs = [f64(e) for e, _, _ in samples]
+        arr = (_dp * len(embs))(*[_d(e) for e in embs])
+        vis = np.array([v for _, v, _ in samples], dtype=np.int32)
+        txt = np.array([t for _, _, t in samples], dtype=np.int32)
+        out = np.empty(4 * self.cfg.n_layers + 1, dtype=np.float64)
+        _check(self.lib.qref_fit_act_scales(self.h, len(embs), arr, _i(vis), _i(txt), self.cfg.act_bits, _d(out)),
+               self.lib, "qref")
+        return out
+
+    def prepare(self, act_scales, weight_axis=None):
+        c = self.cfg
+        a = f64(act_scales)
+        ax = c.weight_axis if weight_axis is None else weight_axis
+        _check(self.lib.qref_model_prepare_quant(self.h, c.weight_bits, c.act_bits, c.kv_bits, ax, _d(a)),
+               self.lib, "qref")
+
+    def weight_codes(self, layer, which, shape, n_scales):
+        codes = np.empty(int(np.prod(shape)), dtype=np.int8)
+        scales = np.empty(n_scales, dtype=np.float64)
+        _check(self.lib.qref_model_weight_codes(self.h, layer, which, _b(codes), _d(scales)), self.lib, "qref")
+        return codes.reshape(shape), scales
+
+    def prefill(self, emb, visual, text, recipe: Recipe | None = None, quantized=True, res_bits=4, pos=None):
+        e = f64(emb)
+        p = None if pos is None else np.ascontiguousarray(pos, dtype=np.int32)
+        rj = recipe.to_json().encode() if recipe is not None else None
+        r = self.lib.qref_prefill(self.h, int(quantized), _d(e), visual, text, _i(p) if p is not None else None,
+                                  rj, None, res_bits)
+        if not r:
+            raise OracleError(self.lib.qref_last_error().decode())
+        return RefRun(self, r)
+
+
+class RefRun:
+    def __init__(self, owner, handle):
+        self.o = owner
+        self.lib = owner.lib
+        self.h = handle
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.lib.qref_run_free(self.h)
+            self.h = None
+
+    def result(self) -> RunResult:
+        rows = self.lib.qref_run_logits_rows(self.h)
+        lg = np.empty((rows, self.o.cfg.d_model), dtype=np.float64)
+        self.lib.qref_run_logits(self.h, _d(lg))
+        v, t = C.c_int(), C.c_int()
+        pos = np.empty(rows + 4096, dtype=np.int32)
+        _check(self.lib.qref_run_layout(self.h, C.byref(v), C.byref(t), _i(pos), pos.size), self.lib, "qref")
+        trace = []
+        for i in range(self.lib.qref_run_n_prunes(self.h)):
+            lay, bud, cnt = C.c_int(), C.c_int(), C.c_int()
+            ps = np.empty(1 << 16, dtype=np.int32)
+            _check(self.lib.qref_run_prune(self.h, i, C.byref(lay), C.byref(bud), _i(ps), ps.size, C.byref(cnt)),
+                   self.lib, "qref")
+            trace.append((lay.value, bud.value, ps[:cnt.value].copy()))
+        return RunResult(lg, v.value, t.value, pos[:v.value + t.value].copy(), trace)
+
+    def kv(self, layer, head, which):
+        rows = C.c_int()
+        _check(self.lib.qref_run_kv(self.h, layer, head, which, None, None, None, C.byref(rows)), self.lib, "qref")
+        dh = self.o.cfg.d_head
+        codes = np.empty((rows.value, dh), dtype=np.int8)
+        scales = np.empty(rows.value, dtype=np.float64)
+        pos = np.empty(rows.value, dtype=np.int32)
+        _check(self.lib.qref_run_kv(self.h, layer, head, which, _b(codes), _d(scales), _i(pos), C.byref(rows)),
+               self.lib, "qref")
+        return codes, scales, pos
+
+    def block_output(self, layer):
+        rows = C.c_int()
+        _check(self.lib.qref_run_block_output(self.h, layer, None, C.byref(rows)), self.lib, "qref")
+        out = np.empty((rows.value, self.o.cfg.d_model), dtype=np.float64)
+        _check(self.lib.qref_run_block_output(self.h, layer, _d(out), C.byref(rows)), self.lib, "qref")
+        return out
+
+    def decode(self, emb):
+        e = f64(emb)
+        out = np.empty(self.o.cfg.d_model, dtype=np.float64)
+        _check(self.lib.qref_decode(self.h, _d(e), _d(out)), self.lib, "qref")
+        return out
+
+
+# ---------------------------------------------------------------- R1 (restatement)
+
+
+class Port:
+    """The restatement (R1) through oracle/_build/libquota_oracle.so."""
+
+    def __init__(self, cfg: ModelCfg):
+        self.lib = port_lib()
+        self.cfg = cfg
+        a = cfg.as_array()
+        self.h = self.lib.qo_model_create(_i(a))
+        if not self.h:
+            raise OracleError(self.lib.qo_last_error().decode())
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.lib.qo_model_free(self.h)
+            self.h = None
+
+    def set_weights(self, w: Weights):
+        names = {"wq": 0, "wk": 1, "wv": 2, "wo": 3, "w1": 4, "w2": 5, "g1": 6, "g2": 7, "w3": 8}
+        for l, lw in enumerate(w.layers):
+            for n, i in names.items():
+                if n not in lw:
+                    continue
+                a = f64(lw[n]).ravel()
+                _check(self.lib.qo_model_set_weight(self.h, l, i, _d(a), a.size), self.lib, "qo")
+        a = f64(w.head).ravel()
+        _check(self.lib.qo_model_set_weight(self.h, -1, 0, _d(a), a.size), self.lib, "qo")
+        a = f64(w.gf).ravel()
+        _check(self.lib.qo_model_set_weight(self.h, -1, 6, _d(a), a.size), self.lib, "qo")
+
+    def prepare(self, act_scales=None):
+        a = None if act_scales is None else f64(act_scales)
+        _check(self.lib.qo_model_prepare(self.h, _d(a) if a is not None else None), self.lib, "qo")
+
+    def weight_codes(self, layer, which, shape, n_scales):
+        codes = np.empty(int(np.prod(shape)), dtype=np.int8)
+        scales = np.empty(n_scales, dtype=np.float64)
+        _check(self.lib.qo_model_weight_codes(self.h, layer, which, _b(codes), _d(scales)), self.lib, "qo")
+        return codes.reshape(shape), scales
+
+    def prefill(self, emb, visual, text, recipe: Recipe | None = None, quantized=True, res_bits=4, pos=None,
+                v0=None):
+        e = f64(emb)
+        p = None if pos is None else np.ascontiguousarray(pos, dtype=np.int32)
+        if recipe is not None:
+            lay = np.array(recipe.candidate_layers, dtype=np.int32)
+            kp = f64(recipe.keep_ratios)
+            wt = f64(recipe.weights)
+            n = len(lay)
+            r = self.lib.qo_prefill(self.h, int(quantized), _d(e), visual, text, _i(p) if p is not None else None,
+                                    n, _i(lay), _d(kp), _d(wt), recipe.v0 if v0 is None else v0, res_bits)
+        else:
+            r = self.lib.qo_prefill(self.h, int(quantized), _d(e), visual, text, _i(p) if p is not None else None,
+                                    0, None, None, None, 0, res_bits)
+        if not r:
+            raise OracleError(self.lib.qo_last_error().decode())
+        return PortRun(self, r)
+
+    def run_batch(self, embs, visual, text, recipe: Recipe, v0s, n_decode, dec_embs, n_threads, quantized=True,
+                  res_bits=4):
+        """prefill + n_decode steps per sequence, one sequence per thread; returns last logits."""
+        n = len(embs)
+        e = [f64(x) for x in embs]
+        de = [f64(x) for x in dec_embs]
+        ea = (_dp * n)(*[_d(x) for x in e])
+        da = (_dp * n)(*[_d(x) for x in de])
+        vis = np.array(visual, dtype=np.int32)
+        txt = np.array(text, dtype=np.int32)
+        lay = np.array(recipe.candidate_layers, dtype=np.int32)
+        kp = f64(recipe.keep_ratios)
+        wt = f64(recipe.weights)
+        v0 = np.array(v0s, dtype=np.int32)
+        out = np.empty((n, self.cfg.d_model), dtype=np.float64)
+        _check(self.lib.qo_run_batch(self.h, int(quantized), n, ea, _i(vis), _i(txt), len(lay), _i(lay), _d(kp),
+                                     _d(wt), _i(v0), res_bits, n_decode, da, n_threads, _d(out)), self.lib, "qo")
+        return out
+
+
+class PortRun:
+    def __init__(self, owner, handle):
+        self.o = owner
+        self.lib = owner.lib
+        self.h = handle
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.lib.qo_run_free(self.h)
+            self.h = None
+
+    def result(self) -> RunResult:
+        rows = self.lib.qo_run_logits_rows(self.h)
+        lg = np.empty((rows, self.o.cfg.d_model), dtype=np.float64)
+        self.lib.qo_run_logits(self.h, _d(lg))
+        v, t = C.c_int(), C.c_int()
+        pos = np.empty(rows + 4096, dtype=np.int32)
+        self.lib.qo_run_layout(self.h, C.byref(v), C.byref(t), _i(pos))
+        trace = []
+        for i in range(self.lib.qo_run_n_prunes(self.h)):
+            lay, bud, cnt = C.c_int(), C.c_int(), C.c_int()
+            ps = np.empty(1 << 16, dtype=np.int32)
+            self.lib.qo_run_prune(self.h, i, C.byref(lay), C.byref(bud), _i(ps), C.byref(cnt))
+            trace.append((lay.value, bud.value, ps[:cnt.value].copy()))
+        return RunResult(lg, v.value, t.value, pos[:v.value + t.value].copy(), trace)
+
+    def last_scores(self):
+        n = C.c_int()
+        if self.lib.qo_run_last_scores(self.h, None, None, C.byref(n)) != 0:
+            return None
+        m = np.empty((4, n.value), dtype=np.float64)
+        f = np.empty(n.value, dtype=np.float64)
+        self.lib.qo_run_last_scores(self.h, _d(m), _d(f), C.byref(n))
+        return m, f
+
+    def kv(self, layer, head, which):
+        rows = C.c_int()
+        _check(self.lib.qo_run_kv(self.h, layer, head, which, None, None, None, C.byref(rows)), self.lib, "qo")
+        dh = self.o.cfg.d_head
+        codes = np.empty((rows.value, dh), dtype=np.int8)
+        scales = np.empty(rows.value, dtype=np.float64)
+        pos = np.empty(rows.value, dtype=np.int32)
+        _check(self.lib.qo_run_kv(self.h, layer, head, which, _b(codes), _d(scales), _i(pos), C.byref(rows)),
+               self.lib, "qo")
+        return codes, scales, pos
+
+    def block_output(self, layer):
+        rows = C.c_int()
+        _check(self.lib.qo_run_block_output(self.h, layer, None, C.byref(rows)), self.lib, "qo")
+        out = np.empty((rows.value, self.o.cfg.d_model), dtype=np.float64)
+        _check(self.lib.qo_run_block_output(self.h, layer, _d(out), C.byref(rows)), self.lib, "qo")
+        return out
+
+    def decode(self, emb):
+        e = f64(emb)
+        out = np.empty(self.o.cfg.d_model, dtype=np.float64)
+        _check(self.lib.qo_decode(self.h, _d(e), _d(out)), self.lib, "qo")
+        return out
+
+
+# ---------------------------------------------------------------- synthetic inputs
+
+
+def synth_weights(cfg: ModelCfg, seed: int, std: float = 0.02) -> Weights:
+    """N(0, std) weights rounded to fp32 (so GPU and CPU see identical values)."""
+    rng = np.random.default_rng(seed)
+    d, f = cfg.d_model, cfg.d_ff
+    kvd = cfg.n_kv_heads * cfg.d_head
+
+    def g(*shape):
+        return rng.normal(0.0, std, size=shape).astype(np.float32).astype(np.float64)
+
+    w = Weights()
+    for _ in range(cfg.n_layers):
+        lw = dict(wq=g(d, d), wk=g(d, kvd), wv=g(d, kvd), wo=g(d, d), w1=g(d, f), w2=g(f, d),
+                  g1=np.ones(d), g2=np.ones(d))
+        if cfg.mlp == 1:
+            lw["w3"] = g(d, f)
+        w.layers.append(lw)
+    w.head = g(d, d)
+    w.gf = np.ones(d)
+    return w
+
+
+def synth_embeddings(n_tokens: int, d: int, seed: int, outlier_frac: float = 0.02, outlier_mult: float = 20.0):
+    """N(0,1) hidden states with a seeded set of outlier channels x outlier_mult (BASELINE.json configs)."""
+    rng = np.random.default_rng(seed)
+    x = rng.normal(0.0, 1.0, size=(n_tokens, d))
+    n_out = max(1, int(round(outlier_frac * d)))
+    ch = rng.choice(d, size=n_out, replace=False)
+    x[:, ch] *= outlier_mult
+    return x.astype(np.float32).astype(np.float64)

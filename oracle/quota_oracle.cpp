@@ -1,0 +1,862 @@
+// oracle/quota_oracle.cpp -- CPU restatement of the QUOTA hot path (R1).
+//
+// TEST INFRASTRUCTURE ONLY (the checker, never the product).  Only tests/,
+// __graft_entry__.smoke() and bench.py's cpu_baseline leg may load
+// oracle/_build/libquota_oracle.so.
+//
+// What it restates: the reference's quantized prefill with recipe-driven
+// visual-token pruning and the decode step over the quantized KV cache
+// (/root/reference/proj/src/model.cpp:315-562, selector.cpp:11-228,
+// quant.cpp:39-119, numeric.cpp:33-96).  Every routine cites the lines it
+// follows and keeps the reference's fp64 operation order, so with the switches
+// at their reference values it reproduces the reference bit for bit
+// (tests/test_oracle_pin.py checks logits, KV codes and prune traces against
+// oracle/_ref/libquota_ref.so, the unmodified reference).
+//
+// Switches (SURVEY.md §0.1 semantic deltas) beyond the reference:
+//   act_mode    0 = static per-tensor site scales (reference, model.cpp:31-33)
+//               1 = dynamic per-token scales (fake_quant_per_row, quant.cpp:108-110)
+//   weight_axis 1 = PerRow (reference prepare_quant_env, model.cpp:220-225)
+//               2 = PerColumn = per output channel (north_star; quant.cpp:15-31)
+//   mlp         0 = SiLU MLP w2(silu(w1 x)) (reference, model.cpp:429-437)
+//               1 = SwiGLU w2(silu(w1 x) * (w3 x))                  [unpinned]
+//   n_kv_heads  == n_heads: MHA (reference); < n_heads: GQA         [unpinned]
+//   d_ff        any (reference hard-codes 4*d_model, model.hpp:36)
+// The unpinned variants rest on the shared primitives plus the R0 self-check.
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+namespace {
+
+thread_local std::string g_err;
+
+constexpr double kEps = 1e-6;       // model.cpp:15
+constexpr double kRopeBase = 1e4;   // model.cpp:16
+constexpr double kNegInf = -1e30;   // model.cpp:17
+
+using Vec = std::vector<double>;
+
+// Row-major dense block.
+struct Mat {
+    int r = 0, c = 0;
+    Vec v;
+    Mat() = default;
+    Mat(int rows, int cols) : r(rows), c(cols), v(static_cast<size_t>(rows) * cols, 0.0) {}
+    double* row(int i) { return v.data() + static_cast<size_t>(i) * c; }
+    const double* row(int i) const { return v.data() + static_cast<size_t>(i) * c; }
+    double& at(int i, int j) { return v[static_cast<size_t>(i) * c + j]; }
+    double at(int i, int j) const { return v[static_cast<size_t>(i) * c + j]; }
+};
+
+// quant.cpp:39-45 -- ties to even, independent of the fenv rounding mode
+double rne(double x) {
+    double f = std::floor(x);
+    double d = x - f;
+    if (d > 0.5) return f + 1.0;
+    if (d < 0.5) return f;
+    return std::fmod(f, 2.0) == 0.0 ? f : f + 1.0;
+}
+
+// quant.cpp:64-66 -- scale from a group's max|x|; an all-zero group gets 1
+double scale_of(double max_abs, int bits) {
+    double qmax = static_cast<double>((1 << (bits - 1)) - 1);
+    return max_abs == 0.0 ? 1.0 : max_abs / qmax;
+}
+
+// quant.cpp:85-87 -- one code
+int8_t code_of(double x, double s, int bits) {
+    double qmax = static_cast<double>((1 << (bits - 1)) - 1);
+    double q = rne(x / s);
+    q = std::min(std::max(q, -qmax), qmax);
+    return static_cast<int8_t>(q);
+}
+
+// fake quant of a whole block with one scale (per-tensor site, model.cpp:31-33)
+void fq_tensor(Mat& x, double s, int bits) {
+    for (double& e : x.v) e = static_cast<double>(code_of(e, s, bits)) * s;
+}
+
+// fake_quant_per_row (quant.cpp:108-110 via fit_params PerRow, quant.cpp:47-69)
+void fq_rows(Mat& x, int bits) {
+    for (int i = 0; i < x.r; ++i) {
+        double m = 0.0;
+        double* p = x.row(i);
+        for (int j = 0; j < x.c; ++j) m = std::max(m, std::fabs(p[j]));  // (a > m) update, quant.cpp:58-60
+        double s = scale_of(m, bits);
+        for (int j = 0; j < x.c; ++j) p[j] = static_cast<double>(code_of(p[j], s, bits)) * s;
+    }
+}
+
+// numeric.cpp:33-46 -- out(i,j) = sum_k a(i,k) b(k,j), k ascending from 0.0.
+// Loop order i-k-j keeps each output's addition sequence identical.
+Mat matmul(const Mat& a, const Mat& b) {
+    if (a.c != b.r) throw std::invalid_argument("matmul shape mismatch");
+    Mat out(a.r, b.c);
+    for (int i = 0; i < a.r; ++i) {
+        double* o = out.row(i);
+        const double* ai = a.row(i);
+        for (int k = 0; k < a.c; ++k) {
+            const double av = ai[k];
+            const double* bk = b.row(k);
+            for (int j = 0; j < b.c; ++j) o[j] += av * bk[j];
+        }
+    }
+    return out;
+}
+
+// model.cpp:137-154
+Mat rms_rows(const Mat& x, const Vec& g) {
+    Mat out(x.r, x.c);
+    for (int i = 0; i < x.r; ++i) {
+        const double* p = x.row(i);
+        double ms = 0.0;
+        for (int j = 0; j < x.c; ++j) ms += p[j] * p[j];
+        ms /= static_cast<double>(x.c);
+        double inv = 1.0 / std::sqrt(ms + kEps);
+        double* o = out.row(i);
+        for (int j = 0; j < x.c; ++j) o[j] = p[j] * inv * g[j];
+    }
+    return out;
+}
+
+// model.cpp:156-168 -- interleaved pairs (2i, 2i+1)
+void rope(double* h, int n, int pos) {
+    const int half = n / 2;
+    for (int i = 0; i < half; ++i) {
+        double freq = std::pow(kRopeBase, -2.0 * static_cast<double>(i) / static_cast<double>(n));
+        double ang = static_cast<double>(pos) * freq;
+        double c = std::cos(ang), s = std::sin(ang);
+        double a = h[2 * i], b = h[2 * i + 1];
+        h[2 * i] = a * c - b * s;
+        h[2 * i + 1] = a * s + b * c;
+    }
+}
+
+// model.cpp:170-172
+double silu(double x) { return x / (1.0 + std::exp(-x)); }
+
+// numeric.cpp:84-96
+double percentile(Vec v, double p) {
+    if (v.empty()) throw std::invalid_argument("empty sample");
+    std::sort(v.begin(), v.end());
+    if (v.size() == 1) return v[0];
+    double h = p / 100.0 * static_cast<double>(v.size() - 1);
+    size_t lo = static_cast<size_t>(std::floor(h));
+    size_t hi = std::min(lo + 1, v.size() - 1);
+    double f = h - static_cast<double>(lo);
+    return v[lo] + f * (v[hi] - v[lo]);
+}
+
+// selector.cpp:70-84
+Vec robust_norm(const Vec& v) {
+    double p5 = percentile(v, 5.0), p95 = percentile(v, 95.0);
+    Vec out(v.size());
+    if (p95 - p5 < 1e-12) {
+        std::fill(out.begin(), out.end(), 0.5);
+        return out;
+    }
+    double inv = 1.0 / (p95 - p5);
+    for (size_t i = 0; i < v.size(); ++i) out[i] = std::clamp((v[i] - p5) * inv, 0.0, 1.0);
+    return out;
+}
+
+struct Cfg {
+    int n_layers, d_model, n_heads, n_kv_heads, d_head, d_ff, mlp, act_mode, weight_axis, act_bits,
+        weight_bits, kv_bits;
+};
+
+struct QW {
+    std::vector<int8_t> codes;  // d_in x d_out
+    Vec scales;                 // d_in (PerRow) or d_out (PerColumn)
+    Mat deq;
+};
+
+struct Layer {
+    Mat wq, wk, wv, wo, w1, w2, w3;
+    Vec g1, g2;
+    QW q[7];  // wq, wk, wv, wo, w1, w2, w3
+};
+
+struct Model {
+    Cfg cfg;
+    std::vector<Layer> layers;
+    Mat head;
+    Vec gf;
+    QW qhead;
+    Vec act;  // 4*L + 1 static site scales
+    bool prepared = false;
+};
+
+// fit_params(axis) + quantize + dequantize (quant.cpp:47-102)
+QW quant_weight(const Mat& w, int bits, int axis) {
+    QW q;
+    const int groups = axis == 1 ? w.r : w.c;
+    Vec mx(static_cast<size_t>(groups), 0.0);
+    for (int i = 0; i < w.r; ++i)
+        for (int j = 0; j < w.c; ++j) {
+            double a = std::fabs(w.at(i, j));
+            double& m = mx[static_cast<size_t>(axis == 1 ? i : j)];
+            if (a > m) m = a;
+        }
+    q.scales.resize(static_cast<size_t>(groups));
+    for (int g = 0; g < groups; ++g) q.scales[static_cast<size_t>(g)] = scale_of(mx[static_cast<size_t>(g)], bits);
+    q.codes.resize(w.v.size());
+    q.deq = Mat(w.r, w.c);
+    for (int i = 0; i < w.r; ++i)
+        for (int j = 0; j < w.c; ++j) {
+            double s = q.scales[static_cast<size_t>(axis == 1 ? i : j)];
+            int8_t c = code_of(w.at(i, j), s, bits);
+            q.codes[static_cast<size_t>(i) * w.c + j] = c;
+            q.deq.at(i, j) = static_cast<double>(c) * s;
+        }
+    return q;
+}
+
+// Per (token, head) KV row quantizer (kv_quantize, quant.cpp:117-119).
+struct KVHead {
+    std::vector<int8_t> k, v;  // rows x d_head
+    Vec ks, vs;                // rows
+};
+
+struct LayerCache {
+    std::vector<KVHead> heads;  // n_kv_heads
+    std::vector<int> pos;
+};
+
+struct Seq {
+    int visual = 0, text = 0;
+    std::vector<int> pos;
+};
+
+struct Recipe {
+    std::vector<int> layers;
+    Vec keeps;
+    double w[4];
+    int v0;
+    int res_bits;  // < 0: nullopt
+};
+
+struct Trace {
+    int layer, budget;
+    std::vector<int> positions;
+};
+
+struct Run {
+    Model* m;
+    bool quant;
+    Mat logits;
+    std::vector<LayerCache> cache;
+    Seq seq;
+    int next_pos = 0;
+    std::vector<Trace> trace;
+    std::vector<Mat> block_out;
+    // metrics of the most recent pruning layer (for kernel-level parity)
+    std::vector<Vec> last_metrics;  // mag, inter, intra, res
+    Vec last_fused;
+};
+
+void kv_quant_rows(const Mat& x, int bits, std::vector<int8_t>& codes, Vec& scales) {
+    for (int i = 0; i < x.r; ++i) {
+        double m = 0.0;
+        for (int j = 0; j < x.c; ++j) m = std::max(m, std::fabs(x.at(i, j)));
+        double s = scale_of(m, bits);
+        scales.push_back(s);
+        for (int j = 0; j < x.c; ++j) codes.push_back(code_of(x.at(i, j), s, bits));
+    }
+}
+
+// model.cpp:35-44 MaskRule
+bool allowed(const Seq& s, int qi, int ki) {
+    bool qv = qi < s.visual, kv = ki < s.visual;
+    if (qv) return kv;
+    if (kv) return true;
+    return s.pos[static_cast<size_t>(ki)] <= s.pos[static_cast<size_t>(qi)];
+}
+
+void site(Mat& x, const Model& m, int layer, int idx, bool quant) {
+    if (!quant) return;
+    if (m.cfg.act_mode == 0) {
+        fq_tensor(x, m.act[static_cast<size_t>(4 * layer + idx)], m.cfg.act_bits);
+    } else {
+        fq_rows(x, m.cfg.act_bits);
+    }
+}
+
+const Mat& W(const Layer& l, int which, bool quant) {
+    const Mat* fp[7] = {&l.wq, &l.wk, &l.wv, &l.wo, &l.w1, &l.w2, &l.w3};
+    return quant ? l.q[which].deq : *fp[which];
+}
+
+// MLP block on the post-prune rows (model.cpp:429-437)
+void mlp(Mat& x, const Model& m, int l, bool quant) {
+    const Layer& L = m.layers[static_cast<size_t>(l)];
+    Mat n2 = rms_rows(x, L.g2);
+    site(n2, m, l, 2, quant);
+    Mat mid = matmul(n2, W(L, 4, quant));
+    for (double& e : mid.v) e = silu(e);
+    if (m.cfg.mlp == 1) {
+        Mat up = matmul(n2, W(L, 6, quant));
+        for (size_t i = 0; i < mid.v.size(); ++i) mid.v[i] = mid.v[i] * up.v[i];
+    }
+    site(mid, m, l, 3, quant);
+    Mat o = matmul(mid, W(L, 5, quant));
+    for (size_t i = 0; i < x.v.size(); ++i) x.v[i] += o.v[i];
+}
+
+// Top-k by (score desc, index asc), returned ascending (selector.cpp:117-136)
+std::vector<int> top_k(const Vec& s, int k) {
+    const int n = static_cast<int>(s.size());
+    std::vector<int> idx(static_cast<size_t>(n));
+    for (int i = 0; i < n; ++i) idx[static_cast<size_t>(i)] = i;
+    if (k >= n) return idx;
+    std::sort(idx.begin(), idx.end(), [&s](int a, int b) {
+        if (s[static_cast<size_t>(a)] != s[static_cast<size_t>(b)]) return s[static_cast<size_t>(a)] > s[static_cast<size_t>(b)];
+        return a < b;
+    });
+    idx.resize(static_cast<size_t>(k));
+    std::sort(idx.begin(), idx.end());
+    return idx;
+}
+
+// forward_prefill (model.cpp:315-453) + recipe hook (selector.cpp:211-228)
+void prefill(Run& run, const Mat& emb, const Recipe* rc) {
+    const Model& m = *run.m;
+    const Cfg& c = m.cfg;
+    const bool quant = run.quant;
+    const int H = c.n_heads, Hk = c.n_kv_heads, dh = c.d_head, grp = H / Hk;
+    Mat x = emb;
+    Seq& cur = run.seq;
+    run.cache.assign(static_cast<size_t>(c.n_layers), LayerCache{});
+    const double inv_sqrt = 1.0 / std::sqrt(static_cast<double>(dh));
+
+    for (int l = 0; l < c.n_layers; ++l) {
+        const Layer& L = m.layers[static_cast<size_t>(l)];
+        const int S = cur.visual + cur.text, V = cur.visual, T = cur.text;
+        Mat n1 = rms_rows(x, L.g1);
+        site(n1, m, l, 0, quant);
+        Mat q = matmul(n1, W(L, 0, quant)), k = matmul(n1, W(L, 1, quant)), v = matmul(n1, W(L, 2, quant));
+        // rope on q/k per head at original positions (model.cpp:246-268)
+        for (int r = 0; r < S; ++r) {
+            for (int h = 0; h < H; ++h) rope(q.row(r) + h * dh, dh, cur.pos[static_cast<size_t>(r)]);
+            for (int h = 0; h < Hk; ++h) rope(k.row(r) + h * dh, dh, cur.pos[static_cast<size_t>(r)]);
+        }
+        LayerCache& lc = run.cache[static_cast<size_t>(l)];
+        lc.heads.assign(static_cast<size_t>(Hk), KVHead{});
+        lc.pos = cur.pos;
+        std::vector<Mat> kh(static_cast<size_t>(Hk)), vh(static_cast<size_t>(Hk));
+        for (int h = 0; h < Hk; ++h) {
+            Mat ks(S, dh), vs(S, dh);
+            for (int r = 0; r < S; ++r)
+                for (int j = 0; j < dh; ++j) {
+                    ks.at(r, j) = k.at(r, h * dh + j);
+                    vs.at(r, j) = v.at(r, h * dh + j);
+                }
+            if (quant) {  // model.cpp:368-374
+                KVHead& hk = lc.heads[static_cast<size_t>(h)];
+                kv_quant_rows(ks, c.kv_bits, hk.k, hk.ks);
+                kv_quant_rows(vs, c.kv_bits, hk.v, hk.vs);
+                for (int r = 0; r < S; ++r)
+                    for (int j = 0; j < dh; ++j) {
+                        ks.at(r, j) = static_cast<double>(hk.k[static_cast<size_t>(r) * dh + j]) * hk.ks[static_cast<size_t>(r)];
+                        vs.at(r, j) = static_cast<double>(hk.v[static_cast<size_t>(r) * dh + j]) * hk.vs[static_cast<size_t>(r)];
+                    }
+            } else {
+                KVHead& hk = lc.heads[static_cast<size_t>(h)];
+                hk.ks.assign(ks.v.begin(), ks.v.end());  // fp cache rows kept as values
+                hk.vs.assign(vs.v.begin(), vs.v.end());
+            }
+            kh[static_cast<size_t>(h)] = std::move(ks);
+            vh[static_cast<size_t>(h)] = std::move(vs);
+        }
+        // attention per query head (model.cpp:366-391, 272-292)
+        Mat cat(S, c.d_model);
+        Vec inter(static_cast<size_t>(V), 0.0), intra(static_cast<size_t>(V), 0.0);
+        std::vector<Mat> probs_keep;
+        for (int h = 0; h < H; ++h) {
+            const Mat& K = kh[static_cast<size_t>(h / grp)];
+            const Mat& Vv = vh[static_cast<size_t>(h / grp)];
+            Mat P(S, S);
+            Vec sc(static_cast<size_t>(S));
+            for (int i = 0; i < S; ++i) {
+                double mx = kNegInf;
+                const double* qi = q.row(i) + h * dh;
+                for (int j = 0; j < S; ++j) {
+                    sc[static_cast<size_t>(j)] = kNegInf;
+                    if (!allowed(cur, i, j)) continue;
+                    double d = 0.0;
+                    const double* kj = K.row(j);
+                    for (int t = 0; t < dh; ++t) d += qi[t] * kj[t];  // numeric.cpp:53-57
+                    sc[static_cast<size_t>(j)] = d * inv_sqrt;
+                    if (sc[static_cast<size_t>(j)] > mx) mx = sc[static_cast<size_t>(j)];
+                }
+                double sum = 0.0;
+                for (int j = 0; j < S; ++j) {
+                    double e = sc[static_cast<size_t>(j)] <= kNegInf ? 0.0 : std::exp(sc[static_cast<size_t>(j)] - mx);
+                    P.at(i, j) = e;
+                    sum += e;
+                }
+                for (int j = 0; j < S; ++j) P.at(i, j) /= sum;
+            }
+            // out_h = P . V (numeric.cpp:33-46 order)
+            for (int i = 0; i < S; ++i)
+                for (int t = 0; t < dh; ++t) {
+                    double acc = 0.0;
+                    for (int j = 0; j < S; ++j) acc += P.at(i, j) * Vv.at(j, t);
+                    cat.at(i, h * dh + t) = acc;
+                }
+            probs_keep.push_back(std::move(P));
+        }
+        site(cat, m, l, 1, quant);
+        Mat proj = matmul(cat, W(L, 3, quant));
+        for (size_t i = 0; i < x.v.size(); ++i) x.v[i] += proj.v[i];
+
+        // recipe hook at candidate layers (selector.cpp:214-227)
+        int cand = -1;
+        if (rc) {
+            for (size_t i = 0; i < rc->layers.size(); ++i)
+                if (rc->layers[i] == l) cand = static_cast<int>(i);
+        }
+        std::vector<int> slots;
+        bool prune = false;
+        if (cand >= 0) {
+            // compute_budget (selector.cpp:11-17)
+            int budget = static_cast<int>(std::ceil(rc->keeps[static_cast<size_t>(cand)] * static_cast<double>(rc->v0)));
+            // compute_metrics (selector.cpp:19-68): head blocks summed head by head
+            Vec mag(static_cast<size_t>(V)), res(static_cast<size_t>(V), 0.0);
+            for (int i = 0; i < V; ++i) {
+                double a = 0.0;
+                for (int j = 0; j < c.d_model; ++j) a += x.at(i, j) * x.at(i, j);
+                mag[static_cast<size_t>(i)] = std::sqrt(a);
+            }
+            for (int h = 0; h < H; ++h) {
+                const Mat& P = probs_keep[static_cast<size_t>(h)];
+                for (int r = 0; r < T; ++r)
+                    for (int i = 0; i < V; ++i) inter[static_cast<size_t>(i)] += P.at(V + r, i);
+            }
+            for (int h = 0; h < H; ++h) {
+                const Mat& P = probs_keep[static_cast<size_t>(h)];
+                for (int r = 0; r < V; ++r)
+                    for (int i = 0; i < V; ++i) intra[static_cast<size_t>(i)] += P.at(r, i);
+            }
+            const double ih = 1.0 / static_cast<double>(H);
+            for (int i = 0; i < V; ++i) {
+                inter[static_cast<size_t>(i)] *= ih;
+                intra[static_cast<size_t>(i)] *= ih;
+            }
+            if (rc->res_bits >= 0) {
+                Mat vis(V, c.d_model);
+                std::copy(x.v.begin(), x.v.begin() + static_cast<long>(V) * c.d_model, vis.v.begin());
+                Mat fq = vis;
+                fq_rows(fq, rc->res_bits);
+                for (int i = 0; i < V; ++i) {
+                    double a = 0.0;
+                    for (int j = 0; j < c.d_model; ++j) {
+                        double d = fq.at(i, j) - vis.at(i, j);
+                        a += d * d;
+                    }
+                    res[static_cast<size_t>(i)] = std::sqrt(a);
+                }
+            }
+            // score_tokens (selector.cpp:106-115) + fuse (86-104)
+            Vec nm = robust_norm(mag), ni = robust_norm(inter), na = robust_norm(intra), nr = robust_norm(res);
+            Vec fused(static_cast<size_t>(V));
+            for (int i = 0; i < V; ++i) {
+                size_t u = static_cast<size_t>(i);
+                fused[u] = rc->w[0] * nm[u] + rc->w[1] * ni[u] + rc->w[2] * na[u] + rc->w[3] * nr[u];
+            }
+            run.last_metrics = {mag, inter, intra, res};
+            run.last_fused = fused;
+            slots = top_k(fused, budget);
+            if (static_cast<int>(slots.size()) < V) {
+                prune = true;
+                Trace tr{l, budget, {}};
+                for (int s : slots) tr.positions.push_back(cur.pos[static_cast<size_t>(s)]);
+                run.trace.push_back(std::move(tr));
+            }
+        }
+        if (prune) {
+            // apply_pruning (selector.cpp:138-209): layout, x rows, and the
+            // layer-l cache rows (deeper layers are not materialised yet)
+            std::vector<int> keep(slots);
+            for (int i = V; i < S; ++i) keep.push_back(i);
+            Seq nxt;
+            nxt.visual = static_cast<int>(slots.size());
+            nxt.text = T;
+            for (int i : keep) nxt.pos.push_back(cur.pos[static_cast<size_t>(i)]);
+            Mat xn(static_cast<int>(keep.size()), c.d_model);
+            for (size_t i = 0; i < keep.size(); ++i)
+                std::copy(x.row(keep[i]), x.row(keep[i]) + c.d_model, xn.row(static_cast<int>(i)));
+            x = std::move(xn);
+            for (KVHead& hk : lc.heads) {
+                KVHead f;
+                const int wcols = quant ? dh : dh;
+                for (int i : keep) {
+                    size_t base = static_cast<size_t>(i) * wcols;
+                    if (quant) {
+                        f.k.insert(f.k.end(), hk.k.begin() + static_cast<long>(base), hk.k.begin() + static_cast<long>(base + wcols));
+                        f.v.insert(f.v.end(), hk.v.begin() + static_cast<long>(base), hk.v.begin() + static_cast<long>(base + wcols));
+                        f.ks.push_back(hk.ks[static_cast<size_t>(i)]);
+                        f.vs.push_back(hk.vs[static_cast<size_t>(i)]);
+                    } else {
+                        f.ks.insert(f.ks.end(), hk.ks.begin() + static_cast<long>(base), hk.ks.begin() + static_cast<long>(base + wcols));
+                        f.vs.insert(f.vs.end(), hk.vs.begin() + static_cast<long>(base), hk.vs.begin() + static_cast<long>(base + wcols));
+                    }
+                }
+                hk = std::move(f);
+            }
+            lc.pos = nxt.pos;
+            cur = std::move(nxt);
+        }
+        mlp(x, m, l, quant);
+        run.block_out.push_back(x);
+    }
+    Mat fn = rms_rows(x, m.gf);
+    if (quant) {
+        if (c.act_mode == 0) fq_tensor(fn, m.act[static_cast<size_t>(4 * c.n_layers)], c.act_bits);
+        else fq_rows(fn, c.act_bits);
+    }
+    run.logits = matmul(fn, quant ? m.qhead.deq : m.head);
+}
+
+// decode_step (model.cpp:455-562)
+Vec decode(Run& run, const double* emb) {
+    const Model& m = *run.m;
+    const Cfg& c = m.cfg;
+    const bool quant = run.quant;
+    const int H = c.n_heads, Hk = c.n_kv_heads, dh = c.d_head, grp = H / Hk;
+    const int pos = run.next_pos;
+    Mat x(1, c.d_model);
+    std::copy(emb, emb + c.d_model, x.v.begin());
+    const double inv_sqrt = 1.0 / std::sqrt(static_cast<double>(dh));
+    for (int l = 0; l < c.n_layers; ++l) {
+        const Layer& L = m.layers[static_cast<size_t>(l)];
+        Mat n1 = rms_rows(x, L.g1);
+        site(n1, m, l, 0, quant);
+        Mat q = matmul(n1, W(L, 0, quant)), k = matmul(n1, W(L, 1, quant)), v = matmul(n1, W(L, 2, quant));
+        for (int h = 0; h < H; ++h) rope(q.row(0) + h * dh, dh, pos);
+        for (int h = 0; h < Hk; ++h) rope(k.row(0) + h * dh, dh, pos);
+        LayerCache& lc = run.cache[static_cast<size_t>(l)];
+        for (int h = 0; h < Hk; ++h) {  // append (model.cpp:497-513)
+            KVHead& hk = lc.heads[static_cast<size_t>(h)];
+            Mat kr(1, dh), vr(1, dh);
+            std::copy(k.row(0) + h * dh, k.row(0) + (h + 1) * dh, kr.v.begin());
+            std::copy(v.row(0) + h * dh, v.row(0) + (h + 1) * dh, vr.v.begin());
+            if (quant) {
+                kv_quant_rows(kr, c.kv_bits, hk.k, hk.ks);
+                kv_quant_rows(vr, c.kv_bits, hk.v, hk.vs);
+            } else {
+                hk.ks.insert(hk.ks.end(), kr.v.begin(), kr.v.end());
+                hk.vs.insert(hk.vs.end(), vr.v.begin(), vr.v.end());
+            }
+        }
+        lc.pos.push_back(pos);
+        Mat cat(1, c.d_model);
+        for (int h = 0; h < H; ++h) {  // unmasked softmax over every cached row (model.cpp:515-535)
+            const KVHead& hk = lc.heads[static_cast<size_t>(h / grp)];
+            const int rows = static_cast<int>(lc.pos.size());
+            auto kval = [&](int j, int t) {
+                return quant ? static_cast<double>(hk.k[static_cast<size_t>(j) * dh + t]) * hk.ks[static_cast<size_t>(j)]
+                             : hk.ks[static_cast<size_t>(j) * dh + t];
+            };
+            auto vval = [&](int j, int t) {
+                return quant ? static_cast<double>(hk.v[static_cast<size_t>(j) * dh + t]) * hk.vs[static_cast<size_t>(j)]
+                             : hk.vs[static_cast<size_t>(j) * dh + t];
+            };
+            Vec sc(static_cast<size_t>(rows));
+            double mx = kNegInf;
+            const double* qh = q.row(0) + h * dh;
+            for (int j = 0; j < rows; ++j) {
+                double d = 0.0;
+                for (int t = 0; t < dh; ++t) d += qh[t] * kval(j, t);
+                sc[static_cast<size_t>(j)] = d * inv_sqrt;
+                if (sc[static_cast<size_t>(j)] > mx) mx = sc[static_cast<size_t>(j)];
+            }
+            double sum = 0.0;
+            for (double& s : sc) {
+                s = std::exp(s - mx);
+                sum += s;
+            }
+            for (int t = 0; t < dh; ++t) {
+                double acc = 0.0;
+                for (int j = 0; j < rows; ++j) acc += (sc[static_cast<size_t>(j)] / sum) * vval(j, t);
+                cat.at(0, h * dh + t) = acc;
+            }
+        }
+        site(cat, m, l, 1, quant);
+        Mat proj = matmul(cat, W(L, 3, quant));
+        for (int j = 0; j < c.d_model; ++j) x.v[static_cast<size_t>(j)] += proj.v[static_cast<size_t>(j)];
+        mlp(x, m, l, quant);
+    }
+    run.seq.text += 1;
+    run.seq.pos.push_back(pos);
+    run.next_pos += 1;
+    Mat fn = rms_rows(x, m.gf);
+    if (quant) {
+        if (c.act_mode == 0) fq_tensor(fn, m.act[static_cast<size_t>(4 * c.n_layers)], c.act_bits);
+        else fq_rows(fn, c.act_bits);
+    }
+    Mat lg = matmul(fn, quant ? m.qhead.deq : m.head);
+    return lg.v;
+}
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return -1;
+    } catch (const std::runtime_error& e) {
+        g_err = e.what();
+        return -2;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -4;
+    }
+}
+
+Mat* weight_slot(Model* m, int layer, int which) {
+    if (layer < 0) return &m->head;
+    Layer& L = m->layers.at(static_cast<size_t>(layer));
+    Mat* ws[9] = {&L.wq, &L.wk, &L.wv, &L.wo, &L.w1, &L.w2, nullptr, nullptr, &L.w3};
+    return ws[which];
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* qo_last_error() { return g_err.c_str(); }
+
+// cfg: {n_layers, d_model, n_heads, n_kv_heads, d_head, d_ff, mlp, act_mode,
+//       weight_axis, act_bits, weight_bits, kv_bits}
+void* qo_model_create(const int* cfg) {
+    Model* out = nullptr;
+    guard([&] {
+        Cfg c{cfg[0], cfg[1], cfg[2], cfg[3], cfg[4], cfg[5], cfg[6], cfg[7], cfg[8], cfg[9], cfg[10], cfg[11]};
+        if (c.n_heads * c.d_head != c.d_model) throw std::invalid_argument("d_model must equal n_heads * d_head");
+        if (c.d_head % 2 != 0) throw std::invalid_argument("d_head must be even and >= 2");
+        if (c.n_kv_heads < 1 || c.n_heads % c.n_kv_heads != 0) throw std::invalid_argument("n_heads % n_kv_heads");
+        auto m = std::make_unique<Model>();
+        m->cfg = c;
+        const int d = c.d_model, kvd = c.n_kv_heads * c.d_head, f = c.d_ff;
+        m->layers.resize(static_cast<size_t>(c.n_layers));
+        for (Layer& L : m->layers) {
+            L.wq = Mat(d, d);
+            L.wk = Mat(d, kvd);
+            L.wv = Mat(d, kvd);
+            L.wo = Mat(d, d);
+            L.w1 = Mat(d, f);
+            L.w2 = Mat(f, d);
+            if (c.mlp == 1) L.w3 = Mat(d, f);
+            L.g1.assign(static_cast<size_t>(d), 1.0);
+            L.g2.assign(static_cast<size_t>(d), 1.0);
+        }
+        m->head = Mat(d, d);
+        m->gf.assign(static_cast<size_t>(d), 1.0);
+        out = m.release();
+    });
+    return out;
+}
+
+void qo_model_free(void* h) { delete static_cast<Model*>(h); }
+
+// which: 0 wq 1 wk 2 wv 3 wo 4 w1(gate) 5 w2(down) 6 norm1 7 norm2 8 w3(up);
+// layer -1: which 0 = head, 6 = final norm gain.  W row-major d_in x d_out.
+int qo_model_set_weight(void* h, int layer, int which, const double* src, int64_t count) {
+    return guard([&] {
+        Model* m = static_cast<Model*>(h);
+        if (which == 6 || which == 7) {
+            Vec& g = layer < 0 ? m->gf : (which == 6 ? m->layers.at(static_cast<size_t>(layer)).g1
+                                                     : m->layers.at(static_cast<size_t>(layer)).g2);
+            if (static_cast<int64_t>(g.size()) != count) throw std::invalid_argument("gain size mismatch");
+            std::copy(src, src + count, g.begin());
+            return;
+        }
+        Mat* w = weight_slot(m, layer, which);
+        if (!w || static_cast<int64_t>(w->v.size()) != count) throw std::invalid_argument("weight size mismatch");
+        std::copy(src, src + count, w->v.begin());
+    });
+}
+
+// Quantize weights (prepare_quant_env, model.cpp:212-237, with the configured
+// axis) and install the static site scales (4*L + 1).
+int qo_model_prepare(void* h, const double* act_scales) {
+    return guard([&] {
+        Model* m = static_cast<Model*>(h);
+        const Cfg& c = m->cfg;
+        for (Layer& L : m->layers) {
+            const Mat* ws[7] = {&L.wq, &L.wk, &L.wv, &L.wo, &L.w1, &L.w2, &L.w3};
+            for (int i = 0; i < 7; ++i) {
+                if (i == 6 && c.mlp != 1) continue;
+                L.q[i] = quant_weight(*ws[i], c.weight_bits, c.weight_axis);
+            }
+        }
+        m->qhead = quant_weight(m->head, c.weight_bits, c.weight_axis);
+        m->act.assign(act_scales ? act_scales : nullptr, act_scales ? act_scales + 4 * c.n_layers + 1 : nullptr);
+        if (!act_scales) m->act.assign(static_cast<size_t>(4 * c.n_layers + 1), 1.0);
+        m->prepared = true;
+    });
+}
+
+int qo_model_weight_codes(void* h, int layer, int which, int8_t* codes, double* scales) {
+    return guard([&] {
+        Model* m = static_cast<Model*>(h);
+        const QW& q = layer < 0 ? m->qhead : m->layers.at(static_cast<size_t>(layer)).q[which == 8 ? 6 : which];
+        std::memcpy(codes, q.codes.data(), q.codes.size());
+        std::copy(q.scales.begin(), q.scales.end(), scales);
+    });
+}
+
+// recipe: n_cand, layers, keeps, weights4, v0, res_bits (-1 = none); n_cand 0 = no hook.
+void* qo_prefill(void* h, int quantized, const double* emb, int visual, int text, const int* pos,
+                 int n_cand, const int* layers, const double* keeps, const double* weights4, int v0,
+                 int res_bits) {
+    Run* out = nullptr;
+    guard([&] {
+        Model* m = static_cast<Model*>(h);
+        if (quantized && !m->prepared) throw std::invalid_argument("quantized mode requires a QuantEnv");
+        auto run = std::make_unique<Run>();
+        run->m = m;
+        run->quant = quantized != 0;
+        run->seq.visual = visual;
+        run->seq.text = text;
+        for (int i = 0; i < visual + text; ++i) run->seq.pos.push_back(pos ? pos[i] : i);
+        Mat e(visual + text, m->cfg.d_model);
+        std::copy(emb, emb + e.v.size(), e.v.begin());
+        Recipe rc;
+        if (n_cand > 0) {
+            rc.layers.assign(layers, layers + n_cand);
+            rc.keeps.assign(keeps, keeps + n_cand);
+            std::copy(weights4, weights4 + 4, rc.w);
+            rc.v0 = v0;
+            rc.res_bits = res_bits;
+        }
+        prefill(*run, e, n_cand > 0 ? &rc : nullptr);
+        run->next_pos = run->seq.pos.empty() ? 0 : run->seq.pos.back() + 1;
+        out = run.release();
+    });
+    return out;
+}
+
+void qo_run_free(void* r) { delete static_cast<Run*>(r); }
+
+int qo_run_logits_rows(void* r) { return static_cast<Run*>(r)->logits.r; }
+
+int qo_run_logits(void* r, double* out) {
+    Run* run = static_cast<Run*>(r);
+    std::copy(run->logits.v.begin(), run->logits.v.end(), out);
+    return 0;
+}
+
+int qo_run_layout(void* r, int* visual, int* text, int* pos) {
+    Run* run = static_cast<Run*>(r);
+    *visual = run->seq.visual;
+    *text = run->seq.text;
+    if (pos) std::copy(run->seq.pos.begin(), run->seq.pos.end(), pos);
+    return 0;
+}
+
+int qo_run_n_prunes(void* r) { return static_cast<int>(static_cast<Run*>(r)->trace.size()); }
+
+int qo_run_prune(void* r, int i, int* layer, int* budget, int* positions, int* count) {
+    const Trace& t = static_cast<Run*>(r)->trace.at(static_cast<size_t>(i));
+    *layer = t.layer;
+    *budget = t.budget;
+    std::copy(t.positions.begin(), t.positions.end(), positions);
+    *count = static_cast<int>(t.positions.size());
+    return 0;
+}
+
+// metrics (4 x V: mag, inter, intra, res) and fused scores of the last candidate layer
+int qo_run_last_scores(void* r, double* metrics, double* fused, int* n) {
+    Run* run = static_cast<Run*>(r);
+    if (run->last_fused.empty()) return -1;
+    size_t V = run->last_fused.size();
+    *n = static_cast<int>(V);
+    for (size_t i = 0; i < 4; ++i)
+        if (metrics) std::copy(run->last_metrics[i].begin(), run->last_metrics[i].end(), metrics + i * V);
+    if (fused) std::copy(run->last_fused.begin(), run->last_fused.end(), fused);
+    return 0;
+}
+
+int qo_run_block_output(void* r, int layer, double* out, int* rows) {
+    return guard([&] {
+        const Mat& b = static_cast<Run*>(r)->block_out.at(static_cast<size_t>(layer));
+        *rows = b.r;
+        if (out) std::copy(b.v.begin(), b.v.end(), out);
+    });
+}
+
+int qo_run_kv(void* r, int layer, int head, int which, int8_t* codes, double* scales, int* pos, int* rows) {
+    return guard([&] {
+        Run* run = static_cast<Run*>(r);
+        const LayerCache& lc = run->cache.at(static_cast<size_t>(layer));
+        const KVHead& hk = lc.heads.at(static_cast<size_t>(head));
+        *rows = static_cast<int>(lc.pos.size());
+        const std::vector<int8_t>& c = which == 0 ? hk.k : hk.v;
+        const Vec& s = which == 0 ? hk.ks : hk.vs;
+        if (codes) std::memcpy(codes, c.data(), c.size());
+        if (scales) std::copy(s.begin(), s.end(), scales);
+        if (pos) std::copy(lc.pos.begin(), lc.pos.end(), pos);
+    });
+}
+
+int qo_decode(void* r, const double* emb, double* logits) {
+    return guard([&] {
+        Vec out = decode(*static_cast<Run*>(r), emb);
+        std::copy(out.begin(), out.end(), logits);
+    });
+}
+
+// Multi-sequence driver for the CPU baseline: one sequence per thread (the
+// reference is thread-safe per sequence).  Runs prefill + n_decode
+// teacher-forced steps for each sequence; returns 0 or the first error.
+int qo_run_batch(void* h, int quantized, int n_seq, const double* const* emb, const int* visual,
+                 const int* text, int n_cand, const int* layers, const double* keeps,
+                 const double* weights4, const int* v0, int res_bits, int n_decode,
+                 const double* const* dec_emb, int n_threads, double* last_logits) {
+    Model* m = static_cast<Model*>(h);
+    std::vector<int> rcs(static_cast<size_t>(n_seq), 0);
+    std::vector<std::string> errs(static_cast<size_t>(n_seq));
+    auto work = [&](int s) {
+        rcs[static_cast<size_t>(s)] = guard([&] {
+            void* r = qo_prefill(m, quantized, emb[s], visual[s], text[s], nullptr, n_cand, layers, keeps,
+                                 weights4, v0[s], res_bits);
+            if (!r) throw std::runtime_error(g_err);
+            std::unique_ptr<Run> run(static_cast<Run*>(r));
+            Vec lg;
+            for (int t = 0; t < n_decode; ++t) lg = decode(*run, dec_emb[s] + static_cast<size_t>(t) * m->cfg.d_model);
+            if (last_logits) {
+                const Vec& src = n_decode > 0 ? lg : Vec(run->logits.row(run->logits.r - 1), run->logits.row(run->logits.r - 1) + m->cfg.d_model);
+                std::copy(src.begin(), src.end(), last_logits + static_cast<size_t>(s) * m->cfg.d_model);
+            }
+        });
+        if (rcs[static_cast<size_t>(s)] != 0) errs[static_cast<size_t>(s)] = g_err;
+    };
+    n_threads = std::max(1, std::min(n_threads, n_seq));
+    std::vector<std::thread> pool;
+    for (int t = 0; t < n_threads; ++t)
+        pool.emplace_back([&, t] {
+            for (int s = t; s < n_seq; s += n_threads) work(s);
+        });
+    for (auto& th : pool) th.join();
+    for (int s = 0; s < n_seq; ++s)
+        if (rcs[static_cast<size_t>(s)] != 0) {
+            g_err = errs[static_cast<size_t>(s)];
+            return rcs[static_cast<size_t>(s)];
+        }
+    return 0;
+}
+
+}  // extern "C"
