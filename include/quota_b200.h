@@ -1,0 +1,137 @@
+/* quota_b200.h -- C ABI of the B200-native QUOTA hot path.
+ *
+ * Drop-in boundary for the reference's deployed low-bit pruned forward pass
+ * (/root/reference/proj/include/quota/model.hpp:158-186, selector.hpp:55-57,
+ * recipe.hpp:25-54).  Plain pointers and sizes, no C++ or torch types:
+ * the reference C++ API (forward_prefill / decode_step / make_recipe_hook /
+ * load_recipe) is re-implemented on top of these calls by the C++ host layer
+ * (include/quota_b200.hpp), and INTEGRATION.md shows the ctypes binding.
+ *
+ * Status: every call returns 0 on success or a negative code; the message is
+ * available from qt_last_error() (thread-local).  The codes mirror the
+ * reference exception types:
+ *   QT_EINVAL   std::invalid_argument   (shape / config / recipe violations)
+ *   QT_ERUNTIME std::runtime_error      (prune / mode violations)
+ *   QT_ERANGE   std::out_of_range
+ *   QT_ECUDA    CUDA error (no CPU fallback exists: the path fails loudly)
+ *
+ * Orientation: weights are given as the reference stores them,
+ * W[d_in x d_out] row-major with y = x W (model.hpp:52-57).  Activations are
+ * row-major [tokens x d_model], sequences packed back to back, each sequence
+ * a visual prefix followed by text (model.hpp:40-50).
+ */
+#ifndef QUOTA_B200_H
+#define QUOTA_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QT_OK 0
+#define QT_EINVAL (-1)
+#define QT_ERUNTIME (-2)
+#define QT_ERANGE (-3)
+#define QT_ECUDA (-4)
+
+/* Model shape + semantic switches.  Reference semantics (model.hpp:29-37,
+ * model.cpp:31-33,212-237): mlp = 0, act_mode = 0, n_kv_heads = n_heads,
+ * d_ff = 4 * d_model.  Weight scales are always per output channel
+ * (GroupAxis::PerColumn, quant.hpp:22) -- the axis an int32-accumulator GEMM
+ * can apply in its epilogue. */
+typedef struct qt_config {
+    int n_layers;
+    int d_model;
+    int n_heads;
+    int n_kv_heads;  /* GQA when < n_heads */
+    int d_head;      /* 64 or 128 */
+    int d_ff;
+    int mlp;         /* 0 = SiLU MLP (reference), 1 = SwiGLU */
+    int act_mode;    /* 0 = static per-tensor site scales (reference), 1 = dynamic per-token */
+    int weight_bits; /* 4 */
+    int act_bits;    /* 4 */
+    int kv_bits;     /* 4 */
+} qt_config;
+
+typedef struct qt_engine qt_engine;
+
+const char* qt_last_error(void);
+
+/* Capacity: max_batch sequences per call, max_tokens packed prefill tokens,
+ * max_seq tokens per sequence, max_decode decode steps after a prefill. */
+int qt_engine_create(const qt_config* cfg, int max_batch, int max_tokens, int max_seq, int max_decode,
+                     qt_engine** out);
+void qt_engine_destroy(qt_engine* e);
+/* cudaStream_t to run on (0 = the engine's own stream). */
+int qt_engine_set_stream(qt_engine* e, void* stream);
+int qt_engine_synchronize(qt_engine* e);
+
+/* init_model / prepare_quant_env (model.cpp:113-135, 212-237): fp32 weights
+ * in reference orientation, quantized on the device to int4 codes with one
+ * fp64-derived scale per output channel.  w3 (SwiGLU up) may be null for
+ * mlp = 0; gains may be null (= 1.0, model.cpp:129-132).  on_device != 0:
+ * the pointers are device pointers. */
+int qt_engine_load_layer(qt_engine* e, int layer, const float* wq, const float* wk, const float* wv,
+                         const float* wo, const float* w1, const float* w2, const float* w3, const float* g1,
+                         const float* g2, int on_device);
+int qt_engine_load_head(qt_engine* e, const float* w_head, const float* final_gain, int on_device);
+/* ActScales (model.hpp:114-133): 4 * n_layers + 1 static per-tensor scales,
+ * order (attn_in, attn_out, mlp_in, mlp_mid) per layer, then head_in. */
+int qt_engine_set_act_scales(qt_engine* e, const double* scales);
+
+/* make_recipe_hook (selector.cpp:211-228) over a PruningRecipe
+ * (recipe.hpp:25-34): validated like PruningRecipe::validate (recipe.cpp:21-46).
+ * res_bits < 0 = nullopt (no quantization-residual metric). n_layers = 0 clears. */
+int qt_engine_set_recipe(qt_engine* e, int n_layers, const int* layers, const double* keep_ratios,
+                         const double* weights4, int v0, int res_bits);
+/* parse_recipe (recipe.cpp:91-116) semantics: strict keys, schema_version 1. */
+int qt_recipe_parse(const char* json, int max_layers, int* n_layers, int* layers, double* keep_ratios,
+                    double* weights4, int* v0, char* quant_digest, int digest_cap);
+
+/* forward_prefill (model.cpp:315-453), quantized mode, recipe hook, for a
+ * batch of independent sequences.  emb: packed [sum(visual+text) x d_model].
+ * v0: per-sequence reference visual length (null = recipe v0).  positions:
+ * packed original position ids (null = 0..S-1 per sequence).  logits_out
+ * (nullable): packed [sum(final rows) x d_model], host or device. */
+int qt_engine_prefill(qt_engine* e, int n_seq, const float* emb, int emb_on_device, const int* visual,
+                      const int* text, const int* v0, const int* positions, float* logits_out, int out_on_device);
+/* rows of the packed prefill logits (sum over sequences of the final layout) */
+int qt_engine_prefill_rows(qt_engine* e);
+/* decode_step (model.cpp:455-562) for every sequence of the last prefill:
+ * emb [n_seq x d_model], logits_out [n_seq x d_model]. */
+int qt_engine_decode(qt_engine* e, const float* emb, int emb_on_device, float* logits_out, int out_on_device);
+
+/* Introspection (parity tests, reports). */
+int qt_engine_layout(qt_engine* e, int seq, int* visual, int* text, int* positions, int cap);
+int qt_engine_n_prunes(qt_engine* e, int seq);
+int qt_engine_prune(qt_engine* e, int seq, int i, int* layer, int* budget, int* positions, int cap, int* count);
+int qt_engine_kv(qt_engine* e, int layer, int seq, int kv_head, int which, int8_t* codes, float* scales,
+                 int* rows, int cap_rows);
+/* device pointers for in-place timing / inspection */
+int qt_engine_info(qt_engine* e, int64_t* out16);
+
+/* ---- per-kernel ABI (caller-owned device buffers, explicit stream) ---- */
+/* K1: RMSNorm (gain != null) + int4 activation quantizer; x fp32 or fp64
+ * (x_is_f64); act_mode 0 = static_scale, 1 = per-row max|x|/7; fp64 scales. */
+int qt_rmsnorm_quant_i4(const void* x, int x_is_f64, int ld_x, const float* gain, int M, int D, int d_pad,
+                        int act_mode, double static_scale, uint8_t* codes, int ld_codes, double* scales,
+                        float* normed, void* stream);
+/* K2: y = s_a[m] s_w[n] sum_k a[m][k] w[n][k]; out is double* for epilogue
+ * 1 (residual add), float* otherwise; acc_out (nullable) receives the int32
+ * accumulators; impl 0 = mma.sync path, 1 = tcgen05 path. */
+int qt_w4a4_gemm(int epilogue, const uint8_t* a_codes, int lda, const double* a_scales, const uint8_t* w_codes,
+                 int ldw, const double* w_scales, int M, int N, int K, void* out, int ldo, int32_t* acc_out,
+                 int impl, void* stream);
+int qt_quant_weight_i4(const float* w, int K, int N, int row_mul, int row_add, uint8_t* codes, int ldc,
+                       double* scales, double* scratch, void* stream);
+int qt_kv_quant_append_i4(float* qkv, int ld_qkv, int M, int H, int Hkv, int d_head, const int* positions,
+                          const int* tok_seq, const int* tok_row, const double* rope_table, const int* page_table,
+                          int max_pages, uint8_t* pool, int64_t page_bytes, float* k_out, void* stream);
+int qt_rope_table(int max_pos, int d_head, double* host_out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* QUOTA_B200_H */

@@ -119,6 +119,8 @@ def port_lib():
         lib.qo_run_block_output.argtypes = [C.c_void_p, C.c_int, _dp, _ip]
         lib.qo_run_kv.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, _i8p, _dp, _ip, _ip]
         lib.qo_decode.argtypes = [C.c_void_p, _dp, _dp]
+        lib.qo_run_tie_margin.restype = C.c_double
+        lib.qo_run_tie_margin.argtypes = [C.c_void_p, C.c_int]
         lib.qo_run_batch.argtypes = [C.c_void_p, C.c_int, C.c_int, C.POINTER(_dp), _ip, _ip, C.c_int, _ip, _dp,
                                      _dp, _ip, C.c_int, C.c_int, C.POINTER(_dp), C.c_int, _dp]
         _port_lib = lib
@@ -471,6 +473,11 @@ class PortRun:
         out = np.empty(self.o.cfg.d_model, dtype=np.float64)
         _check(self.lib.qo_decode(self.h, _d(e), _d(out)), self.lib, "qo")
         return out
+
+    def tie_margin(self, which):
+        """Smallest |frac(x/s) - 0.5| over activation/KV quantizations of the last
+        prefill (which=0) or decode step (which=1)."""
+        return self.lib.qo_run_tie_margin(self.h, which)
 
 
 # ---------------------------------------------------------------- synthetic inputs

@@ -72,9 +72,28 @@ double scale_of(double max_abs, int bits) {
     return max_abs == 0.0 ? 1.0 : max_abs / qmax;
 }
 
+// Smallest distance (in code units) of any unclamped activation / KV value to
+// a rounding tie during the current prefill / decode call.  Not part of the
+// reference: it lets parity tests tell a genuine mismatch from a quantization
+// decision that sits on a tie (where fp32-vs-fp64 arithmetic may legitimately
+// round the other way).
+// The margin is divided by the site's error budget on the GPU path (g_site_tol,
+// in code units): inputs derived from the fp64 residual are exact to ~1e-14,
+// fp32-stored activations (k/v, MLP hidden) to ~1e-7, attention outputs to
+// ~1e-5.  A ratio < 1 marks the call as tie-ambiguous.
+thread_local double g_tie_margin = 1e300;
+thread_local bool g_track = false;
+thread_local double g_site_tol = 0.0;  // 0 = decision not tracked
+constexpr double kTolResidual = 1e-9, kTolAttn = 1e-4, kTolFp32 = 1e-6;
+
 // quant.cpp:85-87 -- one code
 int8_t code_of(double x, double s, int bits) {
     double qmax = static_cast<double>((1 << (bits - 1)) - 1);
+    if (g_track && g_site_tol > 0.0) {
+        double r = x / s;
+        if (std::fabs(r) <= qmax + 0.5)
+            g_tie_margin = std::min(g_tie_margin, std::fabs(std::fabs(r - std::floor(r)) - 0.5) / g_site_tol);
+    }
     double q = rne(x / s);
     q = std::min(std::max(q, -qmax), qmax);
     return static_cast<int8_t>(q);
@@ -262,9 +281,11 @@ struct Run {
     // metrics of the most recent pruning layer (for kernel-level parity)
     std::vector<Vec> last_metrics;  // mag, inter, intra, res
     Vec last_fused;
+    double margin_prefill = 1e300, margin_decode = 1e300;
 };
 
 void kv_quant_rows(const Mat& x, int bits, std::vector<int8_t>& codes, Vec& scales) {
+    g_site_tol = kTolFp32;
     for (int i = 0; i < x.r; ++i) {
         double m = 0.0;
         for (int j = 0; j < x.c; ++j) m = std::max(m, std::fabs(x.at(i, j)));
@@ -284,6 +305,7 @@ bool allowed(const Seq& s, int qi, int ki) {
 
 void site(Mat& x, const Model& m, int layer, int idx, bool quant) {
     if (!quant) return;
+    g_site_tol = idx == 1 ? kTolAttn : (idx == 3 ? kTolFp32 : kTolResidual);
     if (m.cfg.act_mode == 0) {
         fq_tensor(x, m.act[static_cast<size_t>(4 * layer + idx)], m.cfg.act_bits);
     } else {
@@ -456,6 +478,7 @@ void prefill(Run& run, const Mat& emb, const Recipe* rc) {
                 Mat vis(V, c.d_model);
                 std::copy(x.v.begin(), x.v.begin() + static_cast<long>(V) * c.d_model, vis.v.begin());
                 Mat fq = vis;
+                g_site_tol = 0.0;  // scoring metric, not a forward decision
                 fq_rows(fq, rc->res_bits);
                 for (int i = 0; i < V; ++i) {
                     double a = 0.0;
@@ -521,6 +544,7 @@ void prefill(Run& run, const Mat& emb, const Recipe* rc) {
     }
     Mat fn = rms_rows(x, m.gf);
     if (quant) {
+        g_site_tol = kTolResidual;
         if (c.act_mode == 0) fq_tensor(fn, m.act[static_cast<size_t>(4 * c.n_layers)], c.act_bits);
         else fq_rows(fn, c.act_bits);
     }
@@ -601,6 +625,7 @@ Vec decode(Run& run, const double* emb) {
     run.next_pos += 1;
     Mat fn = rms_rows(x, m.gf);
     if (quant) {
+        g_site_tol = kTolResidual;
         if (c.act_mode == 0) fq_tensor(fn, m.act[static_cast<size_t>(4 * c.n_layers)], c.act_bits);
         else fq_rows(fn, c.act_bits);
     }
@@ -742,7 +767,11 @@ void* qo_prefill(void* h, int quantized, const double* emb, int visual, int text
             rc.v0 = v0;
             rc.res_bits = res_bits;
         }
+        g_tie_margin = 1e300;
+        g_track = true;
         prefill(*run, e, n_cand > 0 ? &rc : nullptr);
+        g_track = false;
+        run->margin_prefill = g_tie_margin;
         run->next_pos = run->seq.pos.empty() ? 0 : run->seq.pos.back() + 1;
         out = run.release();
     });
@@ -812,9 +841,18 @@ int qo_run_kv(void* r, int layer, int head, int which, int8_t* codes, double* sc
     });
 }
 
+double qo_run_tie_margin(void* r, int which) {
+    Run* run = static_cast<Run*>(r);
+    return which == 0 ? run->margin_prefill : run->margin_decode;
+}
+
 int qo_decode(void* r, const double* emb, double* logits) {
     return guard([&] {
+        g_tie_margin = 1e300;
+        g_track = true;
         Vec out = decode(*static_cast<Run*>(r), emb);
+        g_track = false;
+        static_cast<Run*>(r)->margin_decode = g_tie_margin;
         std::copy(out.begin(), out.end(), logits);
     });
 }

@@ -1,0 +1,338 @@
+"""paper_2604_17320_b200 -- B200-native QUOTA hot path (W4A4 prefill with
+recipe-driven visual-token pruning, decode over an int4 paged KV cache).
+
+The product is the C-ABI library ``_build/libquota_b200.so`` (CUDA kernels for
+sm_100a + the C++ host engine, declared in ``include/quota_b200.h``).  This
+module is a thin ctypes binding used by tests and bench.py; it never computes
+anything itself and there is no CPU fallback: if the library or a GPU is
+missing every call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_build", "libquota_b200.so")
+ROOT = os.path.dirname(HERE)
+HEADER = os.path.join(ROOT, "include", "quota_b200.h")
+
+QT_EINVAL, QT_ERUNTIME, QT_ERANGE, QT_ECUDA = -1, -2, -3, -4
+EPI_STORE, EPI_RESADD, EPI_SILU, EPI_SWIGLU = 0, 1, 2, 3
+
+
+class QuotaError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(msg)
+        self.code = code
+
+
+class QuotaInvalidArgument(QuotaError, ValueError):
+    """std::invalid_argument in the reference."""
+
+
+class QuotaRuntimeError(QuotaError):
+    """std::runtime_error in the reference."""
+
+
+class QuotaOutOfRange(QuotaError, IndexError):
+    """std::out_of_range in the reference."""
+
+
+_lib = None
+
+
+class _Config(C.Structure):
+    _fields_ = [(n, C.c_int) for n in ("n_layers", "d_model", "n_heads", "n_kv_heads", "d_head", "d_ff", "mlp",
+                                        "act_mode", "weight_bits", "act_bits", "kv_bits")]
+
+
+def lib():
+    """Load the CUDA library (fails loudly when it is missing)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback exists)")
+        L = C.CDLL(LIB_PATH)
+        vp, ip, dp, fp = C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_double), C.POINTER(C.c_float)
+        L.qt_last_error.restype = C.c_char_p
+        L.qt_engine_create.argtypes = [C.POINTER(_Config), C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(vp)]
+        L.qt_engine_destroy.argtypes = [vp]
+        L.qt_engine_destroy.restype = None
+        L.qt_engine_set_stream.argtypes = [vp, vp]
+        L.qt_engine_synchronize.argtypes = [vp]
+        L.qt_engine_load_layer.argtypes = [vp, C.c_int] + [vp] * 9 + [C.c_int]
+        L.qt_engine_load_head.argtypes = [vp, vp, vp, C.c_int]
+        L.qt_engine_set_act_scales.argtypes = [vp, dp]
+        L.qt_engine_set_recipe.argtypes = [vp, C.c_int, ip, dp, dp, C.c_int, C.c_int]
+        L.qt_recipe_parse.argtypes = [C.c_char_p, C.c_int, ip, ip, dp, dp, ip, C.c_char_p, C.c_int]
+        L.qt_engine_prefill.argtypes = [vp, C.c_int, vp, C.c_int, ip, ip, ip, ip, vp, C.c_int]
+        L.qt_engine_prefill_rows.argtypes = [vp]
+        L.qt_engine_decode.argtypes = [vp, vp, C.c_int, vp, C.c_int]
+        L.qt_engine_layout.argtypes = [vp, C.c_int, ip, ip, ip, C.c_int]
+        L.qt_engine_n_prunes.argtypes = [vp, C.c_int]
+        L.qt_engine_prune.argtypes = [vp, C.c_int, C.c_int, ip, ip, ip, C.c_int, ip]
+        L.qt_engine_kv.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_int, vp, fp, ip, C.c_int]
+        L.qt_engine_info.argtypes = [vp, C.POINTER(C.c_int64)]
+        L.qt_rmsnorm_quant_i4.argtypes = [vp, C.c_int, C.c_int, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double,
+                                          vp, C.c_int, vp, vp, vp]
+        L.qt_w4a4_gemm.argtypes = [C.c_int, vp, C.c_int, vp, vp, C.c_int, vp, C.c_int, C.c_int, C.c_int, vp, C.c_int,
+                                   vp, C.c_int, vp]
+        L.qt_quant_weight_i4.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_int, vp, C.c_int, vp, vp, vp]
+        L.qt_kv_quant_append_i4.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp, vp, vp,
+                                            C.c_int, vp, C.c_int64, vp, vp]
+        L.qt_rope_table.argtypes = [C.c_int, C.c_int, dp]
+        _lib = L
+    return _lib
+
+
+def _raise(rc):
+    msg = lib().qt_last_error().decode()
+    cls = {QT_EINVAL: QuotaInvalidArgument, QT_ERUNTIME: QuotaRuntimeError, QT_ERANGE: QuotaOutOfRange}.get(
+        rc, QuotaError)
+    raise cls(rc, msg)
+
+
+def check(rc):
+    if rc != 0:
+        _raise(rc)
+    return rc
+
+
+def _ptr(t):
+    """Device or host pointer of a torch tensor / numpy array (None passes through)."""
+    if t is None:
+        return None
+    if isinstance(t, np.ndarray):
+        return t.ctypes.data_as(C.c_void_p)
+    return C.c_void_p(t.data_ptr())
+
+
+def _i32(a):
+    return None if a is None else np.ascontiguousarray(a, dtype=np.int32)
+
+
+def _ip(a):
+    return None if a is None else a.ctypes.data_as(C.POINTER(C.c_int))
+
+
+@dataclass
+class Config:
+    """Shape + semantic switches (include/quota_b200.h qt_config)."""
+
+    n_layers: int = 4
+    d_model: int = 256
+    n_heads: int = 4
+    n_kv_heads: int = 4
+    d_head: int = 64
+    d_ff: int = 1024
+    mlp: int = 0
+    act_mode: int = 0
+    weight_bits: int = 4
+    act_bits: int = 4
+    kv_bits: int = 4
+
+    def c(self):
+        return _Config(*[getattr(self, f) for f, _ in _Config._fields_])
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        return None
+    if isinstance(stream, int):
+        return C.c_void_p(stream)
+    return C.c_void_p(stream.cuda_stream)
+
+
+class Engine:
+    """Owner of one device engine (weights, KV pool, buffers) on the current GPU."""
+
+    def __init__(self, cfg: Config, max_batch=8, max_tokens=8192, max_seq=4096, max_decode=128):
+        self.cfg = cfg
+        self.h = C.c_void_p()
+        check(lib().qt_engine_create(C.byref(cfg.c()), max_batch, max_tokens, max_seq, max_decode, C.byref(self.h)))
+
+    def close(self):
+        if self.h:
+            lib().qt_engine_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_stream(self, stream):
+        check(lib().qt_engine_set_stream(self.h, _stream_ptr(stream)))
+
+    def synchronize(self):
+        check(lib().qt_engine_synchronize(self.h))
+
+    def load_layer(self, layer, wq, wk, wv, wo, w1, w2, w3=None, g1=None, g2=None):
+        """Weights in reference orientation [d_in x d_out]: numpy fp32 (host) or torch fp32 cuda tensors."""
+        arrs = [wq, wk, wv, wo, w1, w2, w3, g1, g2]
+        on_dev = int(any(a is not None and not isinstance(a, np.ndarray) for a in arrs))
+        keep = [None if a is None else (np.ascontiguousarray(a, dtype=np.float32) if isinstance(a, np.ndarray)
+                                        else a.contiguous()) for a in arrs]
+        check(lib().qt_engine_load_layer(self.h, layer, *[_ptr(a) for a in keep], on_dev))
+
+    def load_head(self, w_head, gf=None):
+        arrs = [w_head, gf]
+        on_dev = int(any(a is not None and not isinstance(a, np.ndarray) for a in arrs))
+        keep = [None if a is None else (np.ascontiguousarray(a, dtype=np.float32) if isinstance(a, np.ndarray)
+                                        else a.contiguous()) for a in arrs]
+        check(lib().qt_engine_load_head(self.h, _ptr(keep[0]), _ptr(keep[1]), on_dev))
+
+    def load_weights(self, w):
+        """w: oracle.Weights-like object (fp64 numpy, reference orientation)."""
+        for l, lw in enumerate(w.layers):
+            self.load_layer(l, lw["wq"], lw["wk"], lw["wv"], lw["wo"], lw["w1"], lw["w2"], lw.get("w3"),
+                            lw.get("g1"), lw.get("g2"))
+        self.load_head(w.head, w.gf)
+
+    def set_act_scales(self, scales):
+        a = np.ascontiguousarray(scales, dtype=np.float64)
+        check(lib().qt_engine_set_act_scales(self.h, a.ctypes.data_as(C.POINTER(C.c_double))))
+
+    def set_recipe(self, layers, keeps, weights=(0.25, 0.45, 0.10, 0.20), v0=64, res_bits=4):
+        la = _i32(layers)
+        ka = np.ascontiguousarray(keeps, dtype=np.float64)
+        wa = np.ascontiguousarray(weights, dtype=np.float64)
+        check(lib().qt_engine_set_recipe(self.h, len(la), _ip(la), ka.ctypes.data_as(C.POINTER(C.c_double)),
+                                         wa.ctypes.data_as(C.POINTER(C.c_double)), v0, res_bits))
+
+    def clear_recipe(self):
+        check(lib().qt_engine_set_recipe(self.h, 0, None, None, None, 1, 4))
+
+    def prefill(self, emb, visual, text, v0=None, positions=None, logits_out=None):
+        """emb: packed [sum(S) x d] (numpy fp32 host or torch fp32 cuda).  Returns logits
+        (numpy, or writes into logits_out when given)."""
+        visual, text = _i32(visual), _i32(text)
+        on_dev = 0 if isinstance(emb, np.ndarray) else 1
+        if on_dev == 0:
+            emb = np.ascontiguousarray(emb, dtype=np.float32)
+        v0a, pa = _i32(v0), _i32(positions)
+        if logits_out is None:
+            # host output sized by the worst case, trimmed after
+            out = np.empty((int(np.sum(visual + text)), self.cfg.d_model), dtype=np.float32)
+            out_dev = 0
+        else:
+            out = logits_out
+            out_dev = 0 if isinstance(out, np.ndarray) else 1
+        check(lib().qt_engine_prefill(self.h, len(visual), _ptr(emb), on_dev, _ip(visual), _ip(text), _ip(v0a),
+                                      _ip(pa), _ptr(out), out_dev))
+        rows = lib().qt_engine_prefill_rows(self.h)
+        return out[:rows]
+
+    def decode(self, emb, logits_out=None):
+        on_dev = 0 if isinstance(emb, np.ndarray) else 1
+        if on_dev == 0:
+            emb = np.ascontiguousarray(emb, dtype=np.float32)
+        if logits_out is None:
+            out = np.empty((emb.shape[0], self.cfg.d_model), dtype=np.float32)
+            out_dev = 0
+        else:
+            out = logits_out
+            out_dev = 0 if isinstance(out, np.ndarray) else 1
+        check(lib().qt_engine_decode(self.h, _ptr(emb), on_dev, _ptr(out), out_dev))
+        return out
+
+    def layout(self, seq):
+        v, t = C.c_int(), C.c_int()
+        pos = np.empty(1 << 16, dtype=np.int32)
+        check(lib().qt_engine_layout(self.h, seq, C.byref(v), C.byref(t), _ip(pos), pos.size))
+        return v.value, t.value, pos[:v.value + t.value].copy()
+
+    def trace(self, seq):
+        n = lib().qt_engine_n_prunes(self.h, seq)
+        out = []
+        for i in range(n):
+            lay, bud, cnt = C.c_int(), C.c_int(), C.c_int()
+            ps = np.empty(1 << 16, dtype=np.int32)
+            check(lib().qt_engine_prune(self.h, seq, i, C.byref(lay), C.byref(bud), _ip(ps), ps.size, C.byref(cnt)))
+            out.append((lay.value, bud.value, ps[:cnt.value].copy()))
+        return out
+
+    def kv(self, layer, seq, head, which):
+        rows = C.c_int()
+        check(lib().qt_engine_kv(self.h, layer, seq, head, which, None, None, C.byref(rows), 0))
+        n = rows.value
+        codes = np.empty((n, self.cfg.d_head), dtype=np.int8)
+        scales = np.empty(n, dtype=np.float32)
+        check(lib().qt_engine_kv(self.h, layer, seq, head, which, codes.ctypes.data_as(C.c_void_p),
+                                 scales.ctypes.data_as(C.POINTER(C.c_float)), C.byref(rows), n))
+        return codes, scales
+
+    def info(self):
+        o = (C.c_int64 * 16)()
+        lib().qt_engine_info(self.h, o)
+        keys = ["stream", "n_pages", "page_bytes", "dec_splits", "dec_pps", "final_rows", "batch", "decode_steps",
+                "decode_weight_bytes", "kv_rows", "pool", "n_qkv", "kd_pad", "kff_pad", "n_gu", "_"]
+        return dict(zip(keys, list(o)))
+
+
+# ---------------------------------------------------------------- kernel-level ABI (torch tensors)
+
+
+def rmsnorm_quant(x, gain, d_pad, act_mode, static_scale=0.0, codes=None, scales=None, normed=None, stream=0):
+    """K1 on a torch fp32/fp64 cuda tensor x [M x D]; returns (packed codes, fp64 scales)."""
+    import torch
+    M, D = x.shape
+    if codes is None:
+        codes = torch.zeros((M, d_pad // 2), dtype=torch.uint8, device=x.device)
+    if scales is None:
+        scales = torch.zeros(M, dtype=torch.float64, device=x.device)
+    is64 = int(x.dtype == torch.float64)
+    check(lib().qt_rmsnorm_quant_i4(_ptr(x), is64, x.stride(0), _ptr(gain), M, D, d_pad, act_mode,
+                                    float(static_scale), _ptr(codes), codes.stride(0), _ptr(scales), _ptr(normed),
+                                    C.c_void_p(stream)))
+    return codes, scales
+
+
+def w4a4_gemm(epi, a_codes, a_scales, w_codes, w_scales, M, N, K, out, acc_out=None, impl=0, stream=0):
+    check(lib().qt_w4a4_gemm(epi, _ptr(a_codes), a_codes.stride(0), _ptr(a_scales), _ptr(w_codes), w_codes.stride(0),
+                             _ptr(w_scales), M, N, K, _ptr(out), out.stride(0), _ptr(acc_out), impl,
+                             C.c_void_p(stream)))
+    return out
+
+
+def quant_weight(w, k_pad, n_pad, row_mul=1, row_add=0, codes=None, scales=None, stream=0):
+    import torch
+    K, N = w.shape
+    if codes is None:
+        codes = torch.zeros((n_pad, k_pad // 2), dtype=torch.uint8, device=w.device)
+    if scales is None:
+        scales = torch.zeros(n_pad, dtype=torch.float64, device=w.device)
+    scratch = torch.zeros(max(N, 64), dtype=torch.float64, device=w.device)
+    check(lib().qt_quant_weight_i4(_ptr(w), K, N, row_mul, row_add, _ptr(codes), codes.stride(0), _ptr(scales),
+                                   _ptr(scratch), C.c_void_p(stream)))
+    return codes, scales
+
+
+def rope_table(max_pos, d_head):
+    out = np.empty((max_pos, d_head // 2, 2), dtype=np.float64)
+    lib().qt_rope_table(max_pos, d_head, out.ctypes.data_as(C.POINTER(C.c_double)))
+    return out
+
+
+def unpack_i4(codes_u8, n):
+    """Host helper for tests: packed int4 (low nibble first) -> int8 [.., n]."""
+    c = np.asarray(codes_u8, dtype=np.uint8)
+    lo = (c & 0xF).astype(np.int16)
+    hi = (c >> 4).astype(np.int16)
+    out = np.empty(c.shape[:-1] + (c.shape[-1] * 2,), dtype=np.int16)
+    out[..., 0::2] = lo
+    out[..., 1::2] = hi
+    out = np.where(out >= 8, out - 16, out).astype(np.int8)
+    return out[..., :n]
+
+
+def exported_symbols():
+    """Function names declared in include/quota_b200.h."""
+    import re
+    txt = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:const\s+char\*|int|void)\s+(qt_\w+)\s*\(", txt, flags=re.M)))

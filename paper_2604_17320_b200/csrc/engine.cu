@@ -1,0 +1,1030 @@
+// engine.cu -- C++ host runtime of the QUOTA hot path + the C ABI
+// (include/quota_b200.h).
+//
+// Restates the control flow of forward_prefill / decode_step
+// (/root/reference/proj/src/model.cpp:315-562) and make_recipe_hook /
+// apply_pruning (selector.cpp:138-228) for a batch of independent sequences
+// packed back to back; every operator is a device kernel (k_*.cu), the host
+// only schedules, allocates and tracks shapes.  All shapes after pruning are
+// known on the host (budget = ceil(r * v0), selector.cpp:11-17), so a prefill
+// never synchronises on device results; a decode step is captured once into a
+// CUDA graph and replayed (its lengths and positions live in device memory).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/quota_b200.h"
+#include "qt_common.cuh"
+#include "qt_kernels.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+struct QtError : std::runtime_error {
+    int code;
+    QtError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw QtError(code, msg); }
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(QT_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+const bool g_trace = std::getenv("QT_TRACE") != nullptr;
+const bool g_nograph = std::getenv("QT_NOGRAPH") != nullptr;
+bool g_capturing = false;
+
+void ckl(int rc, const char* what) {
+    if (g_trace && !g_capturing) {
+        cudaError_t se = cudaDeviceSynchronize();
+        std::fprintf(stderr, "[qt] %s rc=%d sync=%s\n", what, rc, cudaGetErrorString(se));
+    }
+    if (rc != 0) {
+        cudaError_t e = cudaGetLastError();
+        fail(rc > 0 ? QT_ECUDA : QT_EINVAL,
+             std::string(what) + (rc > 0 ? std::string(": ") + cudaGetErrorString((cudaError_t)rc)
+                                          : std::string(": unsupported shape")) +
+                 (e != cudaSuccess ? std::string(" / ") + cudaGetErrorString(e) : std::string()));
+    }
+}
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return QT_OK;
+    } catch (const QtError& e) {
+        g_err = e.what();
+        return e.code;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return QT_EINVAL;
+    } catch (const std::out_of_range& e) {
+        g_err = e.what();
+        return QT_ERANGE;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return QT_ERUNTIME;
+    }
+}
+
+int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+template <class T>
+T* dalloc(size_t n) {
+    void* p = nullptr;
+    if (n == 0) n = 1;
+    ck(cudaMalloc(&p, n * sizeof(T)), "cudaMalloc");
+    ck(cudaMemset(p, 0, n * sizeof(T)), "cudaMemset");
+    return static_cast<T*>(p);
+}
+
+struct LayerW {
+    uint8_t* qkv = nullptr;
+    double* s_qkv = nullptr;
+    uint8_t* o = nullptr;
+    double* s_o = nullptr;
+    uint8_t* gu = nullptr;
+    double* s_gu = nullptr;
+    uint8_t* down = nullptr;
+    double* s_down = nullptr;
+    float* g1 = nullptr;
+    float* g2 = nullptr;
+    bool loaded = false;
+};
+
+struct Recipe {
+    std::vector<int> layers;
+    std::vector<double> keeps;
+    double w[4] = {0.25, 0.45, 0.10, 0.20};
+    int v0 = 64;
+    int res_bits = 4;
+};
+
+struct PruneEv {
+    int layer, budget;
+    std::vector<int> positions;
+};
+
+}  // namespace
+
+struct qt_engine {
+    qt_config cfg{};
+    int L = 0, d = 0, H = 0, Hkv = 0, dh = 0, dff = 0;
+    int n_qkv = 0, n_qkv_pad = 0, kd_pad = 0, kff_pad = 0, n_gu = 0, n_gu_pad = 0, nd_pad = 0;
+    int max_batch = 0, max_tokens = 0, max_seq = 0, max_decode = 0, max_pos = 0;
+    cudaStream_t own_stream = nullptr, st = nullptr;
+
+    std::vector<LayerW> lw;
+    uint8_t* head = nullptr;
+    double* s_head = nullptr;
+    float* gf = nullptr;
+    bool head_loaded = false;
+    std::vector<double> act;  // 4L + 1
+    bool act_set = false;
+    Recipe recipe;
+    bool have_recipe = false;
+
+    // activations (prefill capacity)
+    double* x[2] = {nullptr, nullptr};  // fp64 residual stream
+    int* pos[2] = {nullptr, nullptr};
+    float* qkv = nullptr;
+    float* attn = nullptr;
+    float* mid = nullptr;
+    uint8_t* codes = nullptr;
+    double* ascale = nullptr;
+    float* logits = nullptr;
+    float* ml = nullptr;
+    int* tok_seq = nullptr;
+    int* tok_row = nullptr;
+    int* seq_off = nullptr;  // [max_batch + 1]
+    int* seq_vis = nullptr;
+    int* seq_txt = nullptr;
+    int* seq_len = nullptr;
+    // scoring
+    int vstride = 0;
+    double* mag = nullptr;
+    double* res = nullptr;
+    float* inter = nullptr;
+    float* intra = nullptr;
+    double* w4 = nullptr;
+    int* budget = nullptr;
+    int* new_off = nullptr;
+    int* new_len = nullptr;
+    int* keep_src = nullptr;
+    int* keep_local = nullptr;
+    int* kept_pos = nullptr;
+    double* rope = nullptr;
+    double* wscratch = nullptr;
+    float* wstage = nullptr;
+    size_t wstage_elems = 0;
+
+    // KV cache
+    uint8_t* pool = nullptr;
+    long long page_bytes = 0;
+    int n_pages_cap = 0;
+    int max_pages = 0;       // per (layer, seq)
+    int* pt = nullptr;       // [L][max_batch][max_pages]
+    int* kv_len = nullptr;   // [L][max_batch]
+    int* next_pos = nullptr; // [max_batch]
+    int* dec_seq = nullptr;  // [max_batch] = 0..B-1
+
+    // decode
+    double* xd = nullptr;      // [max_batch x d] fp64 residual
+    float* xd_in = nullptr;    // [max_batch x d] fp32 input staging
+    float* dlogits = nullptr;  // [max_batch x d]
+    float* part_ml = nullptr;
+    float* part_o = nullptr;
+    int dec_splits = 1, dec_pps = 1;
+    cudaGraphExec_t graph = nullptr;
+    bool graph_ok = false;
+    int decode_steps = 0;
+
+    // host staging (pinned)
+    char* pin = nullptr;
+    size_t pin_cap = 0, pin_used = 0;
+
+    // state of the last prefill
+    int B = 0;
+    int final_rows = 0;
+    std::vector<int> h_vis, h_txt, h_off;
+    std::vector<std::vector<int>> h_pos;  // final layout positions per seq
+    std::vector<std::vector<PruneEv>> trace;
+    std::vector<int> h_kvlen;             // [L][B]
+    bool prefilled = false;
+    bool use_tc05 = false;
+    std::vector<int> h_next;
+
+    ~qt_engine() {
+        cudaStreamSynchronize(st ? st : 0);
+        if (graph) cudaGraphExecDestroy(graph);
+        auto f = [](void* p) {
+            if (p) cudaFree(p);
+        };
+        for (auto& l : lw) {
+            f(l.qkv); f(l.s_qkv); f(l.o); f(l.s_o); f(l.gu); f(l.s_gu); f(l.down); f(l.s_down); f(l.g1); f(l.g2);
+        }
+        f(head); f(s_head); f(gf);
+        f(x[0]); f(x[1]); f(pos[0]); f(pos[1]); f(qkv); f(attn); f(mid); f(codes); f(ascale); f(logits); f(ml);
+        f(tok_seq); f(tok_row); f(seq_off); f(seq_vis); f(seq_txt); f(seq_len);
+        f(mag); f(res); f(inter); f(intra); f(w4); f(budget); f(new_off); f(new_len); f(keep_src); f(keep_local);
+        f(kept_pos); f(rope); f(wscratch); f(wstage); f(pool); f(pt); f(kv_len); f(next_pos); f(dec_seq);
+        f(xd); f(xd_in); f(dlogits); f(part_ml); f(part_o);
+        if (pin) cudaFreeHost(pin);
+        if (own_stream) cudaStreamDestroy(own_stream);
+    }
+
+    // ------------------------------------------------------------ staging
+    template <class T>
+    T* stage(const T* src, size_t n) {
+        size_t bytes = (n * sizeof(T) + 255) / 256 * 256;
+        if (pin_used + bytes > pin_cap) fail(QT_EINVAL, "host staging buffer exhausted");
+        T* p = reinterpret_cast<T*>(pin + pin_used);
+        pin_used += bytes;
+        std::memcpy(p, src, n * sizeof(T));
+        return p;
+    }
+    template <class T>
+    void upload(T* dst, const std::vector<T>& v) {
+        if (v.empty()) return;
+        T* p = stage(v.data(), v.size());
+        ck(cudaMemcpyAsync(dst, p, v.size() * sizeof(T), cudaMemcpyHostToDevice, st), "upload");
+    }
+    void reset_staging() {
+        ck(cudaStreamSynchronize(st), "stream sync");
+        pin_used = 0;
+    }
+
+    // ------------------------------------------------------------ setup
+    void init(const qt_config& c, int mb, int mt, int ms, int md) {
+        cfg = c;
+        L = c.n_layers; d = c.d_model; H = c.n_heads; Hkv = c.n_kv_heads; dh = c.d_head; dff = c.d_ff;
+        if (L < 1 || d < 8 || H < 1 || dh < 2) fail(QT_EINVAL, "invalid model config");
+        if (dh % 2 != 0) fail(QT_EINVAL, "d_head must be even and >= 2");            // model.cpp:50-52
+        if (d != H * dh) fail(QT_EINVAL, "d_model must equal n_heads * d_head");     // model.cpp:53-55
+        if (dh != 64 && dh != 128) fail(QT_EINVAL, "d_head must be 64 or 128 on the B200 path");
+        if (Hkv < 1 || H % Hkv != 0) fail(QT_EINVAL, "n_heads must be a multiple of n_kv_heads");
+        if (c.weight_bits != 4 || c.act_bits != 4 || c.kv_bits != 4)
+            fail(QT_EINVAL, "the B200 path implements W4A4KV4 only");
+        if (c.mlp != 0 && c.mlp != 1) fail(QT_EINVAL, "mlp must be 0 (SiLU) or 1 (SwiGLU)");
+        if (c.act_mode != 0 && c.act_mode != 1) fail(QT_EINVAL, "act_mode must be 0 (static) or 1 (dynamic)");
+        if (d % 8 != 0 || dff % 8 != 0) fail(QT_EINVAL, "d_model and d_ff must be multiples of 8");
+        max_batch = mb; max_tokens = mt; max_seq = ms; max_decode = md;
+        if (mb < 1 || mt < 1 || ms < 1 || md < 0) fail(QT_EINVAL, "invalid capacity");
+        n_qkv = (H + 2 * Hkv) * dh;
+        n_qkv_pad = round_up(n_qkv, 128);
+        kd_pad = round_up(d, 128);
+        kff_pad = round_up(dff, 128);
+        n_gu = c.mlp == 1 ? 2 * dff : dff;
+        n_gu_pad = round_up(n_gu, 128);
+        nd_pad = round_up(d, 128);
+        max_pos = ms + md + 1;
+
+        ck(cudaStreamCreateWithFlags(&own_stream, cudaStreamNonBlocking), "stream");
+        st = own_stream;
+        lw.resize(L);
+        for (auto& l : lw) {
+            l.qkv = dalloc<uint8_t>((size_t)n_qkv_pad * kd_pad / 2);
+            l.s_qkv = dalloc<double>(n_qkv_pad);
+            l.o = dalloc<uint8_t>((size_t)nd_pad * kd_pad / 2);
+            l.s_o = dalloc<double>(nd_pad);
+            l.gu = dalloc<uint8_t>((size_t)n_gu_pad * kd_pad / 2);
+            l.s_gu = dalloc<double>(n_gu_pad);
+            l.down = dalloc<uint8_t>((size_t)nd_pad * kff_pad / 2);
+            l.s_down = dalloc<double>(nd_pad);
+            l.g1 = dalloc<float>(d);
+            l.g2 = dalloc<float>(d);
+        }
+        head = dalloc<uint8_t>((size_t)nd_pad * kd_pad / 2);
+        s_head = dalloc<double>(nd_pad);
+        gf = dalloc<float>(d);
+
+        const size_t T = mt;
+        x[0] = dalloc<double>(T * d);
+        x[1] = dalloc<double>(T * d);
+        pos[0] = dalloc<int>(T);
+        pos[1] = dalloc<int>(T);
+        qkv = dalloc<float>(T * n_qkv);
+        attn = dalloc<float>(T * d);
+        mid = dalloc<float>(T * dff);
+        codes = dalloc<uint8_t>(T * (size_t)std::max(kd_pad, kff_pad) / 2);
+        ascale = dalloc<double>(T);
+        logits = dalloc<float>(T * d);
+        ml = dalloc<float>(T * H * 2);
+        tok_seq = dalloc<int>(T);
+        tok_row = dalloc<int>(T);
+        seq_off = dalloc<int>(mb + 1);
+        seq_vis = dalloc<int>(mb);
+        seq_txt = dalloc<int>(mb);
+        seq_len = dalloc<int>(mb);
+        vstride = round_up(std::min(ms, mt), 64);
+        mag = dalloc<double>((size_t)mb * vstride);
+        res = dalloc<double>((size_t)mb * vstride);
+        inter = dalloc<float>((size_t)mb * H * vstride);
+        intra = dalloc<float>((size_t)mb * H * vstride);
+        w4 = dalloc<double>(4);
+        budget = dalloc<int>(mb);
+        new_off = dalloc<int>(mb + 1);
+        new_len = dalloc<int>(mb);
+        keep_src = dalloc<int>(T);
+        keep_local = dalloc<int>((size_t)mb * vstride);
+        kept_pos = dalloc<int>((size_t)L * mb * vstride);
+        wscratch = dalloc<double>(std::max({n_qkv_pad, n_gu_pad, nd_pad, kff_pad}) + 64);
+
+        // RoPE table with the reference's own libm (model.cpp:156-168)
+        std::vector<double> tab((size_t)max_pos * dh);
+        qt_rope_table(max_pos, dh, tab.data());
+        rope = dalloc<double>(tab.size());
+        ck(cudaMemcpy(rope, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice), "rope upload");
+
+        page_bytes = (long long)2 * Hkv * qt::kPage * (dh / 2 + 4);
+        max_pages = (ms + md + qt::kPage - 1) / qt::kPage;
+        pt = dalloc<int>((size_t)L * mb * max_pages);
+        kv_len = dalloc<int>((size_t)L * mb);
+        next_pos = dalloc<int>(mb);
+        dec_seq = dalloc<int>(mb);
+        xd = dalloc<double>((size_t)mb * d);
+        xd_in = dalloc<float>((size_t)mb * d);
+        dlogits = dalloc<float>((size_t)mb * d);
+        dec_pps = 1;
+        dec_splits = max_pages;
+        part_ml = dalloc<float>((size_t)mb * H * dec_splits * 2);
+        part_o = dalloc<float>((size_t)mb * H * dec_splits * dh);
+        pin_cap = (size_t)64 << 20;
+        pin_cap += (size_t)mt * (sizeof(int) * 8);
+        ck(cudaMallocHost(&pin, pin_cap), "cudaMallocHost");
+    }
+
+    void ensure_pool(int pages) {
+        if (pages <= n_pages_cap) return;
+        ck(cudaStreamSynchronize(st), "sync");
+        if (pool) cudaFree(pool);
+        pool = nullptr;
+        n_pages_cap = 0;
+        void* p = nullptr;
+        ck(cudaMalloc(&p, (size_t)pages * page_bytes), "KV pool cudaMalloc");
+        ck(cudaMemset(p, 0, (size_t)pages * page_bytes), "KV pool memset");
+        pool = static_cast<uint8_t*>(p);
+        n_pages_cap = pages;
+    }
+
+    const float* to_device_f32(const float* src, size_t n, int on_device, float* slot_hint) {
+        if (on_device) return src;
+        (void)slot_hint;
+        if (n > wstage_elems) {
+            if (wstage) cudaFree(wstage);
+            wstage = dalloc<float>(n);
+            wstage_elems = n;
+        }
+        ck(cudaMemcpyAsync(wstage, src, n * sizeof(float), cudaMemcpyHostToDevice, st), "weight upload");
+        return wstage;
+    }
+
+    void quant_into(const float* w, int K, int N, int on_device, int row_mul, int row_add, uint8_t* codes_dst,
+                    int ldc, double* scales_dst) {
+        const float* dw = to_device_f32(w, (size_t)K * N, on_device, nullptr);
+        ckl(qt_launch_weight_quant(dw, K, N, 4, row_mul, row_add, codes_dst, ldc, scales_dst, wscratch, st),
+            "weight quantize");
+        ck(cudaStreamSynchronize(st), "weight quantize");
+    }
+
+    void load_gain(float* dst, const float* g, int on_device) {
+        if (!g) {
+            std::vector<float> ones(d, 1.0f);
+            ck(cudaMemcpy(dst, ones.data(), d * sizeof(float), cudaMemcpyHostToDevice), "gain");
+            return;
+        }
+        ck(cudaMemcpy(dst, g, d * sizeof(float), on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice),
+           "gain");
+    }
+
+    // ------------------------------------------------------------ kernels
+    void norm_quant(const void* xin, int is_f64, int ldx, const float* gain, int M, int D, int dpad, int site_idx) {
+        const int mode = cfg.act_mode;
+        const double s = mode == 0 ? act[site_idx] : 0.0;
+        ckl(qt_launch_norm_quant(xin, is_f64, ldx, gain, M, D, dpad, 4, mode, s, codes, dpad / 2, ascale, nullptr, st),
+            "rmsnorm+quant");
+    }
+    void gemm(int epi, const uint8_t* w, const double* sw, int M, int N, int K, void* out, int ldo) {
+        int rc = (use_tc05 && M > 16)
+                     ? qt_launch_w4a4_tc05(epi, codes, K / 2, ascale, w, K / 2, sw, M, N, K, out, ldo, nullptr, st)
+                     : qt_launch_w4a4_mma(epi, codes, K / 2, ascale, w, K / 2, sw, M, N, K, out, ldo, nullptr, st);
+        ckl(rc, "w4a4 gemm");
+    }
+
+    // ------------------------------------------------------------ prefill
+    struct SeqPlan {
+        int V, T, v0;
+        std::vector<int> vis_at;  // visual count entering each layer
+    };
+
+    void prefill(int nseq, const float* emb, int emb_dev, const int* vis, const int* txt, const int* v0s,
+                 const int* positions, float* logits_out, int out_dev) {
+        for (auto& l : lw)
+            if (!l.loaded) fail(QT_EINVAL, "model weights not loaded");
+        if (!head_loaded) fail(QT_EINVAL, "model head not loaded");
+        if (cfg.act_mode == 0 && !act_set) fail(QT_EINVAL, "quantized mode requires a QuantEnv");  // model.cpp:323-325
+        if (nseq < 1 || nseq > max_batch) fail(QT_EINVAL, "batch size outside engine capacity");
+        reset_staging();
+        graph_ok = false;
+        prefilled = false;
+        B = nseq;
+        h_vis.assign(vis, vis + B);
+        h_txt.assign(txt, txt + B);
+        std::vector<int> v0v(B);
+        int total = 0;
+        for (int b = 0; b < B; ++b) {
+            if (h_vis[b] < 0 || h_txt[b] < 0) fail(QT_EINVAL, "negative token count");  // model.cpp:59
+            const int S = h_vis[b] + h_txt[b];
+            if (S < 1) fail(QT_EINVAL, "empty sequence");
+            if (S > max_seq) fail(QT_EINVAL, "sequence longer than engine capacity");
+            total += S;
+            v0v[b] = v0s ? v0s[b] : recipe.v0;
+            if (have_recipe && v0v[b] < 1) fail(QT_EINVAL, "v0 must be >= 1");
+        }
+        if (total > max_tokens) fail(QT_EINVAL, "batch tokens exceed engine capacity");
+        // positions: strictly increasing per sequence (model.cpp:64-68)
+        std::vector<int> hpos(total);
+        {
+            int o = 0;
+            for (int b = 0; b < B; ++b) {
+                const int S = h_vis[b] + h_txt[b];
+                for (int i = 0; i < S; ++i) hpos[o + i] = positions ? positions[o + i] : i;
+                for (int i = 0; i + 1 < S; ++i)
+                    if (hpos[o + i] >= hpos[o + i + 1]) fail(QT_EINVAL, "position_ids must be strictly increasing");
+                if (hpos[o + S - 1] + 1 + max_decode >= max_pos || hpos[o] < 0)
+                    fail(QT_EINVAL, "position ids outside the engine's RoPE table");
+                o += S;
+            }
+        }
+        // per-layer visual counts (host-side shape plan; selector.cpp:11-17, gflops.cpp:53-72)
+        std::vector<std::vector<int>> vis_at(B, std::vector<int>(L + 1));
+        std::vector<std::vector<int>> kbud(B, std::vector<int>(L, -1));  // budget at candidate layers
+        for (int b = 0; b < B; ++b) {
+            int v = h_vis[b];
+            for (int l = 0; l < L; ++l) {
+                vis_at[b][l] = v;
+                if (have_recipe) {
+                    for (size_t i = 0; i < recipe.layers.size(); ++i) {
+                        if (recipe.layers[i] != l) continue;
+                        const int K = (int)std::ceil(recipe.keeps[i] * (double)v0v[b]);
+                        kbud[b][l] = K;
+                        if (K < v) v = K;
+                    }
+                }
+            }
+            vis_at[b][L] = v;
+        }
+        // KV pages: capacity per (layer, seq) = tokens entering the layer + decode steps
+        std::vector<int> hpt((size_t)L * max_batch * max_pages, 0);
+        int npages = 0;
+        for (int l = 0; l < L; ++l)
+            for (int b = 0; b < B; ++b) {
+                const int cap = vis_at[b][l] + h_txt[b] + max_decode;
+                const int np = (cap + qt::kPage - 1) / qt::kPage;
+                for (int p = 0; p < np; ++p) hpt[((size_t)l * max_batch + b) * max_pages + p] = npages++;
+            }
+        ensure_pool(npages);
+        upload(pt, hpt);
+
+        // inputs
+        double* xc = x[0];
+        int* pc = pos[0];
+        const float* emb_d = emb;
+        if (!emb_dev) {  // stage through the fp32 attention buffer, widen on device
+            ck(cudaMemcpyAsync(attn, emb, (size_t)total * d * sizeof(float), cudaMemcpyHostToDevice, st), "emb");
+            emb_d = attn;
+        }
+        ckl(qt_launch_f32_to_f64(emb_d, xc, (long long)total * d, st), "embedding widen");
+        upload(pc, hpos);
+        std::vector<int> cur_v(h_vis);
+        auto upload_layout = [&]() {
+            std::vector<int> off(B + 1), ts, tr, ln(B);
+            off[0] = 0;
+            for (int b = 0; b < B; ++b) {
+                const int S = cur_v[b] + h_txt[b];
+                off[b + 1] = off[b] + S;
+                ln[b] = S;
+                for (int i = 0; i < S; ++i) {
+                    ts.push_back(b);
+                    tr.push_back(i);
+                }
+            }
+            upload(seq_off, off);
+            upload(seq_vis, cur_v);
+            upload(seq_txt, h_txt);
+            upload(seq_len, ln);
+            upload(tok_seq, ts);
+            upload(tok_row, tr);
+            return off;
+        };
+        std::vector<int> off = upload_layout();
+        int M = off[B];
+        std::vector<double> hw4(recipe.w, recipe.w + 4);
+        upload(w4, hw4);
+        trace.assign(B, {});
+        std::vector<int> trace_layers;  // candidate layers that pruned something, in order
+        std::vector<std::vector<int>> ev_prev_v, ev_new_v;
+        h_kvlen.assign((size_t)L * B, 0);
+        std::vector<std::vector<int>> pos_host(B);
+        {
+            int o = 0;
+            for (int b = 0; b < B; ++b) {
+                const int S = h_vis[b] + h_txt[b];
+                pos_host[b].assign(hpos.begin() + o, hpos.begin() + o + S);
+                o += S;
+            }
+        }
+
+        for (int l = 0; l < L; ++l) {
+            const LayerW& w = lw[l];
+            int* ptl = pt + (size_t)l * max_batch * max_pages;
+            // attention block (model.cpp:347-396)
+            norm_quant(xc, 1, d, w.g1, M, d, kd_pad, 4 * l + 0);
+            gemm(QT_EPI_STORE, w.qkv, w.s_qkv, M, n_qkv, kd_pad, qkv, n_qkv);
+            ckl(qt_launch_rope_kv_append(qkv, n_qkv, M, H, Hkv, dh, pc, tok_seq, tok_row, rope, ptl, max_pages, pool,
+                                         page_bytes, 4, nullptr, st),
+                "rope+kv append");
+            int smax = 0, vmax = 0;
+            bool prune_any = false;
+            for (int b = 0; b < B; ++b) {
+                smax = std::max(smax, cur_v[b] + h_txt[b]);
+                vmax = std::max(vmax, cur_v[b]);
+                if (kbud[b][l] >= 0 && kbud[b][l] < cur_v[b]) prune_any = true;
+            }
+            const bool cand = have_recipe && std::any_of(kbud.begin(), kbud.end(), [l](const std::vector<int>& k) { return k[l] >= 0; });
+            ckl(qt_launch_attn_prefill(qkv, n_qkv, H, Hkv, dh, seq_off, seq_vis, seq_len, B, smax, pool, page_bytes,
+                                       ptl, max_pages, attn, d, prune_any ? ml : nullptr, st),
+                "prefill attention");
+            norm_quant(attn, 0, d, nullptr, M, d, kd_pad, 4 * l + 1);
+            gemm(QT_EPI_RESADD, w.o, w.s_o, M, d, kd_pad, xc, d);
+            for (int b = 0; b < B; ++b) h_kvlen[(size_t)l * B + b] = cur_v[b] + h_txt[b];
+
+            // recipe hook at candidate layers (selector.cpp:214-227, model.cpp:404-427)
+            if (cand && prune_any) {
+                if (vmax > vstride) fail(QT_EINVAL, "visual prefix exceeds engine capacity");
+                ckl(qt_launch_attn_colsum(qkv, n_qkv, H, Hkv, dh, seq_off, seq_vis, seq_len, B, vmax, pool, page_bytes,
+                                          ptl, max_pages, ml, vstride, inter, intra, st),
+                    "quota attention metrics");
+                ckl(qt_launch_token_metrics(xc, d, seq_off, seq_vis, vmax, B, vstride, recipe.res_bits, mag, res, st),
+                    "quota token metrics");
+                std::vector<int> bud(B), noff(B + 1), nlen(B), nv(B);
+                noff[0] = 0;
+                for (int b = 0; b < B; ++b) {
+                    const int K = kbud[b][l] >= 0 ? kbud[b][l] : cur_v[b];
+                    nv[b] = std::min(K, cur_v[b]);
+                    bud[b] = std::max(1, nv[b]);
+                    nlen[b] = nv[b] + h_txt[b];
+                    noff[b + 1] = noff[b] + nlen[b];
+                }
+                upload(budget, bud);
+                upload(new_off, noff);
+                upload(new_len, nlen);
+                int* kp_ev = kept_pos + (size_t)trace_layers.size() * max_batch * vstride;
+                ckl(qt_launch_select_topk(mag, res, inter, intra, H, vstride, seq_vis, seq_txt, budget, seq_off, new_off,
+                                          B, vmax, hw4.data(), keep_src, keep_local, vstride, pc, kp_ev, nullptr,
+                                          nullptr, st),
+                    "quota top-k");
+                double* xn = x[xc == x[0] ? 1 : 0];
+                int* pn = pos[pc == pos[0] ? 1 : 0];
+                ckl(qt_launch_gather_rows(xc, xn, d, pc, pn, keep_src, noff[B], st), "compaction gather");
+                ckl(qt_launch_kv_compact(pool, page_bytes, ptl, max_pages, Hkv, dh, keep_local, vstride, new_len, B, st),
+                    "kv compaction");
+                // trace: kept visual positions, read back once after the prefill
+                trace_layers.push_back(l);
+                ev_prev_v.push_back(cur_v);
+                ev_new_v.push_back(nv);
+                for (int b = 0; b < B; ++b) {
+                    h_kvlen[(size_t)l * B + b] = nlen[b];
+                    cur_v[b] = nv[b];
+                }
+                xc = xn;
+                pc = pn;
+                off = upload_layout();
+                M = off[B];
+            }
+            // MLP block (model.cpp:429-437)
+            norm_quant(xc, 1, d, w.g2, M, d, kd_pad, 4 * l + 2);
+            if (cfg.mlp == 1) gemm(QT_EPI_SWIGLU, w.gu, w.s_gu, M, n_gu, kd_pad, mid, dff);
+            else gemm(QT_EPI_SILU, w.gu, w.s_gu, M, n_gu, kd_pad, mid, dff);
+            norm_quant(mid, 0, dff, nullptr, M, dff, kff_pad, 4 * l + 3);
+            gemm(QT_EPI_RESADD, w.down, w.s_down, M, d, kff_pad, xc, d);
+        }
+        // final norm + head (model.cpp:442-445)
+        norm_quant(xc, 1, d, gf, M, d, kd_pad, 4 * L);
+        gemm(QT_EPI_STORE, head, s_head, M, d, kd_pad, logits, d);
+        final_rows = M;
+        if (logits_out)
+            ck(cudaMemcpyAsync(logits_out, logits, (size_t)M * d * sizeof(float),
+                               out_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st),
+               "logits readback");
+
+        // prune trace (PruneEvent, model.cpp:408-418) and final layout positions
+        if (!trace_layers.empty()) {
+            std::vector<int> kp(trace_layers.size() * (size_t)max_batch * vstride);
+            ck(cudaMemcpyAsync(kp.data(), kept_pos, kp.size() * sizeof(int), cudaMemcpyDeviceToHost, st), "trace");
+            ck(cudaStreamSynchronize(st), "trace");
+            for (size_t ev = 0; ev < trace_layers.size(); ++ev) {
+                const int l = trace_layers[ev];
+                for (int b = 0; b < B; ++b) {
+                    const int pv = ev_prev_v[ev][b], nvb = ev_new_v[ev][b];
+                    if (nvb >= pv) continue;
+                    PruneEv e{l, kbud[b][l], {}};
+                    const int* kpv = kp.data() + (ev * max_batch + b) * (size_t)vstride;
+                    e.positions.assign(kpv, kpv + nvb);
+                    trace[b].push_back(e);
+                    std::vector<int> npos(e.positions);
+                    npos.insert(npos.end(), pos_host[b].begin() + pv, pos_host[b].end());
+                    pos_host[b] = npos;
+                }
+            }
+        }
+        // decode state: cache lengths, next positions (model.cpp:447-451)
+        {  // device layout is [L][max_batch]
+            std::vector<int> kl((size_t)L * max_batch, 0);
+            for (int l = 0; l < L; ++l)
+                for (int b = 0; b < B; ++b) kl[(size_t)l * max_batch + b] = h_kvlen[(size_t)l * B + b];
+            upload(kv_len, kl);
+        }
+        std::vector<int> np(B), ds(B);
+        for (int b = 0; b < B; ++b) {
+            np[b] = pos_host[b].back() + 1;
+            ds[b] = b;
+        }
+        // next_position = last ORIGINAL position + 1 of the input layout
+        {
+            int o = 0;
+            for (int b = 0; b < B; ++b) {
+                const int S = h_vis[b] + h_txt[b];
+                np[b] = hpos[o + S - 1] + 1;
+                o += S;
+            }
+        }
+        upload(next_pos, np);
+        upload(dec_seq, ds);
+        h_next = np;
+        h_off = off;
+        h_vis = cur_v;
+        h_pos = pos_host;
+        // decode attention split plan over the largest per-layer capacity
+        int maxp = 1;
+        for (int l = 0; l < L; ++l)
+            for (int b = 0; b < B; ++b) {
+                const int cap = h_kvlen[(size_t)l * B + b] + max_decode;
+                maxp = std::max(maxp, (cap + qt::kPage - 1) / qt::kPage);
+            }
+        const int want_blocks = 4 * 148;
+        int pps = std::max(1, (int)std::ceil((double)maxp * B * H / want_blocks));
+        dec_pps = pps;
+        dec_splits = (maxp + pps - 1) / pps;
+        ck(cudaStreamSynchronize(st), "prefill");
+        decode_steps = 0;
+        prefilled = true;
+    }
+
+    // ------------------------------------------------------------ decode
+    void decode_body() {
+        double* xcur = xd;
+        ckl(qt_launch_f32_to_f64(xd_in, xd, (long long)B * d, st), "embedding widen");
+        for (int l = 0; l < L; ++l) {
+            const LayerW& w = lw[l];
+            int* ptl = pt + (size_t)l * max_batch * max_pages;
+            int* lenl = kv_len + (size_t)l * max_batch;
+            norm_quant(xcur, 1, d, w.g1, B, d, kd_pad, 4 * l + 0);
+            gemm(QT_EPI_STORE, w.qkv, w.s_qkv, B, n_qkv, kd_pad, qkv, n_qkv);
+            ckl(qt_launch_rope_kv_append(qkv, n_qkv, B, H, Hkv, dh, next_pos, dec_seq, lenl, rope, ptl, max_pages,
+                                         pool, page_bytes, 4, nullptr, st),
+                "decode kv append");
+            ckl(qt_launch_attn_decode(qkv, n_qkv, H, Hkv, dh, lenl, 1, B, pool, page_bytes, ptl, max_pages, dec_splits,
+                                      dec_pps, part_ml, part_o, attn, d, st),
+                "decode attention");
+            norm_quant(attn, 0, d, nullptr, B, d, kd_pad, 4 * l + 1);
+            gemm(QT_EPI_RESADD, w.o, w.s_o, B, d, kd_pad, xcur, d);
+            norm_quant(xcur, 1, d, w.g2, B, d, kd_pad, 4 * l + 2);
+            if (cfg.mlp == 1) gemm(QT_EPI_SWIGLU, w.gu, w.s_gu, B, n_gu, kd_pad, mid, dff);
+            else gemm(QT_EPI_SILU, w.gu, w.s_gu, B, n_gu, kd_pad, mid, dff);
+            norm_quant(mid, 0, dff, nullptr, B, dff, kff_pad, 4 * l + 3);
+            gemm(QT_EPI_RESADD, w.down, w.s_down, B, d, kff_pad, xcur, d);
+        }
+        norm_quant(xcur, 1, d, gf, B, d, kd_pad, 4 * L);
+        gemm(QT_EPI_STORE, head, s_head, B, d, kd_pad, dlogits, d);
+        ckl(qt_launch_kv_len_bump(kv_len, L * max_batch, next_pos, B, st), "kv length / position bump");
+    }
+
+    void decode(const float* emb, int emb_dev, float* out, int out_dev) {
+        if (!prefilled) fail(QT_ERUNTIME, "cache and execution mode mismatch");
+        if (decode_steps >= max_decode) fail(QT_EINVAL, "decode steps exceed engine capacity");
+        ck(cudaMemcpyAsync(xd_in, emb, (size_t)B * d * sizeof(float),
+                           emb_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st),
+           "decode emb");
+        if (g_nograph) {
+            decode_body();
+        } else if (!graph_ok) {
+            if (graph) cudaGraphExecDestroy(graph);
+            graph = nullptr;
+            cudaGraph_t g = nullptr;
+            ck(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "graph capture");
+            g_capturing = true;
+            try {
+                decode_body();
+            } catch (...) {
+                g_capturing = false;
+                cudaStreamEndCapture(st, &g);
+                if (g) cudaGraphDestroy(g);
+                throw;
+            }
+            g_capturing = false;
+            ck(cudaStreamEndCapture(st, &g), "graph capture end");
+            ck(cudaGraphInstantiate(&graph, g, 0), "graph instantiate");
+            cudaGraphDestroy(g);
+            graph_ok = true;
+        }
+        if (!g_nograph) ck(cudaGraphLaunch(graph, st), "graph launch");
+        if (out)
+            ck(cudaMemcpyAsync(out, dlogits, (size_t)B * d * sizeof(float),
+                               out_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st),
+               "decode logits");
+        ++decode_steps;
+        for (int b = 0; b < B; ++b) {  // model.cpp:553-556
+            h_txt[b] += 1;
+            h_pos[b].push_back(h_next[b]++);
+        }
+        for (auto& v : h_kvlen) v += 1;
+    }
+};
+
+// kv length / position bump after a decode step (device-resident so the
+// captured graph replays unchanged)
+namespace qt {
+__global__ void k_bump(int* kv_len, int n, int* next_pos, int B) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) kv_len[i] += 1;
+    if (i < B) next_pos[i] += 1;  // model.cpp:556
+}
+}  // namespace qt
+
+extern "C" {
+
+int qt_launch_kv_len_bump(int* kv_len, int n, int* next_pos, int B, cudaStream_t st) {
+    qt::k_bump<<<(std::max(n, B) + 255) / 256, 256, 0, st>>>(kv_len, n, next_pos, B);
+    return (int)cudaGetLastError();
+}
+
+const char* qt_last_error(void) { return g_err.c_str(); }
+
+void qt_set_last_error(const char* msg) { g_err = msg ? msg : ""; }
+
+int qt_rope_table(int max_pos, int d_head, double* out) {
+    // cos/sin of pos * 10000^(-2i/d_head), exactly as rope_in_place (model.cpp:156-168)
+    for (int p = 0; p < max_pos; ++p)
+        for (int i = 0; i < d_head / 2; ++i) {
+            double freq = std::pow(10000.0, -2.0 * static_cast<double>(i) / static_cast<double>(d_head));
+            double ang = static_cast<double>(p) * freq;
+            out[((size_t)p * (d_head / 2) + i) * 2] = std::cos(ang);
+            out[((size_t)p * (d_head / 2) + i) * 2 + 1] = std::sin(ang);
+        }
+    return 0;
+}
+
+int qt_engine_create(const qt_config* cfg, int max_batch, int max_tokens, int max_seq, int max_decode,
+                     qt_engine** out) {
+    return guard([&] {
+        if (!cfg || !out) fail(QT_EINVAL, "null argument");
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+            fail(QT_ECUDA, "no CUDA device: the B200 path has no CPU fallback");
+        auto e = std::make_unique<qt_engine>();
+        e->init(*cfg, max_batch, max_tokens, max_seq, max_decode);
+        *out = e.release();
+    });
+}
+
+void qt_engine_destroy(qt_engine* e) { delete e; }
+
+int qt_engine_set_stream(qt_engine* e, void* stream) {
+    return guard([&] {
+        e->st = stream ? static_cast<cudaStream_t>(stream) : e->own_stream;
+        e->graph_ok = false;
+    });
+}
+
+int qt_engine_synchronize(qt_engine* e) {
+    return guard([&] { ck(cudaStreamSynchronize(e->st), "synchronize"); });
+}
+
+int qt_engine_load_layer(qt_engine* e, int layer, const float* wq, const float* wk, const float* wv,
+                         const float* wo, const float* w1, const float* w2, const float* w3, const float* g1,
+                         const float* g2, int on_device) {
+    return guard([&] {
+        if (layer < 0 || layer >= e->L) fail(QT_ERANGE, "layer out of range");
+        if (!wq || !wk || !wv || !wo || !w1 || !w2) fail(QT_EINVAL, "null weight");
+        if (e->cfg.mlp == 1 && !w3) fail(QT_EINVAL, "SwiGLU needs w3 (up projection)");
+        LayerW& l = e->lw[layer];
+        const int d = e->d, kvd = e->Hkv * e->dh, f = e->dff, ldc = e->kd_pad / 2;
+        e->quant_into(wq, d, d, on_device, 1, 0, l.qkv, ldc, l.s_qkv);
+        e->quant_into(wk, d, kvd, on_device, 1, d, l.qkv, ldc, l.s_qkv);
+        e->quant_into(wv, d, kvd, on_device, 1, d + kvd, l.qkv, ldc, l.s_qkv);
+        e->quant_into(wo, d, d, on_device, 1, 0, l.o, ldc, l.s_o);
+        if (e->cfg.mlp == 1) {
+            e->quant_into(w1, d, f, on_device, 2, 0, l.gu, ldc, l.s_gu);
+            e->quant_into(w3, d, f, on_device, 2, 1, l.gu, ldc, l.s_gu);
+        } else {
+            e->quant_into(w1, d, f, on_device, 1, 0, l.gu, ldc, l.s_gu);
+        }
+        e->quant_into(w2, f, d, on_device, 1, 0, l.down, e->kff_pad / 2, l.s_down);
+        e->load_gain(l.g1, g1, on_device);
+        e->load_gain(l.g2, g2, on_device);
+        l.loaded = true;
+        e->graph_ok = false;
+    });
+}
+
+int qt_engine_load_head(qt_engine* e, const float* w_head, const float* final_gain, int on_device) {
+    return guard([&] {
+        if (!w_head) fail(QT_EINVAL, "null weight");
+        e->quant_into(w_head, e->d, e->d, on_device, 1, 0, e->head, e->kd_pad / 2, e->s_head);
+        e->load_gain(e->gf, final_gain, on_device);
+        e->head_loaded = true;
+        e->graph_ok = false;
+    });
+}
+
+int qt_engine_set_act_scales(qt_engine* e, const double* scales) {
+    return guard([&] {
+        if (!scales) fail(QT_EINVAL, "activation scales do not cover all layers");
+        e->act.assign(scales, scales + 4 * e->L + 1);
+        for (double s : e->act)
+            if (!(s > 0.0) || !std::isfinite(s)) fail(QT_EINVAL, "activation scales must be positive");
+        e->act_set = true;
+        e->graph_ok = false;
+    });
+}
+
+int qt_engine_set_recipe(qt_engine* e, int n, const int* layers, const double* keeps, const double* w4, int v0,
+                         int res_bits) {
+    return guard([&] {
+        if (n == 0) {
+            e->have_recipe = false;
+            return;
+        }
+        // PruningRecipe::validate (recipe.cpp:21-46)
+        if (n < 0 || !layers || !keeps) fail(QT_EINVAL, "candidate_layers and keep_ratios must align and be nonempty");
+        for (int i = 0; i < n; ++i) {
+            if (layers[i] < 0) fail(QT_EINVAL, "negative candidate layer");
+            if (i > 0 && layers[i] <= layers[i - 1]) fail(QT_EINVAL, "candidate layers must be strictly increasing");
+            const double r = keeps[i];
+            if (!(r > 0.0 && r <= 1.0)) fail(QT_EINVAL, "keep ratio outside (0,1]");
+            if (i > 0 && r > keeps[i - 1] + 1e-12) fail(QT_EINVAL, "keep ratios must be non-increasing");
+        }
+        const double w[4] = {w4 ? w4[0] : 0.25, w4 ? w4[1] : 0.45, w4 ? w4[2] : 0.10, w4 ? w4[3] : 0.20};
+        for (double x : w)
+            if (x < 0) fail(QT_EINVAL, "negative metric weight");
+        if (std::fabs(w[0] + w[1] + w[2] + w[3] - 1.0) > 1e-9) fail(QT_EINVAL, "metric weights must sum to 1");
+        if (v0 < 1) fail(QT_EINVAL, "v0 must be >= 1");
+        if (layers[n - 1] >= e->L) fail(QT_ERUNTIME, "recipe candidate layers do not fit the model");  // harness.cpp:86-88
+        if (res_bits == 0 || res_bits == 1 || res_bits > 8) fail(QT_EINVAL, "bits out of range [2,8]");
+        e->recipe.layers.assign(layers, layers + n);
+        e->recipe.keeps.assign(keeps, keeps + n);
+        std::copy(w, w + 4, e->recipe.w);
+        e->recipe.v0 = v0;
+        e->recipe.res_bits = res_bits < 0 ? 0 : res_bits;
+        e->have_recipe = true;
+    });
+}
+
+int qt_engine_prefill(qt_engine* e, int n_seq, const float* emb, int emb_on_device, const int* visual,
+                      const int* text, const int* v0, const int* positions, float* logits_out, int out_on_device) {
+    return guard([&] {
+        if (!emb || !visual || !text) fail(QT_EINVAL, "null argument");
+        e->prefill(n_seq, emb, emb_on_device, visual, text, v0, positions, logits_out, out_on_device);
+    });
+}
+
+int qt_engine_prefill_rows(qt_engine* e) { return e->final_rows; }
+
+int qt_engine_decode(qt_engine* e, const float* emb, int emb_on_device, float* logits_out, int out_on_device) {
+    return guard([&] {
+        if (!emb) fail(QT_EINVAL, "embedding width mismatch");
+        e->decode(emb, emb_on_device, logits_out, out_on_device);
+    });
+}
+
+int qt_engine_layout(qt_engine* e, int seq, int* visual, int* text, int* positions, int cap) {
+    return guard([&] {
+        if (seq < 0 || seq >= e->B) fail(QT_ERANGE, "sequence out of range");
+        *visual = e->h_vis[seq];
+        *text = e->h_txt[seq];
+        const auto& p = e->h_pos[seq];
+        if ((int)p.size() > cap) fail(QT_EINVAL, "buffer too small");
+        if (positions) std::copy(p.begin(), p.end(), positions);
+    });
+}
+
+int qt_engine_n_prunes(qt_engine* e, int seq) {
+    if (seq < 0 || seq >= e->B) return -1;
+    return (int)e->trace[seq].size();
+}
+
+int qt_engine_prune(qt_engine* e, int seq, int i, int* layer, int* budget, int* positions, int cap, int* count) {
+    return guard([&] {
+        const PruneEv& ev = e->trace.at(seq).at(i);
+        *layer = ev.layer;
+        *budget = ev.budget;
+        if ((int)ev.positions.size() > cap) fail(QT_EINVAL, "buffer too small");
+        std::copy(ev.positions.begin(), ev.positions.end(), positions);
+        *count = (int)ev.positions.size();
+    });
+}
+
+int qt_engine_kv(qt_engine* e, int layer, int seq, int kv_head, int which, int8_t* codes, float* scales, int* rows,
+                 int cap_rows) {
+    return guard([&] {
+        if (layer < 0 || layer >= e->L || seq < 0 || seq >= e->B || kv_head < 0 || kv_head >= e->Hkv)
+            fail(QT_ERANGE, "kv index out of range");
+        ck(cudaStreamSynchronize(e->st), "sync");
+        const int n = e->h_kvlen[(size_t)layer * e->B + seq];
+        *rows = n;
+        if (!codes) return;
+        if (n > cap_rows) fail(QT_EINVAL, "buffer too small");
+        std::vector<int> hpt(e->max_pages);
+        ck(cudaMemcpy(hpt.data(), e->pt + ((size_t)layer * e->max_batch + seq) * e->max_pages,
+                      e->max_pages * sizeof(int), cudaMemcpyDeviceToHost),
+           "page table");
+        const int dh = e->dh;
+        const size_t cb = (size_t)e->Hkv * qt::kPage * (dh / 2);
+        std::vector<uint8_t> page(e->page_bytes);
+        for (int r0 = 0; r0 < n; r0 += qt::kPage) {
+            ck(cudaMemcpy(page.data(), e->pool + (long long)hpt[r0 / qt::kPage] * e->page_bytes, e->page_bytes,
+                          cudaMemcpyDeviceToHost),
+               "page");
+            for (int r = r0; r < std::min(n, r0 + qt::kPage); ++r) {
+                const int slot = r % qt::kPage;
+                const uint8_t* src = page.data() + (which ? cb : 0) + ((size_t)kv_head * qt::kPage + slot) * (dh / 2);
+                for (int c = 0; c < dh; ++c) {
+                    int nibv = (src[c / 2] >> (4 * (c & 1))) & 0xF;
+                    codes[(size_t)r * dh + c] = (int8_t)(nibv >= 8 ? nibv - 16 : nibv);
+                }
+                const float* sc = reinterpret_cast<const float*>(page.data() + 2 * cb);
+                scales[r] = sc[(which ? e->Hkv * qt::kPage : 0) + kv_head * qt::kPage + slot];
+            }
+        }
+    });
+}
+
+int qt_engine_info(qt_engine* e, int64_t* o) {
+    o[0] = (int64_t)(uintptr_t)e->st;
+    o[1] = e->n_pages_cap;
+    o[2] = e->page_bytes;
+    o[3] = e->dec_splits;
+    o[4] = e->dec_pps;
+    o[5] = e->final_rows;
+    o[6] = e->B;
+    o[7] = e->decode_steps;
+    // weight bytes (codes + scales) streamed per decode step
+    int64_t wb = 0;
+    wb += (int64_t)e->L * ((int64_t)e->n_qkv * e->kd_pad / 2 + (int64_t)e->d * e->kd_pad / 2 +
+                           (int64_t)e->n_gu * e->kd_pad / 2 + (int64_t)e->d * e->kff_pad / 2);
+    wb += (int64_t)e->d * e->kd_pad / 2;
+    wb += (int64_t)4 * (e->L * (e->n_qkv + e->d + e->n_gu + e->d) + e->d);
+    o[8] = wb;
+    int64_t kvb = 0;
+    for (int v : e->h_kvlen) kvb += (int64_t)v;
+    o[9] = kvb;  // cached rows summed over (layer, seq)
+    o[10] = (int64_t)(uintptr_t)e->pool;
+    o[11] = e->n_qkv;
+    o[12] = e->kd_pad;
+    o[13] = e->kff_pad;
+    o[14] = e->n_gu;
+    o[15] = 0;
+    return 0;
+}
+
+// ---- per-kernel ABI -------------------------------------------------------
+
+int qt_rmsnorm_quant_i4(const void* x, int x_is_f64, int ld_x, const float* gain, int M, int D, int d_pad,
+                        int act_mode, double static_scale, uint8_t* codes, int ld_codes, double* scales,
+                        float* normed, void* stream) {
+    return guard([&] {
+        ckl(qt_launch_norm_quant(x, x_is_f64, ld_x, gain, M, D, d_pad, 4, act_mode, static_scale, codes, ld_codes,
+                                 scales, normed, (cudaStream_t)stream),
+            "rmsnorm+quant");
+    });
+}
+
+int qt_w4a4_gemm(int epi, const uint8_t* a, int lda, const double* sa, const uint8_t* w, int ldw, const double* sw,
+                 int M, int N, int K, void* out, int ldo, int32_t* acc_out, int impl, void* stream) {
+    return guard([&] {
+        int rc = impl == 1 ? qt_launch_w4a4_tc05(epi, a, lda, sa, w, ldw, sw, M, N, K, out, ldo, acc_out, (cudaStream_t)stream)
+                           : qt_launch_w4a4_mma(epi, a, lda, sa, w, ldw, sw, M, N, K, out, ldo, acc_out, (cudaStream_t)stream);
+        ckl(rc, "w4a4 gemm");
+    });
+}
+
+int qt_quant_weight_i4(const float* w, int K, int N, int row_mul, int row_add, uint8_t* codes, int ldc,
+                       double* scales, double* scratch, void* stream) {
+    return guard([&] {
+        ckl(qt_launch_weight_quant(w, K, N, 4, row_mul, row_add, codes, ldc, scales, scratch, (cudaStream_t)stream),
+            "weight quantize");
+    });
+}
+
+int qt_kv_quant_append_i4(float* qkv, int ld_qkv, int M, int H, int Hkv, int d_head, const int* positions,
+                          const int* tok_seq, const int* tok_row, const double* rope_table, const int* page_table,
+                          int max_pages, uint8_t* pool, int64_t page_bytes, float* k_out, void* stream) {
+    return guard([&] {
+        ckl(qt_launch_rope_kv_append(qkv, ld_qkv, M, H, Hkv, d_head, positions, tok_seq, tok_row, rope_table,
+                                     page_table, max_pages, pool, page_bytes, 4, k_out, (cudaStream_t)stream),
+            "kv quant append");
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,524 @@
+// k_attn.cu -- attention over the paged int4 KV cache.
+//
+//   K7  prefill attention with the reference mask (model.cpp:35-44,272-292,385):
+//       visual queries see only visual keys (bidirectional); text queries see
+//       every visual key plus causal text.  Keys/values are the dequantised
+//       int4 rows k^ = code * s (model.cpp:371-372).  Optionally emits the row
+//       max / sum so K3a can rebuild normalised probabilities.
+//   K3a QUOTA attention-received metrics (selector.cpp:40-49): per visual key
+//       i and head h, column sums of softmax probabilities over text queries
+//       (m^inter) and over visual queries (m^intra).  Deterministic: partial
+//       sums per (seq, head, key) in fixed order, no float atomics.
+//   K6  decode attention (model.cpp:515-535): one query row per sequence over
+//       all cached rows, unmasked, 128-bit coalesced int4 loads dequantised in
+//       registers, split over pages + a fixed-order merge.
+//
+// Tensor-core math (mma.sync m16n8k16 f16->f32) uses hi/lo fp16 splits of the
+// fp32 operand (q, or p * s_v); int4 codes are exact in fp16, so products are
+// accurate to ~2^-22 relative -- well inside the 1e-3 score tolerance.
+#include "qt_common.cuh"
+#include "qt_kernels.h"
+
+namespace qt {
+
+constexpr int AT_Q = 64;   // query rows per CTA (16 per warp)
+constexpr int AT_K = 64;   // key rows per tile == kPage
+
+struct PageRef {
+    const uint8_t* codes;  // K codes for (kv head) rows of this page: [kPage][dh/2]
+    const float* scales;   // [kPage]
+};
+
+// Page p of (seq b): K codes at page + kh*kPage*dh/2, V codes after Hkv*kPage*dh/2,
+// K scales after 2*Hkv*kPage*dh/2, V scales after those.
+QT_DEV const uint8_t* page_base(const uint8_t* pool, long long page_bytes, const int* pt, int max_pages, int b,
+                                int j) {
+    return pool + (long long)pt[b * max_pages + j / kPage] * page_bytes;
+}
+
+// Load one 64-key tile of K (row layout [key][dh] fp16 codes) and V
+// (transposed [dh][key] fp16 codes) plus scales into shared memory.
+template <int DH>
+QT_DEV void load_kv_tile(const uint8_t* page, int Hkv, int kh, int nkeys, __half* Ks, __half* Vt, float* ks,
+                         float* vs, bool need_v) {
+    constexpr int KLD = DH + 8, VLD = AT_K + 8;
+    const size_t cb = (size_t)Hkv * kPage * (DH / 2);
+    const uint8_t* kc = page + (size_t)kh * kPage * (DH / 2);
+    const uint8_t* vc = page + cb + (size_t)kh * kPage * (DH / 2);
+    const float* ksc = reinterpret_cast<const float*>(page + 2 * cb) + kh * kPage;
+    const float* vsc = reinterpret_cast<const float*>(page + 2 * cb) + Hkv * kPage + kh * kPage;
+    // 16-byte chunks: AT_K * DH/2 / 16 per matrix
+    constexpr int CH = AT_K * (DH / 2) / 16;
+    for (int c = threadIdx.x; c < CH; c += blockDim.x) {
+        const int row = c / (DH / 32), col = (c % (DH / 32)) * 32;  // 32 codes per chunk
+        uint4 w = row < nkeys ? *reinterpret_cast<const uint4*>(kc + (size_t)c * 16) : make_uint4(0, 0, 0, 0);
+        uint32_t* dst = reinterpret_cast<uint32_t*>(Ks + row * KLD + col);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            uint32_t word = (&w.x)[q];
+#pragma unroll
+            for (int bb = 0; bb < 4; ++bb) dst[q * 4 + bb] = nib2_to_h2((word >> (8 * bb)) & 0xFF);
+        }
+        if (need_v) {
+            uint4 v = row < nkeys ? *reinterpret_cast<const uint4*>(vc + (size_t)c * 16) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                uint32_t word = (&v.x)[q];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const int ch = col + q * 8 + e;
+                    Vt[ch * VLD + row] = __int2half_rn(nib(word, e));
+                }
+            }
+        }
+    }
+    for (int r = threadIdx.x; r < AT_K; r += blockDim.x) {
+        ks[r] = r < nkeys ? ksc[r] : 0.f;
+        if (need_v) vs[r] = r < nkeys ? vsc[r] : 0.f;
+    }
+}
+
+// Q fragments (hi/lo) for 16 query rows of one head: qf[s][0..3] hi, ql lo.
+template <int DH>
+QT_DEV void load_q_frags(const float* qkv, int ldq, int tok0, int rows_valid, int h, uint32_t (*qh)[4],
+                         uint32_t (*ql)[4]) {
+    const int lane = threadIdx.x & 31, g = lane >> 2, tig = lane & 3;
+#pragma unroll
+    for (int s = 0; s < DH / 16; ++s) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int row = g + ((r & 1) ? 8 : 0);
+            const int col = s * 16 + ((r & 2) ? 8 : 0) + 2 * tig;
+            float2 v = make_float2(0.f, 0.f);
+            if (row < rows_valid) v = *reinterpret_cast<const float2*>(qkv + (size_t)(tok0 + row) * ldq + h * DH + col);
+            split_h2(v.x, v.y, qh[s][r], ql[s][r]);
+        }
+    }
+}
+
+// S(16 x 64) = Q(16 x DH) . K^T with hi/lo split of Q.
+template <int DH>
+QT_DEV void qk_tile(const uint32_t (*qh)[4], const uint32_t (*ql)[4], const __half* Ks, float (*sc)[4]) {
+    constexpr int KLD = DH + 8;
+    const int lane = threadIdx.x & 31, g = lane >> 2, tig = lane & 3;
+#pragma unroll
+    for (int t = 0; t < AT_K / 8; ++t) {
+        sc[t][0] = sc[t][1] = sc[t][2] = sc[t][3] = 0.f;
+#pragma unroll
+        for (int s = 0; s < DH / 16; ++s) {
+            uint32_t b[2];
+            const __half* kr = Ks + (t * 8 + g) * KLD + s * 16 + 2 * tig;
+            b[0] = *reinterpret_cast<const uint32_t*>(kr);
+            b[1] = *reinterpret_cast<const uint32_t*>(kr + 8);
+            mma_f16_16816(sc[t], qh[s], b);
+            mma_f16_16816(sc[t], ql[s], b);
+        }
+    }
+}
+
+// ============================================================== K7
+template <int DH>
+__global__ void __launch_bounds__(128) k_attn_prefill(const float* __restrict__ qkv, int ldq, int H, int Hkv,
+                                                      const int* __restrict__ seq_off, const int* __restrict__ vis,
+                                                      const int* __restrict__ seq_len,
+                                                      const uint8_t* __restrict__ pool, long long page_bytes,
+                                                      const int* __restrict__ pt, int max_pages, float inv_sqrt,
+                                                      float* __restrict__ out, int ldo, float2* __restrict__ ml) {
+    constexpr int KLD = DH + 8, VLD = AT_K + 8;
+    __shared__ __align__(16) __half Ks[AT_K * KLD];
+    __shared__ __align__(16) __half Vt[DH * VLD];
+    __shared__ float ks[AT_K], vs[AT_K];
+    const int b = blockIdx.z, h = blockIdx.y;
+    const int S = seq_len[b], V = vis[b];
+    const int q0 = blockIdx.x * AT_Q;
+    if (q0 >= S) return;
+    const int kh = h / (H / Hkv);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, tig = lane & 3;
+    const int tok0 = seq_off[b];
+    const int wq0 = q0 + warp * 16;  // first query row of this warp (index in sequence)
+
+    uint32_t qh[DH / 16][4], ql[DH / 16][4];
+    load_q_frags<DH>(qkv, ldq, tok0 + wq0, S - wq0, h, qh, ql);
+
+    float o[DH / 8][4];
+#pragma unroll
+    for (int t = 0; t < DH / 8; ++t) o[t][0] = o[t][1] = o[t][2] = o[t][3] = 0.f;
+    float mrow[2] = {-1e30f, -1e30f}, lrow[2] = {0.f, 0.f};
+    const int qi[2] = {wq0 + g, wq0 + g + 8};
+
+    const int kend = max(V, min(S, q0 + AT_Q));
+    for (int k0 = 0; k0 < kend; k0 += AT_K) {
+        __syncthreads();
+        const uint8_t* page = page_base(pool, page_bytes, pt, max_pages, b, k0);
+        load_kv_tile<DH>(page, Hkv, kh, min(AT_K, S - k0), Ks, Vt, ks, vs, true);
+        __syncthreads();
+        float sc[AT_K / 8][4];
+        qk_tile<DH>(qh, ql, Ks, sc);
+        // scale, mask, row max
+        float tmax[2] = {-1e30f, -1e30f};
+#pragma unroll
+        for (int t = 0; t < AT_K / 8; ++t) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int r = e >> 1;
+                const int kj = k0 + t * 8 + 2 * tig + (e & 1);
+                const int q = qi[r];
+                bool ok = q < S && kj < S && (q < V ? kj < V : (kj < V || kj <= q));
+                float s = ok ? sc[t][e] * ks[t * 8 + 2 * tig + (e & 1)] * inv_sqrt : -1e30f;
+                sc[t][e] = s;
+                tmax[r] = fmaxf(tmax[r], s);
+            }
+        }
+        float alpha[2];
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            tmax[r] = fmaxf(tmax[r], __shfl_xor_sync(0xffffffffu, tmax[r], 1));
+            tmax[r] = fmaxf(tmax[r], __shfl_xor_sync(0xffffffffu, tmax[r], 2));
+            const float mn = fmaxf(mrow[r], tmax[r]);
+            alpha[r] = expf(mrow[r] - mn);
+            mrow[r] = mn;
+        }
+        float psum[2] = {0.f, 0.f};
+        uint32_t ph[AT_K / 16][4], pl[AT_K / 16][4];
+#pragma unroll
+        for (int t = 0; t < AT_K / 8; ++t) {
+            float p[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int r = e >> 1;
+                p[e] = sc[t][e] <= -1e30f ? 0.f : expf(sc[t][e] - mrow[r]);
+                psum[r] += p[e];
+                p[e] *= vs[t * 8 + 2 * tig + (e & 1)];
+            }
+            // A fragment of step u = t/2: tile 2u -> regs 0,1; tile 2u+1 -> regs 2,3
+            const int u = t >> 1, hi2 = (t & 1) * 2;
+            split_h2(p[0], p[1], ph[u][hi2 + 0], pl[u][hi2 + 0]);
+            split_h2(p[2], p[3], ph[u][hi2 + 1], pl[u][hi2 + 1]);
+        }
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            psum[r] += __shfl_xor_sync(0xffffffffu, psum[r], 1);
+            psum[r] += __shfl_xor_sync(0xffffffffu, psum[r], 2);
+            lrow[r] = lrow[r] * alpha[r] + psum[r];
+        }
+#pragma unroll
+        for (int t = 0; t < DH / 8; ++t) {
+            o[t][0] *= alpha[0];
+            o[t][1] *= alpha[0];
+            o[t][2] *= alpha[1];
+            o[t][3] *= alpha[1];
+#pragma unroll
+            for (int u = 0; u < AT_K / 16; ++u) {
+                uint32_t bb[2];
+                const __half* vr = Vt + (t * 8 + g) * VLD + u * 16 + 2 * tig;
+                bb[0] = *reinterpret_cast<const uint32_t*>(vr);
+                bb[1] = *reinterpret_cast<const uint32_t*>(vr + 8);
+                mma_f16_16816(o[t], ph[u], bb);
+                mma_f16_16816(o[t], pl[u], bb);
+            }
+        }
+    }
+    // finalize
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+        const int q = qi[r];
+        if (q >= S) continue;
+        const float inv_l = 1.f / lrow[r];
+        float* orow = out + (size_t)(tok0 + q) * ldo + h * DH;
+#pragma unroll
+        for (int t = 0; t < DH / 8; ++t) {
+            float2 v = make_float2(o[t][2 * r] * inv_l, o[t][2 * r + 1] * inv_l);
+            *reinterpret_cast<float2*>(orow + t * 8 + 2 * tig) = v;
+        }
+        if (ml && tig == 0) ml[(size_t)(tok0 + q) * H + h] = make_float2(mrow[r], lrow[r]);
+    }
+}
+
+// ============================================================== K3a
+// grid (ceil(Vmax/64), H, B).  colsum[(b*H + h)*vstride + i] for i < V.
+template <int DH>
+__global__ void __launch_bounds__(128) k_attn_colsum(const float* __restrict__ qkv, int ldq, int H, int Hkv,
+                                                     const int* __restrict__ seq_off, const int* __restrict__ vis,
+                                                     const int* __restrict__ seq_len,
+                                                     const uint8_t* __restrict__ pool, long long page_bytes,
+                                                     const int* __restrict__ pt, int max_pages, float inv_sqrt,
+                                                     const float2* __restrict__ ml, int vstride,
+                                                     float* __restrict__ inter, float* __restrict__ intra) {
+    constexpr int KLD = DH + 8;
+    __shared__ __align__(16) __half Ks[AT_K * KLD];
+    __shared__ float ks[AT_K], vs_unused[AT_K];
+    __shared__ float red[2][4][AT_K];
+    const int b = blockIdx.z, h = blockIdx.y;
+    const int S = seq_len[b], V = vis[b];
+    const int k0 = blockIdx.x * AT_K;
+    if (k0 >= V) return;
+    const int kh = h / (H / Hkv);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, tig = lane & 3;
+    const int tok0 = seq_off[b];
+    const uint8_t* page = page_base(pool, page_bytes, pt, max_pages, b, k0);
+    load_kv_tile<DH>(page, Hkv, kh, min(AT_K, V - k0), Ks, nullptr, ks, vs_unused, false);
+    __syncthreads();
+
+    float ci[AT_K / 8][2], ca[AT_K / 8][2];  // inter (text q), intra (visual q)
+#pragma unroll
+    for (int t = 0; t < AT_K / 8; ++t) ci[t][0] = ci[t][1] = ca[t][0] = ca[t][1] = 0.f;
+
+    for (int q0 = warp * 16; q0 < S; q0 += 64) {
+        uint32_t qh[DH / 16][4], ql[DH / 16][4];
+        load_q_frags<DH>(qkv, ldq, tok0 + q0, S - q0, h, qh, ql);
+        float sc[AT_K / 8][4];
+        qk_tile<DH>(qh, ql, Ks, sc);
+        float mr[2], il[2];
+        bool valid[2], isvis[2];
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const int q = q0 + g + 8 * r;
+            valid[r] = q < S;
+            isvis[r] = q < V;
+            float2 v = valid[r] ? ml[(size_t)(tok0 + q) * H + h] : make_float2(0.f, 1.f);
+            mr[r] = v.x;
+            il[r] = 1.f / v.y;
+        }
+#pragma unroll
+        for (int t = 0; t < AT_K / 8; ++t) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int r = e >> 1, c = e & 1;
+                if (!valid[r]) continue;
+                const float s = sc[t][e] * ks[t * 8 + 2 * tig + c] * inv_sqrt;
+                const float p = expf(s - mr[r]) * il[r];
+                if (isvis[r]) ca[t][c] += p;
+                else ci[t][c] += p;
+            }
+        }
+    }
+    // reduce over g (lanes differing in bits 2..4), then over warps
+#pragma unroll
+    for (int t = 0; t < AT_K / 8; ++t)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+#pragma unroll
+            for (int o = 4; o < 32; o <<= 1) {
+                ci[t][c] += __shfl_xor_sync(0xffffffffu, ci[t][c], o);
+                ca[t][c] += __shfl_xor_sync(0xffffffffu, ca[t][c], o);
+            }
+            if (g == 0) {
+                red[0][warp][t * 8 + 2 * tig + c] = ci[t][c];
+                red[1][warp][t * 8 + 2 * tig + c] = ca[t][c];
+            }
+        }
+    __syncthreads();
+    for (int i = threadIdx.x; i < AT_K; i += blockDim.x) {
+        if (k0 + i >= V) continue;
+        const float si = ((red[0][0][i] + red[0][1][i]) + red[0][2][i]) + red[0][3][i];
+        const float sa = ((red[1][0][i] + red[1][1][i]) + red[1][2][i]) + red[1][3][i];
+        inter[((size_t)b * H + h) * vstride + k0 + i] = si;
+        intra[((size_t)b * H + h) * vstride + k0 + i] = sa;
+    }
+}
+
+// ============================================================== K6
+// grid (splits, H, B), 128 threads.  Each split covers pages_per_split pages of
+// the sequence's layer cache (length read from device memory so the decode
+// step can be replayed from a CUDA graph).  4 lanes per key row: each lane
+// holds 32 channels (16 bytes of int4 codes) of the row.
+template <int DH>
+__global__ void __launch_bounds__(128) k_attn_decode(const float* __restrict__ qkv, int ldq, int H, int Hkv,
+                                                     const int* __restrict__ kv_len, int len_add,
+                                                     const uint8_t* __restrict__ pool, long long page_bytes,
+                                                     const int* __restrict__ pt, int max_pages, int pages_per_split,
+                                                     float inv_sqrt, float* __restrict__ part_ml,
+                                                     float* __restrict__ part_o) {
+    constexpr int CPL = DH / 4;  // channels per lane (32 for dh=128, 16 for dh=64)
+    const int b = blockIdx.z, h = blockIdx.y, sp = blockIdx.x, nsp = gridDim.x;
+    const int kh = h / (H / Hkv);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int q4 = lane & 3, quad = lane >> 2;
+    const int len = kv_len[b] + len_add;
+    const int r0 = sp * pages_per_split * kPage, r1 = min(len, r0 + pages_per_split * kPage);
+
+    float q[CPL];
+    const float* qp = qkv + (size_t)b * ldq + h * DH + q4 * CPL;
+#pragma unroll
+    for (int i = 0; i < CPL; i += 4) {
+        float4 v = *reinterpret_cast<const float4*>(qp + i);
+        q[i] = v.x;
+        q[i + 1] = v.y;
+        q[i + 2] = v.z;
+        q[i + 3] = v.w;
+    }
+    float acc[CPL];
+#pragma unroll
+    for (int i = 0; i < CPL; ++i) acc[i] = 0.f;
+    float m = -1e30f, l = 0.f;
+    const size_t cb = (size_t)Hkv * kPage * (DH / 2);
+    // rows r = base + quad with a warp-uniform base (stride 32) so every lane
+    // takes part in the quad shuffles; rows past the end contribute nothing
+    for (int base = r0 + warp * 8; base < r1; base += 32) {
+        const int r = base + quad;
+        const bool valid = r < r1;
+        uint32_t kw[CPL / 8], vw[CPL / 8];
+        float sk = 0.f, sv = 0.f;
+#pragma unroll
+        for (int w = 0; w < CPL / 8; ++w) kw[w] = vw[w] = 0u;
+        if (valid) {
+            const uint8_t* page = pool + (long long)pt[b * max_pages + r / kPage] * page_bytes;
+            const int slot = r % kPage;
+            const uint8_t* krow = page + ((size_t)kh * kPage + slot) * (DH / 2) + q4 * (CPL / 2);
+            const uint8_t* vrow = krow + cb;
+            const float* sc = reinterpret_cast<const float*>(page + 2 * cb);
+            sk = sc[kh * kPage + slot];
+            sv = sc[Hkv * kPage + kh * kPage + slot];
+            if (CPL == 32) {
+                uint4 a = ldg_nc_v4(krow), c = ldg_nc_v4(vrow);
+                kw[0] = a.x; kw[1] = a.y; kw[2] = a.z; kw[3] = a.w;
+                vw[0] = c.x; vw[1] = c.y; vw[2] = c.z; vw[3] = c.w;
+            } else {
+                uint2 a = *reinterpret_cast<const uint2*>(krow), c = *reinterpret_cast<const uint2*>(vrow);
+                kw[0] = a.x; kw[1] = a.y;
+                vw[0] = c.x; vw[1] = c.y;
+            }
+        }
+        float d = 0.f;
+#pragma unroll
+        for (int w = 0; w < CPL / 8; ++w)
+#pragma unroll
+            for (int e = 0; e < 8; ++e) d = fmaf(q[w * 8 + e], (float)nib(kw[w], e), d);
+        d += __shfl_xor_sync(0xffffffffu, d, 1);
+        d += __shfl_xor_sync(0xffffffffu, d, 2);
+        if (valid) {
+            const float s = d * sk * inv_sqrt;
+            const float mn = fmaxf(m, s);
+            const float alpha = expf(m - mn);
+            const float p = expf(s - mn);
+            l = l * alpha + p;
+            m = mn;
+            const float pv = p * sv;
+#pragma unroll
+            for (int w = 0; w < CPL / 8; ++w)
+#pragma unroll
+                for (int e = 0; e < 8; ++e) acc[w * 8 + e] = fmaf(pv, (float)nib(vw[w], e), acc[w * 8 + e] * alpha);
+        }
+    }
+    // merge the 8 quads of the warp (lanes with equal q4)
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+        const float mo = __shfl_xor_sync(0xffffffffu, m, o);
+        const float lo = __shfl_xor_sync(0xffffffffu, l, o);
+        const float mn = fmaxf(m, mo);
+        const float a1 = expf(m - mn), a2 = expf(mo - mn);
+        l = l * a1 + lo * a2;
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) {
+            const float ao = __shfl_xor_sync(0xffffffffu, acc[i], o);
+            acc[i] = acc[i] * a1 + ao * a2;
+        }
+        m = mn;
+    }
+    // merge the 4 warps through smem (fixed order)
+    __shared__ float sm[4][2];
+    __shared__ float so[4][DH];
+    if (quad == 0) {
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) so[warp][q4 * CPL + i] = acc[i];
+        if (q4 == 0) {
+            sm[warp][0] = m;
+            sm[warp][1] = l;
+        }
+    }
+    __syncthreads();
+    const size_t pidx = ((size_t)b * H + h) * nsp + sp;
+    if (threadIdx.x < DH) {
+        float mm = -1e30f;
+        for (int w = 0; w < 4; ++w) mm = fmaxf(mm, sm[w][0]);
+        float ll = 0.f, oo = 0.f;
+        for (int w = 0; w < 4; ++w) {
+            const float a = expf(sm[w][0] - mm);
+            ll += sm[w][1] * a;
+            oo += so[w][threadIdx.x] * a;
+        }
+        part_o[pidx * DH + threadIdx.x] = oo;
+        if (threadIdx.x == 0) {
+            part_ml[pidx * 2] = mm;
+            part_ml[pidx * 2 + 1] = ll;
+        }
+    }
+}
+
+// merge splits in fixed order: out[b][h*DH + c]
+__global__ void k_attn_decode_merge(const float* __restrict__ part_ml, const float* __restrict__ part_o, int nsp,
+                                    int H, int DH, float* __restrict__ out, int ldo) {
+    const int b = blockIdx.y, h = blockIdx.x, c = threadIdx.x;
+    const size_t base = ((size_t)b * H + h) * nsp;
+    float mm = -1e30f;
+    for (int s = 0; s < nsp; ++s) mm = fmaxf(mm, part_ml[(base + s) * 2]);
+    float ll = 0.f, oo = 0.f;
+    for (int s = 0; s < nsp; ++s) {
+        const float a = expf(part_ml[(base + s) * 2] - mm);
+        ll += part_ml[(base + s) * 2 + 1] * a;
+        if (c < DH) oo += part_o[(base + s) * DH + c] * a;
+    }
+    if (c < DH) out[(size_t)b * ldo + h * DH + c] = oo / ll;
+}
+
+}  // namespace qt
+
+using namespace qt;
+
+extern "C" {
+
+int qt_launch_attn_prefill(const float* qkv, int ldq, int H, int Hkv, int dh, const int* seq_off, const int* vis,
+                           const int* seq_len, int B, int smax, const uint8_t* pool, long long page_bytes,
+                           const int* pt, int max_pages, float* out, int ldo, float* ml, cudaStream_t st) {
+    if (B <= 0 || smax <= 0) return 0;
+    const dim3 grid((smax + AT_Q - 1) / AT_Q, H, B);
+    const float inv_sqrt = (float)(1.0 / sqrt((double)dh));
+    if (dh == 128)
+        k_attn_prefill<128><<<grid, 128, 0, st>>>(qkv, ldq, H, Hkv, seq_off, vis, seq_len, pool, page_bytes, pt,
+                                                  max_pages, inv_sqrt, out, ldo, reinterpret_cast<float2*>(ml));
+    else if (dh == 64)
+        k_attn_prefill<64><<<grid, 128, 0, st>>>(qkv, ldq, H, Hkv, seq_off, vis, seq_len, pool, page_bytes, pt,
+                                                 max_pages, inv_sqrt, out, ldo, reinterpret_cast<float2*>(ml));
+    else
+        return -1;
+    return (int)cudaGetLastError();
+}
+
+int qt_launch_attn_colsum(const float* qkv, int ldq, int H, int Hkv, int dh, const int* seq_off, const int* vis,
+                          const int* seq_len, int B, int vmax, const uint8_t* pool, long long page_bytes,
+                          const int* pt, int max_pages, const float* ml, int vstride, float* inter, float* intra,
+                          cudaStream_t st) {
+    if (B <= 0 || vmax <= 0) return 0;
+    const dim3 grid((vmax + AT_K - 1) / AT_K, H, B);
+    const float inv_sqrt = (float)(1.0 / sqrt((double)dh));
+    const float2* m2 = reinterpret_cast<const float2*>(ml);
+    if (dh == 128)
+        k_attn_colsum<128><<<grid, 128, 0, st>>>(qkv, ldq, H, Hkv, seq_off, vis, seq_len, pool, page_bytes, pt,
+                                                 max_pages, inv_sqrt, m2, vstride, inter, intra);
+    else if (dh == 64)
+        k_attn_colsum<64><<<grid, 128, 0, st>>>(qkv, ldq, H, Hkv, seq_off, vis, seq_len, pool, page_bytes, pt,
+                                                max_pages, inv_sqrt, m2, vstride, inter, intra);
+    else
+        return -1;
+    return (int)cudaGetLastError();
+}
+
+int qt_launch_attn_decode(const float* qkv, int ldq, int H, int Hkv, int dh, const int* kv_len, int len_add, int B,
+                          const uint8_t* pool, long long page_bytes, const int* pt, int max_pages, int splits,
+                          int pages_per_split, float* part_ml, float* part_o, float* out, int ldo, cudaStream_t st) {
+    if (B <= 0) return 0;
+    const dim3 grid(splits, H, B);
+    const float inv_sqrt = (float)(1.0 / sqrt((double)dh));
+    if (dh == 128)
+        k_attn_decode<128><<<grid, 128, 0, st>>>(qkv, ldq, H, Hkv, kv_len, len_add, pool, page_bytes, pt, max_pages,
+                                                 pages_per_split, inv_sqrt, part_ml, part_o);
+    else if (dh == 64)
+        k_attn_decode<64><<<grid, 128, 0, st>>>(qkv, ldq, H, Hkv, kv_len, len_add, pool, page_bytes, pt, max_pages,
+                                                pages_per_split, inv_sqrt, part_ml, part_o);
+    else
+        return -1;
+    k_attn_decode_merge<<<dim3(H, B), 128, 0, st>>>(part_ml, part_o, splits, H, dh, out, ldo);
+    return (int)cudaGetLastError();
+}
+
+}  // extern "C"

@@ -1,0 +1,318 @@
+// k_quant.cu -- memory-bound quantizer kernels (HBM roofline):
+//   K1  RMSNorm + symmetric int4 activation quantizer (site_quant), static
+//       per-tensor or dynamic per-token scale           model.cpp:31-33,147-154,
+//                                                        347-349,394,429-435,442-444
+//   K5  RoPE + per-(token, kv-head) int4 KV quantize + paged append
+//                                                        model.cpp:156-168,368-374,494-501
+//   K3b QUOTA token magnitude / quantization-residual metrics
+//                                                        selector.cpp:38,56-66
+//   weight quantizer (prepare_quant_env, per output channel) model.cpp:212-237
+//
+// All quantizer arithmetic is fp64 (the reference's type), so an int4 code
+// equals the reference code for the same fp32 input; the fp32 scale handed to
+// the GEMM epilogue is the rounded fp64 scale.
+#include "qt_common.cuh"
+#include "qt_kernels.h"
+
+namespace qt {
+
+// ============================================================== K1
+// One CTA per token row.  gain == nullptr: no RMSNorm (attn_out / mlp_mid sites).
+// mode 0: static per-tensor scale `static_scale`; mode 1: dynamic per-row
+// max|n|/qmax.  codes: packed int4 [M x ld_codes bytes], zero-padded to
+// d_pad; scales: fp32 [M] (the scale each row was quantized with).
+template <typename TX>
+QT_DEV void load8(const TX* p, double* v);
+template <>
+QT_DEV void load8<float>(const float* p, double* v) {
+    float4 a = *reinterpret_cast<const float4*>(p);
+    float4 b = *reinterpret_cast<const float4*>(p + 4);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+template <>
+QT_DEV void load8<double>(const double* p, double* v) {
+#pragma unroll
+    for (int j = 0; j < 8; j += 2) {
+        double2 a = *reinterpret_cast<const double2*>(p + j);
+        v[j] = a.x;
+        v[j + 1] = a.y;
+    }
+}
+
+template <typename TX>
+__global__ void __launch_bounds__(256) k_norm_quant(const TX* __restrict__ x, int ld_x,
+                                                    const float* __restrict__ gain, int M, int D, int d_pad,
+                                                    int qmax, int mode, double static_scale,
+                                                    uint8_t* __restrict__ codes, int ld_codes,
+                                                    double* __restrict__ scales, float* __restrict__ normed) {
+    __shared__ double red[32];
+    const int row = blockIdx.x;
+    if (row >= M) return;
+    const TX* xr = x + (size_t)row * ld_x;
+    double inv = 1.0;
+    if (gain) {
+        double ss = 0.0;
+        for (int i = threadIdx.x * 8; i < D; i += blockDim.x * 8) {
+            double v[8];
+            load8<TX>(xr + i, v);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) ss += v[j] * v[j];
+        }
+        ss = block_sum(ss, red);
+        inv = 1.0 / sqrt(ss / (double)D + kNormEps);
+    }
+    double s;
+    if (mode == 0) {
+        s = static_scale;
+    } else {
+        double mx = 0.0;
+        for (int i = threadIdx.x * 8; i < D; i += blockDim.x * 8) {
+            double v[8];
+            load8<TX>(xr + i, v);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                double n = gain ? __dmul_rn(__dmul_rn(v[j], inv), (double)gain[i + j]) : v[j];
+                mx = fmax(mx, fabs(n));
+            }
+        }
+        mx = block_max(mx, red);
+        s = q_scale(mx, qmax);
+    }
+    // codes, 8 per 32-bit word
+    uint32_t* cw = reinterpret_cast<uint32_t*>(codes + (size_t)row * ld_codes);
+    const int n_words = d_pad / 8;
+    for (int w = threadIdx.x; w < n_words; w += blockDim.x) {
+        int c[8];
+        const int base = w * 8;
+        if (base < D) {
+            double v[8];
+            load8<TX>(xr + base, v);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                double n = gain ? __dmul_rn(__dmul_rn(v[j], inv), (double)gain[base + j]) : v[j];
+                c[j] = q_code(n, s, qmax);
+                if (normed) normed[(size_t)row * D + base + j] = (float)n;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) c[j] = 0;
+        }
+        cw[w] = pack8(c);
+    }
+    if (threadIdx.x == 0) scales[row] = s;
+}
+
+// ============================================================== K5
+// One CTA per token.  qkv row layout: [q (H*dh) | k (Hkv*dh) | v (Hkv*dh)],
+// fp32, ld = ld_qkv.  RoPE (interleaved pairs, model.cpp:156-168) is applied to
+// q in place and to k, with the cos/sin table computed on the host with the
+// reference's own libm calls.  k and v rows of each kv head are then
+// quantized per (token, head) (kv_quantize, quant.cpp:117-119) and appended
+// into the paged cache at (page_table[seq][row / kPage], row % kPage).
+__global__ void __launch_bounds__(256) k_rope_kv_append(
+    float* __restrict__ qkv, int ld_qkv, int M, int H, int Hkv, int dh, const int* __restrict__ pos,
+    const int* __restrict__ tok_seq, const int* __restrict__ tok_row, const double2* __restrict__ rope,
+    const int* __restrict__ page_table, int max_pages, uint8_t* __restrict__ pool, long long page_bytes,
+    int qmax, float* __restrict__ k_dbg) {
+    const int m = blockIdx.x;
+    if (m >= M) return;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int E = dh / 32;  // elements per lane (2 or 4)
+    const int p = pos[m];
+    const double2* rt = rope + (size_t)p * (dh / 2);
+    float* row = qkv + (size_t)m * ld_qkv;
+    const int b = tok_seq[m], r = tok_row[m];
+    uint8_t* page = pool + (long long)page_table[b * max_pages + r / kPage] * page_bytes;
+    const int slot = r % kPage;
+    const size_t codes_bytes = (size_t)Hkv * kPage * (dh / 2);
+    for (int t = wid; t < H + 2 * Hkv; t += nw) {
+        float* v = row + t * dh;  // q heads, then k heads, then v heads: contiguous
+        double val[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (j < E) val[j] = (double)v[lane * E + j];
+        if (t < H + Hkv) {  // rope q and k
+#pragma unroll
+            for (int j = 0; j < 4; j += 2) {
+                if (j < E) {
+                    double2 cs = rt[(lane * E + j) / 2];
+                    double a = val[j], bb = val[j + 1];
+                    val[j] = __dsub_rn(__dmul_rn(a, cs.x), __dmul_rn(bb, cs.y));
+                    val[j + 1] = __dadd_rn(__dmul_rn(a, cs.y), __dmul_rn(bb, cs.x));
+                }
+            }
+        }
+        if (t < H) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (j < E) v[lane * E + j] = (float)val[j];
+            continue;
+        }
+        // k or v head: quantize per (token, head)
+        double mx = 0.0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (j < E) mx = fmax(mx, fabs(val[j]));
+        mx = warp_max(mx);
+        const double s = q_scale(mx, qmax);
+        const bool is_k = t < H + Hkv;
+        const int kh = is_k ? t - H : t - H - Hkv;
+        if (is_k && k_dbg) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (j < E) k_dbg[(size_t)m * Hkv * dh + kh * dh + lane * E + j] = (float)val[j];
+        }
+        int c[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) c[j] = j < E ? q_code(val[j], s, qmax) : 0;
+        uint8_t* dst = page + (is_k ? 0 : codes_bytes) + ((size_t)kh * kPage + slot) * (dh / 2) + lane * E / 2;
+        if (E == 4) {
+            uint16_t pk = (uint16_t)((c[0] & 0xF) | ((c[1] & 0xF) << 4) | ((c[2] & 0xF) << 8) | ((c[3] & 0xF) << 12));
+            *reinterpret_cast<uint16_t*>(dst) = pk;
+        } else {
+            *dst = (uint8_t)((c[0] & 0xF) | ((c[1] & 0xF) << 4));
+        }
+        if (lane == 0) {
+            float* sc = reinterpret_cast<float*>(page + 2 * codes_bytes) + (is_k ? 0 : Hkv * kPage);
+            sc[kh * kPage + slot] = (float)s;
+        }
+    }
+}
+
+// ============================================================== K3b
+// QUOTA per-visual-token metrics on the post-attention residual x
+// (selector.cpp:19-68): mag = ||x_i||_2, res = ||fq_row(x_i) - x_i||_2 with
+// the per-row quantizer fake_quant_per_row (quant.cpp:108-110).  grid (Vmax, B).
+__global__ void __launch_bounds__(256) k_token_metrics(const double* __restrict__ x, int D,
+                                                       const int* __restrict__ seq_off,
+                                                       const int* __restrict__ vis, int vstride, int qmax,
+                                                       int with_res, double* __restrict__ mag,
+                                                       double* __restrict__ res) {
+    __shared__ double red[32];
+    const int b = blockIdx.y, i = blockIdx.x;
+    if (i >= vis[b]) return;
+    const double* xr = x + (size_t)(seq_off[b] + i) * D;
+    double ss = 0.0, mx = 0.0;
+    for (int j = threadIdx.x; j < D; j += blockDim.x) {
+        double v = xr[j];
+        ss += v * v;
+        mx = fmax(mx, fabs(v));
+    }
+    ss = block_sum(ss, red);
+    double rr = 0.0;
+    if (with_res) {
+        mx = block_max(mx, red);
+        const double s = q_scale(mx, qmax);
+        for (int j = threadIdx.x; j < D; j += blockDim.x) {
+            double v = xr[j];
+            double d = __dsub_rn(__dmul_rn((double)q_code(v, s, qmax), s), v);
+            rr += d * d;
+        }
+        rr = block_sum(rr, red);
+    }
+    if (threadIdx.x == 0) {
+        mag[(size_t)b * vstride + i] = sqrt(ss);
+        res[(size_t)b * vstride + i] = with_res ? sqrt(rr) : 0.0;
+    }
+}
+
+// ============================================================== weights
+// prepare_quant_env for one weight W[K x N] given in the reference orientation
+// (row-major d_in x d_out, y = x W).  One scale per output column n
+// (GroupAxis::PerColumn, quant.cpp:15-31): s_n = max_k |W[k][n]| / qmax.
+// Output: packed codes [N_pad x ldc] (row n = column n of W, K contiguous,
+// zero-padded), fp32 scales.  dst_row maps column n to its storage row
+// (identity, or the gate/up interleave for SwiGLU).
+__global__ void k_weight_colmax(const float* __restrict__ w, int K, int N, double* __restrict__ colmax) {
+    const int n = blockIdx.x * blockDim.x + threadIdx.x;
+    if (n >= N) return;
+    double m = 0.0;
+    for (int k = 0; k < K; ++k) m = fmax(m, fabs((double)w[(size_t)k * N + n]));
+    colmax[n] = m;
+}
+
+__global__ void k_weight_pack(const float* __restrict__ w, int K, int N, const double* __restrict__ colmax,
+                              int qmax, int row_mul, int row_add, uint8_t* __restrict__ codes, int ldc,
+                              double* __restrict__ scales) {
+    // thread per (n, word of 8 k)
+    const int n = blockIdx.x * blockDim.x + threadIdx.x;
+    const int wd = blockIdx.y;
+    if (n >= N) return;
+    const double s = q_scale(colmax[n], qmax);
+    int c[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        int k = wd * 8 + j;
+        c[j] = k < K ? q_code((double)w[(size_t)k * N + n], s, qmax) : 0;
+    }
+    const int dst = n * row_mul + row_add;
+    reinterpret_cast<uint32_t*>(codes + (size_t)dst * ldc)[wd] = pack8(c);
+    if (wd == 0) scales[dst] = s;
+}
+
+__global__ void k_f32_to_f64(const float* __restrict__ a, double* __restrict__ b, long long n) {
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) b[i] = (double)a[i];
+}
+
+}  // namespace qt
+
+// ---------------------------------------------------------------- launchers
+using namespace qt;
+
+extern "C" {
+
+int qt_launch_f32_to_f64(const float* a, double* b, long long n, cudaStream_t st) {
+    if (n <= 0) return 0;
+    k_f32_to_f64<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(a, b, n);
+    return (int)cudaGetLastError();
+}
+
+int qt_launch_norm_quant(const void* x, int x_is_f64, int ld_x, const float* gain, int M, int D, int d_pad,
+                         int bits, int mode, double static_scale, uint8_t* codes, int ld_codes, double* scales,
+                         float* normed, cudaStream_t st) {
+    if (M <= 0) return 0;
+    if (D % 8 || d_pad % 8 || ld_x % 4) return -1;
+    const int qmax = (1 << (bits - 1)) - 1;
+    const int threads = D >= 2048 ? 256 : 128;
+    if (x_is_f64)
+        k_norm_quant<double><<<M, threads, 0, st>>>(static_cast<const double*>(x), ld_x, gain, M, D, d_pad, qmax,
+                                                    mode, static_scale, codes, ld_codes, scales, normed);
+    else
+        k_norm_quant<float><<<M, threads, 0, st>>>(static_cast<const float*>(x), ld_x, gain, M, D, d_pad, qmax, mode,
+                                                   static_scale, codes, ld_codes, scales, normed);
+    return (int)cudaGetLastError();
+}
+
+int qt_launch_rope_kv_append(float* qkv, int ld_qkv, int M, int H, int Hkv, int dh, const int* pos,
+                             const int* tok_seq, const int* tok_row, const double* rope, const int* page_table,
+                             int max_pages, uint8_t* pool, long long page_bytes, int bits, float* k_dbg,
+                             cudaStream_t st) {
+    if (M <= 0) return 0;
+    if (dh != 64 && dh != 128) return -1;
+    const int qmax = (1 << (bits - 1)) - 1;
+    k_rope_kv_append<<<M, 256, 0, st>>>(qkv, ld_qkv, M, H, Hkv, dh, pos, tok_seq, tok_row,
+                                        reinterpret_cast<const double2*>(rope), page_table, max_pages, pool,
+                                        page_bytes, qmax, k_dbg);
+    return (int)cudaGetLastError();
+}
+
+int qt_launch_token_metrics(const double* x, int D, const int* seq_off, const int* vis, int vmax, int B,
+                            int vstride, int res_bits, double* mag, double* res, cudaStream_t st) {
+    if (vmax <= 0 || B <= 0) return 0;
+    const int qmax = res_bits > 0 ? (1 << (res_bits - 1)) - 1 : 7;
+    k_token_metrics<<<dim3(vmax, B), 256, 0, st>>>(x, D, seq_off, vis, vstride, qmax, res_bits > 0, mag, res);
+    return (int)cudaGetLastError();
+}
+
+int qt_launch_weight_quant(const float* w, int K, int N, int bits, int row_mul, int row_add, uint8_t* codes,
+                           int ldc, double* scales, double* colmax_scratch, cudaStream_t st) {
+    const int qmax = (1 << (bits - 1)) - 1;
+    k_weight_colmax<<<(N + 127) / 128, 128, 0, st>>>(w, K, N, colmax_scratch);
+    const int words = (K + 7) / 8;
+    k_weight_pack<<<dim3((N + 127) / 128, words), 128, 0, st>>>(w, K, N, colmax_scratch, qmax, row_mul, row_add,
+                                                                 codes, ldc, scales);
+    return (int)cudaGetLastError();
+}
+
+}  // extern "C"

@@ -1,0 +1,145 @@
+// qt_common.cuh -- shared device helpers for the QUOTA B200 kernels (sm_100a).
+#pragma once
+
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define QT_DEV __device__ __forceinline__
+
+namespace qt {
+
+// ---------------------------------------------------------------- constants
+constexpr double kNormEps = 1e-6;   // model.cpp:15
+constexpr int kWarp = 32;
+constexpr int kPage = 64;           // KV page: 64 token rows per (layer, sequence)
+
+// ---------------------------------------------------------------- reductions
+template <typename T>
+QT_DEV T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+template <typename T>
+QT_DEV T warp_max(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Block-wide sum/max through shared scratch (>= 32 entries); result broadcast.
+template <typename T>
+QT_DEV T block_sum(T v, T* scratch) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    v = warp_sum(v);
+    __syncthreads();
+    if (lane == 0) scratch[wid] = v;
+    __syncthreads();
+    T r = lane < nw ? scratch[lane] : T(0);
+    r = warp_sum(r);
+    return r;
+}
+template <typename T>
+QT_DEV T block_max(T v, T* scratch) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    v = warp_max(v);
+    __syncthreads();
+    if (lane == 0) scratch[wid] = v;
+    __syncthreads();
+    T r = lane < nw ? scratch[lane] : T(0);
+    r = warp_max(r);
+    return r;
+}
+
+// ---------------------------------------------------------------- quantizer
+// Reference quantizer (quant.cpp:39-45, 64-66, 85-87): symmetric, codes
+// clamp(rne(x/s), -qmax, qmax), scale max|x|/qmax (1 for an all-zero group).
+// Evaluated in fp64 so a code equals the reference code for the same input.
+QT_DEV double q_scale(double max_abs, int qmax) { return max_abs == 0.0 ? 1.0 : max_abs / (double)qmax; }
+
+QT_DEV int q_code(double x, double s, int qmax) {
+    double q = rint(x / s);  // cvt.rni: round half to even == round_half_even
+    q = fmin(fmax(q, -(double)qmax), (double)qmax);
+    return (int)q;
+}
+
+// int4 two's-complement nibble packing: low nibble = even k.
+QT_DEV uint32_t pack8(const int* c) {
+    uint32_t w = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) w |= (uint32_t)(c[i] & 0xF) << (4 * i);
+    return w;
+}
+
+// Unpack 8 int4 nibbles into two int8x4 registers holding 16*code: the
+// nibble lands in the high half of each byte so the byte's sign bit is the
+// nibble's.  lo = even k (nibbles 0,2,4,6), hi = odd k (1,3,5,7).  Products of
+// two such operands carry a factor 256, removed exactly after accumulation.
+QT_DEV void unpack_x16(uint32_t w, uint32_t& lo, uint32_t& hi) {
+    lo = (w << 4) & 0xF0F0F0F0u;
+    hi = w & 0xF0F0F0F0u;
+}
+
+QT_DEV int nib(uint32_t w, int i) { return ((int)(w << (28 - 4 * i))) >> 28; }
+
+// ---------------------------------------------------------------- mma.sync
+// D(16x8 s32) += A(16x32 s8, row) * B(32x8 s8, col)
+QT_DEV void mma_s8_16832(int* d, const uint32_t* a, const uint32_t* b) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k32.row.col.s32.s8.s8.s32 "
+        "{%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+        : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+
+// D(16x8 f32) += A(16x16 f16, row) * B(16x8 f16, col)
+QT_DEV void mma_f16_16816(float* d, const uint32_t* a, const uint32_t* b) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 "
+        "{%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+
+QT_DEV uint32_t h2_as_u32(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
+
+// split an fp32 pair into hi/lo fp16 pairs: x ~= hi + lo to ~2^-22 relative
+QT_DEV void split_h2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
+    __half2 h = __floats2half2_rn(x0, x1);
+    float2 hf = __half22float2(h);
+    __half2 l = __floats2half2_rn(x0 - hf.x, x1 - hf.y);
+    hi = h2_as_u32(h);
+    lo = h2_as_u32(l);
+}
+
+// int4 nibble pair (one byte: even k low, odd k high) -> half2(code_even, code_odd)
+QT_DEV uint32_t nib2_to_h2(uint32_t byte) {
+    int lo = ((int)(byte << 28)) >> 28;
+    int hi = ((int)(byte << 24)) >> 28;
+    return h2_as_u32(__halves2half2(__int2half_rn(lo), __int2half_rn(hi)));
+}
+
+// ---------------------------------------------------------------- cp.async
+QT_DEV void cp_async16(void* smem, const void* gmem, bool pred) {
+    uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+    int n = pred ? 16 : 0;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
+}
+QT_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+QT_DEV void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+QT_DEV uint4 ldg_nc_v4(const void* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];\n"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+QT_DEV float silu_f(float x) { return x / (1.0f + expf(-x)); }
+
+}  // namespace qt

@@ -1,0 +1,58 @@
+// qt_kernels.h -- internal launcher prototypes (host side, C linkage).
+// Every launcher takes caller-owned device buffers and an explicit stream and
+// returns 0 or a CUDA/argument error code; no hidden allocation.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define QT_EPI_STORE 0   // out = y
+#define QT_EPI_RESADD 1  // out += y           (residual add, model.cpp:396,437)
+#define QT_EPI_SILU 2    // out = silu(y)      (model.cpp:433)
+#define QT_EPI_SWIGLU 3  // out[n/2] = silu(y[n]) * y[n+1], gate/up interleaved columns
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+int qt_launch_f32_to_f64(const float* a, double* b, long long n, cudaStream_t st);
+int qt_launch_norm_quant(const void* x, int x_is_f64, int ld_x, const float* gain, int M, int D, int d_pad,
+                         int bits, int mode, double static_scale, uint8_t* codes, int ld_codes, double* scales,
+                         float* normed, cudaStream_t st);
+int qt_launch_rope_kv_append(float* qkv, int ld_qkv, int M, int H, int Hkv, int dh, const int* pos,
+                             const int* tok_seq, const int* tok_row, const double* rope, const int* page_table,
+                             int max_pages, uint8_t* pool, long long page_bytes, int bits, float* k_dbg,
+                             cudaStream_t st);
+int qt_launch_token_metrics(const double* x, int D, const int* seq_off, const int* vis, int vmax, int B,
+                            int vstride, int res_bits, double* mag, double* res, cudaStream_t st);
+int qt_launch_weight_quant(const float* w, int K, int N, int bits, int row_mul, int row_add, uint8_t* codes,
+                           int ldc, double* scales, double* colmax_scratch, cudaStream_t st);
+// out: double* for QT_EPI_RESADD (the fp64 residual stream), float* otherwise
+int qt_launch_w4a4_mma(int epi, const uint8_t* A, int lda, const double* sa, const uint8_t* W, int ldw,
+                       const double* sw, int M, int N, int K, void* out, int ldo, int* acc_dbg, cudaStream_t st);
+int qt_launch_w4a4_tc05(int epi, const uint8_t* A, int lda, const double* sa, const uint8_t* W, int ldw,
+                        const double* sw, int M, int N, int K, void* out, int ldo, int* acc_dbg, cudaStream_t st);
+int qt_launch_attn_prefill(const float* qkv, int ldq, int H, int Hkv, int dh, const int* seq_off, const int* vis,
+                           const int* seq_len, int B, int smax, const uint8_t* pool, long long page_bytes,
+                           const int* pt, int max_pages, float* out, int ldo, float* ml, cudaStream_t st);
+int qt_launch_attn_colsum(const float* qkv, int ldq, int H, int Hkv, int dh, const int* seq_off, const int* vis,
+                          const int* seq_len, int B, int vmax, const uint8_t* pool, long long page_bytes,
+                          const int* pt, int max_pages, const float* ml, int vstride, float* inter, float* intra,
+                          cudaStream_t st);
+int qt_launch_attn_decode(const float* qkv, int ldq, int H, int Hkv, int dh, const int* kv_len, int len_add, int B,
+                          const uint8_t* pool, long long page_bytes, const int* pt, int max_pages, int splits,
+                          int pages_per_split, float* part_ml, float* part_o, float* out, int ldo, cudaStream_t st);
+int qt_launch_select_topk(const double* mag, const double* res, const float* inter, const float* intra, int H,
+                          int vstride, const int* vis, const int* txt, const int* budget, const int* old_off,
+                          const int* new_off, int B, int vmax, const double* w4, int* keep_src, int* keep_local,
+                          int kl_stride, const int* pos, int* kept_pos, double* fused_out, double* norm_out,
+                          cudaStream_t st);
+int qt_launch_gather_rows(const double* x, double* xn, int D, const int* pos, int* posn, const int* src, int M,
+                          cudaStream_t st);
+int qt_launch_kv_compact(uint8_t* pool, long long page_bytes, const int* pt, int max_pages, int Hkv, int dh,
+                         const int* keep_local, int kl_stride, const int* new_len, int B, cudaStream_t st);
+int qt_launch_kv_len_bump(int* kv_len, int n, int* next_pos, int B, cudaStream_t st);
+
+#ifdef __cplusplus
+}
+#endif
