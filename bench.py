@@ -1,0 +1,403 @@
+#!/usr/bin/env python3
+"""bench.py -- QUOTA hot path on B200: W4A4 prefill with recipe-driven
+visual-token pruning, then decode over the int4 paged KV cache.
+
+One *step* = one request batch of the workload (BASELINE.json configs[1],
+LLaVA-1.5-7B shape): B sequences of 576 visual + 64 text tokens prefilled
+through 32 W4A4 layers with the QUOTA recipe (30 % visual retention from layer
+2: 576 -> 173), then 128 teacher-forced decode steps over the int4 cache,
+then the (N>1) gather of the final logits to rank 0.
+
+  value  = whole-job tokens/s = N * B * (S + D) / step time, inputs resident in HBM
+  e2e    = the same through the public API with pinned HOST buffers
+           (embeddings H2D and logits D2H inside the timed region, every step)
+
+Synthetic data: seeded N(0, 0.02) weights generated on the device, N(0, 1)
+hidden states with 1 % of the channels x20 (the configs' outlier model).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 is launched by torchrun (one rank per GPU, NCCL); each rank runs its own
+batch (weak scaling), NCCL only gathers outputs and timings.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "W4A4+QUOTA prefill ms & decode tok/s, 7B-shape, 1/2/4/8 B200, % roofline"
+UNIT = "tokens/s"
+
+CONFIGS = {
+    # BASELINE.json configs[1]
+    "c2": dict(workload="LLaVA-1.5-7B-shaped W4A4 + QUOTA 30% visual retention from layer 2 (configs[1])",
+               n_layers=32, d_model=4096, n_heads=32, n_kv_heads=32, d_head=128, d_ff=11008, mlp=1, act_mode=1,
+               batch=8, visual=576, text=64, decode=128, layers=[2], keeps=[0.3], v0=576, outlier=0.01),
+    # BASELINE.json configs[0] (tiny; parity case, also handy for a quick smoke bench)
+    "c1": dict(workload="tiny VLM decoder (configs[0])", n_layers=4, d_model=256, n_heads=4, n_kv_heads=4,
+               d_head=64, d_ff=688, mlp=1, act_mode=1, batch=1, visual=152, text=32, decode=16,
+               layers=[0, 1, 2, 3], keeps=[1.0, 0.5, 0.3, 0.3], v0=152, outlier=0.02),
+}
+
+
+def load_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi sampling of SM clocks + throttle reasons during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 4 + i and s[4 + i].lower() == "active"})
+        under = [v for v in sm if v > 0.5 * max(sm)] if sm else []
+        return {"sm_mhz": float(np.median(under)) if under else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# --------------------------------------------------------------------------- reference arm
+
+
+def reference_sample(threads, d_model, n_heads, d_head):
+    """The UNMODIFIED reference (oracle/_ref) at 7B width: 4 layers (ModelConfig minimum),
+    d_ff = 4 d SiLU MLP (the reference's fixed MLP; same FLOPs as SwiGLU 11008 within 1 %),
+    static act scales, quantized mode.  Returns (model, setup seconds)."""
+    import oracle as O
+    t0 = time.time()
+    cfg = O.ModelCfg(n_layers=4, d_model=d_model, n_heads=n_heads, n_kv_heads=n_heads, d_head=d_head,
+                     d_ff=4 * d_model, weight_axis=1)
+    ref = O.Ref(cfg, seed=1)
+    ref.prepare(np.ones(4 * 4 + 1), weight_axis=1)
+    return ref, time.time() - t0
+
+
+def reference_tokens_per_s(ref, threads, n_layers_full, tokens_per_seq=1):
+    """One bounded sample: `threads` sequences of `tokens_per_seq` tokens, one per host thread,
+    through the 4-layer reference; scaled to the full depth (x 4 / n_layers_full)."""
+    sec = ref.prefill_threads(threads, tokens_per_seq, 0, seed=int(time.time()) & 0xFFFF)
+    return threads * tokens_per_seq / sec * (4.0 / n_layers_full), sec
+
+
+def run_reference(args, cfg):
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    ref, setup_s = reference_sample(threads, cfg["d_model"], cfg["n_heads"], cfg["d_head"])
+    vals = []
+    for i in range(args.warmup + args.steps):
+        v, sec = reference_tokens_per_s(ref, threads, cfg["n_layers"])
+        if i >= args.warmup:
+            vals.append(v)
+    value = float(np.mean(vals))
+    sample = (f"{threads} threads x 1-token sequence through the unmodified reference forward_prefill, 4 layers "
+              f"at 7B width (d 4096, 32x128 heads, d_ff 16384 SiLU, static scales), quantized mode; "
+              f"tokens/s extrapolated to {cfg['n_layers']} layers (x4/{cfg['n_layers']}); setup {setup_s:.1f}s")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg["workload"], "batch_per_gpu": cfg["batch"],
+                       "visual": cfg["visual"], "text": cfg["text"], "decode_steps": cfg["decode"]},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- our arm
+
+
+def build_engine(cfg, torch, Q, seed=1234):
+    c = Q.Config(n_layers=cfg["n_layers"], d_model=cfg["d_model"], n_heads=cfg["n_heads"],
+                 n_kv_heads=cfg["n_kv_heads"], d_head=cfg["d_head"], d_ff=cfg["d_ff"], mlp=cfg["mlp"],
+                 act_mode=cfg["act_mode"])
+    B, S, D = cfg["batch"], cfg["visual"] + cfg["text"], cfg["decode"]
+    eng = Q.Engine(c, max_batch=B, max_tokens=B * S, max_seq=S, max_decode=D + 2)
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    d, kvd, f = cfg["d_model"], cfg["n_kv_heads"] * cfg["d_head"], cfg["d_ff"]
+
+    def rnd(*shape):
+        return torch.randn(*shape, device="cuda", generator=g) * 0.02
+
+    for l in range(cfg["n_layers"]):
+        eng.load_layer(l, rnd(d, d), rnd(d, kvd), rnd(d, kvd), rnd(d, d), rnd(d, f), rnd(f, d),
+                       rnd(d, f) if cfg["mlp"] == 1 else None)
+    eng.load_head(rnd(d, d))
+    eng.set_recipe(cfg["layers"], cfg["keeps"], v0=cfg["v0"], res_bits=4)
+    torch.cuda.synchronize()
+    return eng
+
+
+def synth_inputs(cfg, torch, seed):
+    """Hidden states N(0,1) with a seeded 1 % of channels x20 (BASELINE.json configs)."""
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    B, S, D, d = cfg["batch"], cfg["visual"] + cfg["text"], cfg["decode"], cfg["d_model"]
+    ch = torch.randperm(d, generator=g)[:max(1, int(round(cfg["outlier"] * d)))]
+    emb = torch.randn(B * S, d, generator=g)
+    emb[:, ch] *= 20.0
+    dec = torch.randn(D, B, d, generator=g)
+    dec[:, :, ch] *= 20.0
+    return emb.contiguous(), dec.contiguous()
+
+
+def run_ours(args, cfg):
+    import torch
+
+    import paper_2604_17320_b200 as Q
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist = None
+        torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    B, V, T, D, d = cfg["batch"], cfg["visual"], cfg["text"], cfg["decode"], cfg["d_model"]
+    S = V + T
+    eng = build_engine(cfg, torch, Q)
+    stream = torch.cuda.Stream(device=dev)
+    eng.set_stream(stream)
+    emb_h, dec_h = synth_inputs(cfg, torch, seed=77 + rank)
+    emb_d, dec_d = emb_h.to(dev), dec_h.to(dev)
+    logits_d = torch.empty(B * S, d, device=dev)
+    dlog_d = torch.empty(B, d, device=dev)
+    vis, txt = [V] * B, [T] * B
+    gathered = torch.empty(ws * B, d, device=dev) if ws > 1 else None
+
+    def gather_outputs():
+        if dist is not None:
+            with torch.cuda.stream(stream):
+                dist.all_gather_into_tensor(gathered, dlog_d)
+
+    def step_device():
+        eng.prefill(emb_d, vis, txt, logits_out=logits_d)
+        for t in range(D):
+            eng.decode(dec_d[t], logits_out=dlog_d)
+        gather_outputs()
+
+    # e2e: pinned host buffers through the public API, copies inside the timed region
+    emb_p, dec_p = emb_h.pin_memory(), dec_h.pin_memory()
+    logits_p = torch.empty(B * S, d).pin_memory()
+    dlog_p = torch.empty(D, B, d).pin_memory()
+
+    def step_e2e():
+        eng.prefill(emb_p, vis, txt, logits_out=logits_p)
+        for t in range(D):
+            eng.decode(dec_p[t], logits_out=dlog_p[t])
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    def timed(fn, steps, sample_clocks=False):
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        sampler = ClockSampler(local) if sample_clocks else None
+        if sampler:
+            sampler.__enter__()
+        e0.record(stream)
+        for _ in range(steps):
+            fn()
+        e1.record(stream)
+        stream.synchronize()
+        if sampler:
+            sampler.__exit__()
+        barrier()
+        ms = e0.elapsed_time(e1) / steps
+        if dist is not None:
+            t = torch.tensor([ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms, (sampler.summary() if sampler else None)
+
+    for _ in range(args.warmup):
+        step_device()
+    ms_step, clocks = timed(step_device, args.steps, sample_clocks=True)
+
+    # phase split (prefill ms, decode ms/step) on the device-resident path
+    barrier()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    ev[0].record(stream)
+    eng.prefill(emb_d, vis, txt, logits_out=logits_d)
+    ev[1].record(stream)
+    for t in range(D):
+        eng.decode(dec_d[t], logits_out=dlog_d)
+    ev[2].record(stream)
+    stream.synchronize()
+    prefill_ms = ev[0].elapsed_time(ev[1])
+    decode_ms = ev[1].elapsed_time(ev[2]) / D
+
+    for _ in range(max(1, args.warmup // 2)):
+        step_e2e()
+    ms_e2e, _ = timed(step_e2e, args.steps)
+
+    # per-kernel-class CUDA-event profile (one prefill + one eager decode step)
+    eng.profile_next()
+    eng.prefill(emb_d, vis, txt, logits_out=logits_d)
+    prof_pre = eng.profile_read()
+    eng.profile_next()
+    eng.decode(dec_d[0], logits_out=dlog_d)
+    prof_dec = eng.profile_read()
+    info = eng.info()
+
+    tokens = ws * B * (S + D)
+    value = tokens / (ms_step / 1e3)
+    e2e_val = tokens / (ms_e2e / 1e3)
+    final_rows = info["final_rows"]
+
+    peaks = load_peaks()
+    hbm = peaks.get("hbm_gbs")
+    peak_src = "MEASURED_PEAKS.json" if hbm else "B200_PROFILING.md fallback"
+    hbm = hbm or 6650.0
+    # dominant kernel class over the whole step
+    per_step = {}
+    for c in prof_pre:
+        per_step[("prefill", c)] = prof_pre[c]["ms"]
+        per_step[("decode", c)] = prof_dec[c]["ms"] * D
+    dom = max(per_step, key=per_step.get)
+    phase, cls = dom
+    src = prof_pre[cls] if phase == "prefill" else prof_dec[cls]
+    avg_ms = src["ms"] / max(1, src["launches"])
+    if phase == "decode" and cls in ("gemm", "attention", "quant", "kv"):
+        achieved = src["bytes"] / max(1, src["launches"]) / (avg_ms / 1e3) / 1e9
+        roofline = {"bound": "hbm", "kernel": f"{phase} {cls} (W4A4 GEMV)" if cls == "gemm" else f"{phase} {cls}",
+                    "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                    "traffic": None, "peak_source": peak_src,
+                    "algorithmic_bytes_per_launch": src["bytes"] / max(1, src["launches"]),
+                    "avg_launch_ms": avg_ms, "share_of_step": per_step[dom] / ms_step}
+    else:
+        tops = src["flops"] / max(1, src["launches"]) / (avg_ms / 1e3) / 1e12
+        roofline = {"bound": "tensor", "kernel": f"{phase} {cls}", "achieved": tops, "peak": 4500.0,
+                    "unit": "TOP/s (int8)", "frac": tops / 4500.0, "traffic": None,
+                    "peak_source": "B200 dense int8 datasheet (MEASURED_PEAKS.json has no int8 figure)",
+                    "avg_launch_ms": avg_ms, "share_of_step": per_step[dom] / ms_step}
+    gemm_pre = prof_pre["gemm"]
+    prefill_gemm_tops = gemm_pre["flops"] / (gemm_pre["ms"] / 1e3) / 1e12 if gemm_pre["ms"] else None
+    gemv = prof_dec["gemm"]
+    decode_gemv_gbs = gemv["bytes"] / (gemv["ms"] / 1e3) / 1e9 if gemv["ms"] else None
+    attn = prof_dec["attention"]
+    decode_attn_gbs = attn["bytes"] / (attn["ms"] / 1e3) / 1e9 if attn["ms"] else None
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        try:
+            threads = os.cpu_count() or 1
+            ref, setup_s = reference_sample(threads, d, cfg["n_heads"], cfg["d_head"])
+            v, sec = reference_tokens_per_s(ref, threads, cfg["n_layers"])
+            cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
+                   "sample": f"{threads} threads x 1-token sequence, unmodified reference forward_prefill, 4 layers "
+                             f"at 7B width (d_ff 16384 SiLU), {sec:.1f}s; extrapolated to {cfg['n_layers']} layers"}
+            del ref
+        except Exception as ex:  # the baseline is reported, never the product
+            cpu = {"value": None, "unit": UNIT, "cores": None, "kind": "reference", "sample": f"failed: {ex}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "int4xint4->int32 (W4A4), fp64 residual, int4 KV", "data": "synthetic",
+            "config": {"workload": cfg["workload"], "batch_per_gpu": B, "visual": V, "text": T,
+                       "decode_steps": D, "recipe": {"candidate_layers": cfg["layers"], "keep_ratios": cfg["keeps"],
+                                                     "v0": cfg["v0"]},
+                       "layers": cfg["n_layers"], "d_model": d, "heads": cfg["n_heads"], "d_ff": cfg["d_ff"],
+                       "parallelism": f"dp{ws} (batch sharded, NCCL gather of outputs only)",
+                       "l2": "working set > L2: 3.25 GB int4 weights streamed every decode step and prefill layer"},
+            "prefill_ms": prefill_ms, "prefill_tokens_per_s": ws * B * S / (prefill_ms / 1e3),
+            "decode_ms_per_step": decode_ms, "decode_tokens_per_s": ws * B / (decode_ms / 1e3),
+            "prefill_gemm_tops": prefill_gemm_tops, "decode_gemv_gbs": decode_gemv_gbs,
+            "decode_attn_gbs": decode_attn_gbs, "final_rows": final_rows,
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_val, "unit": UNIT, "ms_per_step": ms_e2e,
+                    "h2d_bytes_per_step": int(emb_p.numel() * 4 + dec_p.numel() * 4),
+                    "d2h_bytes_per_step": int(final_rows * d * 4 + D * B * d * 4)},
+            "gpu_launches": int(sum(v["launches"] for v in prof_pre.values())
+                                + D * sum(v["launches"] for v in prof_dec.values())),
+            "clocks": clocks,
+            "profile": {"prefill": prof_pre, "decode_step": prof_dec},
+        }
+        print(json.dumps(line), flush=True)
+    eng.close()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -110,6 +110,11 @@ int qt_engine_kv(qt_engine* e, int layer, int seq, int kv_head, int which, int8_
                  int* rows, int cap_rows);
 /* device pointers for in-place timing / inspection */
 int qt_engine_info(qt_engine* e, int64_t* out16);
+/* Profile the next prefill or decode call (decode runs eagerly, not from the
+ * graph): per kernel class {gemm, attention, quant, kv, select, other} the
+ * CUDA-event time (ms), launches, algorithmic bytes and flops -> out[6*4]. */
+int qt_engine_profile_next(qt_engine* e);
+int qt_engine_profile_read(qt_engine* e, double* out24);
 
 /* ---- per-kernel ABI (caller-owned device buffers, explicit stream) ---- */
 /* K1: RMSNorm (gain != null) + int4 activation quantizer; x fp32 or fp64

@@ -90,6 +90,7 @@ def ref_lib():
         lib.qref_layer_cost.restype = C.c_double
         lib.qref_layer_cost.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int]
         lib.qref_percentile.argtypes = [_dp, C.c_int, C.c_double, _dp]
+        lib.qref_prefill_threads.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_uint64, _dp]
         _ref_lib = lib
     return _ref_lib
 
@@ -271,6 +272,13 @@ class Ref:
         scales = np.empty(n_scales, dtype=np.float64)
         _check(self.lib.qref_model_weight_codes(self.h, layer, which, _b(codes), _d(scales)), self.lib, "qref")
         return codes.reshape(shape), scales
+
+    def prefill_threads(self, n_threads, visual, text, seed=1):
+        """Reference forward_prefill on n_threads independent synthetic sequences, one per
+        std::thread; returns wall seconds (CPU baseline)."""
+        sec = np.zeros(1)
+        _check(self.lib.qref_prefill_threads(self.h, n_threads, visual, text, seed, _d(sec)), self.lib, "qref")
+        return float(sec[0])
 
     def prefill(self, emb, visual, text, recipe: Recipe | None = None, quantized=True, res_bits=4, pos=None):
         e = f64(emb)

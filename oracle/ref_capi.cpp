@@ -11,11 +11,13 @@
 // Error convention: 0 = OK, -1 = std::invalid_argument, -2 = runtime_error,
 // -3 = out_of_range, -4 = other; qref_last_error() returns the message.
 
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "quota/calibrator.hpp"
@@ -25,6 +27,7 @@
 #include "quota/numeric.hpp"
 #include "quota/quant.hpp"
 #include "quota/recipe.hpp"
+#include "quota/rng.hpp"
 #include "quota/selector.hpp"
 
 using namespace quota;
@@ -530,6 +533,45 @@ int qref_decode(void* r, const double* emb, double* logits_out) {
         Vector out = decode_step(run->owner->model, env, run->result.cache,
                                  std::span<const double>(emb, static_cast<size_t>(run->owner->model.config.d_model)));
         std::copy(out.begin(), out.end(), logits_out);
+    });
+}
+
+// CPU baseline driver: n_threads independent sequences (visual + text tokens,
+// U(-1,1) embeddings from SplitMix64), one per std::thread, each through the
+// reference forward_prefill in quantized mode (thread-safe per sequence,
+// SPEC.md:224).  Returns wall seconds of the parallel region in *seconds.
+int qref_prefill_threads(void* h, int n_threads, int visual, int text, uint64_t seed, double* seconds) {
+    return guard([&] {
+        RefModel* m = static_cast<RefModel*>(h);
+        if (!m->env) throw std::invalid_argument("quantized mode requires a QuantEnv");
+        const int d = m->model.config.d_model, S = visual + text;
+        std::vector<Matrix> embs;
+        for (int t = 0; t < n_threads; ++t) {
+            SplitMix64 rng(mix_seed(seed, static_cast<uint64_t>(t)));
+            Matrix e(S, d);
+            for (double& v : e.data) v = rng.next_uniform(-1.0, 1.0);
+            embs.push_back(std::move(e));
+        }
+        SequenceLayout layout = SequenceLayout::prefix(visual, text);
+        std::vector<std::string> errs(static_cast<size_t>(n_threads));
+        auto t0 = std::chrono::steady_clock::now();
+        std::vector<std::thread> pool;
+        for (int t = 0; t < n_threads; ++t) {
+            pool.emplace_back([&, t] {
+                try {
+                    ForwardOptions o;
+                    o.mode = ExecMode::Quantized;
+                    o.quant = m->env.get();
+                    forward_prefill(m->model, embs[static_cast<size_t>(t)], layout, o);
+                } catch (const std::exception& e) {
+                    errs[static_cast<size_t>(t)] = e.what();
+                }
+            });
+        }
+        for (auto& th : pool) th.join();
+        *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        for (auto& e : errs)
+            if (!e.empty()) throw std::runtime_error(e);
     });
 }
 

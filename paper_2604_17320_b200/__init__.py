@@ -77,6 +77,8 @@ def lib():
         L.qt_engine_prune.argtypes = [vp, C.c_int, C.c_int, ip, ip, ip, C.c_int, ip]
         L.qt_engine_kv.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_int, vp, fp, ip, C.c_int]
         L.qt_engine_info.argtypes = [vp, C.POINTER(C.c_int64)]
+        L.qt_engine_profile_next.argtypes = [vp]
+        L.qt_engine_profile_read.argtypes = [vp, C.POINTER(C.c_double)]
         L.qt_rmsnorm_quant_i4.argtypes = [vp, C.c_int, C.c_int, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double,
                                           vp, C.c_int, vp, vp, vp]
         L.qt_w4a4_gemm.argtypes = [C.c_int, vp, C.c_int, vp, vp, C.c_int, vp, C.c_int, C.c_int, C.c_int, vp, C.c_int,
@@ -109,6 +111,11 @@ def _ptr(t):
     if isinstance(t, np.ndarray):
         return t.ctypes.data_as(C.c_void_p)
     return C.c_void_p(t.data_ptr())
+
+
+def _on_device(t):
+    """1 for a CUDA torch tensor, 0 for numpy / CPU (e.g. pinned) torch tensors."""
+    return 0 if isinstance(t, np.ndarray) else int(bool(getattr(t, "is_cuda", False)))
 
 
 def _i32(a):
@@ -209,36 +216,28 @@ class Engine:
         check(lib().qt_engine_set_recipe(self.h, 0, None, None, None, 1, 4))
 
     def prefill(self, emb, visual, text, v0=None, positions=None, logits_out=None):
-        """emb: packed [sum(S) x d] (numpy fp32 host or torch fp32 cuda).  Returns logits
-        (numpy, or writes into logits_out when given)."""
+        """emb: packed [sum(S) x d] fp32 -- numpy / CPU (pinned) torch on the host, or a
+        CUDA torch tensor.  Returns the logits rows (numpy, or a view of logits_out)."""
         visual, text = _i32(visual), _i32(text)
-        on_dev = 0 if isinstance(emb, np.ndarray) else 1
-        if on_dev == 0:
+        on_dev = _on_device(emb)
+        if isinstance(emb, np.ndarray):
             emb = np.ascontiguousarray(emb, dtype=np.float32)
         v0a, pa = _i32(v0), _i32(positions)
         if logits_out is None:
-            # host output sized by the worst case, trimmed after
             out = np.empty((int(np.sum(visual + text)), self.cfg.d_model), dtype=np.float32)
-            out_dev = 0
         else:
             out = logits_out
-            out_dev = 0 if isinstance(out, np.ndarray) else 1
         check(lib().qt_engine_prefill(self.h, len(visual), _ptr(emb), on_dev, _ip(visual), _ip(text), _ip(v0a),
-                                      _ip(pa), _ptr(out), out_dev))
+                                      _ip(pa), _ptr(out), _on_device(out)))
         rows = lib().qt_engine_prefill_rows(self.h)
         return out[:rows]
 
     def decode(self, emb, logits_out=None):
-        on_dev = 0 if isinstance(emb, np.ndarray) else 1
-        if on_dev == 0:
+        on_dev = _on_device(emb)
+        if isinstance(emb, np.ndarray):
             emb = np.ascontiguousarray(emb, dtype=np.float32)
-        if logits_out is None:
-            out = np.empty((emb.shape[0], self.cfg.d_model), dtype=np.float32)
-            out_dev = 0
-        else:
-            out = logits_out
-            out_dev = 0 if isinstance(out, np.ndarray) else 1
-        check(lib().qt_engine_decode(self.h, _ptr(emb), on_dev, _ptr(out), out_dev))
+        out = np.empty((emb.shape[0], self.cfg.d_model), dtype=np.float32) if logits_out is None else logits_out
+        check(lib().qt_engine_decode(self.h, _ptr(emb), on_dev, _ptr(out), _on_device(out)))
         return out
 
     def layout(self, seq):
@@ -266,6 +265,18 @@ class Engine:
         check(lib().qt_engine_kv(self.h, layer, seq, head, which, codes.ctypes.data_as(C.c_void_p),
                                  scales.ctypes.data_as(C.POINTER(C.c_float)), C.byref(rows), n))
         return codes, scales
+
+    PROFILE_CLASSES = ("gemm", "attention", "quant", "kv", "select", "other")
+
+    def profile_next(self):
+        """Time every kernel of the next prefill/decode call with CUDA events."""
+        check(lib().qt_engine_profile_next(self.h))
+
+    def profile_read(self):
+        o = (C.c_double * 24)()
+        lib().qt_engine_profile_read(self.h, o)
+        return {c: dict(ms=o[4 * i], launches=int(o[4 * i + 1]), bytes=o[4 * i + 2], flops=o[4 * i + 3])
+                for i, c in enumerate(self.PROFILE_CLASSES)}
 
     def info(self):
         o = (C.c_int64 * 16)()

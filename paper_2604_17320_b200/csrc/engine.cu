@@ -115,6 +115,52 @@ struct PruneEv {
     std::vector<int> positions;
 };
 
+// Per-launch CUDA-event profiler (bench.py roofline): kernel classes
+enum ProfClass { P_GEMM = 0, P_ATTN = 1, P_QUANT = 2, P_KV = 3, P_SELECT = 4, P_OTHER = 5, P_NCLASS = 6 };
+
+struct Profiler {
+    struct Rec {
+        int cls;
+        cudaEvent_t a, b;
+        double bytes, flops;
+    };
+    std::vector<Rec> recs;
+    cudaStream_t st = nullptr;
+    int open_cls = -1;
+    cudaEvent_t open_ev = nullptr;
+    void begin(int cls) {
+        cudaEventCreate(&open_ev);
+        cudaEventRecord(open_ev, st);
+        open_cls = cls;
+    }
+    void end(double bytes, double flops) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, st);
+        recs.push_back({open_cls, open_ev, e, bytes, flops});
+        open_cls = -1;
+    }
+    // out[c*4 + {0,1,2,3}] = {ms, launches, bytes, flops}
+    void read(double* out) {
+        cudaStreamSynchronize(st);
+        for (int i = 0; i < P_NCLASS * 4; ++i) out[i] = 0;
+        for (auto& r : recs) {
+            float ms = 0;
+            cudaEventElapsedTime(&ms, r.a, r.b);
+            out[r.cls * 4 + 0] += ms;
+            out[r.cls * 4 + 1] += 1;
+            out[r.cls * 4 + 2] += r.bytes;
+            out[r.cls * 4 + 3] += r.flops;
+        }
+    }
+    ~Profiler() {
+        for (auto& r : recs) {
+            cudaEventDestroy(r.a);
+            cudaEventDestroy(r.b);
+        }
+    }
+};
+
 }  // namespace
 
 struct qt_engine {
@@ -202,6 +248,15 @@ struct qt_engine {
     std::vector<int> h_kvlen;             // [L][B]
     bool prefilled = false;
     bool use_tc05 = false;
+    std::unique_ptr<Profiler> prof;      // active while profiling one call
+    bool prof_next = false;
+    double prof_out[P_NCLASS * 4] = {0};
+    void pb(int cls) {
+        if (prof) prof->begin(cls);
+    }
+    void pe(double bytes, double flops = 0) {
+        if (prof) prof->end(bytes, flops);
+    }
     std::vector<int> h_next;
 
     ~qt_engine() {
@@ -391,14 +446,19 @@ struct qt_engine {
     void norm_quant(const void* xin, int is_f64, int ldx, const float* gain, int M, int D, int dpad, int site_idx) {
         const int mode = cfg.act_mode;
         const double s = mode == 0 ? act[site_idx] : 0.0;
+        pb(P_QUANT);
         ckl(qt_launch_norm_quant(xin, is_f64, ldx, gain, M, D, dpad, 4, mode, s, codes, dpad / 2, ascale, nullptr, st),
             "rmsnorm+quant");
+        pe((double)M * D * (is_f64 ? 8 : 4) + (double)M * dpad / 2 + 8.0 * M);
     }
     void gemm(int epi, const uint8_t* w, const double* sw, int M, int N, int K, void* out, int ldo) {
+        pb(P_GEMM);
         int rc = (use_tc05 && M > 16)
                      ? qt_launch_w4a4_tc05(epi, codes, K / 2, ascale, w, K / 2, sw, M, N, K, out, ldo, nullptr, st)
                      : qt_launch_w4a4_mma(epi, codes, K / 2, ascale, w, K / 2, sw, M, N, K, out, ldo, nullptr, st);
         ckl(rc, "w4a4 gemm");
+        const double out_bytes = epi == QT_EPI_RESADD ? 16.0 * M * N : (epi == QT_EPI_SWIGLU ? 2.0 * M * N : 4.0 * M * N);
+        pe((double)N * K / 2 + 8.0 * N + (double)M * K / 2 + 8.0 * M + out_bytes, 2.0 * M * N * K);
     }
 
     // ------------------------------------------------------------ prefill
@@ -417,6 +477,10 @@ struct qt_engine {
         reset_staging();
         graph_ok = false;
         prefilled = false;
+        if (prof_next) {
+            prof = std::make_unique<Profiler>();
+            prof->st = st;
+        }
         B = nseq;
         h_vis.assign(vis, vis + B);
         h_txt.assign(txt, txt + B);
@@ -531,9 +595,11 @@ struct qt_engine {
             // attention block (model.cpp:347-396)
             norm_quant(xc, 1, d, w.g1, M, d, kd_pad, 4 * l + 0);
             gemm(QT_EPI_STORE, w.qkv, w.s_qkv, M, n_qkv, kd_pad, qkv, n_qkv);
+            pb(P_KV);
             ckl(qt_launch_rope_kv_append(qkv, n_qkv, M, H, Hkv, dh, pc, tok_seq, tok_row, rope, ptl, max_pages, pool,
                                          page_bytes, 4, nullptr, st),
                 "rope+kv append");
+            pe((double)M * n_qkv * 8 + (double)M * Hkv * 2 * (dh / 2 + 4));
             int smax = 0, vmax = 0;
             bool prune_any = false;
             for (int b = 0; b < B; ++b) {
@@ -542,9 +608,18 @@ struct qt_engine {
                 if (kbud[b][l] >= 0 && kbud[b][l] < cur_v[b]) prune_any = true;
             }
             const bool cand = have_recipe && std::any_of(kbud.begin(), kbud.end(), [l](const std::vector<int>& k) { return k[l] >= 0; });
+            pb(P_ATTN);
             ckl(qt_launch_attn_prefill(qkv, n_qkv, H, Hkv, dh, seq_off, seq_vis, seq_len, B, smax, pool, page_bytes,
                                        ptl, max_pages, attn, d, prune_any ? ml : nullptr, st),
                 "prefill attention");
+            {  // mask-allowed (query, key) pairs x 4 dh flops per head
+                double pairs = 0;
+                for (int b = 0; b < B; ++b) {
+                    const double V = cur_v[b], T = h_txt[b];
+                    pairs += V * V + T * V + T * (T + 1) / 2;
+                }
+                pe((double)M * (n_qkv * 4.0 + d * 4.0), 4.0 * pairs * dh * H);
+            }
             norm_quant(attn, 0, d, nullptr, M, d, kd_pad, 4 * l + 1);
             gemm(QT_EPI_RESADD, w.o, w.s_o, M, d, kd_pad, xc, d);
             for (int b = 0; b < B; ++b) h_kvlen[(size_t)l * B + b] = cur_v[b] + h_txt[b];
@@ -552,6 +627,7 @@ struct qt_engine {
             // recipe hook at candidate layers (selector.cpp:214-227, model.cpp:404-427)
             if (cand && prune_any) {
                 if (vmax > vstride) fail(QT_EINVAL, "visual prefix exceeds engine capacity");
+                pb(P_SELECT);
                 ckl(qt_launch_attn_colsum(qkv, n_qkv, H, Hkv, dh, seq_off, seq_vis, seq_len, B, vmax, pool, page_bytes,
                                           ptl, max_pages, ml, vstride, inter, intra, st),
                     "quota attention metrics");
@@ -579,6 +655,7 @@ struct qt_engine {
                 ckl(qt_launch_gather_rows(xc, xn, d, pc, pn, keep_src, noff[B], st), "compaction gather");
                 ckl(qt_launch_kv_compact(pool, page_bytes, ptl, max_pages, Hkv, dh, keep_local, vstride, new_len, B, st),
                     "kv compaction");
+                pe((double)M * d * 8 * 2);
                 // trace: kept visual positions, read back once after the prefill
                 trace_layers.push_back(l);
                 ev_prev_v.push_back(cur_v);
@@ -669,6 +746,7 @@ struct qt_engine {
         ck(cudaStreamSynchronize(st), "prefill");
         decode_steps = 0;
         prefilled = true;
+        finish_profile();
     }
 
     // ------------------------------------------------------------ decode
@@ -681,12 +759,20 @@ struct qt_engine {
             int* lenl = kv_len + (size_t)l * max_batch;
             norm_quant(xcur, 1, d, w.g1, B, d, kd_pad, 4 * l + 0);
             gemm(QT_EPI_STORE, w.qkv, w.s_qkv, B, n_qkv, kd_pad, qkv, n_qkv);
+            pb(P_KV);
             ckl(qt_launch_rope_kv_append(qkv, n_qkv, B, H, Hkv, dh, next_pos, dec_seq, lenl, rope, ptl, max_pages,
                                          pool, page_bytes, 4, nullptr, st),
                 "decode kv append");
+            pe((double)B * n_qkv * 8 + (double)B * Hkv * 2 * (dh / 2 + 4));
+            pb(P_ATTN);
             ckl(qt_launch_attn_decode(qkv, n_qkv, H, Hkv, dh, lenl, 1, B, pool, page_bytes, ptl, max_pages, dec_splits,
                                       dec_pps, part_ml, part_o, attn, d, st),
                 "decode attention");
+            {  // decode attention streams every cached K/V row of this layer once
+                double rows = 0;
+                for (int b = 0; b < B; ++b) rows += h_kvlen[(size_t)l * B + b] + 1;
+                pe(rows * Hkv * 2 * (dh / 2 + 4) + (double)B * H * dh * 8);
+            }
             norm_quant(attn, 0, d, nullptr, B, d, kd_pad, 4 * l + 1);
             gemm(QT_EPI_RESADD, w.o, w.s_o, B, d, kd_pad, xcur, d);
             norm_quant(xcur, 1, d, w.g2, B, d, kd_pad, 4 * l + 2);
@@ -700,14 +786,26 @@ struct qt_engine {
         ckl(qt_launch_kv_len_bump(kv_len, L * max_batch, next_pos, B, st), "kv length / position bump");
     }
 
+    void finish_profile() {
+        if (!prof) return;
+        prof->read(prof_out);
+        prof.reset();
+        prof_next = false;
+    }
+
     void decode(const float* emb, int emb_dev, float* out, int out_dev) {
         if (!prefilled) fail(QT_ERUNTIME, "cache and execution mode mismatch");
         if (decode_steps >= max_decode) fail(QT_EINVAL, "decode steps exceed engine capacity");
+        const bool profiling = prof_next;
+        if (profiling) {
+            prof = std::make_unique<Profiler>();
+            prof->st = st;
+        }
         ck(cudaMemcpyAsync(xd_in, emb, (size_t)B * d * sizeof(float),
                            emb_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st),
            "decode emb");
-        if (g_nograph) {
-            decode_body();
+        if (g_nograph || profiling) {
+            decode_body();  // eager launches so every kernel gets its own events
         } else if (!graph_ok) {
             if (graph) cudaGraphExecDestroy(graph);
             graph = nullptr;
@@ -728,12 +826,13 @@ struct qt_engine {
             cudaGraphDestroy(g);
             graph_ok = true;
         }
-        if (!g_nograph) ck(cudaGraphLaunch(graph, st), "graph launch");
+        if (!g_nograph && !profiling) ck(cudaGraphLaunch(graph, st), "graph launch");
         if (out)
             ck(cudaMemcpyAsync(out, dlogits, (size_t)B * d * sizeof(float),
                                out_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st),
                "decode logits");
         ++decode_steps;
+        finish_profile();
         for (int b = 0; b < B; ++b) {  // model.cpp:553-556
             h_txt[b] += 1;
             h_pos[b].push_back(h_next[b]++);
@@ -958,6 +1057,16 @@ int qt_engine_kv(qt_engine* e, int layer, int seq, int kv_head, int which, int8_
             }
         }
     });
+}
+
+int qt_engine_profile_next(qt_engine* e) {
+    e->prof_next = true;
+    return 0;
+}
+
+int qt_engine_profile_read(qt_engine* e, double* out) {
+    std::copy(e->prof_out, e->prof_out + P_NCLASS * 4, out);
+    return P_NCLASS;
 }
 
 int qt_engine_info(qt_engine* e, int64_t* o) {

@@ -79,6 +79,7 @@ __global__ void __launch_bounds__(256) k_norm_quant(const TX* __restrict__ x, in
         s = q_scale(mx, qmax);
     }
     // codes, 8 per 32-bit word
+    const double inv_s = 1.0 / s;
     uint32_t* cw = reinterpret_cast<uint32_t*>(codes + (size_t)row * ld_codes);
     const int n_words = d_pad / 8;
     for (int w = threadIdx.x; w < n_words; w += blockDim.x) {
@@ -90,7 +91,7 @@ __global__ void __launch_bounds__(256) k_norm_quant(const TX* __restrict__ x, in
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
                 double n = gain ? __dmul_rn(__dmul_rn(v[j], inv), (double)gain[base + j]) : v[j];
-                c[j] = q_code(n, s, qmax);
+                c[j] = q_code_r(n, s, inv_s, qmax);
                 if (normed) normed[(size_t)row * D + base + j] = (float)n;
             }
         } else {
@@ -117,6 +118,8 @@ __global__ void __launch_bounds__(256) k_rope_kv_append(
     const int m = blockIdx.x;
     if (m >= M) return;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int t = blockIdx.y * nw + wid;  // head slot: q heads, k heads, v heads
+    if (t >= H + 2 * Hkv) return;
     const int E = dh / 32;  // elements per lane (2 or 4)
     const int p = pos[m];
     const double2* rt = rope + (size_t)p * (dh / 2);
@@ -125,7 +128,7 @@ __global__ void __launch_bounds__(256) k_rope_kv_append(
     uint8_t* page = pool + (long long)page_table[b * max_pages + r / kPage] * page_bytes;
     const int slot = r % kPage;
     const size_t codes_bytes = (size_t)Hkv * kPage * (dh / 2);
-    for (int t = wid; t < H + 2 * Hkv; t += nw) {
+    {
         float* v = row + t * dh;  // q heads, then k heads, then v heads: contiguous
         double val[4];
 #pragma unroll
@@ -146,7 +149,7 @@ __global__ void __launch_bounds__(256) k_rope_kv_append(
 #pragma unroll
             for (int j = 0; j < 4; ++j)
                 if (j < E) v[lane * E + j] = (float)val[j];
-            continue;
+            return;
         }
         // k or v head: quantize per (token, head)
         double mx = 0.0;
@@ -154,7 +157,7 @@ __global__ void __launch_bounds__(256) k_rope_kv_append(
         for (int j = 0; j < 4; ++j)
             if (j < E) mx = fmax(mx, fabs(val[j]));
         mx = warp_max(mx);
-        const double s = q_scale(mx, qmax);
+        const double s = q_scale(mx, qmax), inv_s = 1.0 / s;
         const bool is_k = t < H + Hkv;
         const int kh = is_k ? t - H : t - H - Hkv;
         if (is_k && k_dbg) {
@@ -164,7 +167,7 @@ __global__ void __launch_bounds__(256) k_rope_kv_append(
         }
         int c[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) c[j] = j < E ? q_code(val[j], s, qmax) : 0;
+        for (int j = 0; j < 4; ++j) c[j] = j < E ? q_code_r(val[j], s, inv_s, qmax) : 0;
         uint8_t* dst = page + (is_k ? 0 : codes_bytes) + ((size_t)kh * kPage + slot) * (dh / 2) + lane * E / 2;
         if (E == 4) {
             uint16_t pk = (uint16_t)((c[0] & 0xF) | ((c[1] & 0xF) << 4) | ((c[2] & 0xF) << 8) | ((c[3] & 0xF) << 12));
@@ -291,7 +294,7 @@ int qt_launch_rope_kv_append(float* qkv, int ld_qkv, int M, int H, int Hkv, int 
     if (M <= 0) return 0;
     if (dh != 64 && dh != 128) return -1;
     const int qmax = (1 << (bits - 1)) - 1;
-    k_rope_kv_append<<<M, 256, 0, st>>>(qkv, ld_qkv, M, H, Hkv, dh, pos, tok_seq, tok_row,
+    k_rope_kv_append<<<dim3(M, (H + 2 * Hkv + 7) / 8), 256, 0, st>>>(qkv, ld_qkv, M, H, Hkv, dh, pos, tok_seq, tok_row,
                                         reinterpret_cast<const double2*>(rope), page_table, max_pages, pool,
                                         page_bytes, qmax, k_dbg);
     return (int)cudaGetLastError();

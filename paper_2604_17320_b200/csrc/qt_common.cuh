@@ -64,6 +64,19 @@ QT_DEV int q_code(double x, double s, int qmax) {
     return (int)q;
 }
 
+// Same code as q_code(x, s) without a per-element fp64 division: x * (1/s)
+// differs from the correctly rounded x / s by at most ~2 ulp, which can only
+// change rint() when the quotient sits within ~1e-15 of a .5 tie -- those
+// elements take the exact division.
+QT_DEV int q_code_r(double x, double s, double inv_s, int qmax) {
+    double q = x * inv_s;
+    const double f = q - floor(q);
+    if (fabs(f - 0.5) < 1e-9) q = x / s;
+    q = rint(q);
+    q = fmin(fmax(q, -(double)qmax), (double)qmax);
+    return (int)q;
+}
+
 // int4 two's-complement nibble packing: low nibble = even k.
 QT_DEV uint32_t pack8(const int* c) {
     uint32_t w = 0;

@@ -1,0 +1,48 @@
+"""Summarise an ncu --metrics gpu__time_duration.sum launch list (csv) by kernel."""
+import collections
+import csv
+import re
+import sys
+
+
+def load(path):
+    lines = [l for l in open(path) if l.startswith('"')]
+    rows = list(csv.reader(lines))
+    hdr = rows[0]
+    idx = {h: i for i, h in enumerate(hdr)}
+    seq = []
+    for r in rows[1:]:
+        if len(r) < len(hdr) or r[idx["Metric Name"]] != "gpu__time_duration.sum":
+            continue
+        v = float(r[idx["Metric Value"]].replace(",", ""))
+        unit = r[idx["Metric Unit"]]
+        v *= {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}.get(unit, 1.0)
+        name = re.sub(r"\(.*", "", r[idx["Kernel Name"]])
+        name = re.sub(r"^void ", "", name)
+        seq.append((name[:70], v, r[idx["Grid Size"]], r[idx["Block Size"]]))
+    return seq
+
+
+def summarize(seq, title=""):
+    tot = collections.defaultdict(float)
+    cnt = collections.Counter()
+    for n, v, _, _ in seq:
+        tot[n] += v
+        cnt[n] += 1
+    total = sum(tot.values())
+    print(f"== {title}: {len(seq)} launches, {total / 1e3:.3f} ms")
+    for n in sorted(tot, key=lambda k: -tot[k])[:20]:
+        print("%-70s %5d %10.1f us %5.1f%%  avg %8.2f us" % (n, cnt[n], tot[n], 100 * tot[n] / total, tot[n] / cnt[n]))
+
+
+if __name__ == "__main__":
+    seq = load(sys.argv[1])
+    marks = [i for i, s in enumerate(seq) if "k_f32_to_f64" in s[0]]
+    # first widen = prefill start; later ones = decode steps
+    if marks:
+        pre = seq[marks[0]:marks[1]] if len(marks) > 1 else seq[marks[0]:]
+        summarize(pre, "prefill")
+        if len(marks) > 1:
+            summarize(seq[marks[1]:marks[2]] if len(marks) > 2 else seq[marks[1]:], "decode step")
+    else:
+        summarize(seq, "all")
