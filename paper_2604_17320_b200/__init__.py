@@ -347,3 +347,17 @@ def exported_symbols():
     import re
     txt = open(HEADER).read()
     return sorted(set(re.findall(r"^\s*(?:const\s+char\*|int|void)\s+(qt_\w+)\s*\(", txt, flags=re.M)))
+
+
+def tile_w4(rows_u8):
+    """Row-major packed int4 [N_pad x K_pad/2] -> the engine's tiled layout (flat uint8):
+    1 KB tiles of 16 rows x 64 bytes, tile (rt, kt) at (rt * KT + kt) * 1024 (qt_common.cuh)."""
+    a = np.ascontiguousarray(rows_u8, dtype=np.uint8)
+    n, rb = a.shape
+    assert n % 16 == 0 and rb % 64 == 0
+    return a.reshape(n // 16, 16, rb // 64, 64).transpose(0, 2, 1, 3).reshape(n, rb).copy()
+
+
+def untile_w4(tiled_u8, n, row_bytes):
+    a = np.ascontiguousarray(tiled_u8, dtype=np.uint8).reshape(n // 16, row_bytes // 64, 16, 64)
+    return a.transpose(0, 2, 1, 3).reshape(n, row_bytes).copy()

@@ -42,6 +42,8 @@ void ck(cudaError_t e, const char* what) {
 const bool g_trace = std::getenv("QT_TRACE") != nullptr;
 const bool g_nograph = std::getenv("QT_NOGRAPH") != nullptr;
 bool g_capturing = false;
+// debug/attribution only: QT_SKIP bit mask drops decode launches (1 gemv, 2 attention, 4 quant, 8 kv append)
+const int g_skip = std::getenv("QT_SKIP") ? std::atoi(std::getenv("QT_SKIP")) : 0;
 
 void ckl(int rc, const char* what) {
     if (g_trace && !g_capturing) {
@@ -739,10 +741,8 @@ struct qt_engine {
                 const int cap = h_kvlen[(size_t)l * B + b] + max_decode;
                 maxp = std::max(maxp, (cap + qt::kPage - 1) / qt::kPage);
             }
-        const int want_blocks = 4 * 148;
-        int pps = std::max(1, (int)std::ceil((double)maxp * B * H / want_blocks));
-        dec_pps = pps;
-        dec_splits = (maxp + pps - 1) / pps;
+        dec_pps = 1;  // one 64-row page per decode-attention CTA
+        dec_splits = maxp;
         ck(cudaStreamSynchronize(st), "prefill");
         decode_steps = 0;
         prefilled = true;
@@ -757,29 +757,31 @@ struct qt_engine {
             const LayerW& w = lw[l];
             int* ptl = pt + (size_t)l * max_batch * max_pages;
             int* lenl = kv_len + (size_t)l * max_batch;
-            norm_quant(xcur, 1, d, w.g1, B, d, kd_pad, 4 * l + 0);
-            gemm(QT_EPI_STORE, w.qkv, w.s_qkv, B, n_qkv, kd_pad, qkv, n_qkv);
+            if (!(g_skip & 4)) norm_quant(xcur, 1, d, w.g1, B, d, kd_pad, 4 * l + 0);
+            if (!(g_skip & 1)) gemm(QT_EPI_STORE, w.qkv, w.s_qkv, B, n_qkv, kd_pad, qkv, n_qkv);
             pb(P_KV);
-            ckl(qt_launch_rope_kv_append(qkv, n_qkv, B, H, Hkv, dh, next_pos, dec_seq, lenl, rope, ptl, max_pages,
+            if (!(g_skip & 8)) ckl(qt_launch_rope_kv_append(qkv, n_qkv, B, H, Hkv, dh, next_pos, dec_seq, lenl, rope, ptl, max_pages,
                                          pool, page_bytes, 4, nullptr, st),
                 "decode kv append");
             pe((double)B * n_qkv * 8 + (double)B * Hkv * 2 * (dh / 2 + 4));
             pb(P_ATTN);
-            ckl(qt_launch_attn_decode(qkv, n_qkv, H, Hkv, dh, lenl, 1, B, pool, page_bytes, ptl, max_pages, dec_splits,
-                                      dec_pps, part_ml, part_o, attn, d, st),
-                "decode attention");
+            // decode attention over int4 pages + split merge fused with the attn_out quantizer
+            if (!(g_skip & 2))
+                ckl(qt_launch_attn_decode(qkv, n_qkv, H, Hkv, dh, lenl, 1, B, pool, page_bytes, ptl, max_pages,
+                                          dec_splits, part_ml, part_o, nullptr, d, codes, kd_pad / 2, ascale,
+                                          cfg.act_mode, cfg.act_mode == 0 ? act[4 * l + 1] : 0.0, kd_pad, 4, st),
+                    "decode attention");
             {  // decode attention streams every cached K/V row of this layer once
                 double rows = 0;
                 for (int b = 0; b < B; ++b) rows += h_kvlen[(size_t)l * B + b] + 1;
                 pe(rows * Hkv * 2 * (dh / 2 + 4) + (double)B * H * dh * 8);
             }
-            norm_quant(attn, 0, d, nullptr, B, d, kd_pad, 4 * l + 1);
-            gemm(QT_EPI_RESADD, w.o, w.s_o, B, d, kd_pad, xcur, d);
-            norm_quant(xcur, 1, d, w.g2, B, d, kd_pad, 4 * l + 2);
-            if (cfg.mlp == 1) gemm(QT_EPI_SWIGLU, w.gu, w.s_gu, B, n_gu, kd_pad, mid, dff);
+            if (!(g_skip & 1)) gemm(QT_EPI_RESADD, w.o, w.s_o, B, d, kd_pad, xcur, d);
+            if (!(g_skip & 4)) norm_quant(xcur, 1, d, w.g2, B, d, kd_pad, 4 * l + 2);
+            if (g_skip & 1) {} else if (cfg.mlp == 1) gemm(QT_EPI_SWIGLU, w.gu, w.s_gu, B, n_gu, kd_pad, mid, dff);
             else gemm(QT_EPI_SILU, w.gu, w.s_gu, B, n_gu, kd_pad, mid, dff);
-            norm_quant(mid, 0, dff, nullptr, B, dff, kff_pad, 4 * l + 3);
-            gemm(QT_EPI_RESADD, w.down, w.s_down, B, d, kff_pad, xcur, d);
+            if (!(g_skip & 4)) norm_quant(mid, 0, dff, nullptr, B, dff, kff_pad, 4 * l + 3);
+            if (!(g_skip & 1)) gemm(QT_EPI_RESADD, w.down, w.s_down, B, d, kff_pad, xcur, d);
         }
         norm_quant(xcur, 1, d, gf, B, d, kd_pad, 4 * L);
         gemm(QT_EPI_STORE, head, s_head, B, d, kd_pad, dlogits, d);
@@ -845,6 +847,8 @@ struct qt_engine {
 // captured graph replays unchanged)
 namespace qt {
 __global__ void k_bump(int* kv_len, int n, int* next_pos, int B) {
+    pdl_launch_dependents();
+    pdl_wait();
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) kv_len[i] += 1;
     if (i < B) next_pos[i] += 1;  // model.cpp:556
@@ -854,8 +858,7 @@ __global__ void k_bump(int* kv_len, int n, int* next_pos, int B) {
 extern "C" {
 
 int qt_launch_kv_len_bump(int* kv_len, int n, int* next_pos, int B, cudaStream_t st) {
-    qt::k_bump<<<(std::max(n, B) + 255) / 256, 256, 0, st>>>(kv_len, n, next_pos, B);
-    return (int)cudaGetLastError();
+    return qt::launch_pdl(qt::k_bump, dim3((std::max(n, B) + 255) / 256), dim3(256), 0, st, kv_len, n, next_pos, B);
 }
 
 const char* qt_last_error(void) { return g_err.c_str(); }

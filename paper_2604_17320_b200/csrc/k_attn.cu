@@ -318,87 +318,95 @@ __global__ void __launch_bounds__(128) k_attn_colsum(const float* __restrict__ q
 }
 
 // ============================================================== K6
-// grid (splits, H, B), 128 threads.  Each split covers pages_per_split pages of
-// the sequence's layer cache (length read from device memory so the decode
-// step can be replayed from a CUDA graph).  4 lanes per key row: each lane
-// holds 32 channels (16 bytes of int4 codes) of the row.
+// grid (pages, H, B), 128 threads: one CTA per (64-row page, query head,
+// sequence) -- the cache length is read from device memory so the decode step
+// replays from a CUDA graph.  Each warp owns 16 rows; 4 lanes per row each
+// hold 32 channels (16 bytes of int4 codes), and both of a lane's rows are
+// loaded before any math so two 128-bit loads per operand are in flight.
 template <int DH>
 __global__ void __launch_bounds__(128) k_attn_decode(const float* __restrict__ qkv, int ldq, int H, int Hkv,
                                                      const int* __restrict__ kv_len, int len_add,
                                                      const uint8_t* __restrict__ pool, long long page_bytes,
-                                                     const int* __restrict__ pt, int max_pages, int pages_per_split,
-                                                     float inv_sqrt, float* __restrict__ part_ml,
-                                                     float* __restrict__ part_o) {
-    constexpr int CPL = DH / 4;  // channels per lane (32 for dh=128, 16 for dh=64)
-    const int b = blockIdx.z, h = blockIdx.y, sp = blockIdx.x, nsp = gridDim.x;
+                                                     const int* __restrict__ pt, int max_pages, float inv_sqrt,
+                                                     float* __restrict__ part_ml, float* __restrict__ part_o) {
+    constexpr int CPL = DH / 4;  // channels per lane
+    constexpr int R = 2;         // rows per lane
+    pdl_launch_dependents();
+    pdl_wait();
+    const int b = blockIdx.z, h = blockIdx.y, pg = blockIdx.x, npg = gridDim.x;
     const int kh = h / (H / Hkv);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int q4 = lane & 3, quad = lane >> 2;
     const int len = kv_len[b] + len_add;
-    const int r0 = sp * pages_per_split * kPage, r1 = min(len, r0 + pages_per_split * kPage);
-
+    const int r0 = pg * kPage;
+    const size_t pidx = ((size_t)b * H + h) * npg + pg;
+    if (r0 >= len) {
+        if (threadIdx.x < DH) part_o[pidx * DH + threadIdx.x] = 0.f;
+        if (threadIdx.x == 0) {
+            part_ml[pidx * 2] = -1e30f;
+            part_ml[pidx * 2 + 1] = 0.f;
+        }
+        return;
+    }
+    const uint8_t* page = pool + (long long)pt[b * max_pages + pg] * page_bytes;
+    const size_t cb = (size_t)Hkv * kPage * (DH / 2);
+    const float* sc = reinterpret_cast<const float*>(page + 2 * cb);
+    uint32_t kw[R][CPL / 8], vw[R][CPL / 8];
+    float sk[R], sv[R];
+    bool valid[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+        const int slot = warp * 16 + quad + 8 * i;
+        valid[i] = r0 + slot < len;
+        const uint8_t* krow = page + ((size_t)kh * kPage + slot) * (DH / 2) + q4 * (CPL / 2);
+        if (CPL == 32) {
+            uint4 ka = valid[i] ? ldg_nc_v4(krow) : make_uint4(0, 0, 0, 0);
+            uint4 va = valid[i] ? ldg_nc_v4(krow + cb) : make_uint4(0, 0, 0, 0);
+            kw[i][0] = ka.x; kw[i][1] = ka.y; kw[i][2] = ka.z; kw[i][3] = ka.w;
+            vw[i][0] = va.x; vw[i][1] = va.y; vw[i][2] = va.z; vw[i][3] = va.w;
+        } else {
+            uint2 ka = valid[i] ? *reinterpret_cast<const uint2*>(krow) : make_uint2(0, 0);
+            uint2 va = valid[i] ? *reinterpret_cast<const uint2*>(krow + cb) : make_uint2(0, 0);
+            kw[i][0] = ka.x; kw[i][1] = ka.y;
+            vw[i][0] = va.x; vw[i][1] = va.y;
+        }
+        sk[i] = valid[i] ? sc[kh * kPage + slot] : 0.f;
+        sv[i] = valid[i] ? sc[Hkv * kPage + kh * kPage + slot] : 0.f;
+    }
     float q[CPL];
     const float* qp = qkv + (size_t)b * ldq + h * DH + q4 * CPL;
 #pragma unroll
     for (int i = 0; i < CPL; i += 4) {
         float4 v = *reinterpret_cast<const float4*>(qp + i);
-        q[i] = v.x;
-        q[i + 1] = v.y;
-        q[i + 2] = v.z;
-        q[i + 3] = v.w;
+        q[i] = v.x; q[i + 1] = v.y; q[i + 2] = v.z; q[i + 3] = v.w;
     }
-    float acc[CPL];
+    float s[R];
 #pragma unroll
-    for (int i = 0; i < CPL; ++i) acc[i] = 0.f;
-    float m = -1e30f, l = 0.f;
-    const size_t cb = (size_t)Hkv * kPage * (DH / 2);
-    // rows r = base + quad with a warp-uniform base (stride 32) so every lane
-    // takes part in the quad shuffles; rows past the end contribute nothing
-    for (int base = r0 + warp * 8; base < r1; base += 32) {
-        const int r = base + quad;
-        const bool valid = r < r1;
-        uint32_t kw[CPL / 8], vw[CPL / 8];
-        float sk = 0.f, sv = 0.f;
-#pragma unroll
-        for (int w = 0; w < CPL / 8; ++w) kw[w] = vw[w] = 0u;
-        if (valid) {
-            const uint8_t* page = pool + (long long)pt[b * max_pages + r / kPage] * page_bytes;
-            const int slot = r % kPage;
-            const uint8_t* krow = page + ((size_t)kh * kPage + slot) * (DH / 2) + q4 * (CPL / 2);
-            const uint8_t* vrow = krow + cb;
-            const float* sc = reinterpret_cast<const float*>(page + 2 * cb);
-            sk = sc[kh * kPage + slot];
-            sv = sc[Hkv * kPage + kh * kPage + slot];
-            if (CPL == 32) {
-                uint4 a = ldg_nc_v4(krow), c = ldg_nc_v4(vrow);
-                kw[0] = a.x; kw[1] = a.y; kw[2] = a.z; kw[3] = a.w;
-                vw[0] = c.x; vw[1] = c.y; vw[2] = c.z; vw[3] = c.w;
-            } else {
-                uint2 a = *reinterpret_cast<const uint2*>(krow), c = *reinterpret_cast<const uint2*>(vrow);
-                kw[0] = a.x; kw[1] = a.y;
-                vw[0] = c.x; vw[1] = c.y;
-            }
-        }
+    for (int i = 0; i < R; ++i) {
         float d = 0.f;
 #pragma unroll
         for (int w = 0; w < CPL / 8; ++w)
 #pragma unroll
-            for (int e = 0; e < 8; ++e) d = fmaf(q[w * 8 + e], (float)nib(kw[w], e), d);
+            for (int e = 0; e < 8; ++e) d = fmaf(q[w * 8 + e], (float)nib(kw[i][w], e), d);
         d += __shfl_xor_sync(0xffffffffu, d, 1);
         d += __shfl_xor_sync(0xffffffffu, d, 2);
-        if (valid) {
-            const float s = d * sk * inv_sqrt;
-            const float mn = fmaxf(m, s);
-            const float alpha = expf(m - mn);
-            const float p = expf(s - mn);
-            l = l * alpha + p;
-            m = mn;
-            const float pv = p * sv;
+        s[i] = valid[i] ? d * sk[i] * inv_sqrt : -1e30f;
+    }
+    float m = fmaxf(s[0], s[1]);
+    float l = 0.f;
+    float acc[CPL];
 #pragma unroll
-            for (int w = 0; w < CPL / 8; ++w)
+    for (int c = 0; c < CPL; ++c) acc[c] = 0.f;
 #pragma unroll
-                for (int e = 0; e < 8; ++e) acc[w * 8 + e] = fmaf(pv, (float)nib(vw[w], e), acc[w * 8 + e] * alpha);
-        }
+    for (int i = 0; i < R; ++i) {
+        if (!valid[i]) continue;
+        const float p = expf(s[i] - m);
+        l += p;
+        const float pv = p * sv[i];
+#pragma unroll
+        for (int w = 0; w < CPL / 8; ++w)
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc[w * 8 + e] = fmaf(pv, (float)nib(vw[i][w], e), acc[w * 8 + e]);
     }
     // merge the 8 quads of the warp (lanes with equal q4)
 #pragma unroll
@@ -409,32 +417,30 @@ __global__ void __launch_bounds__(128) k_attn_decode(const float* __restrict__ q
         const float a1 = expf(m - mn), a2 = expf(mo - mn);
         l = l * a1 + lo * a2;
 #pragma unroll
-        for (int i = 0; i < CPL; ++i) {
-            const float ao = __shfl_xor_sync(0xffffffffu, acc[i], o);
-            acc[i] = acc[i] * a1 + ao * a2;
+        for (int c = 0; c < CPL; ++c) {
+            const float ao = __shfl_xor_sync(0xffffffffu, acc[c], o);
+            acc[c] = acc[c] * a1 + ao * a2;
         }
         m = mn;
     }
-    // merge the 4 warps through smem (fixed order)
-    __shared__ float sm[4][2];
+    __shared__ float smx[4][2];
     __shared__ float so[4][DH];
     if (quad == 0) {
 #pragma unroll
-        for (int i = 0; i < CPL; ++i) so[warp][q4 * CPL + i] = acc[i];
+        for (int c = 0; c < CPL; ++c) so[warp][q4 * CPL + c] = acc[c];
         if (q4 == 0) {
-            sm[warp][0] = m;
-            sm[warp][1] = l;
+            smx[warp][0] = m;
+            smx[warp][1] = l;
         }
     }
     __syncthreads();
-    const size_t pidx = ((size_t)b * H + h) * nsp + sp;
     if (threadIdx.x < DH) {
         float mm = -1e30f;
-        for (int w = 0; w < 4; ++w) mm = fmaxf(mm, sm[w][0]);
+        for (int w = 0; w < 4; ++w) mm = fmaxf(mm, smx[w][0]);
         float ll = 0.f, oo = 0.f;
         for (int w = 0; w < 4; ++w) {
-            const float a = expf(sm[w][0] - mm);
-            ll += sm[w][1] * a;
+            const float a = smx[w][1] > 0.f ? expf(smx[w][0] - mm) : 0.f;
+            ll += smx[w][1] * a;
             oo += so[w][threadIdx.x] * a;
         }
         part_o[pidx * DH + threadIdx.x] = oo;
@@ -445,20 +451,81 @@ __global__ void __launch_bounds__(128) k_attn_decode(const float* __restrict__ q
     }
 }
 
-// merge splits in fixed order: out[b][h*DH + c]
-__global__ void k_attn_decode_merge(const float* __restrict__ part_ml, const float* __restrict__ part_o, int nsp,
-                                    int H, int DH, float* __restrict__ out, int ldo) {
-    const int b = blockIdx.y, h = blockIdx.x, c = threadIdx.x;
-    const size_t base = ((size_t)b * H + h) * nsp;
-    float mm = -1e30f;
-    for (int s = 0; s < nsp; ++s) mm = fmaxf(mm, part_ml[(base + s) * 2]);
-    float ll = 0.f, oo = 0.f;
-    for (int s = 0; s < nsp; ++s) {
-        const float a = expf(part_ml[(base + s) * 2] - mm);
-        ll += part_ml[(base + s) * 2 + 1] * a;
-        if (c < DH) oo += part_o[(base + s) * DH + c] * a;
+// Merge the page partials of every head of one sequence (fixed page order) and,
+// optionally, quantize the concatenated attention row (the attn_out site,
+// model.cpp:394/539) in the same kernel.  grid B, 1024 threads: warp w merges
+// heads w, w+32, ...; lane c holds channels c*CPL.. of that head.
+template <int DH, int MAXH>
+__global__ void __launch_bounds__(1024) k_attn_merge_quant(const float* __restrict__ part_ml,
+                                                           const float* __restrict__ part_o, int npg, int H,
+                                                           float* __restrict__ out, int ldo,
+                                                           uint8_t* __restrict__ codes, int ld_codes,
+                                                           double* __restrict__ scales, int mode, double static_scale,
+                                                           int d_pad, int qmax) {
+    constexpr int CPL = DH / 32;
+    __shared__ double red[32];
+    pdl_launch_dependents();
+    pdl_wait();
+    const int b = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int HPW = (MAXH + 31) / 32;  // heads per warp
+    float o[HPW][CPL];
+    double mx = 0.0;
+#pragma unroll
+    for (int hh = 0; hh < HPW; ++hh) {
+        const int h = warp + 32 * hh;
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) o[hh][c] = 0.f;
+        if (h >= H) continue;
+        const size_t base = ((size_t)b * H + h) * npg;
+        float M = -1e30f;
+        for (int p = lane; p < npg; p += 32) M = fmaxf(M, part_ml[(base + p) * 2]);
+        M = warp_max(M);
+        float L = 0.f;
+        for (int p = 0; p < npg; ++p) {
+            const float lp = part_ml[(base + p) * 2 + 1];
+            if (lp == 0.f) continue;
+            const float a = expf(part_ml[(base + p) * 2] - M);
+            L += lp * a;
+#pragma unroll
+            for (int c = 0; c < CPL; ++c) o[hh][c] += part_o[(base + p) * DH + lane * CPL + c] * a;
+        }
+        const float il = 1.f / L;
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+            o[hh][c] *= il;
+            mx = fmax(mx, fabs((double)o[hh][c]));
+            if (out) out[(size_t)b * ldo + h * DH + lane * CPL + c] = o[hh][c];
+        }
     }
-    if (c < DH) out[(size_t)b * ldo + h * DH + c] = oo / ll;
+    if (!codes) return;
+    double s;
+    if (mode == 0) {
+        s = static_scale;
+    } else {
+        mx = block_max(mx, red);
+        s = q_scale(mx, qmax);
+    }
+    const double inv_s = 1.0 / s;
+    uint8_t* crow = codes + (size_t)b * ld_codes;
+#pragma unroll
+    for (int hh = 0; hh < HPW; ++hh) {
+        const int h = warp + 32 * hh;
+        if (h >= H) continue;
+        int c[CPL];
+#pragma unroll
+        for (int e = 0; e < CPL; ++e) c[e] = q_code_r((double)o[hh][e], s, inv_s, qmax);
+        const int k0 = h * DH + lane * CPL;
+        if (CPL == 4) {
+            *reinterpret_cast<uint16_t*>(crow + k0 / 2) =
+                (uint16_t)((c[0] & 0xF) | ((c[1] & 0xF) << 4) | ((c[2] & 0xF) << 8) | ((c[3] & 0xF) << 12));
+        } else {
+            crow[k0 / 2] = (uint8_t)((c[0] & 0xF) | ((c[1] & 0xF) << 4));
+        }
+    }
+    // zero the K padding of this row
+    for (int k = H * DH + threadIdx.x * 2; k < d_pad; k += blockDim.x * 2) crow[k / 2] = 0;
+    if (threadIdx.x == 0) scales[b] = s;
 }
 
 }  // namespace qt
@@ -504,21 +571,32 @@ int qt_launch_attn_colsum(const float* qkv, int ldq, int H, int Hkv, int dh, con
 }
 
 int qt_launch_attn_decode(const float* qkv, int ldq, int H, int Hkv, int dh, const int* kv_len, int len_add, int B,
-                          const uint8_t* pool, long long page_bytes, const int* pt, int max_pages, int splits,
-                          int pages_per_split, float* part_ml, float* part_o, float* out, int ldo, cudaStream_t st) {
+                          const uint8_t* pool, long long page_bytes, const int* pt, int max_pages, int n_pages,
+                          float* part_ml, float* part_o, float* out, int ldo, uint8_t* codes, int ld_codes,
+                          double* scales, int qmode, double static_scale, int d_pad, int bits, cudaStream_t st) {
     if (B <= 0) return 0;
-    const dim3 grid(splits, H, B);
+    if (H > 64) return -1;
+    const dim3 grid(n_pages, H, B);
     const float inv_sqrt = (float)(1.0 / sqrt((double)dh));
-    if (dh == 128)
-        k_attn_decode<128><<<grid, 128, 0, st>>>(qkv, ldq, H, Hkv, kv_len, len_add, pool, page_bytes, pt, max_pages,
-                                                 pages_per_split, inv_sqrt, part_ml, part_o);
-    else if (dh == 64)
-        k_attn_decode<64><<<grid, 128, 0, st>>>(qkv, ldq, H, Hkv, kv_len, len_add, pool, page_bytes, pt, max_pages,
-                                                pages_per_split, inv_sqrt, part_ml, part_o);
-    else
-        return -1;
-    k_attn_decode_merge<<<dim3(H, B), 128, 0, st>>>(part_ml, part_o, splits, H, dh, out, ldo);
-    return (int)cudaGetLastError();
+    const int qmax = (1 << (bits - 1)) - 1;
+    int rc;
+    if (dh == 128) {
+        rc = launch_pdl(k_attn_decode<128>, grid, dim3(128), 0, st, qkv, ldq, H, Hkv, kv_len, len_add, pool,
+                        page_bytes, pt, max_pages, inv_sqrt, part_ml, part_o);
+        if (rc) return rc;
+        auto mk = H > 32 ? k_attn_merge_quant<128, 64> : k_attn_merge_quant<128, 32>;
+        return launch_pdl(mk, dim3(B), dim3(1024), 0, st, (const float*)part_ml, (const float*)part_o, n_pages, H, out,
+                          ldo, codes, ld_codes, scales, qmode, static_scale, d_pad, qmax);
+    }
+    if (dh == 64) {
+        rc = launch_pdl(k_attn_decode<64>, grid, dim3(128), 0, st, qkv, ldq, H, Hkv, kv_len, len_add, pool,
+                        page_bytes, pt, max_pages, inv_sqrt, part_ml, part_o);
+        if (rc) return rc;
+        auto mk = H > 32 ? k_attn_merge_quant<64, 64> : k_attn_merge_quant<64, 32>;
+        return launch_pdl(mk, dim3(B), dim3(1024), 0, st, (const float*)part_ml, (const float*)part_o, n_pages, H, out,
+                          ldo, codes, ld_codes, scales, qmode, static_scale, d_pad, qmax);
+    }
+    return -1;
 }
 
 }  // extern "C"

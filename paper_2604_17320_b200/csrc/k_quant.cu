@@ -39,66 +39,79 @@ QT_DEV void load8<double>(const double* p, double* v) {
     }
 }
 
-template <typename TX>
-__global__ void __launch_bounds__(256) k_norm_quant(const TX* __restrict__ x, int ld_x,
-                                                    const float* __restrict__ gain, int M, int D, int d_pad,
-                                                    int qmax, int mode, double static_scale,
-                                                    uint8_t* __restrict__ codes, int ld_codes,
-                                                    double* __restrict__ scales, float* __restrict__ normed) {
+// Register-resident: each thread owns G groups of 8 consecutive elements
+// (words w = tid + j * blockDim), read once from global memory; the RMS sum
+// and the row max are block reductions over those registers.
+template <typename TX, int G>
+__global__ void __launch_bounds__(1024) k_norm_quant(const TX* __restrict__ x, int ld_x,
+                                                     const float* __restrict__ gain, int M, int D, int d_pad,
+                                                     int qmax, int mode, double static_scale,
+                                                     uint8_t* __restrict__ codes, int ld_codes,
+                                                     double* __restrict__ scales, float* __restrict__ normed) {
     __shared__ double red[32];
+    pdl_launch_dependents();
+    pdl_wait();  // x is produced by the previous kernel
     const int row = blockIdx.x;
     if (row >= M) return;
     const TX* xr = x + (size_t)row * ld_x;
-    double inv = 1.0;
+    const int n_words = d_pad / 8;
+    double v[G][8];
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+        const int base = (threadIdx.x + j * blockDim.x) * 8;
+        if (base < D) {
+            load8<TX>(xr + base, v[j]);
+        } else {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) v[j][e] = 0.0;
+        }
+    }
     if (gain) {
         double ss = 0.0;
-        for (int i = threadIdx.x * 8; i < D; i += blockDim.x * 8) {
-            double v[8];
-            load8<TX>(xr + i, v);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) ss += v[j] * v[j];
-        }
+        for (int j = 0; j < G; ++j)
+#pragma unroll
+            for (int e = 0; e < 8; ++e) ss += v[j][e] * v[j][e];
         ss = block_sum(ss, red);
-        inv = 1.0 / sqrt(ss / (double)D + kNormEps);
+        const double inv = 1.0 / sqrt(ss / (double)D + kNormEps);
+#pragma unroll
+        for (int j = 0; j < G; ++j) {
+            const int base = (threadIdx.x + j * blockDim.x) * 8;
+            if (base < D) {
+                float4 g0 = *reinterpret_cast<const float4*>(gain + base);
+                float4 g1 = *reinterpret_cast<const float4*>(gain + base + 4);
+                const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+#pragma unroll
+                for (int e = 0; e < 8; ++e) v[j][e] = __dmul_rn(__dmul_rn(v[j][e], inv), (double)gg[e]);
+            }
+        }
     }
     double s;
     if (mode == 0) {
         s = static_scale;
     } else {
         double mx = 0.0;
-        for (int i = threadIdx.x * 8; i < D; i += blockDim.x * 8) {
-            double v[8];
-            load8<TX>(xr + i, v);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                double n = gain ? __dmul_rn(__dmul_rn(v[j], inv), (double)gain[i + j]) : v[j];
-                mx = fmax(mx, fabs(n));
-            }
-        }
+        for (int j = 0; j < G; ++j)
+#pragma unroll
+            for (int e = 0; e < 8; ++e) mx = fmax(mx, fabs(v[j][e]));
         mx = block_max(mx, red);
         s = q_scale(mx, qmax);
     }
-    // codes, 8 per 32-bit word
     const double inv_s = 1.0 / s;
     uint32_t* cw = reinterpret_cast<uint32_t*>(codes + (size_t)row * ld_codes);
-    const int n_words = d_pad / 8;
-    for (int w = threadIdx.x; w < n_words; w += blockDim.x) {
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+        const int w = threadIdx.x + j * blockDim.x;
+        if (w >= n_words) continue;
         int c[8];
-        const int base = w * 8;
-        if (base < D) {
-            double v[8];
-            load8<TX>(xr + base, v);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                double n = gain ? __dmul_rn(__dmul_rn(v[j], inv), (double)gain[base + j]) : v[j];
-                c[j] = q_code_r(n, s, inv_s, qmax);
-                if (normed) normed[(size_t)row * D + base + j] = (float)n;
-            }
-        } else {
-#pragma unroll
-            for (int j = 0; j < 8; ++j) c[j] = 0;
-        }
+        for (int e = 0; e < 8; ++e) c[e] = w * 8 + e < D ? q_code_r(v[j][e], s, inv_s, qmax) : 0;
         cw[w] = pack8(c);
+        if (normed && w * 8 < D) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) normed[(size_t)row * D + w * 8 + e] = (float)v[j][e];
+        }
     }
     if (threadIdx.x == 0) scales[row] = s;
 }
@@ -115,6 +128,8 @@ __global__ void __launch_bounds__(256) k_rope_kv_append(
     const int* __restrict__ tok_seq, const int* __restrict__ tok_row, const double2* __restrict__ rope,
     const int* __restrict__ page_table, int max_pages, uint8_t* __restrict__ pool, long long page_bytes,
     int qmax, float* __restrict__ k_dbg) {
+    pdl_launch_dependents();
+    pdl_wait();
     const int m = blockIdx.x;
     if (m >= M) return;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -249,11 +264,13 @@ __global__ void k_weight_pack(const float* __restrict__ w, int K, int N, const d
         c[j] = k < K ? q_code((double)w[(size_t)k * N + n], s, qmax) : 0;
     }
     const int dst = n * row_mul + row_add;
-    reinterpret_cast<uint32_t*>(codes + (size_t)dst * ldc)[wd] = pack8(c);
+    *reinterpret_cast<uint32_t*>(codes + w4t_offset(dst, wd * 4, ldc)) = pack8(c);  // tiled layout
     if (wd == 0) scales[dst] = s;
 }
 
 __global__ void k_f32_to_f64(const float* __restrict__ a, double* __restrict__ b, long long n) {
+    pdl_launch_dependents();
+    pdl_wait();
     long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) b[i] = (double)a[i];
 }
@@ -267,8 +284,7 @@ extern "C" {
 
 int qt_launch_f32_to_f64(const float* a, double* b, long long n, cudaStream_t st) {
     if (n <= 0) return 0;
-    k_f32_to_f64<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(a, b, n);
-    return (int)cudaGetLastError();
+    return launch_pdl(k_f32_to_f64, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, a, b, n);
 }
 
 int qt_launch_norm_quant(const void* x, int x_is_f64, int ld_x, const float* gain, int M, int D, int d_pad,
@@ -277,14 +293,23 @@ int qt_launch_norm_quant(const void* x, int x_is_f64, int ld_x, const float* gai
     if (M <= 0) return 0;
     if (D % 8 || d_pad % 8 || ld_x % 4) return -1;
     const int qmax = (1 << (bits - 1)) - 1;
-    const int threads = D >= 2048 ? 256 : 128;
-    if (x_is_f64)
-        k_norm_quant<double><<<M, threads, 0, st>>>(static_cast<const double*>(x), ld_x, gain, M, D, d_pad, qmax,
-                                                    mode, static_scale, codes, ld_codes, scales, normed);
-    else
-        k_norm_quant<float><<<M, threads, 0, st>>>(static_cast<const float*>(x), ld_x, gain, M, D, d_pad, qmax, mode,
-                                                   static_scale, codes, ld_codes, scales, normed);
-    return (int)cudaGetLastError();
+    const int words = d_pad / 8;
+    int threads = words <= 256 ? 256 : (words <= 512 ? 512 : 1024);
+    const int G = (words + threads - 1) / threads;
+    if (G > 3) return -1;
+#define QT_NQ(TX, GG)                                                                                        \
+    return launch_pdl(k_norm_quant<TX, GG>, dim3(M), dim3(threads), 0, st, static_cast<const TX*>(x), ld_x, \
+                      gain, M, D, d_pad, qmax, mode, static_scale, codes, ld_codes, scales, normed)
+    if (x_is_f64) {
+        if (G == 1) QT_NQ(double, 1);
+        if (G == 2) QT_NQ(double, 2);
+        QT_NQ(double, 3);
+    } else {
+        if (G == 1) QT_NQ(float, 1);
+        if (G == 2) QT_NQ(float, 2);
+        QT_NQ(float, 3);
+    }
+#undef QT_NQ
 }
 
 int qt_launch_rope_kv_append(float* qkv, int ld_qkv, int M, int H, int Hkv, int dh, const int* pos,
@@ -294,10 +319,9 @@ int qt_launch_rope_kv_append(float* qkv, int ld_qkv, int M, int H, int Hkv, int 
     if (M <= 0) return 0;
     if (dh != 64 && dh != 128) return -1;
     const int qmax = (1 << (bits - 1)) - 1;
-    k_rope_kv_append<<<dim3(M, (H + 2 * Hkv + 7) / 8), 256, 0, st>>>(qkv, ld_qkv, M, H, Hkv, dh, pos, tok_seq, tok_row,
-                                        reinterpret_cast<const double2*>(rope), page_table, max_pages, pool,
-                                        page_bytes, qmax, k_dbg);
-    return (int)cudaGetLastError();
+    return launch_pdl(k_rope_kv_append, dim3(M, (H + 2 * Hkv + 7) / 8), dim3(256), 0, st, qkv, ld_qkv, M, H, Hkv,
+                      dh, pos, tok_seq, tok_row, reinterpret_cast<const double2*>(rope), page_table, max_pages, pool,
+                      page_bytes, qmax, k_dbg);
 }
 
 int qt_launch_token_metrics(const double* x, int D, const int* seq_off, const int* vis, int vmax, int B,

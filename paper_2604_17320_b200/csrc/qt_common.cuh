@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #define QT_DEV __device__ __forceinline__
+#define QT_HD __host__ __device__ __forceinline__
 
 namespace qt {
 
@@ -96,6 +97,49 @@ QT_DEV void unpack_x16(uint32_t w, uint32_t& lo, uint32_t& hi) {
 
 QT_DEV int nib(uint32_t w, int i) { return ((int)(w << (28 - 4 * i))) >> 28; }
 
+// ---------------------------------------------------------------- W4 tiled layout
+// Packed int4 weights [N_pad x K_pad] are stored as 1 KB tiles of 16 rows x 128 k
+// (16 rows x 64 bytes, row-major inside the tile); tile (rt, kt) sits at
+// ((rt * KT) + kt) * 1024 with KT = K_pad / 128, so one 16-row block's whole K
+// slab is contiguous (TMA bulk copies) and a lane (g, tig) of an mma.sync
+// fragment reads 16 contiguous bytes at tile + g*64 + tig*16 (+512 for rows 8-15).
+QT_HD size_t w4t_offset(int row, int kbyte, int row_bytes) {
+    const int KT = row_bytes / 64;
+    return ((size_t)(row >> 4) * KT + (kbyte >> 6)) * 1024 + (size_t)(row & 15) * 64 + (kbyte & 63);
+}
+
+// ---------------------------------------------------------------- mbarrier / TMA bulk
+QT_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+QT_DEV void mbar_init(uint64_t* bar, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+QT_DEV void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
+QT_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+QT_DEV void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+QT_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// 1D TMA bulk copy global -> shared, completion counted on an mbarrier
+QT_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
 // ---------------------------------------------------------------- mma.sync
 // D(16x8 s32) += A(16x32 s8, row) * B(32x8 s8, col)
 QT_DEV void mma_s8_16832(int* d, const uint32_t* a, const uint32_t* b) {
@@ -154,5 +198,39 @@ QT_DEV uint4 ldg_nc_v4(const void* p) {
 }
 
 QT_DEV float silu_f(float x) { return x / (1.0f + expf(-x)); }
+
+// ---------------------------------------------------------------- PDL
+// Programmatic dependent launch: a kernel launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization may start while its
+// predecessor drains; pdl_wait() blocks until the predecessor grid completed
+// and its writes are visible.  Every kernel calls pdl_wait() before touching
+// data produced upstream (and before exiting), so completion stays transitive.
+QT_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+QT_DEV void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
+}  // namespace qt
+
+#ifndef __CUDACC_RTC__
+namespace qt {
+template <typename... KArgs, typename... Args>
+inline int launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                      Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+    return (int)e;
+}
+}  // namespace qt
+#endif
+
+namespace qt {
 
 }  // namespace qt

@@ -88,7 +88,7 @@ def test_weight_quant_per_output_channel(torch_cuda):
     k_pad, n_pad = 384, 256
     codes, scales = Q.quant_weight(torch.from_numpy(w).cuda(), k_pad, n_pad)
     exp_codes, exp_scales = ref_quant_fit(w.astype(np.float64), 2)
-    got = Q.unpack_i4(codes.cpu().numpy(), k_pad)
+    got = Q.unpack_i4(Q.untile_w4(codes.cpu().numpy(), n_pad, k_pad // 2), k_pad)
     assert np.array_equal(got[:N, :K], exp_codes.T)
     assert np.all(got[:N, K:] == 0)
     assert np.array_equal(scales.cpu().numpy()[:N], exp_scales)
@@ -111,7 +111,7 @@ def test_w4a4_gemm_int32_exact(torch_cuda, M, impl):
     sa = rng.uniform(0.01, 0.5, M)
     sw = rng.uniform(0.001, 0.01, N)
     ad = torch.from_numpy(_pack(a)).cuda()
-    wd = torch.from_numpy(_pack(w)).cuda()
+    wd = torch.from_numpy(Q.tile_w4(_pack(w))).cuda()
     sad, swd = torch.from_numpy(sa).cuda(), torch.from_numpy(sw).cuda()
     out = torch.zeros((M, N), dtype=torch.float32, device="cuda")
     acc = torch.zeros((M, N), dtype=torch.int32, device="cuda")
@@ -148,7 +148,7 @@ def test_w4a4_gemm_epilogues(torch_cuda, M, epi):
         out = torch.zeros((M, N), dtype=torch.float32, device="cuda")
         exp = y / (1 + np.exp(-y))
         tol = dict(rtol=1e-6, atol=1e-7)
-    Q.w4a4_gemm(epi, torch.from_numpy(_pack(a)).cuda(), torch.from_numpy(sa).cuda(), torch.from_numpy(_pack(w)).cuda(),
+    Q.w4a4_gemm(epi, torch.from_numpy(_pack(a)).cuda(), torch.from_numpy(sa).cuda(), torch.from_numpy(Q.tile_w4(_pack(w))).cuda(),
                 torch.from_numpy(sw).cuda(), M, N, K, out)
     torch.cuda.synchronize()
     np.testing.assert_allclose(out.cpu().numpy(), exp, **tol)
