@@ -293,8 +293,8 @@ def rmsnorm_quant(x, gain, d_pad, act_mode, static_scale=0.0, codes=None, scales
     """K1 on a torch fp32/fp64 cuda tensor x [M x D]; returns (packed codes, fp64 scales)."""
     import torch
     M, D = x.shape
-    if codes is None:
-        codes = torch.zeros((M, d_pad // 2), dtype=torch.uint8, device=x.device)
+    if codes is None:  # tiled layout: rows padded to 16
+        codes = torch.zeros(((M + 15) // 16 * 16, d_pad // 2), dtype=torch.uint8, device=x.device)
     if scales is None:
         scales = torch.zeros(M, dtype=torch.float64, device=x.device)
     is64 = int(x.dtype == torch.float64)

@@ -249,7 +249,7 @@ struct qt_engine {
     std::vector<std::vector<PruneEv>> trace;
     std::vector<int> h_kvlen;             // [L][B]
     bool prefilled = false;
-    bool use_tc05 = false;
+    bool use_tc05 = !(std::getenv("QT_TC05") && std::atoi(std::getenv("QT_TC05")) == 0);  // tcgen05 GEMM for M > 16
     std::unique_ptr<Profiler> prof;      // active while profiling one call
     bool prof_next = false;
     double prof_out[P_NCLASS * 4] = {0};
@@ -353,7 +353,7 @@ struct qt_engine {
         qkv = dalloc<float>(T * n_qkv);
         attn = dalloc<float>(T * d);
         mid = dalloc<float>(T * dff);
-        codes = dalloc<uint8_t>(T * (size_t)std::max(kd_pad, kff_pad) / 2);
+        codes = dalloc<uint8_t>((size_t)round_up((int)T, 16) * std::max(kd_pad, kff_pad) / 2);  // tiled rows
         ascale = dalloc<double>(T);
         logits = dalloc<float>(T * d);
         ml = dalloc<float>(T * H * 2);

@@ -507,7 +507,6 @@ __global__ void __launch_bounds__(1024) k_attn_merge_quant(const float* __restri
         s = q_scale(mx, qmax);
     }
     const double inv_s = 1.0 / s;
-    uint8_t* crow = codes + (size_t)b * ld_codes;
 #pragma unroll
     for (int hh = 0; hh < HPW; ++hh) {
         const int h = warp + 32 * hh;
@@ -517,14 +516,14 @@ __global__ void __launch_bounds__(1024) k_attn_merge_quant(const float* __restri
         for (int e = 0; e < CPL; ++e) c[e] = q_code_r((double)o[hh][e], s, inv_s, qmax);
         const int k0 = h * DH + lane * CPL;
         if (CPL == 4) {
-            *reinterpret_cast<uint16_t*>(crow + k0 / 2) =
+            *reinterpret_cast<uint16_t*>(codes + w4t_offset(b, k0 / 2, ld_codes)) =
                 (uint16_t)((c[0] & 0xF) | ((c[1] & 0xF) << 4) | ((c[2] & 0xF) << 8) | ((c[3] & 0xF) << 12));
         } else {
-            crow[k0 / 2] = (uint8_t)((c[0] & 0xF) | ((c[1] & 0xF) << 4));
+            codes[w4t_offset(b, k0 / 2, ld_codes)] = (uint8_t)((c[0] & 0xF) | ((c[1] & 0xF) << 4));
         }
     }
     // zero the K padding of this row
-    for (int k = H * DH + threadIdx.x * 2; k < d_pad; k += blockDim.x * 2) crow[k / 2] = 0;
+    for (int k = H * DH + threadIdx.x * 2; k < d_pad; k += blockDim.x * 2) codes[w4t_offset(b, k / 2, ld_codes)] = 0;
     if (threadIdx.x == 0) scales[b] = s;
 }
 

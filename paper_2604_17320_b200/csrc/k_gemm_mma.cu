@@ -25,45 +25,10 @@
 #include <cstdlib>
 
 #include "qt_common.cuh"
+#include "qt_epilogue.cuh"
 #include "qt_kernels.h"
 
 namespace qt {
-
-// y = (acc / 256) * s_a[m] * s_w[n] in fp64 (scales are the reference's fp64
-// scales; the integer sum is exact), then the epilogue: store fp32, add into
-// the fp64 residual, SiLU, or SwiGLU over interleaved (gate, up) columns.
-template <int EPI>
-QT_DEV void epi_store(void* __restrict__ outv, int ldo, int m, int n, double y0, double y1, int N) {
-    if (EPI == QT_EPI_RESADD) {
-        double* p = static_cast<double*>(outv) + (size_t)m * ldo + n;
-        if (n + 1 < N) {
-            double2 v = *reinterpret_cast<double2*>(p);
-            v.x += y0;
-            v.y += y1;
-            *reinterpret_cast<double2*>(p) = v;
-        } else if (n < N) {
-            p[0] += y0;
-        }
-        return;
-    }
-    float* out = static_cast<float*>(outv);
-    if (EPI == QT_EPI_SWIGLU) {
-        // silu(g) * u (model.cpp:170-172 silu; SwiGLU is the R1 extension)
-        if (n < N) out[(size_t)m * ldo + n / 2] = (float)(y0 / (1.0 + exp(-y0)) * y1);
-        return;
-    }
-    float* p = out + (size_t)m * ldo + n;
-    float v0, v1;
-    if (EPI == QT_EPI_SILU) {
-        v0 = (float)(y0 / (1.0 + exp(-y0)));
-        v1 = (float)(y1 / (1.0 + exp(-y1)));
-    } else {
-        v0 = (float)y0;
-        v1 = (float)y1;
-    }
-    if (n + 1 < N) *reinterpret_cast<float2*>(p) = make_float2(v0, v1);
-    else if (n < N) p[0] = v0;
-}
 
 // ---------------------------------------------------------------- prefill GEMM
 constexpr int GB_N = 128, GB_K = 128, G_STAGES = 3, G_ROWB = GB_K / 2;  // 64 bytes per row per stage
@@ -93,7 +58,7 @@ __global__ void __launch_bounds__(256) k_gemm_tc(const uint8_t* __restrict__ A, 
         for (int c = tid; c < BM * 4; c += 256) {
             int r = c >> 2, q = c & 3;
             bool ok = m0 + r < M;
-            const uint8_t* src = A + (size_t)(ok ? m0 + r : 0) * lda + kb + q * 16;
+            const uint8_t* src = A + w4t_offset(ok ? m0 + r : 0, kb + q * 16, lda);  // tiled rows
             cp_async16(as + c * 16, src, ok);
         }
 #pragma unroll
@@ -247,7 +212,7 @@ __global__ void __launch_bounds__(288, 1) k_gemv_tc(const uint8_t* __restrict__ 
     for (int c = tid; c < TOK * (kb / 16); c += 256) {
         int r = c / (kb / 16), q = c % (kb / 16);
         bool ok = r < M;
-        cp_async16(As + r * ldsA + q * 16, A + (size_t)(ok ? r : 0) * lda + q * 16, ok);
+        cp_async16(As + r * ldsA + q * 16, A + w4t_offset(ok ? r : 0, q * 16, lda), ok);
     }
     cp_async_commit();
     cp_async_wait<0>();
@@ -362,7 +327,7 @@ __global__ void __launch_bounds__(256) k_gemv_reg(const uint8_t* __restrict__ A,
     for (int c = tid; c < TOK * (kb / 16); c += 256) {
         int r = c / (kb / 16), q = c % (kb / 16);
         bool ok = r < M;
-        cp_async16(As + r * ldsA + q * 16, A + (size_t)(ok ? r : 0) * lda + q * 16, ok);
+        cp_async16(As + r * ldsA + q * 16, A + w4t_offset(ok ? r : 0, q * 16, lda), ok);
     }
     cp_async_commit();
     cp_async_wait<0>();

@@ -1,8 +1,275 @@
-// k_gemm_tc05.cu -- tcgen05 (kind::i8, TMEM accumulators) W4A4 GEMM.  (in progress)
+// k_gemm_tc05.cu -- W4A4 prefill GEMM on the 5th-generation tensor cores
+// (tcgen05.mma kind::i8, int32 accumulators in TMEM), sm_100a.
+//
+//   y[m][n] = s_a[m] * s_w[n] * sum_k a[m][k] * w[n][k]
+//
+// replaces matmul(fake_quant(x), W.deq) (numeric.cpp:33-46 at
+// model.cpp:351-353,395,432,436,445) for the prefill token batch.
+//
+// Pipeline per CTA (one 128 x 256 output tile, K in 128-wide blocks):
+//   warp 0      TMA producer: 1D bulk copies of the packed int4 tiles (both
+//               operands use the 16-row x 128-k 1 KB tile layout) into a
+//               3-stage packed ring (mbarrier complete_tx).
+//   warps 2..5  converters: packed int4 -> int8 (x16, two's complement in the
+//               high nibble, exact) written in the UMMA canonical K-major
+//               SWIZZLE_128B layout of a 2-stage int8 ring; fence.proxy.async
+//               then arrive.  Afterwards the same 4 warps are the epilogue:
+//               tcgen05.ld 32x32b from TMEM, exact >>8, fp64 scale epilogue.
+//   warp 1      TMEM allocator + single-thread MMA issuer: 4 x
+//               tcgen05.mma.cta_group::1.kind::i8 (M128 N256 K32) per k-block,
+//               tcgen05.commit releases the int8 stage / signals the epilogue.
+#include <algorithm>
+#include <cstdlib>
+
 #include "qt_common.cuh"
+#include "qt_epilogue.cuh"
 #include "qt_kernels.h"
 
-extern "C" int qt_launch_w4a4_tc05(int, const uint8_t*, int, const double*, const uint8_t*, int, const double*, int,
-                                   int, int, void*, int, int*, cudaStream_t) {
+namespace qt {
+
+constexpr int T5_BM = 128, T5_BN = 256, T5_BKB = 64;  // BK = 128 int4 = 64 packed bytes
+constexpr int T5_PS = 3, T5_IS = 2;
+constexpr int T5_PA = T5_BM * T5_BKB, T5_PB = T5_BN * T5_BKB;  // packed bytes per stage
+constexpr int T5_IA = T5_BM * 128, T5_IB = T5_BN * 128;        // int8 bytes per stage
+constexpr int T5_THREADS = 192;
+
+struct T5Smem {
+    // int8 ring first: 1024-byte aligned SW128 atoms
+    static constexpr size_t ia = 0;
+    static constexpr size_t ib = ia + (size_t)T5_IS * T5_IA;
+    static constexpr size_t pa = ib + (size_t)T5_IS * T5_IB;
+    static constexpr size_t pb = pa + (size_t)T5_PS * T5_PA;
+    static constexpr size_t bars = pb + (size_t)T5_PS * T5_PB;
+    static constexpr size_t total = bars + 256;
+};
+
+QT_DEV uint64_t umma_desc_sw128(uint32_t saddr) {
+    // SmemDescriptor (cute/arch/mma_sm100_desc.hpp): start>>4 [0,14), LBO>>4 [16,30)
+    // = 1 (ignored for swizzled K-major), SBO>>4 [32,46) = 1024>>4 (8-row atom
+    // stride), version [46,48) = 1, base_offset 0, layout [61,64) = 2 (SW128).
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)1 << 16;
+    d |= (uint64_t)(1024 >> 4) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)2 << 61;
+    return d;
+}
+
+// InstrDescriptor: c_format S32 (2) [4,6), a/b format signed int8 (1) [7,10)/[10,13),
+// K-major A/B, n_dim = N>>3 [17,23), m_dim = M>>4 [24,29).
+constexpr uint32_t t5_idesc() {
+    return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(T5_BN >> 3) << 17) | ((uint32_t)(T5_BM >> 4) << 24);
+}
+
+QT_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+QT_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+
+QT_DEV void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accum) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
+        : "memory");
+}
+
+QT_DEV void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+QT_DEV void tmem_ld32(uint32_t taddr, uint32_t* r) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+}
+
+// one packed 16-byte chunk (32 k of one row) -> two swizzled int8 16-byte chunks
+QT_DEV void convert_chunk(const uint8_t* packed, uint8_t* i8, int row, int q) {
+    const uint4 w = *reinterpret_cast<const uint4*>(packed + (size_t)row * T5_BKB + q * 16);
+    uint4 o0, o1;
+    unpack_x16(w.x, o0.x, o0.y);
+    unpack_x16(w.y, o0.z, o0.w);
+    unpack_x16(w.z, o1.x, o1.y);
+    unpack_x16(w.w, o1.z, o1.w);
+    uint8_t* atom = i8 + (size_t)(row >> 3) * 1024 + (row & 7) * 128;
+    const int c0 = 2 * q, c1 = 2 * q + 1, sw = row & 7;
+    *reinterpret_cast<uint4*>(atom + ((c0 ^ sw) << 4)) = o0;
+    *reinterpret_cast<uint4*>(atom + ((c1 ^ sw) << 4)) = o1;
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(T5_THREADS, 1) k_gemm_tc05(const uint8_t* __restrict__ A, int lda,
+                                                              const double* __restrict__ sa,
+                                                              const uint8_t* __restrict__ W, int ldw,
+                                                              const double* __restrict__ sw, int M, int N, int K,
+                                                              void* __restrict__ out, int ldo,
+                                                              int* __restrict__ acc_dbg) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint64_t* pfull = reinterpret_cast<uint64_t*>(smem + T5Smem::bars);
+    uint64_t* pempty = pfull + T5_PS;
+    uint64_t* ifull = pempty + T5_PS;
+    uint64_t* iempty = ifull + T5_IS;
+    uint64_t* tmem_full = iempty + T5_IS;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int KB = K / 128;
+    const int KT = lda / 64;  // tiles per row block (A and W share K)
+    const int m0 = blockIdx.y * T5_BM, n0 = blockIdx.x * T5_BN;
+    const int a_rb0 = m0 / 16, w_rb0 = n0 / 16;
+    const int a_rbs = min(T5_BM / 16, (M + 15) / 16 - a_rb0);   // valid A row blocks in this tile
+    const int w_rbs = min(T5_BN / 16, (N + 15) / 16 - w_rb0);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < T5_PS; ++s) {
+            mbar_init(&pfull[s], 1);
+            mbar_init(&pempty[s], 4);
+        }
+        for (int s = 0; s < T5_IS; ++s) {
+            mbar_init(&ifull[s], 4);
+            mbar_init(&iempty[s], 1);
+        }
+        mbar_init(tmem_full, 1);
+        mbar_fence_init();
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                     "n"(T5_BN));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ---------------- TMA producer (weights need no upstream data)
+        if (lane == 0) {
+            for (int kb = 0; kb < KB; ++kb) {
+                const int s = kb % T5_PS;
+                if (kb >= T5_PS) mbar_wait(&pempty[s], ((kb / T5_PS) - 1) & 1);
+                if (kb == 0) pdl_wait();  // activation codes come from the upstream kernel
+                mbar_arrive_expect_tx(&pfull[s], (uint32_t)(a_rbs + w_rbs) * 1024u);
+                uint8_t* pa = smem + T5Smem::pa + (size_t)s * T5_PA;
+                uint8_t* pb = smem + T5Smem::pb + (size_t)s * T5_PB;
+                for (int i = 0; i < a_rbs; ++i)
+                    bulk_g2s(pa + i * 1024, A + ((size_t)(a_rb0 + i) * KT + kb) * 1024, 1024u, &pfull[s]);
+                for (int i = 0; i < w_rbs; ++i)
+                    bulk_g2s(pb + i * 1024, W + ((size_t)(w_rb0 + i) * KT + kb) * 1024, 1024u, &pfull[s]);
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer
+        if (lane == 0) {
+            const uint32_t idesc = t5_idesc();
+            for (int kb = 0; kb < KB; ++kb) {
+                const int s = kb % T5_IS;
+                mbar_wait(&ifull[s], (kb / T5_IS) & 1);
+                tc_fence_after();
+                const uint32_t a0 = smem_u32(smem + T5Smem::ia + (size_t)s * T5_IA);
+                const uint32_t b0 = smem_u32(smem + T5Smem::ib + (size_t)s * T5_IB);
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    mma_i8(tmem, umma_desc_sw128(a0 + 32 * k), umma_desc_sw128(b0 + 32 * k), idesc, (kb | k) != 0);
+                mma_commit(&iempty[s]);
+            }
+            mma_commit(tmem_full);
+        }
+        __syncwarp();
+    } else {
+        // ---------------- converters (128 threads), then epilogue
+        const int ct = threadIdx.x - 64;
+        for (int kb = 0; kb < KB; ++kb) {
+            const int ps = kb % T5_PS, is = kb % T5_IS;
+            mbar_wait(&pfull[ps], (kb / T5_PS) & 1);
+            if (kb >= T5_IS) mbar_wait(&iempty[is], ((kb / T5_IS) - 1) & 1);
+            const uint8_t* pa = smem + T5Smem::pa + (size_t)ps * T5_PA;
+            const uint8_t* pb = smem + T5Smem::pb + (size_t)ps * T5_PB;
+            uint8_t* ia = smem + T5Smem::ia + (size_t)is * T5_IA;
+            uint8_t* ib = smem + T5Smem::ib + (size_t)is * T5_IB;
+            // A: 128 rows x 4 chunks, B: 256 rows x 4 chunks (rows past the valid
+            // row blocks convert stale bytes; their outputs are never stored)
+#pragma unroll
+            for (int i = 0; i < (T5_BM * 4) / 128; ++i) {
+                const int c = ct + 128 * i;
+                convert_chunk(pa, ia, c >> 2, c & 3);
+            }
+#pragma unroll
+            for (int i = 0; i < (T5_BN * 4) / 128; ++i) {
+                const int c = ct + 128 * i;
+                convert_chunk(pb, ib, c >> 2, c & 3);
+            }
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(&ifull[is]);
+                mbar_arrive(&pempty[ps]);
+            }
+        }
+        // epilogue: TMEM lanes 32*(warp%4) .. +31 are this warp's rows
+        pdl_wait();  // scales / residual come from upstream kernels
+        pdl_launch_dependents();
+        mbar_wait(tmem_full, 0);
+        tc_fence_after();
+        const int q = warp & 3;
+        const int m = m0 + q * 32 + lane;
+        const double a_s = m < M ? sa[m] : 0.0;
+        for (int j = 0; j < T5_BN / 32; ++j) {
+            uint32_t r[32];
+            tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(j * 32), r);
+            if (m >= M) continue;
+#pragma unroll
+            for (int e = 0; e < 32; e += 2) {
+                const int n = n0 + j * 32 + e;
+                if (n >= N) break;
+                const int c0 = (int)r[e] >> 8, c1 = (int)r[e + 1] >> 8;
+                if (acc_dbg) {
+                    acc_dbg[(size_t)m * N + n] = c0;
+                    if (n + 1 < N) acc_dbg[(size_t)m * N + n + 1] = c1;
+                }
+                epi_store<EPI>(out, ldo, m, n, (double)c0 * (a_s * sw[n]), (double)c1 * (a_s * sw[n + 1]), N);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(T5_BN));
+    }
+}
+
+}  // namespace qt
+
+extern "C" int qt_launch_w4a4_tc05(int epi, const uint8_t* A, int lda, const double* sa, const uint8_t* W, int ldw,
+                                   const double* sw, int M, int N, int K, void* out, int ldo, int* acc_dbg,
+                                   cudaStream_t st) {
+    using namespace qt;
+    if (M <= 0) return 0;
+    if (K % 128 || lda != K / 2 || ldw != K / 2) return -1;
+    const dim3 grid((N + T5_BN - 1) / T5_BN, (M + T5_BM - 1) / T5_BM);
+    const size_t smem = T5Smem::total;
+#define QT_T5(E)                                                                                                \
+    do {                                                                                                        \
+        auto kfn = k_gemm_tc05<E>;                                                                              \
+        cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                      \
+        return launch_pdl(kfn, grid, dim3(T5_THREADS), smem, st, A, lda, sa, W, ldw, sw, M, N, K, out, ldo, acc_dbg); \
+    } while (0)
+    switch (epi) {
+        case QT_EPI_STORE: QT_T5(QT_EPI_STORE);
+        case QT_EPI_RESADD: QT_T5(QT_EPI_RESADD);
+        case QT_EPI_SILU: QT_T5(QT_EPI_SILU);
+        case QT_EPI_SWIGLU: QT_T5(QT_EPI_SWIGLU);
+    }
+#undef QT_T5
     return -1;
 }

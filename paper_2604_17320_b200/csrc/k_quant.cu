@@ -99,7 +99,6 @@ __global__ void __launch_bounds__(1024) k_norm_quant(const TX* __restrict__ x, i
         s = q_scale(mx, qmax);
     }
     const double inv_s = 1.0 / s;
-    uint32_t* cw = reinterpret_cast<uint32_t*>(codes + (size_t)row * ld_codes);
 #pragma unroll
     for (int j = 0; j < G; ++j) {
         const int w = threadIdx.x + j * blockDim.x;
@@ -107,7 +106,7 @@ __global__ void __launch_bounds__(1024) k_norm_quant(const TX* __restrict__ x, i
         int c[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) c[e] = w * 8 + e < D ? q_code_r(v[j][e], s, inv_s, qmax) : 0;
-        cw[w] = pack8(c);
+        *reinterpret_cast<uint32_t*>(codes + w4t_offset(row, w * 4, ld_codes)) = pack8(c);  // tiled layout
         if (normed && w * 8 < D) {
 #pragma unroll
             for (int e = 0; e < 8; ++e) normed[(size_t)row * D + w * 8 + e] = (float)v[j][e];

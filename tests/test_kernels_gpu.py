@@ -63,7 +63,7 @@ def test_rmsnorm_quant_codes_bit_exact(torch_cuda, M, D, mode):
         s_static = 0.0
     codes, scales = Q.rmsnorm_quant(xd.double() if M % 2 else xd, gd, d_pad, mode, s_static)
     torch.cuda.synchronize()
-    got = Q.unpack_i4(codes.cpu().numpy(), d_pad)
+    got = Q.unpack_i4(Q.untile_w4(codes.cpu().numpy(), codes.shape[0], d_pad // 2), d_pad)[:M]
     assert np.array_equal(got[:, :D], exp_codes)
     assert np.all(got[:, D:] == 0)
     # the RMS sum is a parallel fp64 reduction: scales agree to a few ulp
@@ -76,7 +76,7 @@ def test_norm_free_site_quant(torch_cuda):
     x = _x(9, 1024, seed=5)
     codes, scales = Q.rmsnorm_quant(torch.from_numpy(x).cuda(), None, 1024, 1)
     exp_codes, exp_scales = ref_quant_fit(x.astype(np.float64), 1)
-    assert np.array_equal(Q.unpack_i4(codes.cpu().numpy(), 1024), exp_codes)
+    assert np.array_equal(Q.unpack_i4(Q.untile_w4(codes.cpu().numpy(), codes.shape[0], 512), 1024)[:9], exp_codes)
     assert np.array_equal(scales.cpu().numpy(), exp_scales)
 
 
@@ -100,18 +100,28 @@ def _pack(c):
     return (c[..., 0::2] | (c[..., 1::2] << 4)).astype(np.uint8)
 
 
-@pytest.mark.parametrize("M", [1, 3, 8, 13, 16, 40, 128, 300])
-@pytest.mark.parametrize("impl", [0])
+def _tiled(c):
+    """int4 codes [rows x K] -> packed + tiled (rows zero-padded to 16), the engine's code layout."""
+    p = _pack(c)
+    rows = (p.shape[0] + 15) // 16 * 16
+    out = np.zeros((rows, p.shape[1]), dtype=np.uint8)
+    out[:p.shape[0]] = p
+    return Q.tile_w4(out)
+
+
+@pytest.mark.parametrize("M,impl", [(1, 0), (3, 0), (8, 0), (13, 0), (16, 0), (40, 0), (128, 0), (300, 0),
+                                    (40, 1), (128, 1), (300, 1), (1000, 1)])
 def test_w4a4_gemm_int32_exact(torch_cuda, M, impl):
+    """impl 0: mma.sync GEMM/GEMV; impl 1: tcgen05 kind::i8 GEMM (TMEM accumulators)."""
     torch = torch_cuda
     rng = np.random.default_rng(M)
-    K, N = 512, 384
+    K, N = (512, 384) if impl == 0 else (1024, 640)
     a = rng.integers(-7, 8, size=(M, K))
     w = rng.integers(-7, 8, size=(N, K))
     sa = rng.uniform(0.01, 0.5, M)
     sw = rng.uniform(0.001, 0.01, N)
-    ad = torch.from_numpy(_pack(a)).cuda()
-    wd = torch.from_numpy(Q.tile_w4(_pack(w))).cuda()
+    ad = torch.from_numpy(_tiled(a)).cuda()
+    wd = torch.from_numpy(_tiled(w)).cuda()
     sad, swd = torch.from_numpy(sa).cuda(), torch.from_numpy(sw).cuda()
     out = torch.zeros((M, N), dtype=torch.float32, device="cuda")
     acc = torch.zeros((M, N), dtype=torch.int32, device="cuda")
@@ -148,7 +158,7 @@ def test_w4a4_gemm_epilogues(torch_cuda, M, epi):
         out = torch.zeros((M, N), dtype=torch.float32, device="cuda")
         exp = y / (1 + np.exp(-y))
         tol = dict(rtol=1e-6, atol=1e-7)
-    Q.w4a4_gemm(epi, torch.from_numpy(_pack(a)).cuda(), torch.from_numpy(sa).cuda(), torch.from_numpy(Q.tile_w4(_pack(w))).cuda(),
+    Q.w4a4_gemm(epi, torch.from_numpy(_tiled(a)).cuda(), torch.from_numpy(sa).cuda(), torch.from_numpy(_tiled(w)).cuda(),
                 torch.from_numpy(sw).cuda(), M, N, K, out)
     torch.cuda.synchronize()
     np.testing.assert_allclose(out.cpu().numpy(), exp, **tol)
