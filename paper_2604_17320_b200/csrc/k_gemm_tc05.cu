@@ -6,18 +6,22 @@
 // replaces matmul(fake_quant(x), W.deq) (numeric.cpp:33-46 at
 // model.cpp:351-353,395,432,436,445) for the prefill token batch.
 //
-// Pipeline per CTA (one 128 x 256 output tile, K in 128-wide blocks):
+// Persistent CTAs (one per SM) walk 128 x 256 output tiles (m-tile fastest,
+// so concurrent CTAs share weight tiles in L2), K in 128-wide blocks:
 //   warp 0      TMA producer: 1D bulk copies of the packed int4 tiles (both
 //               operands use the 16-row x 128-k 1 KB tile layout) into a
-//               3-stage packed ring (mbarrier complete_tx).
+//               5-stage packed ring (mbarrier complete_tx).
 //   warps 2..5  converters: packed int4 -> int8 (x16, two's complement in the
 //               high nibble, exact) written in the UMMA canonical K-major
 //               SWIZZLE_128B layout of a 2-stage int8 ring; fence.proxy.async
-//               then arrive.  Afterwards the same 4 warps are the epilogue:
-//               tcgen05.ld 32x32b from TMEM, exact >>8, fp64 scale epilogue.
+//               then arrive.
 //   warp 1      TMEM allocator + single-thread MMA issuer: 4 x
-//               tcgen05.mma.cta_group::1.kind::i8 (M128 N256 K32) per k-block,
-//               tcgen05.commit releases the int8 stage / signals the epilogue.
+//               tcgen05.mma.cta_group::1.kind::i8 (M128 N256 K32) per k-block
+//               into one of two 256-column TMEM accumulators; tcgen05.commit
+//               releases the int8 stage / hands the accumulator to the epilogue.
+//   warps 6..9  epilogue: tcgen05.ld 32x32b, exact >>8, fp64 scales, fused
+//               store / residual add / SiLU / SwiGLU -- overlapping the next
+//               tile's main loop (double-buffered accumulators).
 #include <algorithm>
 #include <cstdlib>
 
@@ -28,10 +32,10 @@
 namespace qt {
 
 constexpr int T5_BM = 128, T5_BN = 256, T5_BKB = 64;  // BK = 128 int4 = 64 packed bytes
-constexpr int T5_PS = 3, T5_IS = 2;
+constexpr int T5_PS = 5, T5_IS = 2, T5_ACC = 2;       // packed stages, int8 stages, TMEM accumulators
 constexpr int T5_PA = T5_BM * T5_BKB, T5_PB = T5_BN * T5_BKB;  // packed bytes per stage
 constexpr int T5_IA = T5_BM * 128, T5_IB = T5_BN * 128;        // int8 bytes per stage
-constexpr int T5_THREADS = 192;
+constexpr int T5_THREADS = 320;  // 0 TMA, 1 MMA, 2-5 converters, 6-9 epilogue
 
 struct T5Smem {
     // int8 ring first: 1024-byte aligned SW128 atoms
@@ -39,7 +43,8 @@ struct T5Smem {
     static constexpr size_t ib = ia + (size_t)T5_IS * T5_IA;
     static constexpr size_t pa = ib + (size_t)T5_IS * T5_IB;
     static constexpr size_t pb = pa + (size_t)T5_PS * T5_PA;
-    static constexpr size_t bars = pb + (size_t)T5_PS * T5_PB;
+    static constexpr size_t swb = pb + (size_t)T5_PS * T5_PB;   // per-accumulator weight scales [2][256] f64
+    static constexpr size_t bars = swb + (size_t)T5_ACC * T5_BN * 8;
     static constexpr size_t total = bars + 256;
 };
 
@@ -120,15 +125,16 @@ __global__ void __launch_bounds__(T5_THREADS, 1) k_gemm_tc05(const uint8_t* __re
     uint64_t* pempty = pfull + T5_PS;
     uint64_t* ifull = pempty + T5_PS;
     uint64_t* iempty = ifull + T5_IS;
-    uint64_t* tmem_full = iempty + T5_IS;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+    uint64_t* tfull = iempty + T5_IS;
+    uint64_t* tempty = tfull + T5_ACC;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + T5_ACC);
+    double* sws = reinterpret_cast<double*>(smem + T5Smem::swb);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int KB = K / 128;
-    const int KT = lda / 64;  // tiles per row block (A and W share K)
-    const int m0 = blockIdx.y * T5_BM, n0 = blockIdx.x * T5_BN;
-    const int a_rb0 = m0 / 16, w_rb0 = n0 / 16;
-    const int a_rbs = min(T5_BM / 16, (M + 15) / 16 - a_rb0);   // valid A row blocks in this tile
-    const int w_rbs = min(T5_BN / 16, (N + 15) / 16 - w_rb0);
+    const int KT = lda / 64;  // 1 KB tiles per row block (A and W share K)
+    const int mt_n = (M + T5_BM - 1) / T5_BM, nt_n = (N + T5_BN - 1) / T5_BN;
+    const int tiles = mt_n * nt_n;
+    const int a_rbs_total = (M + 15) / 16, w_rbs_total = (N + 15) / 16;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < T5_PS; ++s) {
@@ -139,12 +145,15 @@ __global__ void __launch_bounds__(T5_THREADS, 1) k_gemm_tc05(const uint8_t* __re
             mbar_init(&ifull[s], 4);
             mbar_init(&iempty[s], 1);
         }
-        mbar_init(tmem_full, 1);
+        for (int s = 0; s < T5_ACC; ++s) {
+            mbar_init(&tfull[s], 1);
+            mbar_init(&tempty[s], 4);
+        }
         mbar_fence_init();
     }
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
-                     "n"(T5_BN));
+                     "n"(T5_ACC * T5_BN));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
     }
     tc_fence_before();
@@ -152,99 +161,137 @@ __global__ void __launch_bounds__(T5_THREADS, 1) k_gemm_tc05(const uint8_t* __re
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
+    // tile t -> (m tile fastest): CTAs running concurrently share weight tiles in L2
     if (warp == 0) {
-        // ---------------- TMA producer (weights need no upstream data)
+        // ---------------- TMA producer
         if (lane == 0) {
-            for (int kb = 0; kb < KB; ++kb) {
-                const int s = kb % T5_PS;
-                if (kb >= T5_PS) mbar_wait(&pempty[s], ((kb / T5_PS) - 1) & 1);
-                if (kb == 0) pdl_wait();  // activation codes come from the upstream kernel
-                mbar_arrive_expect_tx(&pfull[s], (uint32_t)(a_rbs + w_rbs) * 1024u);
-                uint8_t* pa = smem + T5Smem::pa + (size_t)s * T5_PA;
-                uint8_t* pb = smem + T5Smem::pb + (size_t)s * T5_PB;
-                for (int i = 0; i < a_rbs; ++i)
-                    bulk_g2s(pa + i * 1024, A + ((size_t)(a_rb0 + i) * KT + kb) * 1024, 1024u, &pfull[s]);
-                for (int i = 0; i < w_rbs; ++i)
-                    bulk_g2s(pb + i * 1024, W + ((size_t)(w_rb0 + i) * KT + kb) * 1024, 1024u, &pfull[s]);
+            pdl_wait();  // activation codes come from the upstream kernel
+            int it = 0;
+            for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+                const int a_rb0 = (t % mt_n) * (T5_BM / 16), w_rb0 = (t / mt_n) * (T5_BN / 16);
+                const int a_rbs = min(T5_BM / 16, a_rbs_total - a_rb0), w_rbs = min(T5_BN / 16, w_rbs_total - w_rb0);
+                for (int kb = 0; kb < KB; ++kb, ++it) {
+                    const int s = it % T5_PS;
+                    if (it >= T5_PS) mbar_wait(&pempty[s], ((it / T5_PS) - 1) & 1);
+                    mbar_arrive_expect_tx(&pfull[s], (uint32_t)(a_rbs + w_rbs) * 1024u);
+                    uint8_t* pa = smem + T5Smem::pa + (size_t)s * T5_PA;
+                    uint8_t* pb = smem + T5Smem::pb + (size_t)s * T5_PB;
+                    for (int i = 0; i < a_rbs; ++i)
+                        bulk_g2s(pa + i * 1024, A + ((size_t)(a_rb0 + i) * KT + kb) * 1024, 1024u, &pfull[s]);
+                    for (int i = 0; i < w_rbs; ++i)
+                        bulk_g2s(pb + i * 1024, W + ((size_t)(w_rb0 + i) * KT + kb) * 1024, 1024u, &pfull[s]);
+                }
             }
         }
     } else if (warp == 1) {
-        // ---------------- MMA issuer
+        // ---------------- MMA issuer (one thread)
         if (lane == 0) {
             const uint32_t idesc = t5_idesc();
-            for (int kb = 0; kb < KB; ++kb) {
-                const int s = kb % T5_IS;
-                mbar_wait(&ifull[s], (kb / T5_IS) & 1);
+            int it = 0, tl = 0;
+            for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++tl) {
+                const int acc = tl % T5_ACC;
+                if (tl >= T5_ACC) mbar_wait(&tempty[acc], ((tl / T5_ACC) - 1) & 1);
                 tc_fence_after();
-                const uint32_t a0 = smem_u32(smem + T5Smem::ia + (size_t)s * T5_IA);
-                const uint32_t b0 = smem_u32(smem + T5Smem::ib + (size_t)s * T5_IB);
+                const uint32_t tacc = tmem + (uint32_t)(acc * T5_BN);
+                for (int kb = 0; kb < KB; ++kb, ++it) {
+                    const int s = it % T5_IS;
+                    mbar_wait(&ifull[s], (it / T5_IS) & 1);
+                    tc_fence_after();
+                    const uint32_t a0 = smem_u32(smem + T5Smem::ia + (size_t)s * T5_IA);
+                    const uint32_t b0 = smem_u32(smem + T5Smem::ib + (size_t)s * T5_IB);
 #pragma unroll
-                for (int k = 0; k < 4; ++k)
-                    mma_i8(tmem, umma_desc_sw128(a0 + 32 * k), umma_desc_sw128(b0 + 32 * k), idesc, (kb | k) != 0);
-                mma_commit(&iempty[s]);
+                    for (int k = 0; k < 4; ++k)
+                        mma_i8(tacc, umma_desc_sw128(a0 + 32 * k), umma_desc_sw128(b0 + 32 * k), idesc, (kb | k) != 0);
+                    mma_commit(&iempty[s]);
+                }
+                mma_commit(&tfull[acc]);
             }
-            mma_commit(tmem_full);
         }
         __syncwarp();
-    } else {
-        // ---------------- converters (128 threads), then epilogue
+    } else if (warp < 6) {
+        // ---------------- converters: packed int4 -> swizzled int8 (128 threads)
         const int ct = threadIdx.x - 64;
-        for (int kb = 0; kb < KB; ++kb) {
-            const int ps = kb % T5_PS, is = kb % T5_IS;
-            mbar_wait(&pfull[ps], (kb / T5_PS) & 1);
-            if (kb >= T5_IS) mbar_wait(&iempty[is], ((kb / T5_IS) - 1) & 1);
-            const uint8_t* pa = smem + T5Smem::pa + (size_t)ps * T5_PA;
-            const uint8_t* pb = smem + T5Smem::pb + (size_t)ps * T5_PB;
-            uint8_t* ia = smem + T5Smem::ia + (size_t)is * T5_IA;
-            uint8_t* ib = smem + T5Smem::ib + (size_t)is * T5_IB;
-            // A: 128 rows x 4 chunks, B: 256 rows x 4 chunks (rows past the valid
-            // row blocks convert stale bytes; their outputs are never stored)
+        int it = 0;
+        for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+            for (int kb = 0; kb < KB; ++kb, ++it) {
+                const int ps = it % T5_PS, is = it % T5_IS;
+                mbar_wait(&pfull[ps], (it / T5_PS) & 1);
+                if (it >= T5_IS) mbar_wait(&iempty[is], ((it / T5_IS) - 1) & 1);
+                const uint8_t* pa = smem + T5Smem::pa + (size_t)ps * T5_PA;
+                const uint8_t* pb = smem + T5Smem::pb + (size_t)ps * T5_PB;
+                uint8_t* ia = smem + T5Smem::ia + (size_t)is * T5_IA;
+                uint8_t* ib = smem + T5Smem::ib + (size_t)is * T5_IB;
+                // rows past the valid row blocks convert stale bytes; never stored
 #pragma unroll
-            for (int i = 0; i < (T5_BM * 4) / 128; ++i) {
-                const int c = ct + 128 * i;
-                convert_chunk(pa, ia, c >> 2, c & 3);
-            }
+                for (int i = 0; i < (T5_BM * 4) / 128; ++i) {
+                    const int c = ct + 128 * i;
+                    convert_chunk(pa, ia, c >> 2, c & 3);
+                }
 #pragma unroll
-            for (int i = 0; i < (T5_BN * 4) / 128; ++i) {
-                const int c = ct + 128 * i;
-                convert_chunk(pb, ib, c >> 2, c & 3);
-            }
-            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-            __syncwarp();
-            if (lane == 0) {
-                mbar_arrive(&ifull[is]);
-                mbar_arrive(&pempty[ps]);
+                for (int i = 0; i < (T5_BN * 4) / 128; ++i) {
+                    const int c = ct + 128 * i;
+                    convert_chunk(pb, ib, c >> 2, c & 3);
+                }
+                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive(&ifull[is]);
+                    mbar_arrive(&pempty[ps]);
+                }
             }
         }
-        // epilogue: TMEM lanes 32*(warp%4) .. +31 are this warp's rows
+    } else {
+        // ---------------- epilogue warpgroup (warps 6..9 -> TMEM lane quarters 2,3,0,1)
         pdl_wait();  // scales / residual come from upstream kernels
         pdl_launch_dependents();
-        mbar_wait(tmem_full, 0);
-        tc_fence_after();
         const int q = warp & 3;
-        const int m = m0 + q * 32 + lane;
-        const double a_s = m < M ? sa[m] : 0.0;
-        for (int j = 0; j < T5_BN / 32; ++j) {
-            uint32_t r[32];
-            tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(j * 32), r);
-            if (m >= M) continue;
-#pragma unroll
-            for (int e = 0; e < 32; e += 2) {
-                const int n = n0 + j * 32 + e;
-                if (n >= N) break;
-                const int c0 = (int)r[e] >> 8, c1 = (int)r[e + 1] >> 8;
-                if (acc_dbg) {
-                    acc_dbg[(size_t)m * N + n] = c0;
-                    if (n + 1 < N) acc_dbg[(size_t)m * N + n + 1] = c1;
+        const int et = threadIdx.x - 192;
+        int tl = 0;
+        for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++tl) {
+            const int acc = tl % T5_ACC;
+            const int m0 = (t % mt_n) * T5_BM, n0 = (t / mt_n) * T5_BN;
+            double* swt = sws + acc * T5_BN;
+            for (int i = et; i < T5_BN; i += 128) swt[i] = n0 + i < N ? sw[n0 + i] : 0.0;
+            asm volatile("bar.sync 2, 128;\n" ::: "memory");
+            mbar_wait(&tfull[acc], (tl / T5_ACC) & 1);
+            tc_fence_after();
+            const int m = m0 + q * 32 + lane;
+            const double a_s = m < M ? sa[m] : 0.0;
+            const uint32_t tacc = tmem + (uint32_t)(acc * T5_BN) + ((uint32_t)(q * 32) << 16);
+#pragma unroll 1
+            for (int j = 0; j < T5_BN / 32; ++j) {
+                uint32_t r[32];
+                tmem_ld32(tacc + (uint32_t)(j * 32), r);
+                if (j == T5_BN / 32 - 1) {
+                    // accumulator fully read: hand it back to the MMA issuer
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&tempty[acc]);
                 }
-                epi_store<EPI>(out, ldo, m, n, (double)c0 * (a_s * sw[n]), (double)c1 * (a_s * sw[n + 1]), N);
+                const int nb = n0 + j * 32;
+                if (m >= M || nb >= N) continue;
+                if (acc_dbg) {
+#pragma unroll
+                    for (int e = 0; e < 32; ++e)
+                        if (nb + e < N) acc_dbg[(size_t)m * N + nb + e] = (int)r[e] >> 8;
+                }
+                if (nb + 32 <= N) {
+                    epi_row32<EPI>(out, ldo, m, nb, r, a_s, swt + j * 32);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 32; e += 2)
+                        if (nb + e < N)
+                            epi_store<EPI>(out, ldo, m, nb + e, (double)((int)r[e] >> 8) * (a_s * swt[j * 32 + e]),
+                                           (double)((int)r[e + 1] >> 8) * (a_s * swt[j * 32 + e + 1]), N);
+                }
             }
+            asm volatile("bar.sync 2, 128;\n" ::: "memory");  // swt reuse
         }
     }
     tc_fence_before();
     __syncthreads();
     if (warp == 1) {
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(T5_BN));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(T5_ACC * T5_BN));
     }
 }
 
@@ -256,7 +303,10 @@ extern "C" int qt_launch_w4a4_tc05(int epi, const uint8_t* A, int lda, const dou
     using namespace qt;
     if (M <= 0) return 0;
     if (K % 128 || lda != K / 2 || ldw != K / 2) return -1;
-    const dim3 grid((N + T5_BN - 1) / T5_BN, (M + T5_BM - 1) / T5_BM);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const int tiles = ((N + T5_BN - 1) / T5_BN) * ((M + T5_BM - 1) / T5_BM);
+    const dim3 grid(std::min(tiles, sms));
     const size_t smem = T5Smem::total;
 #define QT_T5(E)                                                                                                \
     do {                                                                                                        \

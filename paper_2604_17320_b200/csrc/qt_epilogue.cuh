@@ -42,4 +42,54 @@ QT_DEV void epi_store(void* __restrict__ outv, int ldo, int m, int n, double y0,
     else if (n < N) p[0] = v0;
 }
 
+// 32 consecutive columns of one row (tcgen05.ld 32x32b: one row per thread).
+template <int EPI>
+QT_DEV void epi_row32(void* __restrict__ outv, int ldo, int m, int n, const uint32_t* r, double a_s,
+                      const double* swt) {
+    if (EPI == QT_EPI_RESADD) {
+        double2* p = reinterpret_cast<double2*>(static_cast<double*>(outv) + (size_t)m * ldo + n);
+#pragma unroll
+        for (int e = 0; e < 32; e += 8) {
+            double2 v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = p[e / 2 + u];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                v[u].x += (double)((int)r[e + 2 * u] >> 8) * (a_s * swt[e + 2 * u]);
+                v[u].y += (double)((int)r[e + 2 * u + 1] >> 8) * (a_s * swt[e + 2 * u + 1]);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) p[e / 2 + u] = v[u];
+        }
+        return;
+    }
+    float* out = static_cast<float*>(outv);
+    if (EPI == QT_EPI_SWIGLU) {
+        float4* p = reinterpret_cast<float4*>(out + (size_t)m * ldo + n / 2);
+#pragma unroll
+        for (int e = 0; e < 32; e += 8) {
+            float v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const double g = (double)((int)r[e + 2 * u] >> 8) * (a_s * swt[e + 2 * u]);
+                const double up = (double)((int)r[e + 2 * u + 1] >> 8) * (a_s * swt[e + 2 * u + 1]);
+                v[u] = (float)(g / (1.0 + exp(-g)) * up);
+            }
+            p[e / 8] = make_float4(v[0], v[1], v[2], v[3]);
+        }
+        return;
+    }
+    float4* p = reinterpret_cast<float4*>(out + (size_t)m * ldo + n);
+#pragma unroll
+    for (int e = 0; e < 32; e += 4) {
+        float v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const double y = (double)((int)r[e + u] >> 8) * (a_s * swt[e + u]);
+            v[u] = EPI == QT_EPI_SILU ? (float)(y / (1.0 + exp(-y))) : (float)y;
+        }
+        p[e / 4] = make_float4(v[0], v[1], v[2], v[3]);
+    }
+}
+
 }  // namespace qt
