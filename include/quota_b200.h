@@ -116,7 +116,11 @@ int qt_engine_info(qt_engine* e, int64_t* out16);
 int qt_engine_profile_next(qt_engine* e);
 int qt_engine_profile_read(qt_engine* e, double* out24);
 
-/* ---- per-kernel ABI (caller-owned device buffers, explicit stream) ---- */
+/* ---- per-kernel ABI (caller-owned device buffers, explicit stream) ----
+ * int4 code matrices (weights and activations) use the tiled layout of
+ * csrc/qt_common.cuh: 1 KB tiles of 16 rows x 128 k, k-block-major; a tiled
+ * matrix is described by its padded row count (ld_codes / lda / ldw / ldc
+ * below = rows_pad, a multiple of 16) and K. */
 /* K1: RMSNorm (gain != null) + int4 activation quantizer; x fp32 or fp64
  * (x_is_f64); act_mode 0 = static_scale, 1 = per-row max|x|/7; fp64 scales. */
 int qt_rmsnorm_quant_i4(const void* x, int x_is_f64, int ld_x, const float* gain, int M, int D, int d_pad,

@@ -299,13 +299,13 @@ def rmsnorm_quant(x, gain, d_pad, act_mode, static_scale=0.0, codes=None, scales
         scales = torch.zeros(M, dtype=torch.float64, device=x.device)
     is64 = int(x.dtype == torch.float64)
     check(lib().qt_rmsnorm_quant_i4(_ptr(x), is64, x.stride(0), _ptr(gain), M, D, d_pad, act_mode,
-                                    float(static_scale), _ptr(codes), codes.stride(0), _ptr(scales), _ptr(normed),
+                                    float(static_scale), _ptr(codes), codes.shape[0], _ptr(scales), _ptr(normed),
                                     C.c_void_p(stream)))
     return codes, scales
 
 
 def w4a4_gemm(epi, a_codes, a_scales, w_codes, w_scales, M, N, K, out, acc_out=None, impl=0, stream=0):
-    check(lib().qt_w4a4_gemm(epi, _ptr(a_codes), a_codes.stride(0), _ptr(a_scales), _ptr(w_codes), w_codes.stride(0),
+    check(lib().qt_w4a4_gemm(epi, _ptr(a_codes), a_codes.shape[0], _ptr(a_scales), _ptr(w_codes), w_codes.shape[0],
                              _ptr(w_scales), M, N, K, _ptr(out), out.stride(0), _ptr(acc_out), impl,
                              C.c_void_p(stream)))
     return out
@@ -319,7 +319,7 @@ def quant_weight(w, k_pad, n_pad, row_mul=1, row_add=0, codes=None, scales=None,
     if scales is None:
         scales = torch.zeros(n_pad, dtype=torch.float64, device=w.device)
     scratch = torch.zeros(max(N, 64), dtype=torch.float64, device=w.device)
-    check(lib().qt_quant_weight_i4(_ptr(w), K, N, row_mul, row_add, _ptr(codes), codes.stride(0), _ptr(scales),
+    check(lib().qt_quant_weight_i4(_ptr(w), K, N, row_mul, row_add, _ptr(codes), codes.shape[0], _ptr(scales),
                                    _ptr(scratch), C.c_void_p(stream)))
     return codes, scales
 
@@ -350,14 +350,14 @@ def exported_symbols():
 
 
 def tile_w4(rows_u8):
-    """Row-major packed int4 [N_pad x K_pad/2] -> the engine's tiled layout (flat uint8):
-    1 KB tiles of 16 rows x 64 bytes, tile (rt, kt) at (rt * KT + kt) * 1024 (qt_common.cuh)."""
+    """Row-major packed int4 [rows_pad x K_pad/2] -> the engine's tiled layout (same shape):
+    1 KB tiles of 16 rows x 64 bytes, k-block-major: tile (rt, kt) at (kt * rows_pad/16 + rt) * 1024."""
     a = np.ascontiguousarray(rows_u8, dtype=np.uint8)
     n, rb = a.shape
     assert n % 16 == 0 and rb % 64 == 0
-    return a.reshape(n // 16, 16, rb // 64, 64).transpose(0, 2, 1, 3).reshape(n, rb).copy()
+    return a.reshape(n // 16, 16, rb // 64, 64).transpose(2, 0, 1, 3).reshape(n, rb).copy()
 
 
 def untile_w4(tiled_u8, n, row_bytes):
-    a = np.ascontiguousarray(tiled_u8, dtype=np.uint8).reshape(n // 16, row_bytes // 64, 16, 64)
-    return a.transpose(0, 2, 1, 3).reshape(n, row_bytes).copy()
+    a = np.ascontiguousarray(tiled_u8, dtype=np.uint8).reshape(row_bytes // 64, n // 16, 16, 64)
+    return a.transpose(1, 2, 0, 3).reshape(n, row_bytes).copy()

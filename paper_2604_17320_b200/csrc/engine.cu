@@ -189,6 +189,7 @@ struct qt_engine {
     float* attn = nullptr;
     float* mid = nullptr;
     uint8_t* codes = nullptr;
+    int codes_rows = 0;  // padded rows of the tiled activation-code buffer
     double* ascale = nullptr;
     float* logits = nullptr;
     float* ml = nullptr;
@@ -353,7 +354,8 @@ struct qt_engine {
         qkv = dalloc<float>(T * n_qkv);
         attn = dalloc<float>(T * d);
         mid = dalloc<float>(T * dff);
-        codes = dalloc<uint8_t>((size_t)round_up((int)T, 16) * std::max(kd_pad, kff_pad) / 2);  // tiled rows
+        codes_rows = round_up(std::max((int)T, mb), 16);
+        codes = dalloc<uint8_t>((size_t)codes_rows * std::max(kd_pad, kff_pad) / 2);  // tiled rows
         ascale = dalloc<double>(T);
         logits = dalloc<float>(T * d);
         ml = dalloc<float>(T * H * 2);
@@ -427,9 +429,9 @@ struct qt_engine {
     }
 
     void quant_into(const float* w, int K, int N, int on_device, int row_mul, int row_add, uint8_t* codes_dst,
-                    int ldc, double* scales_dst) {
+                    int rows_pad, double* scales_dst) {
         const float* dw = to_device_f32(w, (size_t)K * N, on_device, nullptr);
-        ckl(qt_launch_weight_quant(dw, K, N, 4, row_mul, row_add, codes_dst, ldc, scales_dst, wscratch, st),
+        ckl(qt_launch_weight_quant(dw, K, N, 4, row_mul, row_add, codes_dst, rows_pad, scales_dst, wscratch, st),
             "weight quantize");
         ck(cudaStreamSynchronize(st), "weight quantize");
     }
@@ -449,15 +451,16 @@ struct qt_engine {
         const int mode = cfg.act_mode;
         const double s = mode == 0 ? act[site_idx] : 0.0;
         pb(P_QUANT);
-        ckl(qt_launch_norm_quant(xin, is_f64, ldx, gain, M, D, dpad, 4, mode, s, codes, dpad / 2, ascale, nullptr, st),
+        ckl(qt_launch_norm_quant(xin, is_f64, ldx, gain, M, D, dpad, 4, mode, s, codes, codes_rows, ascale, nullptr, st),
             "rmsnorm+quant");
         pe((double)M * D * (is_f64 ? 8 : 4) + (double)M * dpad / 2 + 8.0 * M);
     }
-    void gemm(int epi, const uint8_t* w, const double* sw, int M, int N, int K, void* out, int ldo) {
+    // w: tiled int4 weights with wrows padded rows; activation codes: tiled with codes_rows rows
+    void gemm(int epi, const uint8_t* w, int wrows, const double* sw, int M, int N, int K, void* out, int ldo) {
         pb(P_GEMM);
         int rc = (use_tc05 && M > 16)
-                     ? qt_launch_w4a4_tc05(epi, codes, K / 2, ascale, w, K / 2, sw, M, N, K, out, ldo, nullptr, st)
-                     : qt_launch_w4a4_mma(epi, codes, K / 2, ascale, w, K / 2, sw, M, N, K, out, ldo, nullptr, st);
+                     ? qt_launch_w4a4_tc05(epi, codes, codes_rows, ascale, w, wrows, sw, M, N, K, out, ldo, nullptr, st)
+                     : qt_launch_w4a4_mma(epi, codes, codes_rows, ascale, w, wrows, sw, M, N, K, out, ldo, nullptr, st);
         ckl(rc, "w4a4 gemm");
         const double out_bytes = epi == QT_EPI_RESADD ? 16.0 * M * N : (epi == QT_EPI_SWIGLU ? 2.0 * M * N : 4.0 * M * N);
         pe((double)N * K / 2 + 8.0 * N + (double)M * K / 2 + 8.0 * M + out_bytes, 2.0 * M * N * K);
@@ -596,7 +599,7 @@ struct qt_engine {
             int* ptl = pt + (size_t)l * max_batch * max_pages;
             // attention block (model.cpp:347-396)
             norm_quant(xc, 1, d, w.g1, M, d, kd_pad, 4 * l + 0);
-            gemm(QT_EPI_STORE, w.qkv, w.s_qkv, M, n_qkv, kd_pad, qkv, n_qkv);
+            gemm(QT_EPI_STORE, w.qkv, n_qkv_pad, w.s_qkv, M, n_qkv, kd_pad, qkv, n_qkv);
             pb(P_KV);
             ckl(qt_launch_rope_kv_append(qkv, n_qkv, M, H, Hkv, dh, pc, tok_seq, tok_row, rope, ptl, max_pages, pool,
                                          page_bytes, 4, nullptr, st),
@@ -623,7 +626,7 @@ struct qt_engine {
                 pe((double)M * (n_qkv * 4.0 + d * 4.0), 4.0 * pairs * dh * H);
             }
             norm_quant(attn, 0, d, nullptr, M, d, kd_pad, 4 * l + 1);
-            gemm(QT_EPI_RESADD, w.o, w.s_o, M, d, kd_pad, xc, d);
+            gemm(QT_EPI_RESADD, w.o, nd_pad, w.s_o, M, d, kd_pad, xc, d);
             for (int b = 0; b < B; ++b) h_kvlen[(size_t)l * B + b] = cur_v[b] + h_txt[b];
 
             // recipe hook at candidate layers (selector.cpp:214-227, model.cpp:404-427)
@@ -673,14 +676,14 @@ struct qt_engine {
             }
             // MLP block (model.cpp:429-437)
             norm_quant(xc, 1, d, w.g2, M, d, kd_pad, 4 * l + 2);
-            if (cfg.mlp == 1) gemm(QT_EPI_SWIGLU, w.gu, w.s_gu, M, n_gu, kd_pad, mid, dff);
-            else gemm(QT_EPI_SILU, w.gu, w.s_gu, M, n_gu, kd_pad, mid, dff);
+            if (cfg.mlp == 1) gemm(QT_EPI_SWIGLU, w.gu, n_gu_pad, w.s_gu, M, n_gu, kd_pad, mid, dff);
+            else gemm(QT_EPI_SILU, w.gu, n_gu_pad, w.s_gu, M, n_gu, kd_pad, mid, dff);
             norm_quant(mid, 0, dff, nullptr, M, dff, kff_pad, 4 * l + 3);
-            gemm(QT_EPI_RESADD, w.down, w.s_down, M, d, kff_pad, xc, d);
+            gemm(QT_EPI_RESADD, w.down, nd_pad, w.s_down, M, d, kff_pad, xc, d);
         }
         // final norm + head (model.cpp:442-445)
         norm_quant(xc, 1, d, gf, M, d, kd_pad, 4 * L);
-        gemm(QT_EPI_STORE, head, s_head, M, d, kd_pad, logits, d);
+        gemm(QT_EPI_STORE, head, nd_pad, s_head, M, d, kd_pad, logits, d);
         final_rows = M;
         if (logits_out)
             ck(cudaMemcpyAsync(logits_out, logits, (size_t)M * d * sizeof(float),
@@ -758,7 +761,7 @@ struct qt_engine {
             int* ptl = pt + (size_t)l * max_batch * max_pages;
             int* lenl = kv_len + (size_t)l * max_batch;
             if (!(g_skip & 4)) norm_quant(xcur, 1, d, w.g1, B, d, kd_pad, 4 * l + 0);
-            if (!(g_skip & 1)) gemm(QT_EPI_STORE, w.qkv, w.s_qkv, B, n_qkv, kd_pad, qkv, n_qkv);
+            if (!(g_skip & 1)) gemm(QT_EPI_STORE, w.qkv, n_qkv_pad, w.s_qkv, B, n_qkv, kd_pad, qkv, n_qkv);
             pb(P_KV);
             if (!(g_skip & 8)) ckl(qt_launch_rope_kv_append(qkv, n_qkv, B, H, Hkv, dh, next_pos, dec_seq, lenl, rope, ptl, max_pages,
                                          pool, page_bytes, 4, nullptr, st),
@@ -768,7 +771,7 @@ struct qt_engine {
             // decode attention over int4 pages + split merge fused with the attn_out quantizer
             if (!(g_skip & 2))
                 ckl(qt_launch_attn_decode(qkv, n_qkv, H, Hkv, dh, lenl, 1, B, pool, page_bytes, ptl, max_pages,
-                                          dec_splits, part_ml, part_o, nullptr, d, codes, kd_pad / 2, ascale,
+                                          dec_splits, part_ml, part_o, nullptr, d, codes, codes_rows, ascale,
                                           cfg.act_mode, cfg.act_mode == 0 ? act[4 * l + 1] : 0.0, kd_pad, 4, st),
                     "decode attention");
             {  // decode attention streams every cached K/V row of this layer once
@@ -776,15 +779,15 @@ struct qt_engine {
                 for (int b = 0; b < B; ++b) rows += h_kvlen[(size_t)l * B + b] + 1;
                 pe(rows * Hkv * 2 * (dh / 2 + 4) + (double)B * H * dh * 8);
             }
-            if (!(g_skip & 1)) gemm(QT_EPI_RESADD, w.o, w.s_o, B, d, kd_pad, xcur, d);
+            if (!(g_skip & 1)) gemm(QT_EPI_RESADD, w.o, nd_pad, w.s_o, B, d, kd_pad, xcur, d);
             if (!(g_skip & 4)) norm_quant(xcur, 1, d, w.g2, B, d, kd_pad, 4 * l + 2);
-            if (g_skip & 1) {} else if (cfg.mlp == 1) gemm(QT_EPI_SWIGLU, w.gu, w.s_gu, B, n_gu, kd_pad, mid, dff);
-            else gemm(QT_EPI_SILU, w.gu, w.s_gu, B, n_gu, kd_pad, mid, dff);
+            if (g_skip & 1) {} else if (cfg.mlp == 1) gemm(QT_EPI_SWIGLU, w.gu, n_gu_pad, w.s_gu, B, n_gu, kd_pad, mid, dff);
+            else gemm(QT_EPI_SILU, w.gu, n_gu_pad, w.s_gu, B, n_gu, kd_pad, mid, dff);
             if (!(g_skip & 4)) norm_quant(mid, 0, dff, nullptr, B, dff, kff_pad, 4 * l + 3);
-            if (!(g_skip & 1)) gemm(QT_EPI_RESADD, w.down, w.s_down, B, d, kff_pad, xcur, d);
+            if (!(g_skip & 1)) gemm(QT_EPI_RESADD, w.down, nd_pad, w.s_down, B, d, kff_pad, xcur, d);
         }
         norm_quant(xcur, 1, d, gf, B, d, kd_pad, 4 * L);
-        gemm(QT_EPI_STORE, head, s_head, B, d, kd_pad, dlogits, d);
+        gemm(QT_EPI_STORE, head, nd_pad, s_head, B, d, kd_pad, dlogits, d);
         ckl(qt_launch_kv_len_bump(kv_len, L * max_batch, next_pos, B, st), "kv length / position bump");
     }
 
@@ -911,18 +914,18 @@ int qt_engine_load_layer(qt_engine* e, int layer, const float* wq, const float* 
         if (!wq || !wk || !wv || !wo || !w1 || !w2) fail(QT_EINVAL, "null weight");
         if (e->cfg.mlp == 1 && !w3) fail(QT_EINVAL, "SwiGLU needs w3 (up projection)");
         LayerW& l = e->lw[layer];
-        const int d = e->d, kvd = e->Hkv * e->dh, f = e->dff, ldc = e->kd_pad / 2;
-        e->quant_into(wq, d, d, on_device, 1, 0, l.qkv, ldc, l.s_qkv);
-        e->quant_into(wk, d, kvd, on_device, 1, d, l.qkv, ldc, l.s_qkv);
-        e->quant_into(wv, d, kvd, on_device, 1, d + kvd, l.qkv, ldc, l.s_qkv);
-        e->quant_into(wo, d, d, on_device, 1, 0, l.o, ldc, l.s_o);
+        const int d = e->d, kvd = e->Hkv * e->dh, f = e->dff;
+        e->quant_into(wq, d, d, on_device, 1, 0, l.qkv, e->n_qkv_pad, l.s_qkv);
+        e->quant_into(wk, d, kvd, on_device, 1, d, l.qkv, e->n_qkv_pad, l.s_qkv);
+        e->quant_into(wv, d, kvd, on_device, 1, d + kvd, l.qkv, e->n_qkv_pad, l.s_qkv);
+        e->quant_into(wo, d, d, on_device, 1, 0, l.o, e->nd_pad, l.s_o);
         if (e->cfg.mlp == 1) {
-            e->quant_into(w1, d, f, on_device, 2, 0, l.gu, ldc, l.s_gu);
-            e->quant_into(w3, d, f, on_device, 2, 1, l.gu, ldc, l.s_gu);
+            e->quant_into(w1, d, f, on_device, 2, 0, l.gu, e->n_gu_pad, l.s_gu);
+            e->quant_into(w3, d, f, on_device, 2, 1, l.gu, e->n_gu_pad, l.s_gu);
         } else {
-            e->quant_into(w1, d, f, on_device, 1, 0, l.gu, ldc, l.s_gu);
+            e->quant_into(w1, d, f, on_device, 1, 0, l.gu, e->n_gu_pad, l.s_gu);
         }
-        e->quant_into(w2, f, d, on_device, 1, 0, l.down, e->kff_pad / 2, l.s_down);
+        e->quant_into(w2, f, d, on_device, 1, 0, l.down, e->nd_pad, l.s_down);
         e->load_gain(l.g1, g1, on_device);
         e->load_gain(l.g2, g2, on_device);
         l.loaded = true;
@@ -933,7 +936,7 @@ int qt_engine_load_layer(qt_engine* e, int layer, const float* wq, const float* 
 int qt_engine_load_head(qt_engine* e, const float* w_head, const float* final_gain, int on_device) {
     return guard([&] {
         if (!w_head) fail(QT_EINVAL, "null weight");
-        e->quant_into(w_head, e->d, e->d, on_device, 1, 0, e->head, e->kd_pad / 2, e->s_head);
+        e->quant_into(w_head, e->d, e->d, on_device, 1, 0, e->head, e->nd_pad, e->s_head);
         e->load_gain(e->gf, final_gain, on_device);
         e->head_loaded = true;
         e->graph_ok = false;

@@ -151,146 +151,14 @@ __global__ void __launch_bounds__(256) k_gemm_tc(const uint8_t* __restrict__ A, 
 }
 
 // ---------------------------------------------------------------- decode GEMV
-// HBM-streaming GEMV for decode (M <= 16 tokens), one CTA per SM.
-//   warp 8 (producer): TMA bulk copies of the CTA's weight slabs -- each stage
-//     is 8 consecutive 1 KB tiles (16 rows x 1024 k) of one 16-row block --
-//     into an 8-stage shared-memory ring, completion on mbarriers.  It starts
-//     before the programmatic-dependency wait, so weight streaming overlaps
-//     the upstream kernel.
-//   warps 0-7 (consumers): token codes staged once in smem; each warp takes
-//     one tile per stage (swap-AB mma.sync m16n8k32: weights = 16-row operand,
-//     tokens = n8 operand), releases the slot, and the 8 partial sums of a row
-//     block are reduced through smem for the fused epilogue.
-constexpr int GV_STAGES = 8, GV_TPS = 8;
-
-template <int NT, int EPI>
-__global__ void __launch_bounds__(288, 1) k_gemv_tc(const uint8_t* __restrict__ A, int lda,
-                                                    const double* __restrict__ sa, const uint8_t* __restrict__ W,
-                                                    int ldw, const double* __restrict__ sw, int M, int N, int K,
-                                                    void* __restrict__ out, int ldo, int* __restrict__ acc_dbg) {
-    constexpr int TOK = 8 * NT;
-    extern __shared__ __align__(1024) uint8_t smem[];
-    const int kb = K / 2;
-    const int ldsA = kb + 64;
-    uint8_t* ring = smem;                                            // [STAGES][TPS][1024]
-    uint8_t* As = smem + GV_STAGES * GV_TPS * 1024;                  // [TOK][ldsA]
-    int* red = reinterpret_cast<int*>(As + TOK * ldsA);              // [8][16][TOK]
-    uint64_t* full = reinterpret_cast<uint64_t*>(red + 8 * 16 * TOK);
-    uint64_t* empty = full + GV_STAGES;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int KT = K / 128;
-    const int spr = (KT + GV_TPS - 1) / GV_TPS;  // stages per row block
-    const int n_rb = (N + 15) / 16;
-    const int my_rb = blockIdx.x < n_rb ? (n_rb - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-    const int items = my_rb * spr;
-
-    if (tid == 0) {
-        for (int s = 0; s < GV_STAGES; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 8);
-        }
-        mbar_fence_init();
-    }
-    __syncthreads();
-
-    if (warp == 8) {  // ---------------- producer
-        if (lane == 0) {
-            for (int it = 0; it < items; ++it) {
-                const int s = it % GV_STAGES;
-                if (it >= GV_STAGES) mbar_wait(&empty[s], ((it / GV_STAGES) - 1) & 1);
-                const int rb = blockIdx.x + (it / spr) * gridDim.x, st = it % spr;
-                const int t0 = st * GV_TPS, nt = min(GV_TPS, KT - t0);
-                mbar_arrive_expect_tx(&full[s], (uint32_t)nt * 1024u);
-                bulk_g2s(ring + (size_t)s * GV_TPS * 1024, W + ((size_t)rb * KT + t0) * 1024, (uint32_t)nt * 1024u,
-                         &full[s]);
-            }
-        }
-        return;
-    }
-    // ------------------------------------ consumers
-    pdl_wait();  // token codes come from the upstream kernel
-    for (int c = tid; c < TOK * (kb / 16); c += 256) {
-        int r = c / (kb / 16), q = c % (kb / 16);
-        bool ok = r < M;
-        cp_async16(As + r * ldsA + q * 16, A + w4t_offset(ok ? r : 0, q * 16, lda), ok);
-    }
-    cp_async_commit();
-    cp_async_wait<0>();
-    asm volatile("bar.sync 1, 256;\n" ::: "memory");
-    pdl_launch_dependents();
-
-    const int g = lane >> 2, tig = lane & 3;
-    int acc[NT][4];
-#pragma unroll
-    for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0;
-    for (int it = 0; it < items; ++it) {
-        const int s = it % GV_STAGES;
-        const int rb = blockIdx.x + (it / spr) * gridDim.x, st = it % spr;
-        const int ch = st * GV_TPS + warp;  // 128-k chunk index of this warp's tile
-        mbar_wait(&full[s], (it / GV_STAGES) & 1);
-        if (ch < KT) {
-            const uint8_t* tile = ring + ((size_t)s * GV_TPS + warp) * 1024;
-            const uint4 wa = *reinterpret_cast<const uint4*>(tile + g * 64 + tig * 16);
-            const uint4 wb = *reinterpret_cast<const uint4*>(tile + 512 + g * 64 + tig * 16);
-            uint4 bv[NT];
-#pragma unroll
-            for (int j = 0; j < NT; ++j)
-                bv[j] = *reinterpret_cast<const uint4*>(As + (j * 8 + g) * ldsA + ch * 64 + tig * 16);
-#pragma unroll
-            for (int s2 = 0; s2 < 4; ++s2) {
-                uint32_t a[4];
-                unpack_x16((&wa.x)[s2], a[0], a[2]);
-                unpack_x16((&wb.x)[s2], a[1], a[3]);
-#pragma unroll
-                for (int j = 0; j < NT; ++j) {
-                    uint32_t b[2];
-                    unpack_x16((&bv[j].x)[s2], b[0], b[1]);
-                    mma_s8_16832(acc[j], a, b);
-                }
-            }
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
-        if (st == spr - 1) {
-            // split-K reduction over the 8 consumer warps + fused epilogue
-            int* base = red + (size_t)warp * (16 * TOK);
-#pragma unroll
-            for (int j = 0; j < NT; ++j) {
-                const int t = j * 8 + tig * 2;
-                base[g * TOK + t] = acc[j][0];
-                base[g * TOK + t + 1] = acc[j][1];
-                base[(g + 8) * TOK + t] = acc[j][2];
-                base[(g + 8) * TOK + t + 1] = acc[j][3];
-                acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0;
-            }
-            asm volatile("bar.sync 1, 256;\n" ::: "memory");
-            for (int e = tid; e < 8 * TOK; e += 256) {
-                const int t = e % TOK, cpair = e / TOK;
-                if (t < M) {
-                    int s0 = 0, s1 = 0;
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) {
-                        s0 += red[(size_t)k * (16 * TOK) + (2 * cpair) * TOK + t];
-                        s1 += red[(size_t)k * (16 * TOK) + (2 * cpair + 1) * TOK + t];
-                    }
-                    s0 >>= 8;
-                    s1 >>= 8;
-                    const int n = rb * 16 + 2 * cpair;
-                    if (acc_dbg) {
-                        if (n < N) acc_dbg[(size_t)t * N + n] = s0;
-                        if (n + 1 < N) acc_dbg[(size_t)t * N + n + 1] = s1;
-                    }
-                    const double a_s = sa[t];
-                    epi_store<EPI>(out, ldo, t, n, (double)s0 * (a_s * sw[n]), (double)s1 * (a_s * sw[n + 1]), N);
-                }
-            }
-            asm volatile("bar.sync 1, 256;\n" ::: "memory");
-        }
-    }
-}
-
-// Register-streaming variant of the decode GEMV (A/B against the TMA ring):
-// persistent CTAs, weights double-buffered in registers, tiled addressing.
+// Persistent, HBM-streaming GEMV for decode (M <= 16 tokens).  Each CTA owns a
+// strided set of 16-channel row blocks; its 8 warps split K.  The token codes
+// are staged once per CTA in smem.  Weight loads run one batch (U tiles of
+// 16 rows x 128 k per warp, each warp load instruction = 512 contiguous bytes
+// of a tile) ahead of the MMAs across row-block boundaries; the first batch is
+// issued before the programmatic-dependency wait and overlaps the upstream
+// kernel.  Swap-AB mma.sync m16n8k32: weights are the 16-row operand, tokens
+// the n8 operand; split-K partials are reduced in smem for the fused epilogue.
 template <int NT, int EPI>
 __global__ void __launch_bounds__(256) k_gemv_reg(const uint8_t* __restrict__ A, int lda, const double* __restrict__ sa,
                                                   const uint8_t* __restrict__ W, int ldw, const double* __restrict__ sw,
@@ -316,7 +184,7 @@ __global__ void __launch_bounds__(256) k_gemv_reg(const uint8_t* __restrict__ A,
         for (int u = 0; u < U; ++u) {
             const int c = ch0 + bat * U + u;
             const bool ok = rb < n_rb && c < ch1;
-            const uint8_t* tile = W + ((size_t)rb * KT + c) * 1024 + g * 64 + tig * 16;
+            const uint8_t* tile = W + ((size_t)c * (ldw >> 4) + rb) * 1024 + g * 64 + tig * 16;
             xa[u] = ok ? ldg_nc_v4(tile) : make_uint4(0, 0, 0, 0);
             xb[u] = ok ? ldg_nc_v4(tile + 512) : make_uint4(0, 0, 0, 0);
         }
@@ -413,10 +281,9 @@ template <int EPI>
 int launch_gemm(const uint8_t* A, int lda, const double* sa, const uint8_t* W, int ldw, const double* sw, int M,
                 int N, int K, void* out, int ldo, int* acc_dbg, cudaStream_t st) {
     if (M <= 0) return 0;
-    if (K % 128 || lda % 16 || ldw % 16) return -1;
+    if (K % 128 || lda % 16 || ldw % 16 || M > lda || N > ldw) return -1;  // lda/ldw = padded rows
     const int nb = (N + GB_N - 1) / GB_N;
-    static const int gemv_impl = getenv("QT_GEMV") ? atoi(getenv("QT_GEMV")) : 1;
-    if (M <= 16 && gemv_impl == 1) {
+    if (M <= 16) {
         const int kb = K / 2;
         const int TOK = M <= 8 ? 8 : 16;
         const size_t smem = (size_t)TOK * (kb + 64) + (size_t)8 * 16 * TOK * 4;
@@ -432,26 +299,6 @@ int launch_gemm(const uint8_t* A, int lda, const double* sa, const uint8_t* W, i
         auto kfn = k_gemv_reg<2, EPI>;
         cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         return launch_pdl(kfn, grid, dim3(256), smem, st, A, lda, sa, W, ldw, sw, M, N, K, out, ldo, acc_dbg);
-    }
-    if (M <= 16) {
-        const int kb = K / 2;
-        const int TOK = M <= 8 ? 8 : 16;
-        const size_t smem = (size_t)GV_STAGES * GV_TPS * 1024 + (size_t)TOK * (kb + 64) + (size_t)8 * 16 * TOK * 4 +
-                            2 * GV_STAGES * sizeof(uint64_t);
-        if (smem > 227 * 1024) return -1;
-        const int n_rb = (N + 15) / 16;
-        int sms = 148;
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-        const dim3 grid(std::min(n_rb, sms));
-#define QT_GEMV(NT_)                                                                                    \
-    do {                                                                                                \
-        auto kfn = k_gemv_tc<NT_, EPI>;                                                                 \
-        cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);              \
-        return launch_pdl(kfn, grid, dim3(288), smem, st, A, lda, sa, W, ldw, sw, M, N, K, out, ldo, acc_dbg); \
-    } while (0)
-        if (TOK == 8) QT_GEMV(1);
-        QT_GEMV(2);
-#undef QT_GEMV
     }
     if (M <= 512 || (long long)((M + 127) / 128) * nb < 148) {
         constexpr int BM = 64;

@@ -32,7 +32,7 @@
 namespace qt {
 
 constexpr int T5_BM = 128, T5_BN = 256, T5_BKB = 64;  // BK = 128 int4 = 64 packed bytes
-constexpr int T5_PS = 5, T5_IS = 2, T5_ACC = 2;       // packed stages, int8 stages, TMEM accumulators
+constexpr int T5_PS = 3, T5_IS = 3, T5_ACC = 2;       // packed stages, int8 stages, TMEM accumulators
 constexpr int T5_PA = T5_BM * T5_BKB, T5_PB = T5_BN * T5_BKB;  // packed bytes per stage
 constexpr int T5_IA = T5_BM * 128, T5_IB = T5_BN * 128;        // int8 bytes per stage
 constexpr int T5_THREADS = 320;  // 0 TMA, 1 MMA, 2-5 converters, 6-9 epilogue
@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(T5_THREADS, 1) k_gemm_tc05(const uint8_t* __re
     double* sws = reinterpret_cast<double*>(smem + T5Smem::swb);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int KB = K / 128;
-    const int KT = lda / 64;  // 1 KB tiles per row block (A and W share K)
+    const int art = lda >> 4, wrt = ldw >> 4;  // row blocks per k-block (tiled, k-block-major)
     const int mt_n = (M + T5_BM - 1) / T5_BM, nt_n = (N + T5_BN - 1) / T5_BN;
     const int tiles = mt_n * nt_n;
     const int a_rbs_total = (M + 15) / 16, w_rbs_total = (N + 15) / 16;
@@ -174,12 +174,11 @@ __global__ void __launch_bounds__(T5_THREADS, 1) k_gemm_tc05(const uint8_t* __re
                     const int s = it % T5_PS;
                     if (it >= T5_PS) mbar_wait(&pempty[s], ((it / T5_PS) - 1) & 1);
                     mbar_arrive_expect_tx(&pfull[s], (uint32_t)(a_rbs + w_rbs) * 1024u);
-                    uint8_t* pa = smem + T5Smem::pa + (size_t)s * T5_PA;
-                    uint8_t* pb = smem + T5Smem::pb + (size_t)s * T5_PB;
-                    for (int i = 0; i < a_rbs; ++i)
-                        bulk_g2s(pa + i * 1024, A + ((size_t)(a_rb0 + i) * KT + kb) * 1024, 1024u, &pfull[s]);
-                    for (int i = 0; i < w_rbs; ++i)
-                        bulk_g2s(pb + i * 1024, W + ((size_t)(w_rb0 + i) * KT + kb) * 1024, 1024u, &pfull[s]);
+                    // one bulk copy per operand: the stage's row blocks are contiguous
+                    bulk_g2s(smem + T5Smem::pa + (size_t)s * T5_PA, A + ((size_t)kb * art + a_rb0) * 1024,
+                             (uint32_t)a_rbs * 1024u, &pfull[s]);
+                    bulk_g2s(smem + T5Smem::pb + (size_t)s * T5_PB, W + ((size_t)kb * wrt + w_rb0) * 1024,
+                             (uint32_t)w_rbs * 1024u, &pfull[s]);
                 }
             }
         }
@@ -302,7 +301,7 @@ extern "C" int qt_launch_w4a4_tc05(int epi, const uint8_t* A, int lda, const dou
                                    cudaStream_t st) {
     using namespace qt;
     if (M <= 0) return 0;
-    if (K % 128 || lda != K / 2 || ldw != K / 2) return -1;
+    if (K % 128 || lda % 16 || ldw % 16 || M > lda || N > ldw) return -1;  // lda/ldw = padded rows
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     const int tiles = ((N + T5_BN - 1) / T5_BN) * ((M + T5_BM - 1) / T5_BM);

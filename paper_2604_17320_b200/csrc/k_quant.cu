@@ -42,6 +42,7 @@ QT_DEV void load8<double>(const double* p, double* v) {
 // Register-resident: each thread owns G groups of 8 consecutive elements
 // (words w = tid + j * blockDim), read once from global memory; the RMS sum
 // and the row max are block reductions over those registers.
+// codes: tiled int4 [rows_pad x d_pad] (ld_codes = rows_pad)
 template <typename TX, int G>
 __global__ void __launch_bounds__(1024) k_norm_quant(const TX* __restrict__ x, int ld_x,
                                                      const float* __restrict__ gain, int M, int D, int d_pad,

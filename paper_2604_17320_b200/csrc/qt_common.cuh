@@ -98,14 +98,15 @@ QT_DEV void unpack_x16(uint32_t w, uint32_t& lo, uint32_t& hi) {
 QT_DEV int nib(uint32_t w, int i) { return ((int)(w << (28 - 4 * i))) >> 28; }
 
 // ---------------------------------------------------------------- W4 tiled layout
-// Packed int4 weights [N_pad x K_pad] are stored as 1 KB tiles of 16 rows x 128 k
-// (16 rows x 64 bytes, row-major inside the tile); tile (rt, kt) sits at
-// ((rt * KT) + kt) * 1024 with KT = K_pad / 128, so one 16-row block's whole K
-// slab is contiguous (TMA bulk copies) and a lane (g, tig) of an mma.sync
-// fragment reads 16 contiguous bytes at tile + g*64 + tig*16 (+512 for rows 8-15).
-QT_HD size_t w4t_offset(int row, int kbyte, int row_bytes) {
-    const int KT = row_bytes / 64;
-    return ((size_t)(row >> 4) * KT + (kbyte >> 6)) * 1024 + (size_t)(row & 15) * 64 + (kbyte & 63);
+// Packed int4 code matrices (weights [N_pad x K_pad] and activations
+// [rows_pad x K_pad]) are stored as 1 KB tiles of 16 rows x 128 k (16 rows x 64
+// bytes, row-major inside the tile), k-block-major: tile (rt, kt) sits at
+// (kt * rows_pad/16 + rt) * 1024.  All row blocks of one k-block are therefore
+// contiguous -- a whole 128/256-row GEMM stage is ONE TMA bulk copy -- and a
+// lane (g, tig) of an mma.sync fragment reads 16 contiguous bytes at
+// tile + g*64 + tig*16 (+512 for rows 8-15).
+QT_HD size_t w4t_offset(int row, int kbyte, int rows_pad) {
+    return ((size_t)(kbyte >> 6) * (rows_pad >> 4) + (row >> 4)) * 1024 + (size_t)(row & 15) * 64 + (kbyte & 63);
 }
 
 // ---------------------------------------------------------------- mbarrier / TMA bulk
@@ -211,6 +212,7 @@ QT_DEV void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_depend
 }  // namespace qt
 
 #ifndef __CUDACC_RTC__
+#include <cstdlib>
 namespace qt {
 template <typename... KArgs, typename... Args>
 inline int launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
@@ -220,11 +222,12 @@ inline int launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t sm
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
+    static const bool no_pdl = getenv("QT_NOPDL") != nullptr;  // debug: plain stream serialization
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = no_pdl ? 0 : 1;
     cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
     return (int)e;
 }
