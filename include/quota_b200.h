@@ -138,6 +138,16 @@ int qt_kv_quant_append_i4(float* qkv, int ld_qkv, int M, int H, int Hkv, int d_h
                           const int* tok_seq, const int* tok_row, const double* rope_table, const int* page_table,
                           int max_pages, uint8_t* pool, int64_t page_bytes, float* k_out, void* stream);
 int qt_rope_table(int max_pos, int d_head, double* host_out);
+/* K3c + K4 on given metrics: score_tokens (robust_normalize x4 + fuse_scores,
+ * selector.cpp:70-115) and select_top_k (selector.cpp:117-136) for B
+ * sequences.  metrics: device fp64 [B][4][vstride] in (mag, inter, intra, res)
+ * order; visual / budget: device int[B] (V_b <= vstride, budget >= 1);
+ * weights4: HOST {mag, inter, intra, quant}, or null = metrics[b][0] already
+ * is the fused score (select_top_k alone).  slots: device int[B][vstride],
+ * the min(budget, V) retained slots ascending; fused_out [B][vstride] and
+ * norm_out [B][4][vstride] nullable. */
+int qt_quota_topk(const double* metrics, int B, int vstride, const int* visual, const int* budget,
+                  const double* weights4, int* slots, double* fused_out, double* norm_out, void* stream);
 
 #ifdef __cplusplus
 }

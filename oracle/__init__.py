@@ -91,8 +91,118 @@ def ref_lib():
         lib.qref_layer_cost.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int]
         lib.qref_percentile.argtypes = [_dp, C.c_int, C.c_double, _dp]
         lib.qref_prefill_threads.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_uint64, _dp]
+        lib.qref_quantize_fit.argtypes = [_dp, C.c_int, C.c_int, C.c_int, C.c_int, _dp, _i8p]
+        lib.qref_quantize_with.argtypes = [_dp, C.c_int, C.c_int, C.c_int, C.c_int, _dp, C.c_int, _i8p, _dp]
+        lib.qref_fake_quant_per_row.argtypes = [_dp, C.c_int, C.c_int, C.c_int, _dp]
+        lib.qref_kv_quantize.argtypes = [_dp, C.c_int, C.c_int, C.c_int, _i8p, _dp]
+        lib.qref_quantized_linear.argtypes = [_dp, C.c_int, C.c_int, _i8p, _dp, C.c_int, C.c_int, C.c_int, _dp]
+        lib.qref_matmul.argtypes = [_dp, C.c_int, C.c_int, _dp, C.c_int, _dp]
+        lib.qref_rms_norm_rows.argtypes = [_dp, C.c_int, C.c_int, _dp, _dp]
+        lib.qref_rope.argtypes = [_dp, C.c_int, C.c_int]
+        lib.qref_silu.argtypes = [C.c_double]
+        lib.qref_compute_budget.argtypes = [C.c_double, C.c_int, _ip]
+        lib.qref_robust_normalize.argtypes = [_dp, C.c_int, _dp]
+        lib.qref_select_top_k.argtypes = [_dp, C.c_int, C.c_int, _ip, _ip]
+        lib.qref_score_tokens.argtypes = [_dp, C.c_int, C.c_int, C.c_int, C.c_int, _dp, _dp, _dp, C.c_int, _dp,
+                                          _dp, _dp]
+        lib.qref_parse_recipe.argtypes = [C.c_char_p, C.c_int, _ip, _ip, _dp, _dp, _ip, C.c_char_p, C.c_int]
+        lib.qref_serialize_recipe.argtypes = [C.c_int, _ip, _dp, _dp, C.c_int, C.c_char_p, C.c_char_p, C.c_int,
+                                              C.c_char_p]
+        lib.qref_executed_visual_lengths.argtypes = [C.c_char_p, C.c_int, _ip]
         _ref_lib = lib
     return _ref_lib
+
+
+# ---------------------------------------------------------------- R0 primitives (kernel-level checkers)
+
+
+def ref_compute_budget(keep_ratio, v0):
+    """compute_budget (selector.cpp:11-17)."""
+    lib = ref_lib()
+    out = C.c_int()
+    _check(lib.qref_compute_budget(keep_ratio, v0, C.byref(out)), lib, "qref")
+    return out.value
+
+
+def ref_percentile(v, p):
+    """percentile (numeric.cpp:84-96)."""
+    lib = ref_lib()
+    a = f64(v)
+    out = C.c_double()
+    _check(lib.qref_percentile(_d(a), a.size, p, C.byref(out)), lib, "qref")
+    return out.value
+
+
+def ref_robust_normalize(v):
+    """robust_normalize (selector.cpp:70-84)."""
+    lib = ref_lib()
+    a = f64(v)
+    out = np.empty_like(a)
+    _check(lib.qref_robust_normalize(_d(a), a.size, _d(out)), lib, "qref")
+    return out
+
+
+def ref_select_top_k(scores, k):
+    """select_top_k (selector.cpp:117-136): ascending retained slots."""
+    lib = ref_lib()
+    a = f64(scores)
+    out = np.empty(max(1, min(k, a.size)), dtype=np.int32)
+    n = C.c_int()
+    _check(lib.qref_select_top_k(_d(a), a.size, k, _i(out), C.byref(n)), lib, "qref")
+    return out[:n.value].copy()
+
+
+def ref_score_tokens(visual, inter, intra, weights=(0.25, 0.45, 0.10, 0.20), res_bits=4):
+    """compute_metrics + score_tokens (selector.cpp:19-115).  visual [n x d], inter [H x T x n],
+    intra [H x n x n].  Returns (metrics [4 x n], normalised [4 x n], fused [n])."""
+    lib = ref_lib()
+    vis, it, ia, w = f64(visual), f64(inter), f64(intra), f64(weights)
+    n, d = vis.shape
+    H, T = it.shape[0], it.shape[1]
+    m = np.empty((4, n))
+    nn = np.empty((4, n))
+    f = np.empty(n)
+    _check(lib.qref_score_tokens(_d(vis), n, d, H, T, _d(it), _d(ia), _d(w), res_bits, _d(m), _d(nn), _d(f)),
+           lib, "qref")
+    return m, nn, f
+
+
+def ref_parse_recipe(text, max_layers=256):
+    """parse_recipe (recipe.cpp:91-116) -> dict; raises OracleError with the reference message."""
+    lib = ref_lib()
+    n = C.c_int()
+    lay = np.empty(max_layers, dtype=np.int32)
+    kp = np.empty(max_layers)
+    w = np.empty(4)
+    v0 = C.c_int()
+    dg = C.create_string_buffer(256)
+    _check(lib.qref_parse_recipe(text.encode() if isinstance(text, str) else text, max_layers, C.byref(n), _i(lay),
+                                 _d(kp), _d(w), C.byref(v0), dg, 256), lib, "qref")
+    k = n.value
+    return dict(candidate_layers=lay[:k].tolist(), keep_ratios=kp[:k].tolist(), weights=tuple(w.tolist()),
+                v0=v0.value, quant_digest=dg.value.decode())
+
+
+def ref_quantize_fit(x, axis, bits=4):
+    """fit_params + quantize (quant.cpp:47-91); axis 0/1/2 = PerTensor/PerRow/PerColumn."""
+    lib = ref_lib()
+    a = f64(x)
+    rows, cols = a.shape
+    sc = np.empty({0: 1, 1: rows, 2: cols}[axis])
+    codes = np.empty(a.size, dtype=np.int8)
+    _check(lib.qref_quantize_fit(_d(a), rows, cols, bits, axis, _d(sc), _b(codes)), lib, "qref")
+    return codes.reshape(a.shape), sc
+
+
+def ref_kv_quantize(x, bits=4):
+    """kv_quantize (quant.cpp:117-119): per-row symmetric codes + scales."""
+    lib = ref_lib()
+    a = f64(x)
+    rows, cols = a.shape
+    codes = np.empty(a.size, dtype=np.int8)
+    sc = np.empty(rows)
+    _check(lib.qref_kv_quantize(_d(a), rows, cols, bits, _b(codes), _d(sc)), lib, "qref")
+    return codes.reshape(a.shape), sc
 
 
 def port_lib():

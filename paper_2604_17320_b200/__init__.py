@@ -87,6 +87,7 @@ def lib():
         L.qt_kv_quant_append_i4.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp, vp, vp,
                                             C.c_int, vp, C.c_int64, vp, vp]
         L.qt_rope_table.argtypes = [C.c_int, C.c_int, dp]
+        L.qt_quota_topk.argtypes = [vp, C.c_int, C.c_int, vp, vp, dp, vp, vp, vp, vp]
         _lib = L
     return _lib
 
@@ -286,6 +287,24 @@ class Engine:
         return dict(zip(keys, list(o)))
 
 
+def parse_recipe(text, max_layers=256):
+    """parse_recipe (recipe.cpp:91-116) through qt_recipe_parse (host-side, strict keys,
+    schema_version 1, PruningRecipe::validate); raises QuotaInvalidArgument like the
+    reference's std::invalid_argument."""
+    n = C.c_int()
+    lay = np.empty(max_layers, dtype=np.int32)
+    kp = np.empty(max_layers, dtype=np.float64)
+    w = np.empty(4, dtype=np.float64)
+    v0 = C.c_int()
+    dg = C.create_string_buffer(256)
+    check(lib().qt_recipe_parse(text.encode() if isinstance(text, str) else text, max_layers, C.byref(n), _ip(lay),
+                                kp.ctypes.data_as(C.POINTER(C.c_double)), w.ctypes.data_as(C.POINTER(C.c_double)),
+                                C.byref(v0), dg, 256))
+    k = n.value
+    return dict(candidate_layers=lay[:k].tolist(), keep_ratios=kp[:k].tolist(), weights=tuple(w.tolist()),
+                v0=v0.value, quant_digest=dg.value.decode())
+
+
 # ---------------------------------------------------------------- kernel-level ABI (torch tensors)
 
 
@@ -322,6 +341,27 @@ def quant_weight(w, k_pad, n_pad, row_mul=1, row_add=0, codes=None, scales=None,
     check(lib().qt_quant_weight_i4(_ptr(w), K, N, row_mul, row_add, _ptr(codes), codes.shape[0], _ptr(scales),
                                    _ptr(scratch), C.c_void_p(stream)))
     return codes, scales
+
+
+def quota_topk(metrics, visual, budget, weights=None, stream=0):
+    """K3c+K4 on device metrics [B x 4 x vstride] (fp64 cuda tensor): returns
+    (slots list per sequence, fused [B x vstride], normalised [B x 4 x vstride]).
+    weights=None: metrics[:, 0] already is the fused score (select_top_k alone)."""
+    import torch
+    B, _, vs = metrics.shape
+    dev = metrics.device
+    vis = torch.tensor(visual, dtype=torch.int32, device=dev)
+    bud = torch.tensor(budget, dtype=torch.int32, device=dev)
+    slots = torch.full((B, vs), -1, dtype=torch.int32, device=dev)
+    fused = torch.zeros((B, vs), dtype=torch.float64, device=dev)
+    norm = torch.zeros((B, 4, vs), dtype=torch.float64, device=dev)
+    w = None if weights is None else np.ascontiguousarray(weights, dtype=np.float64)
+    check(lib().qt_quota_topk(_ptr(metrics.contiguous()), B, vs, _ptr(vis), _ptr(bud),
+                              None if w is None else w.ctypes.data_as(C.POINTER(C.c_double)), _ptr(slots),
+                              _ptr(fused), _ptr(norm), C.c_void_p(stream)))
+    torch.cuda.current_stream(dev).synchronize() if stream == 0 else None
+    s = slots.cpu().numpy()
+    return [s[b, :min(budget[b], visual[b])].copy() for b in range(B)], fused, norm
 
 
 def rope_table(max_pos, d_head):

@@ -653,7 +653,7 @@ struct qt_engine {
                 int* kp_ev = kept_pos + (size_t)trace_layers.size() * max_batch * vstride;
                 ckl(qt_launch_select_topk(mag, res, inter, intra, H, vstride, seq_vis, seq_txt, budget, seq_off, new_off,
                                           B, vmax, hw4.data(), keep_src, keep_local, vstride, pc, kp_ev, nullptr,
-                                          nullptr, st),
+                                          nullptr, nullptr, 0, st),
                     "quota top-k");
                 double* xn = x[xc == x[0] ? 1 : 0];
                 int* pn = pos[pc == pos[0] ? 1 : 0];
@@ -1139,6 +1139,17 @@ int qt_kv_quant_append_i4(float* qkv, int ld_qkv, int M, int H, int Hkv, int d_h
         ckl(qt_launch_rope_kv_append(qkv, ld_qkv, M, H, Hkv, d_head, positions, tok_seq, tok_row, rope_table,
                                      page_table, max_pages, pool, page_bytes, 4, k_out, (cudaStream_t)stream),
             "kv quant append");
+    });
+}
+
+int qt_quota_topk(const double* metrics, int B, int vstride, const int* visual, const int* budget,
+                  const double* weights4, int* slots, double* fused_out, double* norm_out, void* stream) {
+    return guard([&] {
+        if (B < 0 || vstride < 1) fail(QT_EINVAL, "invalid top-k shape");
+        ckl(qt_launch_select_topk(nullptr, nullptr, nullptr, nullptr, 1, vstride, visual, nullptr, budget, nullptr,
+                                  nullptr, B, vstride, weights4, nullptr, slots, vstride, nullptr, nullptr, fused_out,
+                                  norm_out, metrics, weights4 ? 0 : 1, (cudaStream_t)stream),
+            "quota top-k");
     });
 }
 

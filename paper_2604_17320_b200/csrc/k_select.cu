@@ -90,20 +90,27 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select_topk(
     const int* __restrict__ budget, const int* __restrict__ old_off, const int* __restrict__ new_off,
     double w_mag, double w_inter, double w_intra, double w_quant, int* __restrict__ keep_src,
     int* __restrict__ keep_local, int kl_stride, const int* __restrict__ pos, int* __restrict__ kept_pos,
-    double* __restrict__ fused_out, double* __restrict__ norm_out) {
+    double* __restrict__ fused_out, double* __restrict__ norm_out, const double* __restrict__ met_in, int raw) {
     extern __shared__ __align__(16) double sm[];
     __shared__ int hist[256];
     __shared__ int scan_sh[33];
     __shared__ unsigned long long s_prefix;
     __shared__ int s_krem, s_digit;
     const int b = blockIdx.x;
-    const int V = vis[b], T = txt[b], K = budget[b];
+    // met_in (kernel-level ABI): metrics [B][4][vstride] given directly; raw: met_in[0] IS the
+    // fused score (select_top_k alone).  txt / offsets / keep_src / pos may then be null.
+    const int V = vis[b], T = txt ? txt[b] : 0, K = budget[b];
+    const int ob = old_off ? old_off[b] : 0, nb = new_off ? new_off[b] : 0;
     int n2 = 1;
     while (n2 < V) n2 <<= 1;
     double* met = sm;            // [4][n2]
     double* srt = sm + 4 * n2;   // [n2]
     const double invH = 1.0 / (double)H;
-    for (int i = threadIdx.x; i < V; i += blockDim.x) {
+    for (int i = threadIdx.x; i < V && met_in; i += blockDim.x) {
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi) met[mi * n2 + i] = met_in[((size_t)b * 4 + mi) * vstride + i];
+    }
+    for (int i = threadIdx.x; i < V && !met_in; i += blockDim.x) {
         double si = 0.0, sa = 0.0;
         for (int h = 0; h < H; ++h) {
             si += (double)inter_p[((size_t)b * H + h) * vstride + i];
@@ -116,7 +123,7 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select_topk(
     }
     __syncthreads();
     // robust_normalize each metric in place (selector.cpp:70-84)
-    for (int mi = 0; mi < 4; ++mi) {
+    for (int mi = 0; mi < 4 && !raw; ++mi) {
         double* m = met + mi * n2;
         for (int i = threadIdx.x; i < n2; i += blockDim.x) srt[i] = i < V ? m[i] : __longlong_as_double(0x7ff0000000000000ll);
         __syncthreads();
@@ -134,7 +141,7 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select_topk(
     // fuse (selector.cpp:86-104), evaluated left to right without contraction
     double* fused = srt;
     for (int i = threadIdx.x; i < V; i += blockDim.x) {
-        double f = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(w_mag, met[i]), __dmul_rn(w_inter, met[n2 + i])),
+        double f = raw ? met[i] : __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(w_mag, met[i]), __dmul_rn(w_inter, met[n2 + i])),
                                        __dmul_rn(w_intra, met[2 * n2 + i])),
                              __dmul_rn(w_quant, met[3 * n2 + i]));
         fused[i] = f;
@@ -198,15 +205,15 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select_topk(
             bool s = k > kth || (k == kth && e < need_eq);
             if (k == kth) ++e;
             if (s) {
-                keep_src[new_off[b] + j] = old_off[b] + i;
+                if (keep_src) keep_src[nb + j] = ob + i;
                 keep_local[(size_t)b * kl_stride + j] = i;
-                kept_pos[(size_t)b * vstride + j] = pos[old_off[b] + i];
+                if (kept_pos) kept_pos[(size_t)b * vstride + j] = pos[ob + i];
                 ++j;
             }
         }
     }
     for (int t = threadIdx.x; t < T; t += blockDim.x) {
-        keep_src[new_off[b] + kk + t] = old_off[b] + V + t;
+        if (keep_src) keep_src[nb + kk + t] = ob + V + t;
         keep_local[(size_t)b * kl_stride + kk + t] = V + t;
     }
 }
@@ -268,16 +275,17 @@ int qt_launch_select_topk(const double* mag, const double* res, const float* int
                           int vstride, const int* vis, const int* txt, const int* budget, const int* old_off,
                           const int* new_off, int B, int vmax, const double* w4, int* keep_src, int* keep_local,
                           int kl_stride, const int* pos, int* kept_pos, double* fused_out, double* norm_out,
-                          cudaStream_t st) {
+                          const double* met_in, int raw, cudaStream_t st) {
     if (B <= 0) return 0;
     int n2 = 1;
     while (n2 < vmax) n2 <<= 1;
     const size_t smem = (size_t)5 * n2 * sizeof(double);
     if (smem > 220 * 1024) return -1;
     cudaFuncSetAttribute(k_select_topk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const double w0 = w4 ? w4[0] : 0.0, w1 = w4 ? w4[1] : 0.0, w2 = w4 ? w4[2] : 0.0, w3 = w4 ? w4[3] : 0.0;
     k_select_topk<<<B, SEL_THREADS, smem, st>>>(mag, res, inter, intra, H, vstride, vis, txt, budget, old_off,
-                                                new_off, w4[0], w4[1], w4[2], w4[3], keep_src, keep_local,
-                                                kl_stride, pos, kept_pos, fused_out, norm_out);
+                                                new_off, w0, w1, w2, w3, keep_src, keep_local,
+                                                kl_stride, pos, kept_pos, fused_out, norm_out, met_in, raw);
     return (int)cudaGetLastError();
 }
 

@@ -47,7 +47,7 @@ int qt_launch_select_topk(const double* mag, const double* res, const float* int
                           int vstride, const int* vis, const int* txt, const int* budget, const int* old_off,
                           const int* new_off, int B, int vmax, const double* w4, int* keep_src, int* keep_local,
                           int kl_stride, const int* pos, int* kept_pos, double* fused_out, double* norm_out,
-                          cudaStream_t st);
+                          const double* met_in, int raw, cudaStream_t st);
 int qt_launch_gather_rows(const double* x, double* xn, int D, const int* pos, int* posn, const int* src, int M,
                           cudaStream_t st);
 int qt_launch_kv_compact(uint8_t* pool, long long page_bytes, const int* pt, int max_pages, int Hkv, int dh,

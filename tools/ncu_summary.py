@@ -16,7 +16,7 @@ def load(path):
             continue
         v = float(r[idx["Metric Value"]].replace(",", ""))
         unit = r[idx["Metric Unit"]]
-        v *= {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}.get(unit, 1.0)
+        v *= {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3, "s": 1e6, "second": 1e6}.get(unit, 1.0)
         name = re.sub(r"\(.*", "", r[idx["Kernel Name"]])
         name = re.sub(r"^void ", "", name)
         seq.append((name[:70], v, r[idx["Grid Size"]], r[idx["Block Size"]]))
