@@ -76,6 +76,15 @@ int qt_engine_load_layer(qt_engine* e, int layer, const float* wq, const float* 
                          const float* wo, const float* w1, const float* w2, const float* w3, const float* g1,
                          const float* g2, int on_device);
 int qt_engine_load_head(qt_engine* e, const float* w_head, const float* final_gain, int on_device);
+/* Packed-weight loader: a QuantEnv's pre-quantized weights as they are
+ * (QuantizedLayerWeights, model.hpp:141-151): int8 codes in [-7, 7], host,
+ * reference orientation [d_in x d_out] row-major, with one fp64 scale per
+ * OUTPUT channel (GroupAxis::PerColumn).  codes/scales: arrays of 7 pointers in
+ * the order wq, wk, wv, wo, w1, w2, w3 (w3 = SwiGLU up; null for mlp = 0).
+ * Gains fp64 (null = 1.0).  Bit-identical weights to the caller's QuantEnv. */
+int qt_engine_load_layer_codes(qt_engine* e, int layer, const int8_t* const* codes, const double* const* scales,
+                               const double* g1, const double* g2);
+int qt_engine_load_head_codes(qt_engine* e, const int8_t* codes, const double* scales, const double* final_gain);
 /* ActScales (model.hpp:114-133): 4 * n_layers + 1 static per-tensor scales,
  * order (attn_in, attn_out, mlp_in, mlp_mid) per layer, then head_in. */
 int qt_engine_set_act_scales(qt_engine* e, const double* scales);
@@ -96,11 +105,15 @@ int qt_recipe_parse(const char* json, int max_layers, int* n_layers, int* layers
  * (nullable): packed [sum(final rows) x d_model], host or device. */
 int qt_engine_prefill(qt_engine* e, int n_seq, const float* emb, int emb_on_device, const int* visual,
                       const int* text, const int* v0, const int* positions, float* logits_out, int out_on_device);
+/* Same with fp64 embeddings (the reference's Matrix element type). */
+int qt_engine_prefill_f64(qt_engine* e, int n_seq, const double* emb, int emb_on_device, const int* visual,
+                          const int* text, const int* v0, const int* positions, float* logits_out, int out_on_device);
 /* rows of the packed prefill logits (sum over sequences of the final layout) */
 int qt_engine_prefill_rows(qt_engine* e);
 /* decode_step (model.cpp:455-562) for every sequence of the last prefill:
  * emb [n_seq x d_model], logits_out [n_seq x d_model]. */
 int qt_engine_decode(qt_engine* e, const float* emb, int emb_on_device, float* logits_out, int out_on_device);
+int qt_engine_decode_f64(qt_engine* e, const double* emb, int emb_on_device, float* logits_out, int out_on_device);
 
 /* Introspection (parity tests, reports). */
 int qt_engine_layout(qt_engine* e, int seq, int* visual, int* text, int* positions, int cap);

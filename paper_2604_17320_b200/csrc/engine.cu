@@ -436,6 +436,34 @@ struct qt_engine {
         ck(cudaStreamSynchronize(st), "weight quantize");
     }
 
+    // pre-quantized codes (host int8 [K x N], reference orientation) + fp64 per-column scales
+    void codes_into(const int8_t* c, const double* sc, int K, int N, int row_mul, int row_add, uint8_t* codes_dst,
+                    int rows_pad, double* scales_dst) {
+        if (!c || !sc) fail(QT_EINVAL, "null weight codes");
+        const size_t n = (size_t)K * N;
+        if ((n + 3) / 4 > wstage_elems) {
+            if (wstage) cudaFree(wstage);
+            wstage = dalloc<float>((n + 3) / 4);
+            wstage_elems = (n + 3) / 4;
+        }
+        for (size_t i = 0; i < n; ++i)
+            if (c[i] < -7 || c[i] > 7) fail(QT_EINVAL, "weight code outside the int4 range");
+        for (int i = 0; i < N; ++i)
+            if (!(sc[i] > 0.0) || !std::isfinite(sc[i])) fail(QT_EINVAL, "weight scales must be positive");
+        ck(cudaMemcpyAsync(wstage, c, n, cudaMemcpyHostToDevice, st), "codes upload");
+        ck(cudaMemcpyAsync(wscratch, sc, (size_t)N * sizeof(double), cudaMemcpyHostToDevice, st), "scales upload");
+        ckl(qt_launch_codes_pack(reinterpret_cast<const int8_t*>(wstage), K, N, wscratch, row_mul, row_add,
+                                 codes_dst, rows_pad, scales_dst, st),
+            "codes pack");
+        ck(cudaStreamSynchronize(st), "codes pack");
+    }
+    void load_gain64(float* dst, const double* g) {
+        std::vector<float> v(d, 1.0f);
+        if (g)
+            for (int i = 0; i < d; ++i) v[i] = (float)g[i];
+        ck(cudaMemcpy(dst, v.data(), d * sizeof(float), cudaMemcpyHostToDevice), "gain");
+    }
+
     void load_gain(float* dst, const float* g, int on_device) {
         if (!g) {
             std::vector<float> ones(d, 1.0f);
@@ -472,7 +500,7 @@ struct qt_engine {
         std::vector<int> vis_at;  // visual count entering each layer
     };
 
-    void prefill(int nseq, const float* emb, int emb_dev, const int* vis, const int* txt, const int* v0s,
+    void prefill(int nseq, const void* emb, int emb_dev, int emb_f64, const int* vis, const int* txt, const int* v0s,
                  const int* positions, float* logits_out, int out_dev) {
         for (auto& l : lw)
             if (!l.loaded) fail(QT_EINVAL, "model weights not loaded");
@@ -548,12 +576,18 @@ struct qt_engine {
         // inputs
         double* xc = x[0];
         int* pc = pos[0];
-        const float* emb_d = emb;
-        if (!emb_dev) {  // stage through the fp32 attention buffer, widen on device
-            ck(cudaMemcpyAsync(attn, emb, (size_t)total * d * sizeof(float), cudaMemcpyHostToDevice, st), "emb");
-            emb_d = attn;
+        if (emb_f64) {  // fp64 embeddings go straight into the residual stream
+            ck(cudaMemcpyAsync(xc, emb, (size_t)total * d * sizeof(double),
+                               emb_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st),
+               "emb");
+        } else {
+            const float* emb_d = static_cast<const float*>(emb);
+            if (!emb_dev) {  // stage through the fp32 attention buffer, widen on device
+                ck(cudaMemcpyAsync(attn, emb, (size_t)total * d * sizeof(float), cudaMemcpyHostToDevice, st), "emb");
+                emb_d = attn;
+            }
+            ckl(qt_launch_f32_to_f64(emb_d, xc, (long long)total * d, st), "embedding widen");
         }
-        ckl(qt_launch_f32_to_f64(emb_d, xc, (long long)total * d, st), "embedding widen");
         upload(pc, hpos);
         std::vector<int> cur_v(h_vis);
         auto upload_layout = [&]() {
@@ -754,8 +788,7 @@ struct qt_engine {
 
     // ------------------------------------------------------------ decode
     void decode_body() {
-        double* xcur = xd;
-        ckl(qt_launch_f32_to_f64(xd_in, xd, (long long)B * d, st), "embedding widen");
+        double* xcur = xd;  // the step's input was written (widened) into xd before the graph
         for (int l = 0; l < L; ++l) {
             const LayerW& w = lw[l];
             int* ptl = pt + (size_t)l * max_batch * max_pages;
@@ -798,7 +831,7 @@ struct qt_engine {
         prof_next = false;
     }
 
-    void decode(const float* emb, int emb_dev, float* out, int out_dev) {
+    void decode(const void* emb, int emb_dev, int emb_f64, float* out, int out_dev) {
         if (!prefilled) fail(QT_ERUNTIME, "cache and execution mode mismatch");
         if (decode_steps >= max_decode) fail(QT_EINVAL, "decode steps exceed engine capacity");
         const bool profiling = prof_next;
@@ -806,9 +839,18 @@ struct qt_engine {
             prof = std::make_unique<Profiler>();
             prof->st = st;
         }
-        ck(cudaMemcpyAsync(xd_in, emb, (size_t)B * d * sizeof(float),
-                           emb_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st),
-           "decode emb");
+        if (emb_f64) {
+            ck(cudaMemcpyAsync(xd, emb, (size_t)B * d * sizeof(double),
+                               emb_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st),
+               "decode emb");
+        } else {
+            ck(cudaMemcpyAsync(xd_in, emb, (size_t)B * d * sizeof(float),
+                               emb_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st),
+               "decode emb");
+            pb(P_OTHER);
+            ckl(qt_launch_f32_to_f64(xd_in, xd, (long long)B * d, st), "embedding widen");
+            pe((double)B * d * 12);
+        }
         if (g_nograph || profiling) {
             decode_body();  // eager launches so every kernel gets its own events
         } else if (!graph_ok) {
@@ -933,6 +975,41 @@ int qt_engine_load_layer(qt_engine* e, int layer, const float* wq, const float* 
     });
 }
 
+int qt_engine_load_layer_codes(qt_engine* e, int layer, const int8_t* const* codes, const double* const* scales,
+                               const double* g1, const double* g2) {
+    return guard([&] {
+        if (layer < 0 || layer >= e->L) fail(QT_ERANGE, "layer out of range");
+        if (!codes || !scales) fail(QT_EINVAL, "null weight codes");
+        LayerW& l = e->lw[layer];
+        const int d = e->d, kvd = e->Hkv * e->dh, f = e->dff;
+        if (e->cfg.mlp == 1 && (!codes[6] || !scales[6])) fail(QT_EINVAL, "SwiGLU needs w3 (up projection)");
+        e->codes_into(codes[0], scales[0], d, d, 1, 0, l.qkv, e->n_qkv_pad, l.s_qkv);
+        e->codes_into(codes[1], scales[1], d, kvd, 1, d, l.qkv, e->n_qkv_pad, l.s_qkv);
+        e->codes_into(codes[2], scales[2], d, kvd, 1, d + kvd, l.qkv, e->n_qkv_pad, l.s_qkv);
+        e->codes_into(codes[3], scales[3], d, d, 1, 0, l.o, e->nd_pad, l.s_o);
+        if (e->cfg.mlp == 1) {
+            e->codes_into(codes[4], scales[4], d, f, 2, 0, l.gu, e->n_gu_pad, l.s_gu);
+            e->codes_into(codes[6], scales[6], d, f, 2, 1, l.gu, e->n_gu_pad, l.s_gu);
+        } else {
+            e->codes_into(codes[4], scales[4], d, f, 1, 0, l.gu, e->n_gu_pad, l.s_gu);
+        }
+        e->codes_into(codes[5], scales[5], f, d, 1, 0, l.down, e->nd_pad, l.s_down);
+        e->load_gain64(l.g1, g1);
+        e->load_gain64(l.g2, g2);
+        l.loaded = true;
+        e->graph_ok = false;
+    });
+}
+
+int qt_engine_load_head_codes(qt_engine* e, const int8_t* codes, const double* scales, const double* final_gain) {
+    return guard([&] {
+        e->codes_into(codes, scales, e->d, e->d, 1, 0, e->head, e->nd_pad, e->s_head);
+        e->load_gain64(e->gf, final_gain);
+        e->head_loaded = true;
+        e->graph_ok = false;
+    });
+}
+
 int qt_engine_load_head(qt_engine* e, const float* w_head, const float* final_gain, int on_device) {
     return guard([&] {
         if (!w_head) fail(QT_EINVAL, "null weight");
@@ -973,7 +1050,7 @@ int qt_engine_set_recipe(qt_engine* e, int n, const int* layers, const double* k
         const double w[4] = {w4 ? w4[0] : 0.25, w4 ? w4[1] : 0.45, w4 ? w4[2] : 0.10, w4 ? w4[3] : 0.20};
         for (double x : w)
             if (x < 0) fail(QT_EINVAL, "negative metric weight");
-        if (std::fabs(w[0] + w[1] + w[2] + w[3] - 1.0) > 1e-9) fail(QT_EINVAL, "metric weights must sum to 1");
+        if (std::fabs(w[0] + w[1] + w[2] + w[3] - 1.0) > 1e-6) fail(QT_EINVAL, "metric weights must sum to 1");  // selector.cpp:91-93
         if (v0 < 1) fail(QT_EINVAL, "v0 must be >= 1");
         if (layers[n - 1] >= e->L) fail(QT_ERUNTIME, "recipe candidate layers do not fit the model");  // harness.cpp:86-88
         if (res_bits == 0 || res_bits == 1 || res_bits > 8) fail(QT_EINVAL, "bits out of range [2,8]");
@@ -990,7 +1067,15 @@ int qt_engine_prefill(qt_engine* e, int n_seq, const float* emb, int emb_on_devi
                       const int* text, const int* v0, const int* positions, float* logits_out, int out_on_device) {
     return guard([&] {
         if (!emb || !visual || !text) fail(QT_EINVAL, "null argument");
-        e->prefill(n_seq, emb, emb_on_device, visual, text, v0, positions, logits_out, out_on_device);
+        e->prefill(n_seq, emb, emb_on_device, 0, visual, text, v0, positions, logits_out, out_on_device);
+    });
+}
+
+int qt_engine_prefill_f64(qt_engine* e, int n_seq, const double* emb, int emb_on_device, const int* visual,
+                          const int* text, const int* v0, const int* positions, float* logits_out, int out_on_device) {
+    return guard([&] {
+        if (!emb || !visual || !text) fail(QT_EINVAL, "null argument");
+        e->prefill(n_seq, emb, emb_on_device, 1, visual, text, v0, positions, logits_out, out_on_device);
     });
 }
 
@@ -999,7 +1084,14 @@ int qt_engine_prefill_rows(qt_engine* e) { return e->final_rows; }
 int qt_engine_decode(qt_engine* e, const float* emb, int emb_on_device, float* logits_out, int out_on_device) {
     return guard([&] {
         if (!emb) fail(QT_EINVAL, "embedding width mismatch");
-        e->decode(emb, emb_on_device, logits_out, out_on_device);
+        e->decode(emb, emb_on_device, 0, logits_out, out_on_device);
+    });
+}
+
+int qt_engine_decode_f64(qt_engine* e, const double* emb, int emb_on_device, float* logits_out, int out_on_device) {
+    return guard([&] {
+        if (!emb) fail(QT_EINVAL, "embedding width mismatch");
+        e->decode(emb, emb_on_device, 1, logits_out, out_on_device);
     });
 }
 

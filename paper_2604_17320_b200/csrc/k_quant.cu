@@ -268,6 +268,25 @@ __global__ void k_weight_pack(const float* __restrict__ w, int K, int N, const d
     if (wd == 0) scales[dst] = s;
 }
 
+// Pre-quantized weights (a QuantEnv's int8 codes, GroupAxis::PerColumn, reference
+// orientation K x N row-major) into the tiled int4 layout, scales copied per row.
+__global__ void k_codes_pack(const int8_t* __restrict__ src, int K, int N, const double* __restrict__ s_in,
+                             int row_mul, int row_add, uint8_t* __restrict__ codes, int ldc,
+                             double* __restrict__ scales) {
+    const int n = blockIdx.x * blockDim.x + threadIdx.x;
+    const int wd = blockIdx.y;
+    if (n >= N) return;
+    int c[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        int k = wd * 8 + j;
+        c[j] = k < K ? (int)src[(size_t)k * N + n] : 0;
+    }
+    const int dst = n * row_mul + row_add;
+    *reinterpret_cast<uint32_t*>(codes + w4t_offset(dst, wd * 4, ldc)) = pack8(c);
+    if (wd == 0) scales[dst] = s_in[n];
+}
+
 __global__ void k_f32_to_f64(const float* __restrict__ a, double* __restrict__ b, long long n) {
     pdl_launch_dependents();
     pdl_wait();
@@ -329,6 +348,14 @@ int qt_launch_token_metrics(const double* x, int D, const int* seq_off, const in
     if (vmax <= 0 || B <= 0) return 0;
     const int qmax = res_bits > 0 ? (1 << (res_bits - 1)) - 1 : 7;
     k_token_metrics<<<dim3(vmax, B), 256, 0, st>>>(x, D, seq_off, vis, vstride, qmax, res_bits > 0, mag, res);
+    return (int)cudaGetLastError();
+}
+
+int qt_launch_codes_pack(const int8_t* src, int K, int N, const double* s_in, int row_mul, int row_add,
+                         uint8_t* codes, int ldc, double* scales, cudaStream_t st) {
+    const int words = (K + 7) / 8;
+    k_codes_pack<<<dim3((N + 127) / 128, words), 128, 0, st>>>(src, K, N, s_in, row_mul, row_add, codes, ldc,
+                                                                scales);
     return (int)cudaGetLastError();
 }
 

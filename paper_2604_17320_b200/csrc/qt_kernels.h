@@ -27,6 +27,8 @@ int qt_launch_token_metrics(const double* x, int D, const int* seq_off, const in
                             int vstride, int res_bits, double* mag, double* res, cudaStream_t st);
 int qt_launch_weight_quant(const float* w, int K, int N, int bits, int row_mul, int row_add, uint8_t* codes,
                            int ldc, double* scales, double* colmax_scratch, cudaStream_t st);
+int qt_launch_codes_pack(const int8_t* src, int K, int N, const double* s_in, int row_mul, int row_add,
+                         uint8_t* codes, int ldc, double* scales, cudaStream_t st);
 // out: double* for QT_EPI_RESADD (the fp64 residual stream), float* otherwise
 int qt_launch_w4a4_mma(int epi, const uint8_t* A, int lda, const double* sa, const uint8_t* W, int ldw,
                        const double* sw, int M, int N, int K, void* out, int ldo, int* acc_dbg, cudaStream_t st);
