@@ -119,6 +119,11 @@ int qt_engine_decode_f64(qt_engine* e, const double* emb, int emb_on_device, flo
 int qt_engine_layout(qt_engine* e, int seq, int* visual, int* text, int* positions, int cap);
 int qt_engine_n_prunes(qt_engine* e, int seq);
 int qt_engine_prune(qt_engine* e, int seq, int i, int* layer, int* budget, int* positions, int cap, int* count);
+/* QUOTA scores of the last prefill at candidate layer `layer` for sequence
+ * `seq` (fuse_scores output, selector.cpp:86-104, and the four
+ * robust-normalised metrics mag/inter/intra/res, [4][n]); *n = visual tokens
+ * scored.  Null buffers: only *n. */
+int qt_engine_scores(qt_engine* e, int layer, int seq, double* fused, double* norm4, int cap, int* n);
 int qt_engine_kv(qt_engine* e, int layer, int seq, int kv_head, int which, int8_t* codes, float* scales,
                  int* rows, int cap_rows);
 /* device pointers for in-place timing / inspection */

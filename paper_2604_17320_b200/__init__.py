@@ -87,6 +87,7 @@ def lib():
         L.qt_kv_quant_append_i4.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp, vp, vp,
                                             C.c_int, vp, C.c_int64, vp, vp]
         L.qt_rope_table.argtypes = [C.c_int, C.c_int, dp]
+        L.qt_engine_scores.argtypes = [vp, C.c_int, C.c_int, dp, dp, C.c_int, ip]
         L.qt_quota_topk.argtypes = [vp, C.c_int, C.c_int, vp, vp, dp, vp, vp, vp, vp]
         _lib = L
     return _lib
@@ -266,6 +267,16 @@ class Engine:
         check(lib().qt_engine_kv(self.h, layer, seq, head, which, codes.ctypes.data_as(C.c_void_p),
                                  scales.ctypes.data_as(C.POINTER(C.c_float)), C.byref(rows), n))
         return codes, scales
+
+    def scores(self, layer, seq):
+        """(fused [n], normalised metrics [4 x n]) of the selection at `layer` in the last prefill."""
+        n = C.c_int()
+        check(lib().qt_engine_scores(self.h, layer, seq, None, None, 0, C.byref(n)))
+        f = np.empty(n.value)
+        m = np.empty((4, n.value))
+        check(lib().qt_engine_scores(self.h, layer, seq, f.ctypes.data_as(C.POINTER(C.c_double)),
+                                     m.ctypes.data_as(C.POINTER(C.c_double)), n.value, C.byref(n)))
+        return f, m
 
     PROFILE_CLASSES = ("gemm", "attention", "quant", "kv", "select", "other")
 

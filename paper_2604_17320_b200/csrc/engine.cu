@@ -24,6 +24,7 @@
 #include "../../include/quota_b200.h"
 #include "qt_common.cuh"
 #include "qt_kernels.h"
+#include "qt_decode_mk.h"
 
 namespace {
 
@@ -212,6 +213,10 @@ struct qt_engine {
     int* keep_src = nullptr;
     int* keep_local = nullptr;
     int* kept_pos = nullptr;
+    double* sc_fused = nullptr;  // [L][mb][vstride] fused scores per prune event (parity readback)
+    double* sc_norm = nullptr;   // [L][mb][4][vstride] robust-normalised metrics
+    std::vector<int> ev_layers;               // candidate layers that ran selection, in order
+    std::vector<std::vector<int>> ev_vis;     // visual count entering each event, per seq
     double* rope = nullptr;
     double* wscratch = nullptr;
     float* wstage = nullptr;
@@ -262,6 +267,22 @@ struct qt_engine {
     }
     std::vector<int> h_next;
 
+    // persistent decode kernel (k_decode_mk.cu) for B <= 8
+    qt::MkLayer* mk_layers = nullptr;
+    int* mk_acc = nullptr;
+    int mk_acc_off[5] = {0, 0, 0, 0, 0};
+    int mk_acc_ld[5] = {0, 0, 0, 0, 0};
+    uint8_t* mk_codes = nullptr;
+    double* mk_sa = nullptr;
+    float* mk_attn = nullptr;
+    unsigned* mk_sync = nullptr;
+    double* mk_act = nullptr;
+    int mk_grid = 0, mk_smem = 0, mk_nslot = 0, mk_a_ld = 0, mk_acc_rows = 0;
+    bool mk_possible = false;
+    unsigned long long* mk_trace = nullptr;
+    // opt-in (QT_DECODE_MK=1): measured slower than the graph path at B = 8
+    bool use_mk = std::getenv("QT_DECODE_MK") && std::atoi(std::getenv("QT_DECODE_MK")) == 1;
+
     ~qt_engine() {
         cudaStreamSynchronize(st ? st : 0);
         if (graph) cudaGraphExecDestroy(graph);
@@ -275,8 +296,9 @@ struct qt_engine {
         f(x[0]); f(x[1]); f(pos[0]); f(pos[1]); f(qkv); f(attn); f(mid); f(codes); f(ascale); f(logits); f(ml);
         f(tok_seq); f(tok_row); f(seq_off); f(seq_vis); f(seq_txt); f(seq_len);
         f(mag); f(res); f(inter); f(intra); f(w4); f(budget); f(new_off); f(new_len); f(keep_src); f(keep_local);
-        f(kept_pos); f(rope); f(wscratch); f(wstage); f(pool); f(pt); f(kv_len); f(next_pos); f(dec_seq);
+        f(kept_pos); f(sc_fused); f(sc_norm); f(rope); f(wscratch); f(wstage); f(pool); f(pt); f(kv_len); f(next_pos); f(dec_seq);
         f(xd); f(xd_in); f(dlogits); f(part_ml); f(part_o);
+        f(mk_trace); f(mk_layers); f(mk_acc); f(mk_codes); f(mk_sa); f(mk_attn); f(mk_sync); f(mk_act);
         if (pin) cudaFreeHost(pin);
         if (own_stream) cudaStreamDestroy(own_stream);
     }
@@ -377,6 +399,8 @@ struct qt_engine {
         keep_src = dalloc<int>(T);
         keep_local = dalloc<int>((size_t)mb * vstride);
         kept_pos = dalloc<int>((size_t)L * mb * vstride);
+        sc_fused = dalloc<double>((size_t)L * mb * vstride);
+        sc_norm = dalloc<double>((size_t)L * mb * 4 * vstride);
         wscratch = dalloc<double>(std::max({n_qkv_pad, n_gu_pad, nd_pad, kff_pad}) + 64);
 
         // RoPE table with the reference's own libm (model.cpp:156-168)
@@ -398,9 +422,115 @@ struct qt_engine {
         dec_splits = max_pages;
         part_ml = dalloc<float>((size_t)mb * H * dec_splits * 2);
         part_o = dalloc<float>((size_t)mb * H * dec_splits * dh);
+        mk_init();
         pin_cap = (size_t)64 << 20;
         pin_cap += (size_t)mt * (sizeof(int) * 8);
         ck(cudaMallocHost(&pin, pin_cap), "cudaMallocHost");
+    }
+
+    // persistent decode kernel: device layer table, accumulators, smem plan
+    void mk_init() {
+        int dev = 0, sms = 0, smem_max = 0;
+        ck(cudaGetDevice(&dev), "device");
+        ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "sm count");
+        ck(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev), "smem");
+        mk_grid = sms;
+        const int Ns[5] = {n_qkv, d, n_gu, d, d};
+        const int Ks[5] = {kd_pad, kd_pad, kd_pad, kff_pad, kd_pad};
+        const int lds[5] = {n_qkv_pad, nd_pad, n_gu_pad, nd_pad, nd_pad};
+        int off = 0;
+        mk_acc_rows = 0;
+        for (int i = 0; i < 5; ++i) {
+            mk_acc_off[i] = off;
+            mk_acc_ld[i] = lds[i];
+            off += 8 * lds[i];
+            const long long rb = (Ns[i] + 15) / 16, kt = Ks[i] / 128, T = rb * kt;
+            const long long per = (T + mk_grid - 1) / mk_grid;
+            mk_acc_rows = std::max(mk_acc_rows, (int)((per + kt - 1) / kt + 2));
+        }
+        mk_acc = dalloc<int>(off);
+        ck(cudaMemset(mk_acc, 0, (size_t)off * sizeof(int)), "mk acc");
+        mk_codes = dalloc<uint8_t>((size_t)16 * std::max(kd_pad, kff_pad) / 2);
+        ck(cudaMemset(mk_codes, 0, (size_t)16 * std::max(kd_pad, kff_pad) / 2), "mk codes");
+        mk_sa = dalloc<double>(16);
+        mk_attn = dalloc<float>((size_t)8 * d);
+        mk_sync = dalloc<unsigned>(256);
+        mk_act = dalloc<double>(4 * L + 1);
+        ck(cudaMemset(mk_act, 0, (4 * L + 1) * sizeof(double)), "mk act");
+        const int fixed = qt_decode_mk_smem(std::max(kd_pad, kff_pad), mk_acc_rows, 0, &mk_a_ld);
+        mk_nslot = (smem_max - fixed - 1024) / (8192 + 16);
+        if (const char* ns = std::getenv("QT_MK_NSLOT")) mk_nslot = std::min(mk_nslot, std::atoi(ns));  // debug
+        mk_smem = qt_decode_mk_smem(std::max(kd_pad, kff_pad), mk_acc_rows, mk_nslot, &mk_a_ld);
+        std::vector<qt::MkLayer> tab(L);
+        for (int l = 0; l < L; ++l) {
+            qt::MkLayer& m = tab[l];
+            m.w[0] = lw[l].qkv; m.w[1] = lw[l].o; m.w[2] = lw[l].gu; m.w[3] = lw[l].down;
+            m.s[0] = lw[l].s_qkv; m.s[1] = lw[l].s_o; m.s[2] = lw[l].s_gu; m.s[3] = lw[l].s_down;
+            m.rows_pad[0] = n_qkv_pad; m.rows_pad[1] = nd_pad; m.rows_pad[2] = n_gu_pad; m.rows_pad[3] = nd_pad;
+            m.g1 = lw[l].g1;
+            m.g2 = lw[l].g2;
+            m.pt = pt + (size_t)l * max_batch * max_pages;
+            m.kv_len = kv_len + (size_t)l * max_batch;
+        }
+        mk_layers = dalloc<qt::MkLayer>(L);
+        ck(cudaMemcpy(mk_layers, tab.data(), L * sizeof(qt::MkLayer), cudaMemcpyHostToDevice), "mk layers");
+        // staging rows of the owner phases live in the activation-row region (8 * a_ld bytes)
+        mk_possible = mk_nslot >= 4 && (dh == 64 || dh == 128) && H <= 64 && 8 * mk_a_ld >= 8 * d &&
+                      8 * mk_a_ld >= 4 * dff && B_MAX_MK >= 1;
+    }
+
+    static constexpr int B_MAX_MK = 8;
+    bool mk_usable() const { return use_mk && mk_possible && B >= 1 && B <= 8; }
+
+    void decode_mk() {
+        qt::MkParams p{};
+        p.layers = mk_layers;
+        p.L = L; p.d = d; p.H = H; p.Hkv = Hkv; p.dh = dh; p.dff = dff; p.mlp = cfg.mlp; p.act_mode = cfg.act_mode;
+        p.B = B;
+        p.N[0] = n_qkv; p.N[1] = d; p.N[2] = n_gu; p.N[3] = d;
+        p.Kp[0] = kd_pad; p.Kp[1] = kd_pad; p.Kp[2] = kd_pad; p.Kp[3] = kff_pad;
+        p.head = head; p.s_head = s_head; p.head_rows_pad = nd_pad; p.gf = gf;
+        p.act = mk_act;
+        p.x = xd;
+        for (int i = 0; i < 5; ++i) {
+            p.acc[i] = mk_acc + mk_acc_off[i];
+            p.acc_ld[i] = mk_acc_ld[i];
+        }
+        p.codes = mk_codes; p.sa = mk_sa; p.attn = mk_attn;
+        p.pool = pool; p.page_bytes = page_bytes; p.max_pages = max_pages;
+        p.rope = reinterpret_cast<const double2*>(rope);
+        p.next_pos = next_pos;
+        p.logits = dlogits;
+        p.sync = mk_sync;
+        p.nslot = mk_nslot; p.a_ld = mk_a_ld; p.acc_rows = mk_acc_rows;
+        static const char* trace_path = std::getenv("QT_MK_TRACE");  // debug: per-phase timestamps
+        const size_t tn = (size_t)mk_grid * (L + 1) * 32;
+        if (trace_path && !mk_trace) {
+            mk_trace = dalloc<unsigned long long>(tn);
+        }
+        if (mk_trace) ck(cudaMemsetAsync(mk_trace, 0, tn * 8, st), "trace");
+        p.trace = mk_trace;
+        ck(cudaMemsetAsync(mk_sync, 0, 256 * sizeof(unsigned), st), "mk sync reset");
+        pb(P_GEMM);
+        ckl(qt_launch_decode_mk(&p, dh, mk_grid, mk_smem, st), "decode megakernel");
+        if (mk_trace) {
+            std::vector<unsigned long long> h(tn);
+            ck(cudaMemcpyAsync(h.data(), mk_trace, tn * 8, cudaMemcpyDeviceToHost, st), "trace");
+            ck(cudaStreamSynchronize(st), "trace");
+            if (FILE* fo = std::fopen(trace_path, "wb")) {
+                std::fwrite(h.data(), 8, tn, fo);
+                std::fclose(fo);
+            }
+        }
+        double wbytes = (double)L * ((double)n_qkv * kd_pad / 2 + (double)d * kd_pad / 2 + (double)n_gu * kd_pad / 2 +
+                                     (double)d * kff_pad / 2 + 8.0 * (n_qkv + d + n_gu + d)) +
+                        (double)d * kd_pad / 2 + 8.0 * d;
+        double kvb = 0;
+        for (int v : h_kvlen) kvb += (double)(v + 1) * Hkv * 2 * (dh / 2 + 4);
+        const double flops = 2.0 * B * ((double)L * ((double)n_qkv * kd_pad + (double)d * kd_pad +
+                                                     (double)n_gu * kd_pad + (double)d * kff_pad) +
+                                        (double)d * kd_pad);
+        pe(wbytes + kvb, flops);
     }
 
     void ensure_pool(int pages) {
@@ -685,9 +815,11 @@ struct qt_engine {
                 upload(new_off, noff);
                 upload(new_len, nlen);
                 int* kp_ev = kept_pos + (size_t)trace_layers.size() * max_batch * vstride;
+                const size_t evi = trace_layers.size();
                 ckl(qt_launch_select_topk(mag, res, inter, intra, H, vstride, seq_vis, seq_txt, budget, seq_off, new_off,
-                                          B, vmax, hw4.data(), keep_src, keep_local, vstride, pc, kp_ev, nullptr,
-                                          nullptr, nullptr, 0, st),
+                                          B, vmax, hw4.data(), keep_src, keep_local, vstride, pc, kp_ev,
+                                          sc_fused + evi * max_batch * vstride,
+                                          sc_norm + evi * max_batch * 4 * vstride, nullptr, 0, st),
                     "quota top-k");
                 double* xn = x[xc == x[0] ? 1 : 0];
                 int* pn = pos[pc == pos[0] ? 1 : 0];
@@ -719,6 +851,8 @@ struct qt_engine {
         norm_quant(xc, 1, d, gf, M, d, kd_pad, 4 * L);
         gemm(QT_EPI_STORE, head, nd_pad, s_head, M, d, kd_pad, logits, d);
         final_rows = M;
+        ev_layers = trace_layers;
+        ev_vis = ev_prev_v;
         if (logits_out)
             ck(cudaMemcpyAsync(logits_out, logits, (size_t)M * d * sizeof(float),
                                out_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st),
@@ -851,7 +985,9 @@ struct qt_engine {
             ckl(qt_launch_f32_to_f64(xd_in, xd, (long long)B * d, st), "embedding widen");
             pe((double)B * d * 12);
         }
-        if (g_nograph || profiling) {
+        if (mk_usable()) {
+            decode_mk();  // one persistent kernel for the whole step
+        } else if (g_nograph || profiling) {
             decode_body();  // eager launches so every kernel gets its own events
         } else if (!graph_ok) {
             if (graph) cudaGraphExecDestroy(graph);
@@ -873,7 +1009,7 @@ struct qt_engine {
             cudaGraphDestroy(g);
             graph_ok = true;
         }
-        if (!g_nograph && !profiling) ck(cudaGraphLaunch(graph, st), "graph launch");
+        if (!mk_usable() && !g_nograph && !profiling) ck(cudaGraphLaunch(graph, st), "graph launch");
         if (out)
             ck(cudaMemcpyAsync(out, dlogits, (size_t)B * d * sizeof(float),
                                out_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st),
@@ -1026,6 +1162,7 @@ int qt_engine_set_act_scales(qt_engine* e, const double* scales) {
         e->act.assign(scales, scales + 4 * e->L + 1);
         for (double s : e->act)
             if (!(s > 0.0) || !std::isfinite(s)) fail(QT_EINVAL, "activation scales must be positive");
+        ck(cudaMemcpy(e->mk_act, e->act.data(), e->act.size() * sizeof(double), cudaMemcpyHostToDevice), "act");
         e->act_set = true;
         e->graph_ok = false;
     });
@@ -1103,6 +1240,31 @@ int qt_engine_layout(qt_engine* e, int seq, int* visual, int* text, int* positio
         const auto& p = e->h_pos[seq];
         if ((int)p.size() > cap) fail(QT_EINVAL, "buffer too small");
         if (positions) std::copy(p.begin(), p.end(), positions);
+    });
+}
+
+int qt_engine_scores(qt_engine* e, int layer, int seq, double* fused, double* norm4, int cap, int* n) {
+    return guard([&] {
+        if (seq < 0 || seq >= e->B) fail(QT_ERANGE, "sequence out of range");
+        size_t ev = e->ev_layers.size();
+        for (size_t i = 0; i < e->ev_layers.size(); ++i)
+            if (e->ev_layers[i] == layer) ev = i;
+        if (ev == e->ev_layers.size()) fail(QT_ERANGE, "no selection ran at this layer");
+        const int V = e->ev_vis[ev][seq];
+        *n = V;
+        if (!fused && !norm4) return;
+        if (V > cap) fail(QT_EINVAL, "buffer too small");
+        ck(cudaStreamSynchronize(e->st), "sync");
+        const size_t vs = e->vstride;
+        if (fused)
+            ck(cudaMemcpy(fused, e->sc_fused + (ev * e->max_batch + seq) * vs, V * sizeof(double),
+                          cudaMemcpyDeviceToHost),
+               "scores");
+        if (norm4)
+            for (int m = 0; m < 4; ++m)
+                ck(cudaMemcpy(norm4 + (size_t)m * V, e->sc_norm + ((ev * e->max_batch + seq) * 4 + m) * vs,
+                              V * sizeof(double), cudaMemcpyDeviceToHost),
+                   "scores");
     });
 }
 

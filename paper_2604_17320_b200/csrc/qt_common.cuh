@@ -65,11 +65,21 @@ QT_DEV int q_code(double x, double s, int qmax) {
     return (int)q;
 }
 
-// Same code as q_code(x, s) without a per-element fp64 division: x * (1/s)
-// differs from the correctly rounded x / s by at most ~2 ulp, which can only
-// change rint() when the quotient sits within ~1e-15 of a .5 tie -- those
-// elements take the exact division.
+// Same code as q_code(x, s) (the reference's fp64 rint(x / s)), computed in
+// fp32 whenever that is provably the same decision: the fp32 quotient is
+// within ~3 ulp (< 1e-5 absolute for |q| < 16) of the exact one, so unless it
+// lies within 1e-4 of a .5 tie, rint() of both agrees; |q| >= 8 clamps either
+// way.  Near-ties take the fp64 path: x * (1/s), and the correctly rounded
+// x / s when even that sits within 1e-9 of the tie.
 QT_DEV int q_code_r(double x, double s, double inv_s, int qmax) {
+    const float qf = (float)x * (float)inv_s;
+    const float af = fabsf(qf);
+    if (af >= (float)qmax + 1.0f) return qf > 0.f ? qmax : -qmax;
+    const float ff = af - floorf(af);
+    if (fabsf(ff - 0.5f) > 1e-4f) {
+        const int c = (int)rintf(qf);
+        return c > qmax ? qmax : (c < -qmax ? -qmax : c);
+    }
     double q = x * inv_s;
     const double f = q - floor(q);
     if (fabs(f - 0.5) < 1e-9) q = x / s;
