@@ -279,6 +279,10 @@ struct qt_engine {
     double* mk_act = nullptr;
     int mk_grid = 0, mk_smem = 0, mk_nslot = 0, mk_a_ld = 0, mk_acc_rows = 0;
     bool mk_possible = false;
+    unsigned* seq_cnt = nullptr;  // per-sequence arrival counters of the fused decode attention block
+    // opt-in (QT_ATTN_FUSED=1): one kernel for RoPE + KV append + attention + attn_out quant; measured
+    // no faster than the three-kernel PDL chain at B = 8
+    bool fused_attn = std::getenv("QT_ATTN_FUSED") && std::atoi(std::getenv("QT_ATTN_FUSED")) == 1;
     unsigned long long* mk_trace = nullptr;
     // opt-in (QT_DECODE_MK=1): measured slower than the graph path at B = 8
     bool use_mk = std::getenv("QT_DECODE_MK") && std::atoi(std::getenv("QT_DECODE_MK")) == 1;
@@ -298,7 +302,7 @@ struct qt_engine {
         f(mag); f(res); f(inter); f(intra); f(w4); f(budget); f(new_off); f(new_len); f(keep_src); f(keep_local);
         f(kept_pos); f(sc_fused); f(sc_norm); f(rope); f(wscratch); f(wstage); f(pool); f(pt); f(kv_len); f(next_pos); f(dec_seq);
         f(xd); f(xd_in); f(dlogits); f(part_ml); f(part_o);
-        f(mk_trace); f(mk_layers); f(mk_acc); f(mk_codes); f(mk_sa); f(mk_attn); f(mk_sync); f(mk_act);
+        f(seq_cnt); f(mk_trace); f(mk_layers); f(mk_acc); f(mk_codes); f(mk_sa); f(mk_attn); f(mk_sync); f(mk_act);
         if (pin) cudaFreeHost(pin);
         if (own_stream) cudaStreamDestroy(own_stream);
     }
@@ -422,6 +426,7 @@ struct qt_engine {
         dec_splits = max_pages;
         part_ml = dalloc<float>((size_t)mb * H * dec_splits * 2);
         part_o = dalloc<float>((size_t)mb * H * dec_splits * dh);
+        seq_cnt = dalloc<unsigned>(mb);
         mk_init();
         pin_cap = (size_t)64 << 20;
         pin_cap += (size_t)mt * (sizeof(int) * 8);
@@ -929,22 +934,34 @@ struct qt_engine {
             int* lenl = kv_len + (size_t)l * max_batch;
             if (!(g_skip & 4)) norm_quant(xcur, 1, d, w.g1, B, d, kd_pad, 4 * l + 0);
             if (!(g_skip & 1)) gemm(QT_EPI_STORE, w.qkv, n_qkv_pad, w.s_qkv, B, n_qkv, kd_pad, qkv, n_qkv);
-            pb(P_KV);
-            if (!(g_skip & 8)) ckl(qt_launch_rope_kv_append(qkv, n_qkv, B, H, Hkv, dh, next_pos, dec_seq, lenl, rope, ptl, max_pages,
-                                         pool, page_bytes, 4, nullptr, st),
-                "decode kv append");
-            pe((double)B * n_qkv * 8 + (double)B * Hkv * 2 * (dh / 2 + 4));
-            pb(P_ATTN);
-            // decode attention over int4 pages + split merge fused with the attn_out quantizer
-            if (!(g_skip & 2))
-                ckl(qt_launch_attn_decode(qkv, n_qkv, H, Hkv, dh, lenl, 1, B, pool, page_bytes, ptl, max_pages,
-                                          dec_splits, part_ml, part_o, nullptr, d, codes, codes_rows, ascale,
-                                          cfg.act_mode, cfg.act_mode == 0 ? act[4 * l + 1] : 0.0, kd_pad, 4, st),
-                    "decode attention");
-            {  // decode attention streams every cached K/V row of this layer once
+            if (fused_attn) {
+                // RoPE + K/V append + attention + attn_out quantizer in one kernel
+                pb(P_ATTN);
+                ckl(qt_launch_attn_dec_fused(qkv, n_qkv, H, Hkv, dh, next_pos, lenl, rope, ptl, max_pages, pool,
+                                             page_bytes, attn, d, seq_cnt, codes, codes_rows, ascale, cfg.act_mode,
+                                             cfg.act_mode == 0 ? act[4 * l + 1] : 0.0, kd_pad, 4, B, st),
+                    "decode attention block");
                 double rows = 0;
                 for (int b = 0; b < B; ++b) rows += h_kvlen[(size_t)l * B + b] + 1;
-                pe(rows * Hkv * 2 * (dh / 2 + 4) + (double)B * H * dh * 8);
+                pe(rows * Hkv * 2 * (dh / 2 + 4) + (double)B * n_qkv * 4 + (double)B * d * 8);
+            } else {
+                pb(P_KV);
+                if (!(g_skip & 8)) ckl(qt_launch_rope_kv_append(qkv, n_qkv, B, H, Hkv, dh, next_pos, dec_seq, lenl, rope, ptl, max_pages,
+                                             pool, page_bytes, 4, nullptr, st),
+                    "decode kv append");
+                pe((double)B * n_qkv * 8 + (double)B * Hkv * 2 * (dh / 2 + 4));
+                pb(P_ATTN);
+                // decode attention over int4 pages + split merge fused with the attn_out quantizer
+                if (!(g_skip & 2))
+                    ckl(qt_launch_attn_decode(qkv, n_qkv, H, Hkv, dh, lenl, 1, B, pool, page_bytes, ptl, max_pages,
+                                              dec_splits, part_ml, part_o, nullptr, d, codes, codes_rows, ascale,
+                                              cfg.act_mode, cfg.act_mode == 0 ? act[4 * l + 1] : 0.0, kd_pad, 4, st),
+                        "decode attention");
+                {  // decode attention streams every cached K/V row of this layer once
+                    double rows = 0;
+                    for (int b = 0; b < B; ++b) rows += h_kvlen[(size_t)l * B + b] + 1;
+                    pe(rows * Hkv * 2 * (dh / 2 + 4) + (double)B * H * dh * 8);
+                }
             }
             if (!(g_skip & 1)) gemm(QT_EPI_RESADD, w.o, nd_pad, w.s_o, B, d, kd_pad, xcur, d);
             if (!(g_skip & 4)) norm_quant(xcur, 1, d, w.g2, B, d, kd_pad, 4 * l + 2);

@@ -11,6 +11,8 @@
 // All quantizer arithmetic is fp64 (the reference's type), so an int4 code
 // equals the reference code for the same fp32 input; the fp32 scale handed to
 // the GEMM epilogue is the rounded fp64 scale.
+#include <cooperative_groups.h>
+
 #include "qt_common.cuh"
 #include "qt_kernels.h"
 
@@ -114,6 +116,91 @@ __global__ void __launch_bounds__(1024) k_norm_quant(const TX* __restrict__ x, i
         }
     }
     if (threadIdx.x == 0) scales[row] = s;
+}
+
+// K1 for few rows (decode): a cluster of CL CTAs per row, each owning a slice
+// of 8-element words in registers; the RMS sum and the row max are reduced
+// across the cluster through distributed shared memory in rank order (fixed,
+// deterministic).  Spreads one row over CL SMs so the row's loads run in
+// parallel instead of through one SM.
+template <typename TX, int CL, int G>
+__global__ void __launch_bounds__(128) k_norm_quant_cl(const TX* __restrict__ x, int ld_x,
+                                                      const float* __restrict__ gain, int M, int D, int d_pad,
+                                                      int qmax, int mode, double static_scale,
+                                                      uint8_t* __restrict__ codes, int ld_codes,
+                                                      double* __restrict__ scales) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    __shared__ double red[32];
+    __shared__ double part[2];
+    pdl_launch_dependents();
+    pdl_wait();
+    const int rank = (int)cluster.block_rank();
+    const int row = blockIdx.y;
+    const TX* xr = x + (size_t)row * ld_x;
+    const int n_words = d_pad / 8;
+    const int w0 = rank * n_words / CL, w1 = (rank + 1) * n_words / CL;
+    double v[G][8];
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+        const int w = w0 + threadIdx.x + j * 128;
+        if (w < w1 && w * 8 < D) {
+            load8<TX>(xr + w * 8, v[j]);
+        } else {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) v[j][e] = 0.0;
+        }
+    }
+    if (gain) {
+        double ss = 0.0;
+#pragma unroll
+        for (int j = 0; j < G; ++j)
+#pragma unroll
+            for (int e = 0; e < 8; ++e) ss += v[j][e] * v[j][e];
+        ss = block_sum(ss, red);
+        if (threadIdx.x == 0) part[0] = ss;
+        cluster.sync();
+        double tot = 0.0;
+        for (int r = 0; r < CL; ++r) tot += *cluster.map_shared_rank(&part[0], r);
+        const double inv = 1.0 / sqrt(tot / (double)D + kNormEps);
+#pragma unroll
+        for (int j = 0; j < G; ++j) {
+            const int w = w0 + threadIdx.x + j * 128;
+            if (w < w1 && w * 8 < D) {
+                float4 g0 = *reinterpret_cast<const float4*>(gain + w * 8);
+                float4 g1 = *reinterpret_cast<const float4*>(gain + w * 8 + 4);
+                const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+#pragma unroll
+                for (int e = 0; e < 8; ++e) v[j][e] = __dmul_rn(__dmul_rn(v[j][e], inv), (double)gg[e]);
+            }
+        }
+    }
+    double s = static_scale;
+    if (mode == 1) {
+        double mx = 0.0;
+#pragma unroll
+        for (int j = 0; j < G; ++j)
+#pragma unroll
+            for (int e = 0; e < 8; ++e) mx = fmax(mx, fabs(v[j][e]));
+        mx = block_max(mx, red);
+        if (threadIdx.x == 0) part[1] = mx;
+        cluster.sync();
+        double m = 0.0;
+        for (int r = 0; r < CL; ++r) m = fmax(m, *cluster.map_shared_rank(&part[1], r));
+        s = q_scale(m, qmax);
+    }
+    const double inv_s = 1.0 / s;
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+        const int w = w0 + threadIdx.x + j * 128;
+        if (w >= w1) continue;
+        int c[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) c[e] = w * 8 + e < D ? q_code_r(v[j][e], s, inv_s, qmax) : 0;
+        *reinterpret_cast<uint32_t*>(codes + w4t_offset(row, w * 4, ld_codes)) = pack8(c);
+    }
+    if (rank == 0 && threadIdx.x == 0) scales[row] = s;
+    cluster.sync();  // no CTA leaves while its shared partials may still be read
 }
 
 // ============================================================== K5
@@ -299,6 +386,26 @@ __global__ void k_f32_to_f64(const float* __restrict__ a, double* __restrict__ b
 // ---------------------------------------------------------------- launchers
 using namespace qt;
 
+template <typename TX, int CL, int G>
+static int launch_nq_cl(const TX* x, int ld_x, const float* gain, int M, int D, int d_pad, int qmax, int mode,
+                        double static_scale, uint8_t* codes, int ld_codes, double* scales, cudaStream_t st) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CL, M);
+    cfg.blockDim = dim3(128);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = getenv("QT_NOPDL") ? 1 : 2;
+    return (int)cudaLaunchKernelEx(&cfg, k_norm_quant_cl<TX, CL, G>, x, ld_x, gain, M, D, d_pad, qmax, mode,
+                                   static_scale, codes, ld_codes, scales);
+}
+
 extern "C" {
 
 int qt_launch_f32_to_f64(const float* a, double* b, long long n, cudaStream_t st) {
@@ -312,6 +419,21 @@ int qt_launch_norm_quant(const void* x, int x_is_f64, int ld_x, const float* gai
     if (M <= 0) return 0;
     if (D % 8 || d_pad % 8 || ld_x % 4) return -1;
     const int qmax = (1 << (bits - 1)) - 1;
+    // opt-in (QT_NQ_CLUSTER=1): rows split over an 8-CTA cluster; not faster at decode sizes
+    static const bool use_cl = getenv("QT_NQ_CLUSTER") && atoi(getenv("QT_NQ_CLUSTER")) == 1;
+    if (M <= 64 && !normed && use_cl && d_pad / 8 <= 8 * 128 * 2) {
+        // decode-sized: 8-CTA cluster per row, up to 2 words per thread
+        const int G = d_pad / 8 <= 8 * 128 ? 1 : 2;
+        if (x_is_f64)
+            return G == 1 ? launch_nq_cl<double, 8, 1>(static_cast<const double*>(x), ld_x, gain, M, D, d_pad, qmax,
+                                                        mode, static_scale, codes, ld_codes, scales, st)
+                          : launch_nq_cl<double, 8, 2>(static_cast<const double*>(x), ld_x, gain, M, D, d_pad, qmax,
+                                                        mode, static_scale, codes, ld_codes, scales, st);
+        return G == 1 ? launch_nq_cl<float, 8, 1>(static_cast<const float*>(x), ld_x, gain, M, D, d_pad, qmax, mode,
+                                                   static_scale, codes, ld_codes, scales, st)
+                      : launch_nq_cl<float, 8, 2>(static_cast<const float*>(x), ld_x, gain, M, D, d_pad, qmax, mode,
+                                                   static_scale, codes, ld_codes, scales, st);
+    }
     const int words = d_pad / 8;
     int threads = words <= 256 ? 256 : (words <= 512 ? 512 : 1024);
     const int G = (words + threads - 1) / threads;
