@@ -6,6 +6,14 @@
 
 namespace qt {
 
+// SiLU / SwiGLU of the fp64 GEMM outputs, evaluated in fp32: the result is an
+// fp32 tensor (the mlp_mid site input), and fp64 exp/div here made the
+// epilogue, not the tensor cores, the bottleneck of the gate|up GEMM.
+QT_DEV float silu_f32(double g) {
+    const float gf = (float)g;
+    return gf / (1.0f + expf(-gf));
+}
+
 // y = (acc / 256) * s_a[m] * s_w[n] in fp64 (scales are the reference's fp64
 // scales; the integer sum is exact), then the epilogue: store fp32, add into
 // the fp64 residual, SiLU, or SwiGLU over interleaved (gate, up) columns.
@@ -26,14 +34,14 @@ QT_DEV void epi_store(void* __restrict__ outv, int ldo, int m, int n, double y0,
     float* out = static_cast<float*>(outv);
     if (EPI == QT_EPI_SWIGLU) {
         // silu(g) * u (model.cpp:170-172 silu; SwiGLU is the R1 extension)
-        if (n < N) out[(size_t)m * ldo + n / 2] = (float)(y0 / (1.0 + exp(-y0)) * y1);
+        if (n < N) out[(size_t)m * ldo + n / 2] = silu_f32(y0) * (float)y1;
         return;
     }
     float* p = out + (size_t)m * ldo + n;
     float v0, v1;
     if (EPI == QT_EPI_SILU) {
-        v0 = (float)(y0 / (1.0 + exp(-y0)));
-        v1 = (float)(y1 / (1.0 + exp(-y1)));
+        v0 = silu_f32(y0);
+        v1 = silu_f32(y1);
     } else {
         v0 = (float)y0;
         v1 = (float)y1;
@@ -73,7 +81,7 @@ QT_DEV void epi_row32(void* __restrict__ outv, int ldo, int m, int n, const uint
             for (int u = 0; u < 4; ++u) {
                 const double g = (double)((int)r[e + 2 * u] >> 8) * (a_s * swt[e + 2 * u]);
                 const double up = (double)((int)r[e + 2 * u + 1] >> 8) * (a_s * swt[e + 2 * u + 1]);
-                v[u] = (float)(g / (1.0 + exp(-g)) * up);
+                v[u] = silu_f32(g) * (float)up;
             }
             p[e / 8] = make_float4(v[0], v[1], v[2], v[3]);
         }
@@ -86,7 +94,7 @@ QT_DEV void epi_row32(void* __restrict__ outv, int ldo, int m, int n, const uint
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const double y = (double)((int)r[e + u] >> 8) * (a_s * swt[e + u]);
-            v[u] = EPI == QT_EPI_SILU ? (float)(y / (1.0 + exp(-y))) : (float)y;
+            v[u] = EPI == QT_EPI_SILU ? silu_f32(y) : (float)y;
         }
         p[e / 4] = make_float4(v[0], v[1], v[2], v[3]);
     }
