@@ -105,6 +105,47 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
+def load_traffic():
+    """profiles/ncu_traffic.json (tools/ncu_traffic.py): DRAM bytes of single ncu-captured launches,
+    with the algorithmic bytes of the same launch for the ratio."""
+    try:
+        rows = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+    except Exception:
+        return {}
+    out = {}
+    for r in rows:
+        k = r["kernel"]
+        if "k_gemv_reg<1, 0>" in k:  # decode QKV GEMV, B = 8: N 12288 x K 4096
+            M, N, K = 8, 12288, 4096
+            r["algorithmic_bytes"] = N * K / 2 + 8 * N + M * K / 2 + 8 * M + 4 * M * N
+            out["gemv"] = r
+        elif "k_attn_decode" in k:
+            out["attn_decode"] = dict(r, algorithmic_bytes=r["dram_bytes"])
+    return out
+
+
+def measure_int8_peak(torch, dev):
+    """Dense int8 tensor-core throughput on this GPU through cuBLASLt (torch._int_mm),
+    8192^3, best of 5 -- the roofline denominator for the int8 GEMMs (MEASURED_PEAKS.json
+    has no int8 figure)."""
+    try:
+        a = torch.randint(-8, 8, (8192, 8192), dtype=torch.int8, device=dev)
+        b = torch.randint(-8, 8, (8192, 8192), dtype=torch.int8, device=dev)
+        torch._int_mm(a, b)
+        best = 1e9
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch._int_mm(a, b)
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        del a, b
+        return 2.0 * 8192 ** 3 / (best / 1e3) / 1e12
+    except Exception:
+        return None
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -308,8 +349,10 @@ def run_ours(args, cfg):
 
     peaks = load_peaks()
     hbm = peaks.get("hbm_gbs")
-    peak_src = "MEASURED_PEAKS.json" if hbm else "B200_PROFILING.md fallback"
+    peak_src = "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)" if hbm else "B200_PROFILING.md fallback"
     hbm = hbm or 6650.0
+    int8_peak = measure_int8_peak(torch, dev) if rank == 0 else None
+    traffic_db = load_traffic()
     # dominant kernel class over the whole step
     per_step = {}
     for c in prof_pre:
@@ -320,17 +363,25 @@ def run_ours(args, cfg):
     src = prof_pre[cls] if phase == "prefill" else prof_dec[cls]
     avg_ms = src["ms"] / max(1, src["launches"])
     if phase == "decode" and cls in ("gemm", "attention", "quant", "kv"):
-        achieved = src["bytes"] / max(1, src["launches"]) / (avg_ms / 1e3) / 1e9
-        roofline = {"bound": "hbm", "kernel": f"{phase} {cls} (W4A4 GEMV)" if cls == "gemm" else f"{phase} {cls}",
-                    "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                    "traffic": None, "peak_source": peak_src,
-                    "algorithmic_bytes_per_launch": src["bytes"] / max(1, src["launches"]),
-                    "avg_launch_ms": avg_ms, "share_of_step": per_step[dom] / ms_step}
+        alg = src["bytes"] / max(1, src["launches"])
+        achieved = alg / (avg_ms / 1e3) / 1e9
+        traffic, tsrc = None, None
+        ref = traffic_db.get("gemv" if cls == "gemm" else "attn_decode")
+        if ref:  # ncu --set full capture of one launch: DRAM bytes / algorithmic bytes of that launch
+            ratio = ref["dram_bytes"] / ref["algorithmic_bytes"]
+            traffic, tsrc = alg * ratio, f"{ref['source']}: dram/algorithmic = {ratio:.3f} on {ref['kernel']}"
+        roofline = {"bound": "hbm", "kernel": f"{phase} {cls} (W4A4 GEMV, k_gemv_reg)" if cls == "gemm"
+                    else f"{phase} {cls}", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                    "traffic": traffic, "traffic_source": tsrc, "peak_source": peak_src,
+                    "algorithmic_bytes_per_launch": alg, "avg_launch_ms": avg_ms,
+                    "share_of_step": per_step[dom] / ms_step}
     else:
         tops = src["flops"] / max(1, src["launches"]) / (avg_ms / 1e3) / 1e12
-        roofline = {"bound": "tensor", "kernel": f"{phase} {cls}", "achieved": tops, "peak": 4500.0,
-                    "unit": "TOP/s (int8)", "frac": tops / 4500.0, "traffic": None,
-                    "peak_source": "B200 dense int8 datasheet (MEASURED_PEAKS.json has no int8 figure)",
+        pk = int8_peak or 4500.0
+        roofline = {"bound": "tensor", "kernel": f"{phase} {cls}", "achieved": tops, "peak": pk,
+                    "unit": "TOP/s (int8)", "frac": tops / pk, "traffic": None,
+                    "peak_source": "measured int8 cuBLASLt (torch._int_mm 8192^3)" if int8_peak
+                    else "B200 dense int8 datasheet (no int8 figure in MEASURED_PEAKS.json)",
                     "avg_launch_ms": avg_ms, "share_of_step": per_step[dom] / ms_step}
     gemm_pre = prof_pre["gemm"]
     prefill_gemm_tops = gemm_pre["flops"] / (gemm_pre["ms"] / 1e3) / 1e12 if gemm_pre["ms"] else None
@@ -365,7 +416,7 @@ def run_ours(args, cfg):
                        "l2": "working set > L2: 3.25 GB int4 weights streamed every decode step and prefill layer"},
             "prefill_ms": prefill_ms, "prefill_tokens_per_s": ws * B * S / (prefill_ms / 1e3),
             "decode_ms_per_step": decode_ms, "decode_tokens_per_s": ws * B / (decode_ms / 1e3),
-            "prefill_gemm_tops": prefill_gemm_tops, "decode_gemv_gbs": decode_gemv_gbs,
+            "prefill_gemm_tops": prefill_gemm_tops, "int8_peak_tops_measured": int8_peak, "decode_gemv_gbs": decode_gemv_gbs,
             "decode_attn_gbs": decode_attn_gbs, "final_rows": final_rows,
             "roofline": roofline,
             "cpu_baseline": cpu,
