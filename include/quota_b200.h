@@ -85,6 +85,13 @@ int qt_engine_load_head(qt_engine* e, const float* w_head, const float* final_ga
 int qt_engine_load_layer_codes(qt_engine* e, int layer, const int8_t* const* codes, const double* const* scales,
                                const double* g1, const double* g2);
 int qt_engine_load_head_codes(qt_engine* e, const int8_t* codes, const double* scales, const double* final_gain);
+/* Packed-int4 weight file (the reference has no checkpoint
+ * format -- it regenerates weights from the seed, model.cpp:113-135): the
+ * engine's device layout byte for byte (tiled int4 codes, fp64 per-channel
+ * scales, gains, static act scales if set) behind a header that must match the
+ * engine's qt_config.  Loading is a straight copy, no quantization. */
+int qt_engine_save(qt_engine* e, const char* path);
+int qt_engine_load(qt_engine* e, const char* path);
 /* ActScales (model.hpp:114-133): 4 * n_layers + 1 static per-tensor scales,
  * order (attn_in, attn_out, mlp_in, mlp_mid) per layer, then head_in. */
 int qt_engine_set_act_scales(qt_engine* e, const double* scales);

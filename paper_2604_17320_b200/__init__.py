@@ -87,6 +87,8 @@ def lib():
         L.qt_kv_quant_append_i4.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp, vp, vp,
                                             C.c_int, vp, C.c_int64, vp, vp]
         L.qt_rope_table.argtypes = [C.c_int, C.c_int, dp]
+        L.qt_engine_save.argtypes = [vp, C.c_char_p]
+        L.qt_engine_load.argtypes = [vp, C.c_char_p]
         L.qt_engine_scores.argtypes = [vp, C.c_int, C.c_int, dp, dp, C.c_int, ip]
         L.qt_quota_topk.argtypes = [vp, C.c_int, C.c_int, vp, vp, dp, vp, vp, vp, vp]
         _lib = L
@@ -202,6 +204,14 @@ class Engine:
             self.load_layer(l, lw["wq"], lw["wk"], lw["wv"], lw["wo"], lw["w1"], lw["w2"], lw.get("w3"),
                             lw.get("g1"), lw.get("g2"))
         self.load_head(w.head, w.gf)
+
+    def save(self, path):
+        """Write the packed-int4 weight file (device layout, include/quota_b200.h)."""
+        check(lib().qt_engine_save(self.h, os.fsencode(path)))
+
+    def load(self, path):
+        """Load a packed-int4 weight file written by save() for the same configuration."""
+        check(lib().qt_engine_load(self.h, os.fsencode(path)))
 
     def set_act_scales(self, scales):
         a = np.ascontiguousarray(scales, dtype=np.float64)

@@ -695,6 +695,10 @@ struct qt_engine {
                 }
             }
             vis_at[b][L] = v;
+            // the reference hook scores every candidate layer it reaches; an empty visual
+            // range makes robust_normalize throw (selector.cpp:70-71) -- checked before any launch
+            for (int l = 0; l < L; ++l)
+                if (kbud[b][l] >= 0 && vis_at[b][l] == 0) fail(QT_EINVAL, "empty sample");
         }
         // KV pages: capacity per (layer, seq) = tokens entering the layer + decode steps
         std::vector<int> hpt((size_t)L * max_batch * max_pages, 0);
@@ -782,6 +786,7 @@ struct qt_engine {
                 if (kbud[b][l] >= 0 && kbud[b][l] < cur_v[b]) prune_any = true;
             }
             const bool cand = have_recipe && std::any_of(kbud.begin(), kbud.end(), [l](const std::vector<int>& k) { return k[l] >= 0; });
+
             pb(P_ATTN);
             ckl(qt_launch_attn_prefill(qkv, n_qkv, H, Hkv, dh, seq_off, seq_vis, seq_len, B, smax, pool, page_bytes,
                                        ptl, max_pages, attn, d, prune_any ? ml : nullptr, st),
@@ -1053,6 +1058,51 @@ __global__ void k_bump(int* kv_len, int n, int* next_pos, int B) {
 }
 }  // namespace qt
 
+// ---- packed-weight file: the device layout, byte for byte -----
+// header: magic "QTW4B200", u32 version, qt_config, the padded geometry, a flag for
+// static activation scales (+ 4L+1 doubles), then per layer the tiled int4 codes
+// and fp64 scales of qkv / o / gate|up / down and the fp32 gains, then the head.
+namespace {
+struct WFileHdr {
+    char magic[8];
+    uint32_t version;
+    qt_config cfg;
+    int32_t geom[6];  // n_qkv_pad, kd_pad, nd_pad, n_gu_pad, kff_pad, L
+    int32_t has_act;
+};
+
+template <class F>
+void for_each_blob(qt_engine* e, F&& f) {
+    for (int l = 0; l < e->L; ++l) {
+        LayerW& w = e->lw[l];
+        f(w.qkv, (size_t)e->n_qkv_pad * e->kd_pad / 2);
+        f(w.s_qkv, (size_t)e->n_qkv_pad * 8);
+        f(w.o, (size_t)e->nd_pad * e->kd_pad / 2);
+        f(w.s_o, (size_t)e->nd_pad * 8);
+        f(w.gu, (size_t)e->n_gu_pad * e->kd_pad / 2);
+        f(w.s_gu, (size_t)e->n_gu_pad * 8);
+        f(w.down, (size_t)e->nd_pad * e->kff_pad / 2);
+        f(w.s_down, (size_t)e->nd_pad * 8);
+        f(w.g1, (size_t)e->d * 4);
+        f(w.g2, (size_t)e->d * 4);
+    }
+    f(e->head, (size_t)e->nd_pad * e->kd_pad / 2);
+    f(e->s_head, (size_t)e->nd_pad * 8);
+    f(e->gf, (size_t)e->d * 4);
+}
+
+WFileHdr make_hdr(qt_engine* e) {
+    WFileHdr h{};
+    std::memcpy(h.magic, "QTW4B200", 8);
+    h.version = 1;
+    h.cfg = e->cfg;
+    const int g[6] = {e->n_qkv_pad, e->kd_pad, e->nd_pad, e->n_gu_pad, e->kff_pad, e->L};
+    std::memcpy(h.geom, g, sizeof(g));
+    h.has_act = e->act_set ? 1 : 0;
+    return h;
+}
+}  // namespace
+
 extern "C" {
 
 int qt_launch_kv_len_bump(int* kv_len, int n, int* next_pos, int B, cudaStream_t st) {
@@ -1163,6 +1213,60 @@ int qt_engine_load_head_codes(qt_engine* e, const int8_t* codes, const double* s
     });
 }
 
+int qt_engine_save(qt_engine* e, const char* path) {
+    return guard([&] {
+        for (auto& l : e->lw)
+            if (!l.loaded) fail(QT_EINVAL, "model weights not loaded");
+        if (!e->head_loaded) fail(QT_EINVAL, "model head not loaded");
+        FILE* f = std::fopen(path, "wb");
+        if (!f) fail(QT_ERUNTIME, std::string("cannot open ") + path);
+        std::unique_ptr<FILE, int (*)(FILE*)> guard_f(f, std::fclose);
+        WFileHdr h = make_hdr(e);
+        if (std::fwrite(&h, sizeof(h), 1, f) != 1) fail(QT_ERUNTIME, "write failed");
+        if (h.has_act && std::fwrite(e->act.data(), sizeof(double), e->act.size(), f) != e->act.size())
+            fail(QT_ERUNTIME, "write failed");
+        ck(cudaStreamSynchronize(e->st), "sync");
+        std::vector<char> buf;
+        for_each_blob(e, [&](void* dev, size_t bytes) {
+            buf.resize(bytes);
+            ck(cudaMemcpy(buf.data(), dev, bytes, cudaMemcpyDeviceToHost), "weights readback");
+            if (std::fwrite(buf.data(), 1, bytes, f) != bytes) fail(QT_ERUNTIME, "write failed");
+        });
+    });
+}
+
+int qt_engine_load(qt_engine* e, const char* path) {
+    return guard([&] {
+        FILE* f = std::fopen(path, "rb");
+        if (!f) fail(QT_EINVAL, std::string("cannot open ") + path);
+        std::unique_ptr<FILE, int (*)(FILE*)> guard_f(f, std::fclose);
+        WFileHdr h{}, mine = make_hdr(e);
+        if (std::fread(&h, sizeof(h), 1, f) != 1 || std::memcmp(h.magic, "QTW4B200", 8) != 0 || h.version != 1)
+            fail(QT_EINVAL, "not a quota_b200 weight file");
+        if (std::memcmp(&h.cfg, &mine.cfg, sizeof(qt_config)) != 0 || std::memcmp(h.geom, mine.geom, sizeof(h.geom)))
+            fail(QT_EINVAL, "weight file does not match the engine configuration");
+        if (h.has_act) {
+            std::vector<double> act(4 * e->L + 1);
+            if (std::fread(act.data(), sizeof(double), act.size(), f) != act.size()) fail(QT_EINVAL, "truncated file");
+            ck(cudaStreamSynchronize(e->st), "sync");
+            if (qt_engine_set_act_scales(e, act.data()) != 0) fail(QT_EINVAL, qt_last_error());
+        }
+        // stream through the pinned staging buffer
+        const size_t chunk = std::min<size_t>(e->pin_cap, (size_t)32 << 20);
+        ck(cudaStreamSynchronize(e->st), "sync");
+        for_each_blob(e, [&](void* dev, size_t bytes) {
+            for (size_t o = 0; o < bytes; o += chunk) {
+                const size_t n = std::min(chunk, bytes - o);
+                if (std::fread(e->pin, 1, n, f) != n) fail(QT_EINVAL, "truncated file");
+                ck(cudaMemcpy(static_cast<char*>(dev) + o, e->pin, n, cudaMemcpyHostToDevice), "weights upload");
+            }
+        });
+        for (auto& l : e->lw) l.loaded = true;
+        e->head_loaded = true;
+        e->graph_ok = false;
+    });
+}
+
 int qt_engine_load_head(qt_engine* e, const float* w_head, const float* final_gain, int on_device) {
     return guard([&] {
         if (!w_head) fail(QT_EINVAL, "null weight");
@@ -1206,7 +1310,9 @@ int qt_engine_set_recipe(qt_engine* e, int n, const int* layers, const double* k
             if (x < 0) fail(QT_EINVAL, "negative metric weight");
         if (std::fabs(w[0] + w[1] + w[2] + w[3] - 1.0) > 1e-6) fail(QT_EINVAL, "metric weights must sum to 1");  // selector.cpp:91-93
         if (v0 < 1) fail(QT_EINVAL, "v0 must be >= 1");
-        if (layers[n - 1] >= e->L) fail(QT_ERUNTIME, "recipe candidate layers do not fit the model");  // harness.cpp:86-88
+        // candidate layers >= n_layers are never reached, as with the reference hook
+        // (model.cpp:404-405 calls it for l < n_layers only); the harness-level check
+        // (harness.cpp:86-88) is the caller's
         if (res_bits == 0 || res_bits == 1 || res_bits > 8) fail(QT_EINVAL, "bits out of range [2,8]");
         e->recipe.layers.assign(layers, layers + n);
         e->recipe.keeps.assign(keeps, keeps + n);
