@@ -6,9 +6,10 @@
 
 namespace qt {
 
-// SiLU / SwiGLU of the fp64 GEMM outputs, evaluated in fp32: the result is an
-// fp32 tensor (the mlp_mid site input), and fp64 exp/div here made the
-// epilogue, not the tensor cores, the bottleneck of the gate|up GEMM.
+// SiLU / SwiGLU of the fp64 GEMM outputs, evaluated in fp32 in the tcgen05
+// prefill epilogue (epi_row32): the result is an fp32 tensor (the mlp_mid site
+// input), and fp64 exp/div there made the epilogue, not the tensor cores, the
+// bottleneck of the gate|up GEMM.  The row-wise epi_store (decode GEMV) keeps fp64.
 QT_DEV float silu_f32(double g) {
     const float gf = (float)g;
     return gf / (1.0f + expf(-gf));
@@ -34,14 +35,16 @@ QT_DEV void epi_store(void* __restrict__ outv, int ldo, int m, int n, double y0,
     float* out = static_cast<float*>(outv);
     if (EPI == QT_EPI_SWIGLU) {
         // silu(g) * u (model.cpp:170-172 silu; SwiGLU is the R1 extension)
-        if (n < N) out[(size_t)m * ldo + n / 2] = silu_f32(y0) * (float)y1;
+        // fp64 here (decode GEMV / small GEMMs: a handful of rows), so the fp32 result is the
+        // correctly rounded value of the reference's fp64 expression
+        if (n < N) out[(size_t)m * ldo + n / 2] = (float)(y0 / (1.0 + exp(-y0)) * y1);
         return;
     }
     float* p = out + (size_t)m * ldo + n;
     float v0, v1;
     if (EPI == QT_EPI_SILU) {
-        v0 = silu_f32(y0);
-        v1 = silu_f32(y1);
+        v0 = (float)(y0 / (1.0 + exp(-y0)));
+        v1 = (float)(y1 / (1.0 + exp(-y1)));
     } else {
         v0 = (float)y0;
         v1 = (float)y1;
