@@ -8,7 +8,7 @@ through 32 W4A4 layers with the QUOTA recipe (30 % visual retention from layer
 2: 576 -> 173), then 128 teacher-forced decode steps over the int4 cache,
 then the (N>1) gather of the final logits to rank 0.
 
-  value  = whole-job tokens/s = N * B * (S + D) / step time, inputs resident in HBM
+  value  = whole-job tokens/s = N * (prefill tokens + B * D) / step time, inputs resident in HBM
   e2e    = the same through the public API with pinned HOST buffers
            (embeddings H2D and logits D2H inside the timed region, every step)
 
@@ -43,6 +43,21 @@ CONFIGS = {
     "c2": dict(workload="LLaVA-1.5-7B-shaped W4A4 + QUOTA 30% visual retention from layer 2 (configs[1])",
                n_layers=32, d_model=4096, n_heads=32, n_kv_heads=32, d_head=128, d_ff=11008, mlp=1, act_mode=1,
                batch=8, visual=576, text=64, decode=128, layers=[2], keeps=[0.3], v0=576, outlier=0.01),
+    # BASELINE.json configs[2]: high-resolution prefix, multi-layer keep schedule
+    "c3": dict(workload="LLaVA-7B shape, 2880 visual (5 tiles x 576) + 128 text, keep [1, 1, 0.25, 0.2 from L8] "
+                        "(configs[2])",
+               n_layers=32, d_model=4096, n_heads=32, n_kv_heads=32, d_head=128, d_ff=11008, mlp=1, act_mode=1,
+               batch=4, visual=2880, text=128, decode=128, layers=[0, 1, 2, 8], keeps=[1.0, 1.0, 0.25, 0.2], v0=2880,
+               outlier=0.01),
+    # BASELINE.json configs[3]: Qwen2-VL shape, GQA, ragged visual lengths U[256, 1280] per sequence
+    "c4": dict(workload="Qwen2-VL-7B shape (28 L, 3584, 28q/4kv GQA, SwiGLU 18944), ragged V~U[256,1280] + 64, "
+                        "30% retention (configs[3])",
+               n_layers=28, d_model=3584, n_heads=28, n_kv_heads=4, d_head=128, d_ff=18944, mlp=1, act_mode=1,
+               batch=16, visual=(256, 1280), text=64, decode=256, layers=[2], keeps=[0.3], v0=None, outlier=0.01),
+    # BASELINE.json configs[4]: decode-bound sweep point (already-pruned prefix 173 + 64); --batch/--decode override
+    "c5": dict(workload="7B shape decode sweep point: pruned prefix 173 + 64, int4 group-128 KV (configs[4])",
+               n_layers=32, d_model=4096, n_heads=32, n_kv_heads=32, d_head=128, d_ff=11008, mlp=1, act_mode=1,
+               batch=64, visual=173, text=64, decode=512, layers=[], keeps=[], v0=173, outlier=0.01),
     # BASELINE.json configs[0] (tiny; parity case, also handy for a quick smoke bench)
     "c1": dict(workload="tiny VLM decoder (configs[0])", n_layers=4, d_model=256, n_heads=4, n_kv_heads=4,
                d_head=64, d_ff=688, mlp=1, act_mode=1, batch=1, visual=152, text=32, decode=16,
@@ -182,17 +197,19 @@ def run_reference(args, cfg):
         return
     threads = os.cpu_count() or 1
     ref, setup_s = reference_sample(threads, cfg["d_model"], cfg["n_heads"], cfg["d_head"])
-    vals = []
+    vals, secs = [], []
     for i in range(args.warmup + args.steps):
         v, sec = reference_tokens_per_s(ref, threads, cfg["n_layers"])
         if i >= args.warmup:
             vals.append(v)
+            secs.append(sec * cfg["n_layers"] / 4.0)
     value = float(np.mean(vals))
     sample = (f"{threads} threads x 1-token sequence through the unmodified reference forward_prefill, 4 layers "
               f"at 7B width (d 4096, 32x128 heads, d_ff 16384 SiLU, static scales), quantized mode; "
               f"tokens/s extrapolated to {cfg['n_layers']} layers (x4/{cfg['n_layers']}); setup {setup_s:.1f}s")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": float(np.mean(secs)) * 1e3,  # one step = the extrapolated 32-layer sample "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg["workload"], "batch_per_gpu": cfg["batch"],
                        "visual": cfg["visual"], "text": cfg["text"], "decode_steps": cfg["decode"]},
@@ -209,8 +226,10 @@ def build_engine(cfg, torch, Q, seed=1234):
     c = Q.Config(n_layers=cfg["n_layers"], d_model=cfg["d_model"], n_heads=cfg["n_heads"],
                  n_kv_heads=cfg["n_kv_heads"], d_head=cfg["d_head"], d_ff=cfg["d_ff"], mlp=cfg["mlp"],
                  act_mode=cfg["act_mode"])
-    B, S, D = cfg["batch"], cfg["visual"] + cfg["text"], cfg["decode"]
-    eng = Q.Engine(c, max_batch=B, max_tokens=B * S, max_seq=S, max_decode=D + 2)
+    B, D = cfg["batch"], cfg["decode"]
+    vis = visual_lengths(cfg)
+    S = max(vis) + cfg["text"]
+    eng = Q.Engine(c, max_batch=B, max_tokens=sum(vis) + B * cfg["text"], max_seq=S, max_decode=D + 2)
     g = torch.Generator(device="cuda").manual_seed(seed)
     d, kvd, f = cfg["d_model"], cfg["n_kv_heads"] * cfg["d_head"], cfg["d_ff"]
 
@@ -221,17 +240,30 @@ def build_engine(cfg, torch, Q, seed=1234):
         eng.load_layer(l, rnd(d, d), rnd(d, kvd), rnd(d, kvd), rnd(d, d), rnd(d, f), rnd(f, d),
                        rnd(d, f) if cfg["mlp"] == 1 else None)
     eng.load_head(rnd(d, d))
-    eng.set_recipe(cfg["layers"], cfg["keeps"], v0=cfg["v0"], res_bits=4)
+    if cfg["layers"]:
+        eng.set_recipe(cfg["layers"], cfg["keeps"], v0=cfg["v0"] or 1, res_bits=4)
+    else:
+        eng.clear_recipe()
     torch.cuda.synchronize()
     return eng
+
+
+def visual_lengths(cfg, seed=2024):
+    """Per-sequence visual counts: fixed, or seeded U[lo, hi] draws for ragged batches (configs[3])."""
+    v = cfg["visual"]
+    if isinstance(v, tuple):
+        rng = np.random.default_rng(seed)
+        return [int(x) for x in rng.integers(v[0], v[1] + 1, size=cfg["batch"])]
+    return [v] * cfg["batch"]
 
 
 def synth_inputs(cfg, torch, seed):
     """Hidden states N(0,1) with a seeded 1 % of channels x20 (BASELINE.json configs)."""
     g = torch.Generator(device="cpu").manual_seed(seed)
-    B, S, D, d = cfg["batch"], cfg["visual"] + cfg["text"], cfg["decode"], cfg["d_model"]
+    B, D, d = cfg["batch"], cfg["decode"], cfg["d_model"]
+    rows = sum(visual_lengths(cfg)) + B * cfg["text"]
     ch = torch.randperm(d, generator=g)[:max(1, int(round(cfg["outlier"] * d)))]
-    emb = torch.randn(B * S, d, generator=g)
+    emb = torch.randn(rows, d, generator=g)
     emb[:, ch] *= 20.0
     dec = torch.randn(D, B, d, generator=g)
     dec[:, :, ch] *= 20.0
@@ -252,16 +284,19 @@ def run_ours(args, cfg):
         dist = None
         torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    B, V, T, D, d = cfg["batch"], cfg["visual"], cfg["text"], cfg["decode"], cfg["d_model"]
-    S = V + T
+    B, T, D, d = cfg["batch"], cfg["text"], cfg["decode"], cfg["d_model"]
+    vis = visual_lengths(cfg)
+    V = max(vis)
+    rows = sum(vis) + B * T  # prefill tokens of the batch
+    v0s = vis if cfg["v0"] is None else None  # ragged: each sequence's own v0
     eng = build_engine(cfg, torch, Q)
     stream = torch.cuda.Stream(device=dev)
     eng.set_stream(stream)
     emb_h, dec_h = synth_inputs(cfg, torch, seed=77 + rank)
     emb_d, dec_d = emb_h.to(dev), dec_h.to(dev)
-    logits_d = torch.empty(B * S, d, device=dev)
+    logits_d = torch.empty(rows, d, device=dev)
     dlog_d = torch.empty(B, d, device=dev)
-    vis, txt = [V] * B, [T] * B
+    txt = [T] * B
     gathered = torch.empty(ws * B, d, device=dev) if ws > 1 else None
 
     def gather_outputs():
@@ -270,18 +305,18 @@ def run_ours(args, cfg):
                 dist.all_gather_into_tensor(gathered, dlog_d)
 
     def step_device():
-        eng.prefill(emb_d, vis, txt, logits_out=logits_d)
+        eng.prefill(emb_d, vis, txt, v0=v0s, logits_out=logits_d)
         for t in range(D):
             eng.decode(dec_d[t], logits_out=dlog_d)
         gather_outputs()
 
     # e2e: pinned host buffers through the public API, copies inside the timed region
     emb_p, dec_p = emb_h.pin_memory(), dec_h.pin_memory()
-    logits_p = torch.empty(B * S, d).pin_memory()
+    logits_p = torch.empty(rows, d).pin_memory()
     dlog_p = torch.empty(D, B, d).pin_memory()
 
     def step_e2e():
-        eng.prefill(emb_p, vis, txt, logits_out=logits_p)
+        eng.prefill(emb_p, vis, txt, v0=v0s, logits_out=logits_p)
         for t in range(D):
             eng.decode(dec_p[t], logits_out=dlog_p[t])
 
@@ -320,7 +355,7 @@ def run_ours(args, cfg):
     barrier()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
     ev[0].record(stream)
-    eng.prefill(emb_d, vis, txt, logits_out=logits_d)
+    eng.prefill(emb_d, vis, txt, v0=v0s, logits_out=logits_d)
     ev[1].record(stream)
     for t in range(D):
         eng.decode(dec_d[t], logits_out=dlog_d)
@@ -335,14 +370,14 @@ def run_ours(args, cfg):
 
     # per-kernel-class CUDA-event profile (one prefill + one eager decode step)
     eng.profile_next()
-    eng.prefill(emb_d, vis, txt, logits_out=logits_d)
+    eng.prefill(emb_d, vis, txt, v0=v0s, logits_out=logits_d)
     prof_pre = eng.profile_read()
     eng.profile_next()
     eng.decode(dec_d[0], logits_out=dlog_d)
     prof_dec = eng.profile_read()
     info = eng.info()
 
-    tokens = ws * B * (S + D)
+    tokens = ws * (rows + B * D)
     value = tokens / (ms_step / 1e3)
     e2e_val = tokens / (ms_e2e / 1e3)
     final_rows = info["final_rows"]
@@ -408,13 +443,14 @@ def run_ours(args, cfg):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "int4xint4->int32 (W4A4), fp64 residual, int4 KV", "data": "synthetic",
-            "config": {"workload": cfg["workload"], "batch_per_gpu": B, "visual": V, "text": T,
+            "config": {"workload": cfg["workload"], "batch_per_gpu": B, "visual": V if len(set(vis)) == 1 else {"ragged": list(cfg["visual"]), "mean": float(np.mean(vis))},
+                       "text": T,
                        "decode_steps": D, "recipe": {"candidate_layers": cfg["layers"], "keep_ratios": cfg["keeps"],
                                                      "v0": cfg["v0"]},
                        "layers": cfg["n_layers"], "d_model": d, "heads": cfg["n_heads"], "d_ff": cfg["d_ff"],
                        "parallelism": f"dp{ws} (batch sharded, NCCL gather of outputs only)",
                        "l2": "working set > L2: 3.25 GB int4 weights streamed every decode step and prefill layer"},
-            "prefill_ms": prefill_ms, "prefill_tokens_per_s": ws * B * S / (prefill_ms / 1e3),
+            "prefill_ms": prefill_ms, "prefill_tokens_per_s": ws * rows / (prefill_ms / 1e3),
             "decode_ms_per_step": decode_ms, "decode_tokens_per_s": ws * B / (decode_ms / 1e3),
             "prefill_gemm_tops": prefill_gemm_tops, "int8_peak_tops_measured": int8_peak, "decode_gemv_gbs": decode_gemv_gbs,
             "decode_attn_gbs": decode_attn_gbs, "final_rows": final_rows,
@@ -442,8 +478,14 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--batch", type=int, default=None, help="override the config's per-GPU batch (c5 sweep)")
+    ap.add_argument("--decode", type=int, default=None, help="override the config's decode steps (c5 sweep)")
     args = ap.parse_args()
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.batch:
+        cfg["batch"] = args.batch
+    if args.decode:
+        cfg["decode"] = args.decode
     if args.impl == "reference":
         run_reference(args, cfg)
     else:

@@ -63,7 +63,10 @@ const char* qt_last_error(void);
 int qt_engine_create(const qt_config* cfg, int max_batch, int max_tokens, int max_seq, int max_decode,
                      qt_engine** out);
 void qt_engine_destroy(qt_engine* e);
-/* cudaStream_t to run on (0 = the engine's own stream). */
+/* cudaStream_t to run on (0 = the engine's own stream).  Device-pointer inputs
+ * of qt_engine_prefill / qt_engine_decode must be ready in stream order on this
+ * stream (the engine stream is non-blocking: it does not wait for the legacy
+ * default stream). */
 int qt_engine_set_stream(qt_engine* e, void* stream);
 int qt_engine_synchronize(qt_engine* e);
 

@@ -87,7 +87,11 @@ T* dalloc(size_t n) {
     void* p = nullptr;
     if (n == 0) n = 1;
     ck(cudaMalloc(&p, n * sizeof(T)), "cudaMalloc");
+    // cudaMemset runs on the legacy stream, which the engine's non-blocking stream does
+    // not order against: finish it here, or a late zero-fill could land on data the
+    // engine stream already wrote (e.g. a regrown weight-staging buffer)
     ck(cudaMemset(p, 0, n * sizeof(T)), "cudaMemset");
+    ck(cudaDeviceSynchronize(), "cudaMemset");
     return static_cast<T*>(p);
 }
 
@@ -307,6 +311,15 @@ struct qt_engine {
         if (own_stream) cudaStreamDestroy(own_stream);
     }
 
+    // Host -> device copy ordered on the ENGINE stream and completed before returning.
+    // (A plain cudaMemcpy/cudaMemset runs on the legacy stream, which the engine's
+    // non-blocking stream does not wait for: a pageable cudaMemcpy may return before
+    // its DMA lands, and a later kernel on `st` could read the old bytes.)
+    void h2d(void* dst, const void* src, size_t bytes, const char* what) {
+        ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st), what);
+        ck(cudaStreamSynchronize(st), what);
+    }
+
     // ------------------------------------------------------------ staging
     template <class T>
     T* stage(const T* src, size_t n) {
@@ -322,6 +335,7 @@ struct qt_engine {
         if (v.empty()) return;
         T* p = stage(v.data(), v.size());
         ck(cudaMemcpyAsync(dst, p, v.size() * sizeof(T), cudaMemcpyHostToDevice, st), "upload");
+        qt::g_pdl_block = true;
     }
     void reset_staging() {
         ck(cudaStreamSynchronize(st), "stream sync");
@@ -411,7 +425,7 @@ struct qt_engine {
         std::vector<double> tab((size_t)max_pos * dh);
         qt_rope_table(max_pos, dh, tab.data());
         rope = dalloc<double>(tab.size());
-        ck(cudaMemcpy(rope, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice), "rope upload");
+        h2d(rope, tab.data(), tab.size() * sizeof(double), "rope upload");
 
         page_bytes = (long long)2 * Hkv * qt::kPage * (dh / 2 + 4);
         max_pages = (ms + md + qt::kPage - 1) / qt::kPage;
@@ -431,6 +445,7 @@ struct qt_engine {
         pin_cap = (size_t)64 << 20;
         pin_cap += (size_t)mt * (sizeof(int) * 8);
         ck(cudaMallocHost(&pin, pin_cap), "cudaMallocHost");
+        ck(cudaDeviceSynchronize(), "init");  // every zero-fill of dalloc (legacy stream) has landed
     }
 
     // persistent decode kernel: device layer table, accumulators, smem plan
@@ -478,7 +493,7 @@ struct qt_engine {
             m.kv_len = kv_len + (size_t)l * max_batch;
         }
         mk_layers = dalloc<qt::MkLayer>(L);
-        ck(cudaMemcpy(mk_layers, tab.data(), L * sizeof(qt::MkLayer), cudaMemcpyHostToDevice), "mk layers");
+        h2d(mk_layers, tab.data(), L * sizeof(qt::MkLayer), "mk layers");
         // staging rows of the owner phases live in the activation-row region (8 * a_ld bytes)
         mk_possible = mk_nslot >= 4 && (dh == 64 || dh == 128) && H <= 64 && 8 * mk_a_ld >= 8 * d &&
                       8 * mk_a_ld >= 4 * dff && B_MAX_MK >= 1;
@@ -516,6 +531,7 @@ struct qt_engine {
         if (mk_trace) ck(cudaMemsetAsync(mk_trace, 0, tn * 8, st), "trace");
         p.trace = mk_trace;
         ck(cudaMemsetAsync(mk_sync, 0, 256 * sizeof(unsigned), st), "mk sync reset");
+        qt::g_pdl_block = true;
         pb(P_GEMM);
         ckl(qt_launch_decode_mk(&p, dh, mk_grid, mk_smem, st), "decode megakernel");
         if (mk_trace) {
@@ -546,7 +562,8 @@ struct qt_engine {
         n_pages_cap = 0;
         void* p = nullptr;
         ck(cudaMalloc(&p, (size_t)pages * page_bytes), "KV pool cudaMalloc");
-        ck(cudaMemset(p, 0, (size_t)pages * page_bytes), "KV pool memset");
+        ck(cudaMemsetAsync(p, 0, (size_t)pages * page_bytes, st), "KV pool memset");  // ordered on the engine stream
+        qt::g_pdl_block = true;
         pool = static_cast<uint8_t*>(p);
         n_pages_cap = pages;
     }
@@ -596,17 +613,18 @@ struct qt_engine {
         std::vector<float> v(d, 1.0f);
         if (g)
             for (int i = 0; i < d; ++i) v[i] = (float)g[i];
-        ck(cudaMemcpy(dst, v.data(), d * sizeof(float), cudaMemcpyHostToDevice), "gain");
+        h2d(dst, v.data(), d * sizeof(float), "gain");
     }
 
     void load_gain(float* dst, const float* g, int on_device) {
         if (!g) {
             std::vector<float> ones(d, 1.0f);
-            ck(cudaMemcpy(dst, ones.data(), d * sizeof(float), cudaMemcpyHostToDevice), "gain");
+            h2d(dst, ones.data(), d * sizeof(float), "gain");
             return;
         }
-        ck(cudaMemcpy(dst, g, d * sizeof(float), on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice),
+        ck(cudaMemcpyAsync(dst, g, d * sizeof(float), on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st),
            "gain");
+        ck(cudaStreamSynchronize(st), "gain");
     }
 
     // ------------------------------------------------------------ kernels
@@ -719,11 +737,13 @@ struct qt_engine {
             ck(cudaMemcpyAsync(xc, emb, (size_t)total * d * sizeof(double),
                                emb_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st),
                "emb");
+            qt::g_pdl_block = true;
         } else {
             const float* emb_d = static_cast<const float*>(emb);
             if (!emb_dev) {  // stage through the fp32 attention buffer, widen on device
                 ck(cudaMemcpyAsync(attn, emb, (size_t)total * d * sizeof(float), cudaMemcpyHostToDevice, st), "emb");
                 emb_d = attn;
+                qt::g_pdl_block = true;
             }
             ckl(qt_launch_f32_to_f64(emb_d, xc, (long long)total * d, st), "embedding widen");
         }
@@ -999,10 +1019,12 @@ struct qt_engine {
             ck(cudaMemcpyAsync(xd, emb, (size_t)B * d * sizeof(double),
                                emb_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st),
                "decode emb");
+            qt::g_pdl_block = true;
         } else {
             ck(cudaMemcpyAsync(xd_in, emb, (size_t)B * d * sizeof(float),
                                emb_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st),
                "decode emb");
+            qt::g_pdl_block = true;
             pb(P_OTHER);
             ckl(qt_launch_f32_to_f64(xd_in, xd, (long long)B * d, st), "embedding widen");
             pe((double)B * d * 12);
@@ -1160,6 +1182,8 @@ int qt_engine_load_layer(qt_engine* e, int layer, const float* wq, const float* 
         if (e->cfg.mlp == 1 && !w3) fail(QT_EINVAL, "SwiGLU needs w3 (up projection)");
         LayerW& l = e->lw[layer];
         const int d = e->d, kvd = e->Hkv * e->dh, f = e->dff;
+        // device weights may come from another stream (e.g. torch's): let them land first
+        if (on_device) ck(cudaDeviceSynchronize(), "weights ready");
         e->quant_into(wq, d, d, on_device, 1, 0, l.qkv, e->n_qkv_pad, l.s_qkv);
         e->quant_into(wk, d, kvd, on_device, 1, d, l.qkv, e->n_qkv_pad, l.s_qkv);
         e->quant_into(wv, d, kvd, on_device, 1, d + kvd, l.qkv, e->n_qkv_pad, l.s_qkv);
@@ -1270,6 +1294,7 @@ int qt_engine_load(qt_engine* e, const char* path) {
 int qt_engine_load_head(qt_engine* e, const float* w_head, const float* final_gain, int on_device) {
     return guard([&] {
         if (!w_head) fail(QT_EINVAL, "null weight");
+        if (on_device) ck(cudaDeviceSynchronize(), "weights ready");
         e->quant_into(w_head, e->d, e->d, on_device, 1, 0, e->head, e->nd_pad, e->s_head);
         e->load_gain(e->gf, final_gain, on_device);
         e->head_loaded = true;
@@ -1283,7 +1308,7 @@ int qt_engine_set_act_scales(qt_engine* e, const double* scales) {
         e->act.assign(scales, scales + 4 * e->L + 1);
         for (double s : e->act)
             if (!(s > 0.0) || !std::isfinite(s)) fail(QT_EINVAL, "activation scales must be positive");
-        ck(cudaMemcpy(e->mk_act, e->act.data(), e->act.size() * sizeof(double), cudaMemcpyHostToDevice), "act");
+        e->h2d(e->mk_act, e->act.data(), e->act.size() * sizeof(double), "act");
         e->act_set = true;
         e->graph_ok = false;
     });

@@ -251,6 +251,16 @@ __global__ void __launch_bounds__(T5_THREADS, 1) k_gemm_tc05(const uint8_t* __re
             const int m0 = (t % mt_n) * T5_BM, n0 = (t / mt_n) * T5_BN;
             double* swt = sws + acc * T5_BN;
             for (int i = et; i < T5_BN; i += 128) swt[i] = n0 + i < N ? sw[n0 + i] : 0.0;
+            if (EPI == QT_EPI_RESADD) {
+                // pull this thread's residual row segment (256 fp64) toward L2 while the
+                // tile's MMAs run: the read-modify-write below then hits L2, not HBM
+                const int mr = m0 + q * 32 + lane;
+                if (mr < M) {
+                    const char* rp = reinterpret_cast<const char*>(static_cast<const double*>(out) + (size_t)mr * ldo + n0);
+                    const int nb = min(T5_BN, N - n0) * 8;
+                    for (int c = 0; c < nb; c += 128) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(rp + c));
+                }
+            }
             asm volatile("bar.sync 2, 128;\n" ::: "memory");
             mbar_wait(&tfull[acc], (tl / T5_ACC) & 1);
             tc_fence_after();

@@ -401,7 +401,8 @@ static int launch_nq_cl(const TX* x, int ld_x, const float* gain, int M, int D, 
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = getenv("QT_NOPDL") ? 1 : 2;
+    cfg.numAttrs = (getenv("QT_NOPDL") || g_pdl_block) ? 1 : 2;
+    g_pdl_block = false;
     return (int)cudaLaunchKernelEx(&cfg, k_norm_quant_cl<TX, CL, G>, x, ld_x, gain, M, D, d_pad, qmax, mode,
                                    static_scale, codes, ld_codes, scales);
 }

@@ -224,6 +224,11 @@ QT_DEV void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_depend
 #ifndef __CUDACC_RTC__
 #include <cstdlib>
 namespace qt {
+// Set by the host engine after it enqueues a copy / memset on the stream: the
+// next launch then takes a full stream dependency instead of a programmatic
+// (PDL) one, so it cannot start before the copy has landed.
+inline thread_local bool g_pdl_block = false;
+
 template <typename... KArgs, typename... Args>
 inline int launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                       Args... args) {
@@ -237,7 +242,8 @@ inline int launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t sm
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = no_pdl ? 0 : 1;
+    cfg.numAttrs = (no_pdl || g_pdl_block) ? 0 : 1;
+    g_pdl_block = false;
     cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
     return (int)e;
 }
