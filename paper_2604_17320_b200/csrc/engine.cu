@@ -283,6 +283,7 @@ struct qt_engine {
     double* mk_act = nullptr;
     int mk_grid = 0, mk_smem = 0, mk_nslot = 0, mk_a_ld = 0, mk_acc_rows = 0;
     bool mk_possible = false;
+    int* splitk_ws = nullptr;     // int32 split-K partials of the tcgen05 GEMM at small M
     unsigned* seq_cnt = nullptr;  // per-sequence arrival counters of the fused decode attention block
     // opt-in (QT_ATTN_FUSED=1): one kernel for RoPE + KV append + attention + attn_out quant; measured
     // no faster than the three-kernel PDL chain at B = 8
@@ -306,7 +307,7 @@ struct qt_engine {
         f(mag); f(res); f(inter); f(intra); f(w4); f(budget); f(new_off); f(new_len); f(keep_src); f(keep_local);
         f(kept_pos); f(sc_fused); f(sc_norm); f(rope); f(wscratch); f(wstage); f(pool); f(pt); f(kv_len); f(next_pos); f(dec_seq);
         f(xd); f(xd_in); f(dlogits); f(part_ml); f(part_o);
-        f(seq_cnt); f(mk_trace); f(mk_layers); f(mk_acc); f(mk_codes); f(mk_sa); f(mk_attn); f(mk_sync); f(mk_act);
+        f(splitk_ws); f(seq_cnt); f(mk_trace); f(mk_layers); f(mk_acc); f(mk_codes); f(mk_sa); f(mk_attn); f(mk_sync); f(mk_act);
         if (pin) cudaFreeHost(pin);
         if (own_stream) cudaStreamDestroy(own_stream);
     }
@@ -441,6 +442,17 @@ struct qt_engine {
         part_ml = dalloc<float>((size_t)mb * H * dec_splits * 2);
         part_o = dalloc<float>((size_t)mb * H * dec_splits * dh);
         seq_cnt = dalloc<unsigned>(mb);
+        {  // split-K workspace: the largest ksplit * M * N over the GEMM shapes that split
+            const int shapes[5][2] = {{n_qkv, kd_pad}, {d, kd_pad}, {n_gu, kd_pad}, {d, kff_pad}, {d, kd_pad}};
+            size_t need = 0;
+            for (auto& sh : shapes)
+                for (int m = 17; m <= std::min(mt, 128 * 148); m = (m < 128 ? 128 : m + 128)) {
+                    const int mm = std::min(m, mt);
+                    const int ks = qt_tc05_splitk(mm, sh[0], sh[1]);
+                    if (ks > 1) need = std::max(need, (size_t)ks * mm * sh[0]);
+                }
+            if (need) splitk_ws = dalloc<int>(need);
+        }
         mk_init();
         pin_cap = (size_t)64 << 20;
         pin_cap += (size_t)mt * (sizeof(int) * 8);
@@ -639,8 +651,10 @@ struct qt_engine {
     // w: tiled int4 weights with wrows padded rows; activation codes: tiled with codes_rows rows
     void gemm(int epi, const uint8_t* w, int wrows, const double* sw, int M, int N, int K, void* out, int ldo) {
         pb(P_GEMM);
-        int rc = (use_tc05 && M > 16)
-                     ? qt_launch_w4a4_tc05(epi, codes, codes_rows, ascale, w, wrows, sw, M, N, K, out, ldo, nullptr, st)
+        // tcgen05 for token-rich GEMMs; the weight-streaming GEMV up to 64 tokens (decode batches)
+        int rc = (use_tc05 && M > 64)
+                     ? qt_launch_w4a4_tc05(epi, codes, codes_rows, ascale, w, wrows, sw, M, N, K, out, ldo, nullptr,
+                                           splitk_ws, st)
                      : qt_launch_w4a4_mma(epi, codes, codes_rows, ascale, w, wrows, sw, M, N, K, out, ldo, nullptr, st);
         ckl(rc, "w4a4 gemm");
         const double out_bytes = epi == QT_EPI_RESADD ? 16.0 * M * N : (epi == QT_EPI_SWIGLU ? 2.0 * M * N : 4.0 * M * N);
@@ -1520,8 +1534,18 @@ int qt_rmsnorm_quant_i4(const void* x, int x_is_f64, int ld_x, const float* gain
 int qt_w4a4_gemm(int epi, const uint8_t* a, int lda, const double* sa, const uint8_t* w, int ldw, const double* sw,
                  int M, int N, int K, void* out, int ldo, int32_t* acc_out, int impl, void* stream) {
     return guard([&] {
-        int rc = impl == 1 ? qt_launch_w4a4_tc05(epi, a, lda, sa, w, ldw, sw, M, N, K, out, ldo, acc_out, (cudaStream_t)stream)
+        int* ws = nullptr;  // impl 2: tcgen05 with split-K (temporary workspace; test / ABI path)
+        if (impl == 2) {
+            const int ks = qt_tc05_splitk(M, N, K);
+            ck(cudaMalloc(&ws, (size_t)std::max(ks, 1) * M * N * sizeof(int)), "split-K workspace");
+        }
+        int rc = impl >= 1 ? qt_launch_w4a4_tc05(epi, a, lda, sa, w, ldw, sw, M, N, K, out, ldo, acc_out, ws,
+                                                  (cudaStream_t)stream)
                            : qt_launch_w4a4_mma(epi, a, lda, sa, w, ldw, sw, M, N, K, out, ldo, acc_out, (cudaStream_t)stream);
+        if (ws) {
+            cudaStreamSynchronize((cudaStream_t)stream);
+            cudaFree(ws);
+        }
         ckl(rc, "w4a4 gemm");
     });
 }

@@ -159,16 +159,22 @@ __global__ void __launch_bounds__(256) k_gemm_tc(const uint8_t* __restrict__ A, 
 // issued before the programmatic-dependency wait and overlaps the upstream
 // kernel.  Swap-AB mma.sync m16n8k32: weights are the 16-row operand, tokens
 // the n8 operand; split-K partials are reduced in smem for the fused epilogue.
+//
+// NT <= 2 (<= 16 tokens): the token codes are staged in smem.  NT 4 / 8 (17..64
+// tokens, decode batches): they do not fit for K = d_ff, so the B fragments are
+// read straight from the (L1/L2-resident) tiled activation codes; each warp
+// keeps re-reading the same k slice across its row blocks.
 template <int NT, int EPI>
 __global__ void __launch_bounds__(256) k_gemv_reg(const uint8_t* __restrict__ A, int lda, const double* __restrict__ sa,
                                                   const uint8_t* __restrict__ W, int ldw, const double* __restrict__ sw,
                                                   int M, int N, int K, void* __restrict__ out, int ldo,
                                                   int* __restrict__ acc_dbg) {
     constexpr int TOK = 8 * NT;
-    constexpr int U = 4;
+    constexpr bool ASM = NT <= 2;     // activation codes staged in smem
+    constexpr int U = NT <= 2 ? 4 : 2;
     extern __shared__ __align__(128) uint8_t smem[];
     const int kb = K / 2;
-    const int ldsA = kb + 64;
+    const int ldsA = ASM ? kb + 64 : 0;
     uint8_t* As = smem;
     int* red = reinterpret_cast<int*>(smem + TOK * ldsA);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -192,14 +198,16 @@ __global__ void __launch_bounds__(256) k_gemv_reg(const uint8_t* __restrict__ A,
     int rb = blockIdx.x, bat = 0;
     fetch(rb, 0, wa, wb);
     pdl_wait();
-    for (int c = tid; c < TOK * (kb / 16); c += 256) {
-        int r = c / (kb / 16), q = c % (kb / 16);
-        bool ok = r < M;
-        cp_async16(As + r * ldsA + q * 16, A + w4t_offset(ok ? r : 0, q * 16, lda), ok);
+    if (ASM) {
+        for (int c = tid; c < TOK * (kb / 16); c += 256) {
+            int r = c / (kb / 16), q = c % (kb / 16);
+            bool ok = r < M;
+            cp_async16(As + r * ldsA + q * 16, A + w4t_offset(ok ? r : 0, q * 16, lda), ok);
+        }
+        cp_async_commit();
+        cp_async_wait<0>();
+        __syncthreads();
     }
-    cp_async_commit();
-    cp_async_wait<0>();
-    __syncthreads();
     pdl_launch_dependents();
     int acc[NT][4];
 #pragma unroll
@@ -218,8 +226,10 @@ __global__ void __launch_bounds__(256) k_gemv_reg(const uint8_t* __restrict__ A,
             if (c >= ch1) break;
             uint4 bv[NT];
 #pragma unroll
-            for (int j = 0; j < NT; ++j)
-                bv[j] = *reinterpret_cast<const uint4*>(As + (j * 8 + g) * ldsA + c * 64 + tig * 16);
+            for (int j = 0; j < NT; ++j) {
+                if (ASM) bv[j] = *reinterpret_cast<const uint4*>(As + (j * 8 + g) * ldsA + c * 64 + tig * 16);
+                else bv[j] = ldg_nc_v4(A + w4t_offset(j * 8 + g, c * 64 + tig * 16, lda));  // rows >= M: discarded
+            }
 #pragma unroll
             for (int s2 = 0; s2 < 4; ++s2) {
                 uint32_t a[4];
@@ -283,6 +293,25 @@ int launch_gemm(const uint8_t* A, int lda, const double* sa, const uint8_t* W, i
     if (M <= 0) return 0;
     if (K % 128 || lda % 16 || ldw % 16 || M > lda || N > ldw) return -1;  // lda/ldw = padded rows
     const int nb = (N + GB_N - 1) / GB_N;
+    if (M > 16 && M <= 64 && lda >= ((M + 31) / 32) * 32) {
+        // 17..64 tokens: B fragments from global (padded tile rows up to 32 / 64 must exist)
+        const int n_rb = (N + 15) / 16;
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+        const dim3 grid(std::min(n_rb, 2 * sms));
+        if (M <= 32) {
+            const size_t smem = (size_t)8 * 16 * 32 * 4;
+            auto kfn = k_gemv_reg<4, EPI>;
+            cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            return launch_pdl(kfn, grid, dim3(256), smem, st, A, lda, sa, W, ldw, sw, M, N, K, out, ldo, acc_dbg);
+        }
+        if (lda >= 64) {
+            const size_t smem = (size_t)8 * 16 * 64 * 4;
+            auto kfn = k_gemv_reg<8, EPI>;
+            cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            return launch_pdl(kfn, grid, dim3(256), smem, st, A, lda, sa, W, ldw, sw, M, N, K, out, ldo, acc_dbg);
+        }
+    }
     if (M <= 16) {
         const int kb = K / 2;
         const int TOK = M <= 8 ? 8 : 16;

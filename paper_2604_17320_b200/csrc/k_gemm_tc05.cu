@@ -119,7 +119,8 @@ __global__ void __launch_bounds__(T5_THREADS, 1) k_gemm_tc05(const uint8_t* __re
                                                               const uint8_t* __restrict__ W, int ldw,
                                                               const double* __restrict__ sw, int M, int N, int K,
                                                               void* __restrict__ out, int ldo,
-                                                              int* __restrict__ acc_dbg) {
+                                                              int* __restrict__ acc_dbg, int ksplit,
+                                                              int* __restrict__ ws) {
     extern __shared__ __align__(1024) uint8_t smem[];
     uint64_t* pfull = reinterpret_cast<uint64_t*>(smem + T5Smem::bars);
     uint64_t* pempty = pfull + T5_PS;
@@ -134,6 +135,10 @@ __global__ void __launch_bounds__(T5_THREADS, 1) k_gemm_tc05(const uint8_t* __re
     const int art = lda >> 4, wrt = ldw >> 4;  // row blocks per k-block (tiled, k-block-major)
     const int mt_n = (M + T5_BM - 1) / T5_BM, nt_n = (N + T5_BN - 1) / T5_BN;
     const int tiles = mt_n * nt_n;
+    // work unit u = slice * tiles + tile; slice s covers k blocks [s*KB/ksplit, (s+1)*KB/ksplit).
+    // ksplit > 1 (few tiles, e.g. decode batches of 17..256 tokens): raw int32 partial sums go
+    // to ws[s][m][n] and k_splitk_epilogue reduces them in fixed order and applies the epilogue.
+    const int units = tiles * ksplit;
     const int a_rbs_total = (M + 15) / 16, w_rbs_total = (N + 15) / 16;
 
     if (threadIdx.x == 0) {
@@ -167,10 +172,11 @@ __global__ void __launch_bounds__(T5_THREADS, 1) k_gemm_tc05(const uint8_t* __re
         if (lane == 0) {
             pdl_wait();  // activation codes come from the upstream kernel
             int it = 0;
-            for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+            for (int u = blockIdx.x; u < units; u += gridDim.x) {
+                const int t = u % tiles, sl = u / tiles;
                 const int a_rb0 = (t % mt_n) * (T5_BM / 16), w_rb0 = (t / mt_n) * (T5_BN / 16);
                 const int a_rbs = min(T5_BM / 16, a_rbs_total - a_rb0), w_rbs = min(T5_BN / 16, w_rbs_total - w_rb0);
-                for (int kb = 0; kb < KB; ++kb, ++it) {
+                for (int kb = sl * KB / ksplit; kb < (sl + 1) * KB / ksplit; ++kb, ++it) {
                     const int s = it % T5_PS;
                     if (it >= T5_PS) mbar_wait(&pempty[s], ((it / T5_PS) - 1) & 1);
                     mbar_arrive_expect_tx(&pfull[s], (uint32_t)(a_rbs + w_rbs) * 1024u);
@@ -187,12 +193,13 @@ __global__ void __launch_bounds__(T5_THREADS, 1) k_gemm_tc05(const uint8_t* __re
         if (lane == 0) {
             const uint32_t idesc = t5_idesc();
             int it = 0, tl = 0;
-            for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++tl) {
+            for (int u = blockIdx.x; u < units; u += gridDim.x, ++tl) {
+                const int sl = u / tiles, kb0 = sl * KB / ksplit, kb1 = (sl + 1) * KB / ksplit;
                 const int acc = tl % T5_ACC;
                 if (tl >= T5_ACC) mbar_wait(&tempty[acc], ((tl / T5_ACC) - 1) & 1);
                 tc_fence_after();
                 const uint32_t tacc = tmem + (uint32_t)(acc * T5_BN);
-                for (int kb = 0; kb < KB; ++kb, ++it) {
+                for (int kb = kb0; kb < kb1; ++kb, ++it) {
                     const int s = it % T5_IS;
                     mbar_wait(&ifull[s], (it / T5_IS) & 1);
                     tc_fence_after();
@@ -200,7 +207,8 @@ __global__ void __launch_bounds__(T5_THREADS, 1) k_gemm_tc05(const uint8_t* __re
                     const uint32_t b0 = smem_u32(smem + T5Smem::ib + (size_t)s * T5_IB);
 #pragma unroll
                     for (int k = 0; k < 4; ++k)
-                        mma_i8(tacc, umma_desc_sw128(a0 + 32 * k), umma_desc_sw128(b0 + 32 * k), idesc, (kb | k) != 0);
+                        mma_i8(tacc, umma_desc_sw128(a0 + 32 * k), umma_desc_sw128(b0 + 32 * k), idesc,
+                               (kb != kb0) || (k != 0));
                     mma_commit(&iempty[s]);
                 }
                 mma_commit(&tfull[acc]);
@@ -211,8 +219,9 @@ __global__ void __launch_bounds__(T5_THREADS, 1) k_gemm_tc05(const uint8_t* __re
         // ---------------- converters: packed int4 -> swizzled int8 (128 threads)
         const int ct = threadIdx.x - 64;
         int it = 0;
-        for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-            for (int kb = 0; kb < KB; ++kb, ++it) {
+        for (int u = blockIdx.x; u < units; u += gridDim.x) {
+            const int sl = u / tiles;
+            for (int kb = sl * KB / ksplit; kb < (sl + 1) * KB / ksplit; ++kb, ++it) {
                 const int ps = it % T5_PS, is = it % T5_IS;
                 mbar_wait(&pfull[ps], (it / T5_PS) & 1);
                 if (it >= T5_IS) mbar_wait(&iempty[is], ((it / T5_IS) - 1) & 1);
@@ -246,12 +255,13 @@ __global__ void __launch_bounds__(T5_THREADS, 1) k_gemm_tc05(const uint8_t* __re
         const int q = warp & 3;
         const int et = threadIdx.x - 192;
         int tl = 0;
-        for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++tl) {
+        for (int u = blockIdx.x; u < units; u += gridDim.x, ++tl) {
+            const int t = u % tiles, sl = u / tiles;
             const int acc = tl % T5_ACC;
             const int m0 = (t % mt_n) * T5_BM, n0 = (t / mt_n) * T5_BN;
             double* swt = sws + acc * T5_BN;
             for (int i = et; i < T5_BN; i += 128) swt[i] = n0 + i < N ? sw[n0 + i] : 0.0;
-            if (EPI == QT_EPI_RESADD) {
+            if (EPI == QT_EPI_RESADD && ksplit == 1) {
                 // pull this thread's residual row segment (256 fp64) toward L2 while the
                 // tile's MMAs run: the read-modify-write below then hits L2, not HBM
                 const int mr = m0 + q * 32 + lane;
@@ -279,6 +289,13 @@ __global__ void __launch_bounds__(T5_THREADS, 1) k_gemm_tc05(const uint8_t* __re
                 }
                 const int nb = n0 + j * 32;
                 if (m >= M || nb >= N) continue;
+                if (ksplit > 1) {  // raw partial sums of this k slice
+                    int* wr = ws + ((size_t)sl * M + m) * N + nb;
+#pragma unroll
+                    for (int e = 0; e < 32; ++e)
+                        if (nb + e < N) wr[e] = (int)r[e] >> 8;
+                    continue;
+                }
                 if (acc_dbg) {
 #pragma unroll
                     for (int e = 0; e < 32; ++e)
@@ -304,24 +321,67 @@ __global__ void __launch_bounds__(T5_THREADS, 1) k_gemm_tc05(const uint8_t* __re
     }
 }
 
+// Split-K reduction + epilogue: y = (sum over slices, fixed order) * s_a[m] * s_w[n],
+// then the same epilogue as the row-wise path.  One thread per output pair.
+template <int EPI>
+__global__ void __launch_bounds__(256) k_splitk_epilogue(const int* __restrict__ ws, int ksplit, int M, int N,
+                                                         const double* __restrict__ sa, const double* __restrict__ sw,
+                                                         void* __restrict__ out, int ldo, int* __restrict__ acc_dbg) {
+    pdl_launch_dependents();
+    pdl_wait();
+    const long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 2;
+    if (i >= (long long)M * N) return;
+    const int m = (int)(i / N), n = (int)(i % N);
+    int s0 = 0, s1 = 0;
+    for (int s = 0; s < ksplit; ++s) {
+        const int* p = ws + ((size_t)s * M + m) * N + n;
+        s0 += p[0];
+        if (n + 1 < N) s1 += p[1];
+    }
+    if (acc_dbg) {
+        acc_dbg[(size_t)m * N + n] = s0;
+        if (n + 1 < N) acc_dbg[(size_t)m * N + n + 1] = s1;
+    }
+    const double a_s = sa[m];
+    epi_store<EPI>(out, ldo, m, n, (double)s0 * (a_s * sw[n]), n + 1 < N ? (double)s1 * (a_s * sw[n + 1]) : 0.0, N);
+}
+
 }  // namespace qt
+
+extern "C" int qt_tc05_splitk(int M, int N, int K) {
+    // slices so that tiles x slices covers the SMs, >= 4 k blocks per slice
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const int tiles = ((N + qt::T5_BN - 1) / qt::T5_BN) * ((M + qt::T5_BM - 1) / qt::T5_BM);
+    const int KB = K / 128;
+    if (tiles >= sms / 2) return 1;
+    int s = (sms + tiles - 1) / tiles;
+    s = std::min(s, std::max(1, KB / 4));
+    return std::max(1, s);
+}
 
 extern "C" int qt_launch_w4a4_tc05(int epi, const uint8_t* A, int lda, const double* sa, const uint8_t* W, int ldw,
                                    const double* sw, int M, int N, int K, void* out, int ldo, int* acc_dbg,
-                                   cudaStream_t st) {
+                                   int* ws, cudaStream_t st) {
     using namespace qt;
     if (M <= 0) return 0;
     if (K % 128 || lda % 16 || ldw % 16 || M > lda || N > ldw) return -1;  // lda/ldw = padded rows
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     const int tiles = ((N + T5_BN - 1) / T5_BN) * ((M + T5_BM - 1) / T5_BM);
-    const dim3 grid(std::min(tiles, sms));
+    const int ksplit = ws ? qt_tc05_splitk(M, N, K) : 1;
+    const dim3 grid(std::min(tiles * ksplit, sms));
     const size_t smem = T5Smem::total;
 #define QT_T5(E)                                                                                                \
     do {                                                                                                        \
         auto kfn = k_gemm_tc05<E>;                                                                              \
         cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                      \
-        return launch_pdl(kfn, grid, dim3(T5_THREADS), smem, st, A, lda, sa, W, ldw, sw, M, N, K, out, ldo, acc_dbg); \
+        int rc = launch_pdl(kfn, grid, dim3(T5_THREADS), smem, st, A, lda, sa, W, ldw, sw, M, N, K, out, ldo,   \
+                            ksplit > 1 ? nullptr : acc_dbg, ksplit, ws);                                         \
+        if (rc || ksplit == 1) return rc;                                                                       \
+        const long long pairs = ((long long)M * N + 1) / 2;                                                     \
+        return launch_pdl(k_splitk_epilogue<E>, dim3((unsigned)((pairs + 255) / 256)), dim3(256), 0, st,      \
+                          (const int*)ws, ksplit, M, N, sa, sw, out, ldo, acc_dbg);                              \
     } while (0)
     switch (epi) {
         case QT_EPI_STORE: QT_T5(QT_EPI_STORE);

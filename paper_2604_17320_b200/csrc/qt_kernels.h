@@ -37,8 +37,12 @@ int qt_launch_codes_pack(const int8_t* src, int K, int N, const double* s_in, in
 // out: double* for QT_EPI_RESADD (the fp64 residual stream), float* otherwise
 int qt_launch_w4a4_mma(int epi, const uint8_t* A, int lda, const double* sa, const uint8_t* W, int ldw,
                        const double* sw, int M, int N, int K, void* out, int ldo, int* acc_dbg, cudaStream_t st);
+// ws (nullable): int32 split-K workspace of qt_tc05_splitk(M, N, K) * M * N entries; with ws the
+// GEMM splits K across CTAs when its tiles would underfill the SMs (decode batches 17..256)
+int qt_tc05_splitk(int M, int N, int K);
 int qt_launch_w4a4_tc05(int epi, const uint8_t* A, int lda, const double* sa, const uint8_t* W, int ldw,
-                        const double* sw, int M, int N, int K, void* out, int ldo, int* acc_dbg, cudaStream_t st);
+                        const double* sw, int M, int N, int K, void* out, int ldo, int* acc_dbg, int* ws,
+                        cudaStream_t st);
 int qt_launch_attn_prefill(const float* qkv, int ldq, int H, int Hkv, int dh, const int* seq_off, const int* vis,
                            const int* seq_len, int B, int smax, const uint8_t* pool, long long page_bytes,
                            const int* pt, int max_pages, float* out, int ldo, float* ml, cudaStream_t st);

@@ -100,22 +100,23 @@ def _pack(c):
     return (c[..., 0::2] | (c[..., 1::2] << 4)).astype(np.uint8)
 
 
-def _tiled(c):
-    """int4 codes [rows x K] -> packed + tiled (rows zero-padded to 16), the engine's code layout."""
+def _tiled(c, pad=16):
+    """int4 codes [rows x K] -> packed + tiled (rows zero-padded to `pad`), the engine's code layout."""
     p = _pack(c)
-    rows = (p.shape[0] + 15) // 16 * 16
+    rows = (p.shape[0] + pad - 1) // pad * pad
     out = np.zeros((rows, p.shape[1]), dtype=np.uint8)
     out[:p.shape[0]] = p
     return Q.tile_w4(out)
 
 
 @pytest.mark.parametrize("M,impl", [(1, 0), (3, 0), (8, 0), (13, 0), (16, 0), (40, 0), (128, 0), (300, 0),
-                                    (40, 1), (128, 1), (300, 1), (1000, 1)])
+                                    (40, 1), (128, 1), (300, 1), (1000, 1), (40, 2), (64, 2), (200, 2)])
 def test_w4a4_gemm_int32_exact(torch_cuda, M, impl):
-    """impl 0: mma.sync GEMM/GEMV; impl 1: tcgen05 kind::i8 GEMM (TMEM accumulators)."""
+    """impl 0: mma.sync GEMM/GEMV; impl 1: tcgen05 kind::i8 GEMM (TMEM accumulators);
+    impl 2: tcgen05 with split-K (int32 partials reduced in fixed order)."""
     torch = torch_cuda
     rng = np.random.default_rng(M)
-    K, N = (512, 384) if impl == 0 else (1024, 640)
+    K, N = (512, 384) if impl == 0 else ((1024, 640) if impl == 1 else (2048, 520))
     a = rng.integers(-7, 8, size=(M, K))
     w = rng.integers(-7, 8, size=(N, K))
     sa = rng.uniform(0.01, 0.5, M)
@@ -182,3 +183,56 @@ def test_gemm_matches_reference_quantized_linear(torch_cuda):
     Q.w4a4_gemm(Q.EPI_STORE, codes, scales, wcd, wsd, M, N, K, out)
     torch.cuda.synchronize()
     np.testing.assert_allclose(out.cpu().numpy(), exp, rtol=1e-6, atol=1e-7)
+
+
+@pytest.mark.parametrize("epi", [Q.EPI_STORE, Q.EPI_RESADD, Q.EPI_SWIGLU])
+def test_w4a4_gemm_splitk_epilogues(torch_cuda, epi):
+    """tcgen05 split-K (decode batches): fixed-order int32 reduction then the row-wise epilogue."""
+    torch = torch_cuda
+    rng = np.random.default_rng(77 + epi)
+    M, K, N = 48, 1024, 512
+    a = rng.integers(-7, 8, size=(M, K))
+    w = rng.integers(-7, 8, size=(N, K))
+    sa = rng.uniform(0.01, 0.5, M)
+    sw = rng.uniform(0.001, 0.01, N)
+    acc_exp = a.astype(np.int64) @ w.T.astype(np.int64)
+    y = acc_exp * (sa[:, None] * sw[None, :])
+    if epi == Q.EPI_SWIGLU:
+        out = torch.zeros((M, N // 2), dtype=torch.float32, device="cuda")
+        g, u = y[:, 0::2], y[:, 1::2]
+        exp, tol = g / (1 + np.exp(-g)) * u, dict(rtol=1e-6, atol=1e-7)
+    elif epi == Q.EPI_RESADD:
+        base = rng.standard_normal((M, N))
+        out = torch.from_numpy(base.copy()).cuda()
+        exp, tol = base + y, dict(rtol=1e-14, atol=1e-14)
+    else:
+        out = torch.zeros((M, N), dtype=torch.float32, device="cuda")
+        exp, tol = y, dict(rtol=2e-7, atol=1e-7)
+    acc = torch.zeros((M, N), dtype=torch.int32, device="cuda")
+    Q.w4a4_gemm(epi, torch.from_numpy(_tiled(a)).cuda(), torch.from_numpy(sa).cuda(),
+                torch.from_numpy(_tiled(w)).cuda(), torch.from_numpy(sw).cuda(), M, N, K, out, acc, impl=2)
+    torch.cuda.synchronize()
+    assert np.array_equal(acc.cpu().numpy(), acc_exp)
+    np.testing.assert_allclose(out.cpu().numpy(), exp, **tol)
+
+
+@pytest.mark.parametrize("M", [17, 24, 32, 40, 64])
+def test_w4a4_gemv_wide_batches_int32_exact(torch_cuda, M):
+    """Decode batches of 17..64 tokens: the weight-streaming GEMV with B fragments read from the
+    tiled codes in global memory (rows padded to 32 / 64)."""
+    torch = torch_cuda
+    rng = np.random.default_rng(300 + M)
+    K, N = 1024, 272
+    a = rng.integers(-7, 8, size=(M, K))
+    w = rng.integers(-7, 8, size=(N, K))
+    sa = rng.uniform(0.01, 0.5, M)
+    sw = rng.uniform(0.001, 0.01, N)
+    ad = torch.from_numpy(_tiled(a, pad=64)).cuda()
+    out = torch.zeros((M, N), dtype=torch.float32, device="cuda")
+    acc = torch.zeros((M, N), dtype=torch.int32, device="cuda")
+    Q.w4a4_gemm(Q.EPI_STORE, ad, torch.from_numpy(sa).cuda(), torch.from_numpy(_tiled(w)).cuda(),
+                torch.from_numpy(sw).cuda(), M, N, K, out, acc, impl=0)
+    torch.cuda.synchronize()
+    exp = a.astype(np.int64) @ w.T.astype(np.int64)
+    assert np.array_equal(acc.cpu().numpy(), exp)
+    np.testing.assert_allclose(out.cpu().numpy(), exp * sa[:, None] * sw[None, :], rtol=2e-7, atol=1e-7)
