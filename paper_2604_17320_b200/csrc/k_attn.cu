@@ -118,7 +118,7 @@ QT_DEV void qk_tile(const uint32_t (*qh)[4], const uint32_t (*ql)[4], const __ha
 
 // ============================================================== K7
 template <int DH>
-__global__ void __launch_bounds__(128) k_attn_prefill(const float* __restrict__ qkv, int ldq, int H, int Hkv,
+__global__ void __launch_bounds__(128, 3) k_attn_prefill(const float* __restrict__ qkv, int ldq, int H, int Hkv,
                                                       const int* __restrict__ seq_off, const int* __restrict__ vis,
                                                       const int* __restrict__ seq_len,
                                                       const uint8_t* __restrict__ pool, long long page_bytes,
@@ -152,6 +152,14 @@ __global__ void __launch_bounds__(128) k_attn_prefill(const float* __restrict__ 
         const uint8_t* page = page_base(pool, page_bytes, pt, max_pages, b, k0);
         load_kv_tile<DH>(page, Hkv, kh, min(AT_K, S - k0), Ks, Vt, ks, vs, true);
         __syncthreads();
+        // warp-uniform tile classification against the reference mask (model.cpp:35-44):
+        // `none` -> no (query, key) pair of this warp's 16 rows x 64 keys is allowed;
+        // `full` -> every pair is allowed and in range, so the per-element test is skipped
+        const int klast = k0 + AT_K - 1, qlast = wq0 + 15;
+        const bool none = wq0 >= S || (qlast < V && k0 >= V);
+        const bool full = qlast < S && klast < S &&
+                          (qlast < V ? klast < V : (wq0 >= V && (klast < V || klast <= wq0)));
+        if (none) continue;  // no MMA needed (the block-wide syncs stay uniform)
         float sc[AT_K / 8][4];
         qk_tile<DH>(qh, ql, Ks, sc);
         // scale, mask, row max
@@ -163,7 +171,7 @@ __global__ void __launch_bounds__(128) k_attn_prefill(const float* __restrict__ 
                 const int r = e >> 1;
                 const int kj = k0 + t * 8 + 2 * tig + (e & 1);
                 const int q = qi[r];
-                bool ok = q < S && kj < S && (q < V ? kj < V : (kj < V || kj <= q));
+                const bool ok = full || (q < S && kj < S && (q < V ? kj < V : (kj < V || kj <= q)));
                 float s = ok ? sc[t][e] * ks[t * 8 + 2 * tig + (e & 1)] * inv_sqrt : -1e30f;
                 sc[t][e] = s;
                 tmax[r] = fmaxf(tmax[r], s);
