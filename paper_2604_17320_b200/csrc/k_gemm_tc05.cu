@@ -35,7 +35,10 @@ constexpr int T5_BM = 128, T5_BN = 256, T5_BKB = 64;  // BK = 128 int4 = 64 pack
 constexpr int T5_PS = 3, T5_IS = 3, T5_ACC = 2;       // packed stages, int8 stages, TMEM accumulators
 constexpr int T5_PA = T5_BM * T5_BKB, T5_PB = T5_BN * T5_BKB;  // packed bytes per stage
 constexpr int T5_IA = T5_BM * 128, T5_IB = T5_BN * 128;        // int8 bytes per stage
-constexpr int T5_THREADS = 320;  // 0 TMA, 1 MMA, 2-5 converters, 6-9 epilogue
+constexpr int T5_CW = 8;                         // converter warps
+constexpr int T5_CT = T5_CW * 32;                // converter threads
+constexpr int T5_EW0 = 2 + T5_CW;                // first epilogue warp
+constexpr int T5_THREADS = (T5_EW0 + 4) * 32;    // 0 TMA, 1 MMA, 2..T5_EW0-1 converters, 4 epilogue warps
 
 struct T5Smem {
     // int8 ring first: 1024-byte aligned SW128 atoms
@@ -113,6 +116,20 @@ QT_DEV void convert_chunk(const uint8_t* packed, uint8_t* i8, int row, int q) {
     *reinterpret_cast<uint4*>(atom + ((c1 ^ sw) << 4)) = o1;
 }
 
+// unpack one packed 16-byte chunk (32 k of one row) already in registers -> two
+// swizzled int8 16-byte chunks
+QT_DEV void store_converted(const uint4 w, uint8_t* i8, int row, int q) {
+    uint4 o0, o1;
+    unpack_x16(w.x, o0.x, o0.y);
+    unpack_x16(w.y, o0.z, o0.w);
+    unpack_x16(w.z, o1.x, o1.y);
+    unpack_x16(w.w, o1.z, o1.w);
+    uint8_t* atom = i8 + (size_t)(row >> 3) * 1024 + (row & 7) * 128;
+    const int c0 = 2 * q, c1 = 2 * q + 1, sw = row & 7;
+    *reinterpret_cast<uint4*>(atom + ((c0 ^ sw) << 4)) = o0;
+    *reinterpret_cast<uint4*>(atom + ((c1 ^ sw) << 4)) = o1;
+}
+
 template <int EPI>
 __global__ void __launch_bounds__(T5_THREADS, 1) k_gemm_tc05(const uint8_t* __restrict__ A, int lda,
                                                               const double* __restrict__ sa,
@@ -144,10 +161,10 @@ __global__ void __launch_bounds__(T5_THREADS, 1) k_gemm_tc05(const uint8_t* __re
     if (threadIdx.x == 0) {
         for (int s = 0; s < T5_PS; ++s) {
             mbar_init(&pfull[s], 1);
-            mbar_init(&pempty[s], 4);
+            mbar_init(&pempty[s], T5_CW);
         }
         for (int s = 0; s < T5_IS; ++s) {
-            mbar_init(&ifull[s], 4);
+            mbar_init(&ifull[s], T5_CW);
             mbar_init(&iempty[s], 1);
         }
         for (int s = 0; s < T5_ACC; ++s) {
@@ -215,8 +232,10 @@ __global__ void __launch_bounds__(T5_THREADS, 1) k_gemm_tc05(const uint8_t* __re
             }
         }
         __syncwarp();
-    } else if (warp < 6) {
-        // ---------------- converters: packed int4 -> swizzled int8 (128 threads)
+    } else if (warp < T5_EW0) {
+        // ---------------- converters: packed int4 -> swizzled int8 (T5_CT threads); every
+        // thread first loads all of its packed chunks of the stage, then unpacks and stores
+        constexpr int CA = (T5_BM * 4) / T5_CT, CB = (T5_BN * 4) / T5_CT;
         const int ct = threadIdx.x - 64;
         int it = 0;
         for (int u = blockIdx.x; u < units; u += gridDim.x) {
@@ -224,36 +243,49 @@ __global__ void __launch_bounds__(T5_THREADS, 1) k_gemm_tc05(const uint8_t* __re
             for (int kb = sl * KB / ksplit; kb < (sl + 1) * KB / ksplit; ++kb, ++it) {
                 const int ps = it % T5_PS, is = it % T5_IS;
                 mbar_wait(&pfull[ps], (it / T5_PS) & 1);
-                if (it >= T5_IS) mbar_wait(&iempty[is], ((it / T5_IS) - 1) & 1);
                 const uint8_t* pa = smem + T5Smem::pa + (size_t)ps * T5_PA;
                 const uint8_t* pb = smem + T5Smem::pb + (size_t)ps * T5_PB;
-                uint8_t* ia = smem + T5Smem::ia + (size_t)is * T5_IA;
-                uint8_t* ib = smem + T5Smem::ib + (size_t)is * T5_IB;
                 // rows past the valid row blocks convert stale bytes; never stored
+                uint4 wa[CA], wb[CB];
 #pragma unroll
-                for (int i = 0; i < (T5_BM * 4) / 128; ++i) {
-                    const int c = ct + 128 * i;
-                    convert_chunk(pa, ia, c >> 2, c & 3);
+                for (int i = 0; i < CA; ++i) {
+                    const int c = ct + T5_CT * i;
+                    wa[i] = *reinterpret_cast<const uint4*>(pa + (size_t)(c >> 2) * T5_BKB + (c & 3) * 16);
                 }
 #pragma unroll
-                for (int i = 0; i < (T5_BN * 4) / 128; ++i) {
-                    const int c = ct + 128 * i;
-                    convert_chunk(pb, ib, c >> 2, c & 3);
+                for (int i = 0; i < CB; ++i) {
+                    const int c = ct + T5_CT * i;
+                    wb[i] = *reinterpret_cast<const uint4*>(pb + (size_t)(c >> 2) * T5_BKB + (c & 3) * 16);
+                }
+                // the packed stage is in registers: order these generic-proxy reads before the
+                // TMA (async proxy) refill of the stage, then release it
+                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&pempty[ps]);
+                if (it >= T5_IS) mbar_wait(&iempty[is], ((it / T5_IS) - 1) & 1);
+                uint8_t* ia = smem + T5Smem::ia + (size_t)is * T5_IA;
+                uint8_t* ib = smem + T5Smem::ib + (size_t)is * T5_IB;
+#pragma unroll
+                for (int i = 0; i < CA; ++i) {
+                    const int c = ct + T5_CT * i;
+                    store_converted(wa[i], ia, c >> 2, c & 3);
+                }
+#pragma unroll
+                for (int i = 0; i < CB; ++i) {
+                    const int c = ct + T5_CT * i;
+                    store_converted(wb[i], ib, c >> 2, c & 3);
                 }
                 asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
                 __syncwarp();
-                if (lane == 0) {
-                    mbar_arrive(&ifull[is]);
-                    mbar_arrive(&pempty[ps]);
-                }
+                if (lane == 0) mbar_arrive(&ifull[is]);
             }
         }
     } else {
-        // ---------------- epilogue warpgroup (warps 6..9 -> TMEM lane quarters 2,3,0,1)
+        // ---------------- epilogue warpgroup (4 consecutive warps -> all four TMEM lane quarters)
         pdl_wait();  // scales / residual come from upstream kernels
         pdl_launch_dependents();
         const int q = warp & 3;
-        const int et = threadIdx.x - 192;
+        const int et = threadIdx.x - T5_EW0 * 32;
         int tl = 0;
         for (int u = blockIdx.x; u < units; u += gridDim.x, ++tl) {
             const int t = u % tiles, sl = u / tiles;
