@@ -38,7 +38,9 @@ constexpr int T5_IA = T5_BM * 128, T5_IB = T5_BN * 128;        // int8 bytes per
 constexpr int T5_CW = 8;                         // converter warps
 constexpr int T5_CT = T5_CW * 32;                // converter threads
 constexpr int T5_EW0 = 2 + T5_CW;                // first epilogue warp
-constexpr int T5_THREADS = (T5_EW0 + 4) * 32;    // 0 TMA, 1 MMA, 2..T5_EW0-1 converters, 4 epilogue warps
+constexpr int T5_EWN = 8;                        // epilogue warps: 2 per TMEM lane quarter (column halves)
+constexpr int T5_ET = T5_EWN * 32;
+constexpr int T5_THREADS = (T5_EW0 + T5_EWN) * 32;  // 0 TMA, 1 MMA, converters, epilogue
 
 struct T5Smem {
     // int8 ring first: 1024-byte aligned SW128 atoms
@@ -169,7 +171,7 @@ __global__ void __launch_bounds__(T5_THREADS, 1) k_gemm_tc05(const uint8_t* __re
         }
         for (int s = 0; s < T5_ACC; ++s) {
             mbar_init(&tfull[s], 1);
-            mbar_init(&tempty[s], 4);
+            mbar_init(&tempty[s], T5_EWN);
         }
         mbar_fence_init();
     }
@@ -281,39 +283,43 @@ __global__ void __launch_bounds__(T5_THREADS, 1) k_gemm_tc05(const uint8_t* __re
             }
         }
     } else {
-        // ---------------- epilogue warpgroup (4 consecutive warps -> all four TMEM lane quarters)
+        // ---------------- epilogue: 8 warps; warp & 3 = TMEM lane quarter (32 rows), and
+        // (warp - T5_EW0) / 4 = column half -- the per-element fp64 scale math is split 2 ways
         pdl_wait();  // scales / residual come from upstream kernels
         pdl_launch_dependents();
         const int q = warp & 3;
         const int et = threadIdx.x - T5_EW0 * 32;
+        const int jh = ((warp - T5_EW0) >> 2) * (T5_BN / 64);  // first 32-column chunk of this half
         int tl = 0;
         for (int u = blockIdx.x; u < units; u += gridDim.x, ++tl) {
             const int t = u % tiles, sl = u / tiles;
             const int acc = tl % T5_ACC;
             const int m0 = (t % mt_n) * T5_BM, n0 = (t / mt_n) * T5_BN;
             double* swt = sws + acc * T5_BN;
-            for (int i = et; i < T5_BN; i += 128) swt[i] = n0 + i < N ? sw[n0 + i] : 0.0;
+            for (int i = et; i < T5_BN; i += T5_ET) swt[i] = n0 + i < N ? sw[n0 + i] : 0.0;
             if (EPI == QT_EPI_RESADD && ksplit == 1) {
                 // pull this thread's residual row segment (256 fp64) toward L2 while the
                 // tile's MMAs run: the read-modify-write below then hits L2, not HBM
                 const int mr = m0 + q * 32 + lane;
-                if (mr < M) {
-                    const char* rp = reinterpret_cast<const char*>(static_cast<const double*>(out) + (size_t)mr * ldo + n0);
-                    const int nb = min(T5_BN, N - n0) * 8;
+                const int c0 = jh * 32;
+                if (mr < M && n0 + c0 < N) {
+                    const char* rp =
+                        reinterpret_cast<const char*>(static_cast<const double*>(out) + (size_t)mr * ldo + n0 + c0);
+                    const int nb = min(T5_BN / 2, N - n0 - c0) * 8;
                     for (int c = 0; c < nb; c += 128) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(rp + c));
                 }
             }
-            asm volatile("bar.sync 2, 128;\n" ::: "memory");
+            asm volatile("bar.sync 2, %0;\n" ::"n"(T5_ET) : "memory");
             mbar_wait(&tfull[acc], (tl / T5_ACC) & 1);
             tc_fence_after();
             const int m = m0 + q * 32 + lane;
             const double a_s = m < M ? sa[m] : 0.0;
             const uint32_t tacc = tmem + (uint32_t)(acc * T5_BN) + ((uint32_t)(q * 32) << 16);
 #pragma unroll 1
-            for (int j = 0; j < T5_BN / 32; ++j) {
+            for (int j = jh; j < jh + T5_BN / 64; ++j) {
                 uint32_t r[32];
                 tmem_ld32(tacc + (uint32_t)(j * 32), r);
-                if (j == T5_BN / 32 - 1) {
+                if (j == jh + T5_BN / 64 - 1) {
                     // accumulator fully read: hand it back to the MMA issuer
                     tc_fence_before();
                     __syncwarp();
@@ -343,7 +349,7 @@ __global__ void __launch_bounds__(T5_THREADS, 1) k_gemm_tc05(const uint8_t* __re
                                            (double)((int)r[e + 1] >> 8) * (a_s * swt[j * 32 + e + 1]), N);
                 }
             }
-            asm volatile("bar.sync 2, 128;\n" ::: "memory");  // swt reuse
+            asm volatile("bar.sync 2, %0;\n" ::"n"(T5_ET) : "memory");  // swt reuse
         }
     }
     tc_fence_before();
