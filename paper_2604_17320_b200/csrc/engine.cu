@@ -287,6 +287,9 @@ struct qt_engine {
     unsigned* seq_cnt = nullptr;  // per-sequence arrival counters of the fused decode attention block
     // opt-in (QT_ATTN_FUSED=1): one kernel for RoPE + KV append + attention + attn_out quant; measured
     // no faster than the three-kernel PDL chain at B = 8
+    // opt-in (QT_DEC_ROPE_FUSED=1): RoPE + new-token K/V append inside the decode attention kernel;
+    // measured slower (the last-page CTAs become stragglers), DESIGN.md §4
+    bool rope_fused = std::getenv("QT_DEC_ROPE_FUSED") && std::atoi(std::getenv("QT_DEC_ROPE_FUSED")) == 1;
     bool fused_attn = std::getenv("QT_ATTN_FUSED") && std::atoi(std::getenv("QT_ATTN_FUSED")) == 1;
     unsigned long long* mk_trace = nullptr;
     // opt-in (QT_DECODE_MK=1): measured slower than the graph path at B = 8
@@ -984,17 +987,21 @@ struct qt_engine {
                 for (int b = 0; b < B; ++b) rows += h_kvlen[(size_t)l * B + b] + 1;
                 pe(rows * Hkv * 2 * (dh / 2 + 4) + (double)B * n_qkv * 4 + (double)B * d * 8);
             } else {
-                pb(P_KV);
-                if (!(g_skip & 8)) ckl(qt_launch_rope_kv_append(qkv, n_qkv, B, H, Hkv, dh, next_pos, dec_seq, lenl, rope, ptl, max_pages,
-                                             pool, page_bytes, 4, nullptr, st),
-                    "decode kv append");
-                pe((double)B * n_qkv * 8 + (double)B * Hkv * 2 * (dh / 2 + 4));
+                if (!rope_fused) {
+                    pb(P_KV);
+                    if (!(g_skip & 8)) ckl(qt_launch_rope_kv_append(qkv, n_qkv, B, H, Hkv, dh, next_pos, dec_seq, lenl, rope, ptl, max_pages,
+                                                 pool, page_bytes, 4, nullptr, st),
+                        "decode kv append");
+                    pe((double)B * n_qkv * 8 + (double)B * Hkv * 2 * (dh / 2 + 4));
+                }
                 pb(P_ATTN);
-                // decode attention over int4 pages + split merge fused with the attn_out quantizer
+                // decode attention over int4 pages (RoPE + K/V append fused in) + split merge fused
+                // with the attn_out quantizer
                 if (!(g_skip & 2))
                     ckl(qt_launch_attn_decode(qkv, n_qkv, H, Hkv, dh, lenl, 1, B, pool, page_bytes, ptl, max_pages,
                                               dec_splits, part_ml, part_o, nullptr, d, codes, codes_rows, ascale,
-                                              cfg.act_mode, cfg.act_mode == 0 ? act[4 * l + 1] : 0.0, kd_pad, 4, st),
+                                              cfg.act_mode, cfg.act_mode == 0 ? act[4 * l + 1] : 0.0, kd_pad, 4,
+                                              rope_fused ? rope : nullptr, rope_fused ? next_pos : nullptr, st),
                         "decode attention");
                 {  // decode attention streams every cached K/V row of this layer once
                     double rows = 0;

@@ -331,12 +331,19 @@ __global__ void __launch_bounds__(128) k_attn_colsum(const float* __restrict__ q
 // replays from a CUDA graph.  Each warp owns 16 rows; 4 lanes per row each
 // hold 32 channels (16 bytes of int4 codes), and both of a lane's rows are
 // loaded before any math so two 128-bit loads per operand are in flight.
+//
+// rope != nullptr (the decode step, K5 fused in): q is RoPE'd in registers from
+// the raw GEMV output, and the CTAs of the page holding the new row (row
+// kv_len) RoPE + quantize that token's K and V (kv_quantize, quant.cpp:117-119)
+// and append them before attending -- one launch instead of two.  With GQA the
+// group's query-head CTAs write identical bytes.
 template <int DH>
 __global__ void __launch_bounds__(128) k_attn_decode(const float* __restrict__ qkv, int ldq, int H, int Hkv,
                                                      const int* __restrict__ kv_len, int len_add,
-                                                     const uint8_t* __restrict__ pool, long long page_bytes,
+                                                     uint8_t* __restrict__ pool, long long page_bytes,
                                                      const int* __restrict__ pt, int max_pages, float inv_sqrt,
-                                                     float* __restrict__ part_ml, float* __restrict__ part_o) {
+                                                     float* __restrict__ part_ml, float* __restrict__ part_o,
+                                                     const double2* __restrict__ rope, const int* __restrict__ pos) {
     constexpr int CPL = DH / 4;  // channels per lane
     constexpr int R = 2;         // rows per lane
     pdl_launch_dependents();
@@ -348,6 +355,45 @@ __global__ void __launch_bounds__(128) k_attn_decode(const float* __restrict__ q
     const int len = kv_len[b] + len_add;
     const int r0 = pg * kPage;
     const size_t pidx = ((size_t)b * H + h) * npg + pg;
+    const double2* rt = rope ? rope + (size_t)pos[b] * (DH / 2) : nullptr;
+    if (rope && pg == (len - 1) / kPage && warp < 2) {
+        // append the new token's K (warp 0, RoPE'd) or V (warp 1) of kv head kh at row len-1
+        constexpr int E = DH / 32;
+        const int r = len - 1;
+        const bool is_k = warp == 0;
+        const float* src = qkv + (size_t)b * ldq + (is_k ? H * DH : (H + Hkv) * DH) + kh * DH;
+        double val[E];
+#pragma unroll
+        for (int j = 0; j < E; ++j) val[j] = (double)src[lane * E + j];
+        if (is_k) {
+#pragma unroll
+            for (int j = 0; j < E; j += 2) {
+                const double2 cs = rt[(lane * E + j) / 2];
+                const double a = val[j], bb = val[j + 1];
+                val[j] = __dsub_rn(__dmul_rn(a, cs.x), __dmul_rn(bb, cs.y));
+                val[j + 1] = __dadd_rn(__dmul_rn(a, cs.y), __dmul_rn(bb, cs.x));
+            }
+        }
+        double mx = 0.0;
+#pragma unroll
+        for (int j = 0; j < E; ++j) mx = fmax(mx, fabs(val[j]));
+        mx = warp_max(mx);
+        const double s = q_scale(mx, 7), inv_s = 1.0 / s;
+        int c[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int j = 0; j < E; ++j) c[j] = q_code_r(val[j], s, inv_s, 7);
+        uint8_t* page = pool + (long long)pt[b * max_pages + r / kPage] * page_bytes;
+        const size_t cbn = (size_t)Hkv * kPage * (DH / 2);
+        uint8_t* dst = page + (is_k ? 0 : cbn) + ((size_t)kh * kPage + r % kPage) * (DH / 2) + lane * E / 2;
+        if (E == 4)
+            *reinterpret_cast<uint16_t*>(dst) =
+                (uint16_t)((c[0] & 0xF) | ((c[1] & 0xF) << 4) | ((c[2] & 0xF) << 8) | ((c[3] & 0xF) << 12));
+        else
+            *dst = (uint8_t)((c[0] & 0xF) | ((c[1] & 0xF) << 4));
+        if (lane == 0)
+            reinterpret_cast<float*>(page + 2 * cbn)[(is_k ? 0 : Hkv * kPage) + kh * kPage + r % kPage] = (float)s;
+    }
+    if (rope) __syncthreads();  // the appended row is visible to the block's loads below
     if (r0 >= len) {
         if (threadIdx.x < DH) part_o[pidx * DH + threadIdx.x] = 0.f;
         if (threadIdx.x == 0) {
@@ -387,6 +433,15 @@ __global__ void __launch_bounds__(128) k_attn_decode(const float* __restrict__ q
     for (int i = 0; i < CPL; i += 4) {
         float4 v = *reinterpret_cast<const float4*>(qp + i);
         q[i] = v.x; q[i + 1] = v.y; q[i + 2] = v.z; q[i + 3] = v.w;
+    }
+    if (rope) {  // interleaved-pair RoPE of q in fp32 (q only feeds fp32 scores; K keeps the fp64 path)
+#pragma unroll
+        for (int i = 0; i < CPL; i += 2) {
+            const double2 cs = rt[(q4 * CPL + i) / 2];
+            const float c = (float)cs.x, sn = (float)cs.y, a = q[i], bb = q[i + 1];
+            q[i] = fmaf(a, c, -bb * sn);
+            q[i + 1] = fmaf(a, sn, bb * c);
+        }
     }
     float s[R];
 #pragma unroll
@@ -578,9 +633,11 @@ int qt_launch_attn_colsum(const float* qkv, int ldq, int H, int Hkv, int dh, con
 }
 
 int qt_launch_attn_decode(const float* qkv, int ldq, int H, int Hkv, int dh, const int* kv_len, int len_add, int B,
-                          const uint8_t* pool, long long page_bytes, const int* pt, int max_pages, int n_pages,
+                          uint8_t* pool, long long page_bytes, const int* pt, int max_pages, int n_pages,
                           float* part_ml, float* part_o, float* out, int ldo, uint8_t* codes, int ld_codes,
-                          double* scales, int qmode, double static_scale, int d_pad, int bits, cudaStream_t st) {
+                          double* scales, int qmode, double static_scale, int d_pad, int bits, const double* rope,
+                          const int* pos, cudaStream_t st) {
+    const double2* rt = reinterpret_cast<const double2*>(rope);
     if (B <= 0) return 0;
     if (H > 64) return -1;
     const dim3 grid(n_pages, H, B);
@@ -589,7 +646,7 @@ int qt_launch_attn_decode(const float* qkv, int ldq, int H, int Hkv, int dh, con
     int rc;
     if (dh == 128) {
         rc = launch_pdl(k_attn_decode<128>, grid, dim3(128), 0, st, qkv, ldq, H, Hkv, kv_len, len_add, pool,
-                        page_bytes, pt, max_pages, inv_sqrt, part_ml, part_o);
+                        page_bytes, pt, max_pages, inv_sqrt, part_ml, part_o, rt, pos);
         if (rc) return rc;
         auto mk = H > 32 ? k_attn_merge_quant<128, 64> : k_attn_merge_quant<128, 32>;
         return launch_pdl(mk, dim3(B), dim3(1024), 0, st, (const float*)part_ml, (const float*)part_o, n_pages, H, out,
@@ -597,7 +654,7 @@ int qt_launch_attn_decode(const float* qkv, int ldq, int H, int Hkv, int dh, con
     }
     if (dh == 64) {
         rc = launch_pdl(k_attn_decode<64>, grid, dim3(128), 0, st, qkv, ldq, H, Hkv, kv_len, len_add, pool,
-                        page_bytes, pt, max_pages, inv_sqrt, part_ml, part_o);
+                        page_bytes, pt, max_pages, inv_sqrt, part_ml, part_o, rt, pos);
         if (rc) return rc;
         auto mk = H > 32 ? k_attn_merge_quant<64, 64> : k_attn_merge_quant<64, 32>;
         return launch_pdl(mk, dim3(B), dim3(1024), 0, st, (const float*)part_ml, (const float*)part_o, n_pages, H, out,

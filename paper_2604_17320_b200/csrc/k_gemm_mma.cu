@@ -151,6 +151,9 @@ __global__ void __launch_bounds__(256) k_gemm_tc(const uint8_t* __restrict__ A, 
 }
 
 // ---------------------------------------------------------------- decode GEMV
+// row blocks per CTA beyond the first whose weights are L2-prefetched before the
+// dependency wait (QT_GEMV_L2 to override; 0 disables)
+static const int qt_gemv_l2_rows_host = getenv("QT_GEMV_L2") ? atoi(getenv("QT_GEMV_L2")) : 1;
 // Persistent, HBM-streaming GEMV for decode (M <= 16 tokens).  Each CTA owns a
 // strided set of 16-channel row blocks; its 8 warps split K.  The token codes
 // are staged once per CTA in smem.  Weight loads run one batch (U tiles of
@@ -168,7 +171,7 @@ template <int NT, int EPI>
 __global__ void __launch_bounds__(256) k_gemv_reg(const uint8_t* __restrict__ A, int lda, const double* __restrict__ sa,
                                                   const uint8_t* __restrict__ W, int ldw, const double* __restrict__ sw,
                                                   int M, int N, int K, void* __restrict__ out, int ldo,
-                                                  int* __restrict__ acc_dbg) {
+                                                  int* __restrict__ acc_dbg, int l2rows) {
     constexpr int TOK = 8 * NT;
     constexpr bool ASM = NT <= 2;     // activation codes staged in smem
     constexpr int U = NT <= 2 ? 4 : 2;
@@ -197,6 +200,21 @@ __global__ void __launch_bounds__(256) k_gemv_reg(const uint8_t* __restrict__ A,
     };
     int rb = blockIdx.x, bat = 0;
     fetch(rb, 0, wa, wb);
+    {   // weights do not depend on the upstream kernel: while it still runs, pull this warp's
+        // k slice of the CTA's next row blocks toward L2 (fire-and-forget, no registers)
+        const int pre_rb = l2rows;
+        for (int j = 1; j <= pre_rb; ++j) {
+            const int r2 = blockIdx.x + j * gridDim.x;
+            if (r2 >= n_rb) break;
+            for (int c = ch0 + (lane >> 3); c < ch1; c += 4)  // 8 lanes x 128 B per 1 KB tile
+                asm volatile("prefetch.global.L2 [%0];\n" ::"l"(W + ((size_t)c * (ldw >> 4) + r2) * 1024 +
+                                                               (lane & 7) * 128));
+        }
+        if (nbat > 1)  // and the rest of the first row block beyond the register batch
+            for (int c = ch0 + U + (lane >> 3); c < ch1; c += 4)
+                asm volatile("prefetch.global.L2 [%0];\n" ::"l"(W + ((size_t)c * (ldw >> 4) + rb) * 1024 +
+                                                               (lane & 7) * 128));
+    }
     pdl_wait();
     if (ASM) {
         for (int c = tid; c < TOK * (kb / 16); c += 256) {
@@ -303,13 +321,15 @@ int launch_gemm(const uint8_t* A, int lda, const double* sa, const uint8_t* W, i
             const size_t smem = (size_t)8 * 16 * 32 * 4;
             auto kfn = k_gemv_reg<4, EPI>;
             cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            return launch_pdl(kfn, grid, dim3(256), smem, st, A, lda, sa, W, ldw, sw, M, N, K, out, ldo, acc_dbg);
+            return launch_pdl(kfn, grid, dim3(256), smem, st, A, lda, sa, W, ldw, sw, M, N, K, out, ldo, acc_dbg,
+                              qt_gemv_l2_rows_host);
         }
         if (lda >= 64) {
             const size_t smem = (size_t)8 * 16 * 64 * 4;
             auto kfn = k_gemv_reg<8, EPI>;
             cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            return launch_pdl(kfn, grid, dim3(256), smem, st, A, lda, sa, W, ldw, sw, M, N, K, out, ldo, acc_dbg);
+            return launch_pdl(kfn, grid, dim3(256), smem, st, A, lda, sa, W, ldw, sw, M, N, K, out, ldo, acc_dbg,
+                              qt_gemv_l2_rows_host);
         }
     }
     if (M <= 16) {
@@ -323,11 +343,13 @@ int launch_gemm(const uint8_t* A, int lda, const double* sa, const uint8_t* W, i
         if (TOK == 8) {
             auto kfn = k_gemv_reg<1, EPI>;
             cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            return launch_pdl(kfn, grid, dim3(256), smem, st, A, lda, sa, W, ldw, sw, M, N, K, out, ldo, acc_dbg);
+            return launch_pdl(kfn, grid, dim3(256), smem, st, A, lda, sa, W, ldw, sw, M, N, K, out, ldo, acc_dbg,
+                              qt_gemv_l2_rows_host);
         }
         auto kfn = k_gemv_reg<2, EPI>;
         cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        return launch_pdl(kfn, grid, dim3(256), smem, st, A, lda, sa, W, ldw, sw, M, N, K, out, ldo, acc_dbg);
+        return launch_pdl(kfn, grid, dim3(256), smem, st, A, lda, sa, W, ldw, sw, M, N, K, out, ldo, acc_dbg,
+                              qt_gemv_l2_rows_host);
     }
     if (M <= 512 || (long long)((M + 127) / 128) * nb < 148) {
         constexpr int BM = 64;

@@ -50,10 +50,12 @@ int qt_launch_attn_colsum(const float* qkv, int ldq, int H, int Hkv, int dh, con
                           const int* seq_len, int B, int vmax, const uint8_t* pool, long long page_bytes,
                           const int* pt, int max_pages, const float* ml, int vstride, float* inter, float* intra,
                           cudaStream_t st);
+// rope/pos non-null: RoPE of q and the new token's K/V append fused in (decode step)
 int qt_launch_attn_decode(const float* qkv, int ldq, int H, int Hkv, int dh, const int* kv_len, int len_add, int B,
-                          const uint8_t* pool, long long page_bytes, const int* pt, int max_pages, int n_pages,
+                          uint8_t* pool, long long page_bytes, const int* pt, int max_pages, int n_pages,
                           float* part_ml, float* part_o, float* out, int ldo, uint8_t* codes, int ld_codes,
-                          double* scales, int qmode, double static_scale, int d_pad, int bits, cudaStream_t st);
+                          double* scales, int qmode, double static_scale, int d_pad, int bits, const double* rope,
+                          const int* pos, cudaStream_t st);
 int qt_launch_select_topk(const double* mag, const double* res, const float* inter, const float* intra, int H,
                           int vstride, const int* vis, const int* txt, const int* budget, const int* old_off,
                           const int* new_off, int B, int vmax, const double* w4, int* keep_src, int* keep_local,
