@@ -136,6 +136,7 @@ __global__ void __launch_bounds__(128, 3) k_attn_prefill(const float* __restrict
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, tig = lane & 3;
     const int tok0 = seq_off[b];
     const int wq0 = q0 + warp * 16;  // first query row of this warp (index in sequence)
+    const float sl2 = inv_sqrt * 1.4426950408889634f;  // 1/sqrt(dh) * log2(e)
 
     uint32_t qh[DH / 16][4], ql[DH / 16][4];
     load_q_frags<DH>(qkv, ldq, tok0 + wq0, S - wq0, h, qh, ql);
@@ -152,6 +153,7 @@ __global__ void __launch_bounds__(128, 3) k_attn_prefill(const float* __restrict
         const uint8_t* page = page_base(pool, page_bytes, pt, max_pages, b, k0);
         load_kv_tile<DH>(page, Hkv, kh, min(AT_K, S - k0), Ks, Vt, ks, vs, true);
         __syncthreads();
+        // scores in log2 units: s2 = q.k * (scale_k / sqrt(dh) * log2 e), p = 2^(s2 - m2)
         // warp-uniform tile classification against the reference mask (model.cpp:35-44):
         // `none` -> no (query, key) pair of this warp's 16 rows x 64 keys is allowed;
         // `full` -> every pair is allowed and in range, so the per-element test is skipped
@@ -172,7 +174,7 @@ __global__ void __launch_bounds__(128, 3) k_attn_prefill(const float* __restrict
                 const int kj = k0 + t * 8 + 2 * tig + (e & 1);
                 const int q = qi[r];
                 const bool ok = full || (q < S && kj < S && (q < V ? kj < V : (kj < V || kj <= q)));
-                float s = ok ? sc[t][e] * ks[t * 8 + 2 * tig + (e & 1)] * inv_sqrt : -1e30f;
+                float s = ok ? sc[t][e] * (ks[t * 8 + 2 * tig + (e & 1)] * sl2) : -1e30f;
                 sc[t][e] = s;
                 tmax[r] = fmaxf(tmax[r], s);
             }
@@ -183,7 +185,7 @@ __global__ void __launch_bounds__(128, 3) k_attn_prefill(const float* __restrict
             tmax[r] = fmaxf(tmax[r], __shfl_xor_sync(0xffffffffu, tmax[r], 1));
             tmax[r] = fmaxf(tmax[r], __shfl_xor_sync(0xffffffffu, tmax[r], 2));
             const float mn = fmaxf(mrow[r], tmax[r]);
-            alpha[r] = expf(mrow[r] - mn);
+            alpha[r] = exp2f(mrow[r] - mn);
             mrow[r] = mn;
         }
         float psum[2] = {0.f, 0.f};
@@ -194,7 +196,7 @@ __global__ void __launch_bounds__(128, 3) k_attn_prefill(const float* __restrict
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 const int r = e >> 1;
-                p[e] = sc[t][e] <= -1e30f ? 0.f : expf(sc[t][e] - mrow[r]);
+                p[e] = sc[t][e] <= -1e30f ? 0.f : exp2f(sc[t][e] - mrow[r]);
                 psum[r] += p[e];
                 p[e] *= vs[t * 8 + 2 * tig + (e & 1)];
             }
@@ -238,7 +240,8 @@ __global__ void __launch_bounds__(128, 3) k_attn_prefill(const float* __restrict
             float2 v = make_float2(o[t][2 * r] * inv_l, o[t][2 * r + 1] * inv_l);
             *reinterpret_cast<float2*>(orow + t * 8 + 2 * tig) = v;
         }
-        if (ml && tig == 0) ml[(size_t)(tok0 + q) * H + h] = make_float2(mrow[r], lrow[r]);
+        // row max back in natural-log units for the QUOTA column sums (k_attn_colsum uses expf)
+        if (ml && tig == 0) ml[(size_t)(tok0 + q) * H + h] = make_float2(mrow[r] * 0.69314718055994531f, lrow[r]);
     }
 }
 
