@@ -8,7 +8,7 @@ Two checkers, both plain fp64 C++ behind ctypes:
 * ``Port``   -- oracle/_build/libquota_oracle.so: the restatement
   oracle/quota_oracle.cpp (R1) with the north_star switches (per-token
   activation scales, per-output-channel weights, SwiGLU, GQA).  Pinned to R0
-  bit-for-bit by tests/test_oracle_pin.py.
+  bit-for-bit by tests/test_oracle_cpu.py.
 
 Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
 ``--impl reference`` leg may import this package.  The product

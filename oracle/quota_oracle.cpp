@@ -10,7 +10,7 @@
 // quant.cpp:39-119, numeric.cpp:33-96).  Every routine cites the lines it
 // follows and keeps the reference's fp64 operation order, so with the switches
 // at their reference values it reproduces the reference bit for bit
-// (tests/test_oracle_pin.py checks logits, KV codes and prune traces against
+// (tests/test_oracle_cpu.py checks logits, KV codes and prune traces against
 // oracle/_ref/libquota_ref.so, the unmodified reference).
 //
 // Switches (SURVEY.md §0.1 semantic deltas) beyond the reference:

@@ -82,3 +82,20 @@ def test_backend_without_gpu_fails_loudly(tmp_path):
     r, _ = _run(tmp_path, "x.txt", True)
     assert r.returncode != 0
     assert "no CPU fallback" in r.stderr
+
+
+@pytest.mark.gpu
+def test_reference_api_client_without_host_kv(tmp_path):
+    """QUOTA_B200_HOST_KV=0: the returned KVCacheState carries layout and positions only (no
+    host copy of the int4 cache); decode still runs on the device session."""
+    r, cpu = _run(tmp_path, "cpu.txt", False)
+    assert r.returncode == 0, r.stderr
+    env = dict(os.environ, LD_PRELOAD=CXX_SO, QUOTA_B200_HOST_KV="0")
+    out = tmp_path / "gpu_nokv.txt"
+    r = subprocess.run([EXE, str(out), "8"], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr
+    a, b = _parse(cpu), _parse(out)
+    assert a["prune"] == b["prune"]
+    assert all(ks == 0 for _, _, ks in b["kv"])  # no host codes materialised
+    for x, y in zip(a["decode"], b["decode"]):
+        assert np.abs(x - y).max() <= 1e-2

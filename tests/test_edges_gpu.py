@@ -129,3 +129,21 @@ def test_packed_weight_file_roundtrip(pair, tmp_path):
         g.load(path)
     f.close()
     g.close()
+
+
+def test_graph_and_eager_decode_identical(pair):
+    """The CUDA-graph replay of a decode step equals the eager launch sequence bitwise
+    (profiling runs the step eagerly)."""
+    cfg, port, e = pair
+    e.clear_recipe()
+    emb = O.synth_embeddings(40, 128, seed=9).astype(np.float32)
+    xs = [O.synth_embeddings(1, 128, seed=60 + i).astype(np.float32) for i in range(4)]
+    e.prefill(emb, [30], [10])
+    g = [e.decode(x).copy() for x in xs]
+    e.prefill(emb, [30], [10])
+    h = []
+    for x in xs:
+        e.profile_next()  # eager path for this step
+        h.append(e.decode(x).copy())
+    for a, b in zip(g, h):
+        assert np.array_equal(a, b)
