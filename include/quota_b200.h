@@ -88,6 +88,17 @@ int qt_engine_load_head(qt_engine* e, const float* w_head, const float* final_ga
 int qt_engine_load_layer_codes(qt_engine* e, int layer, const int8_t* const* codes, const double* const* scales,
                                const double* g1, const double* g2);
 int qt_engine_load_head_codes(qt_engine* e, const int8_t* codes, const double* scales, const double* final_gain);
+/* Calibration.  keep_fp_weights(1) before loading keeps fp64
+ * copies of the full-precision weights on the device; fit_act_scales then runs
+ * fit_act_scales (calibrator.cpp:237-249): full-precision forward_prefill of
+ * each sample (fp64, model.cpp:315-453 with ExecMode::Fp) collecting max|x|
+ * at the five quantizer sites (model.cpp:348,393,430,434,443), returning the
+ * 4 * n_layers + 1 static per-tensor scales (max/7, all-zero -> 1.0); apply != 0
+ * also installs them (qt_engine_set_act_scales).  embs: host fp64
+ * [visual+text x d_model] per sample. */
+int qt_engine_keep_fp_weights(qt_engine* e, int on);
+int qt_engine_fit_act_scales(qt_engine* e, int n_samples, const double* const* embs, const int* visual,
+                             const int* text, double* scales_out, int apply);
 /* Packed-int4 weight file (the reference has no checkpoint
  * format -- it regenerates weights from the seed, model.cpp:113-135): the
  * engine's device layout byte for byte (tiled int4 codes, fp64 per-channel

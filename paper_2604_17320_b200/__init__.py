@@ -87,6 +87,8 @@ def lib():
         L.qt_kv_quant_append_i4.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp, vp, vp,
                                             C.c_int, vp, C.c_int64, vp, vp]
         L.qt_rope_table.argtypes = [C.c_int, C.c_int, dp]
+        L.qt_engine_keep_fp_weights.argtypes = [vp, C.c_int]
+        L.qt_engine_fit_act_scales.argtypes = [vp, C.c_int, C.POINTER(dp), ip, ip, dp, C.c_int]
         L.qt_engine_save.argtypes = [vp, C.c_char_p]
         L.qt_engine_load.argtypes = [vp, C.c_char_p]
         L.qt_engine_scores.argtypes = [vp, C.c_int, C.c_int, dp, dp, C.c_int, ip]
@@ -204,6 +206,22 @@ class Engine:
             self.load_layer(l, lw["wq"], lw["wk"], lw["wv"], lw["wo"], lw["w1"], lw["w2"], lw.get("w3"),
                             lw.get("g1"), lw.get("g2"))
         self.load_head(w.head, w.gf)
+
+    def keep_fp_weights(self, on=True):
+        """Keep fp64 copies of the full-precision weights (call before load_*) for calibration."""
+        check(lib().qt_engine_keep_fp_weights(self.h, int(on)))
+
+    def fit_act_scales(self, samples, apply=True):
+        """fit_act_scales (calibrator.cpp:237-249) on the device: samples = [(emb fp64 [S x d],
+        visual, text)] -> 4 * n_layers + 1 static scales (installed when apply)."""
+        embs = [np.ascontiguousarray(e, dtype=np.float64) for e, _, _ in samples]
+        arr = (C.POINTER(C.c_double) * len(embs))(*[e.ctypes.data_as(C.POINTER(C.c_double)) for e in embs])
+        vis = _i32([v for _, v, _ in samples])
+        txt = _i32([t for _, _, t in samples])
+        out = np.empty(4 * self.cfg.n_layers + 1, dtype=np.float64)
+        check(lib().qt_engine_fit_act_scales(self.h, len(embs), arr, _ip(vis), _ip(txt),
+                                             out.ctypes.data_as(C.POINTER(C.c_double)), int(apply)))
+        return out
 
     def save(self, path):
         """Write the packed-int4 weight file (device layout, include/quota_b200.h)."""

@@ -25,6 +25,7 @@
 #include "qt_common.cuh"
 #include "qt_kernels.h"
 #include "qt_decode_mk.h"
+#include <cublas_v2.h>
 
 namespace {
 
@@ -107,6 +108,12 @@ struct LayerW {
     float* g1 = nullptr;
     float* g2 = nullptr;
     bool loaded = false;
+};
+
+// fp64 copies of the full-precision weights (reference orientation [d_in x d_out]),
+// kept only when calibration is enabled (qt_engine_keep_fp_weights)
+struct FpLayer {
+    double* w[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};  // q k v o w1 w2 w3
 };
 
 struct Recipe {
@@ -283,6 +290,11 @@ struct qt_engine {
     double* mk_act = nullptr;
     int mk_grid = 0, mk_smem = 0, mk_nslot = 0, mk_a_ld = 0, mk_acc_rows = 0;
     bool mk_possible = false;
+    // full-precision calibration forward (k_fp.cu)
+    bool keep_fp = false;
+    std::vector<FpLayer> fpw;
+    double* fp_head = nullptr;
+    cublasHandle_t blas = nullptr;
     int* splitk_ws = nullptr;     // int32 split-K partials of the tcgen05 GEMM at small M
     unsigned* seq_cnt = nullptr;  // per-sequence arrival counters of the fused decode attention block
     // opt-in (QT_ATTN_FUSED=1): one kernel for RoPE + KV append + attention + attn_out quant; measured
@@ -310,6 +322,10 @@ struct qt_engine {
         f(mag); f(res); f(inter); f(intra); f(w4); f(budget); f(new_off); f(new_len); f(keep_src); f(keep_local);
         f(kept_pos); f(sc_fused); f(sc_norm); f(rope); f(wscratch); f(wstage); f(pool); f(pt); f(kv_len); f(next_pos); f(dec_seq);
         f(xd); f(xd_in); f(dlogits); f(part_ml); f(part_o);
+        for (auto& fl : fpw)
+            for (double* p : fl.w) f(p);
+        f(fp_head);
+        if (blas) cublasDestroy(blas);
         f(splitk_ws); f(seq_cnt); f(mk_trace); f(mk_layers); f(mk_acc); f(mk_codes); f(mk_sa); f(mk_attn); f(mk_sync); f(mk_act);
         if (pin) cudaFreeHost(pin);
         if (own_stream) cudaStreamDestroy(own_stream);
@@ -514,6 +530,87 @@ struct qt_engine {
                       8 * mk_a_ld >= 4 * dff && B_MAX_MK >= 1;
     }
 
+    // ------------------------------------------------------------ calibration (fp64 forward)
+    // y[M x N] (+)= x[M x K] . W[K x N], all row-major fp64 (DGEMM on the transposed views)
+    void dgemm(const double* x, int M, int K, const double* W, int N, double* y, int ldy, double beta) {
+        const double one = 1.0;
+        if (cublasDgemm(blas, CUBLAS_OP_N, CUBLAS_OP_N, N, M, K, &one, W, N, x, K, &beta, y, ldy) !=
+            CUBLAS_STATUS_SUCCESS)
+            fail(QT_ECUDA, "cublasDgemm failed");
+    }
+
+    // fit_act_scales (calibrator.cpp:237-249): full-precision forwards of the samples with
+    // an ActStats collector; returns max|x| / qmax per site (0 -> 1.0, model.cpp:198-210)
+    void fit_act_scales(int n, const double* const* embs, const int* vis, const int* txt, double* out) {
+        if (!keep_fp || fpw.empty() || !fp_head) fail(QT_EINVAL, "calibration needs the full-precision weights "
+                                                                 "(qt_engine_keep_fp_weights before loading)");
+        if (n < 1) fail(QT_EINVAL, "no calibration samples");  // calibrator.cpp:239
+        if (!blas) {
+            if (cublasCreate(&blas) != CUBLAS_STATUS_SUCCESS) fail(QT_ECUDA, "cublasCreate failed");
+        }
+        cublasSetStream(blas, st);
+        int smax = 0;
+        for (int i = 0; i < n; ++i) {
+            if (vis[i] < 0 || txt[i] < 0 || vis[i] + txt[i] < 1) fail(QT_EINVAL, "invalid sample layout");
+            smax = std::max(smax, vis[i] + txt[i]);
+        }
+        if (smax > max_pos - max_decode - 1) fail(QT_EINVAL, "sample longer than the engine's RoPE table");
+        const int kvd = Hkv * dh, ldq = n_qkv;
+        const size_t S = smax;
+        double* xb = dalloc<double>(S * d);
+        double* nb = dalloc<double>(S * d);
+        double* qb = dalloc<double>(S * ldq);
+        double* ab = dalloc<double>(S * d);
+        double* gb = dalloc<double>(S * dff);
+        double* ub = cfg.mlp == 1 ? dalloc<double>(S * dff) : nullptr;
+        double* mb = dalloc<double>(S * dff);
+        int* pb_ = dalloc<int>(S);
+        unsigned long long* obs = dalloc<unsigned long long>(4 * L + 1);
+        std::vector<int> hp(S);
+        for (size_t i = 0; i < S; ++i) hp[i] = (int)i;
+        h2d(pb_, hp.data(), S * sizeof(int), "positions");
+        auto cleanup = [&]() {
+            for (void* p : {(void*)xb, (void*)nb, (void*)qb, (void*)ab, (void*)gb, (void*)ub, (void*)mb, (void*)pb_,
+                            (void*)obs})
+                if (p) cudaFree(p);
+        };
+        try {
+            for (int sidx = 0; sidx < n; ++sidx) {
+                const int V = vis[sidx], Sq = vis[sidx] + txt[sidx];
+                h2d(xb, embs[sidx], (size_t)Sq * d * sizeof(double), "calibration sample");
+                for (int l = 0; l < L; ++l) {
+                    const FpLayer& fl = fpw[l];
+                    ckl(qt_launch_fp_rmsnorm(xb, lw[l].g1, Sq, d, nb, obs + 4 * l + 0, st), "fp rmsnorm");
+                    dgemm(nb, Sq, d, fl.w[0], d, qb, ldq, 0.0);
+                    dgemm(nb, Sq, d, fl.w[1], kvd, qb + d, ldq, 0.0);
+                    dgemm(nb, Sq, d, fl.w[2], kvd, qb + d + kvd, ldq, 0.0);
+                    ckl(qt_launch_fp_rope(qb, ldq, Sq, H + Hkv, dh, pb_, rope, st), "fp rope");
+                    ckl(qt_launch_fp_attention(qb, ldq, H, Hkv, dh, Sq, V, ab, d, obs + 4 * l + 1, st),
+                        "fp attention");
+                    dgemm(ab, Sq, d, fl.w[3], d, xb, d, 1.0);  // x += attn . Wo
+                    ckl(qt_launch_fp_rmsnorm(xb, lw[l].g2, Sq, d, nb, obs + 4 * l + 2, st), "fp rmsnorm");
+                    dgemm(nb, Sq, d, fl.w[4], dff, gb, dff, 0.0);
+                    if (ub) dgemm(nb, Sq, d, fl.w[6], dff, ub, dff, 0.0);
+                    ckl(qt_launch_fp_mlp_act(gb, ub, (long long)Sq * dff, mb, obs + 4 * l + 3, st), "fp mlp");
+                    dgemm(mb, Sq, dff, fl.w[5], d, xb, d, 1.0);  // x += mid . W2
+                }
+                ckl(qt_launch_fp_rmsnorm(xb, gf, Sq, d, nb, obs + 4 * L, st), "fp final norm");
+            }
+            std::vector<unsigned long long> hm(4 * L + 1);
+            ck(cudaMemcpyAsync(hm.data(), obs, hm.size() * 8, cudaMemcpyDeviceToHost, st), "stats");
+            ck(cudaStreamSynchronize(st), "stats");
+            for (size_t i = 0; i < hm.size(); ++i) {
+                double m;
+                std::memcpy(&m, &hm[i], 8);
+                out[i] = m == 0.0 ? 1.0 : m / 7.0;  // qmax at 4 act bits
+            }
+        } catch (...) {
+            cleanup();
+            throw;
+        }
+        cleanup();
+    }
+
     static constexpr int B_MAX_MK = 8;
     bool mk_usable() const { return use_mk && mk_possible && B >= 1 && B <= 8; }
 
@@ -601,6 +698,15 @@ struct qt_engine {
         ckl(qt_launch_weight_quant(dw, K, N, 4, row_mul, row_add, codes_dst, rows_pad, scales_dst, wscratch, st),
             "weight quantize");
         ck(cudaStreamSynchronize(st), "weight quantize");
+    }
+
+    // fp64 copy of a full-precision weight for the calibration forward
+    void keep64(double*& dst, const float* w, size_t n, int on_device) {
+        if (!keep_fp || !w) return;
+        const float* dw = to_device_f32(w, n, on_device, nullptr);
+        if (!dst) dst = dalloc<double>(n);
+        ckl(qt_launch_f32_to_f64(dw, dst, (long long)n, st), "fp64 weight copy");
+        ck(cudaStreamSynchronize(st), "fp64 weight copy");
     }
 
     // pre-quantized codes (host int8 [K x N], reference orientation) + fp64 per-column scales
@@ -1216,6 +1322,13 @@ int qt_engine_load_layer(qt_engine* e, int layer, const float* wq, const float* 
             e->quant_into(w1, d, f, on_device, 1, 0, l.gu, e->n_gu_pad, l.s_gu);
         }
         e->quant_into(w2, f, d, on_device, 1, 0, l.down, e->nd_pad, l.s_down);
+        if (e->keep_fp) {
+            FpLayer& fl = e->fpw[layer];
+            const float* ws[7] = {wq, wk, wv, wo, w1, w2, w3};
+            const size_t ns[7] = {(size_t)d * d, (size_t)d * kvd, (size_t)d * kvd, (size_t)d * d, (size_t)d * f,
+                                  (size_t)f * d, (size_t)d * f};
+            for (int i = 0; i < 7; ++i) e->keep64(fl.w[i], ws[i], ns[i], on_device);
+        }
         e->load_gain(l.g1, g1, on_device);
         e->load_gain(l.g2, g2, on_device);
         l.loaded = true;
@@ -1255,6 +1368,22 @@ int qt_engine_load_head_codes(qt_engine* e, const int8_t* codes, const double* s
         e->load_gain64(e->gf, final_gain);
         e->head_loaded = true;
         e->graph_ok = false;
+    });
+}
+
+int qt_engine_keep_fp_weights(qt_engine* e, int on) {
+    return guard([&] {
+        e->keep_fp = on != 0;
+        if (e->keep_fp && e->fpw.empty()) e->fpw.resize(e->L);
+    });
+}
+
+int qt_engine_fit_act_scales(qt_engine* e, int n_samples, const double* const* embs, const int* visual,
+                             const int* text, double* scales_out, int apply) {
+    return guard([&] {
+        if (!embs || !visual || !text || !scales_out) fail(QT_EINVAL, "null argument");
+        e->fit_act_scales(n_samples, embs, visual, text, scales_out);
+        if (apply && qt_engine_set_act_scales(e, scales_out) != 0) fail(QT_EINVAL, qt_last_error());
     });
 }
 
@@ -1317,6 +1446,7 @@ int qt_engine_load_head(qt_engine* e, const float* w_head, const float* final_ga
         if (!w_head) fail(QT_EINVAL, "null weight");
         if (on_device) ck(cudaDeviceSynchronize(), "weights ready");
         e->quant_into(w_head, e->d, e->d, on_device, 1, 0, e->head, e->nd_pad, e->s_head);
+        e->keep64(e->fp_head, w_head, (size_t)e->d * e->d, on_device);
         e->load_gain(e->gf, final_gain, on_device);
         e->head_loaded = true;
         e->graph_ok = false;

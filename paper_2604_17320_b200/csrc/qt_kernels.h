@@ -32,6 +32,15 @@ int qt_launch_attn_dec_fused(float* qkv, int ldq, int H, int Hkv, int dh, const 
                              const double* rope, const int* pt, int max_pages, uint8_t* pool, long long page_bytes,
                              float* attn, int d, unsigned* seq_cnt, uint8_t* codes, int ld_codes, double* scales,
                              int qmode, double static_scale, int d_pad, int bits, int B, cudaStream_t st);
+// full-precision (fp64) calibration forward pieces (k_fp.cu)
+int qt_launch_fp_rmsnorm(const double* x, const float* gain, int M, int D, double* out, unsigned long long* obs,
+                         cudaStream_t st);
+int qt_launch_fp_rope(double* qkv, int ldq, int M, int nheads_qk, int dh, const int* pos, const double* rope,
+                      cudaStream_t st);
+int qt_launch_fp_attention(const double* qkv, int ldq, int H, int Hkv, int dh, int S, int V, double* out, int ldo,
+                           unsigned long long* obs, cudaStream_t st);
+int qt_launch_fp_mlp_act(const double* g, const double* u, long long n, double* mid, unsigned long long* obs,
+                         cudaStream_t st);
 int qt_launch_codes_pack(const int8_t* src, int K, int N, const double* s_in, int row_mul, int row_add,
                          uint8_t* codes, int ldc, double* scales, cudaStream_t st);
 // out: double* for QT_EPI_RESADD (the fp64 residual stream), float* otherwise

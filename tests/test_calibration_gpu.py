@@ -1,0 +1,51 @@
+"""Calibration on the B200: fit_act_scales (calibrator.cpp:237-249)
+-- full-precision forwards with the ActStats collector (model.cpp:174-210) -- against
+the unmodified reference on identical weights and samples, then the quantized
+prefill with the device-fitted scales against the reference prefill with its own."""
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2604_17320_b200 as Q
+
+pytestmark = pytest.mark.gpu
+
+
+def _setup(L=4, d=256, H=4):
+    cfg = O.ModelCfg(n_layers=L, d_model=d, n_heads=H, n_kv_heads=H, d_head=d // H, d_ff=4 * d, weight_axis=2)
+    ref = O.Ref(cfg, seed=7)
+    w = O.synth_weights(cfg, seed=3)
+    ref.set_weights(w)
+    calib = [(O.synth_embeddings(144 + 16 + 4 * i, d, seed=100 + i), 144, 16 + 4 * i) for i in range(4)]
+    return cfg, ref, w, calib
+
+
+def test_fit_act_scales_matches_reference(torch_cuda):
+    cfg, ref, w, calib = _setup()
+    exp = ref.fit_act_scales(calib)
+    e = Q.Engine(Q.Config(n_layers=4, d_model=256, n_heads=4, n_kv_heads=4, d_head=64, d_ff=1024),
+                 max_batch=2, max_tokens=1024, max_seq=512, max_decode=16)
+    e.keep_fp_weights(True)
+    e.load_weights(w)
+    got = e.fit_act_scales(calib)
+    # fp64 on both sides; only reduction order (DGEMM, tree sums) differs
+    np.testing.assert_allclose(got, exp, rtol=1e-10)
+    # the quantized prefill with the device-fitted scales tracks the reference with its own
+    ref.prepare(exp, weight_axis=2)
+    rec = O.Recipe([0, 1, 2, 3], [1.0, 0.5, 0.3, 0.3], v0=144)
+    emb = O.synth_embeddings(184, 256, seed=11)
+    res = ref.prefill(emb, 144, 40, rec).result()
+    e.set_recipe(rec.candidate_layers, rec.keep_ratios, rec.weights, rec.v0, 4)
+    lg = e.prefill(emb.astype(np.float32), [144], [40])
+    for (l1, b1, p1), (l2, b2, p2) in zip(e.trace(0), res.trace):
+        assert (l1, b1) == (l2, b2) and np.array_equal(p1, p2)
+    assert np.abs(lg - res.logits).max() <= 1e-2
+
+
+def test_fit_act_scales_requires_fp_weights(torch_cuda):
+    cfg, ref, w, calib = _setup()
+    e = Q.Engine(Q.Config(n_layers=4, d_model=256, n_heads=4, n_kv_heads=4, d_head=64, d_ff=1024),
+                 max_batch=1, max_tokens=512, max_seq=512, max_decode=1)
+    e.load_weights(w)
+    with pytest.raises(Q.QuotaInvalidArgument, match="full-precision weights"):
+        e.fit_act_scales(calib)
