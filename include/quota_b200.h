@@ -99,6 +99,13 @@ int qt_engine_load_head_codes(qt_engine* e, const int8_t* codes, const double* s
 int qt_engine_keep_fp_weights(qt_engine* e, int on);
 int qt_engine_fit_act_scales(qt_engine* e, int n_samples, const double* const* embs, const int* visual,
                              const int* text, double* scales_out, int apply);
+/* profile_sensitivity (calibrator.cpp:42-82), QUOTA Eq. 1: per listed layer the
+ * median over samples of ||x_q - x||_F / (||x||_F + eta) between this engine's
+ * quantized block outputs and the fp64 forward's, plus normalize_sensitivities
+ * (calibrator.cpp:84-98: P10/P90 clip to [0.1, 0.9], flat -> 0.5). */
+int qt_engine_profile_sensitivity(qt_engine* e, int n_samples, const double* const* embs, const int* visual,
+                                  const int* text, int n_layers, const int* layers, double eta, double* raw,
+                                  double* normalized);
 /* Packed-int4 weight file (the reference has no checkpoint
  * format -- it regenerates weights from the seed, model.cpp:113-135): the
  * engine's device layout byte for byte (tiled int4 codes, fp64 per-channel

@@ -109,6 +109,8 @@ def ref_lib():
         lib.qref_serialize_recipe.argtypes = [C.c_int, _ip, _dp, _dp, C.c_int, C.c_char_p, C.c_char_p, C.c_int,
                                               C.c_char_p]
         lib.qref_executed_visual_lengths.argtypes = [C.c_char_p, C.c_int, _ip]
+        lib.qref_profile_sensitivity.argtypes = [C.c_void_p, C.c_int, C.POINTER(_dp), _ip, _ip, C.c_int, _ip,
+                                                 C.c_double, _dp, _dp]
         _ref_lib = lib
     return _ref_lib
 
@@ -369,6 +371,19 @@ class Ref:
         _check(self.lib.qref_fit_act_scales(self.h, len(embs), arr, _i(vis), _i(txt), self.cfg.act_bits, _d(out)),
                self.lib, "qref")
         return out
+
+    def profile_sensitivity(self, samples, layers, eta=1e-6):
+        """profile_sensitivity (calibrator.cpp:42-82) with the prepared env -> (raw, normalized)."""
+        embs = [f64(e) for e, _, _ in samples]
+        arr = (_dp * len(embs))(*[_d(e) for e in embs])
+        vis = np.array([v for _, v, _ in samples], dtype=np.int32)
+        txt = np.array([t for _, _, t in samples], dtype=np.int32)
+        lay = np.array(layers, dtype=np.int32)
+        raw = np.empty(len(lay))
+        nrm = np.empty(len(lay))
+        _check(self.lib.qref_profile_sensitivity(self.h, len(embs), arr, _i(vis), _i(txt), len(lay), _i(lay), eta,
+                                                 _d(raw), _d(nrm)), self.lib, "qref")
+        return raw, nrm
 
     def prepare(self, act_scales, weight_axis=None):
         c = self.cfg

@@ -367,6 +367,29 @@ int qref_fit_act_scales(void* h, int n_samples, const double* const* embeddings,
     });
 }
 
+// profile_sensitivity (calibrator.cpp:42-82) against the prepared QuantEnv:
+// per listed layer the median over samples of ||x_q - x|| / (||x|| + eta) of the
+// block outputs (raw) and normalize_sensitivities of them (calibrator.cpp:84-98).
+int qref_profile_sensitivity(void* h, int n_samples, const double* const* embeddings, const int* visual,
+                             const int* text, int n_layers, const int* layers, double eta, double* raw,
+                             double* normalized) {
+    return guard([&] {
+        RefModel* m = static_cast<RefModel*>(h);
+        if (!m->env) throw std::invalid_argument("quantized mode requires a QuantEnv");
+        std::vector<CalibSample> samples;
+        for (int i = 0; i < n_samples; ++i) {
+            CalibSample s;
+            s.layout = SequenceLayout::prefix(visual[i], text[i]);
+            s.embeddings = mat(embeddings[i], s.layout.total(), m->model.config.d_model);
+            samples.push_back(std::move(s));
+        }
+        SensitivityProfile p = profile_sensitivity(m->model, samples, std::span<const int>(layers, n_layers), eta,
+                                                   m->env.get());
+        std::copy(p.raw.begin(), p.raw.end(), raw);
+        std::copy(p.normalized.begin(), p.normalized.end(), normalized);
+    });
+}
+
 // QuantEnv with the reference's prepare_quant_env (model.cpp:212-237) when
 // weight_axis == 1 (PerRow, the reference default), or the same construction
 // with GroupAxis::PerColumn (quant.hpp:22) when weight_axis == 2 -- the

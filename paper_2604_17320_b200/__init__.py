@@ -89,6 +89,8 @@ def lib():
         L.qt_rope_table.argtypes = [C.c_int, C.c_int, dp]
         L.qt_engine_keep_fp_weights.argtypes = [vp, C.c_int]
         L.qt_engine_fit_act_scales.argtypes = [vp, C.c_int, C.POINTER(dp), ip, ip, dp, C.c_int]
+        L.qt_engine_profile_sensitivity.argtypes = [vp, C.c_int, C.POINTER(dp), ip, ip, C.c_int, ip, C.c_double,
+                                                    dp, dp]
         L.qt_engine_save.argtypes = [vp, C.c_char_p]
         L.qt_engine_load.argtypes = [vp, C.c_char_p]
         L.qt_engine_scores.argtypes = [vp, C.c_int, C.c_int, dp, dp, C.c_int, ip]
@@ -222,6 +224,18 @@ class Engine:
         check(lib().qt_engine_fit_act_scales(self.h, len(embs), arr, _ip(vis), _ip(txt),
                                              out.ctypes.data_as(C.POINTER(C.c_double)), int(apply)))
         return out
+
+    def profile_sensitivity(self, samples, layers, eta=1e-6):
+        """QUOTA Eq. 1 sensitivities (calibrator.cpp:42-82) -> (raw, normalized)."""
+        embs = [np.ascontiguousarray(e, dtype=np.float64) for e, _, _ in samples]
+        arr = (C.POINTER(C.c_double) * len(embs))(*[e.ctypes.data_as(C.POINTER(C.c_double)) for e in embs])
+        vis, txt = _i32([v for _, v, _ in samples]), _i32([t for _, _, t in samples])
+        lay = _i32(layers)
+        raw, nrm = np.empty(len(lay)), np.empty(len(lay))
+        check(lib().qt_engine_profile_sensitivity(self.h, len(embs), arr, _ip(vis), _ip(txt), len(lay), _ip(lay),
+                                                  eta, raw.ctypes.data_as(C.POINTER(C.c_double)),
+                                                  nrm.ctypes.data_as(C.POINTER(C.c_double))))
+        return raw, nrm
 
     def save(self, path):
         """Write the packed-int4 weight file (device layout, include/quota_b200.h)."""

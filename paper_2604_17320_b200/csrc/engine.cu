@@ -292,6 +292,7 @@ struct qt_engine {
     bool mk_possible = false;
     // full-precision calibration forward (k_fp.cu)
     bool keep_fp = false;
+    std::vector<std::vector<double>>* rec_blocks = nullptr;  // block outputs of the next prefill (B = 1)
     std::vector<FpLayer> fpw;
     double* fp_head = nullptr;
     cublasHandle_t blas = nullptr;
@@ -539,76 +540,166 @@ struct qt_engine {
             fail(QT_ECUDA, "cublasDgemm failed");
     }
 
+    // Scratch of the fp64 forward (sized for the longest sample of one call).
+    struct FpScratch {
+        double *x = nullptr, *n = nullptr, *q = nullptr, *a = nullptr, *g = nullptr, *u = nullptr, *m = nullptr;
+        int* pos = nullptr;
+        unsigned long long* obs = nullptr;
+        void release() {
+            for (void* p : {(void*)x, (void*)n, (void*)q, (void*)a, (void*)g, (void*)u, (void*)m, (void*)pos,
+                            (void*)obs})
+                if (p) cudaFree(p);
+            *this = FpScratch{};
+        }
+    };
+
+    void fp_setup(FpScratch& fs, int smax) {
+        if (!keep_fp || fpw.empty() || !fp_head) fail(QT_EINVAL, "calibration needs the full-precision weights "
+                                                                 "(qt_engine_keep_fp_weights before loading)");
+        if (!blas && cublasCreate(&blas) != CUBLAS_STATUS_SUCCESS) fail(QT_ECUDA, "cublasCreate failed");
+        cublasSetStream(blas, st);
+        if (smax > max_pos - max_decode - 1) fail(QT_EINVAL, "sample longer than the engine's RoPE table");
+        const size_t S = smax;
+        fs.x = dalloc<double>(S * d);
+        fs.n = dalloc<double>(S * d);
+        fs.q = dalloc<double>(S * n_qkv);
+        fs.a = dalloc<double>(S * d);
+        fs.g = dalloc<double>(S * dff);
+        fs.u = cfg.mlp == 1 ? dalloc<double>(S * dff) : nullptr;
+        fs.m = dalloc<double>(S * dff);
+        fs.pos = dalloc<int>(S);
+        fs.obs = dalloc<unsigned long long>(4 * L + 1);
+        std::vector<int> hp(S);
+        for (size_t i = 0; i < S; ++i) hp[i] = (int)i;
+        h2d(fs.pos, hp.data(), S * sizeof(int), "positions");
+    }
+
+    // forward_prefill in ExecMode::Fp (model.cpp:315-453) for one sample, fp64; max|x| per
+    // site into fs.obs (ActStats, model.cpp:348,393,430,434,443); blocks (optional) gets the
+    // post-block hidden states (ForwardResult::block_outputs, model.cpp:439)
+    void fp_forward(FpScratch& fs, const double* emb, int V, int T, std::vector<std::vector<double>>* blocks) {
+        const int Sq = V + T, kvd = Hkv * dh, ldq = n_qkv;
+        h2d(fs.x, emb, (size_t)Sq * d * sizeof(double), "calibration sample");
+        if (blocks) blocks->assign(L, {});
+        for (int l = 0; l < L; ++l) {
+            const FpLayer& fl = fpw[l];
+            ckl(qt_launch_fp_rmsnorm(fs.x, lw[l].g1, Sq, d, fs.n, fs.obs + 4 * l + 0, st), "fp rmsnorm");
+            dgemm(fs.n, Sq, d, fl.w[0], d, fs.q, ldq, 0.0);
+            dgemm(fs.n, Sq, d, fl.w[1], kvd, fs.q + d, ldq, 0.0);
+            dgemm(fs.n, Sq, d, fl.w[2], kvd, fs.q + d + kvd, ldq, 0.0);
+            ckl(qt_launch_fp_rope(fs.q, ldq, Sq, H + Hkv, dh, fs.pos, rope, st), "fp rope");
+            ckl(qt_launch_fp_attention(fs.q, ldq, H, Hkv, dh, Sq, V, fs.a, d, fs.obs + 4 * l + 1, st),
+                "fp attention");
+            dgemm(fs.a, Sq, d, fl.w[3], d, fs.x, d, 1.0);  // x += attn . Wo
+            ckl(qt_launch_fp_rmsnorm(fs.x, lw[l].g2, Sq, d, fs.n, fs.obs + 4 * l + 2, st), "fp rmsnorm");
+            dgemm(fs.n, Sq, d, fl.w[4], dff, fs.g, dff, 0.0);
+            if (fs.u) dgemm(fs.n, Sq, d, fl.w[6], dff, fs.u, dff, 0.0);
+            ckl(qt_launch_fp_mlp_act(fs.g, fs.u, (long long)Sq * dff, fs.m, fs.obs + 4 * l + 3, st), "fp mlp");
+            dgemm(fs.m, Sq, dff, fl.w[5], d, fs.x, d, 1.0);  // x += mid . W2
+            if (blocks) {
+                (*blocks)[l].resize((size_t)Sq * d);
+                ck(cudaMemcpyAsync((*blocks)[l].data(), fs.x, (size_t)Sq * d * sizeof(double), cudaMemcpyDeviceToHost,
+                                   st),
+                   "block output");
+            }
+        }
+        ckl(qt_launch_fp_rmsnorm(fs.x, gf, Sq, d, fs.n, fs.obs + 4 * L, st), "fp final norm");
+        ck(cudaStreamSynchronize(st), "fp forward");
+    }
+
     // fit_act_scales (calibrator.cpp:237-249): full-precision forwards of the samples with
     // an ActStats collector; returns max|x| / qmax per site (0 -> 1.0, model.cpp:198-210)
     void fit_act_scales(int n, const double* const* embs, const int* vis, const int* txt, double* out) {
-        if (!keep_fp || fpw.empty() || !fp_head) fail(QT_EINVAL, "calibration needs the full-precision weights "
-                                                                 "(qt_engine_keep_fp_weights before loading)");
         if (n < 1) fail(QT_EINVAL, "no calibration samples");  // calibrator.cpp:239
-        if (!blas) {
-            if (cublasCreate(&blas) != CUBLAS_STATUS_SUCCESS) fail(QT_ECUDA, "cublasCreate failed");
-        }
-        cublasSetStream(blas, st);
         int smax = 0;
         for (int i = 0; i < n; ++i) {
             if (vis[i] < 0 || txt[i] < 0 || vis[i] + txt[i] < 1) fail(QT_EINVAL, "invalid sample layout");
             smax = std::max(smax, vis[i] + txt[i]);
         }
-        if (smax > max_pos - max_decode - 1) fail(QT_EINVAL, "sample longer than the engine's RoPE table");
-        const int kvd = Hkv * dh, ldq = n_qkv;
-        const size_t S = smax;
-        double* xb = dalloc<double>(S * d);
-        double* nb = dalloc<double>(S * d);
-        double* qb = dalloc<double>(S * ldq);
-        double* ab = dalloc<double>(S * d);
-        double* gb = dalloc<double>(S * dff);
-        double* ub = cfg.mlp == 1 ? dalloc<double>(S * dff) : nullptr;
-        double* mb = dalloc<double>(S * dff);
-        int* pb_ = dalloc<int>(S);
-        unsigned long long* obs = dalloc<unsigned long long>(4 * L + 1);
-        std::vector<int> hp(S);
-        for (size_t i = 0; i < S; ++i) hp[i] = (int)i;
-        h2d(pb_, hp.data(), S * sizeof(int), "positions");
-        auto cleanup = [&]() {
-            for (void* p : {(void*)xb, (void*)nb, (void*)qb, (void*)ab, (void*)gb, (void*)ub, (void*)mb, (void*)pb_,
-                            (void*)obs})
-                if (p) cudaFree(p);
-        };
+        FpScratch fs;
         try {
-            for (int sidx = 0; sidx < n; ++sidx) {
-                const int V = vis[sidx], Sq = vis[sidx] + txt[sidx];
-                h2d(xb, embs[sidx], (size_t)Sq * d * sizeof(double), "calibration sample");
-                for (int l = 0; l < L; ++l) {
-                    const FpLayer& fl = fpw[l];
-                    ckl(qt_launch_fp_rmsnorm(xb, lw[l].g1, Sq, d, nb, obs + 4 * l + 0, st), "fp rmsnorm");
-                    dgemm(nb, Sq, d, fl.w[0], d, qb, ldq, 0.0);
-                    dgemm(nb, Sq, d, fl.w[1], kvd, qb + d, ldq, 0.0);
-                    dgemm(nb, Sq, d, fl.w[2], kvd, qb + d + kvd, ldq, 0.0);
-                    ckl(qt_launch_fp_rope(qb, ldq, Sq, H + Hkv, dh, pb_, rope, st), "fp rope");
-                    ckl(qt_launch_fp_attention(qb, ldq, H, Hkv, dh, Sq, V, ab, d, obs + 4 * l + 1, st),
-                        "fp attention");
-                    dgemm(ab, Sq, d, fl.w[3], d, xb, d, 1.0);  // x += attn . Wo
-                    ckl(qt_launch_fp_rmsnorm(xb, lw[l].g2, Sq, d, nb, obs + 4 * l + 2, st), "fp rmsnorm");
-                    dgemm(nb, Sq, d, fl.w[4], dff, gb, dff, 0.0);
-                    if (ub) dgemm(nb, Sq, d, fl.w[6], dff, ub, dff, 0.0);
-                    ckl(qt_launch_fp_mlp_act(gb, ub, (long long)Sq * dff, mb, obs + 4 * l + 3, st), "fp mlp");
-                    dgemm(mb, Sq, dff, fl.w[5], d, xb, d, 1.0);  // x += mid . W2
-                }
-                ckl(qt_launch_fp_rmsnorm(xb, gf, Sq, d, nb, obs + 4 * L, st), "fp final norm");
-            }
+            fp_setup(fs, smax);
+            for (int i = 0; i < n; ++i) fp_forward(fs, embs[i], vis[i], txt[i], nullptr);
             std::vector<unsigned long long> hm(4 * L + 1);
-            ck(cudaMemcpyAsync(hm.data(), obs, hm.size() * 8, cudaMemcpyDeviceToHost, st), "stats");
+            ck(cudaMemcpyAsync(hm.data(), fs.obs, hm.size() * 8, cudaMemcpyDeviceToHost, st), "stats");
             ck(cudaStreamSynchronize(st), "stats");
             for (size_t i = 0; i < hm.size(); ++i) {
-                double m;
-                std::memcpy(&m, &hm[i], 8);
-                out[i] = m == 0.0 ? 1.0 : m / 7.0;  // qmax at 4 act bits
+                double mxv;
+                std::memcpy(&mxv, &hm[i], 8);
+                out[i] = mxv == 0.0 ? 1.0 : mxv / 7.0;  // qmax at 4 act bits
             }
         } catch (...) {
-            cleanup();
+            fs.release();
             throw;
         }
-        cleanup();
+        fs.release();
+    }
+
+    // percentile (numeric.cpp:84-96) on a copy
+    static double pctl(std::vector<double> v, double p) {
+        if (v.empty()) fail(QT_EINVAL, "empty sample");
+        std::sort(v.begin(), v.end());
+        if (v.size() == 1) return v[0];
+        const double hh = p / 100.0 * (double)(v.size() - 1);
+        const size_t lo = (size_t)std::floor(hh), hi = std::min(lo + 1, v.size() - 1);
+        return v[lo] + (hh - (double)lo) * (v[hi] - v[lo]);
+    }
+
+    // profile_sensitivity (calibrator.cpp:42-82): per listed layer, the median over samples of
+    // ||x_q - x|| / (||x|| + eta) between the quantized (this engine) and fp64 block outputs,
+    // then normalize_sensitivities (calibrator.cpp:84-98)
+    void profile_sensitivity(int n, const double* const* embs, const int* vis, const int* txt, int nl,
+                             const int* layers, double eta, double* raw, double* normd) {
+        if (n < 1) fail(QT_EINVAL, "no calibration samples");
+        if (nl < 1) fail(QT_EINVAL, "no layers to profile");
+        for (int i = 0; i < nl; ++i)
+            if (layers[i] < 0 || layers[i] >= L) fail(QT_EINVAL, "layer out of range");
+        if (cfg.act_mode == 0 && !act_set) fail(QT_EINVAL, "quantized mode requires a QuantEnv");
+        int smax = 0;
+        for (int i = 0; i < n; ++i) {
+            if (vis[i] < 0 || txt[i] < 0 || vis[i] + txt[i] < 1) fail(QT_EINVAL, "invalid sample layout");
+            smax = std::max(smax, vis[i] + txt[i]);
+        }
+        std::vector<std::vector<double>> dev(nl);
+        FpScratch fs;
+        const bool had_recipe = have_recipe;
+        have_recipe = false;  // no hook: the block outputs of unpruned forwards
+        try {
+            fp_setup(fs, smax);
+            std::vector<std::vector<double>> fb, qb;
+            std::vector<float> emb32;
+            for (int i = 0; i < n; ++i) {
+                const int Sq = vis[i] + txt[i];
+                fp_forward(fs, embs[i], vis[i], txt[i], &fb);
+                rec_blocks = &qb;
+                prefill(1, embs[i], 0, 1, &vis[i], &txt[i], nullptr, nullptr, nullptr, 0);
+                rec_blocks = nullptr;
+                for (int k = 0; k < nl; ++k) {
+                    const std::vector<double>& x = fb[layers[k]];
+                    const std::vector<double>& xq = qb[layers[k]];
+                    if (xq.size() != (size_t)Sq * d) fail(QT_ERUNTIME, "block output shape mismatch");
+                    double acc = 0.0, nn = 0.0;
+                    for (size_t j = 0; j < x.size(); ++j) {
+                        const double df = xq[j] - x[j];
+                        acc += df * df;  // l2_distance, numeric.cpp:61-71
+                        nn += x[j] * x[j];  // frobenius_norm
+                    }
+                    dev[k].push_back(std::sqrt(acc) / (std::sqrt(nn) + eta));
+                }
+            }
+        } catch (...) {
+            rec_blocks = nullptr;
+            have_recipe = had_recipe;
+            fs.release();
+            throw;
+        }
+        have_recipe = had_recipe;
+        fs.release();
+        std::vector<double> r(nl);
+        for (int k = 0; k < nl; ++k) r[k] = raw[k] = pctl(dev[k], 50.0);  // median
+        const double p10 = pctl(r, 10.0), p90 = pctl(r, 90.0);
+        for (int k = 0; k < nl; ++k)
+            normd[k] = p90 - p10 < 1e-12 ? 0.5 : std::clamp((r[k] - p10) * (1.0 / (p90 - p10)), 0.1, 0.9);
     }
 
     static constexpr int B_MAX_MK = 8;
@@ -999,6 +1090,13 @@ struct qt_engine {
             else gemm(QT_EPI_SILU, w.gu, n_gu_pad, w.s_gu, M, n_gu, kd_pad, mid, dff);
             norm_quant(mid, 0, dff, nullptr, M, dff, kff_pad, 4 * l + 3);
             gemm(QT_EPI_RESADD, w.down, nd_pad, w.s_down, M, d, kff_pad, xc, d);
+            if (rec_blocks) {  // ForwardResult::block_outputs (model.cpp:439), calibration only
+                if (l == 0) rec_blocks->assign(L, {});
+                (*rec_blocks)[l].resize((size_t)M * d);
+                ck(cudaMemcpyAsync((*rec_blocks)[l].data(), xc, (size_t)M * d * sizeof(double), cudaMemcpyDeviceToHost,
+                                   st),
+                   "block output");
+            }
         }
         // final norm + head (model.cpp:442-445)
         norm_quant(xc, 1, d, gf, M, d, kd_pad, 4 * L);
@@ -1384,6 +1482,15 @@ int qt_engine_fit_act_scales(qt_engine* e, int n_samples, const double* const* e
         if (!embs || !visual || !text || !scales_out) fail(QT_EINVAL, "null argument");
         e->fit_act_scales(n_samples, embs, visual, text, scales_out);
         if (apply && qt_engine_set_act_scales(e, scales_out) != 0) fail(QT_EINVAL, qt_last_error());
+    });
+}
+
+int qt_engine_profile_sensitivity(qt_engine* e, int n_samples, const double* const* embs, const int* visual,
+                                  const int* text, int n_layers, const int* layers, double eta, double* raw,
+                                  double* normalized) {
+    return guard([&] {
+        if (!embs || !visual || !text || !layers || !raw || !normalized) fail(QT_EINVAL, "null argument");
+        e->profile_sensitivity(n_samples, embs, visual, text, n_layers, layers, eta, raw, normalized);
     });
 }
 
