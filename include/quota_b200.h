@@ -106,6 +106,22 @@ int qt_engine_fit_act_scales(qt_engine* e, int n_samples, const double* const* e
 int qt_engine_profile_sensitivity(qt_engine* e, int n_samples, const double* const* embs, const int* visual,
                                   const int* text, int n_layers, const int* layers, double eta, double* raw,
                                   double* normalized);
+/* profile_diagnostics (calibrator.cpp:147-195) with the quantized forward:
+ * per layer, over samples, the median and IQR of the text queries' summed
+ * top-10 visual attention mass (averaged over heads and text rows) and the
+ * median of the visual rows' median pairwise cosine (numeric.cpp:117-127). */
+int qt_engine_profile_diagnostics(qt_engine* e, int n_samples, const double* const* embs, const int* visual,
+                                  const int* text, double* conc_median, double* conc_iqr, double* red_median);
+/* run_quota_calibration (calibrator.cpp:251-268) on explicit
+ * samples: fit_act_scales (installed), profile_diagnostics, select_candidate_
+ * layers (window, first 2 and last n_layers/4 excluded, calibrator.cpp:197-223),
+ * profile_sensitivity, make_budget_schedule (Eqs. 3-4, calibrator.cpp:100-141).
+ * Outputs the recipe's candidate_layers / keep_ratios (window entries each) and
+ * optionally the sensitivities [window] and diagnostics [n_layers]. */
+int qt_engine_run_quota_calibration(qt_engine* e, int n_samples, const double* const* embs, const int* visual,
+                                    const int* text, int window, double p_min, double tau, double eta,
+                                    double* act_scales, int* layers, double* keep_ratios, double* raw,
+                                    double* normalized, double* conc_median, double* red_median);
 /* Packed-int4 weight file (the reference has no checkpoint
  * format -- it regenerates weights from the seed, model.cpp:113-135): the
  * engine's device layout byte for byte (tiled int4 codes, fp64 per-channel

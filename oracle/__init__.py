@@ -109,6 +109,8 @@ def ref_lib():
         lib.qref_serialize_recipe.argtypes = [C.c_int, _ip, _dp, _dp, C.c_int, C.c_char_p, C.c_char_p, C.c_int,
                                               C.c_char_p]
         lib.qref_executed_visual_lengths.argtypes = [C.c_char_p, C.c_int, _ip]
+        lib.qref_run_calibration.argtypes = [C.c_void_p, C.c_int, C.POINTER(_dp), _ip, _ip, C.c_int, C.c_double,
+                                             C.c_double, C.c_double, _dp, _ip, _dp, _dp, _dp, _dp, _dp]
         lib.qref_profile_sensitivity.argtypes = [C.c_void_p, C.c_int, C.POINTER(_dp), _ip, _ip, C.c_int, _ip,
                                                  C.c_double, _dp, _dp]
         _ref_lib = lib
@@ -384,6 +386,20 @@ class Ref:
         _check(self.lib.qref_profile_sensitivity(self.h, len(embs), arr, _i(vis), _i(txt), len(lay), _i(lay), eta,
                                                  _d(raw), _d(nrm)), self.lib, "qref")
         return raw, nrm
+
+    def run_calibration(self, samples, window=5, p_min=0.3, tau=0.25, eta=1e-6):
+        """run_quota_calibration (calibrator.cpp:251-268) on explicit samples with the per-column env."""
+        embs = [f64(e) for e, _, _ in samples]
+        arr = (_dp * len(embs))(*[_d(e) for e in embs])
+        vis = np.array([v for _, v, _ in samples], dtype=np.int32)
+        txt = np.array([t for _, _, t in samples], dtype=np.int32)
+        L = self.cfg.n_layers
+        acts, lay, kp = np.empty(4 * L + 1), np.empty(window, dtype=np.int32), np.empty(window)
+        raw, nrm, cm, rm = np.empty(window), np.empty(window), np.empty(L), np.empty(L)
+        _check(self.lib.qref_run_calibration(self.h, len(embs), arr, _i(vis), _i(txt), window, p_min, tau, eta,
+                                             _d(acts), _i(lay), _d(kp), _d(raw), _d(nrm), _d(cm), _d(rm)),
+               self.lib, "qref")
+        return dict(act_scales=acts, layers=lay, keeps=kp, raw=raw, normalized=nrm, conc=cm, red=rm)
 
     def prepare(self, act_scales, weight_axis=None):
         c = self.cfg

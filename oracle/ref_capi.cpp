@@ -603,4 +603,46 @@ uint64_t qref_fnv1a64(const double* v, int64_t n) {
     return fnv1a64(std::span<const double>(v, static_cast<size_t>(n)));
 }
 
+// run_quota_calibration (calibrator.cpp:251-268) on explicit samples with the
+// per-output-channel QuantEnv (the axis the B200 GEMM uses):
+// fit_act_scales -> env -> profile_diagnostics -> select_candidate_layers ->
+// profile_sensitivity -> make_budget_schedule, all reference functions.
+int qref_run_calibration(void* h, int n_samples, const double* const* embeddings, const int* visual, const int* text,
+                         int window, double p_min, double tau, double eta, double* act_scales, int* layers,
+                         double* keeps, double* raw, double* normalized, double* conc_median, double* red_median) {
+    return guard([&] {
+        RefModel* m = static_cast<RefModel*>(h);
+        std::vector<CalibSample> samples;
+        for (int i = 0; i < n_samples; ++i) {
+            CalibSample s;
+            s.layout = SequenceLayout::prefix(visual[i], text[i]);
+            s.embeddings = mat(embeddings[i], s.layout.total(), m->model.config.d_model);
+            samples.push_back(std::move(s));
+        }
+        const int L = m->model.config.n_layers;
+        ActScales a = fit_act_scales(m->model, samples, 4);
+        size_t k = 0;
+        for (const auto& l : a.layers) {
+            act_scales[k++] = l.attn_in.scales[0];
+            act_scales[k++] = l.attn_out.scales[0];
+            act_scales[k++] = l.mlp_in.scales[0];
+            act_scales[k++] = l.mlp_mid.scales[0];
+        }
+        act_scales[k] = a.head_in.scales[0];
+        if (qref_model_prepare_quant(h, 4, 4, 4, 2, act_scales) != 0) throw std::runtime_error(g_err);
+        LayerDiagnostics diag = profile_diagnostics(m->model, samples, m->env.get());
+        std::vector<int> cand = select_candidate_layers(diag, window);
+        SensitivityProfile prof = profile_sensitivity(m->model, samples, cand, eta, m->env.get());
+        BudgetSchedule sched = make_budget_schedule(prof, tau, p_min);
+        std::copy(cand.begin(), cand.end(), layers);
+        std::copy(sched.keep_ratios.begin(), sched.keep_ratios.end(), keeps);
+        std::copy(prof.raw.begin(), prof.raw.end(), raw);
+        std::copy(prof.normalized.begin(), prof.normalized.end(), normalized);
+        for (int l = 0; l < L; ++l) {
+            conc_median[l] = diag.concentration_median[l];
+            red_median[l] = diag.redundancy_median[l];
+        }
+    });
+}
+
 }  // extern "C"

@@ -91,6 +91,9 @@ def lib():
         L.qt_engine_fit_act_scales.argtypes = [vp, C.c_int, C.POINTER(dp), ip, ip, dp, C.c_int]
         L.qt_engine_profile_sensitivity.argtypes = [vp, C.c_int, C.POINTER(dp), ip, ip, C.c_int, ip, C.c_double,
                                                     dp, dp]
+        L.qt_engine_profile_diagnostics.argtypes = [vp, C.c_int, C.POINTER(dp), ip, ip, dp, dp, dp]
+        L.qt_engine_run_quota_calibration.argtypes = [vp, C.c_int, C.POINTER(dp), ip, ip, C.c_int, C.c_double,
+                                                      C.c_double, C.c_double, dp, ip, dp, dp, dp, dp, dp]
         L.qt_engine_save.argtypes = [vp, C.c_char_p]
         L.qt_engine_load.argtypes = [vp, C.c_char_p]
         L.qt_engine_scores.argtypes = [vp, C.c_int, C.c_int, dp, dp, C.c_int, ip]
@@ -236,6 +239,21 @@ class Engine:
                                                   eta, raw.ctypes.data_as(C.POINTER(C.c_double)),
                                                   nrm.ctypes.data_as(C.POINTER(C.c_double))))
         return raw, nrm
+
+    def run_quota_calibration(self, samples, window=5, p_min=0.3, tau=0.25, eta=1e-6):
+        """run_quota_calibration (calibrator.cpp:251-268) on the device -> dict with the
+        act scales (installed), recipe layers / keep ratios, sensitivities and diagnostics."""
+        embs = [np.ascontiguousarray(e, dtype=np.float64) for e, _, _ in samples]
+        arr = (C.POINTER(C.c_double) * len(embs))(*[e.ctypes.data_as(C.POINTER(C.c_double)) for e in embs])
+        vis, txt = _i32([v for _, v, _ in samples]), _i32([t for _, _, t in samples])
+        L = self.cfg.n_layers
+        acts, lay, kp = np.empty(4 * L + 1), np.empty(window, dtype=np.int32), np.empty(window)
+        raw, nrm, cm, rm = np.empty(window), np.empty(window), np.empty(L), np.empty(L)
+        dp_ = lambda a: a.ctypes.data_as(C.POINTER(C.c_double))
+        check(lib().qt_engine_run_quota_calibration(self.h, len(embs), arr, _ip(vis), _ip(txt), window, p_min, tau,
+                                                    eta, dp_(acts), _ip(lay), dp_(kp), dp_(raw), dp_(nrm), dp_(cm),
+                                                    dp_(rm)))
+        return dict(act_scales=acts, layers=lay, keeps=kp, raw=raw, normalized=nrm, conc=cm, red=rm)
 
     def save(self, path):
         """Write the packed-int4 weight file (device layout, include/quota_b200.h)."""

@@ -293,6 +293,12 @@ struct qt_engine {
     // full-precision calibration forward (k_fp.cu)
     bool keep_fp = false;
     std::vector<std::vector<double>>* rec_blocks = nullptr;  // block outputs of the next prefill (B = 1)
+    // QUOTA diagnostics of the next prefill (B = 1, calibration only): per layer the text
+    // queries' top-10 visual attention mass [H x T] and the visual-state cosine Gram [V x V]
+    struct DiagRec {
+        std::vector<std::vector<double>> top10, gram;
+    };
+    DiagRec* rec_diag = nullptr;
     std::vector<FpLayer> fpw;
     double* fp_head = nullptr;
     cublasHandle_t blas = nullptr;
@@ -702,6 +708,86 @@ struct qt_engine {
             normd[k] = p90 - p10 < 1e-12 ? 0.5 : std::clamp((r[k] - p10) * (1.0 / (p90 - p10)), 0.1, 0.9);
     }
 
+    // one layer's diagnostics record (LayerActivationRecord, model.cpp:382-402) for B = 1
+    void diag_layer(int l, const int* ptl, int V, int T, const double* x) {
+        if (l == 0) {
+            rec_diag->top10.assign(L, {});
+            rec_diag->gram.assign(L, {});
+        }
+        const int S = V + T;
+        if (T > 0 && V > 0) {
+            double* dt = dalloc<double>((size_t)H * T);
+            ckl(qt_launch_diag_top10(qkv, n_qkv, H, Hkv, dh, V, S, pool, page_bytes, ptl, dt, st), "diag top-10");
+            rec_diag->top10[l].resize((size_t)H * T);
+            ck(cudaMemcpyAsync(rec_diag->top10[l].data(), dt, (size_t)H * T * 8, cudaMemcpyDeviceToHost, st), "diag");
+            ck(cudaStreamSynchronize(st), "diag");
+            cudaFree(dt);
+        }
+        if (V >= 2) {  // Gram of the visual rows of the post-attention residual (fp64 DGEMM)
+            if (!blas && cublasCreate(&blas) != CUBLAS_STATUS_SUCCESS) fail(QT_ECUDA, "cublasCreate failed");
+            cublasSetStream(blas, st);
+            double* g = dalloc<double>((size_t)V * V);
+            const double one = 1.0, zero = 0.0;
+            if (cublasDgemm(blas, CUBLAS_OP_T, CUBLAS_OP_N, V, V, d, &one, x, d, x, d, &zero, g, V) !=
+                CUBLAS_STATUS_SUCCESS)
+                fail(QT_ECUDA, "cublasDgemm failed");
+            rec_diag->gram[l].resize((size_t)V * V);
+            ck(cudaMemcpyAsync(rec_diag->gram[l].data(), g, (size_t)V * V * 8, cudaMemcpyDeviceToHost, st), "diag");
+            ck(cudaStreamSynchronize(st), "diag");
+            cudaFree(g);
+        }
+    }
+
+    // profile_diagnostics (calibrator.cpp:147-195) with this engine's quantized forward:
+    // per layer, over samples, the median / IQR of the text queries' top-10 visual mass
+    // (averaged over heads and text rows) and the median of the visual rows' median
+    // pairwise cosine (numeric.cpp:117-127)
+    void profile_diagnostics(int n, const double* const* embs, const int* vis, const int* txt, double* conc_med,
+                             double* conc_iqr, double* red_med) {
+        if (n < 1) fail(QT_EINVAL, "no calibration samples");
+        if (cfg.act_mode == 0 && !act_set) fail(QT_EINVAL, "quantized mode requires a QuantEnv");
+        std::vector<std::vector<double>> conc(L), red(L);
+        const bool had_recipe = have_recipe;
+        have_recipe = false;
+        DiagRec dr;
+        try {
+            for (int i = 0; i < n; ++i) {
+                if (vis[i] < 2) fail(QT_EINVAL, "need at least two token rows");  // numeric.cpp:118
+                rec_diag = &dr;
+                prefill(1, embs[i], 0, 1, &vis[i], &txt[i], nullptr, nullptr, nullptr, 0);
+                rec_diag = nullptr;
+                const int V = vis[i], T = txt[i];
+                for (int l = 0; l < L; ++l) {
+                    double total = 0.0;
+                    for (double v : dr.top10[l]) total += v;  // heads, then text rows
+                    conc[l].push_back(T == 0 ? 0.0 : total / (double)(H * T));
+                    const std::vector<double>& g = dr.gram[l];
+                    std::vector<double> sims;
+                    sims.reserve((size_t)V * (V - 1) / 2);
+                    for (int a = 0; a < V; ++a) {
+                        const double na = std::sqrt(g[(size_t)a * V + a]);
+                        for (int b = a + 1; b < V; ++b) {
+                            const double nb = std::sqrt(g[(size_t)b * V + b]);
+                            if (na == 0.0 || nb == 0.0) fail(QT_EINVAL, "degenerate token");  // numeric.cpp:80
+                            sims.push_back(g[(size_t)a * V + b] / (na * nb));
+                        }
+                    }
+                    red[l].push_back(pctl(sims, 50.0));
+                }
+            }
+        } catch (...) {
+            rec_diag = nullptr;
+            have_recipe = had_recipe;
+            throw;
+        }
+        have_recipe = had_recipe;
+        for (int l = 0; l < L; ++l) {
+            conc_med[l] = pctl(conc[l], 50.0);
+            conc_iqr[l] = pctl(conc[l], 75.0) - pctl(conc[l], 25.0);
+            red_med[l] = pctl(red[l], 50.0);
+        }
+    }
+
     static constexpr int B_MAX_MK = 8;
     bool mk_usable() const { return use_mk && mk_possible && B >= 1 && B <= 8; }
 
@@ -1035,6 +1121,7 @@ struct qt_engine {
             }
             norm_quant(attn, 0, d, nullptr, M, d, kd_pad, 4 * l + 1);
             gemm(QT_EPI_RESADD, w.o, nd_pad, w.s_o, M, d, kd_pad, xc, d);
+            if (rec_diag) diag_layer(l, ptl, cur_v[0], h_txt[0], xc);
             for (int b = 0; b < B; ++b) h_kvlen[(size_t)l * B + b] = cur_v[b] + h_txt[b];
 
             // recipe hook at candidate layers (selector.cpp:214-227, model.cpp:404-427)
@@ -1491,6 +1578,94 @@ int qt_engine_profile_sensitivity(qt_engine* e, int n_samples, const double* con
     return guard([&] {
         if (!embs || !visual || !text || !layers || !raw || !normalized) fail(QT_EINVAL, "null argument");
         e->profile_sensitivity(n_samples, embs, visual, text, n_layers, layers, eta, raw, normalized);
+    });
+}
+
+int qt_engine_profile_diagnostics(qt_engine* e, int n_samples, const double* const* embs, const int* visual,
+                                  const int* text, double* conc_median, double* conc_iqr, double* red_median) {
+    return guard([&] {
+        if (!embs || !visual || !text || !conc_median || !conc_iqr || !red_median) fail(QT_EINVAL, "null argument");
+        e->profile_diagnostics(n_samples, embs, visual, text, conc_median, conc_iqr, red_median);
+    });
+}
+
+// select_candidate_layers (calibrator.cpp:197-223): the window maximising mean(concentration)
+// - mean(redundancy), excluding the first front_exclude and last tail_exclude layers
+static std::vector<int> quota_select_window(const double* conc, const double* red, int n, int window,
+                                            int front_exclude, int tail_exclude) {
+    if (window < 1) fail(QT_EINVAL, "window must be >= 1");
+    if (tail_exclude < 0) tail_exclude = n / 4;
+    const int first = front_exclude, last = n - tail_exclude;
+    if (last - first < window) fail(QT_EINVAL, "infeasible candidate window");
+    int best = first;
+    double best_score = -1e300;
+    for (int st0 = first; st0 + window <= last; ++st0) {
+        double c = 0.0, r = 0.0;
+        for (int l = st0; l < st0 + window; ++l) {
+            c += conc[l];
+            r += red[l];
+        }
+        const double score = (c - r) / (double)window;
+        if (score > best_score) {  // strict: ties keep the earliest window
+            best_score = score;
+            best = st0;
+        }
+    }
+    std::vector<int> out(window);
+    for (int i = 0; i < window; ++i) out[i] = best + i;
+    return out;
+}
+
+// make_budget_schedule (calibrator.cpp:100-141): Eq. 3 drop shares softmax((1 - s)/tau),
+// Eq. 4 cumulative keep ratios floored at p_min, the last one exactly p_min
+static std::vector<double> quota_keep_schedule(const std::vector<double>& normalized, double tau, double p_min) {
+    if (tau <= 0.0) fail(QT_EINVAL, "invalid temperature");
+    if (!(p_min > 0.0 && p_min <= 1.0)) fail(QT_EINVAL, "p_min outside (0,1]");
+    const size_t n = normalized.size();
+    std::vector<double> logits(n), share(n);
+    double mx = 1.0 - normalized[0];
+    for (size_t i = 0; i < n; ++i) {
+        logits[i] = 1.0 - normalized[i];
+        mx = std::max(mx, logits[i]);
+    }
+    double sum = 0.0;
+    for (size_t i = 0; i < n; ++i) {
+        share[i] = std::exp((logits[i] - mx) / tau);
+        sum += share[i];
+    }
+    for (double& v : share) v /= sum;
+    const double budget = 1.0 - p_min;
+    std::vector<double> keep(n);
+    double dropped = 0.0;
+    for (size_t i = 0; i < n; ++i) {
+        dropped += budget * share[i];
+        keep[i] = std::max(p_min, 1.0 - dropped);
+    }
+    keep.back() = p_min;
+    return keep;
+}
+
+int qt_engine_run_quota_calibration(qt_engine* e, int n_samples, const double* const* embs, const int* visual,
+                                    const int* text, int window, double p_min, double tau, double eta,
+                                    double* act_scales, int* layers, double* keep_ratios, double* raw,
+                                    double* normalized, double* conc_median, double* red_median) {
+    return guard([&] {
+        if (!embs || !visual || !text || !act_scales || !layers || !keep_ratios) fail(QT_EINVAL, "null argument");
+        // run_quota_calibration (calibrator.cpp:251-268) on explicit samples
+        e->fit_act_scales(n_samples, embs, visual, text, act_scales);
+        if (qt_engine_set_act_scales(e, act_scales) != 0) fail(QT_EINVAL, qt_last_error());
+        std::vector<double> cm(e->L), ci(e->L), rm(e->L);
+        e->profile_diagnostics(n_samples, embs, visual, text, cm.data(), ci.data(), rm.data());
+        const std::vector<int> cand = quota_select_window(cm.data(), rm.data(), e->L, window, 2, -1);
+        std::vector<double> rw(cand.size()), nm(cand.size());
+        e->profile_sensitivity(n_samples, embs, visual, text, (int)cand.size(), cand.data(), eta, rw.data(), nm.data());
+        const std::vector<double> keep = quota_keep_schedule(nm, tau, p_min);
+        std::copy(cand.begin(), cand.end(), layers);
+        std::copy(keep.begin(), keep.end(), keep_ratios);
+        if (raw) std::copy(rw.begin(), rw.end(), raw);
+        if (normalized) std::copy(nm.begin(), nm.end(), normalized);
+        if (conc_median) std::copy(cm.begin(), cm.end(), conc_median);
+        if (red_median) std::copy(rm.begin(), rm.end(), red_median);
     });
 }
 

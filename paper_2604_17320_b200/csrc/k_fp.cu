@@ -115,6 +115,78 @@ __global__ void k_fp_mlp_act(const double* __restrict__ g, const double* __restr
     if (threadIdx.x == 0) atomic_max_abs(obs, mx);
 }
 
+// QUOTA diagnostics (profile_diagnostics, calibrator.cpp:147-195): for text query i
+// and head h of the quantized forward, the attention probabilities over the
+// allowed keys (every visual key + causal text, model.cpp:35-44) from q and the
+// dequantised int4 keys of the cache (model.cpp:371-381); out = the summed top-10
+// mass on the visual keys (concentration_for_record, calibrator.cpp:151-167).
+// One warp per (text query, head); scores staged in shared memory.
+__global__ void k_diag_top10(const float* __restrict__ qkv, int ldq, int H, int Hkv, int dh, int V, int S,
+                             const uint8_t* __restrict__ pool, long long page_bytes, const int* __restrict__ pt,
+                             double* __restrict__ out) {
+    extern __shared__ float sc[];  // [warps][S]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int item = blockIdx.x * nw + warp;  // (text query t, head h)
+    const int T = S - V;
+    if (item >= T * H) return;
+    const int t = item / H, h = item % H, i = V + t;
+    const int kh = h / (H / Hkv);
+    float* s = sc + (size_t)warp * S;
+    const float* q = qkv + (size_t)i * ldq + h * dh;
+    const float inv_sqrt = (float)(1.0 / sqrt((double)dh));
+    const size_t cb = (size_t)Hkv * kPage * (dh / 2);
+    float mx = -1e30f;
+    const int nkeys = i + 1;  // visual prefix + causal text up to i
+    for (int j = lane; j < nkeys; j += 32) {
+        const uint8_t* page = pool + (long long)pt[j / kPage] * page_bytes;
+        const uint8_t* kr = page + ((size_t)kh * kPage + j % kPage) * (dh / 2);
+        const float ks = reinterpret_cast<const float*>(page + 2 * cb)[kh * kPage + j % kPage];
+        float dsum = 0.f;
+        for (int c = 0; c < dh / 2; ++c) {
+            const int b = kr[c];
+            dsum = fmaf(q[2 * c], (float)(((int)(b << 28)) >> 28), dsum);
+            dsum = fmaf(q[2 * c + 1], (float)(((int)(b << 24)) >> 28), dsum);
+        }
+        const float v = dsum * ks * inv_sqrt;
+        s[j] = v;
+        mx = fmaxf(mx, v);
+    }
+    mx = warp_max(mx);
+    float sum = 0.f;
+    for (int j = lane; j < nkeys; j += 32) {
+        const float e = expf(s[j] - mx);
+        s[j] = e;
+        sum += e;
+    }
+    sum = warp_sum(sum);
+    __syncwarp();
+    // top-10 of the visual probabilities: 10 rounds of a warp argmax, each removing the winner
+    double mass = 0.0;
+    const int k = min(10, V);
+    for (int r = 0; r < k; ++r) {
+        float best = -1.f;
+        int bj = -1;
+        for (int j = lane; j < V; j += 32)
+            if (s[j] > best) {
+                best = s[j];
+                bj = j;
+            }
+        for (int o = 16; o > 0; o >>= 1) {
+            const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+            const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+            if (ob > best || (ob == best && oj < bj)) {
+                best = ob;
+                bj = oj;
+            }
+        }
+        mass += (double)best / (double)sum;
+        __syncwarp();
+        if (lane == 0 && bj >= 0) s[bj] = -2.f;
+        __syncwarp();
+    }
+    if (lane == 0) out[(size_t)h * T + t] = mass;
+}
+
 }  // namespace qt
 
 using namespace qt;
@@ -149,6 +221,18 @@ int qt_launch_fp_mlp_act(const double* g, const double* u, long long n, double* 
                          cudaStream_t st) {
     if (n <= 0) return 0;
     k_fp_mlp_act<<<296, 256, 0, st>>>(g, u, n, mid, obs);
+    return (int)cudaGetLastError();
+}
+
+int qt_launch_diag_top10(const float* qkv, int ldq, int H, int Hkv, int dh, int V, int S, const uint8_t* pool,
+                         long long page_bytes, const int* pt, double* out, cudaStream_t st) {
+    const int T = S - V;
+    if (T <= 0 || V <= 0) return 0;
+    const int nw = 4;
+    const size_t smem = (size_t)nw * S * sizeof(float);
+    if (smem > 200 * 1024) return -1;
+    cudaFuncSetAttribute(k_diag_top10, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_diag_top10<<<(T * H + nw - 1) / nw, nw * 32, smem, st>>>(qkv, ldq, H, Hkv, dh, V, S, pool, page_bytes, pt, out);
     return (int)cudaGetLastError();
 }
 

@@ -41,6 +41,8 @@ int qt_launch_fp_attention(const double* qkv, int ldq, int H, int Hkv, int dh, i
                            unsigned long long* obs, cudaStream_t st);
 int qt_launch_fp_mlp_act(const double* g, const double* u, long long n, double* mid, unsigned long long* obs,
                          cudaStream_t st);
+int qt_launch_diag_top10(const float* qkv, int ldq, int H, int Hkv, int dh, int V, int S, const uint8_t* pool,
+                         long long page_bytes, const int* pt, double* out, cudaStream_t st);
 int qt_launch_codes_pack(const int8_t* src, int K, int N, const double* s_in, int row_mul, int row_add,
                          uint8_t* codes, int ldc, double* scales, cudaStream_t st);
 // out: double* for QT_EPI_RESADD (the fp64 residual stream), float* otherwise

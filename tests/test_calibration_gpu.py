@@ -71,3 +71,27 @@ def test_profile_sensitivity_matches_reference(torch_cuda):
     np.testing.assert_allclose(raw, raw_ref, rtol=1e-4)
     np.testing.assert_allclose(nrm, nrm_ref, atol=1e-3)
     assert np.all((nrm >= 0.1) & (nrm <= 0.9))
+
+
+def test_quota_calibration_recipe_matches_reference(torch_cuda):
+    """The offline QUOTA pipeline on the device: act scales, layer diagnostics
+    (top-10 text->visual attention mass, median pairwise cosine), the candidate window, Eq. 1
+    sensitivities and the Eqs. 3-4 keep schedule -> the same recipe as the reference pipeline."""
+    cfg = O.ModelCfg(n_layers=8, d_model=256, n_heads=4, n_kv_heads=4, d_head=64, d_ff=1024, weight_axis=2)
+    ref = O.Ref(cfg, seed=7)
+    w = O.synth_weights(cfg, seed=5)
+    ref.set_weights(w)
+    samples = [(O.synth_embeddings(64 + 8 + 4 * i, 256, seed=300 + i), 64, 8 + 4 * i) for i in range(6)]
+    exp = ref.run_calibration(samples, window=3)
+    e = Q.Engine(Q.Config(n_layers=8, d_model=256, n_heads=4, n_kv_heads=4, d_head=64, d_ff=1024),
+                 max_batch=1, max_tokens=512, max_seq=512, max_decode=4)
+    e.keep_fp_weights(True)
+    e.load_weights(w)
+    got = e.run_quota_calibration(samples, window=3)
+    np.testing.assert_allclose(got["act_scales"], exp["act_scales"], rtol=1e-10)
+    np.testing.assert_allclose(got["conc"], exp["conc"], rtol=1e-4)
+    np.testing.assert_allclose(got["red"], exp["red"], rtol=1e-6, atol=1e-9)
+    assert got["layers"].tolist() == exp["layers"].tolist()
+    np.testing.assert_allclose(got["raw"], exp["raw"], rtol=1e-4)
+    np.testing.assert_allclose(got["keeps"], exp["keeps"], rtol=1e-3)
+    assert got["keeps"][-1] == 0.3 and np.all(np.diff(got["keeps"]) <= 1e-12)
