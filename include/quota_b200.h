@@ -23,6 +23,7 @@
 #ifndef QUOTA_B200_H
 #define QUOTA_B200_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -99,6 +100,22 @@ int qt_engine_load_head_codes(qt_engine* e, const int8_t* codes, const double* s
 int qt_engine_keep_fp_weights(qt_engine* e, int on);
 int qt_engine_fit_act_scales(qt_engine* e, int n_samples, const double* const* embs, const int* visual,
                              const int* text, double* scales_out, int apply);
+/* fit_act_scales with a prune hook (calibrator.cpp:237-249 given calib_hook):
+ * the fp64 forwards run under the engine's recipe (qt_engine_set_recipe: layers,
+ * keeps, v0, metric weights, res_bits -- -1 for nullopt), the scale fit of the
+ * prune_then_quant harness mode (harness.cpp:103-106). */
+int qt_engine_fit_act_scales_hooked(qt_engine* e, int n_samples, const double* const* embs, const int* visual,
+                                    const int* text, double* scales_out, int apply);
+/* forward_prefill in ExecMode::Fp (model.cpp:315-453) of n_seq independent
+ * samples, fp64 on the device, hook != 0 under the engine's recipe
+ * (make_recipe_hook, selector.cpp:211-228, on the fp64 LayerActivationRecord).
+ * The fp_baseline / prune_only forwards of the harness (harness.cpp:134-137).
+ * logits_out (host fp64, may be NULL): each sample's [final rows x d_model]
+ * logits, concatenated, at most cap_rows rows; the trace and final layouts are
+ * read with qt_engine_n_prunes / qt_engine_prune / qt_engine_layout.  No device
+ * KV cache is kept: qt_engine_decode after this call fails. */
+int qt_engine_prefill_fp(qt_engine* e, int n_seq, const double* const* embs, const int* visual, const int* text,
+                         int hook, double* logits_out, long long cap_rows);
 /* profile_sensitivity (calibrator.cpp:42-82), QUOTA Eq. 1: per listed layer the
  * median over samples of ||x_q - x||_F / (||x||_F + eta) between this engine's
  * quantized block outputs and the fp64 forward's, plus normalize_sensitivities
@@ -202,6 +219,10 @@ int qt_kv_quant_append_i4(float* qkv, int ld_qkv, int M, int H, int Hkv, int d_h
                           const int* tok_seq, const int* tok_row, const double* rope_table, const int* page_table,
                           int max_pages, uint8_t* pool, int64_t page_bytes, float* k_out, void* stream);
 int qt_rope_table(int max_pos, int d_head, double* host_out);
+/* FNV-1a 64 over raw bytes (digest.hpp:12-20; seed 0xcbf29ce484222325 to
+ * start): the harness report digests (sample_set_digest, calibrator.cpp:31-40;
+ * recipe_digest, recipe.cpp:132-134; sample_logits_digests, harness.cpp:144). */
+uint64_t qt_fnv1a64(const void* data, size_t len, uint64_t seed);
 /* K3c + K4 on given metrics: score_tokens (robust_normalize x4 + fuse_scores,
  * selector.cpp:70-115) and select_top_k (selector.cpp:117-136) for B
  * sequences.  metrics: device fp64 [B][4][vstride] in (mag, inter, intra, res)

@@ -75,6 +75,12 @@ def ref_lib():
         lib.qref_model_prepare_quant.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, _dp]
         lib.qref_model_weight_codes.argtypes = [C.c_void_p, C.c_int, C.c_int, _i8p, _dp]
         lib.qref_fit_act_scales.argtypes = [C.c_void_p, C.c_int, C.POINTER(_dp), _ip, _ip, C.c_int, _dp]
+        lib.qref_fit_act_scales_hooked.argtypes = [C.c_void_p, C.c_int, C.POINTER(_dp), _ip, _ip, C.c_int,
+                                                   C.c_char_p, _dp, _dp]
+        lib.qref_make_samples.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _ip, _dp,
+                                          C.c_int64, C.c_char_p]
+        lib.qref_pipeline_flops.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                            C.c_double, C.c_double, _dp, _dp]
         lib.qref_prefill.restype = C.c_void_p
         lib.qref_prefill.argtypes = [C.c_void_p, C.c_int, _dp, C.c_int, C.c_int, _ip, C.c_char_p, _dp, C.c_int]
         for n in ("qref_run_free", "qref_run_logits_rows", "qref_run_n_prunes"):
@@ -118,6 +124,34 @@ def ref_lib():
 
 
 # ---------------------------------------------------------------- R0 primitives (kernel-level checkers)
+
+
+def ref_make_samples(seed, count, v0, d_model, text_min, text_max):
+    """make_calibration_samples + sample_set_digest (calibrator.cpp:12-40) of the reference:
+    ([(emb fp64, v0, text)], digest)."""
+    lib = ref_lib()
+    txt = np.empty(count, dtype=np.int32)
+    cap = count * (v0 + text_max) * d_model
+    emb = np.empty(cap, dtype=np.float64)
+    dg = C.create_string_buffer(17)
+    _check(lib.qref_make_samples(seed, count, v0, d_model, text_min, text_max, _i(txt), _d(emb), cap, dg), lib,
+           "qref")
+    out, o = [], 0
+    for t in txt:
+        n = (v0 + int(t)) * d_model
+        out.append((emb[o:o + n].reshape(v0 + int(t), d_model).copy(), v0, int(t)))
+        o += n
+    return out, dg.value.decode()
+
+
+def ref_pipeline_flops(recipe_json, n_layers, v0, d_model, d_ff, n_heads, text_len, f_vt=0.0, f_pj=0.0):
+    """pipeline_flops (gflops.cpp:24-51) of the recipe's executed lengths (None: all at v0)."""
+    lib = ref_lib()
+    costs, o3 = np.empty(n_layers), np.empty(3)
+    rj = recipe_json.encode() if recipe_json is not None else None
+    _check(lib.qref_pipeline_flops(rj, n_layers, v0, d_model, d_ff, n_heads, text_len, f_vt, f_pj, _d(costs),
+                                   _d(o3)), lib, "qref")
+    return costs, float(o3[0]), float(o3[1]), float(o3[2])
 
 
 def ref_compute_budget(keep_ratio, v0):
@@ -363,15 +397,22 @@ class Ref:
     def checksum(self):
         return self.lib.qref_model_weight_checksum(self.h)
 
-    def fit_act_scales(self, samples):
-        """fit_act_scales (calibrator.cpp:237-249); samples = [(emb, visual, text)]."""
+    def fit_act_scales(self, samples, recipe: "Recipe | None" = None, weights=None):
+        """fit_act_scales (calibrator.cpp:237-249); samples = [(emb, visual, text)].  With a
+        recipe: under make_recipe_hook(recipe, weights or recipe.weights, nullopt)."""
         embs = [f64(e) for e, _, _ in samples]
         arr = (_dp * len(embs))(*[_d(e) for e in embs])
         vis = np.array([v for _, v, _ in samples], dtype=np.int32)
         txt = np.array([t for _, _, t in samples], dtype=np.int32)
         out = np.empty(4 * self.cfg.n_layers + 1, dtype=np.float64)
-        _check(self.lib.qref_fit_act_scales(self.h, len(embs), arr, _i(vis), _i(txt), self.cfg.act_bits, _d(out)),
-               self.lib, "qref")
+        if recipe is None:
+            _check(self.lib.qref_fit_act_scales(self.h, len(embs), arr, _i(vis), _i(txt), self.cfg.act_bits,
+                                                _d(out)), self.lib, "qref")
+        else:
+            w = None if weights is None else f64(weights)
+            _check(self.lib.qref_fit_act_scales_hooked(self.h, len(embs), arr, _i(vis), _i(txt), self.cfg.act_bits,
+                                                       recipe.to_json().encode(), _d(w) if w is not None else None,
+                                                       _d(out)), self.lib, "qref")
         return out
 
     def profile_sensitivity(self, samples, layers, eta=1e-6):
@@ -421,12 +462,15 @@ class Ref:
         _check(self.lib.qref_prefill_threads(self.h, n_threads, visual, text, seed, _d(sec)), self.lib, "qref")
         return float(sec[0])
 
-    def prefill(self, emb, visual, text, recipe: Recipe | None = None, quantized=True, res_bits=4, pos=None):
+    def prefill(self, emb, visual, text, recipe: Recipe | None = None, quantized=True, res_bits=4, pos=None,
+                weights=None):
+        """forward_prefill; weights (4 fp64, optional): the hook's MetricWeights instead of the recipe's."""
         e = f64(emb)
         p = None if pos is None else np.ascontiguousarray(pos, dtype=np.int32)
         rj = recipe.to_json().encode() if recipe is not None else None
+        w = None if weights is None else f64(weights)
         r = self.lib.qref_prefill(self.h, int(quantized), _d(e), visual, text, _i(p) if p is not None else None,
-                                  rj, None, res_bits)
+                                  rj, _d(w) if w is not None else None, res_bits)
         if not r:
             raise OracleError(self.lib.qref_last_error().decode())
         return RefRun(self, r)

@@ -344,26 +344,85 @@ int qref_model_set_weight(void* h, int layer, int which, const double* in, int64
 
 // fit_act_scales (calibrator.cpp:237-249) over caller samples (all share d_model).
 // out: n_layers*4 + 1 scales (attn_in, attn_out, mlp_in, mlp_mid per layer; head_in last).
+static void fit_into(void* h, int n_samples, const double* const* embeddings, const int* visual, const int* text,
+                     int act_bits, const PruneHook& hook, double* out) {
+    RefModel* m = static_cast<RefModel*>(h);
+    std::vector<CalibSample> samples;
+    for (int i = 0; i < n_samples; ++i) {
+        CalibSample s;
+        s.layout = SequenceLayout::prefix(visual[i], text[i]);
+        s.embeddings = mat(embeddings[i], s.layout.total(), m->model.config.d_model);
+        samples.push_back(std::move(s));
+    }
+    ActScales a = fit_act_scales(m->model, samples, act_bits, hook);
+    size_t k = 0;
+    for (const auto& l : a.layers) {
+        out[k++] = l.attn_in.scales[0];
+        out[k++] = l.attn_out.scales[0];
+        out[k++] = l.mlp_in.scales[0];
+        out[k++] = l.mlp_mid.scales[0];
+    }
+    out[k] = a.head_in.scales[0];
+}
+
 int qref_fit_act_scales(void* h, int n_samples, const double* const* embeddings, const int* visual,
                         const int* text, int act_bits, double* out) {
+    return guard([&] { fit_into(h, n_samples, embeddings, visual, text, act_bits, PruneHook{}, out); });
+}
+
+// fit_act_scales under make_recipe_hook(recipe, weights4, nullopt): the prune_then_quant
+// scale fit of run_pipeline (harness.cpp:103-106).
+int qref_fit_act_scales_hooked(void* h, int n_samples, const double* const* embeddings, const int* visual,
+                               const int* text, int act_bits, const char* recipe_json, const double* weights4,
+                               double* out) {
     return guard([&] {
-        RefModel* m = static_cast<RefModel*>(h);
-        std::vector<CalibSample> samples;
-        for (int i = 0; i < n_samples; ++i) {
-            CalibSample s;
-            s.layout = SequenceLayout::prefix(visual[i], text[i]);
-            s.embeddings = mat(embeddings[i], s.layout.total(), m->model.config.d_model);
-            samples.push_back(std::move(s));
+        PruningRecipe r = parse_recipe(recipe_json);
+        MetricWeights w = weights4 ? MetricWeights{weights4[0], weights4[1], weights4[2], weights4[3]} : r.weights;
+        fit_into(h, n_samples, embeddings, visual, text, act_bits, make_recipe_hook(r, w, std::nullopt), out);
+    });
+}
+
+// make_calibration_samples (calibrator.cpp:12-29) + sample_set_digest (31-40).
+// text_out[count]; emb_out (may be null): the samples' embeddings concatenated,
+// cap doubles at most; digest17: 16 hex chars + NUL.
+int qref_make_samples(uint64_t seed, int count, int v0, int d_model, int text_min, int text_max, int* text_out,
+                      double* emb_out, int64_t cap, char* digest17) {
+    return guard([&] {
+        std::vector<CalibSample> ss = make_calibration_samples(seed, count, v0, d_model, text_min, text_max);
+        int64_t o = 0;
+        for (int i = 0; i < count; ++i) {
+            text_out[i] = ss[i].layout.text_count;
+            const auto& e = ss[i].embeddings.data;
+            if (emb_out) {
+                if (o + static_cast<int64_t>(e.size()) > cap) throw std::invalid_argument("buffer too small");
+                std::copy(e.begin(), e.end(), emb_out + o);
+            }
+            o += static_cast<int64_t>(e.size());
         }
-        ActScales a = fit_act_scales(m->model, samples, act_bits);
-        size_t k = 0;
-        for (const auto& l : a.layers) {
-            out[k++] = l.attn_in.scales[0];
-            out[k++] = l.attn_out.scales[0];
-            out[k++] = l.mlp_in.scales[0];
-            out[k++] = l.mlp_mid.scales[0];
-        }
-        out[k] = a.head_in.scales[0];
+        std::string dg = sample_set_digest(ss);
+        std::memcpy(digest17, dg.c_str(), 17);
+    });
+}
+
+// pipeline_flops (gflops.cpp:24-51) of a recipe's executed lengths (recipe_json null: every
+// layer at v0, the non-pruning modes, harness.cpp:167-176).  out3 = f_vlm, f_base, ratio_pct.
+int qref_pipeline_flops(const char* recipe_json, int n_layers, int v0, int d_model, int d_ff, int n_heads,
+                        int text_len, double f_vt, double f_pj, double* layer_costs, double* out3) {
+    return guard([&] {
+        CostModel cm;
+        cm.f_vt = f_vt;
+        cm.f_pj = f_pj;
+        cm.d_model = d_model;
+        cm.d_ff = d_ff;
+        cm.n_heads = n_heads;
+        cm.text_len = text_len;
+        std::vector<int> v_hat = recipe_json ? executed_visual_lengths(parse_recipe(recipe_json), n_layers)
+                                             : std::vector<int>(n_layers, v0);
+        GflopsReport g = pipeline_flops(v_hat, v0, cm);
+        for (size_t l = 0; l < g.layers.size(); ++l) layer_costs[l] = g.layers[l].cost;
+        out3[0] = g.f_vlm;
+        out3[1] = g.f_base;
+        out3[2] = g.ratio_pct;
     });
 }
 

@@ -89,6 +89,8 @@ def lib():
         L.qt_rope_table.argtypes = [C.c_int, C.c_int, dp]
         L.qt_engine_keep_fp_weights.argtypes = [vp, C.c_int]
         L.qt_engine_fit_act_scales.argtypes = [vp, C.c_int, C.POINTER(dp), ip, ip, dp, C.c_int]
+        L.qt_engine_fit_act_scales_hooked.argtypes = [vp, C.c_int, C.POINTER(dp), ip, ip, dp, C.c_int]
+        L.qt_engine_prefill_fp.argtypes = [vp, C.c_int, C.POINTER(dp), ip, ip, C.c_int, dp, C.c_int64]
         L.qt_engine_profile_sensitivity.argtypes = [vp, C.c_int, C.POINTER(dp), ip, ip, C.c_int, ip, C.c_double,
                                                     dp, dp]
         L.qt_engine_profile_diagnostics.argtypes = [vp, C.c_int, C.POINTER(dp), ip, ip, dp, dp, dp]
@@ -170,6 +172,7 @@ class Engine:
 
     def __init__(self, cfg: Config, max_batch=8, max_tokens=8192, max_seq=4096, max_decode=128):
         self.cfg = cfg
+        self.max_batch, self.max_tokens, self.max_seq, self.max_decode = max_batch, max_tokens, max_seq, max_decode
         self.h = C.c_void_p()
         check(lib().qt_engine_create(C.byref(cfg.c()), max_batch, max_tokens, max_seq, max_decode, C.byref(self.h)))
 
@@ -216,17 +219,37 @@ class Engine:
         """Keep fp64 copies of the full-precision weights (call before load_*) for calibration."""
         check(lib().qt_engine_keep_fp_weights(self.h, int(on)))
 
-    def fit_act_scales(self, samples, apply=True):
+    def fit_act_scales(self, samples, apply=True, hooked=False):
         """fit_act_scales (calibrator.cpp:237-249) on the device: samples = [(emb fp64 [S x d],
-        visual, text)] -> 4 * n_layers + 1 static scales (installed when apply)."""
+        visual, text)] -> 4 * n_layers + 1 static scales (installed when apply).  hooked: the
+        forwards run under the engine's recipe (the prune_then_quant fit, harness.cpp:103-106)."""
         embs = [np.ascontiguousarray(e, dtype=np.float64) for e, _, _ in samples]
         arr = (C.POINTER(C.c_double) * len(embs))(*[e.ctypes.data_as(C.POINTER(C.c_double)) for e in embs])
         vis = _i32([v for _, v, _ in samples])
         txt = _i32([t for _, _, t in samples])
         out = np.empty(4 * self.cfg.n_layers + 1, dtype=np.float64)
-        check(lib().qt_engine_fit_act_scales(self.h, len(embs), arr, _ip(vis), _ip(txt),
-                                             out.ctypes.data_as(C.POINTER(C.c_double)), int(apply)))
+        fn = lib().qt_engine_fit_act_scales_hooked if hooked else lib().qt_engine_fit_act_scales
+        check(fn(self.h, len(embs), arr, _ip(vis), _ip(txt), out.ctypes.data_as(C.POINTER(C.c_double)), int(apply)))
         return out
+
+    def prefill_fp(self, samples, hook=False):
+        """forward_prefill in ExecMode::Fp (model.cpp:315-453), fp64 on the device, of each
+        sample (emb fp64 [S x d], visual, text); hook: under the engine's recipe.  Returns the
+        per-sample fp64 logits of the final layouts; trace() / layout() read the rest."""
+        embs = [np.ascontiguousarray(e, dtype=np.float64) for e, _, _ in samples]
+        arr = (C.POINTER(C.c_double) * len(embs))(*[e.ctypes.data_as(C.POINTER(C.c_double)) for e in embs])
+        vis = _i32([v for _, v, _ in samples])
+        txt = _i32([t for _, _, t in samples])
+        cap = int(np.sum(vis + txt))
+        out = np.empty((cap, self.cfg.d_model), dtype=np.float64)
+        check(lib().qt_engine_prefill_fp(self.h, len(embs), arr, _ip(vis), _ip(txt), int(hook),
+                                         out.ctypes.data_as(C.POINTER(C.c_double)), cap))
+        res, o = [], 0
+        for b in range(len(embs)):
+            v, t, _ = self.layout(b)
+            res.append(out[o:o + v + t])
+            o += v + t
+        return res
 
     def profile_sensitivity(self, samples, layers, eta=1e-6):
         """QUOTA Eq. 1 sensitivities (calibrator.cpp:42-82) -> (raw, normalized)."""

@@ -548,23 +548,26 @@ struct qt_engine {
 
     // Scratch of the fp64 forward (sized for the longest sample of one call).
     struct FpScratch {
-        double *x = nullptr, *n = nullptr, *q = nullptr, *a = nullptr, *g = nullptr, *u = nullptr, *m = nullptr;
-        int* pos = nullptr;
+        double *x = nullptr, *x2 = nullptr, *n = nullptr, *q = nullptr, *a = nullptr, *g = nullptr, *u = nullptr,
+               *m = nullptr, *probs = nullptr, *met = nullptr;
+        int *pos = nullptr, *pos2 = nullptr, *pid = nullptr;
         unsigned long long* obs = nullptr;
         void release() {
-            for (void* p : {(void*)x, (void*)n, (void*)q, (void*)a, (void*)g, (void*)u, (void*)m, (void*)pos,
-                            (void*)obs})
+            for (void* p : {(void*)x, (void*)x2, (void*)n, (void*)q, (void*)a, (void*)g, (void*)u, (void*)m,
+                            (void*)probs, (void*)met, (void*)pos, (void*)pos2, (void*)pid, (void*)obs})
                 if (p) cudaFree(p);
             *this = FpScratch{};
         }
     };
 
-    void fp_setup(FpScratch& fs, int smax) {
+    // hook_vmax > 0: the recipe hook runs, on visual prefixes up to hook_vmax tokens
+    void fp_setup(FpScratch& fs, int smax, int hook_vmax = 0) {
         if (!keep_fp || fpw.empty() || !fp_head) fail(QT_EINVAL, "calibration needs the full-precision weights "
                                                                  "(qt_engine_keep_fp_weights before loading)");
         if (!blas && cublasCreate(&blas) != CUBLAS_STATUS_SUCCESS) fail(QT_ECUDA, "cublasCreate failed");
         cublasSetStream(blas, st);
         if (smax > max_pos - max_decode - 1) fail(QT_EINVAL, "sample longer than the engine's RoPE table");
+        if (hook_vmax > vstride) fail(QT_EINVAL, "visual prefix exceeds engine capacity");
         const size_t S = smax;
         fs.x = dalloc<double>(S * d);
         fs.n = dalloc<double>(S * d);
@@ -574,58 +577,143 @@ struct qt_engine {
         fs.u = cfg.mlp == 1 ? dalloc<double>(S * dff) : nullptr;
         fs.m = dalloc<double>(S * dff);
         fs.pos = dalloc<int>(S);
+        fs.pid = dalloc<int>(S);
         fs.obs = dalloc<unsigned long long>(4 * L + 1);
+        if (hook_vmax > 0) {
+            fs.x2 = dalloc<double>(S * d);
+            fs.pos2 = dalloc<int>(S);
+            fs.probs = dalloc<double>((size_t)H * S * hook_vmax);
+            fs.met = dalloc<double>((size_t)4 * vstride);
+        }
         std::vector<int> hp(S);
         for (size_t i = 0; i < S; ++i) hp[i] = (int)i;
-        h2d(fs.pos, hp.data(), S * sizeof(int), "positions");
+        h2d(fs.pid, hp.data(), S * sizeof(int), "positions");
     }
+
+    // what a hooked / logits-producing fp64 forward reports (forward_prefill in ExecMode::Fp)
+    struct FpOut {
+        bool hook = false;                     // options.hook = make_recipe_hook(recipe, ...)
+        std::vector<PruneEv>* trace = nullptr;  // ForwardResult::prune_trace
+        std::vector<int>* positions = nullptr;  // final_layout.position_ids
+        int* visual = nullptr;                  // final_layout.visual_count
+        std::vector<double>* logits = nullptr;  // ForwardResult::logits
+    };
 
     // forward_prefill in ExecMode::Fp (model.cpp:315-453) for one sample, fp64; max|x| per
     // site into fs.obs (ActStats, model.cpp:348,393,430,434,443); blocks (optional) gets the
-    // post-block hidden states (ForwardResult::block_outputs, model.cpp:439)
-    void fp_forward(FpScratch& fs, const double* emb, int V, int T, std::vector<std::vector<double>>* blocks) {
-        const int Sq = V + T, kvd = Hkv * dh, ldq = n_qkv;
-        h2d(fs.x, emb, (size_t)Sq * d * sizeof(double), "calibration sample");
+    // post-block hidden states (ForwardResult::block_outputs, model.cpp:439).  With o->hook the
+    // engine's recipe prunes at its candidate layers exactly as make_recipe_hook does
+    // (selector.cpp:211-228): compute_metrics on the fp64 record (model.cpp:382-402), the
+    // device robust-normalise + top-k, and the row compaction of apply_pruning (model.cpp:404-427).
+    void fp_forward(FpScratch& fs, const double* emb, int V, int T, std::vector<std::vector<double>>* blocks,
+                    const FpOut* o = nullptr) {
+        const int kvd = Hkv * dh, ldq = n_qkv;
+        const bool hook = o && o->hook;
+        reset_staging();
+        double *xc = fs.x, *xo = fs.x2;
+        int *pc = fs.pos, *po = fs.pos2;
+        h2d(xc, emb, (size_t)(V + T) * d * sizeof(double), "calibration sample");
+        ck(cudaMemcpyAsync(pc, fs.pid, (size_t)(V + T) * sizeof(int), cudaMemcpyDeviceToDevice, st), "positions");
         if (blocks) blocks->assign(L, {});
+        if (o && o->trace) o->trace->clear();
+        std::vector<int> hpos(V + T);
+        for (int i = 0; i < V + T; ++i) hpos[i] = i;
+        int v = V;
         for (int l = 0; l < L; ++l) {
             const FpLayer& fl = fpw[l];
-            ckl(qt_launch_fp_rmsnorm(fs.x, lw[l].g1, Sq, d, fs.n, fs.obs + 4 * l + 0, st), "fp rmsnorm");
+            const int Sq = v + T;
+            int K = -1;  // budget when l is a candidate layer of the hook's recipe
+            if (hook)
+                for (size_t i = 0; i < recipe.layers.size(); ++i)
+                    if (recipe.layers[i] == l) K = (int)std::ceil(recipe.keeps[i] * (double)recipe.v0);
+            if (K >= 0 && v == 0) fail(QT_EINVAL, "empty sample");  // robust_normalize, selector.cpp:70-71
+            const bool prune = K >= 0 && K < v;
+            ckl(qt_launch_fp_rmsnorm(xc, lw[l].g1, Sq, d, fs.n, fs.obs + 4 * l + 0, st), "fp rmsnorm");
             dgemm(fs.n, Sq, d, fl.w[0], d, fs.q, ldq, 0.0);
             dgemm(fs.n, Sq, d, fl.w[1], kvd, fs.q + d, ldq, 0.0);
             dgemm(fs.n, Sq, d, fl.w[2], kvd, fs.q + d + kvd, ldq, 0.0);
-            ckl(qt_launch_fp_rope(fs.q, ldq, Sq, H + Hkv, dh, fs.pos, rope, st), "fp rope");
-            ckl(qt_launch_fp_attention(fs.q, ldq, H, Hkv, dh, Sq, V, fs.a, d, fs.obs + 4 * l + 1, st),
+            ckl(qt_launch_fp_rope(fs.q, ldq, Sq, H + Hkv, dh, pc, rope, st), "fp rope");
+            ckl(qt_launch_fp_attention(fs.q, ldq, H, Hkv, dh, Sq, v, fs.a, d, fs.obs + 4 * l + 1,
+                                       prune ? fs.probs : nullptr, st),
                 "fp attention");
-            dgemm(fs.a, Sq, d, fl.w[3], d, fs.x, d, 1.0);  // x += attn . Wo
-            ckl(qt_launch_fp_rmsnorm(fs.x, lw[l].g2, Sq, d, fs.n, fs.obs + 4 * l + 2, st), "fp rmsnorm");
-            dgemm(fs.n, Sq, d, fl.w[4], dff, fs.g, dff, 0.0);
-            if (fs.u) dgemm(fs.n, Sq, d, fl.w[6], dff, fs.u, dff, 0.0);
-            ckl(qt_launch_fp_mlp_act(fs.g, fs.u, (long long)Sq * dff, fs.m, fs.obs + 4 * l + 3, st), "fp mlp");
-            dgemm(fs.m, Sq, dff, fl.w[5], d, fs.x, d, 1.0);  // x += mid . W2
+            dgemm(fs.a, Sq, d, fl.w[3], d, xc, d, 1.0);  // x += attn . Wo
+            int S2 = Sq;
+            if (prune) {
+                double* met = fs.met;
+                const std::vector<int> zero{0}, vv{v}, tt{T}, kk{K};
+                upload(seq_off, zero);
+                upload(new_off, zero);
+                upload(seq_vis, vv);
+                upload(seq_txt, tt);
+                upload(budget, kk);
+                ckl(qt_launch_token_metrics(xc, d, seq_off, seq_vis, v, 1, vstride, recipe.res_bits, met,
+                                            met + 3 * vstride, st),
+                    "fp token metrics");
+                ckl(qt_launch_fp_colsum(fs.probs, H, Sq, v, met + vstride, met + 2 * vstride, st),
+                    "fp attention metrics");
+                ckl(qt_launch_select_topk(nullptr, nullptr, nullptr, nullptr, H, vstride, seq_vis, seq_txt, budget,
+                                          seq_off, new_off, 1, v, recipe.w, keep_src, keep_local, vstride, pc,
+                                          kept_pos, nullptr, nullptr, met, 0, st),
+                    "quota top-k");
+                S2 = K + T;
+                ckl(qt_launch_gather_rows(xc, xo, d, pc, po, keep_src, S2, st), "compaction gather");
+                std::swap(xc, xo);
+                std::swap(pc, po);
+                PruneEv e{l, K, std::vector<int>(K)};
+                ck(cudaMemcpyAsync(e.positions.data(), kept_pos, K * sizeof(int), cudaMemcpyDeviceToHost, st),
+                   "trace");
+                ck(cudaStreamSynchronize(st), "trace");
+                std::vector<int> np(e.positions);
+                np.insert(np.end(), hpos.begin() + v, hpos.end());
+                hpos = np;
+                if (o->trace) o->trace->push_back(std::move(e));
+                v = K;
+            }
+            ckl(qt_launch_fp_rmsnorm(xc, lw[l].g2, S2, d, fs.n, fs.obs + 4 * l + 2, st), "fp rmsnorm");
+            dgemm(fs.n, S2, d, fl.w[4], dff, fs.g, dff, 0.0);
+            if (fs.u) dgemm(fs.n, S2, d, fl.w[6], dff, fs.u, dff, 0.0);
+            ckl(qt_launch_fp_mlp_act(fs.g, fs.u, (long long)S2 * dff, fs.m, fs.obs + 4 * l + 3, st), "fp mlp");
+            dgemm(fs.m, S2, dff, fl.w[5], d, xc, d, 1.0);  // x += mid . W2
             if (blocks) {
-                (*blocks)[l].resize((size_t)Sq * d);
-                ck(cudaMemcpyAsync((*blocks)[l].data(), fs.x, (size_t)Sq * d * sizeof(double), cudaMemcpyDeviceToHost,
+                (*blocks)[l].resize((size_t)S2 * d);
+                ck(cudaMemcpyAsync((*blocks)[l].data(), xc, (size_t)S2 * d * sizeof(double), cudaMemcpyDeviceToHost,
                                    st),
                    "block output");
             }
         }
-        ckl(qt_launch_fp_rmsnorm(fs.x, gf, Sq, d, fs.n, fs.obs + 4 * L, st), "fp final norm");
+        const int Sf = v + T;
+        ckl(qt_launch_fp_rmsnorm(xc, gf, Sf, d, fs.n, fs.obs + 4 * L, st), "fp final norm");
+        if (o && o->logits) {  // logits = final_norm . W_head (model.cpp:442-445)
+            dgemm(fs.n, Sf, d, fp_head, d, fs.a, d, 0.0);
+            o->logits->resize((size_t)Sf * d);
+            ck(cudaMemcpyAsync(o->logits->data(), fs.a, (size_t)Sf * d * sizeof(double), cudaMemcpyDeviceToHost, st),
+               "fp logits");
+        }
+        if (o && o->positions) *o->positions = hpos;
+        if (o && o->visual) *o->visual = v;
         ck(cudaStreamSynchronize(st), "fp forward");
     }
 
     // fit_act_scales (calibrator.cpp:237-249): full-precision forwards of the samples with
-    // an ActStats collector; returns max|x| / qmax per site (0 -> 1.0, model.cpp:198-210)
-    void fit_act_scales(int n, const double* const* embs, const int* vis, const int* txt, double* out) {
+    // an ActStats collector; returns max|x| / qmax per site (0 -> 1.0, model.cpp:198-210).
+    // hook: the forwards run under the engine's recipe (the prune_then_quant calibration,
+    // harness.cpp:103-106).
+    void fit_act_scales(int n, const double* const* embs, const int* vis, const int* txt, double* out,
+                        bool hook = false) {
         if (n < 1) fail(QT_EINVAL, "no calibration samples");  // calibrator.cpp:239
-        int smax = 0;
+        if (hook && !have_recipe) fail(QT_EINVAL, "no recipe set");
+        int smax = 0, vmax = 0;
         for (int i = 0; i < n; ++i) {
             if (vis[i] < 0 || txt[i] < 0 || vis[i] + txt[i] < 1) fail(QT_EINVAL, "invalid sample layout");
             smax = std::max(smax, vis[i] + txt[i]);
+            vmax = std::max(vmax, vis[i]);
         }
         FpScratch fs;
         try {
-            fp_setup(fs, smax);
-            for (int i = 0; i < n; ++i) fp_forward(fs, embs[i], vis[i], txt[i], nullptr);
+            fp_setup(fs, smax, hook ? std::max(vmax, 1) : 0);
+            FpOut fo;
+            fo.hook = hook;
+            for (int i = 0; i < n; ++i) fp_forward(fs, embs[i], vis[i], txt[i], nullptr, &fo);
             std::vector<unsigned long long> hm(4 * L + 1);
             ck(cudaMemcpyAsync(hm.data(), fs.obs, hm.size() * 8, cudaMemcpyDeviceToHost, st), "stats");
             ck(cudaStreamSynchronize(st), "stats");
@@ -634,6 +722,62 @@ struct qt_engine {
                 std::memcpy(&mxv, &hm[i], 8);
                 out[i] = mxv == 0.0 ? 1.0 : mxv / 7.0;  // qmax at 4 act bits
             }
+        } catch (...) {
+            fs.release();
+            throw;
+        }
+        fs.release();
+    }
+
+    // forward_prefill in ExecMode::Fp (model.cpp:315-453) of n independent samples, fp64 on the
+    // device; hook: under the engine's recipe (make_recipe_hook, selector.cpp:211-228).  The
+    // logits of each sample's final layout are concatenated into logits_out (cap_rows rows of
+    // d); trace and final layout are readable with qt_engine_n_prunes / prune / layout.  The
+    // fp64 forward keeps no device KV cache: qt_engine_decode after it fails.
+    void prefill_fp(int n, const double* const* embs, const int* vis, const int* txt, bool hook, double* logits_out,
+                    long long cap_rows) {
+        for (auto& l : lw)
+            if (!l.loaded) fail(QT_EINVAL, "model weights not loaded");
+        if (!head_loaded) fail(QT_EINVAL, "model head not loaded");
+        if (n < 1 || n > max_batch) fail(QT_EINVAL, "batch size outside engine capacity");
+        if (hook && !have_recipe) fail(QT_EINVAL, "no recipe set");
+        int smax = 0, vmax = 0;
+        for (int i = 0; i < n; ++i) {
+            if (vis[i] < 0 || txt[i] < 0) fail(QT_EINVAL, "negative token count");
+            if (vis[i] + txt[i] < 1) fail(QT_EINVAL, "empty sequence");
+            smax = std::max(smax, vis[i] + txt[i]);
+            vmax = std::max(vmax, vis[i]);
+        }
+        graph_ok = false;
+        prefilled = false;
+        ev_layers.clear();
+        ev_vis.clear();
+        FpScratch fs;
+        try {
+            fp_setup(fs, smax, hook ? std::max(vmax, 1) : 0);
+            B = n;
+            h_txt.assign(txt, txt + n);
+            h_vis.assign(n, 0);
+            h_pos.assign(n, {});
+            trace.assign(n, {});
+            long long rows = 0;
+            std::vector<double> lg;
+            for (int i = 0; i < n; ++i) {
+                FpOut fo;
+                fo.hook = hook;
+                fo.trace = &trace[i];
+                fo.positions = &h_pos[i];
+                fo.visual = &h_vis[i];
+                fo.logits = &lg;
+                fp_forward(fs, embs[i], vis[i], txt[i], nullptr, &fo);
+                const long long r = (long long)lg.size() / d;
+                if (logits_out) {
+                    if (rows + r > cap_rows) fail(QT_EINVAL, "buffer too small");
+                    std::memcpy(logits_out + rows * d, lg.data(), lg.size() * sizeof(double));
+                }
+                rows += r;
+            }
+            final_rows = (int)rows;
         } catch (...) {
             fs.release();
             throw;
@@ -1447,6 +1591,16 @@ const char* qt_last_error(void) { return g_err.c_str(); }
 
 void qt_set_last_error(const char* msg) { g_err = msg ? msg : ""; }
 
+uint64_t qt_fnv1a64(const void* data, size_t len, uint64_t seed) {
+    const unsigned char* p = static_cast<const unsigned char*>(data);
+    uint64_t h = seed;
+    for (size_t i = 0; i < len; ++i) {
+        h ^= p[i];
+        h *= 0x100000001b3ULL;
+    }
+    return h;
+}
+
 int qt_rope_table(int max_pos, int d_head, double* out) {
     // cos/sin of pos * 10000^(-2i/d_head), exactly as rope_in_place (model.cpp:156-168)
     for (int p = 0; p < max_pos; ++p)
@@ -1569,6 +1723,23 @@ int qt_engine_fit_act_scales(qt_engine* e, int n_samples, const double* const* e
         if (!embs || !visual || !text || !scales_out) fail(QT_EINVAL, "null argument");
         e->fit_act_scales(n_samples, embs, visual, text, scales_out);
         if (apply && qt_engine_set_act_scales(e, scales_out) != 0) fail(QT_EINVAL, qt_last_error());
+    });
+}
+
+int qt_engine_fit_act_scales_hooked(qt_engine* e, int n_samples, const double* const* embs, const int* visual,
+                                    const int* text, double* scales_out, int apply) {
+    return guard([&] {
+        if (!embs || !visual || !text || !scales_out) fail(QT_EINVAL, "null argument");
+        e->fit_act_scales(n_samples, embs, visual, text, scales_out, true);
+        if (apply && qt_engine_set_act_scales(e, scales_out) != 0) fail(QT_EINVAL, qt_last_error());
+    });
+}
+
+int qt_engine_prefill_fp(qt_engine* e, int n_seq, const double* const* embs, const int* visual, const int* text,
+                         int hook, double* logits_out, long long cap_rows) {
+    return guard([&] {
+        if (!embs || !visual || !text) fail(QT_EINVAL, "null argument");
+        e->prefill_fp(n_seq, embs, visual, text, hook != 0, logits_out, cap_rows);
     });
 }
 

@@ -57,9 +57,12 @@ __global__ void k_fp_rope(double* __restrict__ qkv, int ldq, int nheads_qk, int 
 
 // masked softmax attention (model.cpp:35-44, 272-292, 385) for one (query row,
 // head) per CTA, fp64: visual queries see visual keys; text queries see every
-// visual key and causal text.  dh threads.
+// visual key and causal text.  dh threads.  probs (optional, recipe hook): the
+// normalised probabilities on the visual keys, [H][S][V] -- the blocks the
+// reference slices into attn_inter / attn_intra (model.cpp:386-389).
 __global__ void k_fp_attention(const double* __restrict__ qkv, int ldq, int H, int Hkv, int dh, int S, int V,
-                               double* __restrict__ out, int ldo, unsigned long long* __restrict__ obs) {
+                               double* __restrict__ out, int ldo, unsigned long long* __restrict__ obs,
+                               double* __restrict__ probs) {
     extern __shared__ double sm[];
     double* qs = sm;           // [dh]
     double* p = sm + dh;       // [S] probabilities
@@ -95,8 +98,29 @@ __global__ void k_fp_attention(const double* __restrict__ qkv, int ldq, int H, i
         out[(size_t)i * ldo + h * dh + c] = o;
         omax = fmax(omax, fabs(o));
     }
-    omax = block_max(omax, red);
-    if (threadIdx.x == 0) atomic_max_abs(obs, omax);
+    if (probs)
+        for (int j = threadIdx.x; j < V; j += blockDim.x) probs[((size_t)h * S + i) * V + j] = p[j] / sum;
+    if (obs) {
+        omax = block_max(omax, red);
+        if (threadIdx.x == 0) atomic_max_abs(obs, omax);
+    }
+}
+
+// compute_metrics' attention cues (selector.cpp:40-53) from the [H][S][V] probabilities:
+// inter[j] = sum over heads, then text query rows, of p(row, j); intra over visual query
+// rows; both * (1/H).  One thread per visual key, summed in the reference's order.
+__global__ void k_fp_colsum(const double* __restrict__ probs, int H, int S, int V, double* __restrict__ inter,
+                            double* __restrict__ intra) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= V) return;
+    double si = 0.0, sa = 0.0;
+    for (int h = 0; h < H; ++h)
+        for (int r = V; r < S; ++r) si = __dadd_rn(si, probs[((size_t)h * S + r) * V + j]);
+    for (int h = 0; h < H; ++h)
+        for (int r = 0; r < V; ++r) sa = __dadd_rn(sa, probs[((size_t)h * S + r) * V + j]);
+    const double inv = 1.0 / (double)H;
+    inter[j] = __dmul_rn(si, inv);
+    intra[j] = __dmul_rn(sa, inv);
 }
 
 // mid = silu(g) (SiLU MLP, model.cpp:432-434) or silu(g) * u (SwiGLU), observed
@@ -208,12 +232,18 @@ int qt_launch_fp_rope(double* qkv, int ldq, int M, int nheads_qk, int dh, const 
 }
 
 int qt_launch_fp_attention(const double* qkv, int ldq, int H, int Hkv, int dh, int S, int V, double* out, int ldo,
-                           unsigned long long* obs, cudaStream_t st) {
+                           unsigned long long* obs, double* probs, cudaStream_t st) {
     if (S <= 0) return 0;
     const size_t smem = (size_t)(dh + S) * sizeof(double);
     if (smem > 200 * 1024) return -1;
     cudaFuncSetAttribute(k_fp_attention, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_fp_attention<<<dim3(S, H), dh, smem, st>>>(qkv, ldq, H, Hkv, dh, S, V, out, ldo, obs);
+    k_fp_attention<<<dim3(S, H), dh, smem, st>>>(qkv, ldq, H, Hkv, dh, S, V, out, ldo, obs, probs);
+    return (int)cudaGetLastError();
+}
+
+int qt_launch_fp_colsum(const double* probs, int H, int S, int V, double* inter, double* intra, cudaStream_t st) {
+    if (V <= 0) return 0;
+    k_fp_colsum<<<(V + 127) / 128, 128, 0, st>>>(probs, H, S, V, inter, intra);
     return (int)cudaGetLastError();
 }
 

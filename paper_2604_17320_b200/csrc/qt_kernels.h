@@ -38,7 +38,8 @@ int qt_launch_fp_rmsnorm(const double* x, const float* gain, int M, int D, doubl
 int qt_launch_fp_rope(double* qkv, int ldq, int M, int nheads_qk, int dh, const int* pos, const double* rope,
                       cudaStream_t st);
 int qt_launch_fp_attention(const double* qkv, int ldq, int H, int Hkv, int dh, int S, int V, double* out, int ldo,
-                           unsigned long long* obs, cudaStream_t st);
+                           unsigned long long* obs, double* probs, cudaStream_t st);
+int qt_launch_fp_colsum(const double* probs, int H, int S, int V, double* inter, double* intra, cudaStream_t st);
 int qt_launch_fp_mlp_act(const double* g, const double* u, long long n, double* mid, unsigned long long* obs,
                          cudaStream_t st);
 int qt_launch_diag_top10(const float* qkv, int ldq, int H, int Hkv, int dh, int V, int S, const uint8_t* pool,
