@@ -16,7 +16,7 @@ from dataclasses import dataclass
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_build", "libquota_b200.so")
+LIB_PATH = os.environ.get("QT_LIB_PATH") or os.path.join(HERE, "_build", "libquota_b200.so")  # override: A/B builds
 ROOT = os.path.dirname(HERE)
 HEADER = os.path.join(ROOT, "include", "quota_b200.h")
 

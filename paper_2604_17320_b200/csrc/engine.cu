@@ -302,6 +302,11 @@ struct qt_engine {
     std::vector<FpLayer> fpw;
     double* fp_head = nullptr;
     cublasHandle_t blas = nullptr;
+    // per-row partial max |x| of the mlp_mid site left by the gate|up GEMM epilogue (act_mode 1)
+    static constexpr int kPmaxLd = 512;
+    const bool use_pmax = !(std::getenv("QT_PMAX") && std::atoi(std::getenv("QT_PMAX")) == 0);
+    float* pmax = nullptr;
+    int pm_parts = 0;
     int* splitk_ws = nullptr;     // int32 split-K partials of the tcgen05 GEMM at small M
     unsigned* seq_cnt = nullptr;  // per-sequence arrival counters of the fused decode attention block
     // opt-in (QT_ATTN_FUSED=1): one kernel for RoPE + KV append + attention + attn_out quant; measured
@@ -333,7 +338,7 @@ struct qt_engine {
             for (double* p : fl.w) f(p);
         f(fp_head);
         if (blas) cublasDestroy(blas);
-        f(splitk_ws); f(seq_cnt); f(mk_trace); f(mk_layers); f(mk_acc); f(mk_codes); f(mk_sa); f(mk_attn); f(mk_sync); f(mk_act);
+        f(splitk_ws); f(pmax); f(seq_cnt); f(mk_trace); f(mk_layers); f(mk_acc); f(mk_codes); f(mk_sa); f(mk_attn); f(mk_sync); f(mk_act);
         if (pin) cudaFreeHost(pin);
         if (own_stream) cudaStreamDestroy(own_stream);
     }
@@ -479,6 +484,7 @@ struct qt_engine {
                 }
             if (need) splitk_ws = dalloc<int>(need);
         }
+        if (cfg.act_mode == 1 && use_pmax) pmax = dalloc<float>((size_t)std::max(mt, mb) * kPmaxLd);
         mk_init();
         pin_cap = (size_t)64 << 20;
         pin_cap += (size_t)mt * (sizeof(int) * 8);
@@ -1070,22 +1076,37 @@ struct qt_engine {
     }
 
     // ------------------------------------------------------------ kernels
-    void norm_quant(const void* xin, int is_f64, int ldx, const float* gain, int M, int D, int dpad, int site_idx) {
+    // from_pmax: the site input is the fp32 output of the last gemm(), whose epilogue left the
+    // per-row partial maxima in pmax (pm_parts > 0): quantize without a row reduction
+    void norm_quant(const void* xin, int is_f64, int ldx, const float* gain, int M, int D, int dpad, int site_idx,
+                    bool from_pmax = false) {
         const int mode = cfg.act_mode;
         const double s = mode == 0 ? act[site_idx] : 0.0;
         pb(P_QUANT);
-        ckl(qt_launch_norm_quant(xin, is_f64, ldx, gain, M, D, dpad, 4, mode, s, codes, codes_rows, ascale, nullptr, st),
-            "rmsnorm+quant");
+        if (from_pmax && pm_parts > 0 && !is_f64 && !gain && mode == 1)
+            ckl(qt_launch_quant_pmax(static_cast<const float*>(xin), ldx, pmax, pm_parts, kPmaxLd, M, D, dpad, 7, mode,
+                                     s, codes, codes_rows, ascale, st),
+                "quant (producer row max)");
+        else
+            ckl(qt_launch_norm_quant(xin, is_f64, ldx, gain, M, D, dpad, 4, mode, s, codes, codes_rows, ascale,
+                                     nullptr, st),
+                "rmsnorm+quant");
         pe((double)M * D * (is_f64 ? 8 : 4) + (double)M * dpad / 2 + 8.0 * M);
     }
     // w: tiled int4 weights with wrows padded rows; activation codes: tiled with codes_rows rows
-    void gemm(int epi, const uint8_t* w, int wrows, const double* sw, int M, int N, int K, void* out, int ldo) {
+    // want_pm: also leave the per-row partial max |out| in pmax (pm_parts slots; 0 = not produced)
+    void gemm(int epi, const uint8_t* w, int wrows, const double* sw, int M, int N, int K, void* out, int ldo,
+              bool want_pm = false) {
         pb(P_GEMM);
+        float* pm = want_pm ? pmax : nullptr;
+        pm_parts = 0;
         // tcgen05 for token-rich GEMMs; the weight-streaming GEMV up to 64 tokens (decode batches)
         int rc = (use_tc05 && M > 64)
-                     ? qt_launch_w4a4_tc05(epi, codes, codes_rows, ascale, w, wrows, sw, M, N, K, out, ldo, nullptr,
-                                           splitk_ws, st)
-                     : qt_launch_w4a4_mma(epi, codes, codes_rows, ascale, w, wrows, sw, M, N, K, out, ldo, nullptr, st);
+                     ? qt_launch_w4a4_tc05_ex(epi, codes, codes_rows, ascale, w, wrows, sw, M, N, K, out, ldo, nullptr,
+                                              splitk_ws, pm, kPmaxLd, &pm_parts, st)
+                     : qt_launch_w4a4_mma_ex(epi, codes, codes_rows, ascale, w, wrows, sw, M, N, K, out, ldo, nullptr,
+                                             pm, kPmaxLd, &pm_parts, st);
+        qt::g_l2_next = nullptr;  // consumed by the GEMV launcher; never carried past this launch
         ckl(rc, "w4a4 gemm");
         const double out_bytes = epi == QT_EPI_RESADD ? 16.0 * M * N : (epi == QT_EPI_SWIGLU ? 2.0 * M * N : 4.0 * M * N);
         pe((double)N * K / 2 + 8.0 * N + (double)M * K / 2 + 8.0 * M + out_bytes, 2.0 * M * N * K);
@@ -1317,9 +1338,9 @@ struct qt_engine {
             }
             // MLP block (model.cpp:429-437)
             norm_quant(xc, 1, d, w.g2, M, d, kd_pad, 4 * l + 2);
-            if (cfg.mlp == 1) gemm(QT_EPI_SWIGLU, w.gu, n_gu_pad, w.s_gu, M, n_gu, kd_pad, mid, dff);
-            else gemm(QT_EPI_SILU, w.gu, n_gu_pad, w.s_gu, M, n_gu, kd_pad, mid, dff);
-            norm_quant(mid, 0, dff, nullptr, M, dff, kff_pad, 4 * l + 3);
+            if (cfg.mlp == 1) gemm(QT_EPI_SWIGLU, w.gu, n_gu_pad, w.s_gu, M, n_gu, kd_pad, mid, dff, true);
+            else gemm(QT_EPI_SILU, w.gu, n_gu_pad, w.s_gu, M, n_gu, kd_pad, mid, dff, true);
+            norm_quant(mid, 0, dff, nullptr, M, dff, kff_pad, 4 * l + 3, true);
             gemm(QT_EPI_RESADD, w.down, nd_pad, w.s_down, M, d, kff_pad, xc, d);
             if (rec_blocks) {  // ForwardResult::block_outputs (model.cpp:439), calibration only
                 if (l == 0) rec_blocks->assign(L, {});
@@ -1403,6 +1424,13 @@ struct qt_engine {
     }
 
     // ------------------------------------------------------------ decode
+    // the next decode GEMV's weights, prefetched toward L2 by the GEMV launched next (qt_common.cuh)
+    const bool l2_next_on = std::getenv("QT_L2NEXT") && std::atoi(std::getenv("QT_L2NEXT")) != 0;  // opt-in: measured slower
+    void l2_next(const void* w, size_t bytes) {
+        if (!l2_next_on) return;
+        qt::g_l2_next = w;
+        qt::g_l2_next_bytes = (long long)bytes;
+    }
     void decode_body() {
         double* xcur = xd;  // the step's input was written (widened) into xd before the graph
         for (int l = 0; l < L; ++l) {
@@ -1410,6 +1438,7 @@ struct qt_engine {
             int* ptl = pt + (size_t)l * max_batch * max_pages;
             int* lenl = kv_len + (size_t)l * max_batch;
             if (!(g_skip & 4)) norm_quant(xcur, 1, d, w.g1, B, d, kd_pad, 4 * l + 0);
+            l2_next(w.o, (size_t)nd_pad * kd_pad / 2);
             if (!(g_skip & 1)) gemm(QT_EPI_STORE, w.qkv, n_qkv_pad, w.s_qkv, B, n_qkv, kd_pad, qkv, n_qkv);
             if (fused_attn) {
                 // RoPE + K/V append + attention + attn_out quantizer in one kernel
@@ -1444,11 +1473,15 @@ struct qt_engine {
                     pe(rows * Hkv * 2 * (dh / 2 + 4) + (double)B * H * dh * 8);
                 }
             }
+            l2_next(w.gu, (size_t)n_gu_pad * kd_pad / 2);
             if (!(g_skip & 1)) gemm(QT_EPI_RESADD, w.o, nd_pad, w.s_o, B, d, kd_pad, xcur, d);
             if (!(g_skip & 4)) norm_quant(xcur, 1, d, w.g2, B, d, kd_pad, 4 * l + 2);
-            if (g_skip & 1) {} else if (cfg.mlp == 1) gemm(QT_EPI_SWIGLU, w.gu, n_gu_pad, w.s_gu, B, n_gu, kd_pad, mid, dff);
-            else gemm(QT_EPI_SILU, w.gu, n_gu_pad, w.s_gu, B, n_gu, kd_pad, mid, dff);
-            if (!(g_skip & 4)) norm_quant(mid, 0, dff, nullptr, B, dff, kff_pad, 4 * l + 3);
+            l2_next(w.down, (size_t)nd_pad * kff_pad / 2);
+            if (g_skip & 1) {} else if (cfg.mlp == 1) gemm(QT_EPI_SWIGLU, w.gu, n_gu_pad, w.s_gu, B, n_gu, kd_pad, mid, dff, true);
+            else gemm(QT_EPI_SILU, w.gu, n_gu_pad, w.s_gu, B, n_gu, kd_pad, mid, dff, true);
+            if (!(g_skip & 4)) norm_quant(mid, 0, dff, nullptr, B, dff, kff_pad, 4 * l + 3, true);
+            if (l + 1 < L) l2_next(lw[l + 1].qkv, (size_t)n_qkv_pad * kd_pad / 2);
+            else l2_next(head, (size_t)nd_pad * kd_pad / 2);
             if (!(g_skip & 1)) gemm(QT_EPI_RESADD, w.down, nd_pad, w.s_down, B, d, kff_pad, xcur, d);
         }
         norm_quant(xcur, 1, d, gf, B, d, kd_pad, 4 * L);

@@ -167,11 +167,17 @@ static const int qt_gemv_l2_rows_host = getenv("QT_GEMV_L2") ? atoi(getenv("QT_G
 // tokens, decode batches): they do not fit for K = d_ff, so the B fragments are
 // read straight from the (L1/L2-resident) tiled activation codes; each warp
 // keeps re-reading the same k slice across its row blocks.
+#ifndef QT_GEMV_MINB
+#define QT_GEMV_MINB 2  // 3 spills (80 regs) and measured slower
+#endif
+static const int qt_gemv_ctas = getenv("QT_GEMV_CTAS") ? atoi(getenv("QT_GEMV_CTAS")) : QT_GEMV_MINB;
 template <int NT, int EPI>
-__global__ void __launch_bounds__(256) k_gemv_reg(const uint8_t* __restrict__ A, int lda, const double* __restrict__ sa,
+__global__ void __launch_bounds__(256, NT <= 2 ? QT_GEMV_MINB : 1) k_gemv_reg(const uint8_t* __restrict__ A, int lda, const double* __restrict__ sa,
                                                   const uint8_t* __restrict__ W, int ldw, const double* __restrict__ sw,
                                                   int M, int N, int K, void* __restrict__ out, int ldo,
-                                                  int* __restrict__ acc_dbg, int l2rows) {
+                                                  int* __restrict__ acc_dbg, int l2rows,
+                                                  const uint8_t* __restrict__ pf, long long pf_bytes,
+                                                  float* __restrict__ pmax, int pmax_ld) {
     constexpr int TOK = 8 * NT;
     constexpr bool ASM = NT <= 2;     // activation codes staged in smem
     constexpr int U = NT <= 2 ? 4 : 2;
@@ -180,7 +186,9 @@ __global__ void __launch_bounds__(256) k_gemv_reg(const uint8_t* __restrict__ A,
     const int ldsA = ASM ? kb + 64 : 0;
     uint8_t* As = smem;
     int* red = reinterpret_cast<int*>(smem + TOK * ldsA);
+    __shared__ int smx[TOK];  // per-token max |v| of this CTA's fp32 outputs (float bits, >= 0)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid < TOK) smx[tid] = 0;
     const int g = lane >> 2, tig = lane & 3;
     const int n_rb = (N + 15) / 16;
     const int KT = K / 128;
@@ -214,6 +222,14 @@ __global__ void __launch_bounds__(256) k_gemv_reg(const uint8_t* __restrict__ A,
             for (int c = ch0 + U + (lane >> 3); c < ch1; c += 4)
                 asm volatile("prefetch.global.L2 [%0];\n" ::"l"(W + ((size_t)c * (ldw >> 4) + rb) * 1024 +
                                                                (lane & 7) * 128));
+    }
+    if (pf && warp == 7) {  // the next GEMV's weights: this CTA's 4 KB-aligned slice, 16 KB per bulk prefetch
+        const long long per = ((pf_bytes / gridDim.x) + 4095) & ~4095LL;
+        const long long end = min(pf_bytes, (long long)(blockIdx.x + 1) * per);
+        for (long long o = (long long)blockIdx.x * per + lane * 16384LL; o < end; o += 32 * 16384LL) {
+            const unsigned sz = (unsigned)min(16384LL, end - o);
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(pf + o), "r"(sz) : "memory");
+        }
     }
     pdl_wait();
     if (ASM) {
@@ -290,7 +306,9 @@ __global__ void __launch_bounds__(256) k_gemv_reg(const uint8_t* __restrict__ A,
                         if (n + 1 < N) acc_dbg[(size_t)t * N + n + 1] = s1;
                     }
                     const double a_s = sa[t];
-                    epi_store<EPI>(out, ldo, t, n, (double)s0 * (a_s * sw[n]), (double)s1 * (a_s * sw[n + 1]), N);
+                    const float v = epi_store<EPI>(out, ldo, t, n, (double)s0 * (a_s * sw[n]),
+                                                   (double)s1 * (a_s * sw[n + 1]), N);
+                    if (pmax) atomicMax(&smx[t], __float_as_int(v));
                 }
             }
             __syncthreads();
@@ -303,14 +321,31 @@ __global__ void __launch_bounds__(256) k_gemv_reg(const uint8_t* __restrict__ A,
             wb[u] = nb[u];
         }
     }
+    if (pmax) {  // this CTA's slot of the per-row partial max (every CTA writes its own)
+        __syncthreads();
+        if (tid < M && tid < TOK) pmax[(size_t)tid * pmax_ld + blockIdx.x] = __int_as_float(smx[tid]);
+    }
 }
 
 template <int EPI>
 int launch_gemm(const uint8_t* A, int lda, const double* sa, const uint8_t* W, int ldw, const double* sw, int M,
-                int N, int K, void* out, int ldo, int* acc_dbg, cudaStream_t st) {
+                int N, int K, void* out, int ldo, int* acc_dbg, cudaStream_t st, float* pmax = nullptr,
+                int pmax_ld = 0, int* n_part = nullptr) {
+    if (n_part) *n_part = 0;
     if (M <= 0) return 0;
     if (K % 128 || lda % 16 || ldw % 16 || M > lda || N > ldw) return -1;  // lda/ldw = padded rows
     const int nb = (N + GB_N - 1) / GB_N;
+    const uint8_t* pf = static_cast<const uint8_t*>(g_l2_next);
+    const long long pf_bytes = g_l2_next_bytes;
+    g_l2_next = nullptr;
+    g_l2_next_bytes = 0;
+    float* pm = nullptr;  // GEMV paths: one partial-max slot per CTA
+    auto want_pmax = [&](int ctas) {
+        if (pmax && ctas <= pmax_ld) {
+            pm = pmax;
+            if (n_part) *n_part = ctas;
+        }
+    };
     if (M > 16 && M <= 64 && lda >= ((M + 31) / 32) * 32) {
         // 17..64 tokens: B fragments from global (padded tile rows up to 32 / 64 must exist)
         const int n_rb = (N + 15) / 16;
@@ -318,18 +353,20 @@ int launch_gemm(const uint8_t* A, int lda, const double* sa, const uint8_t* W, i
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
         const dim3 grid(std::min(n_rb, 2 * sms));
         if (M <= 32) {
+            want_pmax((int)grid.x);
             const size_t smem = (size_t)8 * 16 * 32 * 4;
             auto kfn = k_gemv_reg<4, EPI>;
             cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             return launch_pdl(kfn, grid, dim3(256), smem, st, A, lda, sa, W, ldw, sw, M, N, K, out, ldo, acc_dbg,
-                              qt_gemv_l2_rows_host);
+                              qt_gemv_l2_rows_host, pf, pf_bytes, pm, pmax_ld);
         }
         if (lda >= 64) {
+            want_pmax((int)grid.x);
             const size_t smem = (size_t)8 * 16 * 64 * 4;
             auto kfn = k_gemv_reg<8, EPI>;
             cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             return launch_pdl(kfn, grid, dim3(256), smem, st, A, lda, sa, W, ldw, sw, M, N, K, out, ldo, acc_dbg,
-                              qt_gemv_l2_rows_host);
+                              qt_gemv_l2_rows_host, pf, pf_bytes, pm, pmax_ld);
         }
     }
     if (M <= 16) {
@@ -339,17 +376,18 @@ int launch_gemm(const uint8_t* A, int lda, const double* sa, const uint8_t* W, i
         const int n_rb = (N + 15) / 16;
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-        const dim3 grid(std::min(n_rb, 2 * sms));
+        const dim3 grid(std::min(n_rb, qt_gemv_ctas * sms));
+        want_pmax((int)grid.x);
         if (TOK == 8) {
             auto kfn = k_gemv_reg<1, EPI>;
             cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             return launch_pdl(kfn, grid, dim3(256), smem, st, A, lda, sa, W, ldw, sw, M, N, K, out, ldo, acc_dbg,
-                              qt_gemv_l2_rows_host);
+                              qt_gemv_l2_rows_host, pf, pf_bytes, pm, pmax_ld);
         }
         auto kfn = k_gemv_reg<2, EPI>;
         cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         return launch_pdl(kfn, grid, dim3(256), smem, st, A, lda, sa, W, ldw, sw, M, N, K, out, ldo, acc_dbg,
-                              qt_gemv_l2_rows_host);
+                              qt_gemv_l2_rows_host, pf, pf_bytes, pm, pmax_ld);
     }
     if (M <= 512 || (long long)((M + 127) / 128) * nb < 148) {
         constexpr int BM = 64;
@@ -368,6 +406,29 @@ int launch_gemm(const uint8_t* A, int lda, const double* sa, const uint8_t* W, i
 }
 
 }  // namespace qt
+
+// pmax (may be null): per-row partial max |v| of the fp32 outputs, pmax[m * pmax_ld + p],
+// p < *n_part (one slot per GEMV CTA); *n_part = 0 when this launch produced none.
+extern "C" int qt_launch_w4a4_mma_ex(int epi, const uint8_t* A, int lda, const double* sa, const uint8_t* W,
+                                     int ldw, const double* sw, int M, int N, int K, void* out, int ldo,
+                                     int* acc_dbg, float* pmax, int pmax_ld, int* n_part, cudaStream_t st) {
+    using namespace qt;
+    switch (epi) {
+        case QT_EPI_STORE:
+            return launch_gemm<QT_EPI_STORE>(A, lda, sa, W, ldw, sw, M, N, K, out, ldo, acc_dbg, st, pmax, pmax_ld,
+                                             n_part);
+        case QT_EPI_RESADD:
+            return launch_gemm<QT_EPI_RESADD>(A, lda, sa, W, ldw, sw, M, N, K, out, ldo, acc_dbg, st, nullptr, 0,
+                                              n_part);
+        case QT_EPI_SILU:
+            return launch_gemm<QT_EPI_SILU>(A, lda, sa, W, ldw, sw, M, N, K, out, ldo, acc_dbg, st, pmax, pmax_ld,
+                                            n_part);
+        case QT_EPI_SWIGLU:
+            return launch_gemm<QT_EPI_SWIGLU>(A, lda, sa, W, ldw, sw, M, N, K, out, ldo, acc_dbg, st, pmax, pmax_ld,
+                                              n_part);
+    }
+    return -1;
+}
 
 extern "C" int qt_launch_w4a4_mma(int epi, const uint8_t* A, int lda, const double* sa, const uint8_t* W, int ldw,
                                   const double* sw, int M, int N, int K, void* out, int ldo, int* acc_dbg,

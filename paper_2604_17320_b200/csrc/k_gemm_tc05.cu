@@ -139,7 +139,8 @@ __global__ void __launch_bounds__(T5_THREADS, 1) k_gemm_tc05(const uint8_t* __re
                                                               const double* __restrict__ sw, int M, int N, int K,
                                                               void* __restrict__ out, int ldo,
                                                               int* __restrict__ acc_dbg, int ksplit,
-                                                              int* __restrict__ ws) {
+                                                              int* __restrict__ ws, float* __restrict__ pmax,
+                                                              int pmax_ld) {
     extern __shared__ __align__(1024) uint8_t smem[];
     uint64_t* pfull = reinterpret_cast<uint64_t*>(smem + T5Smem::bars);
     uint64_t* pempty = pfull + T5_PS;
@@ -315,6 +316,7 @@ __global__ void __launch_bounds__(T5_THREADS, 1) k_gemm_tc05(const uint8_t* __re
             const int m = m0 + q * 32 + lane;
             const double a_s = m < M ? sa[m] : 0.0;
             const uint32_t tacc = tmem + (uint32_t)(acc * T5_BN) + ((uint32_t)(q * 32) << 16);
+            float mx = 0.f;  // max |v| over this thread's (row, column half) of the tile
 #pragma unroll 1
             for (int j = jh; j < jh + T5_BN / 64; ++j) {
                 uint32_t r[32];
@@ -340,15 +342,19 @@ __global__ void __launch_bounds__(T5_THREADS, 1) k_gemm_tc05(const uint8_t* __re
                         if (nb + e < N) acc_dbg[(size_t)m * N + nb + e] = (int)r[e] >> 8;
                 }
                 if (nb + 32 <= N) {
-                    epi_row32<EPI>(out, ldo, m, nb, r, a_s, swt + j * 32);
+                    epi_row32<EPI>(out, ldo, m, nb, r, a_s, swt + j * 32, mx);
                 } else {
 #pragma unroll
                     for (int e = 0; e < 32; e += 2)
                         if (nb + e < N)
-                            epi_store<EPI>(out, ldo, m, nb + e, (double)((int)r[e] >> 8) * (a_s * swt[j * 32 + e]),
-                                           (double)((int)r[e + 1] >> 8) * (a_s * swt[j * 32 + e + 1]), N);
+                            mx = fmaxf(mx, epi_store<EPI>(out, ldo, m, nb + e,
+                                                          (double)((int)r[e] >> 8) * (a_s * swt[j * 32 + e]),
+                                                          (double)((int)r[e + 1] >> 8) * (a_s * swt[j * 32 + e + 1]),
+                                                          N));
                 }
             }
+            // partial row max for the next site's dynamic quantizer: slot (n tile, column half)
+            if (pmax && ksplit == 1 && m < M) pmax[(size_t)m * pmax_ld + (t / mt_n) * 2 + jh / (T5_BN / 64)] = mx;
             asm volatile("bar.sync 2, %0;\n" ::"n"(T5_ET) : "memory");  // swt reuse
         }
     }
@@ -401,7 +407,17 @@ extern "C" int qt_tc05_splitk(int M, int N, int K) {
 extern "C" int qt_launch_w4a4_tc05(int epi, const uint8_t* A, int lda, const double* sa, const uint8_t* W, int ldw,
                                    const double* sw, int M, int N, int K, void* out, int ldo, int* acc_dbg,
                                    int* ws, cudaStream_t st) {
+    return qt_launch_w4a4_tc05_ex(epi, A, lda, sa, W, ldw, sw, M, N, K, out, ldo, acc_dbg, ws, nullptr, 0, nullptr, st);
+}
+
+// pmax (may be null): per-row partial max |v| of the fp32 outputs, pmax[m * pmax_ld + p],
+// p < *n_part = 2 x N tiles; *n_part = 0 when this launch produced none (split-K path).
+extern "C" int qt_launch_w4a4_tc05_ex(int epi, const uint8_t* A, int lda, const double* sa, const uint8_t* W,
+                                      int ldw, const double* sw, int M, int N, int K, void* out, int ldo,
+                                      int* acc_dbg, int* ws, float* pmax, int pmax_ld, int* n_part,
+                                      cudaStream_t st) {
     using namespace qt;
+    if (n_part) *n_part = 0;
     if (M <= 0) return 0;
     if (K % 128 || lda % 16 || ldw % 16 || M > lda || N > ldw) return -1;  // lda/ldw = padded rows
     int sms = 148;
@@ -409,13 +425,16 @@ extern "C" int qt_launch_w4a4_tc05(int epi, const uint8_t* A, int lda, const dou
     const int tiles = ((N + T5_BN - 1) / T5_BN) * ((M + T5_BM - 1) / T5_BM);
     const int ksplit = ws ? qt_tc05_splitk(M, N, K) : 1;
     const dim3 grid(std::min(tiles * ksplit, sms));
+    const int parts = 2 * ((N + T5_BN - 1) / T5_BN);
+    if (pmax && (ksplit > 1 || parts > pmax_ld)) pmax = nullptr;
+    if (pmax && n_part) *n_part = parts;
     const size_t smem = T5Smem::total;
 #define QT_T5(E)                                                                                                \
     do {                                                                                                        \
         auto kfn = k_gemm_tc05<E>;                                                                              \
         cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                      \
         int rc = launch_pdl(kfn, grid, dim3(T5_THREADS), smem, st, A, lda, sa, W, ldw, sw, M, N, K, out, ldo,   \
-                            ksplit > 1 ? nullptr : acc_dbg, ksplit, ws);                                         \
+                            ksplit > 1 ? nullptr : acc_dbg, ksplit, ws, pmax, pmax_ld);                          \
         if (rc || ksplit == 1) return rc;                                                                       \
         const long long pairs = ((long long)M * N + 1) / 2;                                                     \
         return launch_pdl(k_splitk_epilogue<E>, dim3((unsigned)((pairs + 255) / 256)), dim3(256), 0, st,      \

@@ -118,6 +118,40 @@ __global__ void __launch_bounds__(1024) k_norm_quant(const TX* __restrict__ x, i
     if (threadIdx.x == 0) scales[row] = s;
 }
 
+// K1 without a row reduction: the row max |x| of an fp32 site input (mlp_mid) arrives
+// as the producing GEMM epilogue's partial maxima (pmax[m][p], p < n_part; max is
+// exact, so the scale is the one a full reduction gives).  One thread per 8-element
+// word, grid (words / 256, M); every warp folds the row's partials itself, so no
+// block barrier sits between the loads and the stores.
+__global__ void __launch_bounds__(256) k_quant_pmax(const float* __restrict__ x, int ld_x,
+                                                    const float* __restrict__ pmax, int n_part, int pmax_ld, int M,
+                                                    int D, int d_pad, int qmax, int mode, double static_scale,
+                                                    uint8_t* __restrict__ codes, int ld_codes,
+                                                    double* __restrict__ scales) {
+    pdl_launch_dependents();
+    pdl_wait();  // x and the partials come from the previous kernel
+    const int row = blockIdx.y, lane = threadIdx.x & 31;
+    const int w = blockIdx.x * blockDim.x + threadIdx.x;
+    if (row >= M) return;
+    double v[8];
+    const bool in = w * 8 < D;
+    if (in) load8<float>(x + (size_t)row * ld_x + w * 8, v);
+    double s = static_scale;
+    if (mode != 0) {
+        float mx = 0.f;
+        for (int p = lane; p < n_part; p += 32) mx = fmaxf(mx, pmax[(size_t)row * pmax_ld + p]);
+        mx = warp_max(mx);
+        s = q_scale((double)mx, qmax);
+    }
+    if (w * 8 >= d_pad) return;
+    const double inv_s = 1.0 / s;
+    int c[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) c[e] = in ? q_code_r(v[e], s, inv_s, qmax) : 0;
+    *reinterpret_cast<uint32_t*>(codes + w4t_offset(row, w * 4, ld_codes)) = pack8(c);
+    if (w == 0) scales[row] = s;
+}
+
 // K1 for few rows (decode): a cluster of CL CTAs per row, each owning a slice
 // of 8-element words in registers; the RMS sum and the row max are reduced
 // across the cluster through distributed shared memory in rank order (fixed,
@@ -452,6 +486,16 @@ int qt_launch_norm_quant(const void* x, int x_is_f64, int ld_x, const float* gai
         QT_NQ(float, 3);
     }
 #undef QT_NQ
+}
+
+int qt_launch_quant_pmax(const float* x, int ld_x, const float* pmax, int n_part, int pmax_ld, int M, int D,
+                         int d_pad, int qmax, int mode, double static_scale, uint8_t* codes, int ld_codes,
+                         double* scales, cudaStream_t st) {
+    if (M <= 0) return 0;
+    if (D % 8 || d_pad % 8 || (mode != 0 && n_part < 1)) return -1;
+    const int words = d_pad / 8;
+    return launch_pdl(k_quant_pmax, dim3((words + 255) / 256, M), dim3(256), 0, st, x, ld_x, pmax, n_part, pmax_ld,
+                      M, D, d_pad, qmax, mode, static_scale, codes, ld_codes, scales);
 }
 
 int qt_launch_rope_kv_append(float* qkv, int ld_qkv, int M, int H, int Hkv, int dh, const int* pos,

@@ -228,6 +228,12 @@ namespace qt {
 // next launch then takes a full stream dependency instead of a programmatic
 // (PDL) one, so it cannot start before the copy has landed.
 inline thread_local bool g_pdl_block = false;
+// Weights of the NEXT weight-streaming GEMV on the stream: the decode GEMV launched next
+// pulls them toward L2 (cp.async.bulk.prefetch) while it streams its own, so HBM keeps
+// streaming through the latency-bound attention / quantizer kernels in between.  Set by
+// the engine right before the launch; consumed (cleared) by the GEMV launcher.
+inline thread_local const void* g_l2_next = nullptr;
+inline thread_local long long g_l2_next_bytes = 0;
 
 template <typename... KArgs, typename... Args>
 inline int launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,

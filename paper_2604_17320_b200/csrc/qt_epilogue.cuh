@@ -18,8 +18,10 @@ QT_DEV float silu_f32(double g) {
 // y = (acc / 256) * s_a[m] * s_w[n] in fp64 (scales are the reference's fp64
 // scales; the integer sum is exact), then the epilogue: store fp32, add into
 // the fp64 residual, SiLU, or SwiGLU over interleaved (gate, up) columns.
+// Returns max |v| over the fp32 values written (0 for the residual add): the
+// producer-side partial row max the dynamic quantizer of the next site reads.
 template <int EPI>
-QT_DEV void epi_store(void* __restrict__ outv, int ldo, int m, int n, double y0, double y1, int N) {
+QT_DEV float epi_store(void* __restrict__ outv, int ldo, int m, int n, double y0, double y1, int N) {
     if (EPI == QT_EPI_RESADD) {
         double* p = static_cast<double*>(outv) + (size_t)m * ldo + n;
         if (n + 1 < N) {
@@ -30,15 +32,17 @@ QT_DEV void epi_store(void* __restrict__ outv, int ldo, int m, int n, double y0,
         } else if (n < N) {
             p[0] += y0;
         }
-        return;
+        return 0.f;
     }
     float* out = static_cast<float*>(outv);
     if (EPI == QT_EPI_SWIGLU) {
         // silu(g) * u (model.cpp:170-172 silu; SwiGLU is the R1 extension)
         // fp64 here (decode GEMV / small GEMMs: a handful of rows), so the fp32 result is the
         // correctly rounded value of the reference's fp64 expression
-        if (n < N) out[(size_t)m * ldo + n / 2] = (float)(y0 / (1.0 + exp(-y0)) * y1);
-        return;
+        if (n >= N) return 0.f;
+        const float v = (float)(y0 / (1.0 + exp(-y0)) * y1);
+        out[(size_t)m * ldo + n / 2] = v;
+        return fabsf(v);
     }
     float* p = out + (size_t)m * ldo + n;
     float v0, v1;
@@ -49,14 +53,22 @@ QT_DEV void epi_store(void* __restrict__ outv, int ldo, int m, int n, double y0,
         v0 = (float)y0;
         v1 = (float)y1;
     }
-    if (n + 1 < N) *reinterpret_cast<float2*>(p) = make_float2(v0, v1);
-    else if (n < N) p[0] = v0;
+    if (n + 1 < N) {
+        *reinterpret_cast<float2*>(p) = make_float2(v0, v1);
+        return fmaxf(fabsf(v0), fabsf(v1));
+    }
+    if (n < N) {
+        p[0] = v0;
+        return fabsf(v0);
+    }
+    return 0.f;
 }
 
 // 32 consecutive columns of one row (tcgen05.ld 32x32b: one row per thread).
+// mx: running max |v| of the fp32 values written (untouched by the residual add).
 template <int EPI>
 QT_DEV void epi_row32(void* __restrict__ outv, int ldo, int m, int n, const uint32_t* r, double a_s,
-                      const double* swt) {
+                      const double* swt, float& mx) {
     if (EPI == QT_EPI_RESADD) {
         double2* p = reinterpret_cast<double2*>(static_cast<double*>(outv) + (size_t)m * ldo + n);
 #pragma unroll
@@ -85,6 +97,7 @@ QT_DEV void epi_row32(void* __restrict__ outv, int ldo, int m, int n, const uint
                 const double g = (double)((int)r[e + 2 * u] >> 8) * (a_s * swt[e + 2 * u]);
                 const double up = (double)((int)r[e + 2 * u + 1] >> 8) * (a_s * swt[e + 2 * u + 1]);
                 v[u] = silu_f32(g) * (float)up;
+                mx = fmaxf(mx, fabsf(v[u]));
             }
             p[e / 8] = make_float4(v[0], v[1], v[2], v[3]);
         }
@@ -98,6 +111,7 @@ QT_DEV void epi_row32(void* __restrict__ outv, int ldo, int m, int n, const uint
         for (int u = 0; u < 4; ++u) {
             const double y = (double)((int)r[e + u] >> 8) * (a_s * swt[e + u]);
             v[u] = EPI == QT_EPI_SILU ? silu_f32(y) : (float)y;
+            mx = fmaxf(mx, fabsf(v[u]));
         }
         p[e / 4] = make_float4(v[0], v[1], v[2], v[3]);
     }

@@ -47,6 +47,17 @@ int qt_launch_diag_top10(const float* qkv, int ldq, int H, int Hkv, int dh, int 
 int qt_launch_codes_pack(const int8_t* src, int K, int N, const double* s_in, int row_mul, int row_add,
                          uint8_t* codes, int ldc, double* scales, cudaStream_t st);
 // out: double* for QT_EPI_RESADD (the fp64 residual stream), float* otherwise
+int qt_launch_w4a4_mma_ex(int epi, const uint8_t* A, int lda, const double* sa, const uint8_t* W, int ldw,
+                          const double* sw, int M, int N, int K, void* out, int ldo, int* acc_dbg, float* pmax,
+                          int pmax_ld, int* n_part, cudaStream_t st);
+int qt_launch_w4a4_tc05_ex(int epi, const uint8_t* A, int lda, const double* sa, const uint8_t* W, int ldw,
+                           const double* sw, int M, int N, int K, void* out, int ldo, int* acc_dbg, int* ws,
+                           float* pmax, int pmax_ld, int* n_part, cudaStream_t st);
+// dynamic int4 quantizer of fp32 rows whose max |x| is given as producer partials
+// (pmax[m * pmax_ld + p], p < n_part): no row reduction; mode 0 = static scale
+int qt_launch_quant_pmax(const float* x, int ld_x, const float* pmax, int n_part, int pmax_ld, int M, int D,
+                         int d_pad, int qmax, int mode, double static_scale, uint8_t* codes, int ld_codes,
+                         double* scales, cudaStream_t st);
 int qt_launch_w4a4_mma(int epi, const uint8_t* A, int lda, const double* sa, const uint8_t* W, int ldw,
                        const double* sw, int M, int N, int K, void* out, int ldo, int* acc_dbg, cudaStream_t st);
 // ws (nullable): int32 split-K workspace of qt_tc05_splitk(M, N, K) * M * N entries; with ws the
