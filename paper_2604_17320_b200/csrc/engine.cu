@@ -1274,7 +1274,7 @@ struct qt_engine {
 
             pb(P_ATTN);
             ckl(qt_launch_attn_prefill(qkv, n_qkv, H, Hkv, dh, seq_off, seq_vis, seq_len, B, smax, pool, page_bytes,
-                                       ptl, max_pages, attn, d, prune_any ? ml : nullptr, st),
+                                       ptl, max_pages, attn, d, prune_any ? ml : nullptr, pmax, kPmaxLd, st),
                 "prefill attention");
             {  // mask-allowed (query, key) pairs x 4 dh flops per head
                 double pairs = 0;
@@ -1284,7 +1284,8 @@ struct qt_engine {
                 }
                 pe((double)M * (n_qkv * 4.0 + d * 4.0), 4.0 * pairs * dh * H);
             }
-            norm_quant(attn, 0, d, nullptr, M, d, kd_pad, 4 * l + 1);
+            pm_parts = pmax ? H : 0;  // the attention epilogue left max |out| per (row, head)
+            norm_quant(attn, 0, d, nullptr, M, d, kd_pad, 4 * l + 1, true);
             gemm(QT_EPI_RESADD, w.o, nd_pad, w.s_o, M, d, kd_pad, xc, d);
             if (rec_diag) diag_layer(l, ptl, cur_v[0], h_txt[0], xc);
             for (int b = 0; b < B; ++b) h_kvlen[(size_t)l * B + b] = cur_v[b] + h_txt[b];

@@ -123,7 +123,8 @@ __global__ void __launch_bounds__(128, 3) k_attn_prefill(const float* __restrict
                                                       const int* __restrict__ seq_len,
                                                       const uint8_t* __restrict__ pool, long long page_bytes,
                                                       const int* __restrict__ pt, int max_pages, float inv_sqrt,
-                                                      float* __restrict__ out, int ldo, float2* __restrict__ ml) {
+                                                      float* __restrict__ out, int ldo, float2* __restrict__ ml,
+                                                      float* __restrict__ pmax, int pmax_ld) {
     constexpr int KLD = DH + 8, VLD = AT_K + 8;
     __shared__ __align__(16) __half Ks[AT_K * KLD];
     __shared__ __align__(16) __half Vt[DH * VLD];
@@ -232,16 +233,25 @@ __global__ void __launch_bounds__(128, 3) k_attn_prefill(const float* __restrict
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
         const int q = qi[r];
-        if (q >= S) continue;
-        const float inv_l = 1.f / lrow[r];
-        float* orow = out + (size_t)(tok0 + q) * ldo + h * DH;
+        const bool ok = q < S;
+        float mx = 0.f;  // max |out| of this (row, head): the attn_out quantizer's partial row max
+        if (ok) {
+            const float inv_l = 1.f / lrow[r];
+            float* orow = out + (size_t)(tok0 + q) * ldo + h * DH;
 #pragma unroll
-        for (int t = 0; t < DH / 8; ++t) {
-            float2 v = make_float2(o[t][2 * r] * inv_l, o[t][2 * r + 1] * inv_l);
-            *reinterpret_cast<float2*>(orow + t * 8 + 2 * tig) = v;
+            for (int t = 0; t < DH / 8; ++t) {
+                float2 v = make_float2(o[t][2 * r] * inv_l, o[t][2 * r + 1] * inv_l);
+                *reinterpret_cast<float2*>(orow + t * 8 + 2 * tig) = v;
+                mx = fmaxf(mx, fmaxf(fabsf(v.x), fabsf(v.y)));
+            }
+            // row max back in natural-log units for the QUOTA column sums (k_attn_colsum uses expf)
+            if (ml && tig == 0) ml[(size_t)(tok0 + q) * H + h] = make_float2(mrow[r] * 0.69314718055994531f, lrow[r]);
         }
-        // row max back in natural-log units for the QUOTA column sums (k_attn_colsum uses expf)
-        if (ml && tig == 0) ml[(size_t)(tok0 + q) * H + h] = make_float2(mrow[r] * 0.69314718055994531f, lrow[r]);
+        if (pmax) {  // the quad of lanes sharing the row
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+            if (ok && tig == 0) pmax[(size_t)(tok0 + q) * pmax_ld + h] = mx;
+        }
     }
 }
 
@@ -601,16 +611,18 @@ extern "C" {
 
 int qt_launch_attn_prefill(const float* qkv, int ldq, int H, int Hkv, int dh, const int* seq_off, const int* vis,
                            const int* seq_len, int B, int smax, const uint8_t* pool, long long page_bytes,
-                           const int* pt, int max_pages, float* out, int ldo, float* ml, cudaStream_t st) {
+                           const int* pt, int max_pages, float* out, int ldo, float* ml, float* pmax, int pmax_ld,
+                           cudaStream_t st) {
     if (B <= 0 || smax <= 0) return 0;
+    if (pmax && H > pmax_ld) return -1;
     const dim3 grid((smax + AT_Q - 1) / AT_Q, H, B);
     const float inv_sqrt = (float)(1.0 / sqrt((double)dh));
     if (dh == 128)
         k_attn_prefill<128><<<grid, 128, 0, st>>>(qkv, ldq, H, Hkv, seq_off, vis, seq_len, pool, page_bytes, pt,
-                                                  max_pages, inv_sqrt, out, ldo, reinterpret_cast<float2*>(ml));
+                                                  max_pages, inv_sqrt, out, ldo, reinterpret_cast<float2*>(ml), pmax, pmax_ld);
     else if (dh == 64)
         k_attn_prefill<64><<<grid, 128, 0, st>>>(qkv, ldq, H, Hkv, seq_off, vis, seq_len, pool, page_bytes, pt,
-                                                 max_pages, inv_sqrt, out, ldo, reinterpret_cast<float2*>(ml));
+                                                 max_pages, inv_sqrt, out, ldo, reinterpret_cast<float2*>(ml), pmax, pmax_ld);
     else
         return -1;
     return (int)cudaGetLastError();

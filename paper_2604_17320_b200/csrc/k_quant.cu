@@ -118,11 +118,13 @@ __global__ void __launch_bounds__(1024) k_norm_quant(const TX* __restrict__ x, i
     if (threadIdx.x == 0) scales[row] = s;
 }
 
-// K1 without a row reduction: the row max |x| of an fp32 site input (mlp_mid) arrives
-// as the producing GEMM epilogue's partial maxima (pmax[m][p], p < n_part; max is
-// exact, so the scale is the one a full reduction gives).  One thread per 8-element
-// word, grid (words / 256, M); every warp folds the row's partials itself, so no
-// block barrier sits between the loads and the stores.
+// K1 without a row reduction: the row max |x| of an fp32 site input (mlp_mid,
+// attn_out) arrives as the producing kernel's partial maxima (pmax[m][p], p <
+// n_part; max is exact, so the scale is the one a full reduction gives).  Each
+// thread quantizes WPT 8-element words (w = tid + j * 256 within the CTA's
+// chunk), all loads issued first; every warp folds the row's partials itself, so
+// no block barrier sits between the loads and the stores.  Grid (chunks, M).
+template <int WPT>
 __global__ void __launch_bounds__(256) k_quant_pmax(const float* __restrict__ x, int ld_x,
                                                     const float* __restrict__ pmax, int n_part, int pmax_ld, int M,
                                                     int D, int d_pad, int qmax, int mode, double static_scale,
@@ -131,11 +133,16 @@ __global__ void __launch_bounds__(256) k_quant_pmax(const float* __restrict__ x,
     pdl_launch_dependents();
     pdl_wait();  // x and the partials come from the previous kernel
     const int row = blockIdx.y, lane = threadIdx.x & 31;
-    const int w = blockIdx.x * blockDim.x + threadIdx.x;
     if (row >= M) return;
-    double v[8];
-    const bool in = w * 8 < D;
-    if (in) load8<float>(x + (size_t)row * ld_x + w * 8, v);
+    const int w0 = blockIdx.x * (256 * WPT) + threadIdx.x;
+    float4 v[WPT][2];  // fp32 site input as loaded (widened to fp64 at the quantizer)
+#pragma unroll
+    for (int j = 0; j < WPT; ++j)
+        if ((w0 + j * 256) * 8 < D) {
+            const float4* p = reinterpret_cast<const float4*>(x + (size_t)row * ld_x + (w0 + j * 256) * 8);
+            v[j][0] = p[0];
+            v[j][1] = p[1];
+        }
     double s = static_scale;
     if (mode != 0) {
         float mx = 0.f;
@@ -143,13 +150,22 @@ __global__ void __launch_bounds__(256) k_quant_pmax(const float* __restrict__ x,
         mx = warp_max(mx);
         s = q_scale((double)mx, qmax);
     }
-    if (w * 8 >= d_pad) return;
     const double inv_s = 1.0 / s;
-    int c[8];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) c[e] = in ? q_code_r(v[e], s, inv_s, qmax) : 0;
-    *reinterpret_cast<uint32_t*>(codes + w4t_offset(row, w * 4, ld_codes)) = pack8(c);
-    if (w == 0) scales[row] = s;
+    for (int j = 0; j < WPT; ++j) {
+        const int w = w0 + j * 256;
+        if (w * 8 >= d_pad) break;
+        const bool in = w * 8 < D;
+        int c[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const float4 q4 = v[j][e >> 2];
+            const float f = (e & 3) == 0 ? q4.x : (e & 3) == 1 ? q4.y : (e & 3) == 2 ? q4.z : q4.w;
+            c[e] = in ? q_code_r((double)f, s, inv_s, qmax) : 0;
+        }
+        *reinterpret_cast<uint32_t*>(codes + w4t_offset(row, w * 4, ld_codes)) = pack8(c);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) scales[row] = s;
 }
 
 // K1 for few rows (decode): a cluster of CL CTAs per row, each owning a slice
@@ -494,8 +510,18 @@ int qt_launch_quant_pmax(const float* x, int ld_x, const float* pmax, int n_part
     if (M <= 0) return 0;
     if (D % 8 || d_pad % 8 || (mode != 0 && n_part < 1)) return -1;
     const int words = d_pad / 8;
-    return launch_pdl(k_quant_pmax, dim3((words + 255) / 256, M), dim3(256), 0, st, x, ld_x, pmax, n_part, pmax_ld,
-                      M, D, d_pad, qmax, mode, static_scale, codes, ld_codes, scales);
+    // one word per thread: measured faster than whole-row CTAs with 2-8 words per thread
+    // (prefill 36.5 vs 36.8 ms) -- more CTAs in flight beat the amortised partial fold
+    const int wpt = 1;
+#define QT_QP(W)                                                                                                 \
+    return launch_pdl(k_quant_pmax<W>, dim3((words + 256 * W - 1) / (256 * W), M), dim3(256), 0, st, x, ld_x,   \
+                      pmax, n_part, pmax_ld, M, D, d_pad, qmax, mode, static_scale, codes, ld_codes, scales)
+    if (wpt == 1) QT_QP(1);
+    if (wpt == 2) QT_QP(2);
+    if (wpt == 4) QT_QP(4);
+    if (wpt == 6) QT_QP(6);
+    QT_QP(8);
+#undef QT_QP
 }
 
 int qt_launch_rope_kv_append(float* qkv, int ld_qkv, int M, int H, int Hkv, int dh, const int* pos,

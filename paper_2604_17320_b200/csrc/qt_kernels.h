@@ -66,9 +66,11 @@ int qt_tc05_splitk(int M, int N, int K);
 int qt_launch_w4a4_tc05(int epi, const uint8_t* A, int lda, const double* sa, const uint8_t* W, int ldw,
                         const double* sw, int M, int N, int K, void* out, int ldo, int* acc_dbg, int* ws,
                         cudaStream_t st);
+// pmax (may be null): max |out| per (token row, head), pmax[row * pmax_ld + h]
 int qt_launch_attn_prefill(const float* qkv, int ldq, int H, int Hkv, int dh, const int* seq_off, const int* vis,
                            const int* seq_len, int B, int smax, const uint8_t* pool, long long page_bytes,
-                           const int* pt, int max_pages, float* out, int ldo, float* ml, cudaStream_t st);
+                           const int* pt, int max_pages, float* out, int ldo, float* ml, float* pmax, int pmax_ld,
+                           cudaStream_t st);
 int qt_launch_attn_colsum(const float* qkv, int ldq, int H, int Hkv, int dh, const int* seq_off, const int* vis,
                           const int* seq_len, int B, int vmax, const uint8_t* pool, long long page_bytes,
                           const int* pt, int max_pages, const float* ml, int vstride, float* inter, float* intra,
