@@ -118,6 +118,66 @@ __global__ void __launch_bounds__(1024) k_norm_quant(const TX* __restrict__ x, i
     if (threadIdx.x == 0) scales[row] = s;
 }
 
+// K1 for decode-sized batches: the k_norm_quant arithmetic with 4 elements per
+// thread (up to 1024 threads per row): half the serial instructions per warp and
+// twice the warps per SM, for a kernel whose time is its own latency chain.
+template <typename TX>
+__global__ void __launch_bounds__(1024) k_norm_quant4(const TX* __restrict__ x, int ld_x,
+                                                      const float* __restrict__ gain, int M, int D, int d_pad,
+                                                      int qmax, int mode, double static_scale,
+                                                      uint8_t* __restrict__ codes, int ld_codes,
+                                                      double* __restrict__ scales) {
+    __shared__ double red[32];
+    pdl_launch_dependents();
+    pdl_wait();  // x is produced by the previous kernel
+    const int row = blockIdx.x;
+    if (row >= M) return;
+    const int base = threadIdx.x * 4;
+    const bool in = base < D;
+    double v[4] = {0.0, 0.0, 0.0, 0.0};
+    if (in) {
+        const TX* xr = x + (size_t)row * ld_x + base;
+        if constexpr (sizeof(TX) == 8) {
+            const double2 a = reinterpret_cast<const double2*>(xr)[0], b = reinterpret_cast<const double2*>(xr)[1];
+            v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+        } else {
+            const float4 a = *reinterpret_cast<const float4*>(xr);
+            v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+        }
+    }
+    if (gain) {
+        double ss = 0.0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) ss += v[e] * v[e];
+        ss = block_sum(ss, red);
+        const double inv = 1.0 / sqrt(ss / (double)D + kNormEps);
+        if (in) {
+            const float4 g = *reinterpret_cast<const float4*>(gain + base);
+            const float gg[4] = {g.x, g.y, g.z, g.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) v[e] = __dmul_rn(__dmul_rn(v[e], inv), (double)gg[e]);
+        }
+    }
+    double s;
+    if (mode == 0) {
+        s = static_scale;
+    } else {
+        double mx = 0.0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) mx = fmax(mx, fabs(v[e]));
+        mx = block_max(mx, red);
+        s = q_scale(mx, qmax);
+    }
+    if (base < d_pad) {
+        const double inv_s = 1.0 / s;
+        uint32_t w = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) w |= (uint32_t)((in ? q_code_r(v[e], s, inv_s, qmax) : 0) & 0xF) << (4 * e);
+        *reinterpret_cast<uint16_t*>(codes + w4t_offset(row, base / 2, ld_codes)) = (uint16_t)w;
+    }
+    if (threadIdx.x == 0) scales[row] = s;
+}
+
 // K1 without a row reduction: the row max |x| of an fp32 site input (mlp_mid,
 // attn_out) arrives as the producing kernel's partial maxima (pmax[m][p], p <
 // n_part; max is exact, so the scale is the one a full reduction gives).  Each
@@ -484,6 +544,15 @@ int qt_launch_norm_quant(const void* x, int x_is_f64, int ld_x, const float* gai
                                                    static_scale, codes, ld_codes, scales, st)
                       : launch_nq_cl<float, 8, 2>(static_cast<const float*>(x), ld_x, gain, M, D, d_pad, qmax, mode,
                                                    static_scale, codes, ld_codes, scales, st);
+    }
+    static const bool nq4 = !(getenv("QT_NQ4") && atoi(getenv("QT_NQ4")) == 0);
+    if (nq4 && M <= 64 && !normed && d_pad / 4 <= 1024 && d_pad / 4 >= 128) {
+        const int th = (d_pad / 4 + 31) / 32 * 32;
+        if (x_is_f64)
+            return launch_pdl(k_norm_quant4<double>, dim3(M), dim3(th), 0, st, static_cast<const double*>(x), ld_x,
+                              gain, M, D, d_pad, qmax, mode, static_scale, codes, ld_codes, scales);
+        return launch_pdl(k_norm_quant4<float>, dim3(M), dim3(th), 0, st, static_cast<const float*>(x), ld_x, gain,
+                          M, D, d_pad, qmax, mode, static_scale, codes, ld_codes, scales);
     }
     const int words = d_pad / 8;
     int threads = words <= 256 ? 256 : (words <= 512 ? 512 : 1024);
