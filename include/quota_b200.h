@@ -194,6 +194,12 @@ int qt_engine_info(qt_engine* e, int64_t* out16);
  * CUDA-event time (ms), launches, algorithmic bytes and flops -> out[6*4]. */
 int qt_engine_profile_next(qt_engine* e);
 int qt_engine_profile_read(qt_engine* e, double* out24);
+/* Device time (ms) of one decode step of the current cache restricted to some
+ * kernel classes -- skip_mask bits 1 GEMM, 2 attention, 4 quantizers, 8 KV
+ * append -- captured as a CUDA graph and replayed reps times back to back
+ * (launch overheads and PDL overlap as in the real step).  Cache lengths and
+ * positions are restored, so decoding continues unaffected. */
+int qt_engine_profile_chain(qt_engine* e, int skip_mask, int reps, double* ms_per_step);
 
 /* ---- per-kernel ABI (caller-owned device buffers, explicit stream) ----
  * int4 code matrices (weights and activations) use the tiled layout of

@@ -90,6 +90,7 @@ def lib():
         L.qt_engine_keep_fp_weights.argtypes = [vp, C.c_int]
         L.qt_engine_fit_act_scales.argtypes = [vp, C.c_int, C.POINTER(dp), ip, ip, dp, C.c_int]
         L.qt_engine_fit_act_scales_hooked.argtypes = [vp, C.c_int, C.POINTER(dp), ip, ip, dp, C.c_int]
+        L.qt_engine_profile_chain.argtypes = [vp, C.c_int, C.c_int, dp]
         L.qt_engine_prefill_fp.argtypes = [vp, C.c_int, C.POINTER(dp), ip, ip, C.c_int, dp, C.c_int64]
         L.qt_engine_profile_sensitivity.argtypes = [vp, C.c_int, C.POINTER(dp), ip, ip, C.c_int, ip, C.c_double,
                                                     dp, dp]
@@ -362,6 +363,13 @@ class Engine:
         return f, m
 
     PROFILE_CLASSES = ("gemm", "attention", "quant", "kv", "select", "other")
+
+    def profile_chain(self, skip_mask, reps=20):
+        """ms per decode step with the kernel classes in skip_mask left out (1 GEMM, 2 attention,
+        4 quantizers, 8 KV append), graph-replayed; the cache state is restored."""
+        ms = C.c_double()
+        check(lib().qt_engine_profile_chain(self.h, int(skip_mask), int(reps), C.byref(ms)))
+        return ms.value
 
     def profile_next(self):
         """Time every kernel of the next prefill/decode call with CUDA events."""

@@ -1432,15 +1432,16 @@ struct qt_engine {
         qt::g_l2_next = w;
         qt::g_l2_next_bytes = (long long)bytes;
     }
+    int skip_mask = g_skip;  // kernel classes left out of decode_body (1 GEMM, 2 attention, 4 quant, 8 kv)
     void decode_body() {
         double* xcur = xd;  // the step's input was written (widened) into xd before the graph
         for (int l = 0; l < L; ++l) {
             const LayerW& w = lw[l];
             int* ptl = pt + (size_t)l * max_batch * max_pages;
             int* lenl = kv_len + (size_t)l * max_batch;
-            if (!(g_skip & 4)) norm_quant(xcur, 1, d, w.g1, B, d, kd_pad, 4 * l + 0);
+            if (!(skip_mask & 4)) norm_quant(xcur, 1, d, w.g1, B, d, kd_pad, 4 * l + 0);
             l2_next(w.o, (size_t)nd_pad * kd_pad / 2);
-            if (!(g_skip & 1)) gemm(QT_EPI_STORE, w.qkv, n_qkv_pad, w.s_qkv, B, n_qkv, kd_pad, qkv, n_qkv);
+            if (!(skip_mask & 1)) gemm(QT_EPI_STORE, w.qkv, n_qkv_pad, w.s_qkv, B, n_qkv, kd_pad, qkv, n_qkv);
             if (fused_attn) {
                 // RoPE + K/V append + attention + attn_out quantizer in one kernel
                 pb(P_ATTN);
@@ -1454,7 +1455,7 @@ struct qt_engine {
             } else {
                 if (!rope_fused) {
                     pb(P_KV);
-                    if (!(g_skip & 8)) ckl(qt_launch_rope_kv_append(qkv, n_qkv, B, H, Hkv, dh, next_pos, dec_seq, lenl, rope, ptl, max_pages,
+                    if (!(skip_mask & 8)) ckl(qt_launch_rope_kv_append(qkv, n_qkv, B, H, Hkv, dh, next_pos, dec_seq, lenl, rope, ptl, max_pages,
                                                  pool, page_bytes, 4, nullptr, st),
                         "decode kv append");
                     pe((double)B * n_qkv * 8 + (double)B * Hkv * 2 * (dh / 2 + 4));
@@ -1462,7 +1463,7 @@ struct qt_engine {
                 pb(P_ATTN);
                 // decode attention over int4 pages (RoPE + K/V append fused in) + split merge fused
                 // with the attn_out quantizer
-                if (!(g_skip & 2))
+                if (!(skip_mask & 2))
                     ckl(qt_launch_attn_decode(qkv, n_qkv, H, Hkv, dh, lenl, 1, B, pool, page_bytes, ptl, max_pages,
                                               dec_splits, part_ml, part_o, nullptr, d, codes, codes_rows, ascale,
                                               cfg.act_mode, cfg.act_mode == 0 ? act[4 * l + 1] : 0.0, kd_pad, 4,
@@ -1475,15 +1476,15 @@ struct qt_engine {
                 }
             }
             l2_next(w.gu, (size_t)n_gu_pad * kd_pad / 2);
-            if (!(g_skip & 1)) gemm(QT_EPI_RESADD, w.o, nd_pad, w.s_o, B, d, kd_pad, xcur, d);
-            if (!(g_skip & 4)) norm_quant(xcur, 1, d, w.g2, B, d, kd_pad, 4 * l + 2);
+            if (!(skip_mask & 1)) gemm(QT_EPI_RESADD, w.o, nd_pad, w.s_o, B, d, kd_pad, xcur, d);
+            if (!(skip_mask & 4)) norm_quant(xcur, 1, d, w.g2, B, d, kd_pad, 4 * l + 2);
             l2_next(w.down, (size_t)nd_pad * kff_pad / 2);
-            if (g_skip & 1) {} else if (cfg.mlp == 1) gemm(QT_EPI_SWIGLU, w.gu, n_gu_pad, w.s_gu, B, n_gu, kd_pad, mid, dff, true);
+            if (skip_mask & 1) {} else if (cfg.mlp == 1) gemm(QT_EPI_SWIGLU, w.gu, n_gu_pad, w.s_gu, B, n_gu, kd_pad, mid, dff, true);
             else gemm(QT_EPI_SILU, w.gu, n_gu_pad, w.s_gu, B, n_gu, kd_pad, mid, dff, true);
-            if (!(g_skip & 4)) norm_quant(mid, 0, dff, nullptr, B, dff, kff_pad, 4 * l + 3, true);
+            if (!(skip_mask & 4)) norm_quant(mid, 0, dff, nullptr, B, dff, kff_pad, 4 * l + 3, true);
             if (l + 1 < L) l2_next(lw[l + 1].qkv, (size_t)n_qkv_pad * kd_pad / 2);
             else l2_next(head, (size_t)nd_pad * kd_pad / 2);
-            if (!(g_skip & 1)) gemm(QT_EPI_RESADD, w.down, nd_pad, w.s_down, B, d, kff_pad, xcur, d);
+            if (!(skip_mask & 1)) gemm(QT_EPI_RESADD, w.down, nd_pad, w.s_down, B, d, kff_pad, xcur, d);
         }
         norm_quant(xcur, 1, d, gf, B, d, kd_pad, 4 * L);
         gemm(QT_EPI_STORE, head, nd_pad, s_head, B, d, kd_pad, dlogits, d);
@@ -1495,6 +1496,67 @@ struct qt_engine {
         prof->read(prof_out);
         prof.reset();
         prof_next = false;
+    }
+
+    // Device time of one decode step restricted to some kernel classes (skip: the classes to
+    // leave out), as a CUDA graph replayed reps times back to back on the engine stream --
+    // the per-class cost inside a graph with PDL, which per-launch events cannot see.  The
+    // cache lengths and positions the step bumps are restored afterwards.
+    double profile_chain(int skip, int reps) {
+        if (!prefilled) fail(QT_ERUNTIME, "cache and execution mode mismatch");
+        if (reps < 1) fail(QT_EINVAL, "reps must be >= 1");
+        const size_t nkv = (size_t)L * max_batch;
+        int* save = dalloc<int>(nkv + max_batch);
+        ck(cudaMemcpyAsync(save, kv_len, nkv * sizeof(int), cudaMemcpyDeviceToDevice, st), "save");
+        ck(cudaMemcpyAsync(save + nkv, next_pos, max_batch * sizeof(int), cudaMemcpyDeviceToDevice, st), "save");
+        qt::g_pdl_block = true;
+        const int old = skip_mask;
+        skip_mask = skip;
+        cudaGraph_t g = nullptr;
+        cudaGraphExec_t ge = nullptr;
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        float ms = 0.f;
+        auto cleanup = [&]() {
+            skip_mask = old;
+            if (ge) cudaGraphExecDestroy(ge);
+            if (g) cudaGraphDestroy(g);
+            if (e0) cudaEventDestroy(e0);
+            if (e1) cudaEventDestroy(e1);
+        };
+        try {
+            ck(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "graph capture");
+            g_capturing = true;
+            try {
+                decode_body();
+            } catch (...) {
+                g_capturing = false;
+                cudaStreamEndCapture(st, &g);
+                throw;
+            }
+            g_capturing = false;
+            ck(cudaStreamEndCapture(st, &g), "graph capture end");
+            ck(cudaGraphInstantiate(&ge, g, 0), "graph instantiate");
+            ck(cudaEventCreate(&e0), "event");
+            ck(cudaEventCreate(&e1), "event");
+            ck(cudaGraphLaunch(ge, st), "graph launch");  // warm
+            ck(cudaEventRecord(e0, st), "event");
+            for (int r = 0; r < reps; ++r) ck(cudaGraphLaunch(ge, st), "graph launch");
+            ck(cudaEventRecord(e1, st), "event");
+            ck(cudaEventSynchronize(e1), "event");
+            ck(cudaEventElapsedTime(&ms, e0, e1), "event");
+            ck(cudaMemcpyAsync(kv_len, save, nkv * sizeof(int), cudaMemcpyDeviceToDevice, st), "restore");
+            ck(cudaMemcpyAsync(next_pos, save + nkv, max_batch * sizeof(int), cudaMemcpyDeviceToDevice, st),
+               "restore");
+            ck(cudaStreamSynchronize(st), "restore");
+        } catch (...) {
+            cleanup();
+            cudaFree(save);
+            throw;
+        }
+        cleanup();
+        cudaFree(save);
+        qt::g_pdl_block = true;
+        return (double)ms / reps;
     }
 
     void decode(const void* emb, int emb_dev, int emb_f64, float* out, int out_dev) {
@@ -2102,6 +2164,13 @@ int qt_engine_kv(qt_engine* e, int layer, int seq, int kv_head, int which, int8_
                 scales[r] = sc[(which ? e->Hkv * qt::kPage : 0) + kv_head * qt::kPage + slot];
             }
         }
+    });
+}
+
+int qt_engine_profile_chain(qt_engine* e, int skip_mask, int reps, double* ms_per_step) {
+    return guard([&] {
+        if (!ms_per_step) fail(QT_EINVAL, "null argument");
+        *ms_per_step = e->profile_chain(skip_mask, reps);
     });
 }
 
