@@ -302,6 +302,10 @@ struct qt_engine {
     std::vector<FpLayer> fpw;
     double* fp_head = nullptr;
     cublasHandle_t blas = nullptr;
+    // decode attention: merge + attn_out quantizer by the last page / head arrivals (k_attn.cu)
+    const bool attn_last = std::getenv("QT_ATTN_LAST") && std::atoi(std::getenv("QT_ATTN_LAST")) == 1;  // opt-in: slower
+    unsigned* dec_cnt = nullptr;
+    float* dec_hmax = nullptr;
     // per-row partial max |x| of the mlp_mid site left by the gate|up GEMM epilogue (act_mode 1)
     static constexpr int kPmaxLd = 512;
     const bool use_pmax = !(std::getenv("QT_PMAX") && std::atoi(std::getenv("QT_PMAX")) == 0);
@@ -338,7 +342,7 @@ struct qt_engine {
             for (double* p : fl.w) f(p);
         f(fp_head);
         if (blas) cublasDestroy(blas);
-        f(splitk_ws); f(pmax); f(seq_cnt); f(mk_trace); f(mk_layers); f(mk_acc); f(mk_codes); f(mk_sa); f(mk_attn); f(mk_sync); f(mk_act);
+        f(splitk_ws); f(pmax); f(dec_cnt); f(dec_hmax); f(seq_cnt); f(mk_trace); f(mk_layers); f(mk_acc); f(mk_codes); f(mk_sa); f(mk_attn); f(mk_sync); f(mk_act);
         if (pin) cudaFreeHost(pin);
         if (own_stream) cudaStreamDestroy(own_stream);
     }
@@ -473,6 +477,8 @@ struct qt_engine {
         part_ml = dalloc<float>((size_t)mb * H * dec_splits * 2);
         part_o = dalloc<float>((size_t)mb * H * dec_splits * dh);
         seq_cnt = dalloc<unsigned>(mb);
+        dec_cnt = dalloc<unsigned>((size_t)mb * H + mb);
+        dec_hmax = dalloc<float>((size_t)mb * H);
         {  // split-K workspace: the largest ksplit * M * N over the GEMM shapes that split
             const int shapes[5][2] = {{n_qkv, kd_pad}, {d, kd_pad}, {n_gu, kd_pad}, {d, kff_pad}, {d, kd_pad}};
             size_t need = 0;
@@ -1467,7 +1473,8 @@ struct qt_engine {
                     ckl(qt_launch_attn_decode(qkv, n_qkv, H, Hkv, dh, lenl, 1, B, pool, page_bytes, ptl, max_pages,
                                               dec_splits, part_ml, part_o, nullptr, d, codes, codes_rows, ascale,
                                               cfg.act_mode, cfg.act_mode == 0 ? act[4 * l + 1] : 0.0, kd_pad, 4,
-                                              rope_fused ? rope : nullptr, rope_fused ? next_pos : nullptr, st),
+                                              rope_fused ? rope : nullptr, rope_fused ? next_pos : nullptr,
+                                              attn_last ? dec_cnt : nullptr, attn, dec_hmax, st),
                         "decode attention");
                 {  // decode attention streams every cached K/V row of this layer once
                     double rows = 0;

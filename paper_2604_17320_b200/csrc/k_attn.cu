@@ -338,6 +338,90 @@ __global__ void __launch_bounds__(128) k_attn_colsum(const float* __restrict__ q
     }
 }
 
+// ============================================================== K6 merge by the last arrival
+// Called by every page CTA of (b, h) after its partial is written (128 threads).
+// The last CTA to arrive for (b, h) merges the head's page partials in fixed page
+// order -- the same arithmetic as k_attn_merge_quant -- into the fp32 attention
+// row and the head's max |o|; the last head of sequence b to finish then
+// quantizes the whole row for the attn_out site.  Both arrival counters
+// (cnt[b*H + h], cnt[B*H + b]) are reset by their last arrival, so the kernel
+// replays from a CUDA graph.  Replaces the separate merge launch.
+template <int DH>
+QT_DEV void attn_dec_arrive(int b, int h, int H, int npg, const float* part_ml, const float* part_o, unsigned* cnt,
+                            float* row, float* hmax, uint8_t* codes, int ld_codes, double* scales, int qmode,
+                            double static_scale, int d_pad, int qmax) {
+    __shared__ unsigned s_last;
+    __shared__ float s_red[4];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int B = gridDim.z;
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = atomicAdd(&cnt[b * H + h], 1u) == (unsigned)npg - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (tid == 0) cnt[b * H + h] = 0;
+    const size_t base = ((size_t)b * H + h) * npg;
+    float M = -1e30f;
+    for (int p = lane; p < npg; p += 32) M = fmaxf(M, part_ml[(base + p) * 2]);
+    M = warp_max(M);
+    float L = 0.f, o = 0.f;
+    for (int p0 = 0; p0 < npg; p0 += 4) {  // 4 pages' loads in flight, summed in page order
+        float2 ml4[4];
+        float ov[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int p = p0 + j;
+            ml4[j] = p < npg ? *reinterpret_cast<const float2*>(part_ml + (base + p) * 2) : make_float2(-1e30f, 0.f);
+            ov[j] = p < npg && tid < DH ? part_o[(base + p) * DH + tid] : 0.f;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (ml4[j].y == 0.f) continue;
+            const float a = expf(ml4[j].x - M);
+            L += ml4[j].y * a;
+            o += ov[j] * a;
+        }
+    }
+    o *= 1.f / L;
+    const int HD = H * DH;
+    if (tid < DH) row[(size_t)b * HD + h * DH + tid] = o;
+    float mx = tid < DH ? fabsf(o) : 0.f;
+    mx = warp_max(mx);
+    if (lane == 0) s_red[warp] = mx;
+    __syncthreads();
+    if (tid == 0) hmax[b * H + h] = fmaxf(fmaxf(s_red[0], s_red[1]), fmaxf(s_red[2], s_red[3]));
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = atomicAdd(&cnt[B * H + b], 1u) == (unsigned)H - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (tid == 0) cnt[B * H + b] = 0;
+    double s = static_scale;
+    if (qmode != 0) {
+        float m2 = 0.f;
+        for (int i = lane; i < H; i += 32) m2 = fmaxf(m2, hmax[b * H + i]);
+        s = q_scale((double)warp_max(m2), qmax);
+    }
+    const double inv_s = 1.0 / s;
+    for (int w = tid; w < d_pad / 8; w += blockDim.x) {
+        int c[8];
+        if (w * 8 < HD) {
+            const float4 a = *reinterpret_cast<const float4*>(row + (size_t)b * HD + w * 8);
+            const float4 bq = *reinterpret_cast<const float4*>(row + (size_t)b * HD + w * 8 + 4);
+            const float f[8] = {a.x, a.y, a.z, a.w, bq.x, bq.y, bq.z, bq.w};
+#pragma unroll
+            for (int e = 0; e < 8; ++e) c[e] = q_code_r((double)f[e], s, inv_s, qmax);
+        } else {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) c[e] = 0;
+        }
+        *reinterpret_cast<uint32_t*>(codes + w4t_offset(b, w * 4, ld_codes)) = pack8(c);
+    }
+    if (tid == 0) scales[b] = s;
+}
+
 // ============================================================== K6
 // grid (pages, H, B), 128 threads: one CTA per (64-row page, query head,
 // sequence) -- the cache length is read from device memory so the decode step
@@ -356,7 +440,11 @@ __global__ void __launch_bounds__(128) k_attn_decode(const float* __restrict__ q
                                                      uint8_t* __restrict__ pool, long long page_bytes,
                                                      const int* __restrict__ pt, int max_pages, float inv_sqrt,
                                                      float* __restrict__ part_ml, float* __restrict__ part_o,
-                                                     const double2* __restrict__ rope, const int* __restrict__ pos) {
+                                                     const double2* __restrict__ rope, const int* __restrict__ pos,
+                                                     unsigned* __restrict__ cnt, float* __restrict__ row,
+                                                     float* __restrict__ hmax, uint8_t* __restrict__ codes,
+                                                     int ld_codes, double* __restrict__ scales, int qmode,
+                                                     double static_scale, int d_pad, int qmax) {
     constexpr int CPL = DH / 4;  // channels per lane
     constexpr int R = 2;         // rows per lane
     pdl_launch_dependents();
@@ -413,6 +501,8 @@ __global__ void __launch_bounds__(128) k_attn_decode(const float* __restrict__ q
             part_ml[pidx * 2] = -1e30f;
             part_ml[pidx * 2 + 1] = 0.f;
         }
+        if (cnt) attn_dec_arrive<DH>(b, h, H, npg, part_ml, part_o, cnt, row, hmax, codes, ld_codes, scales, qmode,
+                                     static_scale, d_pad, qmax);
         return;
     }
     const uint8_t* page = pool + (long long)pt[b * max_pages + pg] * page_bytes;
@@ -525,6 +615,8 @@ __global__ void __launch_bounds__(128) k_attn_decode(const float* __restrict__ q
             part_ml[pidx * 2 + 1] = ll;
         }
     }
+    if (cnt) attn_dec_arrive<DH>(b, h, H, npg, part_ml, part_o, cnt, row, hmax, codes, ld_codes, scales, qmode,
+                                 static_scale, d_pad, qmax);
 }
 
 // Merge the page partials of every head of one sequence (fixed page order) and,
@@ -651,8 +743,9 @@ int qt_launch_attn_decode(const float* qkv, int ldq, int H, int Hkv, int dh, con
                           uint8_t* pool, long long page_bytes, const int* pt, int max_pages, int n_pages,
                           float* part_ml, float* part_o, float* out, int ldo, uint8_t* codes, int ld_codes,
                           double* scales, int qmode, double static_scale, int d_pad, int bits, const double* rope,
-                          const int* pos, cudaStream_t st) {
+                          const int* pos, unsigned* counters, float* row, float* hmax, cudaStream_t st) {
     const double2* rt = reinterpret_cast<const double2*>(rope);
+    if (counters && (!row || !hmax || !codes || (H * dh) % 8)) return -1;
     if (B <= 0) return 0;
     if (H > 64) return -1;
     const dim3 grid(n_pages, H, B);
@@ -661,16 +754,18 @@ int qt_launch_attn_decode(const float* qkv, int ldq, int H, int Hkv, int dh, con
     int rc;
     if (dh == 128) {
         rc = launch_pdl(k_attn_decode<128>, grid, dim3(128), 0, st, qkv, ldq, H, Hkv, kv_len, len_add, pool,
-                        page_bytes, pt, max_pages, inv_sqrt, part_ml, part_o, rt, pos);
-        if (rc) return rc;
+                        page_bytes, pt, max_pages, inv_sqrt, part_ml, part_o, rt, pos, counters, row, hmax, codes,
+                        ld_codes, scales, qmode, static_scale, d_pad, qmax);
+        if (rc || counters) return rc;  // counters: merged + quantized by the last arrivals
         auto mk = H > 32 ? k_attn_merge_quant<128, 64> : k_attn_merge_quant<128, 32>;
         return launch_pdl(mk, dim3(B), dim3(1024), 0, st, (const float*)part_ml, (const float*)part_o, n_pages, H, out,
                           ldo, codes, ld_codes, scales, qmode, static_scale, d_pad, qmax);
     }
     if (dh == 64) {
         rc = launch_pdl(k_attn_decode<64>, grid, dim3(128), 0, st, qkv, ldq, H, Hkv, kv_len, len_add, pool,
-                        page_bytes, pt, max_pages, inv_sqrt, part_ml, part_o, rt, pos);
-        if (rc) return rc;
+                        page_bytes, pt, max_pages, inv_sqrt, part_ml, part_o, rt, pos, counters, row, hmax, codes,
+                        ld_codes, scales, qmode, static_scale, d_pad, qmax);
+        if (rc || counters) return rc;  // counters: merged + quantized by the last arrivals
         auto mk = H > 32 ? k_attn_merge_quant<64, 64> : k_attn_merge_quant<64, 32>;
         return launch_pdl(mk, dim3(B), dim3(1024), 0, st, (const float*)part_ml, (const float*)part_o, n_pages, H, out,
                           ldo, codes, ld_codes, scales, qmode, static_scale, d_pad, qmax);

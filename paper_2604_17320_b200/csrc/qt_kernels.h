@@ -76,11 +76,14 @@ int qt_launch_attn_colsum(const float* qkv, int ldq, int H, int Hkv, int dh, con
                           const int* pt, int max_pages, const float* ml, int vstride, float* inter, float* intra,
                           cudaStream_t st);
 // rope/pos non-null: RoPE of q and the new token's K/V append fused in (decode step)
+// counters (B*H + B, zeroed once): merge + attn_out quantization by the last arrivals in the
+// same launch (row: fp32 [B x H*dh] scratch, hmax: [B*H]); null: separate merge launch
 int qt_launch_attn_decode(const float* qkv, int ldq, int H, int Hkv, int dh, const int* kv_len, int len_add, int B,
                           uint8_t* pool, long long page_bytes, const int* pt, int max_pages, int n_pages,
                           float* part_ml, float* part_o, float* out, int ldo, uint8_t* codes, int ld_codes,
                           double* scales, int qmode, double static_scale, int d_pad, int bits, const double* rope,
-                          const int* pos, cudaStream_t st);
+                          const int* pos, unsigned* counters, float* row, float* hmax,
+                          cudaStream_t st);
 int qt_launch_select_topk(const double* mag, const double* res, const float* inter, const float* intra, int H,
                           int vstride, const int* vis, const int* txt, const int* budget, const int* old_off,
                           const int* new_off, int B, int vmax, const double* w4, int* keep_src, int* keep_local,
