@@ -394,6 +394,74 @@ __global__ void __launch_bounds__(256) k_rope_kv_append(
     }
 }
 
+// K5 for token-rich launches (prefill), d_head = 128: one CTA per token, its 8
+// warps loop over the token's head slots, 4 at a time with every load of the
+// group issued first (float4 per lane); the RoPE cos/sin of the token's position
+// are read once per lane and reused by every q and k head.  Same arithmetic as
+// k_rope_kv_append.
+__global__ void __launch_bounds__(256) k_rope_kv_append_tok(
+    float* __restrict__ qkv, int ld_qkv, int M, int H, int Hkv, const int* __restrict__ pos,
+    const int* __restrict__ tok_seq, const int* __restrict__ tok_row, const double2* __restrict__ rope,
+    const int* __restrict__ page_table, int max_pages, uint8_t* __restrict__ pool, long long page_bytes, int qmax) {
+    constexpr int DH = 128, E = 4, G = 4;
+    pdl_launch_dependents();
+    pdl_wait();
+    const int m = blockIdx.x;
+    if (m >= M) return;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const double2* rt = rope + (size_t)pos[m] * (DH / 2);
+    const double2 cs0 = rt[lane * 2], cs1 = rt[lane * 2 + 1];
+    float* row = qkv + (size_t)m * ld_qkv;
+    const int b = tok_seq[m], r = tok_row[m];
+    uint8_t* page = pool + (long long)page_table[b * max_pages + r / kPage] * page_bytes;
+    const int slot = r % kPage;
+    const size_t codes_bytes = (size_t)Hkv * kPage * (DH / 2);
+    const int nt = H + 2 * Hkv;
+    for (int t0 = wid; t0 < nt; t0 += 8 * G) {
+        float4 x4[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            const int t = t0 + 8 * g;
+            x4[g] = t < nt ? *reinterpret_cast<const float4*>(row + t * DH + lane * E) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            const int t = t0 + 8 * g;
+            if (t >= nt) break;
+            double val[4] = {(double)x4[g].x, (double)x4[g].y, (double)x4[g].z, (double)x4[g].w};
+            if (t < H + Hkv) {  // rope q and k
+                double a = val[0], bb = val[1];
+                val[0] = __dsub_rn(__dmul_rn(a, cs0.x), __dmul_rn(bb, cs0.y));
+                val[1] = __dadd_rn(__dmul_rn(a, cs0.y), __dmul_rn(bb, cs0.x));
+                a = val[2];
+                bb = val[3];
+                val[2] = __dsub_rn(__dmul_rn(a, cs1.x), __dmul_rn(bb, cs1.y));
+                val[3] = __dadd_rn(__dmul_rn(a, cs1.y), __dmul_rn(bb, cs1.x));
+            }
+            if (t < H) {
+                *reinterpret_cast<float4*>(row + t * DH + lane * E) =
+                    make_float4((float)val[0], (float)val[1], (float)val[2], (float)val[3]);
+                continue;
+            }
+            double mx = fmax(fmax(fabs(val[0]), fabs(val[1])), fmax(fabs(val[2]), fabs(val[3])));
+            mx = warp_max(mx);
+            const double sc = q_scale(mx, qmax), inv_s = 1.0 / sc;
+            const bool is_k = t < H + Hkv;
+            const int kh = is_k ? t - H : t - H - Hkv;
+            int c[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) c[j] = q_code_r(val[j], sc, inv_s, qmax);
+            uint8_t* dst = page + (is_k ? 0 : codes_bytes) + ((size_t)kh * kPage + slot) * (DH / 2) + lane * E / 2;
+            *reinterpret_cast<uint16_t*>(dst) =
+                (uint16_t)((c[0] & 0xF) | ((c[1] & 0xF) << 4) | ((c[2] & 0xF) << 8) | ((c[3] & 0xF) << 12));
+            if (lane == 0) {
+                float* scp = reinterpret_cast<float*>(page + 2 * codes_bytes) + (is_k ? 0 : Hkv * kPage);
+                scp[kh * kPage + slot] = (float)sc;
+            }
+        }
+    }
+}
+
 // ============================================================== K3b
 // QUOTA per-visual-token metrics on the post-attention residual x
 // (selector.cpp:19-68): mag = ||x_i||_2, res = ||fq_row(x_i) - x_i||_2 with
@@ -600,6 +668,11 @@ int qt_launch_rope_kv_append(float* qkv, int ld_qkv, int M, int H, int Hkv, int 
     if (M <= 0) return 0;
     if (dh != 64 && dh != 128) return -1;
     const int qmax = (1 << (bits - 1)) - 1;
+    static const bool per_tok = !(getenv("QT_KV_TOK") && atoi(getenv("QT_KV_TOK")) == 0);
+    if (per_tok && dh == 128 && M >= 64 && !k_dbg)
+        return launch_pdl(k_rope_kv_append_tok, dim3(M), dim3(256), 0, st, qkv, ld_qkv, M, H, Hkv, pos, tok_seq,
+                          tok_row, reinterpret_cast<const double2*>(rope), page_table, max_pages, pool, page_bytes,
+                          qmax);
     return launch_pdl(k_rope_kv_append, dim3(M, (H + 2 * Hkv + 7) / 8), dim3(256), 0, st, qkv, ld_qkv, M, H, Hkv,
                       dh, pos, tok_seq, tok_row, reinterpret_cast<const double2*>(rope), page_table, max_pages, pool,
                       page_bytes, qmax, k_dbg);
