@@ -108,6 +108,9 @@ struct LayerW {
     float* g1 = nullptr;
     float* g2 = nullptr;
     bool loaded = false;
+    // int8 copies (16 x code, row-major, k natural) for the int8-operand prefill GEMM, made lazily
+    int8_t *qkv8 = nullptr, *o8 = nullptr, *gu8 = nullptr, *down8 = nullptr;
+    bool w8_ok = false;
 };
 
 // fp64 copies of the full-precision weights (reference orientation [d_in x d_out]),
@@ -302,6 +305,31 @@ struct qt_engine {
     std::vector<FpLayer> fpw;
     double* fp_head = nullptr;
     cublasHandle_t blas = nullptr;
+    // int8-operand prefill GEMM (k_gemm_tc05_i8): activation codes as int8 next to the packed ones
+    const bool i8_on = !(std::getenv("QT_I8") && std::atoi(std::getenv("QT_I8")) == 0);
+    int8_t* codes8 = nullptr;
+    int ld8 = 0;
+    int8_t* head8 = nullptr;
+    bool head8_ok = false;
+    void ensure_w8() {
+        auto conv = [&](const uint8_t* w, int rows, int K, int8_t*& dst) {
+            if (!dst) dst = dalloc<int8_t>((size_t)rows * K);
+            ckl(qt_launch_w4t_to_i8(w, rows, K, dst, st), "int8 weight copy");
+        };
+        for (auto& l : lw) {
+            if (l.w8_ok) continue;
+            conv(l.qkv, n_qkv_pad, kd_pad, l.qkv8);
+            conv(l.o, nd_pad, kd_pad, l.o8);
+            conv(l.gu, n_gu_pad, kd_pad, l.gu8);
+            conv(l.down, nd_pad, kff_pad, l.down8);
+            l.w8_ok = true;
+        }
+        if (!head8_ok) {
+            conv(head, nd_pad, kd_pad, head8);
+            head8_ok = true;
+        }
+        qt::g_pdl_block = true;
+    }
     // decode attention: merge + attn_out quantizer by the last page / head arrivals (k_attn.cu)
     const bool attn_last = std::getenv("QT_ATTN_LAST") && std::atoi(std::getenv("QT_ATTN_LAST")) == 1;  // opt-in: slower
     unsigned* dec_cnt = nullptr;
@@ -331,6 +359,7 @@ struct qt_engine {
         };
         for (auto& l : lw) {
             f(l.qkv); f(l.s_qkv); f(l.o); f(l.s_o); f(l.gu); f(l.s_gu); f(l.down); f(l.s_down); f(l.g1); f(l.g2);
+            f(l.qkv8); f(l.o8); f(l.gu8); f(l.down8);
         }
         f(head); f(s_head); f(gf);
         f(x[0]); f(x[1]); f(pos[0]); f(pos[1]); f(qkv); f(attn); f(mid); f(codes); f(ascale); f(logits); f(ml);
@@ -342,7 +371,7 @@ struct qt_engine {
             for (double* p : fl.w) f(p);
         f(fp_head);
         if (blas) cublasDestroy(blas);
-        f(splitk_ws); f(pmax); f(dec_cnt); f(dec_hmax); f(seq_cnt); f(mk_trace); f(mk_layers); f(mk_acc); f(mk_codes); f(mk_sa); f(mk_attn); f(mk_sync); f(mk_act);
+        f(splitk_ws); f(codes8); f(head8); f(pmax); f(dec_cnt); f(dec_hmax); f(seq_cnt); f(mk_trace); f(mk_layers); f(mk_acc); f(mk_codes); f(mk_sa); f(mk_attn); f(mk_sync); f(mk_act);
         if (pin) cudaFreeHost(pin);
         if (own_stream) cudaStreamDestroy(own_stream);
     }
@@ -432,6 +461,10 @@ struct qt_engine {
         mid = dalloc<float>(T * dff);
         codes_rows = round_up(std::max((int)T, mb), 16);
         codes = dalloc<uint8_t>((size_t)codes_rows * std::max(kd_pad, kff_pad) / 2);  // tiled rows
+        if (i8_on && use_tc05 && (int)T > 64) {
+            ld8 = std::max(kd_pad, kff_pad);
+            codes8 = dalloc<int8_t>((size_t)codes_rows * ld8);
+        }
         ascale = dalloc<double>(T);
         logits = dalloc<float>(T * d);
         ml = dalloc<float>(T * H * 2);
@@ -1089,25 +1122,30 @@ struct qt_engine {
         const int mode = cfg.act_mode;
         const double s = mode == 0 ? act[site_idx] : 0.0;
         pb(P_QUANT);
+        int8_t* c8 = codes8 && M > 64 ? codes8 : nullptr;  // the next GEMM runs on int8 operands
         if (from_pmax && pm_parts > 0 && !is_f64 && !gain && mode == 1)
             ckl(qt_launch_quant_pmax(static_cast<const float*>(xin), ldx, pmax, pm_parts, kPmaxLd, M, D, dpad, 7, mode,
-                                     s, codes, codes_rows, ascale, st),
+                                     s, codes, codes_rows, ascale, c8, ld8, st),
                 "quant (producer row max)");
         else
             ckl(qt_launch_norm_quant(xin, is_f64, ldx, gain, M, D, dpad, 4, mode, s, codes, codes_rows, ascale,
-                                     nullptr, st),
+                                     nullptr, c8, ld8, st),
                 "rmsnorm+quant");
         pe((double)M * D * (is_f64 ? 8 : 4) + (double)M * dpad / 2 + 8.0 * M);
     }
     // w: tiled int4 weights with wrows padded rows; activation codes: tiled with codes_rows rows
     // want_pm: also leave the per-row partial max |out| in pmax (pm_parts slots; 0 = not produced)
     void gemm(int epi, const uint8_t* w, int wrows, const double* sw, int M, int N, int K, void* out, int ldo,
-              bool want_pm = false) {
+              bool want_pm = false, const int8_t* w8 = nullptr) {
         pb(P_GEMM);
         float* pm = want_pm ? pmax : nullptr;
         pm_parts = 0;
+        const bool split = splitk_ws && qt_tc05_splitk(M, N, K) > 1;
         // tcgen05 for token-rich GEMMs; the weight-streaming GEMV up to 64 tokens (decode batches)
-        int rc = (use_tc05 && M > 64)
+        int rc = (use_tc05 && M > 64 && codes8 && w8 && !split)
+                     ? qt_launch_w4a4_tc05_i8(epi, codes8, ld8, ascale, w8, wrows, K, sw, M, N, K, out, ldo, nullptr, pm,
+                                              kPmaxLd, &pm_parts, st)
+                 : (use_tc05 && M > 64)
                      ? qt_launch_w4a4_tc05_ex(epi, codes, codes_rows, ascale, w, wrows, sw, M, N, K, out, ldo, nullptr,
                                               splitk_ws, pm, kPmaxLd, &pm_parts, st)
                      : qt_launch_w4a4_mma_ex(epi, codes, codes_rows, ascale, w, wrows, sw, M, N, K, out, ldo, nullptr,
@@ -1132,6 +1170,7 @@ struct qt_engine {
         if (cfg.act_mode == 0 && !act_set) fail(QT_EINVAL, "quantized mode requires a QuantEnv");  // model.cpp:323-325
         if (nseq < 1 || nseq > max_batch) fail(QT_EINVAL, "batch size outside engine capacity");
         reset_staging();
+        if (codes8) ensure_w8();
         graph_ok = false;
         prefilled = false;
         if (prof_next) {
@@ -1263,7 +1302,7 @@ struct qt_engine {
             int* ptl = pt + (size_t)l * max_batch * max_pages;
             // attention block (model.cpp:347-396)
             norm_quant(xc, 1, d, w.g1, M, d, kd_pad, 4 * l + 0);
-            gemm(QT_EPI_STORE, w.qkv, n_qkv_pad, w.s_qkv, M, n_qkv, kd_pad, qkv, n_qkv);
+            gemm(QT_EPI_STORE, w.qkv, n_qkv_pad, w.s_qkv, M, n_qkv, kd_pad, qkv, n_qkv, false, w.qkv8);
             pb(P_KV);
             ckl(qt_launch_rope_kv_append(qkv, n_qkv, M, H, Hkv, dh, pc, tok_seq, tok_row, rope, ptl, max_pages, pool,
                                          page_bytes, 4, nullptr, st),
@@ -1292,7 +1331,7 @@ struct qt_engine {
             }
             pm_parts = pmax ? H : 0;  // the attention epilogue left max |out| per (row, head)
             norm_quant(attn, 0, d, nullptr, M, d, kd_pad, 4 * l + 1, true);
-            gemm(QT_EPI_RESADD, w.o, nd_pad, w.s_o, M, d, kd_pad, xc, d);
+            gemm(QT_EPI_RESADD, w.o, nd_pad, w.s_o, M, d, kd_pad, xc, d, false, w.o8);
             if (rec_diag) diag_layer(l, ptl, cur_v[0], h_txt[0], xc);
             for (int b = 0; b < B; ++b) h_kvlen[(size_t)l * B + b] = cur_v[b] + h_txt[b];
 
@@ -1345,10 +1384,10 @@ struct qt_engine {
             }
             // MLP block (model.cpp:429-437)
             norm_quant(xc, 1, d, w.g2, M, d, kd_pad, 4 * l + 2);
-            if (cfg.mlp == 1) gemm(QT_EPI_SWIGLU, w.gu, n_gu_pad, w.s_gu, M, n_gu, kd_pad, mid, dff, true);
-            else gemm(QT_EPI_SILU, w.gu, n_gu_pad, w.s_gu, M, n_gu, kd_pad, mid, dff, true);
+            if (cfg.mlp == 1) gemm(QT_EPI_SWIGLU, w.gu, n_gu_pad, w.s_gu, M, n_gu, kd_pad, mid, dff, true, w.gu8);
+            else gemm(QT_EPI_SILU, w.gu, n_gu_pad, w.s_gu, M, n_gu, kd_pad, mid, dff, true, w.gu8);
             norm_quant(mid, 0, dff, nullptr, M, dff, kff_pad, 4 * l + 3, true);
-            gemm(QT_EPI_RESADD, w.down, nd_pad, w.s_down, M, d, kff_pad, xc, d);
+            gemm(QT_EPI_RESADD, w.down, nd_pad, w.s_down, M, d, kff_pad, xc, d, false, w.down8);
             if (rec_blocks) {  // ForwardResult::block_outputs (model.cpp:439), calibration only
                 if (l == 0) rec_blocks->assign(L, {});
                 (*rec_blocks)[l].resize((size_t)M * d);
@@ -1359,7 +1398,7 @@ struct qt_engine {
         }
         // final norm + head (model.cpp:442-445)
         norm_quant(xc, 1, d, gf, M, d, kd_pad, 4 * L);
-        gemm(QT_EPI_STORE, head, nd_pad, s_head, M, d, kd_pad, logits, d);
+        gemm(QT_EPI_STORE, head, nd_pad, s_head, M, d, kd_pad, logits, d, false, head8);
         final_rows = M;
         ev_layers = trace_layers;
         ev_vis = ev_prev_v;
@@ -1774,6 +1813,7 @@ int qt_engine_load_layer(qt_engine* e, int layer, const float* wq, const float* 
         e->load_gain(l.g1, g1, on_device);
         e->load_gain(l.g2, g2, on_device);
         l.loaded = true;
+        l.w8_ok = false;
         e->graph_ok = false;
     });
 }
@@ -1800,6 +1840,7 @@ int qt_engine_load_layer_codes(qt_engine* e, int layer, const int8_t* const* cod
         e->load_gain64(l.g1, g1);
         e->load_gain64(l.g2, g2);
         l.loaded = true;
+        l.w8_ok = false;
         e->graph_ok = false;
     });
 }
@@ -1809,6 +1850,7 @@ int qt_engine_load_head_codes(qt_engine* e, const int8_t* codes, const double* s
         e->codes_into(codes, scales, e->d, e->d, 1, 0, e->head, e->nd_pad, e->s_head);
         e->load_gain64(e->gf, final_gain);
         e->head_loaded = true;
+        e->head8_ok = false;
         e->graph_ok = false;
     });
 }
@@ -1991,8 +2033,12 @@ int qt_engine_load(qt_engine* e, const char* path) {
                 ck(cudaMemcpy(static_cast<char*>(dev) + o, e->pin, n, cudaMemcpyHostToDevice), "weights upload");
             }
         });
-        for (auto& l : e->lw) l.loaded = true;
+        for (auto& l : e->lw) {
+            l.loaded = true;
+            l.w8_ok = false;
+        }
         e->head_loaded = true;
+        e->head8_ok = false;
         e->graph_ok = false;
     });
 }
@@ -2005,6 +2051,7 @@ int qt_engine_load_head(qt_engine* e, const float* w_head, const float* final_ga
         e->keep64(e->fp_head, w_head, (size_t)e->d * e->d, on_device);
         e->load_gain(e->gf, final_gain, on_device);
         e->head_loaded = true;
+        e->head8_ok = false;
         e->graph_ok = false;
     });
 }
@@ -2226,7 +2273,7 @@ int qt_rmsnorm_quant_i4(const void* x, int x_is_f64, int ld_x, const float* gain
                         float* normed, void* stream) {
     return guard([&] {
         ckl(qt_launch_norm_quant(x, x_is_f64, ld_x, gain, M, D, d_pad, 4, act_mode, static_scale, codes, ld_codes,
-                                 scales, normed, (cudaStream_t)stream),
+                                 scales, normed, nullptr, 0, (cudaStream_t)stream),
             "rmsnorm+quant");
     });
 }
@@ -2234,16 +2281,31 @@ int qt_rmsnorm_quant_i4(const void* x, int x_is_f64, int ld_x, const float* gain
 int qt_w4a4_gemm(int epi, const uint8_t* a, int lda, const double* sa, const uint8_t* w, int ldw, const double* sw,
                  int M, int N, int K, void* out, int ldo, int32_t* acc_out, int impl, void* stream) {
     return guard([&] {
+        const cudaStream_t cs = (cudaStream_t)stream;
+        if (impl == 3) {  // int8-operand tcgen05 GEMM: both operands widened to int8 first (test / ABI path)
+            int8_t *a8 = nullptr, *w8 = nullptr;
+            ck(cudaMalloc(&a8, (size_t)lda * K), "int8 activations");
+            ck(cudaMalloc(&w8, (size_t)ldw * K), "int8 weights");
+            int rc = qt_launch_w4t_to_i8(a, lda, K, a8, cs);
+            if (!rc) rc = qt_launch_w4t_to_i8(w, ldw, K, w8, cs);
+            if (!rc)
+                rc = qt_launch_w4a4_tc05_i8(epi, a8, K, sa, w8, ldw, K, sw, M, N, K, out, ldo, acc_out, nullptr, 0,
+                                            nullptr, cs);
+            cudaStreamSynchronize(cs);
+            cudaFree(a8);
+            cudaFree(w8);
+            ckl(rc, "w4a4 gemm (int8 operands)");
+            return;
+        }
         int* ws = nullptr;  // impl 2: tcgen05 with split-K (temporary workspace; test / ABI path)
         if (impl == 2) {
             const int ks = qt_tc05_splitk(M, N, K);
             ck(cudaMalloc(&ws, (size_t)std::max(ks, 1) * M * N * sizeof(int)), "split-K workspace");
         }
-        int rc = impl >= 1 ? qt_launch_w4a4_tc05(epi, a, lda, sa, w, ldw, sw, M, N, K, out, ldo, acc_out, ws,
-                                                  (cudaStream_t)stream)
-                           : qt_launch_w4a4_mma(epi, a, lda, sa, w, ldw, sw, M, N, K, out, ldo, acc_out, (cudaStream_t)stream);
+        int rc = impl >= 1 ? qt_launch_w4a4_tc05(epi, a, lda, sa, w, ldw, sw, M, N, K, out, ldo, acc_out, ws, cs)
+                           : qt_launch_w4a4_mma(epi, a, lda, sa, w, ldw, sw, M, N, K, out, ldo, acc_out, cs);
         if (ws) {
-            cudaStreamSynchronize((cudaStream_t)stream);
+            cudaStreamSynchronize(cs);
             cudaFree(ws);
         }
         ckl(rc, "w4a4 gemm");

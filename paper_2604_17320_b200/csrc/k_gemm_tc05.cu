@@ -22,6 +22,8 @@
 //   warps 6..9  epilogue: tcgen05.ld 32x32b, exact >>8, fp64 scales, fused
 //               store / residual add / SiLU / SwiGLU -- overlapping the next
 //               tile's main loop (double-buffered accumulators).
+#include <cuda.h>  // CUtensorMap (types only; the encoder comes from cudaGetDriverEntryPoint)
+
 #include <algorithm>
 #include <cstdlib>
 
@@ -130,6 +132,88 @@ QT_DEV void store_converted(const uint4 w, uint8_t* i8, int row, int q) {
     const int c0 = 2 * q, c1 = 2 * q + 1, sw = row & 7;
     *reinterpret_cast<uint4*>(atom + ((c0 ^ sw) << 4)) = o0;
     *reinterpret_cast<uint4*>(atom + ((c1 ^ sw) << 4)) = o1;
+}
+
+// Epilogue warps (T5_EWN of them, first warp ew0): warp & 3 = TMEM lane quarter (32 rows),
+// (warp - ew0) / 4 = column half.  Shared by the packed-int4 and the int8-operand kernels.
+template <int EPI>
+QT_DEV void t5_epilogue(int ew0, int warp, int lane, uint32_t tmem, int units, int tiles, int mt_n, int M, int N,
+                        const double* __restrict__ sa, const double* __restrict__ sw, double* sws,
+                        void* __restrict__ out, int ldo, int* __restrict__ acc_dbg, int ksplit, int* __restrict__ ws,
+                        float* __restrict__ pmax, int pmax_ld, uint64_t* tfull, uint64_t* tempty) {
+    // ---------------- epilogue: 8 warps; warp & 3 = TMEM lane quarter (32 rows), and
+    // (warp - ew0) / 4 = column half -- the per-element fp64 scale math is split 2 ways
+    pdl_wait();  // scales / residual come from upstream kernels
+    pdl_launch_dependents();
+    const int q = warp & 3;
+    const int et = threadIdx.x - ew0 * 32;
+    const int jh = ((warp - ew0) >> 2) * (T5_BN / 64);  // first 32-column chunk of this half
+    int tl = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++tl) {
+        const int t = u % tiles, sl = u / tiles;
+        const int acc = tl % T5_ACC;
+        const int m0 = (t % mt_n) * T5_BM, n0 = (t / mt_n) * T5_BN;
+        double* swt = sws + acc * T5_BN;
+        for (int i = et; i < T5_BN; i += T5_ET) swt[i] = n0 + i < N ? sw[n0 + i] : 0.0;
+        if (EPI == QT_EPI_RESADD && ksplit == 1) {
+            // pull this thread's residual row segment (256 fp64) toward L2 while the
+            // tile's MMAs run: the read-modify-write below then hits L2, not HBM
+            const int mr = m0 + q * 32 + lane;
+            const int c0 = jh * 32;
+            if (mr < M && n0 + c0 < N) {
+                const char* rp =
+                    reinterpret_cast<const char*>(static_cast<const double*>(out) + (size_t)mr * ldo + n0 + c0);
+                const int nb = min(T5_BN / 2, N - n0 - c0) * 8;
+                for (int c = 0; c < nb; c += 128) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(rp + c));
+            }
+        }
+        asm volatile("bar.sync 2, %0;\n" ::"n"(T5_ET) : "memory");
+        mbar_wait(&tfull[acc], (tl / T5_ACC) & 1);
+        tc_fence_after();
+        const int m = m0 + q * 32 + lane;
+        const double a_s = m < M ? sa[m] : 0.0;
+        const uint32_t tacc = tmem + (uint32_t)(acc * T5_BN) + ((uint32_t)(q * 32) << 16);
+        float mx = 0.f;  // max |v| over this thread's (row, column half) of the tile
+#pragma unroll 1
+        for (int j = jh; j < jh + T5_BN / 64; ++j) {
+            uint32_t r[32];
+            tmem_ld32(tacc + (uint32_t)(j * 32), r);
+            if (j == jh + T5_BN / 64 - 1) {
+                // accumulator fully read: hand it back to the MMA issuer
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty[acc]);
+            }
+            const int nb = n0 + j * 32;
+            if (m >= M || nb >= N) continue;
+            if (ksplit > 1) {  // raw partial sums of this k slice
+                int* wr = ws + ((size_t)sl * M + m) * N + nb;
+#pragma unroll
+                for (int e = 0; e < 32; ++e)
+                    if (nb + e < N) wr[e] = (int)r[e] >> 8;
+                continue;
+            }
+            if (acc_dbg) {
+#pragma unroll
+                for (int e = 0; e < 32; ++e)
+                    if (nb + e < N) acc_dbg[(size_t)m * N + nb + e] = (int)r[e] >> 8;
+            }
+            if (nb + 32 <= N) {
+                epi_row32<EPI>(out, ldo, m, nb, r, a_s, swt + j * 32, mx);
+            } else {
+#pragma unroll
+                for (int e = 0; e < 32; e += 2)
+                    if (nb + e < N)
+                        mx = fmaxf(mx, epi_store<EPI>(out, ldo, m, nb + e,
+                                                      (double)((int)r[e] >> 8) * (a_s * swt[j * 32 + e]),
+                                                      (double)((int)r[e + 1] >> 8) * (a_s * swt[j * 32 + e + 1]),
+                                                      N));
+            }
+        }
+        // partial row max for the next site's dynamic quantizer: slot (n tile, column half)
+        if (pmax && ksplit == 1 && m < M) pmax[(size_t)m * pmax_ld + (t / mt_n) * 2 + jh / (T5_BN / 64)] = mx;
+        asm volatile("bar.sync 2, %0;\n" ::"n"(T5_ET) : "memory");  // swt reuse
+    }
 }
 
 template <int EPI>
@@ -284,85 +368,148 @@ __global__ void __launch_bounds__(T5_THREADS, 1) k_gemm_tc05(const uint8_t* __re
             }
         }
     } else {
-        // ---------------- epilogue: 8 warps; warp & 3 = TMEM lane quarter (32 rows), and
-        // (warp - T5_EW0) / 4 = column half -- the per-element fp64 scale math is split 2 ways
-        pdl_wait();  // scales / residual come from upstream kernels
-        pdl_launch_dependents();
-        const int q = warp & 3;
-        const int et = threadIdx.x - T5_EW0 * 32;
-        const int jh = ((warp - T5_EW0) >> 2) * (T5_BN / 64);  // first 32-column chunk of this half
-        int tl = 0;
-        for (int u = blockIdx.x; u < units; u += gridDim.x, ++tl) {
-            const int t = u % tiles, sl = u / tiles;
-            const int acc = tl % T5_ACC;
-            const int m0 = (t % mt_n) * T5_BM, n0 = (t / mt_n) * T5_BN;
-            double* swt = sws + acc * T5_BN;
-            for (int i = et; i < T5_BN; i += T5_ET) swt[i] = n0 + i < N ? sw[n0 + i] : 0.0;
-            if (EPI == QT_EPI_RESADD && ksplit == 1) {
-                // pull this thread's residual row segment (256 fp64) toward L2 while the
-                // tile's MMAs run: the read-modify-write below then hits L2, not HBM
-                const int mr = m0 + q * 32 + lane;
-                const int c0 = jh * 32;
-                if (mr < M && n0 + c0 < N) {
-                    const char* rp =
-                        reinterpret_cast<const char*>(static_cast<const double*>(out) + (size_t)mr * ldo + n0 + c0);
-                    const int nb = min(T5_BN / 2, N - n0 - c0) * 8;
-                    for (int c = 0; c < nb; c += 128) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(rp + c));
-                }
-            }
-            asm volatile("bar.sync 2, %0;\n" ::"n"(T5_ET) : "memory");
-            mbar_wait(&tfull[acc], (tl / T5_ACC) & 1);
-            tc_fence_after();
-            const int m = m0 + q * 32 + lane;
-            const double a_s = m < M ? sa[m] : 0.0;
-            const uint32_t tacc = tmem + (uint32_t)(acc * T5_BN) + ((uint32_t)(q * 32) << 16);
-            float mx = 0.f;  // max |v| over this thread's (row, column half) of the tile
-#pragma unroll 1
-            for (int j = jh; j < jh + T5_BN / 64; ++j) {
-                uint32_t r[32];
-                tmem_ld32(tacc + (uint32_t)(j * 32), r);
-                if (j == jh + T5_BN / 64 - 1) {
-                    // accumulator fully read: hand it back to the MMA issuer
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&tempty[acc]);
-                }
-                const int nb = n0 + j * 32;
-                if (m >= M || nb >= N) continue;
-                if (ksplit > 1) {  // raw partial sums of this k slice
-                    int* wr = ws + ((size_t)sl * M + m) * N + nb;
-#pragma unroll
-                    for (int e = 0; e < 32; ++e)
-                        if (nb + e < N) wr[e] = (int)r[e] >> 8;
-                    continue;
-                }
-                if (acc_dbg) {
-#pragma unroll
-                    for (int e = 0; e < 32; ++e)
-                        if (nb + e < N) acc_dbg[(size_t)m * N + nb + e] = (int)r[e] >> 8;
-                }
-                if (nb + 32 <= N) {
-                    epi_row32<EPI>(out, ldo, m, nb, r, a_s, swt + j * 32, mx);
-                } else {
-#pragma unroll
-                    for (int e = 0; e < 32; e += 2)
-                        if (nb + e < N)
-                            mx = fmaxf(mx, epi_store<EPI>(out, ldo, m, nb + e,
-                                                          (double)((int)r[e] >> 8) * (a_s * swt[j * 32 + e]),
-                                                          (double)((int)r[e + 1] >> 8) * (a_s * swt[j * 32 + e + 1]),
-                                                          N));
-                }
-            }
-            // partial row max for the next site's dynamic quantizer: slot (n tile, column half)
-            if (pmax && ksplit == 1 && m < M) pmax[(size_t)m * pmax_ld + (t / mt_n) * 2 + jh / (T5_BN / 64)] = mx;
-            asm volatile("bar.sync 2, %0;\n" ::"n"(T5_ET) : "memory");  // swt reuse
-        }
+        t5_epilogue<EPI>(T5_EW0, warp, lane, tmem, units, tiles, mt_n, M, N, sa, sw, sws, out, ldo, acc_dbg, ksplit, ws,
+                         pmax, pmax_ld, tfull, tempty);
     }
     tc_fence_before();
     __syncthreads();
     if (warp == 1) {
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(T5_ACC * T5_BN));
     }
+}
+
+// ============================================================== int8-operand variant
+// Both operands arrive as int8 (16 x the int4 code, k in natural order) row-major in
+// HBM: the weights converted once at load (k_w4t_to_i8), the activations written by
+// the quantizer next to the packed codes.  TMA tensor loads (SWIZZLE_128B) put them
+// straight into the UMMA canonical K-major layout, so there are no converter warps:
+//   warp 0      TMA producer (2D tensor loads, 4-stage 48 KB ring)
+//   warp 1      TMEM allocator + MMA issuer (same UMMA as k_gemm_tc05)
+//   warps 2..9  epilogue (t5_epilogue)
+constexpr int T8_S = 4;
+constexpr int T8_EW0 = 2;
+constexpr int T8_THREADS = (T8_EW0 + T5_EWN) * 32;
+
+struct T8Smem {
+    static constexpr size_t ia = 0;
+    static constexpr size_t ib = ia + (size_t)T8_S * T5_IA;
+    static constexpr size_t swb = ib + (size_t)T8_S * T5_IB;
+    static constexpr size_t bars = swb + (size_t)T5_ACC * T5_BN * 8;
+    static constexpr size_t total = bars + 256;
+};
+
+QT_DEV void tma_load_2d(void* dst, const CUtensorMap* tm, int c0, int c1, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+            smem_u32(dst)),
+        "l"(tm), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(T8_THREADS, 1) k_gemm_tc05_i8(const __grid_constant__ CUtensorMap tmA,
+                                                                 const __grid_constant__ CUtensorMap tmB,
+                                                                 const double* __restrict__ sa,
+                                                                 const double* __restrict__ sw, int M, int N, int K,
+                                                                 void* __restrict__ out, int ldo,
+                                                                 int* __restrict__ acc_dbg, float* __restrict__ pmax,
+                                                                 int pmax_ld) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + T8Smem::bars);
+    uint64_t* empty = full + T8_S;
+    uint64_t* tfull = empty + T8_S;
+    uint64_t* tempty = tfull + T5_ACC;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + T5_ACC);
+    double* sws = reinterpret_cast<double*>(smem + T8Smem::swb);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int KB = K / 128;
+    const int mt_n = (M + T5_BM - 1) / T5_BM, nt_n = (N + T5_BN - 1) / T5_BN;
+    const int tiles = mt_n * nt_n;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < T8_S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int s = 0; s < T5_ACC; ++s) {
+            mbar_init(&tfull[s], 1);
+            mbar_init(&tempty[s], T5_EWN);
+        }
+        mbar_fence_init();
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                     "n"(T5_ACC * T5_BN));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    if (warp == 0) {
+        if (lane == 0) {
+            asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmA) : "memory");
+            asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmB) : "memory");
+            pdl_wait();  // activation codes come from the upstream kernel
+            int it = 0;
+            for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+                const int m0 = (t % mt_n) * T5_BM, n0 = (t / mt_n) * T5_BN;
+                for (int kb = 0; kb < KB; ++kb, ++it) {
+                    const int s = it % T8_S;
+                    if (it >= T8_S) mbar_wait(&empty[s], ((it / T8_S) - 1) & 1);
+                    mbar_arrive_expect_tx(&full[s], (uint32_t)(T5_IA + T5_IB));
+                    tma_load_2d(smem + T8Smem::ia + (size_t)s * T5_IA, &tmA, kb * 128, m0, &full[s]);
+                    tma_load_2d(smem + T8Smem::ib + (size_t)s * T5_IB, &tmB, kb * 128, n0, &full[s]);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            const uint32_t idesc = t5_idesc();
+            int it = 0, tl = 0;
+            for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++tl) {
+                const int acc = tl % T5_ACC;
+                if (tl >= T5_ACC) mbar_wait(&tempty[acc], ((tl / T5_ACC) - 1) & 1);
+                tc_fence_after();
+                const uint32_t tacc = tmem + (uint32_t)(acc * T5_BN);
+                for (int kb = 0; kb < KB; ++kb, ++it) {
+                    const int s = it % T8_S;
+                    mbar_wait(&full[s], (it / T8_S) & 1);
+                    tc_fence_after();
+                    const uint32_t a0 = smem_u32(smem + T8Smem::ia + (size_t)s * T5_IA);
+                    const uint32_t b0 = smem_u32(smem + T8Smem::ib + (size_t)s * T5_IB);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        mma_i8(tacc, umma_desc_sw128(a0 + 32 * k), umma_desc_sw128(b0 + 32 * k), idesc,
+                               (kb != 0) || (k != 0));
+                    mma_commit(&empty[s]);
+                }
+                mma_commit(&tfull[acc]);
+            }
+        }
+        __syncwarp();
+    } else {
+        t5_epilogue<EPI>(T8_EW0, warp, lane, tmem, tiles, tiles, mt_n, M, N, sa, sw, sws, out, ldo, acc_dbg, 1, nullptr,
+                         pmax, pmax_ld, tfull, tempty);
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(T5_ACC * T5_BN));
+    }
+}
+
+// packed tiled int4 (w4t layout, rows_pad rows) -> row-major int8 [rows_pad x K], 16 x code,
+// k in natural order (the int8-operand GEMM's weight copy)
+__global__ void k_w4t_to_i8(const uint8_t* __restrict__ tiled, int rows_pad, int K, int8_t* __restrict__ out) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // one packed byte pair-of-k
+    const long long nb = (long long)rows_pad * (K / 2);
+    if (i >= nb) return;
+    const int row = (int)(i / (K / 2)), kb = (int)(i % (K / 2));
+    const uint8_t b = tiled[w4t_offset(row, kb, rows_pad)];
+    char2 v;
+    v.x = (char)(uint8_t)(b << 4);
+    v.y = (char)(uint8_t)(b & 0xF0);
+    reinterpret_cast<char2*>(out)[i] = v;
 }
 
 // Split-K reduction + epilogue: y = (sum over slices, fixed order) * s_a[m] * s_w[n],
@@ -447,5 +594,79 @@ extern "C" int qt_launch_w4a4_tc05_ex(int epi, const uint8_t* A, int lda, const 
         case QT_EPI_SWIGLU: QT_T5(QT_EPI_SWIGLU);
     }
 #undef QT_T5
+    return -1;
+}
+
+// ---------------------------------------------------------------- int8-operand launcher
+typedef CUresult (*qt_encode_fn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static qt_encode_fn qt_encoder() {
+    static qt_encode_fn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return (qt_encode_fn) nullptr;
+        return reinterpret_cast<qt_encode_fn>(p);
+    }();
+    return fn;
+}
+
+// int8 row-major [rows x K] with row stride ld bytes; box 128 k x box_rows rows, SW128
+static int qt_tmap_i8(CUtensorMap* tm, const int8_t* base, int rows, int K, int ld, int box_rows) {
+    qt_encode_fn enc = qt_encoder();
+    if (!enc) return -1;
+    const cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)ld};
+    const cuuint32_t box[2] = {128, (cuuint32_t)box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    return enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS
+               ? 0
+               : -1;
+}
+
+extern "C" int qt_launch_w4t_to_i8(const uint8_t* tiled, int rows_pad, int K, int8_t* out, cudaStream_t st) {
+    const long long nb = (long long)rows_pad * (K / 2);
+    if (nb <= 0) return 0;
+    qt::k_w4t_to_i8<<<(unsigned)((nb + 255) / 256), 256, 0, st>>>(tiled, rows_pad, K, out);
+    return (int)cudaGetLastError();
+}
+
+// A8: int8 activations [>= M rows x K], row stride lda8; W8: int8 weights [w_rows x K], stride ldw8.
+extern "C" int qt_launch_w4a4_tc05_i8(int epi, const int8_t* A8, int lda8, const double* sa, const int8_t* W8,
+                                      int w_rows, int ldw8, const double* sw, int M, int N, int K, void* out, int ldo,
+                                      int* acc_dbg, float* pmax, int pmax_ld, int* n_part, cudaStream_t st) {
+    using namespace qt;
+    if (n_part) *n_part = 0;
+    if (M <= 0) return 0;
+    if (K % 128 || lda8 % 16 || ldw8 % 16 || N > w_rows) return -1;
+    CUtensorMap ta, tb;
+    if (qt_tmap_i8(&ta, A8, M, K, lda8, T5_BM) || qt_tmap_i8(&tb, W8, w_rows, K, ldw8, T5_BN)) return -2;
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const int tiles = ((N + T5_BN - 1) / T5_BN) * ((M + T5_BM - 1) / T5_BM);
+    const dim3 grid(std::min(tiles, sms));
+    const int parts = 2 * ((N + T5_BN - 1) / T5_BN);
+    if (pmax && parts > pmax_ld) pmax = nullptr;
+    if (pmax && n_part) *n_part = parts;
+    const size_t smem = T8Smem::total;
+#define QT_T8(E)                                                                                              \
+    do {                                                                                                      \
+        auto kfn = k_gemm_tc05_i8<E>;                                                                         \
+        cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                    \
+        return launch_pdl(kfn, grid, dim3(T8_THREADS), smem, st, ta, tb, sa, sw, M, N, K, out, ldo, acc_dbg,  \
+                          pmax, pmax_ld);                                                                     \
+    } while (0)
+    switch (epi) {
+        case QT_EPI_STORE: QT_T8(QT_EPI_STORE);
+        case QT_EPI_RESADD: QT_T8(QT_EPI_RESADD);
+        case QT_EPI_SILU: QT_T8(QT_EPI_SILU);
+        case QT_EPI_SWIGLU: QT_T8(QT_EPI_SWIGLU);
+    }
+#undef QT_T8
     return -1;
 }

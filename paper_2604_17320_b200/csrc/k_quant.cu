@@ -50,7 +50,8 @@ __global__ void __launch_bounds__(1024) k_norm_quant(const TX* __restrict__ x, i
                                                      const float* __restrict__ gain, int M, int D, int d_pad,
                                                      int qmax, int mode, double static_scale,
                                                      uint8_t* __restrict__ codes, int ld_codes,
-                                                     double* __restrict__ scales, float* __restrict__ normed) {
+                                                     double* __restrict__ scales, float* __restrict__ normed,
+                                                     int8_t* __restrict__ codes8, int ld8) {
     __shared__ double red[32];
     pdl_launch_dependents();
     pdl_wait();  // x is produced by the previous kernel
@@ -110,6 +111,7 @@ __global__ void __launch_bounds__(1024) k_norm_quant(const TX* __restrict__ x, i
 #pragma unroll
         for (int e = 0; e < 8; ++e) c[e] = w * 8 + e < D ? q_code_r(v[j][e], s, inv_s, qmax) : 0;
         *reinterpret_cast<uint32_t*>(codes + w4t_offset(row, w * 4, ld_codes)) = pack8(c);  // tiled layout
+        if (codes8) *reinterpret_cast<uint2*>(codes8 + (size_t)row * ld8 + w * 8) = pack8_i8x16(c);
         if (normed && w * 8 < D) {
 #pragma unroll
             for (int e = 0; e < 8; ++e) normed[(size_t)row * D + w * 8 + e] = (float)v[j][e];
@@ -189,7 +191,8 @@ __global__ void __launch_bounds__(256) k_quant_pmax(const float* __restrict__ x,
                                                     const float* __restrict__ pmax, int n_part, int pmax_ld, int M,
                                                     int D, int d_pad, int qmax, int mode, double static_scale,
                                                     uint8_t* __restrict__ codes, int ld_codes,
-                                                    double* __restrict__ scales) {
+                                                    double* __restrict__ scales, int8_t* __restrict__ codes8,
+                                                    int ld8) {
     pdl_launch_dependents();
     pdl_wait();  // x and the partials come from the previous kernel
     const int row = blockIdx.y, lane = threadIdx.x & 31;
@@ -224,6 +227,7 @@ __global__ void __launch_bounds__(256) k_quant_pmax(const float* __restrict__ x,
             c[e] = in ? q_code_r((double)f, s, inv_s, qmax) : 0;
         }
         *reinterpret_cast<uint32_t*>(codes + w4t_offset(row, w * 4, ld_codes)) = pack8(c);
+        if (codes8) *reinterpret_cast<uint2*>(codes8 + (size_t)row * ld8 + w * 8) = pack8_i8x16(c);
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) scales[row] = s;
 }
@@ -594,13 +598,13 @@ int qt_launch_f32_to_f64(const float* a, double* b, long long n, cudaStream_t st
 
 int qt_launch_norm_quant(const void* x, int x_is_f64, int ld_x, const float* gain, int M, int D, int d_pad,
                          int bits, int mode, double static_scale, uint8_t* codes, int ld_codes, double* scales,
-                         float* normed, cudaStream_t st) {
+                         float* normed, int8_t* codes8, int ld8, cudaStream_t st) {
     if (M <= 0) return 0;
     if (D % 8 || d_pad % 8 || ld_x % 4) return -1;
     const int qmax = (1 << (bits - 1)) - 1;
     // opt-in (QT_NQ_CLUSTER=1): rows split over an 8-CTA cluster; not faster at decode sizes
     static const bool use_cl = getenv("QT_NQ_CLUSTER") && atoi(getenv("QT_NQ_CLUSTER")) == 1;
-    if (M <= 64 && !normed && use_cl && d_pad / 8 <= 8 * 128 * 2) {
+    if (M <= 64 && !normed && !codes8 && use_cl && d_pad / 8 <= 8 * 128 * 2) {
         // decode-sized: 8-CTA cluster per row, up to 2 words per thread
         const int G = d_pad / 8 <= 8 * 128 ? 1 : 2;
         if (x_is_f64)
@@ -614,7 +618,7 @@ int qt_launch_norm_quant(const void* x, int x_is_f64, int ld_x, const float* gai
                                                    static_scale, codes, ld_codes, scales, st);
     }
     static const bool nq4 = !(getenv("QT_NQ4") && atoi(getenv("QT_NQ4")) == 0);
-    if (nq4 && M <= 64 && !normed && d_pad / 4 <= 1024 && d_pad / 4 >= 128) {
+    if (nq4 && M <= 64 && !normed && !codes8 && d_pad / 4 <= 1024 && d_pad / 4 >= 128) {
         const int th = (d_pad / 4 + 31) / 32 * 32;
         if (x_is_f64)
             return launch_pdl(k_norm_quant4<double>, dim3(M), dim3(th), 0, st, static_cast<const double*>(x), ld_x,
@@ -628,7 +632,7 @@ int qt_launch_norm_quant(const void* x, int x_is_f64, int ld_x, const float* gai
     if (G > 3) return -1;
 #define QT_NQ(TX, GG)                                                                                        \
     return launch_pdl(k_norm_quant<TX, GG>, dim3(M), dim3(threads), 0, st, static_cast<const TX*>(x), ld_x, \
-                      gain, M, D, d_pad, qmax, mode, static_scale, codes, ld_codes, scales, normed)
+                      gain, M, D, d_pad, qmax, mode, static_scale, codes, ld_codes, scales, normed, codes8, ld8)
     if (x_is_f64) {
         if (G == 1) QT_NQ(double, 1);
         if (G == 2) QT_NQ(double, 2);
@@ -643,7 +647,7 @@ int qt_launch_norm_quant(const void* x, int x_is_f64, int ld_x, const float* gai
 
 int qt_launch_quant_pmax(const float* x, int ld_x, const float* pmax, int n_part, int pmax_ld, int M, int D,
                          int d_pad, int qmax, int mode, double static_scale, uint8_t* codes, int ld_codes,
-                         double* scales, cudaStream_t st) {
+                         double* scales, int8_t* codes8, int ld8, cudaStream_t st) {
     if (M <= 0) return 0;
     if (D % 8 || d_pad % 8 || (mode != 0 && n_part < 1)) return -1;
     const int words = d_pad / 8;
@@ -652,7 +656,8 @@ int qt_launch_quant_pmax(const float* x, int ld_x, const float* pmax, int n_part
     const int wpt = 1;
 #define QT_QP(W)                                                                                                 \
     return launch_pdl(k_quant_pmax<W>, dim3((words + 256 * W - 1) / (256 * W), M), dim3(256), 0, st, x, ld_x,   \
-                      pmax, n_part, pmax_ld, M, D, d_pad, qmax, mode, static_scale, codes, ld_codes, scales)
+                      pmax, n_part, pmax_ld, M, D, d_pad, qmax, mode, static_scale, codes, ld_codes, scales, codes8, \
+                      ld8)
     if (wpt == 1) QT_QP(1);
     if (wpt == 2) QT_QP(2);
     if (wpt == 4) QT_QP(4);

@@ -96,6 +96,17 @@ QT_DEV uint32_t pack8(const int* c) {
     return w;
 }
 
+// 8 codes -> 8 int8 bytes holding 16 x code (the int8-operand GEMM's activation layout)
+QT_DEV uint2 pack8_i8x16(const int* c) {
+    uint32_t lo = 0, hi = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        lo |= (uint32_t)((c[i] << 4) & 0xFF) << (8 * i);
+        hi |= (uint32_t)((c[i + 4] << 4) & 0xFF) << (8 * i);
+    }
+    return make_uint2(lo, hi);
+}
+
 // Unpack 8 int4 nibbles into two int8x4 registers holding 16*code: the
 // nibble lands in the high half of each byte so the byte's sign bit is the
 // nibble's.  lo = even k (nibbles 0,2,4,6), hi = odd k (1,3,5,7).  Products of

@@ -18,7 +18,7 @@ extern "C" {
 int qt_launch_f32_to_f64(const float* a, double* b, long long n, cudaStream_t st);
 int qt_launch_norm_quant(const void* x, int x_is_f64, int ld_x, const float* gain, int M, int D, int d_pad,
                          int bits, int mode, double static_scale, uint8_t* codes, int ld_codes, double* scales,
-                         float* normed, cudaStream_t st);
+                         float* normed, int8_t* codes8, int ld8, cudaStream_t st);
 int qt_launch_rope_kv_append(float* qkv, int ld_qkv, int M, int H, int Hkv, int dh, const int* pos,
                              const int* tok_seq, const int* tok_row, const double* rope, const int* page_table,
                              int max_pages, uint8_t* pool, long long page_bytes, int bits, float* k_dbg,
@@ -47,6 +47,11 @@ int qt_launch_diag_top10(const float* qkv, int ldq, int H, int Hkv, int dh, int 
 int qt_launch_codes_pack(const int8_t* src, int K, int N, const double* s_in, int row_mul, int row_add,
                          uint8_t* codes, int ldc, double* scales, cudaStream_t st);
 // out: double* for QT_EPI_RESADD (the fp64 residual stream), float* otherwise
+// int8-operand tcgen05 GEMM (operands 16 x code, k natural order, row-major; TMA SW128)
+int qt_launch_w4a4_tc05_i8(int epi, const int8_t* A8, int lda8, const double* sa, const int8_t* W8, int w_rows,
+                           int ldw8, const double* sw, int M, int N, int K, void* out, int ldo, int* acc_dbg,
+                           float* pmax, int pmax_ld, int* n_part, cudaStream_t st);
+int qt_launch_w4t_to_i8(const uint8_t* tiled, int rows_pad, int K, int8_t* out, cudaStream_t st);
 int qt_launch_w4a4_mma_ex(int epi, const uint8_t* A, int lda, const double* sa, const uint8_t* W, int ldw,
                           const double* sw, int M, int N, int K, void* out, int ldo, int* acc_dbg, float* pmax,
                           int pmax_ld, int* n_part, cudaStream_t st);
@@ -57,7 +62,7 @@ int qt_launch_w4a4_tc05_ex(int epi, const uint8_t* A, int lda, const double* sa,
 // (pmax[m * pmax_ld + p], p < n_part): no row reduction; mode 0 = static scale
 int qt_launch_quant_pmax(const float* x, int ld_x, const float* pmax, int n_part, int pmax_ld, int M, int D,
                          int d_pad, int qmax, int mode, double static_scale, uint8_t* codes, int ld_codes,
-                         double* scales, cudaStream_t st);
+                         double* scales, int8_t* codes8, int ld8, cudaStream_t st);
 int qt_launch_w4a4_mma(int epi, const uint8_t* A, int lda, const double* sa, const uint8_t* W, int ldw,
                        const double* sw, int M, int N, int K, void* out, int ldo, int* acc_dbg, cudaStream_t st);
 // ws (nullable): int32 split-K workspace of qt_tc05_splitk(M, N, K) * M * N entries; with ws the

@@ -216,6 +216,41 @@ def test_w4a4_gemm_splitk_epilogues(torch_cuda, epi):
     np.testing.assert_allclose(out.cpu().numpy(), exp, **tol)
 
 
+@pytest.mark.parametrize("epi", [Q.EPI_STORE, Q.EPI_RESADD, Q.EPI_SILU, Q.EPI_SWIGLU])
+@pytest.mark.parametrize("M,N,K", [(300, 640, 1024), (129, 256, 512), (1000, 1536, 384), (64, 4096, 256)])
+def test_w4a4_gemm_int8_operands(torch_cuda, epi, M, N, K):
+    """impl 3: the int8-operand tcgen05 GEMM (TMA SWIZZLE_128B tensor loads, no converter warps):
+    int32 accumulators bit-exact, epilogues as the other paths; ragged M and N tiles."""
+    torch = torch_cuda
+    rng = np.random.default_rng(1000 * epi + M)
+    a = rng.integers(-7, 8, size=(M, K))
+    w = rng.integers(-7, 8, size=(N, K))
+    sa = rng.uniform(0.01, 0.5, M)
+    sw = rng.uniform(0.001, 0.01, N)
+    acc_exp = a.astype(np.int64) @ w.T.astype(np.int64)
+    y = acc_exp * (sa[:, None] * sw[None, :])
+    if epi == Q.EPI_SWIGLU:
+        out = torch.zeros((M, N // 2), dtype=torch.float32, device="cuda")
+        g, u = y[:, 0::2], y[:, 1::2]
+        exp, tol = g / (1 + np.exp(-g)) * u, dict(rtol=1e-5, atol=1e-6)
+    elif epi == Q.EPI_SILU:
+        out = torch.zeros((M, N), dtype=torch.float32, device="cuda")
+        exp, tol = y / (1 + np.exp(-y)), dict(rtol=1e-5, atol=1e-6)
+    elif epi == Q.EPI_RESADD:
+        base = rng.standard_normal((M, N))
+        out = torch.from_numpy(base.copy()).cuda()
+        exp, tol = base + y, dict(rtol=1e-14, atol=1e-14)
+    else:
+        out = torch.zeros((M, N), dtype=torch.float32, device="cuda")
+        exp, tol = y, dict(rtol=2e-7, atol=1e-7)
+    acc = torch.zeros((M, N), dtype=torch.int32, device="cuda")
+    Q.w4a4_gemm(epi, torch.from_numpy(_tiled(a)).cuda(), torch.from_numpy(sa).cuda(),
+                torch.from_numpy(_tiled(w, 128)).cuda(), torch.from_numpy(sw).cuda(), M, N, K, out, acc, impl=3)
+    torch.cuda.synchronize()
+    assert np.array_equal(acc.cpu().numpy(), acc_exp)
+    np.testing.assert_allclose(out.cpu().numpy(), exp, **tol)
+
+
 @pytest.mark.parametrize("M", [17, 24, 32, 40, 64])
 def test_w4a4_gemv_wide_batches_int32_exact(torch_cuda, M):
     """Decode batches of 17..64 tokens: the weight-streaming GEMV with B fragments read from the
