@@ -253,6 +253,8 @@ struct qt_engine {
     float* part_ml = nullptr;
     float* part_o = nullptr;
     int dec_splits = 1, dec_pps = 1;
+    std::vector<int> dec_pages;  // decode-attention page CTAs per layer
+    const bool per_layer_pages = !(std::getenv("QT_DEC_PAGES") && std::atoi(std::getenv("QT_DEC_PAGES")) == 0);
     cudaGraphExec_t graph = nullptr;
     bool graph_ok = false;
     int decode_steps = 0;
@@ -1454,13 +1456,17 @@ struct qt_engine {
         h_off = off;
         h_vis = cur_v;
         h_pos = pos_host;
-        // decode attention split plan over the largest per-layer capacity
+        // decode attention split plan: per layer, the pages its longest sequence can reach over
+        // the decode horizon (pruned layers need fewer page CTAs than the unpruned ones)
         int maxp = 1;
+        dec_pages.assign(L, 1);
         for (int l = 0; l < L; ++l)
             for (int b = 0; b < B; ++b) {
                 const int cap = h_kvlen[(size_t)l * B + b] + max_decode;
-                maxp = std::max(maxp, (cap + qt::kPage - 1) / qt::kPage);
+                dec_pages[l] = std::max(dec_pages[l], (cap + qt::kPage - 1) / qt::kPage);
+                maxp = std::max(maxp, dec_pages[l]);
             }
+        if (!per_layer_pages) std::fill(dec_pages.begin(), dec_pages.end(), maxp);
         dec_pps = 1;  // one 64-row page per decode-attention CTA
         dec_splits = maxp;
         ck(cudaStreamSynchronize(st), "prefill");
@@ -1510,7 +1516,7 @@ struct qt_engine {
                 // with the attn_out quantizer
                 if (!(skip_mask & 2))
                     ckl(qt_launch_attn_decode(qkv, n_qkv, H, Hkv, dh, lenl, 1, B, pool, page_bytes, ptl, max_pages,
-                                              dec_splits, part_ml, part_o, nullptr, d, codes, codes_rows, ascale,
+                                              dec_pages[l], part_ml, part_o, nullptr, d, codes, codes_rows, ascale,
                                               cfg.act_mode, cfg.act_mode == 0 ? act[4 * l + 1] : 0.0, kd_pad, 4,
                                               rope_fused ? rope : nullptr, rope_fused ? next_pos : nullptr,
                                               attn_last ? dec_cnt : nullptr, attn, dec_hmax, st),
