@@ -36,12 +36,12 @@ QT_DEV const uint8_t* page_base(const uint8_t* pool, long long page_bytes, const
     return pool + (long long)pt[b * max_pages + j / kPage] * page_bytes;
 }
 
-// Load one 64-key tile of K (row layout [key][dh] fp16 codes) and V
-// (transposed [dh][key] fp16 codes) plus scales into shared memory.
+// Load one 64-key tile of K and V (both row layout [key][dh] fp16 codes, row
+// stride DH + 8) plus scales into shared memory.
 template <int DH>
 QT_DEV void load_kv_tile(const uint8_t* page, int Hkv, int kh, int nkeys, __half* Ks, __half* Vt, float* ks,
                          float* vs, bool need_v) {
-    constexpr int KLD = DH + 8, VLD = AT_K + 8;
+    constexpr int KLD = DH + 8;
     const size_t cb = (size_t)Hkv * kPage * (DH / 2);
     const uint8_t* kc = page + (size_t)kh * kPage * (DH / 2);
     const uint8_t* vc = page + cb + (size_t)kh * kPage * (DH / 2);
@@ -59,16 +59,14 @@ QT_DEV void load_kv_tile(const uint8_t* page, int Hkv, int kh, int nkeys, __half
 #pragma unroll
             for (int bb = 0; bb < 4; ++bb) dst[q * 4 + bb] = nib2_to_h2((word >> (8 * bb)) & 0xFF);
         }
-        if (need_v) {
+        if (need_v) {  // row-major like K; the PV MMA reads it transposed with ldmatrix.trans
             uint4 v = row < nkeys ? *reinterpret_cast<const uint4*>(vc + (size_t)c * 16) : make_uint4(0, 0, 0, 0);
+            uint32_t* vd = reinterpret_cast<uint32_t*>(Vt + row * KLD + col);
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 uint32_t word = (&v.x)[q];
 #pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    const int ch = col + q * 8 + e;
-                    Vt[ch * VLD + row] = __int2half_rn(nib(word, e));
-                }
+                for (int bb = 0; bb < 4; ++bb) vd[q * 4 + bb] = nib2_to_h2((word >> (8 * bb)) & 0xFF);
             }
         }
     }
@@ -125,9 +123,9 @@ __global__ void __launch_bounds__(128, 3) k_attn_prefill(const float* __restrict
                                                       const int* __restrict__ pt, int max_pages, float inv_sqrt,
                                                       float* __restrict__ out, int ldo, float2* __restrict__ ml,
                                                       float* __restrict__ pmax, int pmax_ld) {
-    constexpr int KLD = DH + 8, VLD = AT_K + 8;
+    constexpr int KLD = DH + 8;
     __shared__ __align__(16) __half Ks[AT_K * KLD];
-    __shared__ __align__(16) __half Vt[DH * VLD];
+    __shared__ __align__(16) __half Vt[AT_K * KLD];  // V, row layout (read with ldmatrix.trans)
     __shared__ float ks[AT_K], vs[AT_K];
     const int b = blockIdx.z, h = blockIdx.y;
     const int S = seq_len[b], V = vis[b];
@@ -221,9 +219,12 @@ __global__ void __launch_bounds__(128, 3) k_attn_prefill(const float* __restrict
 #pragma unroll
             for (int u = 0; u < AT_K / 16; ++u) {
                 uint32_t bb[2];
-                const __half* vr = Vt + (t * 8 + g) * VLD + u * 16 + 2 * tig;
-                bb[0] = *reinterpret_cast<const uint32_t*>(vr);
-                bb[1] = *reinterpret_cast<const uint32_t*>(vr + 8);
+                // B fragment (keys u*16.., channels t*8..) of row-major V: 8x8 halves of rows
+                // u*16 + lane (lanes 0..15), transposed on load
+                const __half* vr = Vt + (u * 16 + (lane & 15)) * KLD + t * 8;
+                asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0, %1}, [%2];\n"
+                             : "=r"(bb[0]), "=r"(bb[1])
+                             : "r"(smem_u32(vr)));
                 mma_f16_16816(o[t], ph[u], bb);
                 mma_f16_16816(o[t], pl[u], bb);
             }
