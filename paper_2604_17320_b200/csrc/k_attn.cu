@@ -76,6 +76,55 @@ QT_DEV void load_kv_tile(const uint8_t* page, int Hkv, int kh, int nkeys, __half
     }
 }
 
+// Raw int4 tile of one page for kv head kh: K codes [AT_K][DH/2], V codes, K and V
+// scales -- issued as cp.async 16-byte copies (rows >= nkeys zero-filled), no registers.
+template <int DH>
+QT_DEV void load_kv_raw_async(const uint8_t* page, int Hkv, int kh, int nkeys, uint8_t* raw) {
+    constexpr int CB = AT_K * (DH / 2);  // code bytes per matrix
+    const size_t cb = (size_t)Hkv * kPage * (DH / 2);
+    const uint8_t* kc = page + (size_t)kh * kPage * (DH / 2);
+    const uint8_t* vc = page + cb + (size_t)kh * kPage * (DH / 2);
+    const uint8_t* ksc = page + 2 * cb + (size_t)kh * kPage * 4;
+    const uint8_t* vsc = page + 2 * cb + ((size_t)Hkv * kPage + kh * kPage) * 4;
+    for (int c = threadIdx.x; c < CB / 16; c += blockDim.x) {
+        const bool ok = c / (DH / 32) < nkeys;
+        cp_async16(raw + c * 16, kc + (size_t)c * 16, ok);
+        cp_async16(raw + CB + c * 16, vc + (size_t)c * 16, ok);
+    }
+    for (int c = threadIdx.x; c < 2 * (AT_K * 4 / 16); c += blockDim.x) {  // 16 chunks of 4 scales each
+        const int m = c / (AT_K * 4 / 16), q = c % (AT_K * 4 / 16);
+        cp_async16(raw + 2 * CB + c * 16, (m ? vsc : ksc) + q * 16, q * 4 < nkeys);
+    }
+    cp_async_commit();
+}
+
+// Dequantise the raw tile (smem) into the fp16 K / V tiles and the scale arrays.
+template <int DH>
+QT_DEV void dequant_kv_raw(const uint8_t* raw, int nkeys, __half* Ks, __half* Vt, float* ks, float* vs) {
+    constexpr int KLD = DH + 8;
+    constexpr int CB = AT_K * (DH / 2);
+    for (int c = threadIdx.x; c < CB / 16; c += blockDim.x) {
+        const int row = c / (DH / 32), col = (c % (DH / 32)) * 32;
+        const uint4 w = *reinterpret_cast<const uint4*>(raw + c * 16);
+        const uint4 v = *reinterpret_cast<const uint4*>(raw + CB + c * 16);
+        uint32_t* kd = reinterpret_cast<uint32_t*>(Ks + row * KLD + col);
+        uint32_t* vd = reinterpret_cast<uint32_t*>(Vt + row * KLD + col);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+#pragma unroll
+            for (int bb = 0; bb < 4; ++bb) {
+                kd[q * 4 + bb] = nib2_to_h2(((&w.x)[q] >> (8 * bb)) & 0xFF);
+                vd[q * 4 + bb] = nib2_to_h2(((&v.x)[q] >> (8 * bb)) & 0xFF);
+            }
+        }
+    }
+    const float* sc = reinterpret_cast<const float*>(raw + 2 * CB);
+    for (int r = threadIdx.x; r < AT_K; r += blockDim.x) {
+        ks[r] = r < nkeys ? sc[r] : 0.f;
+        vs[r] = r < nkeys ? sc[AT_K + r] : 0.f;
+    }
+}
+
 // Q fragments (hi/lo) for 16 query rows of one head: qf[s][0..3] hi, ql lo.
 template <int DH>
 QT_DEV void load_q_frags(const float* qkv, int ldq, int tok0, int rows_valid, int h, uint32_t (*qh)[4],
@@ -127,6 +176,7 @@ __global__ void __launch_bounds__(128, 3) k_attn_prefill(const float* __restrict
     __shared__ __align__(16) __half Ks[AT_K * KLD];
     __shared__ __align__(16) __half Vt[AT_K * KLD];  // V, row layout (read with ldmatrix.trans)
     __shared__ float ks[AT_K], vs[AT_K];
+    __shared__ __align__(16) uint8_t raw[AT_K * DH + 2 * AT_K * 4];  // next tile's int4 codes + scales
     const int b = blockIdx.z, h = blockIdx.y;
     const int S = seq_len[b], V = vis[b];
     const int q0 = blockIdx.x * AT_Q;
@@ -147,11 +197,16 @@ __global__ void __launch_bounds__(128, 3) k_attn_prefill(const float* __restrict
     const int qi[2] = {wq0 + g, wq0 + g + 8};
 
     const int kend = max(V, min(S, q0 + AT_Q));
+    // two-stage: the raw int4 codes of tile k0 + AT_K stream in (cp.async) while tile k0 computes
+    load_kv_raw_async<DH>(page_base(pool, page_bytes, pt, max_pages, b, 0), Hkv, kh, min(AT_K, S), raw);
     for (int k0 = 0; k0 < kend; k0 += AT_K) {
-        __syncthreads();
-        const uint8_t* page = page_base(pool, page_bytes, pt, max_pages, b, k0);
-        load_kv_tile<DH>(page, Hkv, kh, min(AT_K, S - k0), Ks, Vt, ks, vs, true);
-        __syncthreads();
+        cp_async_wait<0>();
+        __syncthreads();  // raw holds tile k0; every warp is done with tile k0 - AT_K
+        dequant_kv_raw<DH>(raw, min(AT_K, S - k0), Ks, Vt, ks, vs);
+        __syncthreads();  // raw free, tile k0 ready
+        if (k0 + AT_K < kend)
+            load_kv_raw_async<DH>(page_base(pool, page_bytes, pt, max_pages, b, k0 + AT_K), Hkv, kh,
+                                  min(AT_K, S - k0 - AT_K), raw);
         // scores in log2 units: s2 = q.k * (scale_k / sqrt(dh) * log2 e), p = 2^(s2 - m2)
         // warp-uniform tile classification against the reference mask (model.cpp:35-44):
         // `none` -> no (query, key) pair of this warp's 16 rows x 64 keys is allowed;
