@@ -128,7 +128,8 @@ __global__ void __launch_bounds__(1024) k_norm_quant4(const TX* __restrict__ x, 
                                                       const float* __restrict__ gain, int M, int D, int d_pad,
                                                       int qmax, int mode, double static_scale,
                                                       uint8_t* __restrict__ codes, int ld_codes,
-                                                      double* __restrict__ scales) {
+                                                      double* __restrict__ scales, int8_t* __restrict__ codes8,
+                                                      int ld8) {
     __shared__ double red[32];
     pdl_launch_dependents();
     pdl_wait();  // x is produced by the previous kernel
@@ -172,10 +173,15 @@ __global__ void __launch_bounds__(1024) k_norm_quant4(const TX* __restrict__ x, 
     }
     if (base < d_pad) {
         const double inv_s = 1.0 / s;
-        uint32_t w = 0;
+        uint32_t w = 0, w8 = 0;
 #pragma unroll
-        for (int e = 0; e < 4; ++e) w |= (uint32_t)((in ? q_code_r(v[e], s, inv_s, qmax) : 0) & 0xF) << (4 * e);
+        for (int e = 0; e < 4; ++e) {
+            const int c = in ? q_code_r(v[e], s, inv_s, qmax) : 0;
+            w |= (uint32_t)(c & 0xF) << (4 * e);
+            w8 |= (uint32_t)((c << 4) & 0xFF) << (8 * e);
+        }
         *reinterpret_cast<uint16_t*>(codes + w4t_offset(row, base / 2, ld_codes)) = (uint16_t)w;
+        if (codes8) *reinterpret_cast<uint32_t*>(codes8 + (size_t)row * ld8 + base) = w8;
     }
     if (threadIdx.x == 0) scales[row] = s;
 }
@@ -207,11 +213,16 @@ __global__ void __launch_bounds__(256) k_quant_pmax(const float* __restrict__ x,
             v[j][1] = p[1];
         }
     double s = static_scale;
-    if (mode != 0) {
-        float mx = 0.f;
-        for (int p = lane; p < n_part; p += 32) mx = fmaxf(mx, pmax[(size_t)row * pmax_ld + p]);
-        mx = warp_max(mx);
-        s = q_scale((double)mx, qmax);
+    if (mode != 0) {  // warp 0 folds the row's partials (loads above already in flight); smem broadcast
+        __shared__ float s_mx;
+        if (threadIdx.x < 32) {
+            float mx = 0.f;
+            for (int p = lane; p < n_part; p += 32) mx = fmaxf(mx, pmax[(size_t)row * pmax_ld + p]);
+            mx = warp_max(mx);
+            if (lane == 0) s_mx = mx;
+        }
+        __syncthreads();
+        s = q_scale((double)s_mx, qmax);
     }
     const double inv_s = 1.0 / s;
 #pragma unroll
@@ -618,13 +629,14 @@ int qt_launch_norm_quant(const void* x, int x_is_f64, int ld_x, const float* gai
                                                    static_scale, codes, ld_codes, scales, st);
     }
     static const bool nq4 = !(getenv("QT_NQ4") && atoi(getenv("QT_NQ4")) == 0);
-    if (nq4 && M <= 64 && !normed && !codes8 && d_pad / 4 <= 1024 && d_pad / 4 >= 128) {
+    static const int nq4_max_m = getenv("QT_NQ4_M") ? atoi(getenv("QT_NQ4_M")) : 64;
+    if (nq4 && M <= nq4_max_m && !normed && d_pad / 4 <= 1024 && d_pad / 4 >= 128) {
         const int th = (d_pad / 4 + 31) / 32 * 32;
         if (x_is_f64)
             return launch_pdl(k_norm_quant4<double>, dim3(M), dim3(th), 0, st, static_cast<const double*>(x), ld_x,
-                              gain, M, D, d_pad, qmax, mode, static_scale, codes, ld_codes, scales);
+                              gain, M, D, d_pad, qmax, mode, static_scale, codes, ld_codes, scales, codes8, ld8);
         return launch_pdl(k_norm_quant4<float>, dim3(M), dim3(th), 0, st, static_cast<const float*>(x), ld_x, gain,
-                          M, D, d_pad, qmax, mode, static_scale, codes, ld_codes, scales);
+                          M, D, d_pad, qmax, mode, static_scale, codes, ld_codes, scales, codes8, ld8);
     }
     const int words = d_pad / 8;
     int threads = words <= 256 ? 256 : (words <= 512 ? 512 : 1024);
