@@ -136,11 +136,14 @@ QT_DEV void store_converted(const uint4 w, uint8_t* i8, int row, int q) {
 
 // Epilogue warps (T5_EWN of them, first warp ew0): warp & 3 = TMEM lane quarter (32 rows),
 // (warp - ew0) / 4 = column half.  Shared by the packed-int4 and the int8-operand kernels.
+// Work unit u (u0, u0 + ustep, ... < units): tile t = u % tiles, k slice u / tiles; the
+// tile's M tile is (t % mtp) * cl + rank (cl = cluster size along M) and its N tile t / mtp.
 template <int EPI>
-QT_DEV void t5_epilogue(int ew0, int warp, int lane, uint32_t tmem, int units, int tiles, int mt_n, int M, int N,
-                        const double* __restrict__ sa, const double* __restrict__ sw, double* sws,
-                        void* __restrict__ out, int ldo, int* __restrict__ acc_dbg, int ksplit, int* __restrict__ ws,
-                        float* __restrict__ pmax, int pmax_ld, uint64_t* tfull, uint64_t* tempty) {
+QT_DEV void t5_epilogue_g(int ew0, int warp, int lane, uint32_t tmem, int u0, int ustep, int units, int tiles,
+                          int mtp, int cl, int rank, int M, int N, const double* __restrict__ sa,
+                          const double* __restrict__ sw, double* sws, void* __restrict__ out, int ldo,
+                          int* __restrict__ acc_dbg, int ksplit, int* __restrict__ ws, float* __restrict__ pmax,
+                          int pmax_ld, uint64_t* tfull, uint64_t* tempty) {
     // ---------------- epilogue: 8 warps; warp & 3 = TMEM lane quarter (32 rows), and
     // (warp - ew0) / 4 = column half -- the per-element fp64 scale math is split 2 ways
     pdl_wait();  // scales / residual come from upstream kernels
@@ -149,10 +152,10 @@ QT_DEV void t5_epilogue(int ew0, int warp, int lane, uint32_t tmem, int units, i
     const int et = threadIdx.x - ew0 * 32;
     const int jh = ((warp - ew0) >> 2) * (T5_BN / 64);  // first 32-column chunk of this half
     int tl = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x, ++tl) {
+    for (int u = u0; u < units; u += ustep, ++tl) {
         const int t = u % tiles, sl = u / tiles;
         const int acc = tl % T5_ACC;
-        const int m0 = (t % mt_n) * T5_BM, n0 = (t / mt_n) * T5_BN;
+        const int m0 = ((t % mtp) * cl + rank) * T5_BM, n0 = (t / mtp) * T5_BN;
         double* swt = sws + acc * T5_BN;
         for (int i = et; i < T5_BN; i += T5_ET) swt[i] = n0 + i < N ? sw[n0 + i] : 0.0;
         if (EPI == QT_EPI_RESADD && ksplit == 1) {
@@ -211,9 +214,27 @@ QT_DEV void t5_epilogue(int ew0, int warp, int lane, uint32_t tmem, int units, i
             }
         }
         // partial row max for the next site's dynamic quantizer: slot (n tile, column half)
-        if (pmax && ksplit == 1 && m < M) pmax[(size_t)m * pmax_ld + (t / mt_n) * 2 + jh / (T5_BN / 64)] = mx;
+        if (pmax && ksplit == 1 && m < M) pmax[(size_t)m * pmax_ld + (t / mtp) * 2 + jh / (T5_BN / 64)] = mx;
         asm volatile("bar.sync 2, %0;\n" ::"n"(T5_ET) : "memory");  // swt reuse
     }
+}
+
+template <int EPI>
+QT_DEV void t5_epilogue(int ew0, int warp, int lane, uint32_t tmem, int units, int tiles, int mt_n, int M, int N,
+                        const double* __restrict__ sa, const double* __restrict__ sw, double* sws,
+                        void* __restrict__ out, int ldo, int* __restrict__ acc_dbg, int ksplit, int* __restrict__ ws,
+                        float* __restrict__ pmax, int pmax_ld, uint64_t* tfull, uint64_t* tempty) {
+    t5_epilogue_g<EPI>(ew0, warp, lane, tmem, blockIdx.x, gridDim.x, units, tiles, mt_n, 1, 0, M, N, sa, sw, sws, out,
+                       ldo, acc_dbg, ksplit, ws, pmax, pmax_ld, tfull, tempty);
+}
+
+template <int EPI, int CL>
+QT_DEV void t5_epilogue_cl(int ew0, int warp, int lane, uint32_t tmem, int tiles, int mtp, int rank, int cid, int ncl,
+                           int mt_n, int M, int N, const double* __restrict__ sa, const double* __restrict__ sw,
+                           double* sws, void* __restrict__ out, int ldo, int* __restrict__ acc_dbg,
+                           float* __restrict__ pmax, int pmax_ld, uint64_t* tfull, uint64_t* tempty) {
+    t5_epilogue_g<EPI>(ew0, warp, lane, tmem, cid, ncl, tiles, tiles, mtp, CL, rank, M, N, sa, sw, sws, out, ldo,
+                       acc_dbg, 1, nullptr, pmax, pmax_ld, tfull, tempty);
 }
 
 template <int EPI>
@@ -406,7 +427,34 @@ QT_DEV void tma_load_2d(void* dst, const CUtensorMap* tm, int c0, int c1, uint64
         : "memory");
 }
 
-template <int EPI>
+// TMA 2D load multicast to the CTAs of ctaMask (same smem offset and mbarrier offset in each)
+QT_DEV void tma_load_2d_mc(void* dst, const CUtensorMap* tm, int c0, int c1, uint64_t* bar, uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster "
+        "[%0], [%1, {%2, %3}], [%4], %5;\n" ::"r"(smem_u32(dst)),
+        "l"(tm), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "h"(mask)
+        : "memory");
+}
+
+// tcgen05.commit arriving on the mbarrier at this smem offset in every CTA of ctaMask
+QT_DEV void mma_commit_mc(uint64_t* bar, uint16_t mask) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+                     smem_u32(bar)),
+                 "h"(mask)
+                 : "memory");
+}
+
+QT_DEV uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+    return r;
+}
+
+QT_DEV void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+template <int EPI, int CL>
 __global__ void __launch_bounds__(T8_THREADS, 1) k_gemm_tc05_i8(const __grid_constant__ CUtensorMap tmA,
                                                                  const __grid_constant__ CUtensorMap tmB,
                                                                  const double* __restrict__ sa,
@@ -424,11 +472,16 @@ __global__ void __launch_bounds__(T8_THREADS, 1) k_gemm_tc05_i8(const __grid_con
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int KB = K / 128;
     const int mt_n = (M + T5_BM - 1) / T5_BM, nt_n = (N + T5_BN - 1) / T5_BN;
-    const int tiles = mt_n * nt_n;
+    // CL = 2: a cluster pair takes M tiles (2p, 2p + 1) of one N tile and shares its weight tile:
+    // each CTA loads half of it and multicasts that half to both (halves the per-SM weight ingress)
+    const int mtp = (mt_n + CL - 1) / CL;  // M-tile groups
+    const int tiles = mtp * nt_n;          // work units per cluster
+    const int rank = CL > 1 ? (int)cluster_rank() : 0;
+    const int cid = blockIdx.x / CL, ncl = gridDim.x / CL;
     if (threadIdx.x == 0) {
         for (int s = 0; s < T8_S; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
+            mbar_init(&empty[s], CL);  // every CTA's MMA must release the stage (peer TMA writes into it)
         }
         for (int s = 0; s < T5_ACC; ++s) {
             mbar_init(&tfull[s], 1);
@@ -443,6 +496,7 @@ __global__ void __launch_bounds__(T8_THREADS, 1) k_gemm_tc05_i8(const __grid_con
     }
     tc_fence_before();
     __syncthreads();
+    if constexpr (CL > 1) cluster_sync_all();  // the peer's barriers exist before any multicast targets them
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     if (warp == 0) {
@@ -451,14 +505,18 @@ __global__ void __launch_bounds__(T8_THREADS, 1) k_gemm_tc05_i8(const __grid_con
             asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmB) : "memory");
             pdl_wait();  // activation codes come from the upstream kernel
             int it = 0;
-            for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-                const int m0 = (t % mt_n) * T5_BM, n0 = (t / mt_n) * T5_BN;
+            for (int t = cid; t < tiles; t += ncl) {
+                const int m0 = ((t % mtp) * CL + rank) * T5_BM, n0 = (t / mtp) * T5_BN;
                 for (int kb = 0; kb < KB; ++kb, ++it) {
                     const int s = it % T8_S;
                     if (it >= T8_S) mbar_wait(&empty[s], ((it / T8_S) - 1) & 1);
                     mbar_arrive_expect_tx(&full[s], (uint32_t)(T5_IA + T5_IB));
                     tma_load_2d(smem + T8Smem::ia + (size_t)s * T5_IA, &tmA, kb * 128, m0, &full[s]);
-                    tma_load_2d(smem + T8Smem::ib + (size_t)s * T5_IB, &tmB, kb * 128, n0, &full[s]);
+                    if constexpr (CL > 1)
+                        tma_load_2d_mc(smem + T8Smem::ib + (size_t)s * T5_IB + (size_t)rank * (T5_IB / 2), &tmB,
+                                       kb * 128, n0 + rank * (T5_BN / 2), &full[s], (uint16_t)0x3);
+                    else
+                        tma_load_2d(smem + T8Smem::ib + (size_t)s * T5_IB, &tmB, kb * 128, n0, &full[s]);
                 }
             }
         }
@@ -466,7 +524,7 @@ __global__ void __launch_bounds__(T8_THREADS, 1) k_gemm_tc05_i8(const __grid_con
         if (lane == 0) {
             const uint32_t idesc = t5_idesc();
             int it = 0, tl = 0;
-            for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++tl) {
+            for (int t = cid; t < tiles; t += ncl, ++tl) {
                 const int acc = tl % T5_ACC;
                 if (tl >= T5_ACC) mbar_wait(&tempty[acc], ((tl / T5_ACC) - 1) & 1);
                 tc_fence_after();
@@ -481,18 +539,20 @@ __global__ void __launch_bounds__(T8_THREADS, 1) k_gemm_tc05_i8(const __grid_con
                     for (int k = 0; k < 4; ++k)
                         mma_i8(tacc, umma_desc_sw128(a0 + 32 * k), umma_desc_sw128(b0 + 32 * k), idesc,
                                (kb != 0) || (k != 0));
-                    mma_commit(&empty[s]);
+                    if constexpr (CL > 1) mma_commit_mc(&empty[s], (uint16_t)0x3);
+                    else mma_commit(&empty[s]);
                 }
                 mma_commit(&tfull[acc]);
             }
         }
         __syncwarp();
     } else {
-        t5_epilogue<EPI>(T8_EW0, warp, lane, tmem, tiles, tiles, mt_n, M, N, sa, sw, sws, out, ldo, acc_dbg, 1, nullptr,
-                         pmax, pmax_ld, tfull, tempty);
+        t5_epilogue_cl<EPI, CL>(T8_EW0, warp, lane, tmem, tiles, mtp, rank, cid, ncl, mt_n, M, N, sa, sw, sws, out,
+                                ldo, acc_dbg, pmax, pmax_ld, tfull, tempty);
     }
     tc_fence_before();
     __syncthreads();
+    if constexpr (CL > 1) cluster_sync_all();  // no CTA leaves while its peer may still multicast / commit into it
     if (warp == 1) {
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(T5_ACC * T5_BN));
     }
@@ -648,18 +708,43 @@ extern "C" int qt_launch_w4a4_tc05_i8(int epi, const int8_t* A8, int lda8, const
     if (qt_tmap_i8(&ta, A8, M, K, lda8, T5_BM) || qt_tmap_i8(&tb, W8, w_rows, K, ldw8, T5_BN)) return -2;
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    const int tiles = ((N + T5_BN - 1) / T5_BN) * ((M + T5_BM - 1) / T5_BM);
-    const dim3 grid(std::min(tiles, sms));
-    const int parts = 2 * ((N + T5_BN - 1) / T5_BN);
+    const int mt_n = (M + T5_BM - 1) / T5_BM, nt_n = (N + T5_BN - 1) / T5_BN;
+    // cluster pairs along M share the weight tile (TMA multicast) when there are M tiles to pair
+    static const int cl_env = getenv("QT_I8_CL") ? atoi(getenv("QT_I8_CL")) : 1;  // 2: opt-in, measured slower
+    const int CL = (cl_env == 2 && mt_n >= 2) ? 2 : 1;
+    const int units = ((mt_n + CL - 1) / CL) * nt_n;
+    const dim3 grid(std::min(units, sms / CL) * CL);
+    const int parts = 2 * nt_n;
     if (pmax && parts > pmax_ld) pmax = nullptr;
     if (pmax && n_part) *n_part = parts;
     const size_t smem = T8Smem::total;
-#define QT_T8(E)                                                                                              \
-    do {                                                                                                      \
-        auto kfn = k_gemm_tc05_i8<E>;                                                                         \
-        cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                    \
-        return launch_pdl(kfn, grid, dim3(T8_THREADS), smem, st, ta, tb, sa, sw, M, N, K, out, ldo, acc_dbg,  \
-                          pmax, pmax_ld);                                                                     \
+    if (CL == 2 && qt_tmap_i8(&tb, W8, w_rows, K, ldw8, T5_BN / 2)) return -2;  // half-tile boxes
+#define QT_T8(E)                                                                                                    \
+    do {                                                                                                            \
+        if (CL == 2) {                                                                                              \
+            auto kfn = k_gemm_tc05_i8<E, 2>;                                                                        \
+            cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                      \
+            cudaLaunchConfig_t cfg = {};                                                                            \
+            cfg.gridDim = grid;                                                                                     \
+            cfg.blockDim = dim3(T8_THREADS);                                                                        \
+            cfg.dynamicSmemBytes = smem;                                                                            \
+            cfg.stream = st;                                                                                        \
+            cudaLaunchAttribute at[2];                                                                              \
+            at[0].id = cudaLaunchAttributeClusterDimension;                                                         \
+            at[0].val.clusterDim.x = 2;                                                                             \
+            at[0].val.clusterDim.y = 1;                                                                             \
+            at[0].val.clusterDim.z = 1;                                                                             \
+            at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;                                          \
+            at[1].val.programmaticStreamSerializationAllowed = 1;                                                   \
+            cfg.attrs = at;                                                                                         \
+            cfg.numAttrs = (getenv("QT_NOPDL") || g_pdl_block) ? 1 : 2;                                             \
+            g_pdl_block = false;                                                                                    \
+            return (int)cudaLaunchKernelEx(&cfg, kfn, ta, tb, sa, sw, M, N, K, out, ldo, acc_dbg, pmax, pmax_ld);   \
+        }                                                                                                           \
+        auto kfn = k_gemm_tc05_i8<E, 1>;                                                                            \
+        cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                          \
+        return launch_pdl(kfn, grid, dim3(T8_THREADS), smem, st, ta, tb, sa, sw, M, N, K, out, ldo, acc_dbg, pmax,  \
+                          pmax_ld);                                                                                 \
     } while (0)
     switch (epi) {
         case QT_EPI_STORE: QT_T8(QT_EPI_STORE);
