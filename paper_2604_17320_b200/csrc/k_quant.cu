@@ -640,19 +640,26 @@ int qt_launch_norm_quant(const void* x, int x_is_f64, int ld_x, const float* gai
     }
     const int words = d_pad / 8;
     int threads = words <= 256 ? 256 : (words <= 512 ? 512 : 1024);
+    // token-rich launches: narrower CTAs holding more of the row per thread, so more rows
+    // (and their loads) are in flight per SM (QT_NQ_WIDE_M: the row-count threshold)
+    static const int wide_m = getenv("QT_NQ_WIDE_M") ? atoi(getenv("QT_NQ_WIDE_M")) : 256;
+    static const int wide_t = getenv("QT_NQ_WIDE_T") ? atoi(getenv("QT_NQ_WIDE_T")) : 256;  // 128 (G = 4) spills
+    if (M >= wide_m && (words + wide_t - 1) / wide_t <= 4) threads = wide_t;
     const int G = (words + threads - 1) / threads;
-    if (G > 3) return -1;
+    if (G > 4) return -1;
 #define QT_NQ(TX, GG)                                                                                        \
     return launch_pdl(k_norm_quant<TX, GG>, dim3(M), dim3(threads), 0, st, static_cast<const TX*>(x), ld_x, \
                       gain, M, D, d_pad, qmax, mode, static_scale, codes, ld_codes, scales, normed, codes8, ld8)
     if (x_is_f64) {
         if (G == 1) QT_NQ(double, 1);
         if (G == 2) QT_NQ(double, 2);
-        QT_NQ(double, 3);
+        if (G == 3) QT_NQ(double, 3);
+        QT_NQ(double, 4);
     } else {
         if (G == 1) QT_NQ(float, 1);
         if (G == 2) QT_NQ(float, 2);
-        QT_NQ(float, 3);
+        if (G == 3) QT_NQ(float, 3);
+        QT_NQ(float, 4);
     }
 #undef QT_NQ
 }
