@@ -672,7 +672,8 @@ int qt_launch_quant_pmax(const float* x, int ld_x, const float* pmax, int n_part
     const int words = d_pad / 8;
     // one word per thread: measured faster than whole-row CTAs with 2-8 words per thread
     // (prefill 36.5 vs 36.8 ms) -- more CTAs in flight beat the amortised partial fold
-    const int wpt = 1;
+    static const int wpt_env = getenv("QT_QP_WPT") ? atoi(getenv("QT_QP_WPT")) : 1;
+    const int wpt = M >= 256 ? wpt_env : 1;
 #define QT_QP(W)                                                                                                 \
     return launch_pdl(k_quant_pmax<W>, dim3((words + 256 * W - 1) / (256 * W), M), dim3(256), 0, st, x, ld_x,   \
                       pmax, n_part, pmax_ld, M, D, d_pad, qmax, mode, static_scale, codes, ld_codes, scales, codes8, \
