@@ -414,11 +414,14 @@ __global__ void __launch_bounds__(256) k_rope_kv_append(
 // group issued first (float4 per lane); the RoPE cos/sin of the token's position
 // are read once per lane and reused by every q and k head.  Same arithmetic as
 // k_rope_kv_append.
+#ifndef QT_KVTOK_G
+#define QT_KVTOK_G 4
+#endif
 __global__ void __launch_bounds__(256) k_rope_kv_append_tok(
     float* __restrict__ qkv, int ld_qkv, int M, int H, int Hkv, const int* __restrict__ pos,
     const int* __restrict__ tok_seq, const int* __restrict__ tok_row, const double2* __restrict__ rope,
     const int* __restrict__ page_table, int max_pages, uint8_t* __restrict__ pool, long long page_bytes, int qmax) {
-    constexpr int DH = 128, E = 4, G = 4;
+    constexpr int DH = 128, E = 4, G = QT_KVTOK_G;
     pdl_launch_dependents();
     pdl_wait();
     const int m = blockIdx.x;
