@@ -209,7 +209,8 @@ def run_reference(args, cfg):
               f"tokens/s extrapolated to {cfg['n_layers']} layers (x4/{cfg['n_layers']}); setup {setup_s:.1f}s")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": float(np.mean(secs)) * 1e3,  # one step = the extrapolated 32-layer sample "higher_is_better": True,
+            # one step = the extrapolated 32-layer sample
+            "ms_per_step": float(np.mean(secs)) * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg["workload"], "batch_per_gpu": cfg["batch"],
                        "visual": cfg["visual"], "text": cfg["text"], "decode_steps": cfg["decode"]},
