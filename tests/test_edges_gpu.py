@@ -147,3 +147,24 @@ def test_graph_and_eager_decode_identical(pair):
         h.append(e.decode(x).copy())
     for a, b in zip(g, h):
         assert np.array_equal(a, b)
+
+
+def test_profile_chain_leaves_decode_state(pair):
+    """qt_engine_profile_chain (bench.py's per-class decode timing) replays graph-captured
+    steps with kernel classes left out, then restores cache lengths and positions: the decode
+    that follows is bitwise the one without profiling."""
+    cfg, port, e = pair
+    e.clear_recipe()
+    emb = O.synth_embeddings(40, 128, seed=19).astype(np.float32)
+    xs = [O.synth_embeddings(1, 128, seed=80 + i).astype(np.float32) for i in range(3)]
+    e.prefill(emb, [30], [10])
+    g = [e.decode(x).copy() for x in xs]
+    e.prefill(emb, [30], [10])
+    h = [e.decode(xs[0]).copy()]
+    for mask in (0, 1 | 4 | 8, 15):
+        assert e.profile_chain(mask, reps=3) > 0.0
+    h += [e.decode(x).copy() for x in xs[1:]]
+    for a, b in zip(g, h):
+        assert np.array_equal(a, b)
+    v, t, pos = e.layout(0)
+    assert (v, t) == (30, 13) and pos[-1] == 42
