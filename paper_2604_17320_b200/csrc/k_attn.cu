@@ -706,13 +706,18 @@ __global__ void __launch_bounds__(1024) k_attn_merge_quant(const float* __restri
         for (int p = lane; p < npg; p += 32) M = fmaxf(M, part_ml[(base + p) * 2]);
         M = warp_max(M);
         float L = 0.f;
+        // branch-free so the loads of consecutive pages overlap; an empty page (l = 0, o = 0,
+        // m = -1e30) contributes exactly 0, as the skipped iteration did
+#pragma unroll 4
         for (int p = 0; p < npg; ++p) {
-            const float lp = part_ml[(base + p) * 2 + 1];
-            if (lp == 0.f) continue;
-            const float a = expf(part_ml[(base + p) * 2] - M);
-            L += lp * a;
+            const float2 mlp = *reinterpret_cast<const float2*>(part_ml + (base + p) * 2);
+            float ov[CPL];
 #pragma unroll
-            for (int c = 0; c < CPL; ++c) o[hh][c] += part_o[(base + p) * DH + lane * CPL + c] * a;
+            for (int c = 0; c < CPL; ++c) ov[c] = part_o[(base + p) * DH + lane * CPL + c];
+            const float a = mlp.y == 0.f ? 0.f : expf(mlp.x - M);
+            L += mlp.y * a;
+#pragma unroll
+            for (int c = 0; c < CPL; ++c) o[hh][c] += ov[c] * a;
         }
         const float il = 1.f / L;
 #pragma unroll
