@@ -171,7 +171,10 @@ static const int qt_gemv_l2_rows_host = getenv("QT_GEMV_L2") ? atoi(getenv("QT_G
 #define QT_GEMV_MINB 2  // 3 spills (80 regs) and measured slower
 #endif
 static const int qt_gemv_ctas = getenv("QT_GEMV_CTAS") ? atoi(getenv("QT_GEMV_CTAS")) : QT_GEMV_MINB;
-template <int NT, int EPI>
+// AREG (NT = 1, K <= 4096: one batch per row block): each lane's activation fragments for its
+// k slice are loaded once into registers after the dependency wait -- no smem staging, no
+// block barrier before the first MMA.
+template <int NT, int EPI, bool AREG = false>
 __global__ void __launch_bounds__(256, NT <= 2 ? QT_GEMV_MINB : 1) k_gemv_reg(const uint8_t* __restrict__ A, int lda, const double* __restrict__ sa,
                                                   const uint8_t* __restrict__ W, int ldw, const double* __restrict__ sw,
                                                   int M, int N, int K, void* __restrict__ out, int ldo,
@@ -179,7 +182,7 @@ __global__ void __launch_bounds__(256, NT <= 2 ? QT_GEMV_MINB : 1) k_gemv_reg(co
                                                   const uint8_t* __restrict__ pf, long long pf_bytes,
                                                   float* __restrict__ pmax, int pmax_ld) {
     constexpr int TOK = 8 * NT;
-    constexpr bool ASM = NT <= 2;     // activation codes staged in smem
+    constexpr bool ASM = NT <= 2 && !AREG;  // activation codes staged in smem
     constexpr int U = NT <= 2 ? 4 : 2;
     extern __shared__ __align__(128) uint8_t smem[];
     const int kb = K / 2;
@@ -232,6 +235,14 @@ __global__ void __launch_bounds__(256, NT <= 2 ? QT_GEMV_MINB : 1) k_gemv_reg(co
         }
     }
     pdl_wait();
+    uint4 bA[AREG ? U : 1];
+    if constexpr (AREG) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int c = ch0 + u;
+            bA[u] = c < ch1 ? ldg_nc_v4(A + w4t_offset(g, c * 64 + tig * 16, lda)) : make_uint4(0, 0, 0, 0);
+        }
+    }
     if (ASM) {
         for (int c = tid; c < TOK * (kb / 16); c += 256) {
             int r = c / (kb / 16), q = c % (kb / 16);
@@ -261,7 +272,8 @@ __global__ void __launch_bounds__(256, NT <= 2 ? QT_GEMV_MINB : 1) k_gemv_reg(co
             uint4 bv[NT];
 #pragma unroll
             for (int j = 0; j < NT; ++j) {
-                if (ASM) bv[j] = *reinterpret_cast<const uint4*>(As + (j * 8 + g) * ldsA + c * 64 + tig * 16);
+                if constexpr (AREG) bv[j] = bA[u];  // nbat == 1: batch u is k tile ch0 + u
+                else if (ASM) bv[j] = *reinterpret_cast<const uint4*>(As + (j * 8 + g) * ldsA + c * 64 + tig * 16);
                 else bv[j] = ldg_nc_v4(A + w4t_offset(j * 8 + g, c * 64 + tig * 16, lda));  // rows >= M: discarded
             }
 #pragma unroll
@@ -378,6 +390,14 @@ int launch_gemm(const uint8_t* A, int lda, const double* sa, const uint8_t* W, i
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
         const dim3 grid(std::min(n_rb, qt_gemv_ctas * sms));
         want_pmax((int)grid.x);
+        static const bool areg_on = !(getenv("QT_GEMV_AREG") && atoi(getenv("QT_GEMV_AREG")) == 0);
+        if (TOK == 8 && areg_on && (K / 128 + 7) / 8 <= 4) {
+            const size_t smem2 = (size_t)8 * 16 * TOK * 4;  // split-K reduction buffer only
+            auto kfn = k_gemv_reg<1, EPI, true>;
+            cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
+            return launch_pdl(kfn, grid, dim3(256), smem2, st, A, lda, sa, W, ldw, sw, M, N, K, out, ldo, acc_dbg,
+                              qt_gemv_l2_rows_host, pf, pf_bytes, pm, pmax_ld);
+        }
         if (TOK == 8) {
             auto kfn = k_gemv_reg<1, EPI>;
             cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
