@@ -243,15 +243,16 @@ __global__ void __launch_bounds__(256, NT <= 2 ? QT_GEMV_MINB : 1) k_gemv_reg(co
             bA[u] = c < ch1 ? ldg_nc_v4(A + w4t_offset(g, c * 64 + tig * 16, lda)) : make_uint4(0, 0, 0, 0);
         }
     }
-    if (ASM) {
-        for (int c = tid; c < TOK * (kb / 16); c += 256) {
-            int r = c / (kb / 16), q = c % (kb / 16);
-            bool ok = r < M;
+    if (ASM) {  // each warp stages only its own k slice of the token codes: no block barrier
+        const int q0 = ch0 * 4, nq = (ch1 - ch0) * 4;  // 16-byte chunks of the slice
+        for (int c = lane; c < TOK * nq; c += 32) {
+            const int r = c / nq, q = q0 + c % nq;
+            const bool ok = r < M;
             cp_async16(As + r * ldsA + q * 16, A + w4t_offset(ok ? r : 0, q * 16, lda), ok);
         }
         cp_async_commit();
         cp_async_wait<0>();
-        __syncthreads();
+        __syncwarp();
     }
     pdl_launch_dependents();
     int acc[NT][4];
