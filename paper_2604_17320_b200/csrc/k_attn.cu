@@ -504,7 +504,12 @@ __global__ void __launch_bounds__(128) k_attn_decode(const float* __restrict__ q
     constexpr int CPL = DH / 4;  // channels per lane
     constexpr int R = 2;         // rows per lane
     pdl_launch_dependents();
-    pdl_wait();
+    // Without the fused append (rope == null) every cached row but the newest (len - 1, written
+    // by the K/V append kernel just before) is final since earlier steps, as are kv_len and the
+    // page table: those loads are issued before the dependency wait and overlap the upstream
+    // kernel; q and the newest row are read after it (the row through L2, not the .nc path,
+    // since its 128-byte line may have been cached with the row before it).
+    if (rope) pdl_wait();
     const int b = blockIdx.z, h = blockIdx.y, pg = blockIdx.x, npg = gridDim.x;
     const int kh = h / (H / Hkv);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -552,6 +557,7 @@ __global__ void __launch_bounds__(128) k_attn_decode(const float* __restrict__ q
     }
     if (rope) __syncthreads();  // the appended row is visible to the block's loads below
     if (r0 >= len) {
+        if (!rope) pdl_wait();  // part buffers are still read by the previous layer's merge
         if (threadIdx.x < DH) part_o[pidx * DH + threadIdx.x] = 0.f;
         if (threadIdx.x == 0) {
             part_ml[pidx * 2] = -1e30f;
@@ -571,20 +577,43 @@ __global__ void __launch_bounds__(128) k_attn_decode(const float* __restrict__ q
     for (int i = 0; i < R; ++i) {
         const int slot = warp * 16 + quad + 8 * i;
         valid[i] = r0 + slot < len;
+        const bool ld = valid[i] && (rope || r0 + slot != len - 1);  // the newest row: after the wait
         const uint8_t* krow = page + ((size_t)kh * kPage + slot) * (DH / 2) + q4 * (CPL / 2);
         if (CPL == 32) {
-            uint4 ka = valid[i] ? ldg_nc_v4(krow) : make_uint4(0, 0, 0, 0);
-            uint4 va = valid[i] ? ldg_nc_v4(krow + cb) : make_uint4(0, 0, 0, 0);
+            uint4 ka = ld ? ldg_nc_v4(krow) : make_uint4(0, 0, 0, 0);
+            uint4 va = ld ? ldg_nc_v4(krow + cb) : make_uint4(0, 0, 0, 0);
             kw[i][0] = ka.x; kw[i][1] = ka.y; kw[i][2] = ka.z; kw[i][3] = ka.w;
             vw[i][0] = va.x; vw[i][1] = va.y; vw[i][2] = va.z; vw[i][3] = va.w;
         } else {
-            uint2 ka = valid[i] ? *reinterpret_cast<const uint2*>(krow) : make_uint2(0, 0);
-            uint2 va = valid[i] ? *reinterpret_cast<const uint2*>(krow + cb) : make_uint2(0, 0);
+            uint2 ka = ld ? *reinterpret_cast<const uint2*>(krow) : make_uint2(0, 0);
+            uint2 va = ld ? *reinterpret_cast<const uint2*>(krow + cb) : make_uint2(0, 0);
             kw[i][0] = ka.x; kw[i][1] = ka.y;
             vw[i][0] = va.x; vw[i][1] = va.y;
         }
-        sk[i] = valid[i] ? sc[kh * kPage + slot] : 0.f;
-        sv[i] = valid[i] ? sc[Hkv * kPage + kh * kPage + slot] : 0.f;
+        sk[i] = ld ? sc[kh * kPage + slot] : 0.f;
+        sv[i] = ld ? sc[Hkv * kPage + kh * kPage + slot] : 0.f;
+    }
+    if (!rope) {
+        pdl_wait();  // q and the newest row come from the upstream kernels
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+            const int slot = warp * 16 + quad + 8 * i;
+            if (!(valid[i] && r0 + slot == len - 1)) continue;
+            const uint8_t* krow = page + ((size_t)kh * kPage + slot) * (DH / 2) + q4 * (CPL / 2);
+            if (CPL == 32) {
+                const uint4 ka = __ldcg(reinterpret_cast<const uint4*>(krow));
+                const uint4 va = __ldcg(reinterpret_cast<const uint4*>(krow + cb));
+                kw[i][0] = ka.x; kw[i][1] = ka.y; kw[i][2] = ka.z; kw[i][3] = ka.w;
+                vw[i][0] = va.x; vw[i][1] = va.y; vw[i][2] = va.z; vw[i][3] = va.w;
+            } else {
+                const uint2 ka = __ldcg(reinterpret_cast<const uint2*>(krow));
+                const uint2 va = __ldcg(reinterpret_cast<const uint2*>(krow + cb));
+                kw[i][0] = ka.x; kw[i][1] = ka.y;
+                vw[i][0] = va.x; vw[i][1] = va.y;
+            }
+            sk[i] = __ldcg(sc + kh * kPage + slot);
+            sv[i] = __ldcg(sc + Hkv * kPage + kh * kPage + slot);
+        }
     }
     float q[CPL];
     const float* qp = qkv + (size_t)b * ldq + h * DH + q4 * CPL;
