@@ -258,11 +258,27 @@ __global__ void __launch_bounds__(256, NT <= 2 ? QT_GEMV_MINB : 1) k_gemv_reg(co
     int acc[NT][4];
 #pragma unroll
     for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0;
+    // epilogue operands of the current row block (8 * TOK <= 256: one (token, column pair) per
+    // thread), loaded when the row block starts so their latency hides behind its MMAs
+    constexpr bool EPRE = 8 * TOK <= 256;
+    const int et = tid % TOK, ecp = tid / TOK;
+    const bool eon = EPRE && tid < 8 * TOK && et < M;
+    const double e_sa = eon ? sa[et] : 0.0;
+    double2 e_sw = make_double2(0.0, 0.0), e_x = make_double2(0.0, 0.0);
     while (rb < n_rb) {
         int nrb = rb, nbt = bat + 1;
         if (nbt == nbat) {
             nbt = 0;
             nrb = rb + gridDim.x;
+        }
+        if (eon && bat == 0) {
+            const int n = rb * 16 + 2 * ecp;
+            e_sw = make_double2(n < N ? sw[n] : 0.0, n + 1 < N ? sw[n + 1] : 0.0);
+            if constexpr (EPI == QT_EPI_RESADD) {
+                const double* p = static_cast<const double*>(out) + (size_t)et * ldo + n;
+                if (n + 1 < N) e_x = *reinterpret_cast<const double2*>(p);
+                else if (n < N) e_x.x = p[0];
+            }
         }
         uint4 na[U], nb[U];
         fetch(nrb, nbt, na, nb);
@@ -318,10 +334,22 @@ __global__ void __launch_bounds__(256, NT <= 2 ? QT_GEMV_MINB : 1) k_gemv_reg(co
                         if (n < N) acc_dbg[(size_t)t * N + n] = s0;
                         if (n + 1 < N) acc_dbg[(size_t)t * N + n + 1] = s1;
                     }
-                    const double a_s = sa[t];
-                    const float v = epi_store<EPI>(out, ldo, t, n, (double)s0 * (a_s * sw[n]),
-                                                   (double)s1 * (a_s * sw[n + 1]), N);
-                    if (pmax) atomicMax(&smx[t], __float_as_int(v));
+                    if constexpr (EPRE) {  // e == tid: the prefetched scales / residual
+                        const double y0 = (double)s0 * (e_sa * e_sw.x), y1 = (double)s1 * (e_sa * e_sw.y);
+                        if constexpr (EPI == QT_EPI_RESADD) {
+                            double* p = static_cast<double*>(out) + (size_t)t * ldo + n;
+                            if (n + 1 < N) *reinterpret_cast<double2*>(p) = make_double2(e_x.x + y0, e_x.y + y1);
+                            else if (n < N) p[0] = e_x.x + y0;
+                        } else {
+                            const float v = epi_store<EPI>(out, ldo, t, n, y0, y1, N);
+                            if (pmax) atomicMax(&smx[t], __float_as_int(v));
+                        }
+                    } else {
+                        const double a_s = sa[t];
+                        const float v = epi_store<EPI>(out, ldo, t, n, (double)s0 * (a_s * sw[n]),
+                                                       (double)s1 * (a_s * sw[n + 1]), N);
+                        if (pmax) atomicMax(&smx[t], __float_as_int(v));
+                    }
                 }
             }
             __syncthreads();
