@@ -132,11 +132,13 @@ __global__ void __launch_bounds__(1024) k_norm_quant4(const TX* __restrict__ x, 
                                                       int ld8) {
     __shared__ double red[32];
     pdl_launch_dependents();
-    pdl_wait();  // x is produced by the previous kernel
     const int row = blockIdx.x;
-    if (row >= M) return;
     const int base = threadIdx.x * 4;
     const bool in = base < D;
+    // the gain is a weight: read before the dependency wait, off the critical path
+    const float4 g4 = gain && in ? *reinterpret_cast<const float4*>(gain + base) : make_float4(1.f, 1.f, 1.f, 1.f);
+    pdl_wait();  // x is produced by the previous kernel
+    if (row >= M) return;
     double v[4] = {0.0, 0.0, 0.0, 0.0};
     if (in) {
         const TX* xr = x + (size_t)row * ld_x + base;
@@ -155,8 +157,7 @@ __global__ void __launch_bounds__(1024) k_norm_quant4(const TX* __restrict__ x, 
         ss = block_sum(ss, red);
         const double inv = 1.0 / sqrt(ss / (double)D + kNormEps);
         if (in) {
-            const float4 g = *reinterpret_cast<const float4*>(gain + base);
-            const float gg[4] = {g.x, g.y, g.z, g.w};
+            const float gg[4] = {g4.x, g4.y, g4.z, g4.w};
 #pragma unroll
             for (int e = 0; e < 4; ++e) v[e] = __dmul_rn(__dmul_rn(v[e], inv), (double)gg[e]);
         }
