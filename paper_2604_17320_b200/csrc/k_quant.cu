@@ -342,13 +342,22 @@ __global__ void __launch_bounds__(256) k_rope_kv_append(
     const int* __restrict__ page_table, int max_pages, uint8_t* __restrict__ pool, long long page_bytes,
     int qmax, float* __restrict__ k_dbg) {
     pdl_launch_dependents();
-    pdl_wait();
     const int m = blockIdx.x;
-    if (m >= M) return;
+    if (m >= M) {
+        pdl_wait();
+        return;
+    }
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int t = blockIdx.y * nw + wid;  // head slot: q heads, k heads, v heads
-    if (t >= H + 2 * Hkv) return;
+    if (t >= H + 2 * Hkv) {
+        pdl_wait();
+        return;
+    }
     const int E = dh / 32;  // elements per lane (2 or 4)
+    // positions, rows, page table and the cos/sin table are final before the upstream kernels
+    // run: host uploads (each followed by a full, non-programmatic dependency -- this also
+    // orders the prefill's compaction gather of the positions), or the decode step's bump at
+    // the end of the previous step.  Read them before the dependency wait, qkv after it.
     const int p = pos[m];
     const double2* rt = rope + (size_t)p * (dh / 2);
     float* row = qkv + (size_t)m * ld_qkv;
@@ -356,6 +365,13 @@ __global__ void __launch_bounds__(256) k_rope_kv_append(
     uint8_t* page = pool + (long long)page_table[b * max_pages + r / kPage] * page_bytes;
     const int slot = r % kPage;
     const size_t codes_bytes = (size_t)Hkv * kPage * (dh / 2);
+    double2 csv[2] = {make_double2(1.0, 0.0), make_double2(1.0, 0.0)};
+    if (t < H + Hkv) {
+#pragma unroll
+        for (int j = 0; j < 4; j += 2)
+            if (j < E) csv[j / 2] = rt[(lane * E + j) / 2];
+    }
+    pdl_wait();
     {
         float* v = row + t * dh;  // q heads, then k heads, then v heads: contiguous
         double val[4];
@@ -366,7 +382,7 @@ __global__ void __launch_bounds__(256) k_rope_kv_append(
 #pragma unroll
             for (int j = 0; j < 4; j += 2) {
                 if (j < E) {
-                    double2 cs = rt[(lane * E + j) / 2];
+                    const double2 cs = csv[j / 2];
                     double a = val[j], bb = val[j + 1];
                     val[j] = __dsub_rn(__dmul_rn(a, cs.x), __dmul_rn(bb, cs.y));
                     val[j + 1] = __dadd_rn(__dmul_rn(a, cs.y), __dmul_rn(bb, cs.x));
