@@ -732,21 +732,40 @@ __global__ void __launch_bounds__(1024) k_attn_merge_quant(const float* __restri
         if (h >= H) continue;
         const size_t base = ((size_t)b * H + h) * npg;
         float M = -1e30f;
-        for (int p = lane; p < npg; p += 32) M = fmaxf(M, part_ml[(base + p) * 2]);
-        M = warp_max(M);
         float L = 0.f;
-        // branch-free so the loads of consecutive pages overlap; an empty page (l = 0, o = 0,
-        // m = -1e30) contributes exactly 0, as the skipped iteration did
+        if (npg <= 32) {
+            // lane p holds page p's (m, l): one load per lane, then the page loop only loads o
+            // (independent of M, so it pipelines) and takes (m, l) by shuffle -- same sums
+            float2 mlv = make_float2(-1e30f, 0.f);
+            if (lane < npg) mlv = *reinterpret_cast<const float2*>(part_ml + (base + lane) * 2);
+            M = warp_max(mlv.x);
 #pragma unroll 4
-        for (int p = 0; p < npg; ++p) {
-            const float2 mlp = *reinterpret_cast<const float2*>(part_ml + (base + p) * 2);
-            float ov[CPL];
+            for (int p = 0; p < npg; ++p) {
+                float ov[CPL];
 #pragma unroll
-            for (int c = 0; c < CPL; ++c) ov[c] = part_o[(base + p) * DH + lane * CPL + c];
-            const float a = mlp.y == 0.f ? 0.f : expf(mlp.x - M);
-            L += mlp.y * a;
+                for (int c = 0; c < CPL; ++c) ov[c] = part_o[(base + p) * DH + lane * CPL + c];
+                const float mp = __shfl_sync(0xffffffffu, mlv.x, p), lp = __shfl_sync(0xffffffffu, mlv.y, p);
+                const float a = lp == 0.f ? 0.f : expf(mp - M);
+                L += lp * a;
 #pragma unroll
-            for (int c = 0; c < CPL; ++c) o[hh][c] += ov[c] * a;
+                for (int c = 0; c < CPL; ++c) o[hh][c] += ov[c] * a;
+            }
+        } else {
+            for (int p = lane; p < npg; p += 32) M = fmaxf(M, part_ml[(base + p) * 2]);
+            M = warp_max(M);
+            // branch-free so the loads of consecutive pages overlap; an empty page (l = 0,
+            // o = 0, m = -1e30) contributes exactly 0, as a skipped iteration would
+#pragma unroll 4
+            for (int p = 0; p < npg; ++p) {
+                const float2 mlp = *reinterpret_cast<const float2*>(part_ml + (base + p) * 2);
+                float ov[CPL];
+#pragma unroll
+                for (int c = 0; c < CPL; ++c) ov[c] = part_o[(base + p) * DH + lane * CPL + c];
+                const float a = mlp.y == 0.f ? 0.f : expf(mlp.x - M);
+                L += mlp.y * a;
+#pragma unroll
+                for (int c = 0; c < CPL; ++c) o[hh][c] += ov[c] * a;
+            }
         }
         const float il = 1.f / L;
 #pragma unroll
