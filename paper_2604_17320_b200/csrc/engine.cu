@@ -341,6 +341,11 @@ struct qt_engine {
     const bool use_pmax = !(std::getenv("QT_PMAX") && std::atoi(std::getenv("QT_PMAX")) == 0);
     float* pmax = nullptr;
     int pm_parts = 0;
+    float* pm_ptr = nullptr;  // where the last producer left them, row stride pm_ld
+    int pm_ld = kPmaxLd;
+    // decode: one atomically reduced max per (layer, token) from the gate|up GEMV (zeroed at the
+    // end of every step) instead of one partial per GEMV CTA
+    float* gmax = nullptr;
     int* splitk_ws = nullptr;     // int32 split-K partials of the tcgen05 GEMM at small M
     unsigned* seq_cnt = nullptr;  // per-sequence arrival counters of the fused decode attention block
     // opt-in (QT_ATTN_FUSED=1): one kernel for RoPE + KV append + attention + attn_out quant; measured
@@ -373,7 +378,7 @@ struct qt_engine {
             for (double* p : fl.w) f(p);
         f(fp_head);
         if (blas) cublasDestroy(blas);
-        f(splitk_ws); f(codes8); f(head8); f(pmax); f(dec_cnt); f(dec_hmax); f(seq_cnt); f(mk_trace); f(mk_layers); f(mk_acc); f(mk_codes); f(mk_sa); f(mk_attn); f(mk_sync); f(mk_act);
+        f(splitk_ws); f(codes8); f(head8); f(pmax); f(gmax); f(dec_cnt); f(dec_hmax); f(seq_cnt); f(mk_trace); f(mk_layers); f(mk_acc); f(mk_codes); f(mk_sa); f(mk_attn); f(mk_sync); f(mk_act);
         if (pin) cudaFreeHost(pin);
         if (own_stream) cudaStreamDestroy(own_stream);
     }
@@ -525,7 +530,10 @@ struct qt_engine {
                 }
             if (need) splitk_ws = dalloc<int>(need);
         }
-        if (cfg.act_mode == 1 && use_pmax) pmax = dalloc<float>((size_t)std::max(mt, mb) * kPmaxLd);
+        if (cfg.act_mode == 1 && use_pmax) {
+            pmax = dalloc<float>((size_t)std::max(mt, mb) * kPmaxLd);
+            gmax = dalloc<float>((size_t)L * mb);
+        }
         mk_init();
         pin_cap = (size_t)64 << 20;
         pin_cap += (size_t)mt * (sizeof(int) * 8);
@@ -1126,7 +1134,7 @@ struct qt_engine {
         pb(P_QUANT);
         int8_t* c8 = codes8 && M > 64 ? codes8 : nullptr;  // the next GEMM runs on int8 operands
         if (from_pmax && pm_parts > 0 && !is_f64 && !gain && mode == 1)
-            ckl(qt_launch_quant_pmax(static_cast<const float*>(xin), ldx, pmax, pm_parts, kPmaxLd, M, D, dpad, 7, mode,
+            ckl(qt_launch_quant_pmax(static_cast<const float*>(xin), ldx, pm_ptr, pm_parts, pm_ld, M, D, dpad, 7, mode,
                                      s, codes, codes_rows, ascale, c8, ld8, st),
                 "quant (producer row max)");
         else
@@ -1138,10 +1146,14 @@ struct qt_engine {
     // w: tiled int4 weights with wrows padded rows; activation codes: tiled with codes_rows rows
     // want_pm: also leave the per-row partial max |out| in pmax (pm_parts slots; 0 = not produced)
     void gemm(int epi, const uint8_t* w, int wrows, const double* sw, int M, int N, int K, void* out, int ldo,
-              bool want_pm = false, const int8_t* w8 = nullptr) {
+              bool want_pm = false, const int8_t* w8 = nullptr, float* pm_atomic = nullptr) {
         pb(P_GEMM);
-        float* pm = want_pm ? pmax : nullptr;
+        const bool atomic_pm = want_pm && pm_atomic && M <= 64;  // GEMV: one reduced max per row
+        float* pm = want_pm ? (atomic_pm ? pm_atomic : pmax) : nullptr;
+        const int pld = atomic_pm ? 0 : kPmaxLd;
         pm_parts = 0;
+        pm_ptr = atomic_pm ? pm_atomic : pmax;
+        pm_ld = atomic_pm ? 1 : kPmaxLd;
         const bool split = splitk_ws && qt_tc05_splitk(M, N, K) > 1;
         // tcgen05 for token-rich GEMMs; the weight-streaming GEMV up to 64 tokens (decode batches)
         int rc = (use_tc05 && M > 64 && codes8 && w8 && !split)
@@ -1151,7 +1163,7 @@ struct qt_engine {
                      ? qt_launch_w4a4_tc05_ex(epi, codes, codes_rows, ascale, w, wrows, sw, M, N, K, out, ldo, nullptr,
                                               splitk_ws, pm, kPmaxLd, &pm_parts, st)
                      : qt_launch_w4a4_mma_ex(epi, codes, codes_rows, ascale, w, wrows, sw, M, N, K, out, ldo, nullptr,
-                                             pm, kPmaxLd, &pm_parts, st);
+                                             pm, pld, &pm_parts, st);
         qt::g_l2_next = nullptr;  // consumed by the GEMV launcher; never carried past this launch
         ckl(rc, "w4a4 gemm");
         const double out_bytes = epi == QT_EPI_RESADD ? 16.0 * M * N : (epi == QT_EPI_SWIGLU ? 2.0 * M * N : 4.0 * M * N);
@@ -1332,6 +1344,8 @@ struct qt_engine {
                 pe((double)M * (n_qkv * 4.0 + d * 4.0), 4.0 * pairs * dh * H);
             }
             pm_parts = pmax ? H : 0;  // the attention epilogue left max |out| per (row, head)
+            pm_ptr = pmax;
+            pm_ld = kPmaxLd;
             norm_quant(attn, 0, d, nullptr, M, d, kd_pad, 4 * l + 1, true);
             gemm(QT_EPI_RESADD, w.o, nd_pad, w.s_o, M, d, kd_pad, xc, d, false, w.o8);
             if (rec_diag) diag_layer(l, ptl, cur_v[0], h_txt[0], xc);
@@ -1531,8 +1545,9 @@ struct qt_engine {
             if (!(skip_mask & 1)) gemm(QT_EPI_RESADD, w.o, nd_pad, w.s_o, B, d, kd_pad, xcur, d);
             if (!(skip_mask & 4)) norm_quant(xcur, 1, d, w.g2, B, d, kd_pad, 4 * l + 2);
             l2_next(w.down, (size_t)nd_pad * kff_pad / 2);
-            if (skip_mask & 1) {} else if (cfg.mlp == 1) gemm(QT_EPI_SWIGLU, w.gu, n_gu_pad, w.s_gu, B, n_gu, kd_pad, mid, dff, true);
-            else gemm(QT_EPI_SILU, w.gu, n_gu_pad, w.s_gu, B, n_gu, kd_pad, mid, dff, true);
+            float* gml = gmax ? gmax + (size_t)l * max_batch : nullptr;
+            if (skip_mask & 1) {} else if (cfg.mlp == 1) gemm(QT_EPI_SWIGLU, w.gu, n_gu_pad, w.s_gu, B, n_gu, kd_pad, mid, dff, true, nullptr, gml);
+            else gemm(QT_EPI_SILU, w.gu, n_gu_pad, w.s_gu, B, n_gu, kd_pad, mid, dff, true, nullptr, gml);
             if (!(skip_mask & 4)) norm_quant(mid, 0, dff, nullptr, B, dff, kff_pad, 4 * l + 3, true);
             if (l + 1 < L) l2_next(lw[l + 1].qkv, (size_t)n_qkv_pad * kd_pad / 2);
             else l2_next(head, (size_t)nd_pad * kd_pad / 2);
@@ -1541,6 +1556,7 @@ struct qt_engine {
         norm_quant(xcur, 1, d, gf, B, d, kd_pad, 4 * L);
         gemm(QT_EPI_STORE, head, nd_pad, s_head, B, d, kd_pad, dlogits, d);
         ckl(qt_launch_kv_len_bump(kv_len, L * max_batch, next_pos, B, st), "kv length / position bump");
+        if (gmax) ck(cudaMemsetAsync(gmax, 0, (size_t)L * max_batch * sizeof(float), st), "row-max reset");
     }
 
     void finish_profile() {

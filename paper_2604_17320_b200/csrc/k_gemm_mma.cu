@@ -362,9 +362,14 @@ __global__ void __launch_bounds__(256, NT <= 2 ? QT_GEMV_MINB : 1) k_gemv_reg(co
             wb[u] = nb[u];
         }
     }
-    if (pmax) {  // this CTA's slot of the per-row partial max (every CTA writes its own)
+    if (pmax) {  // this CTA's slot of the per-row partial max (every CTA writes its own), or with
+        // pmax_ld == 0 one max per row by integer atomicMax (non-negative float bits: exact,
+        // order-independent); the caller zeroes those slots between uses
         __syncthreads();
-        if (tid < M && tid < TOK) pmax[(size_t)tid * pmax_ld + blockIdx.x] = __int_as_float(smx[tid]);
+        if (tid < M && tid < TOK) {
+            if (pmax_ld == 0) atomicMax(reinterpret_cast<int*>(pmax) + tid, smx[tid]);
+            else pmax[(size_t)tid * pmax_ld + blockIdx.x] = __int_as_float(smx[tid]);
+        }
     }
 }
 
@@ -382,9 +387,9 @@ int launch_gemm(const uint8_t* A, int lda, const double* sa, const uint8_t* W, i
     g_l2_next_bytes = 0;
     float* pm = nullptr;  // GEMV paths: one partial-max slot per CTA
     auto want_pmax = [&](int ctas) {
-        if (pmax && ctas <= pmax_ld) {
+        if (pmax && (pmax_ld == 0 || ctas <= pmax_ld)) {
             pm = pmax;
-            if (n_part) *n_part = ctas;
+            if (n_part) *n_part = pmax_ld == 0 ? 1 : ctas;
         }
     };
     if (M > 16 && M <= 64 && lda >= ((M + 31) / 32) * 32) {
