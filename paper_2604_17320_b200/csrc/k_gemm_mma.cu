@@ -235,12 +235,15 @@ __global__ void __launch_bounds__(256, NT <= 2 ? QT_GEMV_MINB : 1) k_gemv_reg(co
         }
     }
     pdl_wait();
-    uint4 bA[AREG ? U : 1];
+    uint4 bA[AREG ? U : 1][AREG ? NT : 1];
     if constexpr (AREG) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int c = ch0 + u;
-            bA[u] = c < ch1 ? ldg_nc_v4(A + w4t_offset(g, c * 64 + tig * 16, lda)) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+            for (int j = 0; j < NT; ++j)
+                bA[u][j] = c < ch1 ? ldg_nc_v4(A + w4t_offset(j * 8 + g, c * 64 + tig * 16, lda))
+                                   : make_uint4(0, 0, 0, 0);
         }
     }
     if (ASM) {  // each warp stages only its own k slice of the token codes: no block barrier
@@ -289,7 +292,7 @@ __global__ void __launch_bounds__(256, NT <= 2 ? QT_GEMV_MINB : 1) k_gemv_reg(co
             uint4 bv[NT];
 #pragma unroll
             for (int j = 0; j < NT; ++j) {
-                if constexpr (AREG) bv[j] = bA[u];  // nbat == 1: batch u is k tile ch0 + u
+                if constexpr (AREG) bv[j] = bA[u][j];  // nbat == 1: batch u is k tile ch0 + u
                 else if (ASM) bv[j] = *reinterpret_cast<const uint4*>(As + (j * 8 + g) * ldsA + c * 64 + tig * 16);
                 else bv[j] = ldg_nc_v4(A + w4t_offset(j * 8 + g, c * 64 + tig * 16, lda));  // rows >= M: discarded
             }
@@ -425,6 +428,14 @@ int launch_gemm(const uint8_t* A, int lda, const double* sa, const uint8_t* W, i
         const dim3 grid(std::min(n_rb, qt_gemv_ctas * sms));
         want_pmax((int)grid.x);
         static const bool areg_on = !(getenv("QT_GEMV_AREG") && atoi(getenv("QT_GEMV_AREG")) == 0);
+        static const bool areg2_on = getenv("QT_GEMV_AREG2") && atoi(getenv("QT_GEMV_AREG2")) == 1;
+        if (TOK == 16 && areg2_on && (K / 128 + 7) / 8 <= 4) {
+            const size_t smem2 = (size_t)8 * 16 * TOK * 4;
+            auto kfn = k_gemv_reg<2, EPI, true>;
+            cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
+            return launch_pdl(kfn, grid, dim3(256), smem2, st, A, lda, sa, W, ldw, sw, M, N, K, out, ldo, acc_dbg,
+                              qt_gemv_l2_rows_host, pf, pf_bytes, pm, pmax_ld);
+        }
         if (TOK == 8 && areg_on && (K / 128 + 7) / 8 <= 4) {
             const size_t smem2 = (size_t)8 * 16 * TOK * 4;  // split-K reduction buffer only
             auto kfn = k_gemv_reg<1, EPI, true>;
