@@ -268,6 +268,7 @@ __global__ void __launch_bounds__(256, NT <= 2 ? QT_GEMV_MINB : 1) k_gemv_reg(co
     const bool eon = EPRE && tid < 8 * TOK && et < M;
     const double e_sa = eon ? sa[et] : 0.0;
     double2 e_sw = make_double2(0.0, 0.0), e_x = make_double2(0.0, 0.0);
+    int rbi = 0;  // row blocks finished (reduction buffer parity)
     while (rb < n_rb) {
         int nrb = rb, nbt = bat + 1;
         if (nbt == nbat) {
@@ -310,7 +311,11 @@ __global__ void __launch_bounds__(256, NT <= 2 ? QT_GEMV_MINB : 1) k_gemv_reg(co
             }
         }
         if (bat == nbat - 1) {
-            int* base = red + (size_t)warp * (16 * TOK);
+            // double-buffered reduction buffer: the 2 epilogue warps finish row block i while the
+            // others run the MMAs of row block i + 1 (no barrier after the epilogue)
+            int* redb = red + (size_t)(rbi & 1) * (8 * 16 * TOK);
+            ++rbi;
+            int* base = redb + (size_t)warp * (16 * TOK);
 #pragma unroll
             for (int j = 0; j < NT; ++j) {
                 const int t = j * 8 + tig * 2;
@@ -327,8 +332,8 @@ __global__ void __launch_bounds__(256, NT <= 2 ? QT_GEMV_MINB : 1) k_gemv_reg(co
                     int s0 = 0, s1 = 0;
 #pragma unroll
                     for (int k = 0; k < 8; ++k) {
-                        s0 += red[(size_t)k * (16 * TOK) + (2 * cpair) * TOK + t];
-                        s1 += red[(size_t)k * (16 * TOK) + (2 * cpair + 1) * TOK + t];
+                        s0 += redb[(size_t)k * (16 * TOK) + (2 * cpair) * TOK + t];
+                        s1 += redb[(size_t)k * (16 * TOK) + (2 * cpair + 1) * TOK + t];
                     }
                     s0 >>= 8;
                     s1 >>= 8;
@@ -355,7 +360,6 @@ __global__ void __launch_bounds__(256, NT <= 2 ? QT_GEMV_MINB : 1) k_gemv_reg(co
                     }
                 }
             }
-            __syncthreads();
         }
         rb = nrb;
         bat = nbt;
@@ -403,7 +407,7 @@ int launch_gemm(const uint8_t* A, int lda, const double* sa, const uint8_t* W, i
         const dim3 grid(std::min(n_rb, 2 * sms));
         if (M <= 32) {
             want_pmax((int)grid.x);
-            const size_t smem = (size_t)8 * 16 * 32 * 4;
+            const size_t smem = (size_t)2 * 8 * 16 * 32 * 4;
             auto kfn = k_gemv_reg<4, EPI>;
             cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             return launch_pdl(kfn, grid, dim3(256), smem, st, A, lda, sa, W, ldw, sw, M, N, K, out, ldo, acc_dbg,
@@ -411,7 +415,7 @@ int launch_gemm(const uint8_t* A, int lda, const double* sa, const uint8_t* W, i
         }
         if (lda >= 64) {
             want_pmax((int)grid.x);
-            const size_t smem = (size_t)8 * 16 * 64 * 4;
+            const size_t smem = (size_t)2 * 8 * 16 * 64 * 4;
             auto kfn = k_gemv_reg<8, EPI>;
             cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             return launch_pdl(kfn, grid, dim3(256), smem, st, A, lda, sa, W, ldw, sw, M, N, K, out, ldo, acc_dbg,
@@ -421,7 +425,7 @@ int launch_gemm(const uint8_t* A, int lda, const double* sa, const uint8_t* W, i
     if (M <= 16) {
         const int kb = K / 2;
         const int TOK = M <= 8 ? 8 : 16;
-        const size_t smem = (size_t)TOK * (kb + 64) + (size_t)8 * 16 * TOK * 4;
+        const size_t smem = (size_t)TOK * (kb + 64) + (size_t)2 * 8 * 16 * TOK * 4;
         const int n_rb = (N + 15) / 16;
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -430,14 +434,14 @@ int launch_gemm(const uint8_t* A, int lda, const double* sa, const uint8_t* W, i
         static const bool areg_on = !(getenv("QT_GEMV_AREG") && atoi(getenv("QT_GEMV_AREG")) == 0);
         static const bool areg2_on = getenv("QT_GEMV_AREG2") && atoi(getenv("QT_GEMV_AREG2")) == 1;
         if (TOK == 16 && areg2_on && (K / 128 + 7) / 8 <= 4) {
-            const size_t smem2 = (size_t)8 * 16 * TOK * 4;
+            const size_t smem2 = (size_t)2 * 8 * 16 * TOK * 4;
             auto kfn = k_gemv_reg<2, EPI, true>;
             cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
             return launch_pdl(kfn, grid, dim3(256), smem2, st, A, lda, sa, W, ldw, sw, M, N, K, out, ldo, acc_dbg,
                               qt_gemv_l2_rows_host, pf, pf_bytes, pm, pmax_ld);
         }
         if (TOK == 8 && areg_on && (K / 128 + 7) / 8 <= 4) {
-            const size_t smem2 = (size_t)8 * 16 * TOK * 4;  // split-K reduction buffer only
+            const size_t smem2 = (size_t)2 * 8 * 16 * TOK * 4;  // split-K reduction buffers only
             auto kfn = k_gemv_reg<1, EPI, true>;
             cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
             return launch_pdl(kfn, grid, dim3(256), smem2, st, A, lda, sa, W, ldw, sw, M, N, K, out, ldo, acc_dbg,
