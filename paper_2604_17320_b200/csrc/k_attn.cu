@@ -164,8 +164,11 @@ QT_DEV void qk_tile(const uint32_t (*qh)[4], const uint32_t (*ql)[4], const __ha
 }
 
 // ============================================================== K7
+#ifndef QT_ATTN_MINB
+#define QT_ATTN_MINB 2  // 3 caps at 168 registers with spills; 2: 255, no spills (prefill -0.15 ms)
+#endif
 template <int DH>
-__global__ void __launch_bounds__(128, 3) k_attn_prefill(const float* __restrict__ qkv, int ldq, int H, int Hkv,
+__global__ void __launch_bounds__(128, QT_ATTN_MINB) k_attn_prefill(const float* __restrict__ qkv, int ldq, int H, int Hkv,
                                                       const int* __restrict__ seq_off, const int* __restrict__ vis,
                                                       const int* __restrict__ seq_len,
                                                       const uint8_t* __restrict__ pool, long long page_bytes,
