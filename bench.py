@@ -130,7 +130,7 @@ def load_traffic():
     out = {}
     for r in rows:
         k = r["kernel"]
-        if "k_gemv_reg<1, 0>" in k:  # decode QKV GEMV, B = 8: N 12288 x K 4096
+        if "k_gemv_reg<1, 0" in k:  # decode QKV GEMV (any variant), B = 8: N 12288 x K 4096
             M, N, K = 8, 12288, 4096
             r["algorithmic_bytes"] = N * K / 2 + 8 * N + M * K / 2 + 8 * M + 4 * M * N
             out["gemv"] = r
