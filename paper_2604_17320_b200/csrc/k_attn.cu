@@ -783,7 +783,7 @@ __global__ void __launch_bounds__(1024) k_attn_merge_quant(const float* __restri
     if (mode == 0) {
         s = static_scale;
     } else {
-        mx = block_max(mx, red);
+        mx = block_max1(mx, red);
         s = q_scale(mx, qmax);
     }
     const double inv_s = 1.0 / s;

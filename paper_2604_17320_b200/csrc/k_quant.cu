@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(1024) k_norm_quant4(const TX* __restrict__ x, 
                                                       uint8_t* __restrict__ codes, int ld_codes,
                                                       double* __restrict__ scales, int8_t* __restrict__ codes8,
                                                       int ld8) {
-    __shared__ double red[32];
+    __shared__ double red[32], red2[32];
     pdl_launch_dependents();
     const int row = blockIdx.x;
     const int base = threadIdx.x * 4;
@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(1024) k_norm_quant4(const TX* __restrict__ x, 
         double ss = 0.0;
 #pragma unroll
         for (int e = 0; e < 4; ++e) ss += v[e] * v[e];
-        ss = block_sum(ss, red);
+        ss = block_sum1(ss, red);
         const double inv = 1.0 / sqrt(ss / (double)D + kNormEps);
         if (in) {
             const float gg[4] = {g4.x, g4.y, g4.z, g4.w};
@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(1024) k_norm_quant4(const TX* __restrict__ x, 
         double mx = 0.0;
 #pragma unroll
         for (int e = 0; e < 4; ++e) mx = fmax(mx, fabs(v[e]));
-        mx = block_max(mx, red);
+        mx = block_max1(mx, red2);
         s = q_scale(mx, qmax);
     }
     if (base < d_pad) {

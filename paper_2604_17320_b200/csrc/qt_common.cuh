@@ -41,6 +41,24 @@ QT_DEV T block_sum(T v, T* scratch) {
     r = warp_sum(r);
     return r;
 }
+// One-barrier block reductions: `scratch` must not be in use by another reduction of the
+// same block (give each reduction of a kernel its own scratch array).
+template <typename T>
+QT_DEV T block_sum1(T v, T* scratch) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    v = warp_sum(v);
+    if (lane == 0) scratch[wid] = v;
+    __syncthreads();
+    return warp_sum(lane < nw ? scratch[lane] : T(0));
+}
+template <typename T>
+QT_DEV T block_max1(T v, T* scratch) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    v = warp_max(v);
+    if (lane == 0) scratch[wid] = v;
+    __syncthreads();
+    return warp_max(lane < nw ? scratch[lane] : T(0));
+}
 template <typename T>
 QT_DEV T block_max(T v, T* scratch) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
