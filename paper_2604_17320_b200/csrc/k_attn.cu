@@ -709,7 +709,7 @@ __global__ void __launch_bounds__(128) k_attn_decode(const float* __restrict__ q
 
 // Two 64-row pages per CTA (4 rows per lane): half the CTAs and half the partials of
 // k_attn_decode.  Unfused path only (rope == nullptr).
-template <int DH>
+template <int DH, int PP = 2>
 __global__ void __launch_bounds__(128) k_attn_decode_pp2(const float* __restrict__ qkv, int ldq, int H, int Hkv,
                                                      const int* __restrict__ kv_len, int len_add,
                                                      uint8_t* __restrict__ pool, long long page_bytes,
@@ -721,8 +721,8 @@ __global__ void __launch_bounds__(128) k_attn_decode_pp2(const float* __restrict
                                                      int ld_codes, double* __restrict__ scales, int qmode,
                                                      double static_scale, int d_pad, int qmax) {
     constexpr int CPL = DH / 4;  // channels per lane
-    constexpr int R = 4;         // rows per lane: two 64-row pages per CTA
-    constexpr int WR = 32;       // rows per warp (one page holds two warps' rows)
+    constexpr int R = 2 * PP;    // rows per lane: PP 64-row pages per CTA
+    constexpr int WR = 16 * PP;  // rows per warp (64 / WR warps per page)
     pdl_launch_dependents();
     // Without the fused append (rope == null) every cached row but the newest (len - 1, written
     // by the K/V append kernel just before) is final since earlier steps, as are kv_len and the
@@ -735,7 +735,7 @@ __global__ void __launch_bounds__(128) k_attn_decode_pp2(const float* __restrict
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int q4 = lane & 3, quad = lane >> 2;
     const int len = kv_len[b] + len_add;
-    const int r0 = pg * 2 * kPage;
+    const int r0 = pg * PP * kPage;
     const size_t pidx = ((size_t)b * H + h) * npg + pg;
     const double2* rt = rope ? rope + (size_t)pos[b] * (DH / 2) : nullptr;
     if (rope && pg == (len - 1) / kPage && warp < 2) {
@@ -866,7 +866,9 @@ __global__ void __launch_bounds__(128) k_attn_decode_pp2(const float* __restrict
         d += __shfl_xor_sync(0xffffffffu, d, 2);
         s[i] = valid[i] ? d * sk[i] * inv_sqrt : -1e30f;
     }
-    float m = fmaxf(fmaxf(s[0], s[1]), fmaxf(s[2], s[3]));
+    float m = s[0];
+#pragma unroll
+    for (int i = 1; i < R; ++i) m = fmaxf(m, s[i]);
     float l = 0.f;
     float acc[CPL];
 #pragma unroll
@@ -1082,14 +1084,15 @@ int qt_launch_attn_decode(const float* qkv, int ldq, int H, int Hkv, int dh, con
     if (H > 64) return -1;
     // two 64-row pages per CTA (unfused path, dh = 128): half the CTAs, half the partials
     static const int ppc_env = getenv("QT_ATTN_PPC") ? atoi(getenv("QT_ATTN_PPC")) : 2;
-    const bool pp2 = ppc_env == 2 && !rope && !counters && dh == 128;
-    if (pp2) n_pages = (n_pages + 1) / 2;
+    const int ppc = (ppc_env == 2 || ppc_env == 4) && !rope && !counters && dh == 128 ? ppc_env : 1;
+    const bool pp2 = ppc > 1;
+    if (pp2) n_pages = (n_pages + ppc - 1) / ppc;
     const dim3 grid(n_pages, H, B);
     const float inv_sqrt = (float)(1.0 / sqrt((double)dh));
     const int qmax = (1 << (bits - 1)) - 1;
     int rc;
     if (dh == 128) {
-        rc = pp2 ? launch_pdl(k_attn_decode_pp2<128>, grid, dim3(128), 0, st, qkv, ldq, H, Hkv, kv_len, len_add, pool,
+        rc = pp2 ? launch_pdl(ppc == 4 ? k_attn_decode_pp2<128, 4> : k_attn_decode_pp2<128, 2>, grid, dim3(128), 0, st, qkv, ldq, H, Hkv, kv_len, len_add, pool,
                               page_bytes, pt, max_pages, inv_sqrt, part_ml, part_o, rt, pos, counters, row, hmax,
                               codes, ld_codes, scales, qmode, static_scale, d_pad, qmax)
                  : launch_pdl(k_attn_decode<128>, grid, dim3(128), 0, st, qkv, ldq, H, Hkv, kv_len, len_add, pool,
