@@ -214,7 +214,10 @@ __global__ void __launch_bounds__(256) k_quant_pmax(const float* __restrict__ x,
             v[j][1] = p[1];
         }
     double s = static_scale;
-    if (mode != 0) {  // warp 0 folds the row's partials (loads above already in flight); smem broadcast
+    if (mode != 0 && n_part <= 32) {  // few partials (decode: one reduced slot): every warp folds
+        const float mx = warp_max(lane < n_part ? pmax[(size_t)row * pmax_ld + lane] : 0.f);
+        s = q_scale((double)mx, qmax);
+    } else if (mode != 0) {  // warp 0 folds the row's partials (loads above already in flight); smem broadcast
         __shared__ float s_mx;
         if (threadIdx.x < 32) {
             float mx = 0.f;
