@@ -317,9 +317,12 @@ def run_ours(args, cfg):
     dlog_p = torch.empty(D, B, d).pin_memory()
 
     def step_e2e():
-        eng.prefill(emb_p, vis, txt, v0=v0s, logits_out=logits_p)
+        # the prefill logits come back on the engine's copy stream while the decode steps run;
+        # join_copies() puts their completion back on the timed stream before the step ends
+        eng.prefill(emb_p, vis, txt, v0=v0s, logits_out=logits_p, logits_async=True)
         for t in range(D):
             eng.decode(dec_p[t], logits_out=dlog_p[t])
+        eng.join_copies()
 
     def barrier():
         torch.cuda.synchronize(dev)

@@ -70,6 +70,8 @@ void qt_engine_destroy(qt_engine* e);
  * default stream). */
 int qt_engine_set_stream(qt_engine* e, void* stream);
 int qt_engine_synchronize(qt_engine* e);
+/* make the engine stream wait for a pending asynchronous logits readback */
+int qt_engine_join_copies(qt_engine* e);
 
 /* init_model / prepare_quant_env (model.cpp:113-135, 212-237): fp32 weights
  * in reference orientation, quantized on the device to int4 codes with one
@@ -163,7 +165,10 @@ int qt_recipe_parse(const char* json, int max_layers, int* n_layers, int* layers
  * batch of independent sequences.  emb: packed [sum(visual+text) x d_model].
  * v0: per-sequence reference visual length (null = recipe v0).  positions:
  * packed original position ids (null = 0..S-1 per sequence).  logits_out
- * (nullable): packed [sum(final rows) x d_model], host or device. */
+ * (nullable): packed [sum(final rows) x d_model]; out_on_device 0 = host,
+ * 1 = device, 2 = host read back asynchronously on a copy stream (overlapping
+ * the decode steps that follow; valid after qt_engine_synchronize, and
+ * qt_engine_join_copies orders the engine stream after it). */
 int qt_engine_prefill(qt_engine* e, int n_seq, const float* emb, int emb_on_device, const int* visual,
                       const int* text, const int* v0, const int* positions, float* logits_out, int out_on_device);
 /* Same with fp64 embeddings (the reference's Matrix element type). */

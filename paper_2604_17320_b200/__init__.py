@@ -91,6 +91,7 @@ def lib():
         L.qt_engine_fit_act_scales.argtypes = [vp, C.c_int, C.POINTER(dp), ip, ip, dp, C.c_int]
         L.qt_engine_fit_act_scales_hooked.argtypes = [vp, C.c_int, C.POINTER(dp), ip, ip, dp, C.c_int]
         L.qt_engine_profile_chain.argtypes = [vp, C.c_int, C.c_int, dp]
+        L.qt_engine_join_copies.argtypes = [vp]
         L.qt_engine_prefill_fp.argtypes = [vp, C.c_int, C.POINTER(dp), ip, ip, C.c_int, dp, C.c_int64]
         L.qt_engine_profile_sensitivity.argtypes = [vp, C.c_int, C.POINTER(dp), ip, ip, C.c_int, ip, C.c_double,
                                                     dp, dp]
@@ -301,7 +302,11 @@ class Engine:
     def clear_recipe(self):
         check(lib().qt_engine_set_recipe(self.h, 0, None, None, None, 1, 4))
 
-    def prefill(self, emb, visual, text, v0=None, positions=None, logits_out=None):
+    def join_copies(self):
+        """Order the engine stream after a pending asynchronous logits readback."""
+        check(lib().qt_engine_join_copies(self.h))
+
+    def prefill(self, emb, visual, text, v0=None, positions=None, logits_out=None, logits_async=False):
         """emb: packed [sum(S) x d] fp32 -- numpy / CPU (pinned) torch on the host, or a
         CUDA torch tensor.  Returns the logits rows (numpy, or a view of logits_out)."""
         visual, text = _i32(visual), _i32(text)
@@ -313,8 +318,11 @@ class Engine:
             out = np.empty((int(np.sum(visual + text)), self.cfg.d_model), dtype=np.float32)
         else:
             out = logits_out
+        odev = _on_device(out)
+        if logits_async and not odev:
+            odev = 2  # host readback on the engine's copy stream; valid after synchronize()
         check(lib().qt_engine_prefill(self.h, len(visual), _ptr(emb), on_dev, _ip(visual), _ip(text), _ip(v0a),
-                                      _ip(pa), _ptr(out), _on_device(out)))
+                                      _ip(pa), _ptr(out), odev))
         rows = lib().qt_engine_prefill_rows(self.h)
         return out[:rows]
 

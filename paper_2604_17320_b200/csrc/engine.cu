@@ -186,6 +186,16 @@ struct qt_engine {
     int n_qkv = 0, n_qkv_pad = 0, kd_pad = 0, kff_pad = 0, n_gu = 0, n_gu_pad = 0, nd_pad = 0;
     int max_batch = 0, max_tokens = 0, max_seq = 0, max_decode = 0, max_pos = 0;
     cudaStream_t own_stream = nullptr, st = nullptr;
+    // asynchronous host readback of prefill logits (qt_engine_prefill out_on_device = 2)
+    cudaStream_t cst = nullptr;
+    cudaEvent_t ev_lg = nullptr, ev_cp = nullptr;
+    bool copy_pending = false;
+    void join_copies() {  // order the engine stream after the pending readback
+        if (!copy_pending) return;
+        ck(cudaStreamWaitEvent(st, ev_cp, 0), "event wait");
+        copy_pending = false;
+        qt::g_pdl_block = true;
+    }
 
     std::vector<LayerW> lw;
     uint8_t* head = nullptr;
@@ -380,6 +390,12 @@ struct qt_engine {
         if (blas) cublasDestroy(blas);
         f(splitk_ws); f(codes8); f(head8); f(pmax); f(gmax); f(dec_cnt); f(dec_hmax); f(seq_cnt); f(mk_trace); f(mk_layers); f(mk_acc); f(mk_codes); f(mk_sa); f(mk_attn); f(mk_sync); f(mk_act);
         if (pin) cudaFreeHost(pin);
+        if (cst) {
+            cudaStreamSynchronize(cst);
+            cudaStreamDestroy(cst);
+            cudaEventDestroy(ev_lg);
+            cudaEventDestroy(ev_cp);
+        }
         if (own_stream) cudaStreamDestroy(own_stream);
     }
 
@@ -1184,6 +1200,7 @@ struct qt_engine {
         if (cfg.act_mode == 0 && !act_set) fail(QT_EINVAL, "quantized mode requires a QuantEnv");  // model.cpp:323-325
         if (nseq < 1 || nseq > max_batch) fail(QT_EINVAL, "batch size outside engine capacity");
         reset_staging();
+        join_copies();  // the previous prefill's async logits readback still reads `logits`
         if (codes8) ensure_w8();
         graph_ok = false;
         prefilled = false;
@@ -1418,10 +1435,25 @@ struct qt_engine {
         final_rows = M;
         ev_layers = trace_layers;
         ev_vis = ev_prev_v;
-        if (logits_out)
+        if (logits_out && out_dev == 2) {
+            // asynchronous host readback on a copy stream: overlaps the decode steps that follow;
+            // complete after qt_engine_synchronize / qt_engine_join_copies
+            if (!cst) {
+                ck(cudaStreamCreateWithFlags(&cst, cudaStreamNonBlocking), "copy stream");
+                ck(cudaEventCreateWithFlags(&ev_lg, cudaEventDisableTiming), "event");
+                ck(cudaEventCreateWithFlags(&ev_cp, cudaEventDisableTiming), "event");
+            }
+            ck(cudaEventRecord(ev_lg, st), "event");
+            ck(cudaStreamWaitEvent(cst, ev_lg, 0), "event wait");
+            ck(cudaMemcpyAsync(logits_out, logits, (size_t)M * d * sizeof(float), cudaMemcpyDeviceToHost, cst),
+               "logits readback");
+            ck(cudaEventRecord(ev_cp, cst), "event");
+            copy_pending = true;
+        } else if (logits_out) {
             ck(cudaMemcpyAsync(logits_out, logits, (size_t)M * d * sizeof(float),
                                out_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st),
                "logits readback");
+        }
 
         // prune trace (PruneEvent, model.cpp:408-418) and final layout positions
         if (!trace_layers.empty()) {
@@ -1800,7 +1832,14 @@ int qt_engine_set_stream(qt_engine* e, void* stream) {
 }
 
 int qt_engine_synchronize(qt_engine* e) {
-    return guard([&] { ck(cudaStreamSynchronize(e->st), "synchronize"); });
+    return guard([&] {
+        e->join_copies();
+        ck(cudaStreamSynchronize(e->st), "synchronize");
+    });
+}
+
+int qt_engine_join_copies(qt_engine* e) {
+    return guard([&] { e->join_copies(); });
 }
 
 int qt_engine_load_layer(qt_engine* e, int layer, const float* wq, const float* wk, const float* wv,

@@ -168,3 +168,22 @@ def test_profile_chain_leaves_decode_state(pair):
         assert np.array_equal(a, b)
     v, t, pos = e.layout(0)
     assert (v, t) == (30, 13) and pos[-1] == 42
+
+
+def test_async_logits_readback(pair):
+    """qt_engine_prefill with out_on_device = 2: the host logits arrive on the copy stream while
+    decode steps run; after synchronize() they equal the synchronous readback, and a following
+    prefill waits for the pending copy before reusing the device buffer."""
+    cfg, port, e = pair
+    e.clear_recipe()
+    emb = O.synth_embeddings(40, 128, seed=29).astype(np.float32)
+    emb2 = O.synth_embeddings(40, 128, seed=30).astype(np.float32)
+    ref = e.prefill(emb, [30], [10]).copy()
+    ref2 = e.prefill(emb2, [30], [10]).copy()
+    out = np.zeros_like(ref)
+    e.prefill(emb, [30], [10], logits_out=out, logits_async=True)
+    e.decode(O.synth_embeddings(1, 128, seed=31).astype(np.float32))
+    out2 = np.zeros_like(ref2)
+    e.prefill(emb2, [30], [10], logits_out=out2, logits_async=True)  # joins the first copy
+    e.synchronize()
+    assert np.array_equal(out, ref) and np.array_equal(out2, ref2)
