@@ -24,7 +24,6 @@
 #include "../../include/quota_b200.h"
 #include "qt_common.cuh"
 #include "qt_kernels.h"
-#include "qt_decode_mk.h"
 #include <cublas_v2.h>
 
 namespace {
@@ -41,17 +40,9 @@ struct QtError : std::runtime_error {
 void ck(cudaError_t e, const char* what) {
     if (e != cudaSuccess) fail(QT_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
-const bool g_trace = std::getenv("QT_TRACE") != nullptr;
-const bool g_nograph = std::getenv("QT_NOGRAPH") != nullptr;
 bool g_capturing = false;
-// debug/attribution only: QT_SKIP bit mask drops decode launches (1 gemv, 2 attention, 4 quant, 8 kv append)
-const int g_skip = std::getenv("QT_SKIP") ? std::atoi(std::getenv("QT_SKIP")) : 0;
 
 void ckl(int rc, const char* what) {
-    if (g_trace && !g_capturing) {
-        cudaError_t se = cudaDeviceSynchronize();
-        std::fprintf(stderr, "[qt] %s rc=%d sync=%s\n", what, rc, cudaGetErrorString(se));
-    }
     if (rc != 0) {
         cudaError_t e = cudaGetLastError();
         fail(rc > 0 ? QT_ECUDA : QT_EINVAL,
@@ -264,7 +255,6 @@ struct qt_engine {
     float* part_o = nullptr;
     int dec_splits = 1, dec_pps = 1;
     std::vector<int> dec_pages;  // decode-attention page CTAs per layer
-    const bool per_layer_pages = !(std::getenv("QT_DEC_PAGES") && std::atoi(std::getenv("QT_DEC_PAGES")) == 0);
     cudaGraphExec_t graph = nullptr;
     bool graph_ok = false;
     int decode_steps = 0;
@@ -281,7 +271,7 @@ struct qt_engine {
     std::vector<std::vector<PruneEv>> trace;
     std::vector<int> h_kvlen;             // [L][B]
     bool prefilled = false;
-    bool use_tc05 = !(std::getenv("QT_TC05") && std::atoi(std::getenv("QT_TC05")) == 0);  // tcgen05 GEMM for M > 16
+    static constexpr bool use_tc05 = true;  // tcgen05 GEMM for token-rich launches (M > 64)
     std::unique_ptr<Profiler> prof;      // active while profiling one call
     bool prof_next = false;
     double prof_out[P_NCLASS * 4] = {0};
@@ -293,18 +283,6 @@ struct qt_engine {
     }
     std::vector<int> h_next;
 
-    // persistent decode kernel (k_decode_mk.cu) for B <= 8
-    qt::MkLayer* mk_layers = nullptr;
-    int* mk_acc = nullptr;
-    int mk_acc_off[5] = {0, 0, 0, 0, 0};
-    int mk_acc_ld[5] = {0, 0, 0, 0, 0};
-    uint8_t* mk_codes = nullptr;
-    double* mk_sa = nullptr;
-    float* mk_attn = nullptr;
-    unsigned* mk_sync = nullptr;
-    double* mk_act = nullptr;
-    int mk_grid = 0, mk_smem = 0, mk_nslot = 0, mk_a_ld = 0, mk_acc_rows = 0;
-    bool mk_possible = false;
     // full-precision calibration forward (k_fp.cu)
     bool keep_fp = false;
     std::vector<std::vector<double>>* rec_blocks = nullptr;  // block outputs of the next prefill (B = 1)
@@ -318,7 +296,6 @@ struct qt_engine {
     double* fp_head = nullptr;
     cublasHandle_t blas = nullptr;
     // int8-operand prefill GEMM (k_gemm_tc05_i8): activation codes as int8 next to the packed ones
-    const bool i8_on = !(std::getenv("QT_I8") && std::atoi(std::getenv("QT_I8")) == 0);
     int8_t* codes8 = nullptr;
     int ld8 = 0;
     int8_t* head8 = nullptr;
@@ -342,13 +319,8 @@ struct qt_engine {
         }
         qt::g_pdl_block = true;
     }
-    // decode attention: merge + attn_out quantizer by the last page / head arrivals (k_attn.cu)
-    const bool attn_last = std::getenv("QT_ATTN_LAST") && std::atoi(std::getenv("QT_ATTN_LAST")) == 1;  // opt-in: slower
-    unsigned* dec_cnt = nullptr;
-    float* dec_hmax = nullptr;
     // per-row partial max |x| of the mlp_mid site left by the gate|up GEMM epilogue (act_mode 1)
     static constexpr int kPmaxLd = 512;
-    const bool use_pmax = !(std::getenv("QT_PMAX") && std::atoi(std::getenv("QT_PMAX")) == 0);
     float* pmax = nullptr;
     int pm_parts = 0;
     float* pm_ptr = nullptr;  // where the last producer left them, row stride pm_ld
@@ -357,16 +329,6 @@ struct qt_engine {
     // end of every step) instead of one partial per GEMV CTA
     float* gmax = nullptr;
     int* splitk_ws = nullptr;     // int32 split-K partials of the tcgen05 GEMM at small M
-    unsigned* seq_cnt = nullptr;  // per-sequence arrival counters of the fused decode attention block
-    // opt-in (QT_ATTN_FUSED=1): one kernel for RoPE + KV append + attention + attn_out quant; measured
-    // no faster than the three-kernel PDL chain at B = 8
-    // opt-in (QT_DEC_ROPE_FUSED=1): RoPE + new-token K/V append inside the decode attention kernel;
-    // measured slower (the last-page CTAs become stragglers), DESIGN.md §4
-    bool rope_fused = std::getenv("QT_DEC_ROPE_FUSED") && std::atoi(std::getenv("QT_DEC_ROPE_FUSED")) == 1;
-    bool fused_attn = std::getenv("QT_ATTN_FUSED") && std::atoi(std::getenv("QT_ATTN_FUSED")) == 1;
-    unsigned long long* mk_trace = nullptr;
-    // opt-in (QT_DECODE_MK=1): measured slower than the graph path at B = 8
-    bool use_mk = std::getenv("QT_DECODE_MK") && std::atoi(std::getenv("QT_DECODE_MK")) == 1;
 
     ~qt_engine() {
         cudaStreamSynchronize(st ? st : 0);
@@ -388,7 +350,7 @@ struct qt_engine {
             for (double* p : fl.w) f(p);
         f(fp_head);
         if (blas) cublasDestroy(blas);
-        f(splitk_ws); f(codes8); f(head8); f(pmax); f(gmax); f(dec_cnt); f(dec_hmax); f(seq_cnt); f(mk_trace); f(mk_layers); f(mk_acc); f(mk_codes); f(mk_sa); f(mk_attn); f(mk_sync); f(mk_act);
+        f(splitk_ws); f(codes8); f(head8); f(pmax); f(gmax);
         if (pin) cudaFreeHost(pin);
         if (cst) {
             cudaStreamSynchronize(cst);
@@ -484,7 +446,7 @@ struct qt_engine {
         mid = dalloc<float>(T * dff);
         codes_rows = round_up(std::max((int)T, mb), 16);
         codes = dalloc<uint8_t>((size_t)codes_rows * std::max(kd_pad, kff_pad) / 2);  // tiled rows
-        if (i8_on && use_tc05 && (int)T > 64) {
+        if ((int)T > 64) {
             ld8 = std::max(kd_pad, kff_pad);
             codes8 = dalloc<int8_t>((size_t)codes_rows * ld8);
         }
@@ -532,9 +494,6 @@ struct qt_engine {
         dec_splits = max_pages;
         part_ml = dalloc<float>((size_t)mb * H * dec_splits * 2);
         part_o = dalloc<float>((size_t)mb * H * dec_splits * dh);
-        seq_cnt = dalloc<unsigned>(mb);
-        dec_cnt = dalloc<unsigned>((size_t)mb * H + mb);
-        dec_hmax = dalloc<float>((size_t)mb * H);
         {  // split-K workspace: the largest ksplit * M * N over the GEMM shapes that split
             const int shapes[5][2] = {{n_qkv, kd_pad}, {d, kd_pad}, {n_gu, kd_pad}, {d, kff_pad}, {d, kd_pad}};
             size_t need = 0;
@@ -546,66 +505,14 @@ struct qt_engine {
                 }
             if (need) splitk_ws = dalloc<int>(need);
         }
-        if (cfg.act_mode == 1 && use_pmax) {
+        if (cfg.act_mode == 1) {
             pmax = dalloc<float>((size_t)std::max(mt, mb) * kPmaxLd);
             gmax = dalloc<float>((size_t)L * mb);
         }
-        mk_init();
         pin_cap = (size_t)64 << 20;
         pin_cap += (size_t)mt * (sizeof(int) * 8);
         ck(cudaMallocHost(&pin, pin_cap), "cudaMallocHost");
         ck(cudaDeviceSynchronize(), "init");  // every zero-fill of dalloc (legacy stream) has landed
-    }
-
-    // persistent decode kernel: device layer table, accumulators, smem plan
-    void mk_init() {
-        int dev = 0, sms = 0, smem_max = 0;
-        ck(cudaGetDevice(&dev), "device");
-        ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "sm count");
-        ck(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev), "smem");
-        mk_grid = sms;
-        const int Ns[5] = {n_qkv, d, n_gu, d, d};
-        const int Ks[5] = {kd_pad, kd_pad, kd_pad, kff_pad, kd_pad};
-        const int lds[5] = {n_qkv_pad, nd_pad, n_gu_pad, nd_pad, nd_pad};
-        int off = 0;
-        mk_acc_rows = 0;
-        for (int i = 0; i < 5; ++i) {
-            mk_acc_off[i] = off;
-            mk_acc_ld[i] = lds[i];
-            off += 8 * lds[i];
-            const long long rb = (Ns[i] + 15) / 16, kt = Ks[i] / 128, T = rb * kt;
-            const long long per = (T + mk_grid - 1) / mk_grid;
-            mk_acc_rows = std::max(mk_acc_rows, (int)((per + kt - 1) / kt + 2));
-        }
-        mk_acc = dalloc<int>(off);
-        ck(cudaMemset(mk_acc, 0, (size_t)off * sizeof(int)), "mk acc");
-        mk_codes = dalloc<uint8_t>((size_t)16 * std::max(kd_pad, kff_pad) / 2);
-        ck(cudaMemset(mk_codes, 0, (size_t)16 * std::max(kd_pad, kff_pad) / 2), "mk codes");
-        mk_sa = dalloc<double>(16);
-        mk_attn = dalloc<float>((size_t)8 * d);
-        mk_sync = dalloc<unsigned>(256);
-        mk_act = dalloc<double>(4 * L + 1);
-        ck(cudaMemset(mk_act, 0, (4 * L + 1) * sizeof(double)), "mk act");
-        const int fixed = qt_decode_mk_smem(std::max(kd_pad, kff_pad), mk_acc_rows, 0, &mk_a_ld);
-        mk_nslot = (smem_max - fixed - 1024) / (8192 + 16);
-        if (const char* ns = std::getenv("QT_MK_NSLOT")) mk_nslot = std::min(mk_nslot, std::atoi(ns));  // debug
-        mk_smem = qt_decode_mk_smem(std::max(kd_pad, kff_pad), mk_acc_rows, mk_nslot, &mk_a_ld);
-        std::vector<qt::MkLayer> tab(L);
-        for (int l = 0; l < L; ++l) {
-            qt::MkLayer& m = tab[l];
-            m.w[0] = lw[l].qkv; m.w[1] = lw[l].o; m.w[2] = lw[l].gu; m.w[3] = lw[l].down;
-            m.s[0] = lw[l].s_qkv; m.s[1] = lw[l].s_o; m.s[2] = lw[l].s_gu; m.s[3] = lw[l].s_down;
-            m.rows_pad[0] = n_qkv_pad; m.rows_pad[1] = nd_pad; m.rows_pad[2] = n_gu_pad; m.rows_pad[3] = nd_pad;
-            m.g1 = lw[l].g1;
-            m.g2 = lw[l].g2;
-            m.pt = pt + (size_t)l * max_batch * max_pages;
-            m.kv_len = kv_len + (size_t)l * max_batch;
-        }
-        mk_layers = dalloc<qt::MkLayer>(L);
-        h2d(mk_layers, tab.data(), L * sizeof(qt::MkLayer), "mk layers");
-        // staging rows of the owner phases live in the activation-row region (8 * a_ld bytes)
-        mk_possible = mk_nslot >= 4 && (dh == 64 || dh == 128) && H <= 64 && 8 * mk_a_ld >= 8 * d &&
-                      8 * mk_a_ld >= 4 * dff && B_MAX_MK >= 1;
     }
 
     // ------------------------------------------------------------ calibration (fp64 forward)
@@ -1003,61 +910,6 @@ struct qt_engine {
         }
     }
 
-    static constexpr int B_MAX_MK = 8;
-    bool mk_usable() const { return use_mk && mk_possible && B >= 1 && B <= 8; }
-
-    void decode_mk() {
-        qt::MkParams p{};
-        p.layers = mk_layers;
-        p.L = L; p.d = d; p.H = H; p.Hkv = Hkv; p.dh = dh; p.dff = dff; p.mlp = cfg.mlp; p.act_mode = cfg.act_mode;
-        p.B = B;
-        p.N[0] = n_qkv; p.N[1] = d; p.N[2] = n_gu; p.N[3] = d;
-        p.Kp[0] = kd_pad; p.Kp[1] = kd_pad; p.Kp[2] = kd_pad; p.Kp[3] = kff_pad;
-        p.head = head; p.s_head = s_head; p.head_rows_pad = nd_pad; p.gf = gf;
-        p.act = mk_act;
-        p.x = xd;
-        for (int i = 0; i < 5; ++i) {
-            p.acc[i] = mk_acc + mk_acc_off[i];
-            p.acc_ld[i] = mk_acc_ld[i];
-        }
-        p.codes = mk_codes; p.sa = mk_sa; p.attn = mk_attn;
-        p.pool = pool; p.page_bytes = page_bytes; p.max_pages = max_pages;
-        p.rope = reinterpret_cast<const double2*>(rope);
-        p.next_pos = next_pos;
-        p.logits = dlogits;
-        p.sync = mk_sync;
-        p.nslot = mk_nslot; p.a_ld = mk_a_ld; p.acc_rows = mk_acc_rows;
-        static const char* trace_path = std::getenv("QT_MK_TRACE");  // debug: per-phase timestamps
-        const size_t tn = (size_t)mk_grid * (L + 1) * 32;
-        if (trace_path && !mk_trace) {
-            mk_trace = dalloc<unsigned long long>(tn);
-        }
-        if (mk_trace) ck(cudaMemsetAsync(mk_trace, 0, tn * 8, st), "trace");
-        p.trace = mk_trace;
-        ck(cudaMemsetAsync(mk_sync, 0, 256 * sizeof(unsigned), st), "mk sync reset");
-        qt::g_pdl_block = true;
-        pb(P_GEMM);
-        ckl(qt_launch_decode_mk(&p, dh, mk_grid, mk_smem, st), "decode megakernel");
-        if (mk_trace) {
-            std::vector<unsigned long long> h(tn);
-            ck(cudaMemcpyAsync(h.data(), mk_trace, tn * 8, cudaMemcpyDeviceToHost, st), "trace");
-            ck(cudaStreamSynchronize(st), "trace");
-            if (FILE* fo = std::fopen(trace_path, "wb")) {
-                std::fwrite(h.data(), 8, tn, fo);
-                std::fclose(fo);
-            }
-        }
-        double wbytes = (double)L * ((double)n_qkv * kd_pad / 2 + (double)d * kd_pad / 2 + (double)n_gu * kd_pad / 2 +
-                                     (double)d * kff_pad / 2 + 8.0 * (n_qkv + d + n_gu + d)) +
-                        (double)d * kd_pad / 2 + 8.0 * d;
-        double kvb = 0;
-        for (int v : h_kvlen) kvb += (double)(v + 1) * Hkv * 2 * (dh / 2 + 4);
-        const double flops = 2.0 * B * ((double)L * ((double)n_qkv * kd_pad + (double)d * kd_pad +
-                                                     (double)n_gu * kd_pad + (double)d * kff_pad) +
-                                        (double)d * kd_pad);
-        pe(wbytes + kvb, flops);
-    }
-
     void ensure_pool(int pages) {
         if (pages <= n_pages_cap) return;
         ck(cudaStreamSynchronize(st), "sync");
@@ -1180,7 +1032,6 @@ struct qt_engine {
                                               splitk_ws, pm, kPmaxLd, &pm_parts, st)
                      : qt_launch_w4a4_mma_ex(epi, codes, codes_rows, ascale, w, wrows, sw, M, N, K, out, ldo, nullptr,
                                              pm, pld, &pm_parts, st);
-        qt::g_l2_next = nullptr;  // consumed by the GEMV launcher; never carried past this launch
         ckl(rc, "w4a4 gemm");
         const double out_bytes = epi == QT_EPI_RESADD ? 16.0 * M * N : (epi == QT_EPI_SWIGLU ? 2.0 * M * N : 4.0 * M * N);
         pe((double)N * K / 2 + 8.0 * N + (double)M * K / 2 + 8.0 * M + out_bytes, 2.0 * M * N * K);
@@ -1512,7 +1363,6 @@ struct qt_engine {
                 dec_pages[l] = std::max(dec_pages[l], (cap + qt::kPage - 1) / qt::kPage);
                 maxp = std::max(maxp, dec_pages[l]);
             }
-        if (!per_layer_pages) std::fill(dec_pages.begin(), dec_pages.end(), maxp);
         dec_pps = 1;  // one 64-row page per decode-attention CTA
         dec_splits = maxp;
         ck(cudaStreamSynchronize(st), "prefill");
@@ -1522,14 +1372,7 @@ struct qt_engine {
     }
 
     // ------------------------------------------------------------ decode
-    // the next decode GEMV's weights, prefetched toward L2 by the GEMV launched next (qt_common.cuh)
-    const bool l2_next_on = std::getenv("QT_L2NEXT") && std::atoi(std::getenv("QT_L2NEXT")) != 0;  // opt-in: measured slower
-    void l2_next(const void* w, size_t bytes) {
-        if (!l2_next_on) return;
-        qt::g_l2_next = w;
-        qt::g_l2_next_bytes = (long long)bytes;
-    }
-    int skip_mask = g_skip;  // kernel classes left out of decode_body (1 GEMM, 2 attention, 4 quant, 8 kv)
+    int skip_mask = 0;  // kernel classes left out of decode_body (profile_chain: 1 GEMM, 2 attention, 4 quant, 8 kv)
     void decode_body() {
         double* xcur = xd;  // the step's input was written (widened) into xd before the graph
         for (int l = 0; l < L; ++l) {
@@ -1537,52 +1380,33 @@ struct qt_engine {
             int* ptl = pt + (size_t)l * max_batch * max_pages;
             int* lenl = kv_len + (size_t)l * max_batch;
             if (!(skip_mask & 4)) norm_quant(xcur, 1, d, w.g1, B, d, kd_pad, 4 * l + 0);
-            l2_next(w.o, (size_t)nd_pad * kd_pad / 2);
             if (!(skip_mask & 1)) gemm(QT_EPI_STORE, w.qkv, n_qkv_pad, w.s_qkv, B, n_qkv, kd_pad, qkv, n_qkv);
-            if (fused_attn) {
-                // RoPE + K/V append + attention + attn_out quantizer in one kernel
-                pb(P_ATTN);
-                ckl(qt_launch_attn_dec_fused(qkv, n_qkv, H, Hkv, dh, next_pos, lenl, rope, ptl, max_pages, pool,
-                                             page_bytes, attn, d, seq_cnt, codes, codes_rows, ascale, cfg.act_mode,
-                                             cfg.act_mode == 0 ? act[4 * l + 1] : 0.0, kd_pad, 4, B, st),
-                    "decode attention block");
+            pb(P_KV);
+            if (!(skip_mask & 8))
+                ckl(qt_launch_rope_kv_append(qkv, n_qkv, B, H, Hkv, dh, next_pos, dec_seq, lenl, rope, ptl, max_pages,
+                                             pool, page_bytes, 4, nullptr, st),
+                    "decode kv append");
+            pe((double)B * n_qkv * 8 + (double)B * Hkv * 2 * (dh / 2 + 4));
+            pb(P_ATTN);
+            // decode attention over the int4 pages + split merge fused with the attn_out quantizer
+            if (!(skip_mask & 2))
+                ckl(qt_launch_attn_decode(qkv, n_qkv, H, Hkv, dh, lenl, 1, B, pool, page_bytes, ptl, max_pages,
+                                          dec_pages[l], part_ml, part_o, nullptr, d, codes, codes_rows, ascale,
+                                          cfg.act_mode, cfg.act_mode == 0 ? act[4 * l + 1] : 0.0, kd_pad, 4, nullptr,
+                                          nullptr, nullptr, nullptr, nullptr, st),
+                    "decode attention");
+            {  // decode attention streams every cached K/V row of this layer once
                 double rows = 0;
                 for (int b = 0; b < B; ++b) rows += h_kvlen[(size_t)l * B + b] + 1;
-                pe(rows * Hkv * 2 * (dh / 2 + 4) + (double)B * n_qkv * 4 + (double)B * d * 8);
-            } else {
-                if (!rope_fused) {
-                    pb(P_KV);
-                    if (!(skip_mask & 8)) ckl(qt_launch_rope_kv_append(qkv, n_qkv, B, H, Hkv, dh, next_pos, dec_seq, lenl, rope, ptl, max_pages,
-                                                 pool, page_bytes, 4, nullptr, st),
-                        "decode kv append");
-                    pe((double)B * n_qkv * 8 + (double)B * Hkv * 2 * (dh / 2 + 4));
-                }
-                pb(P_ATTN);
-                // decode attention over int4 pages (RoPE + K/V append fused in) + split merge fused
-                // with the attn_out quantizer
-                if (!(skip_mask & 2))
-                    ckl(qt_launch_attn_decode(qkv, n_qkv, H, Hkv, dh, lenl, 1, B, pool, page_bytes, ptl, max_pages,
-                                              dec_pages[l], part_ml, part_o, nullptr, d, codes, codes_rows, ascale,
-                                              cfg.act_mode, cfg.act_mode == 0 ? act[4 * l + 1] : 0.0, kd_pad, 4,
-                                              rope_fused ? rope : nullptr, rope_fused ? next_pos : nullptr,
-                                              attn_last ? dec_cnt : nullptr, attn, dec_hmax, st),
-                        "decode attention");
-                {  // decode attention streams every cached K/V row of this layer once
-                    double rows = 0;
-                    for (int b = 0; b < B; ++b) rows += h_kvlen[(size_t)l * B + b] + 1;
-                    pe(rows * Hkv * 2 * (dh / 2 + 4) + (double)B * H * dh * 8);
-                }
+                pe(rows * Hkv * 2 * (dh / 2 + 4) + (double)B * H * dh * 8);
             }
-            l2_next(w.gu, (size_t)n_gu_pad * kd_pad / 2);
             if (!(skip_mask & 1)) gemm(QT_EPI_RESADD, w.o, nd_pad, w.s_o, B, d, kd_pad, xcur, d);
             if (!(skip_mask & 4)) norm_quant(xcur, 1, d, w.g2, B, d, kd_pad, 4 * l + 2);
-            l2_next(w.down, (size_t)nd_pad * kff_pad / 2);
             float* gml = gmax ? gmax + (size_t)l * max_batch : nullptr;
-            if (skip_mask & 1) {} else if (cfg.mlp == 1) gemm(QT_EPI_SWIGLU, w.gu, n_gu_pad, w.s_gu, B, n_gu, kd_pad, mid, dff, true, nullptr, gml);
-            else gemm(QT_EPI_SILU, w.gu, n_gu_pad, w.s_gu, B, n_gu, kd_pad, mid, dff, true, nullptr, gml);
+            if (!(skip_mask & 1))
+                gemm(cfg.mlp == 1 ? QT_EPI_SWIGLU : QT_EPI_SILU, w.gu, n_gu_pad, w.s_gu, B, n_gu, kd_pad, mid, dff, true,
+                     nullptr, gml);
             if (!(skip_mask & 4)) norm_quant(mid, 0, dff, nullptr, B, dff, kff_pad, 4 * l + 3, true);
-            if (l + 1 < L) l2_next(lw[l + 1].qkv, (size_t)n_qkv_pad * kd_pad / 2);
-            else l2_next(head, (size_t)nd_pad * kd_pad / 2);
             if (!(skip_mask & 1)) gemm(QT_EPI_RESADD, w.down, nd_pad, w.s_down, B, d, kff_pad, xcur, d);
         }
         norm_quant(xcur, 1, d, gf, B, d, kd_pad, 4 * L);
@@ -1681,9 +1505,7 @@ struct qt_engine {
             ckl(qt_launch_f32_to_f64(xd_in, xd, (long long)B * d, st), "embedding widen");
             pe((double)B * d * 12);
         }
-        if (mk_usable()) {
-            decode_mk();  // one persistent kernel for the whole step
-        } else if (g_nograph || profiling) {
+        if (profiling) {
             decode_body();  // eager launches so every kernel gets its own events
         } else if (!graph_ok) {
             if (graph) cudaGraphExecDestroy(graph);
@@ -1705,7 +1527,7 @@ struct qt_engine {
             cudaGraphDestroy(g);
             graph_ok = true;
         }
-        if (!mk_usable() && !g_nograph && !profiling) ck(cudaGraphLaunch(graph, st), "graph launch");
+        if (!profiling) ck(cudaGraphLaunch(graph, st), "graph launch");
         if (out)
             ck(cudaMemcpyAsync(out, dlogits, (size_t)B * d * sizeof(float),
                                out_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st),
@@ -2123,7 +1945,6 @@ int qt_engine_set_act_scales(qt_engine* e, const double* scales) {
         e->act.assign(scales, scales + 4 * e->L + 1);
         for (double s : e->act)
             if (!(s > 0.0) || !std::isfinite(s)) fail(QT_EINVAL, "activation scales must be positive");
-        e->h2d(e->mk_act, e->act.data(), e->act.size() * sizeof(double), "act");
         e->act_set = true;
         e->graph_ok = false;
     });

@@ -1083,8 +1083,7 @@ int qt_launch_attn_decode(const float* qkv, int ldq, int H, int Hkv, int dh, con
     if (B <= 0) return 0;
     if (H > 64) return -1;
     // two 64-row pages per CTA (unfused path, dh = 128): half the CTAs, half the partials
-    static const int ppc_env = getenv("QT_ATTN_PPC") ? atoi(getenv("QT_ATTN_PPC")) : 2;
-    const int ppc = (ppc_env == 2 || ppc_env == 4) && !rope && !counters && dh == 128 ? ppc_env : 1;
+    const int ppc = !rope && !counters && dh == 128 ? 2 : 1;
     const bool pp2 = ppc > 1;
     if (pp2) n_pages = (n_pages + ppc - 1) / ppc;
     const dim3 grid(n_pages, H, B);
@@ -1092,7 +1091,7 @@ int qt_launch_attn_decode(const float* qkv, int ldq, int H, int Hkv, int dh, con
     const int qmax = (1 << (bits - 1)) - 1;
     int rc;
     if (dh == 128) {
-        rc = pp2 ? launch_pdl(ppc == 4 ? k_attn_decode_pp2<128, 4> : k_attn_decode_pp2<128, 2>, grid, dim3(128), 0, st, qkv, ldq, H, Hkv, kv_len, len_add, pool,
+        rc = pp2 ? launch_pdl(k_attn_decode_pp2<128, 2>, grid, dim3(128), 0, st, qkv, ldq, H, Hkv, kv_len, len_add, pool,
                               page_bytes, pt, max_pages, inv_sqrt, part_ml, part_o, rt, pos, counters, row, hmax,
                               codes, ld_codes, scales, qmode, static_scale, d_pad, qmax)
                  : launch_pdl(k_attn_decode<128>, grid, dim3(128), 0, st, qkv, ldq, H, Hkv, kv_len, len_add, pool,

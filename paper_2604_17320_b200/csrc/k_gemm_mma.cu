@@ -152,8 +152,8 @@ __global__ void __launch_bounds__(256) k_gemm_tc(const uint8_t* __restrict__ A, 
 
 // ---------------------------------------------------------------- decode GEMV
 // row blocks per CTA beyond the first whose weights are L2-prefetched before the
-// dependency wait (QT_GEMV_L2 to override; 0 disables)
-static const int qt_gemv_l2_rows_host = getenv("QT_GEMV_L2") ? atoi(getenv("QT_GEMV_L2")) : 1;
+// dependency wait
+constexpr int kGemvL2Rows = 1;
 // Persistent, HBM-streaming GEMV for decode (M <= 16 tokens).  Each CTA owns a
 // strided set of 16-channel row blocks; its 8 warps split K.  The token codes
 // are staged once per CTA in smem.  Weight loads run one batch (U tiles of
@@ -170,7 +170,6 @@ static const int qt_gemv_l2_rows_host = getenv("QT_GEMV_L2") ? atoi(getenv("QT_G
 #ifndef QT_GEMV_MINB
 #define QT_GEMV_MINB 2  // 3 spills (80 regs) and measured slower
 #endif
-static const int qt_gemv_ctas = getenv("QT_GEMV_CTAS") ? atoi(getenv("QT_GEMV_CTAS")) : QT_GEMV_MINB;
 // AREG (NT = 1, K <= 4096: one batch per row block): each lane's activation fragments for its
 // k slice are loaded once into registers after the dependency wait -- no smem staging, no
 // block barrier before the first MMA.
@@ -179,7 +178,6 @@ __global__ void __launch_bounds__(256, NT <= 2 ? QT_GEMV_MINB : 1) k_gemv_reg(co
                                                   const uint8_t* __restrict__ W, int ldw, const double* __restrict__ sw,
                                                   int M, int N, int K, void* __restrict__ out, int ldo,
                                                   int* __restrict__ acc_dbg, int l2rows,
-                                                  const uint8_t* __restrict__ pf, long long pf_bytes,
                                                   float* __restrict__ pmax, int pmax_ld) {
     constexpr int TOK = 8 * NT;
     constexpr bool ASM = NT <= 2 && !AREG;  // activation codes staged in smem
@@ -225,14 +223,6 @@ __global__ void __launch_bounds__(256, NT <= 2 ? QT_GEMV_MINB : 1) k_gemv_reg(co
             for (int c = ch0 + U + (lane >> 3); c < ch1; c += 4)
                 asm volatile("prefetch.global.L2 [%0];\n" ::"l"(W + ((size_t)c * (ldw >> 4) + rb) * 1024 +
                                                                (lane & 7) * 128));
-    }
-    if (pf && warp == 7) {  // the next GEMV's weights: this CTA's 4 KB-aligned slice, 16 KB per bulk prefetch
-        const long long per = ((pf_bytes / gridDim.x) + 4095) & ~4095LL;
-        const long long end = min(pf_bytes, (long long)(blockIdx.x + 1) * per);
-        for (long long o = (long long)blockIdx.x * per + lane * 16384LL; o < end; o += 32 * 16384LL) {
-            const unsigned sz = (unsigned)min(16384LL, end - o);
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(pf + o), "r"(sz) : "memory");
-        }
     }
     pdl_wait();
     uint4 bA[AREG ? U : 1][AREG ? NT : 1];
@@ -388,10 +378,6 @@ int launch_gemm(const uint8_t* A, int lda, const double* sa, const uint8_t* W, i
     if (M <= 0) return 0;
     if (K % 128 || lda % 16 || ldw % 16 || M > lda || N > ldw) return -1;  // lda/ldw = padded rows
     const int nb = (N + GB_N - 1) / GB_N;
-    const uint8_t* pf = static_cast<const uint8_t*>(g_l2_next);
-    const long long pf_bytes = g_l2_next_bytes;
-    g_l2_next = nullptr;
-    g_l2_next_bytes = 0;
     float* pm = nullptr;  // GEMV paths: one partial-max slot per CTA
     auto want_pmax = [&](int ctas) {
         if (pmax && (pmax_ld == 0 || ctas <= pmax_ld)) {
@@ -411,7 +397,7 @@ int launch_gemm(const uint8_t* A, int lda, const double* sa, const uint8_t* W, i
             auto kfn = k_gemv_reg<4, EPI>;
             cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             return launch_pdl(kfn, grid, dim3(256), smem, st, A, lda, sa, W, ldw, sw, M, N, K, out, ldo, acc_dbg,
-                              qt_gemv_l2_rows_host, pf, pf_bytes, pm, pmax_ld);
+                              kGemvL2Rows, pm, pmax_ld);
         }
         if (lda >= 64) {
             want_pmax((int)grid.x);
@@ -419,7 +405,7 @@ int launch_gemm(const uint8_t* A, int lda, const double* sa, const uint8_t* W, i
             auto kfn = k_gemv_reg<8, EPI>;
             cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             return launch_pdl(kfn, grid, dim3(256), smem, st, A, lda, sa, W, ldw, sw, M, N, K, out, ldo, acc_dbg,
-                              qt_gemv_l2_rows_host, pf, pf_bytes, pm, pmax_ld);
+                              kGemvL2Rows, pm, pmax_ld);
         }
     }
     if (M <= 16) {
@@ -429,34 +415,26 @@ int launch_gemm(const uint8_t* A, int lda, const double* sa, const uint8_t* W, i
         const int n_rb = (N + 15) / 16;
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-        const dim3 grid(std::min(n_rb, qt_gemv_ctas * sms));
+        const dim3 grid(std::min(n_rb, QT_GEMV_MINB * sms));
         want_pmax((int)grid.x);
-        static const bool areg_on = !(getenv("QT_GEMV_AREG") && atoi(getenv("QT_GEMV_AREG")) == 0);
-        static const bool areg2_on = getenv("QT_GEMV_AREG2") && atoi(getenv("QT_GEMV_AREG2")) == 1;
-        if (TOK == 16 && areg2_on && (K / 128 + 7) / 8 <= 4) {
-            const size_t smem2 = (size_t)2 * 8 * 16 * TOK * 4;
-            auto kfn = k_gemv_reg<2, EPI, true>;
-            cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
-            return launch_pdl(kfn, grid, dim3(256), smem2, st, A, lda, sa, W, ldw, sw, M, N, K, out, ldo, acc_dbg,
-                              qt_gemv_l2_rows_host, pf, pf_bytes, pm, pmax_ld);
-        }
-        if (TOK == 8 && areg_on && (K / 128 + 7) / 8 <= 4) {
+        // AREG: K <= 4096 is one register batch per warp (the 9..16-token variant spills)
+        if (TOK == 8 && (K / 128 + 7) / 8 <= 4) {
             const size_t smem2 = (size_t)2 * 8 * 16 * TOK * 4;  // split-K reduction buffers only
             auto kfn = k_gemv_reg<1, EPI, true>;
             cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
             return launch_pdl(kfn, grid, dim3(256), smem2, st, A, lda, sa, W, ldw, sw, M, N, K, out, ldo, acc_dbg,
-                              qt_gemv_l2_rows_host, pf, pf_bytes, pm, pmax_ld);
+                              kGemvL2Rows, pm, pmax_ld);
         }
         if (TOK == 8) {
             auto kfn = k_gemv_reg<1, EPI>;
             cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             return launch_pdl(kfn, grid, dim3(256), smem, st, A, lda, sa, W, ldw, sw, M, N, K, out, ldo, acc_dbg,
-                              qt_gemv_l2_rows_host, pf, pf_bytes, pm, pmax_ld);
+                              kGemvL2Rows, pm, pmax_ld);
         }
         auto kfn = k_gemv_reg<2, EPI>;
         cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         return launch_pdl(kfn, grid, dim3(256), smem, st, A, lda, sa, W, ldw, sw, M, N, K, out, ldo, acc_dbg,
-                              qt_gemv_l2_rows_host, pf, pf_bytes, pm, pmax_ld);
+                              kGemvL2Rows, pm, pmax_ld);
     }
     if (M <= 512 || (long long)((M + 127) / 128) * nb < 148) {
         constexpr int BM = 64;

@@ -709,38 +709,14 @@ extern "C" int qt_launch_w4a4_tc05_i8(int epi, const int8_t* A8, int lda8, const
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     const int mt_n = (M + T5_BM - 1) / T5_BM, nt_n = (N + T5_BN - 1) / T5_BN;
-    // cluster pairs along M share the weight tile (TMA multicast) when there are M tiles to pair
-    static const int cl_env = getenv("QT_I8_CL") ? atoi(getenv("QT_I8_CL")) : 1;  // 2: opt-in, measured slower
-    const int CL = (cl_env == 2 && mt_n >= 2) ? 2 : 1;
-    const int units = ((mt_n + CL - 1) / CL) * nt_n;
-    const dim3 grid(std::min(units, sms / CL) * CL);
+    const int units = mt_n * nt_n;
+    const dim3 grid(std::min(units, sms));
     const int parts = 2 * nt_n;
     if (pmax && parts > pmax_ld) pmax = nullptr;
     if (pmax && n_part) *n_part = parts;
     const size_t smem = T8Smem::total;
-    if (CL == 2 && qt_tmap_i8(&tb, W8, w_rows, K, ldw8, T5_BN / 2)) return -2;  // half-tile boxes
 #define QT_T8(E)                                                                                                    \
     do {                                                                                                            \
-        if (CL == 2) {                                                                                              \
-            auto kfn = k_gemm_tc05_i8<E, 2>;                                                                        \
-            cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                      \
-            cudaLaunchConfig_t cfg = {};                                                                            \
-            cfg.gridDim = grid;                                                                                     \
-            cfg.blockDim = dim3(T8_THREADS);                                                                        \
-            cfg.dynamicSmemBytes = smem;                                                                            \
-            cfg.stream = st;                                                                                        \
-            cudaLaunchAttribute at[2];                                                                              \
-            at[0].id = cudaLaunchAttributeClusterDimension;                                                         \
-            at[0].val.clusterDim.x = 2;                                                                             \
-            at[0].val.clusterDim.y = 1;                                                                             \
-            at[0].val.clusterDim.z = 1;                                                                             \
-            at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;                                          \
-            at[1].val.programmaticStreamSerializationAllowed = 1;                                                   \
-            cfg.attrs = at;                                                                                         \
-            cfg.numAttrs = (getenv("QT_NOPDL") || g_pdl_block) ? 1 : 2;                                             \
-            g_pdl_block = false;                                                                                    \
-            return (int)cudaLaunchKernelEx(&cfg, kfn, ta, tb, sa, sw, M, N, K, out, ldo, acc_dbg, pmax, pmax_ld);   \
-        }                                                                                                           \
         auto kfn = k_gemm_tc05_i8<E, 1>;                                                                            \
         cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                          \
         return launch_pdl(kfn, grid, dim3(T8_THREADS), smem, st, ta, tb, sa, sw, M, N, K, out, ldo, acc_dbg, pmax,  \

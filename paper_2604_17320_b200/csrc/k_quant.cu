@@ -11,8 +11,6 @@
 // All quantizer arithmetic is fp64 (the reference's type), so an int4 code
 // equals the reference code for the same fp32 input; the fp32 scale handed to
 // the GEMM epilogue is the rounded fp64 scale.
-#include <cooperative_groups.h>
-
 #include "qt_common.cuh"
 #include "qt_kernels.h"
 
@@ -245,91 +243,6 @@ __global__ void __launch_bounds__(256) k_quant_pmax(const float* __restrict__ x,
         if (codes8) *reinterpret_cast<uint2*>(codes8 + (size_t)row * ld8 + w * 8) = pack8_i8x16(c);
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) scales[row] = s;
-}
-
-// K1 for few rows (decode): a cluster of CL CTAs per row, each owning a slice
-// of 8-element words in registers; the RMS sum and the row max are reduced
-// across the cluster through distributed shared memory in rank order (fixed,
-// deterministic).  Spreads one row over CL SMs so the row's loads run in
-// parallel instead of through one SM.
-template <typename TX, int CL, int G>
-__global__ void __launch_bounds__(128) k_norm_quant_cl(const TX* __restrict__ x, int ld_x,
-                                                      const float* __restrict__ gain, int M, int D, int d_pad,
-                                                      int qmax, int mode, double static_scale,
-                                                      uint8_t* __restrict__ codes, int ld_codes,
-                                                      double* __restrict__ scales) {
-    namespace cg = cooperative_groups;
-    cg::cluster_group cluster = cg::this_cluster();
-    __shared__ double red[32];
-    __shared__ double part[2];
-    pdl_launch_dependents();
-    pdl_wait();
-    const int rank = (int)cluster.block_rank();
-    const int row = blockIdx.y;
-    const TX* xr = x + (size_t)row * ld_x;
-    const int n_words = d_pad / 8;
-    const int w0 = rank * n_words / CL, w1 = (rank + 1) * n_words / CL;
-    double v[G][8];
-#pragma unroll
-    for (int j = 0; j < G; ++j) {
-        const int w = w0 + threadIdx.x + j * 128;
-        if (w < w1 && w * 8 < D) {
-            load8<TX>(xr + w * 8, v[j]);
-        } else {
-#pragma unroll
-            for (int e = 0; e < 8; ++e) v[j][e] = 0.0;
-        }
-    }
-    if (gain) {
-        double ss = 0.0;
-#pragma unroll
-        for (int j = 0; j < G; ++j)
-#pragma unroll
-            for (int e = 0; e < 8; ++e) ss += v[j][e] * v[j][e];
-        ss = block_sum(ss, red);
-        if (threadIdx.x == 0) part[0] = ss;
-        cluster.sync();
-        double tot = 0.0;
-        for (int r = 0; r < CL; ++r) tot += *cluster.map_shared_rank(&part[0], r);
-        const double inv = 1.0 / sqrt(tot / (double)D + kNormEps);
-#pragma unroll
-        for (int j = 0; j < G; ++j) {
-            const int w = w0 + threadIdx.x + j * 128;
-            if (w < w1 && w * 8 < D) {
-                float4 g0 = *reinterpret_cast<const float4*>(gain + w * 8);
-                float4 g1 = *reinterpret_cast<const float4*>(gain + w * 8 + 4);
-                const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
-#pragma unroll
-                for (int e = 0; e < 8; ++e) v[j][e] = __dmul_rn(__dmul_rn(v[j][e], inv), (double)gg[e]);
-            }
-        }
-    }
-    double s = static_scale;
-    if (mode == 1) {
-        double mx = 0.0;
-#pragma unroll
-        for (int j = 0; j < G; ++j)
-#pragma unroll
-            for (int e = 0; e < 8; ++e) mx = fmax(mx, fabs(v[j][e]));
-        mx = block_max(mx, red);
-        if (threadIdx.x == 0) part[1] = mx;
-        cluster.sync();
-        double m = 0.0;
-        for (int r = 0; r < CL; ++r) m = fmax(m, *cluster.map_shared_rank(&part[1], r));
-        s = q_scale(m, qmax);
-    }
-    const double inv_s = 1.0 / s;
-#pragma unroll
-    for (int j = 0; j < G; ++j) {
-        const int w = w0 + threadIdx.x + j * 128;
-        if (w >= w1) continue;
-        int c[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) c[e] = w * 8 + e < D ? q_code_r(v[j][e], s, inv_s, qmax) : 0;
-        *reinterpret_cast<uint32_t*>(codes + w4t_offset(row, w * 4, ld_codes)) = pack8(c);
-    }
-    if (rank == 0 && threadIdx.x == 0) scales[row] = s;
-    cluster.sync();  // no CTA leaves while its shared partials may still be read
 }
 
 // ============================================================== K5
@@ -602,27 +515,6 @@ __global__ void k_f32_to_f64(const float* __restrict__ a, double* __restrict__ b
 // ---------------------------------------------------------------- launchers
 using namespace qt;
 
-template <typename TX, int CL, int G>
-static int launch_nq_cl(const TX* x, int ld_x, const float* gain, int M, int D, int d_pad, int qmax, int mode,
-                        double static_scale, uint8_t* codes, int ld_codes, double* scales, cudaStream_t st) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(CL, M);
-    cfg.blockDim = dim3(128);
-    cfg.stream = st;
-    cudaLaunchAttribute attr[2];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CL;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[1].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = (getenv("QT_NOPDL") || g_pdl_block) ? 1 : 2;
-    g_pdl_block = false;
-    return (int)cudaLaunchKernelEx(&cfg, k_norm_quant_cl<TX, CL, G>, x, ld_x, gain, M, D, d_pad, qmax, mode,
-                                   static_scale, codes, ld_codes, scales);
-}
-
 extern "C" {
 
 int qt_launch_f32_to_f64(const float* a, double* b, long long n, cudaStream_t st) {
@@ -636,24 +528,8 @@ int qt_launch_norm_quant(const void* x, int x_is_f64, int ld_x, const float* gai
     if (M <= 0) return 0;
     if (D % 8 || d_pad % 8 || ld_x % 4) return -1;
     const int qmax = (1 << (bits - 1)) - 1;
-    // opt-in (QT_NQ_CLUSTER=1): rows split over an 8-CTA cluster; not faster at decode sizes
-    static const bool use_cl = getenv("QT_NQ_CLUSTER") && atoi(getenv("QT_NQ_CLUSTER")) == 1;
-    if (M <= 64 && !normed && !codes8 && use_cl && d_pad / 8 <= 8 * 128 * 2) {
-        // decode-sized: 8-CTA cluster per row, up to 2 words per thread
-        const int G = d_pad / 8 <= 8 * 128 ? 1 : 2;
-        if (x_is_f64)
-            return G == 1 ? launch_nq_cl<double, 8, 1>(static_cast<const double*>(x), ld_x, gain, M, D, d_pad, qmax,
-                                                        mode, static_scale, codes, ld_codes, scales, st)
-                          : launch_nq_cl<double, 8, 2>(static_cast<const double*>(x), ld_x, gain, M, D, d_pad, qmax,
-                                                        mode, static_scale, codes, ld_codes, scales, st);
-        return G == 1 ? launch_nq_cl<float, 8, 1>(static_cast<const float*>(x), ld_x, gain, M, D, d_pad, qmax, mode,
-                                                   static_scale, codes, ld_codes, scales, st)
-                      : launch_nq_cl<float, 8, 2>(static_cast<const float*>(x), ld_x, gain, M, D, d_pad, qmax, mode,
-                                                   static_scale, codes, ld_codes, scales, st);
-    }
-    static const bool nq4 = !(getenv("QT_NQ4") && atoi(getenv("QT_NQ4")) == 0);
-    static const int nq4_max_m = getenv("QT_NQ4_M") ? atoi(getenv("QT_NQ4_M")) : 64;
-    if (nq4 && M <= nq4_max_m && !normed && d_pad / 4 <= 1024 && d_pad / 4 >= 128) {
+    // decode-sized batches: 4 elements per thread (prefill sizes measured slower with it)
+    if (M <= 64 && !normed && d_pad / 4 <= 1024 && d_pad / 4 >= 128) {
         const int th = (d_pad / 4 + 31) / 32 * 32;
         if (x_is_f64)
             return launch_pdl(k_norm_quant4<double>, dim3(M), dim3(th), 0, st, static_cast<const double*>(x), ld_x,
@@ -664,10 +540,8 @@ int qt_launch_norm_quant(const void* x, int x_is_f64, int ld_x, const float* gai
     const int words = d_pad / 8;
     int threads = words <= 256 ? 256 : (words <= 512 ? 512 : 1024);
     // token-rich launches: narrower CTAs holding more of the row per thread, so more rows
-    // (and their loads) are in flight per SM (QT_NQ_WIDE_M: the row-count threshold)
-    static const int wide_m = getenv("QT_NQ_WIDE_M") ? atoi(getenv("QT_NQ_WIDE_M")) : 256;
-    static const int wide_t = getenv("QT_NQ_WIDE_T") ? atoi(getenv("QT_NQ_WIDE_T")) : 256;  // 128 (G = 4) spills
-    if (M >= wide_m && (words + wide_t - 1) / wide_t <= 4) threads = wide_t;
+    // (and their loads) are in flight per SM (128 threads with G = 4 spills)
+    if (M >= 256 && (words + 255) / 256 <= 4) threads = 256;
     const int G = (words + threads - 1) / threads;
     if (G > 4) return -1;
 #define QT_NQ(TX, GG)                                                                                        \
@@ -695,18 +569,8 @@ int qt_launch_quant_pmax(const float* x, int ld_x, const float* pmax, int n_part
     const int words = d_pad / 8;
     // one word per thread: measured faster than whole-row CTAs with 2-8 words per thread
     // (prefill 36.5 vs 36.8 ms) -- more CTAs in flight beat the amortised partial fold
-    static const int wpt_env = getenv("QT_QP_WPT") ? atoi(getenv("QT_QP_WPT")) : 1;
-    const int wpt = M >= 256 ? wpt_env : 1;
-#define QT_QP(W)                                                                                                 \
-    return launch_pdl(k_quant_pmax<W>, dim3((words + 256 * W - 1) / (256 * W), M), dim3(256), 0, st, x, ld_x,   \
-                      pmax, n_part, pmax_ld, M, D, d_pad, qmax, mode, static_scale, codes, ld_codes, scales, codes8, \
-                      ld8)
-    if (wpt == 1) QT_QP(1);
-    if (wpt == 2) QT_QP(2);
-    if (wpt == 4) QT_QP(4);
-    if (wpt == 6) QT_QP(6);
-    QT_QP(8);
-#undef QT_QP
+    return launch_pdl(k_quant_pmax<1>, dim3((words + 255) / 256, M), dim3(256), 0, st, x, ld_x, pmax, n_part, pmax_ld,
+                      M, D, d_pad, qmax, mode, static_scale, codes, ld_codes, scales, codes8, ld8);
 }
 
 int qt_launch_rope_kv_append(float* qkv, int ld_qkv, int M, int H, int Hkv, int dh, const int* pos,
@@ -716,8 +580,7 @@ int qt_launch_rope_kv_append(float* qkv, int ld_qkv, int M, int H, int Hkv, int 
     if (M <= 0) return 0;
     if (dh != 64 && dh != 128) return -1;
     const int qmax = (1 << (bits - 1)) - 1;
-    static const bool per_tok = !(getenv("QT_KV_TOK") && atoi(getenv("QT_KV_TOK")) == 0);
-    if (per_tok && dh == 128 && M >= 64 && !k_dbg)
+    if (dh == 128 && M >= 64 && !k_dbg)
         return launch_pdl(k_rope_kv_append_tok, dim3(M), dim3(256), 0, st, qkv, ld_qkv, M, H, Hkv, pos, tok_seq,
                           tok_row, reinterpret_cast<const double2*>(rope), page_table, max_pages, pool, page_bytes,
                           qmax);

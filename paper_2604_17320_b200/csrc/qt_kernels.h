@@ -27,11 +27,6 @@ int qt_launch_token_metrics(const double* x, int D, const int* seq_off, const in
                             int vstride, int res_bits, double* mag, double* res, cudaStream_t st);
 int qt_launch_weight_quant(const float* w, int K, int N, int bits, int row_mul, int row_add, uint8_t* codes,
                            int ldc, double* scales, double* colmax_scratch, cudaStream_t st);
-// decode attention block: RoPE + int4 K/V append + attention + attn_out quantizer (k_attn_dec.cu)
-int qt_launch_attn_dec_fused(float* qkv, int ldq, int H, int Hkv, int dh, const int* pos, const int* kv_len,
-                             const double* rope, const int* pt, int max_pages, uint8_t* pool, long long page_bytes,
-                             float* attn, int d, unsigned* seq_cnt, uint8_t* codes, int ld_codes, double* scales,
-                             int qmode, double static_scale, int d_pad, int bits, int B, cudaStream_t st);
 // full-precision (fp64) calibration forward pieces (k_fp.cu)
 int qt_launch_fp_rmsnorm(const double* x, const float* gain, int M, int D, double* out, unsigned long long* obs,
                          cudaStream_t st);

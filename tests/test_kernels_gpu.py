@@ -251,37 +251,6 @@ def test_w4a4_gemm_int8_operands(torch_cuda, epi, M, N, K):
     np.testing.assert_allclose(out.cpu().numpy(), exp, **tol)
 
 
-def test_w4a4_gemm_int8_cluster_multicast(torch_cuda):
-    """The opt-in cluster-pair variant of the int8-operand GEMM (QT_I8_CL=2, read once per
-    process): weight tile halves TMA-multicast to both CTAs, stages released by both MMA
-    commits.  Odd M-tile count (3) and a ragged N tile; int32 accumulators bit-exact."""
-    import os
-    import subprocess
-    import sys
-    code = """
-import numpy as np, torch, sys
-sys.path.insert(0, %r)
-sys.path.insert(0, %r)
-import paper_2604_17320_b200 as Q
-from test_kernels_gpu import _tiled
-rng = np.random.default_rng(5)
-for M, N, K in [(300, 640, 1024), (1000, 1536, 384)]:
-    a = rng.integers(-7, 8, size=(M, K)); w = rng.integers(-7, 8, size=(N, K))
-    sa = rng.uniform(0.01, 0.5, M); sw = rng.uniform(0.001, 0.01, N)
-    out = torch.zeros((M, N), dtype=torch.float32, device="cuda")
-    acc = torch.zeros((M, N), dtype=torch.int32, device="cuda")
-    Q.w4a4_gemm(Q.EPI_STORE, torch.from_numpy(_tiled(a)).cuda(), torch.from_numpy(sa).cuda(),
-                torch.from_numpy(_tiled(w, 128)).cuda(), torch.from_numpy(sw).cuda(), M, N, K, out, acc, impl=3)
-    torch.cuda.synchronize()
-    exp = a.astype(np.int64) @ w.T.astype(np.int64)
-    assert np.array_equal(acc.cpu().numpy(), exp), (M, N, K)
-print("OK")
-""" % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))), os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, QT_I8_CL="2"), capture_output=True,
-                       text=True, timeout=300)
-    assert r.returncode == 0 and "OK" in r.stdout, r.stdout + r.stderr
-
-
 @pytest.mark.parametrize("M", [17, 24, 32, 40, 64])
 def test_w4a4_gemv_wide_batches_int32_exact(torch_cuda, M):
     """Decode batches of 17..64 tokens: the weight-streaming GEMV with B fragments read from the

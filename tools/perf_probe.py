@@ -1,5 +1,5 @@
 import sys, time, numpy as np, torch
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__))))
 import paper_2604_17320_b200 as Q
 L = int(sys.argv[1]) if len(sys.argv) > 1 else 32
 cfg = Q.Config(n_layers=L, d_model=4096, n_heads=32, n_kv_heads=32, d_head=128, d_ff=11008, mlp=1, act_mode=1)
