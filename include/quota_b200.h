@@ -205,6 +205,19 @@ int qt_engine_profile_read(qt_engine* e, double* out24);
  * (launch overheads and PDL overlap as in the real step).  Cache lengths and
  * positions are restored, so decoding continues unaffected. */
 int qt_engine_profile_chain(qt_engine* e, int skip_mask, int reps, double* ms_per_step);
+/* Decision capture (parity / debugging only; never on the product path): with on != 0
+ * the following prefill / decode calls read back, after every quantizer site, the int4
+ * codes and scales it produced (synchronously; decode steps then run eagerly instead of
+ * from the CUDA graph).  Records: meta = {phase (0 prefill, 1 + t decode step t), layer
+ * (n_layers for head_in), site (0 attn_in, 1 attn_out, 2 mlp_in, 3 mlp_mid, 4 head_in,
+ * 5 K cache rows, 6 V cache rows), rows, cols, groups}; codes int8 [rows x cols] (rows
+ * packed by sequence), scales fp64 [rows x groups] (groups = n_kv_heads for K / V, else 1).
+ * The quantizer sites are model.cpp:349,394,431,435,444 (static) / quant.cpp:108-110
+ * (per token) and the cache rows kv_quantize (quant.cpp:117-119, model.cpp:368-374,499-501).
+ * Calling it clears earlier records. */
+int qt_engine_capture(qt_engine* e, int on);
+int qt_engine_capture_count(qt_engine* e);
+int qt_engine_capture_get(qt_engine* e, int i, int* meta6, int8_t* codes, double* scales);
 
 /* ---- per-kernel ABI (caller-owned device buffers, explicit stream) ----
  * int4 code matrices (weights and activations) use the tiled layout of
@@ -230,6 +243,55 @@ int qt_kv_quant_append_i4(float* qkv, int ld_qkv, int M, int H, int Hkv, int d_h
                           const int* tok_seq, const int* tok_row, const double* rope_table, const int* page_table,
                           int max_pages, uint8_t* pool, int64_t page_bytes, float* k_out, void* stream);
 int qt_rope_table(int max_pos, int d_head, double* host_out);
+/* Tiled int4 code matrix (activations or weights, layout above) -> row-major int8
+ * [rows x K], one code per byte (parity readback of QuantizedTensor::codes,
+ * quant.hpp:32-39). */
+int qt_unpack_codes(const uint8_t* tiled, int rows_pad, int rows, int K, int8_t* out, void* stream);
+/* K7: masked prefill attention over the paged int4 cache -- masked_attention_probs +
+ * matmul(probs, v^) (model.cpp:272-292,366-391) with the reference mask (model.cpp:35-44:
+ * visual queries see visual keys only, text queries see every visual key + causal text),
+ * keys/values dequantised from the int4 rows (model.cpp:371-372).  q: fp32 post-RoPE
+ * queries [sum(S_b) x ldq], head h at column h * d_head; the cache as written by
+ * qt_kv_quant_append_i4; seq_off [B + 1], visual [B], seq_len [B]: device ints; smax =
+ * max S_b.  out: fp32 [sum(S_b) x ldo]; row_stats (nullable): fp32 [sum(S_b) x H x 2]
+ * = (row max, row sum) of the unnormalised softmax (natural-log units), the input of
+ * qt_quota_score. */
+int qt_attn_prefill_i4kv(const float* q, int ldq, int B, int H, int Hkv, int d_head, const int* seq_off,
+                         const int* visual, const int* seq_len, int smax, const uint8_t* pool, int64_t page_bytes,
+                         const int* page_table, int max_pages, float* out, int ldo, float* row_stats, void* stream);
+/* K6: decode attention (model.cpp:515-535): for each of B sequences one query row, an
+ * unmasked softmax over its kv_len[b] (device int) cached rows, int4 K/V dequantised in
+ * registers.  q: fp32 post-RoPE [B x ldq]; max_len >= every kv_len[b]; out fp32 [B x ldo];
+ * workspace: qt_attn_decode_workspace(B, H, d_head, max_len) bytes of device memory. */
+int64_t qt_attn_decode_workspace(int B, int H, int d_head, int max_len);
+int qt_attn_decode_i4kv(const float* q, int ldq, int B, int H, int Hkv, int d_head, const int* kv_len, int max_len,
+                        const uint8_t* pool, int64_t page_bytes, const int* page_table, int max_pages, float* out,
+                        int ldo, void* workspace, void* stream);
+/* K3a + K3b: QUOTA token metrics at a candidate layer -- compute_metrics
+ * (selector.cpp:19-68): mag_i = ||x_i||, inter_i / intra_i = attention received from
+ * text / visual queries summed over heads and divided by H (softmax rebuilt from
+ * qt_attn_prefill_i4kv's row_stats), res_i = ||fake_quant_per_row(x_i, res_bits) - x_i||
+ * (res_bits < 0: nullopt, 0).  x: fp64 residual [sum(S_b) x d_model]; metrics out: fp64
+ * [B][4][vstride] (mag, inter, intra, res), vstride >= vmax = max visual_b; workspace:
+ * qt_quota_score_workspace(B, H, vstride) bytes. */
+int64_t qt_quota_score_workspace(int B, int H, int vstride);
+int qt_quota_score(const double* x, int d_model, const float* q, int ldq, int B, int H, int Hkv, int d_head,
+                   const int* seq_off, const int* visual, const int* seq_len, int vmax, const uint8_t* pool,
+                   int64_t page_bytes, const int* page_table, int max_pages, const float* row_stats, int res_bits,
+                   double* metrics, int vstride, void* workspace, void* stream);
+/* K3c + K4 + compaction: score_tokens / select_top_k / apply_pruning (selector.cpp:70-209,
+ * numeric.cpp:22-31) for B sequences: robust-normalised metrics fused with weights4
+ * (host {mag, inter, intra, quant}), the budget[b] best visual slots (ties to the smaller
+ * index, ascending), then x / positions gathered into the new packed layout (retained
+ * visual rows, then every text row: new_off [B + 1], new_len [B], new_rows = new_off[B],
+ * device) and -- pool != null -- the layer's K/V rows filtered in place.  keep_local
+ * [B x vstride] and keep_src [new_rows]: device int scratch (keep_local holds the kept
+ * slots); kept_pos (nullable) [B x vstride]: the kept visual positions (PruneEvent). */
+int qt_topk_compact(const double* metrics, int B, int vstride, const int* visual, const int* text, const int* budget,
+                    const double* weights4, const int* seq_off, const int* new_off, const int* new_len,
+                    const double* x, int d_model, const int* pos, int new_rows, double* x_out, int* pos_out,
+                    uint8_t* pool, int64_t page_bytes, const int* page_table, int max_pages, int Hkv, int d_head,
+                    int* keep_local, int* keep_src, int* kept_pos, void* stream);
 /* FNV-1a 64 over raw bytes (digest.hpp:12-20; seed 0xcbf29ce484222325 to
  * start): the harness report digests (sample_set_digest, calibrator.cpp:31-40;
  * recipe_digest, recipe.cpp:132-134; sample_logits_digests, harness.cpp:144). */

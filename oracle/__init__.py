@@ -119,6 +119,7 @@ def ref_lib():
                                              C.c_double, C.c_double, _dp, _ip, _dp, _dp, _dp, _dp, _dp]
         lib.qref_profile_sensitivity.argtypes = [C.c_void_p, C.c_int, C.POINTER(_dp), _ip, _ip, C.c_int, _ip,
                                                  C.c_double, _dp, _dp]
+        lib.qref_compute_metrics.argtypes = [_dp, C.c_int, C.c_int, _dp, C.c_int, C.c_int, _dp, _dp, C.c_int, _dp]
         _ref_lib = lib
     return _ref_lib
 
@@ -243,6 +244,66 @@ def ref_kv_quantize(x, bits=4):
     return codes.reshape(a.shape), sc
 
 
+def ref_rope(v, position):
+    """rope_in_place (model.cpp:156-168) of one head vector (fp64), returned as a copy."""
+    lib = ref_lib()
+    a = f64(v).copy()
+    _check(lib.qref_rope(_d(a), a.size, int(position)), lib, "qref")
+    return a
+
+
+def ref_fake_quant_per_row(x, bits=4):
+    lib = ref_lib()
+    a = f64(x)
+    out = np.empty_like(a)
+    _check(lib.qref_fake_quant_per_row(_d(a), a.shape[0], a.shape[1], bits, _d(out)), lib, "qref")
+    return out
+
+
+def ref_compute_metrics(visual_states, text_states, inter_blocks, intra_blocks, res_bits=4):
+    """compute_metrics (selector.cpp:19-68) of the unmodified reference on a
+    LayerActivationRecord: inter_blocks [H x T x N], intra_blocks [H x N x N] post-softmax
+    probabilities.  res_bits None = nullopt.  Returns [4 x N] (mag, inter, intra, res)."""
+    lib = ref_lib()
+    vs, ts = f64(visual_states), f64(text_states)
+    ib, ab = f64(inter_blocks), f64(intra_blocks)
+    n, d = vs.shape
+    out = np.empty((4, n))
+    _check(lib.qref_compute_metrics(_d(vs), n, d, _d(ts), ts.shape[0], ib.shape[0], _d(ib), _d(ab),
+                                    -1 if res_bits is None else int(res_bits), _d(out)), lib, "qref")
+    return out
+
+
+def port_masked_attention(q, k_codes, k_scales, v_codes, v_scales, pos, visual, H, Hkv, dh, want_probs=False):
+    """The restatement's masked prefill attention (model.cpp:272-292,366-391) on given int4
+    K/V rows: q fp64 [S x H*dh] post-RoPE, codes int8 [S x Hkv*dh], scales [S x Hkv].
+    Returns out [S x H*dh] (and probs [H x S x S])."""
+    lib = port_lib()
+    qa = f64(q)
+    S = qa.shape[0]
+    kc, vc = (np.ascontiguousarray(a, dtype=np.int8) for a in (k_codes, v_codes))
+    ks, vs = f64(k_scales), f64(v_scales)
+    p = np.ascontiguousarray(pos, dtype=np.int32)
+    out = np.empty((S, H * dh))
+    probs = np.empty((H, S, S)) if want_probs else None
+    _check(lib.qo_masked_attention(_d(qa), _b(kc), _d(ks), _b(vc), _d(vs), _i(p), S, visual, H, Hkv, dh, _d(out),
+                                   _d(probs) if want_probs else None), lib, "qo")
+    return (out, probs) if want_probs else out
+
+
+def port_decode_attention(q, k_codes, k_scales, v_codes, v_scales, H, Hkv, dh):
+    """The restatement's decode attention (model.cpp:515-535): q fp64 [H*dh]; codes int8
+    [rows x Hkv*dh]; scales [rows x Hkv] -> out [H*dh]."""
+    lib = port_lib()
+    qa = f64(q).ravel()
+    kc, vc = (np.ascontiguousarray(a, dtype=np.int8) for a in (k_codes, v_codes))
+    ks, vs = f64(k_scales), f64(v_scales)
+    out = np.empty(H * dh)
+    _check(lib.qo_decode_attention(_d(qa), _b(kc), _d(ks), _b(vc), _d(vs), kc.shape[0], H, Hkv, dh, _d(out)), lib,
+           "qo")
+    return out
+
+
 def port_lib():
     global _port_lib
     if _port_lib is None:
@@ -272,6 +333,21 @@ def port_lib():
         lib.qo_run_tie_margin.argtypes = [C.c_void_p, C.c_int]
         lib.qo_run_batch.argtypes = [C.c_void_p, C.c_int, C.c_int, C.POINTER(_dp), _ip, _ip, C.c_int, _ip, _dp,
                                      _dp, _ip, C.c_int, C.c_int, C.POINTER(_dp), C.c_int, _dp]
+        lib.qo_masked_attention.argtypes = [_dp, _i8p, _dp, _i8p, _dp, _ip, C.c_int, C.c_int, C.c_int, C.c_int,
+                                            C.c_int, _dp, _dp]
+        lib.qo_decode_attention.argtypes = [_dp, _i8p, _dp, _i8p, _dp, C.c_int, C.c_int, C.c_int, C.c_int, _dp]
+        lib.qo_set_threads.argtypes = [C.c_int]
+        lib.qo_set_threads.restype = None
+        u64p = C.POINTER(C.c_uint64)
+        lib.qo_prefill_ex.restype = C.c_void_p
+        lib.qo_prefill_ex.argtypes = [C.c_void_p, C.c_int, _dp, C.c_int, C.c_int, _ip, C.c_int, _ip, _dp, _dp,
+                                      C.c_int, C.c_int, C.c_int, C.c_int, u64p, _i8p]
+        lib.qo_run_n_recs.argtypes = [C.c_void_p]
+        lib.qo_run_rec.argtypes = [C.c_void_p, C.c_int, _ip, _i8p, _dp]
+        lib.qo_run_clear_recs.argtypes = [C.c_void_p]
+        lib.qo_run_clear_recs.restype = None
+        lib.qo_run_n_ties.argtypes = [C.c_void_p]
+        lib.qo_run_ties.argtypes = [C.c_void_p, u64p, _i8p, _dp]
         _port_lib = lib
     return _port_lib
 
@@ -570,20 +646,33 @@ class Port:
         _check(self.lib.qo_model_weight_codes(self.h, layer, which, _b(codes), _d(scales)), self.lib, "qo")
         return codes.reshape(shape), scales
 
+    @staticmethod
+    def set_threads(n):
+        """Worker threads of the row-parallel matmul / attention loops (results are
+        bit-identical for any count)."""
+        port_lib().qo_set_threads(int(n))
+
     def prefill(self, emb, visual, text, recipe: Recipe | None = None, quantized=True, res_bits=4, pos=None,
-                v0=None):
+                v0=None, record=False, overrides=None):
+        """record: keep every quantizer site's codes (PortRun.records); overrides: {decision
+        key: code} the run follows instead of its own rounding (forced replay, tests/replay.py)."""
         e = f64(emb)
         p = None if pos is None else np.ascontiguousarray(pos, dtype=np.int32)
+        ok = np.zeros(0, dtype=np.uint64) if not overrides else np.fromiter(overrides.keys(), dtype=np.uint64)
+        oc = np.zeros(0, dtype=np.int8) if not overrides else np.fromiter(overrides.values(), dtype=np.int8)
+        okp = ok.ctypes.data_as(C.POINTER(C.c_uint64))
         if recipe is not None:
             lay = np.array(recipe.candidate_layers, dtype=np.int32)
             kp = f64(recipe.keep_ratios)
             wt = f64(recipe.weights)
             n = len(lay)
-            r = self.lib.qo_prefill(self.h, int(quantized), _d(e), visual, text, _i(p) if p is not None else None,
-                                    n, _i(lay), _d(kp), _d(wt), recipe.v0 if v0 is None else v0, res_bits)
+            r = self.lib.qo_prefill_ex(self.h, int(quantized), _d(e), visual, text,
+                                       _i(p) if p is not None else None, n, _i(lay), _d(kp), _d(wt),
+                                       recipe.v0 if v0 is None else v0, res_bits, int(record), ok.size, okp, _b(oc))
         else:
-            r = self.lib.qo_prefill(self.h, int(quantized), _d(e), visual, text, _i(p) if p is not None else None,
-                                    0, None, None, None, 0, res_bits)
+            r = self.lib.qo_prefill_ex(self.h, int(quantized), _d(e), visual, text,
+                                       _i(p) if p is not None else None, 0, None, None, None, 0, res_bits,
+                                       int(record), ok.size, okp, _b(oc))
         if not r:
             raise OracleError(self.lib.qo_last_error().decode())
         return PortRun(self, r)
@@ -666,6 +755,33 @@ class PortRun:
         out = np.empty(self.o.cfg.d_model, dtype=np.float64)
         _check(self.lib.qo_decode(self.h, _d(e), _d(out)), self.lib, "qo")
         return out
+
+    def records(self):
+        """Recorded quantizer sites: list of dicts (phase, layer, site, codes [rows x cols],
+        scales [rows x groups]); see tests/replay.py for the site numbering."""
+        out = []
+        for i in range(self.lib.qo_run_n_recs(self.h)):
+            meta = np.empty(6, dtype=np.int32)
+            _check(self.lib.qo_run_rec(self.h, i, _i(meta), None, None), self.lib, "qo")
+            ph, ly, st, rows, cols, grp = (int(v) for v in meta)
+            codes = np.empty((rows, cols), dtype=np.int8)
+            scales = np.empty((rows, grp), dtype=np.float64)
+            _check(self.lib.qo_run_rec(self.h, i, _i(meta), _b(codes), _d(scales)), self.lib, "qo")
+            out.append(dict(phase=ph, layer=ly, site=st, codes=codes, scales=scales))
+        return out
+
+    def ties(self):
+        """Decisions within the GPU's error budget of a rounding tie: (keys u64, codes, ratios)."""
+        n = self.lib.qo_run_n_ties(self.h)
+        k = np.empty(n, dtype=np.uint64)
+        c = np.empty(n, dtype=np.int8)
+        r = np.empty(n, dtype=np.float64)
+        if n:
+            self.lib.qo_run_ties(self.h, k.ctypes.data_as(C.POINTER(C.c_uint64)), _b(c), _d(r))
+        return k, c, r
+
+    def clear_records(self):
+        self.lib.qo_run_clear_recs(self.h)
 
     def tie_margin(self, which):
         """Smallest |frac(x/s) - 0.5| over activation/KV quantizations of the last

@@ -175,6 +175,25 @@ double qref_silu(double x) { return silu(x); }
 
 // ---- selector (selector.cpp) --------------------------------------------------
 
+// compute_metrics (selector.cpp:19-68) on a LayerActivationRecord built from flat arrays:
+// visual [n x d], text [t x d], inter [heads][t x n], intra [heads][n x n];
+// res_bits < 0 = nullopt.  out: [4][n] = mag, inter, intra, res.
+int qref_compute_metrics(const double* visual, int n, int d, const double* text, int t, int heads,
+                         const double* inter, const double* intra, int res_bits, double* out) {
+    return guard([&] {
+        LayerActivationRecord rec;
+        rec.visual_states = mat(visual, n, d);
+        rec.text_states = mat(text, t, d);
+        for (int h = 0; h < heads; ++h) {
+            rec.attn_inter.push_back(mat(inter + static_cast<size_t>(h) * t * n, t, n));
+            rec.attn_intra.push_back(mat(intra + static_cast<size_t>(h) * n * n, n, n));
+        }
+        TokenMetrics m = compute_metrics(rec, res_bits < 0 ? std::nullopt : std::optional<int>(res_bits));
+        const Vector* v[4] = {&m.mag, &m.inter, &m.intra, &m.res};
+        for (int i = 0; i < 4; ++i) std::copy(v[i]->begin(), v[i]->end(), out + static_cast<size_t>(i) * n);
+    });
+}
+
 int qref_compute_budget(double keep_ratio, int v0, int* out) {
     return guard([&] { *out = compute_budget(keep_ratio, v0); });
 }

@@ -102,6 +102,22 @@ def lib():
         L.qt_engine_load.argtypes = [vp, C.c_char_p]
         L.qt_engine_scores.argtypes = [vp, C.c_int, C.c_int, dp, dp, C.c_int, ip]
         L.qt_quota_topk.argtypes = [vp, C.c_int, C.c_int, vp, vp, dp, vp, vp, vp, vp]
+        L.qt_engine_capture.argtypes = [vp, C.c_int]
+        L.qt_engine_capture_count.argtypes = [vp]
+        L.qt_engine_capture_get.argtypes = [vp, C.c_int, ip, vp, dp]
+        L.qt_unpack_codes.argtypes = [vp, C.c_int, C.c_int, C.c_int, vp, vp]
+        ci = C.c_int
+        L.qt_attn_prefill_i4kv.argtypes = [vp, ci, ci, ci, ci, ci, vp, vp, vp, ci, vp, C.c_int64, vp, ci, vp, ci, vp,
+                                           vp]
+        L.qt_attn_decode_workspace.restype = C.c_int64
+        L.qt_attn_decode_workspace.argtypes = [ci, ci, ci, ci]
+        L.qt_attn_decode_i4kv.argtypes = [vp, ci, ci, ci, ci, ci, vp, ci, vp, C.c_int64, vp, ci, vp, ci, vp, vp]
+        L.qt_quota_score_workspace.restype = C.c_int64
+        L.qt_quota_score_workspace.argtypes = [ci, ci, ci]
+        L.qt_quota_score.argtypes = [vp, ci, vp, ci, ci, ci, ci, ci, vp, vp, vp, ci, vp, C.c_int64, vp, ci, vp, ci,
+                                     vp, ci, vp, vp]
+        L.qt_topk_compact.argtypes = [vp, ci, ci, vp, vp, vp, dp, vp, vp, vp, vp, ci, vp, ci, vp, vp, vp, C.c_int64,
+                                      vp, ci, ci, ci, vp, vp, vp, vp]
         _lib = L
     return _lib
 
@@ -370,6 +386,26 @@ class Engine:
                                      m.ctypes.data_as(C.POINTER(C.c_double)), n.value, C.byref(n)))
         return f, m
 
+    def capture(self, on=True):
+        """Record every quantizer site's codes of the following prefill / decode calls
+        (parity tests; decode steps then run eagerly).  Clears earlier records."""
+        check(lib().qt_engine_capture(self.h, int(on)))
+
+    def captured(self):
+        """The records of capture(): list of dicts (phase, layer, site, codes [rows x cols]
+        int8, scales [rows x groups] fp64), rows packed by sequence."""
+        out = []
+        for i in range(lib().qt_engine_capture_count(self.h)):
+            meta = np.empty(6, dtype=np.int32)
+            check(lib().qt_engine_capture_get(self.h, i, _ip(meta), None, None))
+            ph, ly, st, rows, cols, grp = (int(v) for v in meta)
+            codes = np.empty((rows, cols), dtype=np.int8)
+            scales = np.empty((rows, grp), dtype=np.float64)
+            check(lib().qt_engine_capture_get(self.h, i, _ip(meta), codes.ctypes.data_as(C.c_void_p),
+                                              scales.ctypes.data_as(C.POINTER(C.c_double))))
+            out.append(dict(phase=ph, layer=ly, site=st, codes=codes, scales=scales))
+        return out
+
     PROFILE_CLASSES = ("gemm", "attention", "quant", "kv", "select", "other")
 
     def profile_chain(self, skip_mask, reps=20):
@@ -474,6 +510,93 @@ def quota_topk(metrics, visual, budget, weights=None, stream=0):
     return [s[b, :min(budget[b], visual[b])].copy() for b in range(B)], fused, norm
 
 
+def unpack_codes(tiled, rows, K, stream=0):
+    """qt_unpack_codes: tiled int4 codes (torch uint8 cuda [rows_pad x K/2]) -> int8 [rows x K]."""
+    import torch
+    out = torch.empty((rows, K), dtype=torch.int8, device=tiled.device)
+    check(lib().qt_unpack_codes(_ptr(tiled), tiled.shape[0], rows, K, _ptr(out), C.c_void_p(stream)))
+    return out
+
+
+def _dev_i32(a, device):
+    import torch
+    return torch.tensor(np.asarray(a, dtype=np.int32), dtype=torch.int32, device=device)
+
+
+def attn_prefill(q, ldq, H, Hkv, d_head, seq_off, visual, seq_len, pool, page_bytes, page_table, max_pages, out,
+                 row_stats=None, stream=0):
+    """qt_attn_prefill_i4kv; int arrays given as device int32 tensors (or lists)."""
+    dev = q.device
+    so, vi, sl = (a if not isinstance(a, (list, tuple, np.ndarray)) else _dev_i32(a, dev)
+                  for a in (seq_off, visual, seq_len))
+    B = vi.numel()
+    smax = int(sl.max().item())
+    check(lib().qt_attn_prefill_i4kv(_ptr(q), ldq, B, H, Hkv, d_head, _ptr(so), _ptr(vi), _ptr(sl), smax, _ptr(pool),
+                                     int(page_bytes), _ptr(page_table), max_pages, _ptr(out), out.stride(0),
+                                     _ptr(row_stats), C.c_void_p(stream)))
+    return out
+
+
+def attn_decode(q, ldq, H, Hkv, d_head, kv_len, pool, page_bytes, page_table, max_pages, out, stream=0):
+    """qt_attn_decode_i4kv over kv_len (list / device int32) cached rows per sequence."""
+    import torch
+    dev = q.device
+    kl = kv_len if not isinstance(kv_len, (list, tuple, np.ndarray)) else _dev_i32(kv_len, dev)
+    B = kl.numel()
+    max_len = int(kl.max().item())
+    ws = torch.empty(int(lib().qt_attn_decode_workspace(B, H, d_head, max_len)), dtype=torch.uint8, device=dev)
+    check(lib().qt_attn_decode_i4kv(_ptr(q), ldq, B, H, Hkv, d_head, _ptr(kl), max_len, _ptr(pool), int(page_bytes),
+                                    _ptr(page_table), max_pages, _ptr(out), out.stride(0), _ptr(ws),
+                                    C.c_void_p(stream)))
+    return out
+
+
+def quota_score(x, q, ldq, H, Hkv, d_head, seq_off, visual, seq_len, pool, page_bytes, page_table, max_pages,
+                row_stats, res_bits=4, vstride=None, stream=0):
+    """qt_quota_score -> fp64 metrics [B x 4 x vstride] (mag, inter, intra, res)."""
+    import torch
+    dev = x.device
+    so, vi, sl = (a if not isinstance(a, (list, tuple, np.ndarray)) else _dev_i32(a, dev)
+                  for a in (seq_off, visual, seq_len))
+    B = vi.numel()
+    vmax = int(vi.max().item())
+    vs = vstride or max(64, (vmax + 63) // 64 * 64)
+    met = torch.zeros((B, 4, vs), dtype=torch.float64, device=dev)
+    ws = torch.empty(int(lib().qt_quota_score_workspace(B, H, vs)), dtype=torch.uint8, device=dev)
+    check(lib().qt_quota_score(_ptr(x), x.shape[1], _ptr(q), ldq, B, H, Hkv, d_head, _ptr(so), _ptr(vi), _ptr(sl),
+                               vmax, _ptr(pool), int(page_bytes), _ptr(page_table), max_pages, _ptr(row_stats),
+                               res_bits, _ptr(met), vs, _ptr(ws), C.c_void_p(stream)))
+    return met
+
+
+def topk_compact(metrics, visual, text, budget, weights, seq_off, x, pos, pool=None, page_bytes=0, page_table=None,
+                 max_pages=0, Hkv=1, d_head=64, stream=0):
+    """qt_topk_compact: returns (x_out, pos_out, kept slots per sequence, new_off)."""
+    import torch
+    dev = metrics.device
+    B, _, vs = metrics.shape
+    vis, txt, bud = (np.asarray(a, dtype=np.int32) for a in (visual, text, budget))
+    nv = np.minimum(bud, vis)
+    nlen = nv + txt
+    noff = np.concatenate([[0], np.cumsum(nlen)]).astype(np.int32)
+    rows = int(noff[-1])
+    x_out = torch.zeros((max(rows, 1), x.shape[1]), dtype=torch.float64, device=dev)
+    pos_out = torch.zeros(max(rows, 1), dtype=torch.int32, device=dev)
+    kl = torch.zeros((B, vs), dtype=torch.int32, device=dev)
+    ks = torch.zeros(max(rows, 1), dtype=torch.int32, device=dev)
+    w = np.ascontiguousarray(weights, dtype=np.float64)
+    d = [_dev_i32(a, dev) for a in (vis, txt, bud, noff, nlen)]
+    so = seq_off if not isinstance(seq_off, (list, tuple, np.ndarray)) else _dev_i32(seq_off, dev)
+    check(lib().qt_topk_compact(_ptr(metrics.contiguous()), B, vs, _ptr(d[0]), _ptr(d[1]), _ptr(d[2]),
+                                w.ctypes.data_as(C.POINTER(C.c_double)), _ptr(so), _ptr(d[3]), _ptr(d[4]), _ptr(x),
+                                x.shape[1], _ptr(pos), rows, _ptr(x_out), _ptr(pos_out), _ptr(pool), int(page_bytes),
+                                _ptr(page_table), max_pages, Hkv, d_head, _ptr(kl), _ptr(ks), None,
+                                C.c_void_p(stream)))
+    torch.cuda.synchronize(dev)
+    k = kl.cpu().numpy()
+    return x_out[:rows], pos_out[:rows], [k[b, :nv[b]].copy() for b in range(B)], noff
+
+
 def rope_table(max_pos, d_head):
     out = np.empty((max_pos, d_head // 2, 2), dtype=np.float64)
     lib().qt_rope_table(max_pos, d_head, out.ctypes.data_as(C.POINTER(C.c_double)))
@@ -496,7 +619,8 @@ def exported_symbols():
     """Function names declared in include/quota_b200.h."""
     import re
     txt = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*(?:const\s+char\*|int|void)\s+(qt_\w+)\s*\(", txt, flags=re.M)))
+    return sorted(set(re.findall(r"^\s*(?:const\s+char\*|int|int64_t|uint64_t|void)\s+(qt_\w+)\s*\(", txt,
+                                 flags=re.M)))
 
 
 def tile_w4(rows_u8):

@@ -992,6 +992,78 @@ struct qt_engine {
         ck(cudaStreamSynchronize(st), "gain");
     }
 
+    // ------------------------------------------------------------ decision capture
+    // Debug / parity mode (qt_engine_capture): after every quantizer site of a prefill or
+    // decode step, the int4 codes and scales are read back (synchronously; decode runs
+    // eagerly, not from the graph).  Sites: 0 attn_in, 1 attn_out, 2 mlp_in, 3 mlp_mid,
+    // 4 head_in (layer = n_layers), 5 K and 6 V cache rows (groups = kv heads); phase 0 =
+    // prefill, 1 + t = decode step t.  The parity tests compare them with the restatement's
+    // decisions (oracle/quota_oracle.cpp dec_key) -- the product path never enables it.
+    struct CapRec {
+        int phase, layer, site, rows, cols, groups;
+        std::vector<int8_t> codes;   // rows x cols
+        std::vector<double> scales;  // rows x groups
+    };
+    bool capture = false;
+    std::vector<CapRec> caps;
+    int cap_phase() const { return prefilled ? 1 + decode_steps : 0; }
+    void cap_site(int layer, int site, int M, int D, int dpad) {
+        if (!capture) return;
+        ck(cudaStreamSynchronize(st), "capture");
+        std::vector<uint8_t> t((size_t)codes_rows * dpad / 2);
+        ck(cudaMemcpy(t.data(), codes, t.size(), cudaMemcpyDeviceToHost), "capture codes");
+        CapRec r{cap_phase(), layer, site, M, D, 1, std::vector<int8_t>((size_t)M * D), std::vector<double>(M)};
+        ck(cudaMemcpy(r.scales.data(), ascale, (size_t)M * sizeof(double), cudaMemcpyDeviceToHost), "capture scales");
+        for (int m = 0; m < M; ++m)
+            for (int k = 0; k < D; ++k) {
+                const int nibv = (t[qt::w4t_offset(m, k / 2, codes_rows)] >> (4 * (k & 1))) & 0xF;
+                r.codes[(size_t)m * D + k] = (int8_t)(nibv >= 8 ? nibv - 16 : nibv);
+            }
+        caps.push_back(std::move(r));
+    }
+    // K / V rows [row0[b], row0[b] + n[b]) of every sequence at `layer`, packed by sequence
+    void cap_kv(int layer, const std::vector<int>& row0, const std::vector<int>& n) {
+        if (!capture) return;
+        ck(cudaStreamSynchronize(st), "capture");
+        int M = 0;
+        for (int v : n) M += v;
+        const int cols = Hkv * dh;
+        const size_t cb = (size_t)Hkv * qt::kPage * (dh / 2);
+        std::vector<int> hpt(max_pages);
+        std::vector<uint8_t> page(page_bytes);
+        for (int which = 0; which < 2; ++which) {
+            CapRec r{cap_phase(), layer, 5 + which, M, cols, Hkv, std::vector<int8_t>((size_t)M * cols),
+                     std::vector<double>((size_t)M * Hkv)};
+            int o = 0;
+            for (int b = 0; b < B; ++b) {
+                ck(cudaMemcpy(hpt.data(), pt + ((size_t)layer * max_batch + b) * max_pages, max_pages * sizeof(int),
+                              cudaMemcpyDeviceToHost),
+                   "capture page table");
+                int cur = -1;
+                for (int i = 0; i < n[b]; ++i, ++o) {
+                    const int row = row0[b] + i;
+                    if (row / qt::kPage != cur) {
+                        cur = row / qt::kPage;
+                        ck(cudaMemcpy(page.data(), pool + (long long)hpt[cur] * page_bytes, page_bytes,
+                                      cudaMemcpyDeviceToHost),
+                           "capture page");
+                    }
+                    const int slot = row % qt::kPage;
+                    const float* sc = reinterpret_cast<const float*>(page.data() + 2 * cb);
+                    for (int h = 0; h < Hkv; ++h) {
+                        const uint8_t* src = page.data() + (which ? cb : 0) + ((size_t)h * qt::kPage + slot) * (dh / 2);
+                        for (int c = 0; c < dh; ++c) {
+                            const int nibv = (src[c / 2] >> (4 * (c & 1))) & 0xF;
+                            r.codes[(size_t)o * cols + h * dh + c] = (int8_t)(nibv >= 8 ? nibv - 16 : nibv);
+                        }
+                        r.scales[(size_t)o * Hkv + h] = sc[(which ? Hkv * qt::kPage : 0) + h * qt::kPage + slot];
+                    }
+                }
+            }
+            caps.push_back(std::move(r));
+        }
+    }
+
     // ------------------------------------------------------------ kernels
     // from_pmax: the site input is the fp32 output of the last gemm(), whose epilogue left the
     // per-row partial maxima in pmax (pm_parts > 0): quantize without a row reduction
@@ -1184,12 +1256,18 @@ struct qt_engine {
             int* ptl = pt + (size_t)l * max_batch * max_pages;
             // attention block (model.cpp:347-396)
             norm_quant(xc, 1, d, w.g1, M, d, kd_pad, 4 * l + 0);
+            cap_site(l, 0, M, d, kd_pad);
             gemm(QT_EPI_STORE, w.qkv, n_qkv_pad, w.s_qkv, M, n_qkv, kd_pad, qkv, n_qkv, false, w.qkv8);
             pb(P_KV);
             ckl(qt_launch_rope_kv_append(qkv, n_qkv, M, H, Hkv, dh, pc, tok_seq, tok_row, rope, ptl, max_pages, pool,
                                          page_bytes, 4, nullptr, st),
                 "rope+kv append");
             pe((double)M * n_qkv * 8 + (double)M * Hkv * 2 * (dh / 2 + 4));
+            if (capture) {
+                std::vector<int> r0(B, 0), nr(B);
+                for (int b = 0; b < B; ++b) nr[b] = cur_v[b] + h_txt[b];
+                cap_kv(l, r0, nr);
+            }
             int smax = 0, vmax = 0;
             bool prune_any = false;
             for (int b = 0; b < B; ++b) {
@@ -1215,6 +1293,7 @@ struct qt_engine {
             pm_ptr = pmax;
             pm_ld = kPmaxLd;
             norm_quant(attn, 0, d, nullptr, M, d, kd_pad, 4 * l + 1, true);
+            cap_site(l, 1, M, d, kd_pad);
             gemm(QT_EPI_RESADD, w.o, nd_pad, w.s_o, M, d, kd_pad, xc, d, false, w.o8);
             if (rec_diag) diag_layer(l, ptl, cur_v[0], h_txt[0], xc);
             for (int b = 0; b < B; ++b) h_kvlen[(size_t)l * B + b] = cur_v[b] + h_txt[b];
@@ -1268,9 +1347,11 @@ struct qt_engine {
             }
             // MLP block (model.cpp:429-437)
             norm_quant(xc, 1, d, w.g2, M, d, kd_pad, 4 * l + 2);
+            cap_site(l, 2, M, d, kd_pad);
             if (cfg.mlp == 1) gemm(QT_EPI_SWIGLU, w.gu, n_gu_pad, w.s_gu, M, n_gu, kd_pad, mid, dff, true, w.gu8);
             else gemm(QT_EPI_SILU, w.gu, n_gu_pad, w.s_gu, M, n_gu, kd_pad, mid, dff, true, w.gu8);
             norm_quant(mid, 0, dff, nullptr, M, dff, kff_pad, 4 * l + 3, true);
+            cap_site(l, 3, M, dff, kff_pad);
             gemm(QT_EPI_RESADD, w.down, nd_pad, w.s_down, M, d, kff_pad, xc, d, false, w.down8);
             if (rec_blocks) {  // ForwardResult::block_outputs (model.cpp:439), calibration only
                 if (l == 0) rec_blocks->assign(L, {});
@@ -1282,6 +1363,7 @@ struct qt_engine {
         }
         // final norm + head (model.cpp:442-445)
         norm_quant(xc, 1, d, gf, M, d, kd_pad, 4 * L);
+        cap_site(L, 4, M, d, kd_pad);
         gemm(QT_EPI_STORE, head, nd_pad, s_head, M, d, kd_pad, logits, d, false, head8);
         final_rows = M;
         ev_layers = trace_layers;
@@ -1380,6 +1462,7 @@ struct qt_engine {
             int* ptl = pt + (size_t)l * max_batch * max_pages;
             int* lenl = kv_len + (size_t)l * max_batch;
             if (!(skip_mask & 4)) norm_quant(xcur, 1, d, w.g1, B, d, kd_pad, 4 * l + 0);
+            cap_site(l, 0, B, d, kd_pad);
             if (!(skip_mask & 1)) gemm(QT_EPI_STORE, w.qkv, n_qkv_pad, w.s_qkv, B, n_qkv, kd_pad, qkv, n_qkv);
             pb(P_KV);
             if (!(skip_mask & 8))
@@ -1387,6 +1470,11 @@ struct qt_engine {
                                              pool, page_bytes, 4, nullptr, st),
                     "decode kv append");
             pe((double)B * n_qkv * 8 + (double)B * Hkv * 2 * (dh / 2 + 4));
+            if (capture) {
+                std::vector<int> r0(B), nr(B, 1);
+                for (int b = 0; b < B; ++b) r0[b] = h_kvlen[(size_t)l * B + b];
+                cap_kv(l, r0, nr);
+            }
             pb(P_ATTN);
             // decode attention over the int4 pages + split merge fused with the attn_out quantizer
             if (!(skip_mask & 2))
@@ -1400,16 +1488,20 @@ struct qt_engine {
                 for (int b = 0; b < B; ++b) rows += h_kvlen[(size_t)l * B + b] + 1;
                 pe(rows * Hkv * 2 * (dh / 2 + 4) + (double)B * H * dh * 8);
             }
+            cap_site(l, 1, B, d, kd_pad);
             if (!(skip_mask & 1)) gemm(QT_EPI_RESADD, w.o, nd_pad, w.s_o, B, d, kd_pad, xcur, d);
             if (!(skip_mask & 4)) norm_quant(xcur, 1, d, w.g2, B, d, kd_pad, 4 * l + 2);
+            cap_site(l, 2, B, d, kd_pad);
             float* gml = gmax ? gmax + (size_t)l * max_batch : nullptr;
             if (!(skip_mask & 1))
                 gemm(cfg.mlp == 1 ? QT_EPI_SWIGLU : QT_EPI_SILU, w.gu, n_gu_pad, w.s_gu, B, n_gu, kd_pad, mid, dff, true,
                      nullptr, gml);
             if (!(skip_mask & 4)) norm_quant(mid, 0, dff, nullptr, B, dff, kff_pad, 4 * l + 3, true);
+            cap_site(l, 3, B, dff, kff_pad);
             if (!(skip_mask & 1)) gemm(QT_EPI_RESADD, w.down, nd_pad, w.s_down, B, d, kff_pad, xcur, d);
         }
         norm_quant(xcur, 1, d, gf, B, d, kd_pad, 4 * L);
+        cap_site(L, 4, B, d, kd_pad);
         gemm(QT_EPI_STORE, head, nd_pad, s_head, B, d, kd_pad, dlogits, d);
         ckl(qt_launch_kv_len_bump(kv_len, L * max_batch, next_pos, B, st), "kv length / position bump");
         if (gmax) ck(cudaMemsetAsync(gmax, 0, (size_t)L * max_batch * sizeof(float), st), "row-max reset");
@@ -1505,8 +1597,8 @@ struct qt_engine {
             ckl(qt_launch_f32_to_f64(xd_in, xd, (long long)B * d, st), "embedding widen");
             pe((double)B * d * 12);
         }
-        if (profiling) {
-            decode_body();  // eager launches so every kernel gets its own events
+        if (profiling || capture) {
+            decode_body();  // eager launches so every kernel gets its own events / capture reads
         } else if (!graph_ok) {
             if (graph) cudaGraphExecDestroy(graph);
             graph = nullptr;
@@ -1527,7 +1619,7 @@ struct qt_engine {
             cudaGraphDestroy(g);
             graph_ok = true;
         }
-        if (!profiling) ck(cudaGraphLaunch(graph, st), "graph launch");
+        if (!profiling && !capture) ck(cudaGraphLaunch(graph, st), "graph launch");
         if (out)
             ck(cudaMemcpyAsync(out, dlogits, (size_t)B * d * sizeof(float),
                                out_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st),
@@ -2110,6 +2202,27 @@ int qt_engine_profile_chain(qt_engine* e, int skip_mask, int reps, double* ms_pe
     });
 }
 
+int qt_engine_capture(qt_engine* e, int on) {
+    return guard([&] {
+        e->capture = on != 0;
+        e->caps.clear();
+        e->caps.shrink_to_fit();
+    });
+}
+
+int qt_engine_capture_count(qt_engine* e) { return (int)e->caps.size(); }
+
+int qt_engine_capture_get(qt_engine* e, int i, int* meta, int8_t* codes, double* scales) {
+    return guard([&] {
+        if (i < 0 || i >= (int)e->caps.size()) fail(QT_ERANGE, "capture record out of range");
+        const auto& r = e->caps[i];
+        const int m[6] = {r.phase, r.layer, r.site, r.rows, r.cols, r.groups};
+        std::copy(m, m + 6, meta);
+        if (codes) std::memcpy(codes, r.codes.data(), r.codes.size());
+        if (scales) std::copy(r.scales.begin(), r.scales.end(), scales);
+    });
+}
+
 int qt_engine_profile_next(qt_engine* e) {
     e->prof_next = true;
     return 0;
@@ -2209,6 +2322,97 @@ int qt_kv_quant_append_i4(float* qkv, int ld_qkv, int M, int H, int Hkv, int d_h
         ckl(qt_launch_rope_kv_append(qkv, ld_qkv, M, H, Hkv, d_head, positions, tok_seq, tok_row, rope_table,
                                      page_table, max_pages, pool, page_bytes, 4, k_out, (cudaStream_t)stream),
             "kv quant append");
+    });
+}
+
+int qt_unpack_codes(const uint8_t* tiled, int rows_pad, int rows, int K, int8_t* out, void* stream) {
+    return guard([&] {
+        if (rows < 0 || rows > rows_pad || rows_pad % 16 || K % 2) fail(QT_EINVAL, "invalid code matrix shape");
+        ckl(qt_launch_unpack_codes(tiled, rows_pad, rows, K, out, (cudaStream_t)stream), "unpack codes");
+    });
+}
+
+int qt_attn_prefill_i4kv(const float* q, int ldq, int B, int H, int Hkv, int d_head, const int* seq_off,
+                         const int* visual, const int* seq_len, int smax, const uint8_t* pool, int64_t page_bytes,
+                         const int* page_table, int max_pages, float* out, int ldo, float* row_stats, void* stream) {
+    return guard([&] {
+        if (B < 0 || H < 1 || Hkv < 1 || H % Hkv) fail(QT_EINVAL, "invalid attention heads");
+        if (d_head != 64 && d_head != 128) fail(QT_EINVAL, "d_head must be 64 or 128 on the B200 path");
+        ckl(qt_launch_attn_prefill(q, ldq, H, Hkv, d_head, seq_off, visual, seq_len, B, smax, pool, page_bytes,
+                                   page_table, max_pages, out, ldo, row_stats, nullptr, 0, (cudaStream_t)stream),
+            "prefill attention");
+    });
+}
+
+int64_t qt_attn_decode_workspace(int B, int H, int d_head, int max_len) {
+    const int pages = (max_len + qt::kPage - 1) / qt::kPage;
+    return (int64_t)B * H * pages * (d_head + 2) * (int64_t)sizeof(float);
+}
+
+int qt_attn_decode_i4kv(const float* q, int ldq, int B, int H, int Hkv, int d_head, const int* kv_len, int max_len,
+                        const uint8_t* pool, int64_t page_bytes, const int* page_table, int max_pages, float* out,
+                        int ldo, void* workspace, void* stream) {
+    return guard([&] {
+        if (B < 0 || H < 1 || Hkv < 1 || H % Hkv) fail(QT_EINVAL, "invalid attention heads");
+        if (d_head != 64 && d_head != 128) fail(QT_EINVAL, "d_head must be 64 or 128 on the B200 path");
+        if (max_len < 1 || (max_len + qt::kPage - 1) / qt::kPage > max_pages) fail(QT_EINVAL, "max_len exceeds the page table");
+        if (!workspace) fail(QT_EINVAL, "null workspace");
+        const int pages = (max_len + qt::kPage - 1) / qt::kPage;
+        float* part_ml = static_cast<float*>(workspace);
+        float* part_o = part_ml + (size_t)B * H * pages * 2;
+        ckl(qt_launch_attn_decode(q, ldq, H, Hkv, d_head, kv_len, 0, B, const_cast<uint8_t*>(pool), page_bytes,
+                                  page_table, max_pages, pages, part_ml, part_o, out, ldo, nullptr, 0, nullptr, 1,
+                                  0.0, 0, 4, nullptr, nullptr, nullptr, nullptr, nullptr, (cudaStream_t)stream),
+            "decode attention");
+    });
+}
+
+int qt_quota_score(const double* x, int d_model, const float* q, int ldq, int B, int H, int Hkv, int d_head,
+                   const int* seq_off, const int* visual, const int* seq_len, int vmax, const uint8_t* pool,
+                   int64_t page_bytes, const int* page_table, int max_pages, const float* row_stats, int res_bits,
+                   double* metrics, int vstride, void* workspace, void* stream) {
+    return guard([&] {
+        if (B < 0 || H < 1 || Hkv < 1 || H % Hkv) fail(QT_EINVAL, "invalid attention heads");
+        if (vmax > vstride) fail(QT_EINVAL, "visual prefix exceeds vstride");
+        if (res_bits == 0 || res_bits == 1 || res_bits > 8) fail(QT_EINVAL, "bits out of range [2,8]");
+        if (!workspace || !row_stats) fail(QT_EINVAL, "null workspace / row statistics");
+        const cudaStream_t cs = (cudaStream_t)stream;
+        float* inter = static_cast<float*>(workspace);
+        float* intra = inter + (size_t)B * H * vstride;
+        double* mag = reinterpret_cast<double*>(intra + (size_t)B * H * vstride);
+        double* res = mag + (size_t)B * vstride;
+        ckl(qt_launch_attn_colsum(q, ldq, H, Hkv, d_head, seq_off, visual, seq_len, B, vmax, pool, page_bytes,
+                                  page_table, max_pages, row_stats, vstride, inter, intra, cs),
+            "quota attention metrics");
+        ckl(qt_launch_token_metrics(x, d_model, seq_off, visual, vmax, B, vstride, res_bits < 0 ? 0 : res_bits, mag,
+                                    res, cs),
+            "quota token metrics");
+        ckl(qt_launch_metrics_pack(mag, res, inter, intra, H, vstride, visual, B, metrics, cs), "metrics pack");
+    });
+}
+
+int64_t qt_quota_score_workspace(int B, int H, int vstride) {
+    return (int64_t)2 * B * H * vstride * (int64_t)sizeof(float) + (int64_t)2 * B * vstride * (int64_t)sizeof(double);
+}
+
+int qt_topk_compact(const double* metrics, int B, int vstride, const int* visual, const int* text, const int* budget,
+                    const double* weights4, const int* seq_off, const int* new_off, const int* new_len,
+                    const double* x, int d_model, const int* pos, int new_rows, double* x_out, int* pos_out,
+                    uint8_t* pool, int64_t page_bytes, const int* page_table, int max_pages, int Hkv, int d_head,
+                    int* keep_local, int* keep_src, int* kept_pos, void* stream) {
+    return guard([&] {
+        if (B < 0 || vstride < 1) fail(QT_EINVAL, "invalid top-k shape");
+        if (!weights4) fail(QT_EINVAL, "null metric weights");
+        const cudaStream_t cs = (cudaStream_t)stream;
+        ckl(qt_launch_select_topk(nullptr, nullptr, nullptr, nullptr, 1, vstride, visual, text, budget, seq_off,
+                                  new_off, B, vstride, weights4, keep_src, keep_local, vstride, pos, kept_pos,
+                                  nullptr, nullptr, metrics, 0, cs),
+            "quota top-k");
+        ckl(qt_launch_gather_rows(x, x_out, d_model, pos, pos_out, keep_src, new_rows, cs), "compaction gather");
+        if (pool)
+            ckl(qt_launch_kv_compact(pool, page_bytes, page_table, max_pages, Hkv, d_head, keep_local, vstride,
+                                     new_len, B, cs),
+                "kv compaction");
     });
 }
 

@@ -503,6 +503,19 @@ __global__ void k_codes_pack(const int8_t* __restrict__ src, int K, int N, const
     if (wd == 0) scales[dst] = s_in[n];
 }
 
+// tiled int4 codes (w4t layout) -> row-major int8 [rows x K] (parity readback, qt_unpack_codes)
+__global__ void k_unpack_codes(const uint8_t* __restrict__ tiled, int rows_pad, int rows, int K,
+                               int8_t* __restrict__ out) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // one packed byte
+    if (i >= (long long)rows * (K / 2)) return;
+    const int row = (int)(i / (K / 2)), kb = (int)(i % (K / 2));
+    const uint8_t b = tiled[w4t_offset(row, kb, rows_pad)];
+    char2 v;
+    v.x = (char)(((int)(b << 28)) >> 28);
+    v.y = (char)(((int)(b << 24)) >> 28);
+    reinterpret_cast<char2*>(out)[i] = v;
+}
+
 __global__ void k_f32_to_f64(const float* __restrict__ a, double* __restrict__ b, long long n) {
     pdl_launch_dependents();
     pdl_wait();
@@ -587,6 +600,13 @@ int qt_launch_rope_kv_append(float* qkv, int ld_qkv, int M, int H, int Hkv, int 
     return launch_pdl(k_rope_kv_append, dim3(M, (H + 2 * Hkv + 7) / 8), dim3(256), 0, st, qkv, ld_qkv, M, H, Hkv,
                       dh, pos, tok_seq, tok_row, reinterpret_cast<const double2*>(rope), page_table, max_pages, pool,
                       page_bytes, qmax, k_dbg);
+}
+
+int qt_launch_unpack_codes(const uint8_t* tiled, int rows_pad, int rows, int K, int8_t* out, cudaStream_t st) {
+    const long long n = (long long)rows * (K / 2);
+    if (n <= 0) return 0;
+    k_unpack_codes<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(tiled, rows_pad, rows, K, out);
+    return (int)cudaGetLastError();
 }
 
 int qt_launch_token_metrics(const double* x, int D, const int* seq_off, const int* vis, int vmax, int B,

@@ -218,6 +218,27 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select_topk(
     }
 }
 
+// compute_metrics output (selector.cpp:19-68) as [B][4][vstride] fp64: the per-head fp32
+// column sums averaged over heads with the arithmetic of k_select_topk (the kernel-level
+// qt_quota_score ABI).  grid B.
+__global__ void k_metrics_pack(const double* __restrict__ mag, const double* __restrict__ res,
+                               const float* __restrict__ inter_p, const float* __restrict__ intra_p, int H,
+                               int vstride, const int* __restrict__ vis, double* __restrict__ met) {
+    const int b = blockIdx.x, V = vis[b];
+    const double invH = 1.0 / (double)H;
+    for (int i = threadIdx.x; i < V; i += blockDim.x) {
+        double si = 0.0, sa = 0.0;
+        for (int h = 0; h < H; ++h) {
+            si += (double)inter_p[((size_t)b * H + h) * vstride + i];
+            sa += (double)intra_p[((size_t)b * H + h) * vstride + i];
+        }
+        met[((size_t)b * 4 + 0) * vstride + i] = mag[(size_t)b * vstride + i];
+        met[((size_t)b * 4 + 1) * vstride + i] = __dmul_rn(si, invH);
+        met[((size_t)b * 4 + 2) * vstride + i] = __dmul_rn(sa, invH);
+        met[((size_t)b * 4 + 3) * vstride + i] = res[(size_t)b * vstride + i];
+    }
+}
+
 // x_new[j] = x_old[src[j]], pos_new[j] = pos_old[src[j]]
 __global__ void k_gather_rows(const double* __restrict__ x, double* __restrict__ xn, int D,
                               const int* __restrict__ pos, int* __restrict__ posn, const int* __restrict__ src, int M) {
@@ -286,6 +307,13 @@ int qt_launch_select_topk(const double* mag, const double* res, const float* int
     k_select_topk<<<B, SEL_THREADS, smem, st>>>(mag, res, inter, intra, H, vstride, vis, txt, budget, old_off,
                                                 new_off, w0, w1, w2, w3, keep_src, keep_local,
                                                 kl_stride, pos, kept_pos, fused_out, norm_out, met_in, raw);
+    return (int)cudaGetLastError();
+}
+
+int qt_launch_metrics_pack(const double* mag, const double* res, const float* inter, const float* intra, int H,
+                           int vstride, const int* vis, int B, double* metrics, cudaStream_t st) {
+    if (B <= 0) return 0;
+    k_metrics_pack<<<B, 256, 0, st>>>(mag, res, inter, intra, H, vstride, vis, metrics);
     return (int)cudaGetLastError();
 }
 

@@ -1,0 +1,150 @@
+"""Forced-replay parity harness (test infrastructure).
+
+The GPU path and the restatement (oracle/quota_oracle.cpp, pinned bit-for-bit to the
+unmodified reference) make the same quantization decisions except where a value sits within
+the GPU's arithmetic error of a rounding tie: attention outputs and MLP hidden states are
+fp32 on the device (relative error ~1e-7 .. 1e-6) while the reference is fp64 throughout.
+Instead of loosening the logit tolerance for such events, the harness makes every decision
+comparable:
+
+1. the engine records every quantizer site's int4 codes (qt_engine_capture: attn_in,
+   attn_out, mlp_in, mlp_mid, head_in, and the K / V cache rows) for a prefill and some
+   decode steps;
+2. the restatement runs the same sequences, recording its codes and listing each decision
+   within the GPU error budget of a tie (`ties`, keyed by (phase, layer, site, row, col));
+3. every GPU code must equal the restatement's, except at listed ties -- a difference
+   anywhere else is a genuine mismatch and fails;
+4. at the listed ties where the GPU rounded the other way, the restatement is re-run told
+   to take the GPU's code (`overrides`), and 2-4 repeat until no differences remain.
+
+After convergence every int4 decision (including all KV-cache codes) is identical, the
+retained token sets must match exactly, and logits are compared at north_star's 1e-2
+max-abs with no escape hatch.
+"""
+import threading
+
+import numpy as np
+
+SITES = {0: "attn_in", 1: "attn_out", 2: "mlp_in", 3: "mlp_mid", 4: "head_in", 5: "K", 6: "V"}
+# scale agreement after convergence: residual-derived sites are fp64 end to end, the
+# fp32-buffered sites (attention output, MLP hidden, K/V) carry fp32 rounding
+SCALE_RTOL = {0: 1e-12, 2: 1e-12, 4: 1e-12, 1: 1e-5, 3: 1e-5, 5: 1e-6, 6: 1e-6}
+
+
+def dec_key(phase, layer, site, row, col):
+    """oracle/quota_oracle.cpp dec_key."""
+    return ((np.uint64(phase) << np.uint64(47)) | (np.uint64(layer) << np.uint64(39)) |
+            (np.uint64(site) << np.uint64(36)) | (np.asarray(row, dtype=np.uint64) << np.uint64(20)) |
+            np.asarray(col, dtype=np.uint64))
+
+
+class Mismatch(AssertionError):
+    pass
+
+
+def _split_gpu(gpu_recs, port_recs_per_seq):
+    """GPU records (rows packed by sequence) -> {seq: {(phase, layer, site): rec}} using the
+    per-sequence row counts of the restatement's records."""
+    out = [dict() for _ in port_recs_per_seq]
+    g = {(r["phase"], r["layer"], r["site"]): r for r in gpu_recs}
+    for (ph, ly, st), r in g.items():
+        o = 0
+        for b, pr in enumerate(port_recs_per_seq):
+            pk = pr.get((ph, ly, st))
+            if pk is None:
+                raise Mismatch(f"GPU site {SITES[st]} phase {ph} layer {ly} has no restatement counterpart")
+            n = pk["codes"].shape[0]
+            out[b][(ph, ly, st)] = dict(codes=r["codes"][o:o + n], scales=r["scales"][o:o + n])
+            o += n
+        if o != r["codes"].shape[0]:
+            raise Mismatch(f"row count mismatch at {SITES[st]} phase {ph} layer {ly}: GPU {r['codes'].shape[0]}, "
+                           f"restatement {o}")
+    return out
+
+
+def compare_decisions(gpu_by_key, port_by_key, tie_keys):
+    """Codes equal except at listed ties.  Returns {key: gpu code} to force, and a summary."""
+    force, summary = {}, []
+    if set(gpu_by_key) != set(port_by_key):
+        raise Mismatch(f"site sets differ: {sorted(set(gpu_by_key) ^ set(port_by_key))[:5]}")
+    for k, g in gpu_by_key.items():
+        p = port_by_key[k]
+        if g["codes"].shape != p["codes"].shape:
+            raise Mismatch(f"shape mismatch at {k}: {g['codes'].shape} vs {p['codes'].shape}")
+        rr, cc = np.nonzero(g["codes"] != p["codes"])
+        if rr.size == 0:
+            continue
+        keys = dec_key(k[0], k[1], k[2], rr, cc)
+        listed = np.isin(keys, tie_keys)
+        if not listed.all():
+            bad = np.nonzero(~listed)[0][:5]
+            raise Mismatch(f"{(~listed).sum()} code(s) differ outside the tie list at {SITES[k[2]]} phase {k[0]} "
+                           f"layer {k[1]}: (row, col, gpu, ref) = "
+                           f"{[(int(rr[i]), int(cc[i]), int(g['codes'][rr[i], cc[i]]), int(p['codes'][rr[i], cc[i]])) for i in bad]}")
+        for kk, r, c in zip(keys, rr, cc):
+            force[int(kk)] = int(g["codes"][r, c])
+        summary.append((SITES[k[2]], k[0], k[1], int(rr.size)))
+    return force, summary
+
+
+def check_scales(gpu_by_key, port_by_key):
+    for k, g in gpu_by_key.items():
+        p = port_by_key[k]
+        np.testing.assert_allclose(g["scales"], p["scales"], rtol=SCALE_RTOL[k[2]], atol=0,
+                                   err_msg=f"scales at {SITES[k[2]]} phase {k[0]} layer {k[1]}")
+
+
+def run_port_seqs(port, seqs, recipe_for, dec_embs, overrides, threads=True):
+    """Restatement runs of each sequence (prefill + teacher-forced decode steps) with
+    recording and the given overrides; seqs = [(emb fp64, visual, text, v0)].  Runs the
+    sequences on parallel Python threads (ctypes releases the GIL)."""
+    res = [None] * len(seqs)
+    errs = []
+
+    def one(b):
+        try:
+            emb, vis, txt, v0 = seqs[b]
+            r = port.prefill(emb, vis, txt, recipe_for(b), v0=v0, record=True, overrides=overrides[b])
+            lg = [r.result()]
+            for de in dec_embs[b]:
+                lg.append(r.decode(de))
+            recs = {(x["phase"], x["layer"], x["site"]): x for x in r.records()}
+            tk, _, _ = r.ties()
+            res[b] = dict(run=r, logits=lg, recs=recs, ties=np.unique(tk))
+            r.clear_records()
+        except Exception as e:  # noqa: BLE001 - re-raised below
+            errs.append(e)
+
+    if threads and len(seqs) > 1:
+        ts = [threading.Thread(target=one, args=(b,)) for b in range(len(seqs))]
+        [t.start() for t in ts]
+        [t.join() for t in ts]
+    else:
+        for b in range(len(seqs)):
+            one(b)
+    if errs:
+        raise errs[0]
+    return res
+
+
+def forced_replay(port, gpu_recs, seqs, recipe_for, dec_embs, max_iter=6, log=print):
+    """Iterate restatement runs until every GPU decision is reproduced.  Returns the final
+    restatement results and the overrides per sequence."""
+    overrides = [dict() for _ in seqs]
+    for it in range(max_iter):
+        res = run_port_seqs(port, seqs, recipe_for, dec_embs, overrides)
+        split = _split_gpu(gpu_recs, [r["recs"] for r in res])
+        changed = False
+        for b, r in enumerate(res):
+            force, summary = compare_decisions(split[b], r["recs"], r["ties"])
+            if force:
+                changed = True
+                overrides[b].update(force)
+                log(f"replay iter {it} seq {b}: forced {len(force)} tie decision(s) {summary}")
+        if not changed:
+            for b, r in enumerate(res):
+                check_scales(split[b], r["recs"])
+            log(f"replay converged after {it} iteration(s); forced per seq: {[len(o) for o in overrides]}; "
+                f"tie candidates per seq: {[int(r['ties'].size) for r in res]}")
+            return res, overrides
+    raise Mismatch(f"forced replay did not converge in {max_iter} iterations")
