@@ -281,7 +281,7 @@ def test_decode_gemv_7b_shapes_int32_exact(torch_cuda, M, K, N, epi):
     K = 4096, smem-staged for the K = 11008 down projection; int32 accumulators exact,
     epilogue within fp64 rounding."""
     torch = torch_cuda
-    from test_kernels_gpu import _tiled
+    from tests.test_kernels_gpu import _tiled
     rng = np.random.default_rng(M * 7 + K + N)
     a = rng.integers(-7, 8, size=(M, K))
     w = rng.integers(-7, 8, size=(N, K))
@@ -310,7 +310,7 @@ def test_decode_gemv_7b_shapes_int32_exact(torch_cuda, M, K, N, epi):
 
 def test_unpack_codes_roundtrip(torch_cuda):
     torch = torch_cuda
-    from test_kernels_gpu import _tiled
+    from tests.test_kernels_gpu import _tiled
     rng = np.random.default_rng(13)
     c = rng.integers(-7, 8, size=(37, 640))
     t = torch.from_numpy(_tiled(c)).cuda()

@@ -21,7 +21,7 @@ import pytest
 
 import oracle as O
 import paper_2604_17320_b200 as Q
-from replay import forced_replay
+from tests.replay import forced_replay
 
 pytestmark = pytest.mark.gpu
 
