@@ -17,8 +17,13 @@ hidden states with 1 % of the channels x20 (the configs' outlier model).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N > 1 is launched by torchrun (one rank per GPU, NCCL); each rank runs its own
-batch (weak scaling), NCCL only gathers outputs and timings.
+N > 1: one rank per GPU (NCCL).  Under torchrun WORLD_SIZE must equal --gpus; without
+it bench.py starts the N ranks itself through torch.distributed.run.  The global
+request batch is N x the per-GPU batch, sharded with shard.shard_range (sequences are
+independent): each rank runs its own sequences (weak scaling) and NCCL only
+gathers the final logits (inside the timed region, both legs) and the max-over-ranks
+step time.  `--impl stub` runs the same rank plumbing on CPU (gloo) with a stand-in
+engine, for the multi-process test (tests/test_bench_cpu.py).
 """
 from __future__ import annotations
 
@@ -168,6 +173,27 @@ def dist_env():
     return ws, rank, local
 
 
+def spawn_ranks(argv, n):
+    """--gpus N > 1 without a torchrun environment: start N ranks of this script (one per
+    GPU) through torch.distributed.run on 127.0.0.1; their rank 0 prints the line."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + list(argv)
+    return subprocess.call(cmd)
+
+
+def local_sequences(cfg, ws, rank):
+    """This rank's share of the global request batch (ws x batch_per_gpu sequences):
+    global sequence indices [first, first + count) (shard.shard_range)."""
+    from paper_2604_17320_b200.shard import shard_range
+    first, count = shard_range(ws * cfg["batch"], ws, rank)
+    return list(range(first, first + count))
+
+
 # --------------------------------------------------------------------------- reference arm
 
 
@@ -223,12 +249,11 @@ def run_reference(args, cfg):
 # --------------------------------------------------------------------------- our arm
 
 
-def build_engine(cfg, torch, Q, seed=1234):
+def build_engine(cfg, torch, Q, vis, seed=1234):
     c = Q.Config(n_layers=cfg["n_layers"], d_model=cfg["d_model"], n_heads=cfg["n_heads"],
                  n_kv_heads=cfg["n_kv_heads"], d_head=cfg["d_head"], d_ff=cfg["d_ff"], mlp=cfg["mlp"],
                  act_mode=cfg["act_mode"])
     B, D = cfg["batch"], cfg["decode"]
-    vis = visual_lengths(cfg)
     S = max(vis) + cfg["text"]
     eng = Q.Engine(c, max_batch=B, max_tokens=sum(vis) + B * cfg["text"], max_seq=S, max_decode=D + 2)
     g = torch.Generator(device="cuda").manual_seed(seed)
@@ -249,32 +274,40 @@ def build_engine(cfg, torch, Q, seed=1234):
     return eng
 
 
-def visual_lengths(cfg, seed=2024):
-    """Per-sequence visual counts: fixed, or seeded U[lo, hi] draws for ragged batches (configs[3])."""
+def visual_lengths(cfg, seqs=None, seed=2024):
+    """Per-sequence visual counts of the given global sequences (default: the first batch):
+    fixed, or seeded U[lo, hi] draws for ragged batches (configs[3])."""
     v = cfg["visual"]
+    seqs = list(range(cfg["batch"])) if seqs is None else seqs
     if isinstance(v, tuple):
-        rng = np.random.default_rng(seed)
-        return [int(x) for x in rng.integers(v[0], v[1] + 1, size=cfg["batch"])]
-    return [v] * cfg["batch"]
+        return [int(np.random.default_rng(seed + i).integers(v[0], v[1] + 1)) for i in seqs]
+    return [v] * len(seqs)
 
 
-def synth_inputs(cfg, torch, seed):
-    """Hidden states N(0,1) with a seeded 1 % of channels x20 (BASELINE.json configs)."""
-    g = torch.Generator(device="cpu").manual_seed(seed)
-    B, D, d = cfg["batch"], cfg["decode"], cfg["d_model"]
-    rows = sum(visual_lengths(cfg)) + B * cfg["text"]
-    ch = torch.randperm(d, generator=g)[:max(1, int(round(cfg["outlier"] * d)))]
-    emb = torch.randn(rows, d, generator=g)
-    emb[:, ch] *= 20.0
-    dec = torch.randn(D, B, d, generator=g)
-    dec[:, :, ch] *= 20.0
-    return emb.contiguous(), dec.contiguous()
+def synth_inputs(cfg, torch, seqs, vis):
+    """Hidden states N(0,1) with a seeded 1 % of channels x20 (BASELINE.json configs), seeded
+    per GLOBAL sequence index so a sequence's inputs do not depend on the sharding."""
+    D, d = cfg["decode"], cfg["d_model"]
+    ch = torch.randperm(d, generator=torch.Generator(device="cpu").manual_seed(77))[
+        :max(1, int(round(cfg["outlier"] * d)))]
+    embs, decs = [], []
+    for i, v in zip(seqs, vis):
+        g = torch.Generator(device="cpu").manual_seed(1000 + i)
+        e = torch.randn(v + cfg["text"], d, generator=g)
+        dd = torch.randn(D, d, generator=g)
+        e[:, ch] *= 20.0
+        dd[:, ch] *= 20.0
+        embs.append(e)
+        decs.append(dd)
+    return torch.cat(embs).contiguous(), torch.stack(decs, dim=1).contiguous()
 
 
 def run_ours(args, cfg):
     import torch
 
     import paper_2604_17320_b200 as Q
+
+    from paper_2604_17320_b200.shard import gather_equal_rows, max_over_ranks
 
     ws, rank, local = dist_env()
     if ws > 1:
@@ -286,24 +319,26 @@ def run_ours(args, cfg):
         torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     B, T, D, d = cfg["batch"], cfg["text"], cfg["decode"], cfg["d_model"]
-    vis = visual_lengths(cfg)
+    seqs = local_sequences(cfg, ws, rank)  # this rank's global sequence indices
+    assert len(seqs) == B
+    vis = visual_lengths(cfg, seqs)
     V = max(vis)
     rows = sum(vis) + B * T  # prefill tokens of the batch
     v0s = vis if cfg["v0"] is None else None  # ragged: each sequence's own v0
-    eng = build_engine(cfg, torch, Q)
+    eng = build_engine(cfg, torch, Q, vis)
     stream = torch.cuda.Stream(device=dev)
     eng.set_stream(stream)
-    emb_h, dec_h = synth_inputs(cfg, torch, seed=77 + rank)
+    emb_h, dec_h = synth_inputs(cfg, torch, seqs, vis)
     emb_d, dec_d = emb_h.to(dev), dec_h.to(dev)
     logits_d = torch.empty(rows, d, device=dev)
     dlog_d = torch.empty(B, d, device=dev)
     txt = [T] * B
     gathered = torch.empty(ws * B, d, device=dev) if ws > 1 else None
 
-    def gather_outputs():
+    def gather_outputs():  # the only collective: every sequence's final logits to rank 0's view
         if dist is not None:
             with torch.cuda.stream(stream):
-                dist.all_gather_into_tensor(gathered, dlog_d)
+                gather_equal_rows(dlog_d, gathered)
 
     def step_device():
         eng.prefill(emb_d, vis, txt, v0=v0s, logits_out=logits_d)
@@ -315,13 +350,20 @@ def run_ours(args, cfg):
     emb_p, dec_p = emb_h.pin_memory(), dec_h.pin_memory()
     logits_p = torch.empty(rows, d).pin_memory()
     dlog_p = torch.empty(D, B, d).pin_memory()
+    gathered_p = torch.empty(ws * B, d).pin_memory() if ws > 1 else None
 
     def step_e2e():
         # the prefill logits come back on the engine's copy stream while the decode steps run;
         # join_copies() puts their completion back on the timed stream before the step ends
         eng.prefill(emb_p, vis, txt, v0=v0s, logits_out=logits_p, logits_async=True)
         for t in range(D):
-            eng.decode(dec_p[t], logits_out=dlog_p[t])
+            eng.decode(dec_p[t], logits_out=dlog_p[t] if t < D - 1 else dlog_d)
+        with torch.cuda.stream(stream):
+            dlog_p[D - 1].copy_(dlog_d, non_blocking=True)
+            if dist is not None:  # the gathered final logits land in rank 0's host memory
+                gather_equal_rows(dlog_d, gathered)
+                if rank == 0:
+                    gathered_p.copy_(gathered, non_blocking=True)
         eng.join_copies()
 
     def barrier():
@@ -345,10 +387,8 @@ def run_ours(args, cfg):
             sampler.__exit__()
         barrier()
         ms = e0.elapsed_time(e1) / steps
-        if dist is not None:
-            t = torch.tensor([ms], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
+        if dist is not None:  # the job's step time is the slowest rank's
+            ms = max_over_ranks(ms, device=dev)
         return ms, (sampler.summary() if sampler else None)
 
     for _ in range(args.warmup):
@@ -460,7 +500,8 @@ def run_ours(args, cfg):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "int4xint4->int32 (W4A4), fp64 residual, int4 KV", "data": "synthetic",
-            "config": {"workload": cfg["workload"], "batch_per_gpu": B, "visual": V if len(set(vis)) == 1 else {"ragged": list(cfg["visual"]), "mean": float(np.mean(vis))},
+            "config": {"workload": cfg["workload"], "batch_per_gpu": B, "global_batch": ws * B,
+                       "visual": V if len(set(vis)) == 1 else {"ragged": list(cfg["visual"]), "mean": float(np.mean(vis))},
                        "text": T,
                        "decode_steps": D, "recipe": {"candidate_layers": cfg["layers"], "keep_ratios": cfg["keeps"],
                                                      "v0": cfg["v0"]},
@@ -475,7 +516,10 @@ def run_ours(args, cfg):
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_val, "unit": UNIT, "ms_per_step": ms_e2e,
                     "h2d_bytes_per_step": int(emb_p.numel() * 4 + dec_p.numel() * 4),
-                    "d2h_bytes_per_step": int(final_rows * d * 4 + D * B * d * 4)},
+                    "d2h_bytes_per_step": int(final_rows * d * 4 + D * B * d * 4 +
+                                              (ws * B * d * 4 if ws > 1 else 0)),
+                    "per_rank": True, "gather": "final decode logits of all ws x B sequences to rank 0 host"
+                    if ws > 1 else None},
             "gpu_launches": int(sum(v["launches"] for v in prof_pre.values())
                                 + D * sum(v["launches"] for v in prof_dec.values())),
             "clocks": clocks,
@@ -487,12 +531,58 @@ def run_ours(args, cfg):
         dist.destroy_process_group()
 
 
+def run_stub(args, cfg):
+    """The multi-rank plumbing of run_ours on CPU (gloo) with a stand-in for the engine:
+    shard the global batch, run each rank's sequences, gather every sequence's final row to
+    rank 0, time steps as the max over ranks.  For tests/test_bench_cpu.py only."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2604_17320_b200.shard import gather_equal_rows, max_over_ranks
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        dist.init_process_group("gloo")
+    B, d = cfg["batch"], 64
+    seqs = local_sequences(cfg, ws, rank)
+    w = torch.randn(d, d, generator=torch.Generator().manual_seed(5))
+
+    def step():
+        x = torch.stack([torch.full((d,), float(i)) for i in seqs])  # sequence i's "state"
+        for _ in range(cfg["decode"]):
+            x = torch.tanh(x @ w) + torch.tensor(seqs, dtype=torch.float32)[:, None]
+        x[:, -1] = torch.tensor(seqs, dtype=torch.float32)  # tag each row with its global sequence
+        out = torch.empty(ws * B, d)
+        if ws > 1:
+            gather_equal_rows(x, out)
+        else:
+            out.copy_(x)
+        return out
+
+    for _ in range(args.warmup):
+        step()
+    if ws > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        out = step()
+    ms = (time.perf_counter() - t0) * 1e3 / args.steps
+    ms_max = max_over_ranks(ms) if ws > 1 else ms
+    if rank == 0:
+        print(json.dumps({"impl": "stub", "metric": METRIC, "n_gpus": ws, "steps": args.steps,
+                          "ms_per_step": ms_max, "value": ws * B * cfg["decode"] / (ms_max / 1e3),
+                          "config": {"batch_per_gpu": B, "global_batch": ws * B},
+                          "gathered_last_col": out[:, -1].tolist(), "local_sequences": seqs}), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference", "stub"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--batch", type=int, default=None, help="override the config's per-GPU batch (c5 sweep)")
@@ -503,8 +593,15 @@ def main():
         cfg["batch"] = args.batch
     if args.decode:
         cfg["decode"] = args.decode
+    ws = int(os.environ.get("WORLD_SIZE", "0"))
+    if ws == 0 and args.gpus > 1:  # start the N ranks (one per GPU) ourselves
+        sys.exit(spawn_ranks(sys.argv[1:], args.gpus))
+    if ws and ws != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} does not match WORLD_SIZE {ws}")
     if args.impl == "reference":
         run_reference(args, cfg)
+    elif args.impl == "stub":
+        run_stub(args, cfg)
     else:
         run_ours(args, cfg)
 

@@ -253,8 +253,10 @@ struct qt_engine {
     float* dlogits = nullptr;  // [max_batch x d]
     float* part_ml = nullptr;
     float* part_o = nullptr;
-    int dec_splits = 1, dec_pps = 1;
-    std::vector<int> dec_pages;  // decode-attention page CTAs per layer
+    int dec_splits = 1, dec_pps = 1;   // the largest split plan over the layers (info)
+    std::vector<int> dec_pages;        // cache pages per (layer, sequence) over the decode horizon
+    std::vector<int> dec_lpps, dec_lsplit;  // decode-attention plan per layer (qt_attn_decode_plan)
+    int n_sms = 148;
     cudaGraphExec_t graph = nullptr;
     bool graph_ok = false;
     int decode_steps = 0;
@@ -491,9 +493,14 @@ struct qt_engine {
         xd_in = dalloc<float>((size_t)mb * d);
         dlogits = dalloc<float>((size_t)mb * d);
         dec_pps = 1;
-        dec_splits = max_pages;
+        dec_splits = max_pages;  // splits never exceed the pages
         part_ml = dalloc<float>((size_t)mb * H * dec_splits * 2);
         part_o = dalloc<float>((size_t)mb * H * dec_splits * dh);
+        {
+            int dev = 0;
+            ck(cudaGetDevice(&dev), "device");
+            ck(cudaDeviceGetAttribute(&n_sms, cudaDevAttrMultiProcessorCount, dev), "sm count");
+        }
         {  // split-K workspace: the largest ksplit * M * N over the GEMM shapes that split
             const int shapes[5][2] = {{n_qkv, kd_pad}, {d, kd_pad}, {n_gu, kd_pad}, {d, kff_pad}, {d, kd_pad}};
             size_t need = 0;
@@ -1445,8 +1452,16 @@ struct qt_engine {
                 dec_pages[l] = std::max(dec_pages[l], (cap + qt::kPage - 1) / qt::kPage);
                 maxp = std::max(maxp, dec_pages[l]);
             }
-        dec_pps = 1;  // one 64-row page per decode-attention CTA
-        dec_splits = maxp;
+        dec_lpps.assign(L, 1);
+        dec_lsplit.assign(L, 1);
+        dec_pps = dec_splits = 1;
+        for (int l = 0; l < L; ++l) {
+            if (qt_attn_decode_plan(B, Hkv, dec_pages[l], n_sms, &dec_lpps[l], &dec_lsplit[l]))
+                fail(QT_EINVAL, "decode attention plan");
+            dec_pps = std::max(dec_pps, dec_lpps[l]);
+            dec_splits = std::max(dec_splits, dec_lsplit[l]);
+        }
+        (void)maxp;
         ck(cudaStreamSynchronize(st), "prefill");
         decode_steps = 0;
         prefilled = true;
@@ -1464,29 +1479,24 @@ struct qt_engine {
             if (!(skip_mask & 4)) norm_quant(xcur, 1, d, w.g1, B, d, kd_pad, 4 * l + 0);
             cap_site(l, 0, B, d, kd_pad);
             if (!(skip_mask & 1)) gemm(QT_EPI_STORE, w.qkv, n_qkv_pad, w.s_qkv, B, n_qkv, kd_pad, qkv, n_qkv);
-            pb(P_KV);
-            if (!(skip_mask & 8))
-                ckl(qt_launch_rope_kv_append(qkv, n_qkv, B, H, Hkv, dh, next_pos, dec_seq, lenl, rope, ptl, max_pages,
-                                             pool, page_bytes, 4, nullptr, st),
-                    "decode kv append");
-            pe((double)B * n_qkv * 8 + (double)B * Hkv * 2 * (dh / 2 + 4));
-            if (capture) {
-                std::vector<int> r0(B), nr(B, 1);
-                for (int b = 0; b < B; ++b) r0[b] = h_kvlen[(size_t)l * B + b];
-                cap_kv(l, r0, nr);
-            }
             pb(P_ATTN);
-            // decode attention over the int4 pages + split merge fused with the attn_out quantizer
+            // decode attention over the int4 pages with the new token's RoPE + K/V quantize +
+            // append fused in, then the split merge fused with the attn_out quantizer
             if (!(skip_mask & 2))
-                ckl(qt_launch_attn_decode(qkv, n_qkv, H, Hkv, dh, lenl, 1, B, pool, page_bytes, ptl, max_pages,
-                                          dec_pages[l], part_ml, part_o, nullptr, d, codes, codes_rows, ascale,
-                                          cfg.act_mode, cfg.act_mode == 0 ? act[4 * l + 1] : 0.0, kd_pad, 4, nullptr,
-                                          nullptr, nullptr, nullptr, nullptr, st),
+                ckl(qt_launch_attn_decode(qkv, n_qkv, H, Hkv, dh, lenl, B, pool, page_bytes, ptl, max_pages,
+                                          dec_lpps[l], dec_lsplit[l], rope, next_pos, part_ml, part_o, nullptr, d,
+                                          codes, codes_rows, ascale, cfg.act_mode,
+                                          cfg.act_mode == 0 ? act[4 * l + 1] : 0.0, kd_pad, 4, st),
                     "decode attention");
             {  // decode attention streams every cached K/V row of this layer once
                 double rows = 0;
                 for (int b = 0; b < B; ++b) rows += h_kvlen[(size_t)l * B + b] + 1;
-                pe(rows * Hkv * 2 * (dh / 2 + 4) + (double)B * H * dh * 8);
+                pe(rows * Hkv * 2 * (dh / 2 + 4) + (double)B * (H + 2 * Hkv) * dh * 4);
+            }
+            if (capture) {
+                std::vector<int> r0(B), nr(B, 1);
+                for (int b = 0; b < B; ++b) r0[b] = h_kvlen[(size_t)l * B + b];
+                cap_kv(l, r0, nr);
             }
             cap_site(l, 1, B, d, kd_pad);
             if (!(skip_mask & 1)) gemm(QT_EPI_RESADD, w.o, nd_pad, w.s_o, B, d, kd_pad, xcur, d);
@@ -2360,9 +2370,13 @@ int qt_attn_decode_i4kv(const float* q, int ldq, int B, int H, int Hkv, int d_he
         const int pages = (max_len + qt::kPage - 1) / qt::kPage;
         float* part_ml = static_cast<float*>(workspace);
         float* part_o = part_ml + (size_t)B * H * pages * 2;
-        ckl(qt_launch_attn_decode(q, ldq, H, Hkv, d_head, kv_len, 0, B, const_cast<uint8_t*>(pool), page_bytes,
-                                  page_table, max_pages, pages, part_ml, part_o, out, ldo, nullptr, 0, nullptr, 1,
-                                  0.0, 0, 4, nullptr, nullptr, nullptr, nullptr, nullptr, (cudaStream_t)stream),
+        int dev = 0, sms = 148, pps = 1, nsplit = 1;
+        ck(cudaGetDevice(&dev), "device");
+        ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "sm count");
+        if (qt_attn_decode_plan(B, Hkv, pages, sms, &pps, &nsplit)) fail(QT_EINVAL, "decode attention plan");
+        ckl(qt_launch_attn_decode(q, ldq, H, Hkv, d_head, kv_len, B, const_cast<uint8_t*>(pool), page_bytes,
+                                  page_table, max_pages, pps, nsplit, nullptr, nullptr, part_ml, part_o, out, ldo,
+                                  nullptr, 0, nullptr, 1, 0.0, 0, 4, (cudaStream_t)stream),
             "decode attention");
     });
 }

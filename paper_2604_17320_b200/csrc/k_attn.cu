@@ -9,9 +9,7 @@
 //       i and head h, column sums of softmax probabilities over text queries
 //       (m^inter) and over visual queries (m^intra).  Deterministic: partial
 //       sums per (seq, head, key) in fixed order, no float atomics.
-//   K6  decode attention (model.cpp:515-535): one query row per sequence over
-//       all cached rows, unmasked, 128-bit coalesced int4 loads dequantised in
-//       registers, split over pages + a fixed-order merge.
+//   (K6, decode attention, is k_attn_decode.cu)
 //
 // Tensor-core math (mma.sync m16n8k16 f16->f32) uses hi/lo fp16 splits of the
 // fp32 operand (q, or p * s_v); int4 codes are exact in fp16, so products are
@@ -397,638 +395,6 @@ __global__ void __launch_bounds__(128) k_attn_colsum(const float* __restrict__ q
     }
 }
 
-// ============================================================== K6 merge by the last arrival
-// Called by every page CTA of (b, h) after its partial is written (128 threads).
-// The last CTA to arrive for (b, h) merges the head's page partials in fixed page
-// order -- the same arithmetic as k_attn_merge_quant -- into the fp32 attention
-// row and the head's max |o|; the last head of sequence b to finish then
-// quantizes the whole row for the attn_out site.  Both arrival counters
-// (cnt[b*H + h], cnt[B*H + b]) are reset by their last arrival, so the kernel
-// replays from a CUDA graph.  Replaces the separate merge launch.
-template <int DH>
-QT_DEV void attn_dec_arrive(int b, int h, int H, int npg, const float* part_ml, const float* part_o, unsigned* cnt,
-                            float* row, float* hmax, uint8_t* codes, int ld_codes, double* scales, int qmode,
-                            double static_scale, int d_pad, int qmax) {
-    __shared__ unsigned s_last;
-    __shared__ float s_red[4];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int B = gridDim.z;
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) s_last = atomicAdd(&cnt[b * H + h], 1u) == (unsigned)npg - 1;
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    if (tid == 0) cnt[b * H + h] = 0;
-    const size_t base = ((size_t)b * H + h) * npg;
-    float M = -1e30f;
-    for (int p = lane; p < npg; p += 32) M = fmaxf(M, part_ml[(base + p) * 2]);
-    M = warp_max(M);
-    float L = 0.f, o = 0.f;
-    for (int p0 = 0; p0 < npg; p0 += 4) {  // 4 pages' loads in flight, summed in page order
-        float2 ml4[4];
-        float ov[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int p = p0 + j;
-            ml4[j] = p < npg ? *reinterpret_cast<const float2*>(part_ml + (base + p) * 2) : make_float2(-1e30f, 0.f);
-            ov[j] = p < npg && tid < DH ? part_o[(base + p) * DH + tid] : 0.f;
-        }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            if (ml4[j].y == 0.f) continue;
-            const float a = expf(ml4[j].x - M);
-            L += ml4[j].y * a;
-            o += ov[j] * a;
-        }
-    }
-    o *= 1.f / L;
-    const int HD = H * DH;
-    if (tid < DH) row[(size_t)b * HD + h * DH + tid] = o;
-    float mx = tid < DH ? fabsf(o) : 0.f;
-    mx = warp_max(mx);
-    if (lane == 0) s_red[warp] = mx;
-    __syncthreads();
-    if (tid == 0) hmax[b * H + h] = fmaxf(fmaxf(s_red[0], s_red[1]), fmaxf(s_red[2], s_red[3]));
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) s_last = atomicAdd(&cnt[B * H + b], 1u) == (unsigned)H - 1;
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    if (tid == 0) cnt[B * H + b] = 0;
-    double s = static_scale;
-    if (qmode != 0) {
-        float m2 = 0.f;
-        for (int i = lane; i < H; i += 32) m2 = fmaxf(m2, hmax[b * H + i]);
-        s = q_scale((double)warp_max(m2), qmax);
-    }
-    const double inv_s = 1.0 / s;
-    for (int w = tid; w < d_pad / 8; w += blockDim.x) {
-        int c[8];
-        if (w * 8 < HD) {
-            const float4 a = *reinterpret_cast<const float4*>(row + (size_t)b * HD + w * 8);
-            const float4 bq = *reinterpret_cast<const float4*>(row + (size_t)b * HD + w * 8 + 4);
-            const float f[8] = {a.x, a.y, a.z, a.w, bq.x, bq.y, bq.z, bq.w};
-#pragma unroll
-            for (int e = 0; e < 8; ++e) c[e] = q_code_r((double)f[e], s, inv_s, qmax);
-        } else {
-#pragma unroll
-            for (int e = 0; e < 8; ++e) c[e] = 0;
-        }
-        *reinterpret_cast<uint32_t*>(codes + w4t_offset(b, w * 4, ld_codes)) = pack8(c);
-    }
-    if (tid == 0) scales[b] = s;
-}
-
-// ============================================================== K6
-// grid (pages, H, B), 128 threads: one CTA per (64-row page, query head,
-// sequence) -- the cache length is read from device memory so the decode step
-// replays from a CUDA graph.  Each warp owns 16 rows; 4 lanes per row each
-// hold 32 channels (16 bytes of int4 codes), and both of a lane's rows are
-// loaded before any math so two 128-bit loads per operand are in flight.
-//
-// rope != nullptr (the decode step, K5 fused in): q is RoPE'd in registers from
-// the raw GEMV output, and the CTAs of the page holding the new row (row
-// kv_len) RoPE + quantize that token's K and V (kv_quantize, quant.cpp:117-119)
-// and append them before attending -- one launch instead of two.  With GQA the
-// group's query-head CTAs write identical bytes.
-template <int DH>
-__global__ void __launch_bounds__(128) k_attn_decode(const float* __restrict__ qkv, int ldq, int H, int Hkv,
-                                                     const int* __restrict__ kv_len, int len_add,
-                                                     uint8_t* __restrict__ pool, long long page_bytes,
-                                                     const int* __restrict__ pt, int max_pages, float inv_sqrt,
-                                                     float* __restrict__ part_ml, float* __restrict__ part_o,
-                                                     const double2* __restrict__ rope, const int* __restrict__ pos,
-                                                     unsigned* __restrict__ cnt, float* __restrict__ row,
-                                                     float* __restrict__ hmax, uint8_t* __restrict__ codes,
-                                                     int ld_codes, double* __restrict__ scales, int qmode,
-                                                     double static_scale, int d_pad, int qmax) {
-    constexpr int CPL = DH / 4;  // channels per lane
-    constexpr int R = 2;         // rows per lane
-    pdl_launch_dependents();
-    // Without the fused append (rope == null) every cached row but the newest (len - 1, written
-    // by the K/V append kernel just before) is final since earlier steps, as are kv_len and the
-    // page table: those loads are issued before the dependency wait and overlap the upstream
-    // kernel; q and the newest row are read after it (the row through L2, not the .nc path,
-    // since its 128-byte line may have been cached with the row before it).
-    if (rope) pdl_wait();
-    const int b = blockIdx.z, h = blockIdx.y, pg = blockIdx.x, npg = gridDim.x;
-    const int kh = h / (H / Hkv);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int q4 = lane & 3, quad = lane >> 2;
-    const int len = kv_len[b] + len_add;
-    const int r0 = pg * kPage;
-    const size_t pidx = ((size_t)b * H + h) * npg + pg;
-    const double2* rt = rope ? rope + (size_t)pos[b] * (DH / 2) : nullptr;
-    if (rope && pg == (len - 1) / kPage && warp < 2) {
-        // append the new token's K (warp 0, RoPE'd) or V (warp 1) of kv head kh at row len-1
-        constexpr int E = DH / 32;
-        const int r = len - 1;
-        const bool is_k = warp == 0;
-        const float* src = qkv + (size_t)b * ldq + (is_k ? H * DH : (H + Hkv) * DH) + kh * DH;
-        double val[E];
-#pragma unroll
-        for (int j = 0; j < E; ++j) val[j] = (double)src[lane * E + j];
-        if (is_k) {
-#pragma unroll
-            for (int j = 0; j < E; j += 2) {
-                const double2 cs = rt[(lane * E + j) / 2];
-                const double a = val[j], bb = val[j + 1];
-                val[j] = __dsub_rn(__dmul_rn(a, cs.x), __dmul_rn(bb, cs.y));
-                val[j + 1] = __dadd_rn(__dmul_rn(a, cs.y), __dmul_rn(bb, cs.x));
-            }
-        }
-        double mx = 0.0;
-#pragma unroll
-        for (int j = 0; j < E; ++j) mx = fmax(mx, fabs(val[j]));
-        mx = warp_max(mx);
-        const double s = q_scale(mx, 7), inv_s = 1.0 / s;
-        int c[4] = {0, 0, 0, 0};
-#pragma unroll
-        for (int j = 0; j < E; ++j) c[j] = q_code_r(val[j], s, inv_s, 7);
-        uint8_t* page = pool + (long long)pt[b * max_pages + r / kPage] * page_bytes;
-        const size_t cbn = (size_t)Hkv * kPage * (DH / 2);
-        uint8_t* dst = page + (is_k ? 0 : cbn) + ((size_t)kh * kPage + r % kPage) * (DH / 2) + lane * E / 2;
-        if (E == 4)
-            *reinterpret_cast<uint16_t*>(dst) =
-                (uint16_t)((c[0] & 0xF) | ((c[1] & 0xF) << 4) | ((c[2] & 0xF) << 8) | ((c[3] & 0xF) << 12));
-        else
-            *dst = (uint8_t)((c[0] & 0xF) | ((c[1] & 0xF) << 4));
-        if (lane == 0)
-            reinterpret_cast<float*>(page + 2 * cbn)[(is_k ? 0 : Hkv * kPage) + kh * kPage + r % kPage] = (float)s;
-    }
-    if (rope) __syncthreads();  // the appended row is visible to the block's loads below
-    if (r0 >= len) {
-        if (!rope) pdl_wait();  // part buffers are still read by the previous layer's merge
-        if (threadIdx.x < DH) part_o[pidx * DH + threadIdx.x] = 0.f;
-        if (threadIdx.x == 0) {
-            part_ml[pidx * 2] = -1e30f;
-            part_ml[pidx * 2 + 1] = 0.f;
-        }
-        if (cnt) attn_dec_arrive<DH>(b, h, H, npg, part_ml, part_o, cnt, row, hmax, codes, ld_codes, scales, qmode,
-                                     static_scale, d_pad, qmax);
-        return;
-    }
-    const uint8_t* page = pool + (long long)pt[b * max_pages + pg] * page_bytes;
-    const size_t cb = (size_t)Hkv * kPage * (DH / 2);
-    const float* sc = reinterpret_cast<const float*>(page + 2 * cb);
-    uint32_t kw[R][CPL / 8], vw[R][CPL / 8];
-    float sk[R], sv[R];
-    bool valid[R];
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-        const int slot = warp * 16 + quad + 8 * i;
-        valid[i] = r0 + slot < len;
-        const bool ld = valid[i] && (rope || r0 + slot != len - 1);  // the newest row: after the wait
-        const uint8_t* krow = page + ((size_t)kh * kPage + slot) * (DH / 2) + q4 * (CPL / 2);
-        if (CPL == 32) {
-            uint4 ka = ld ? ldg_nc_v4(krow) : make_uint4(0, 0, 0, 0);
-            uint4 va = ld ? ldg_nc_v4(krow + cb) : make_uint4(0, 0, 0, 0);
-            kw[i][0] = ka.x; kw[i][1] = ka.y; kw[i][2] = ka.z; kw[i][3] = ka.w;
-            vw[i][0] = va.x; vw[i][1] = va.y; vw[i][2] = va.z; vw[i][3] = va.w;
-        } else {
-            uint2 ka = ld ? *reinterpret_cast<const uint2*>(krow) : make_uint2(0, 0);
-            uint2 va = ld ? *reinterpret_cast<const uint2*>(krow + cb) : make_uint2(0, 0);
-            kw[i][0] = ka.x; kw[i][1] = ka.y;
-            vw[i][0] = va.x; vw[i][1] = va.y;
-        }
-        sk[i] = ld ? sc[kh * kPage + slot] : 0.f;
-        sv[i] = ld ? sc[Hkv * kPage + kh * kPage + slot] : 0.f;
-    }
-    if (!rope) {
-        pdl_wait();  // q and the newest row come from the upstream kernels
-#pragma unroll
-        for (int i = 0; i < R; ++i) {
-            const int slot = warp * 16 + quad + 8 * i;
-            if (!(valid[i] && r0 + slot == len - 1)) continue;
-            const uint8_t* krow = page + ((size_t)kh * kPage + slot) * (DH / 2) + q4 * (CPL / 2);
-            if (CPL == 32) {
-                const uint4 ka = __ldcg(reinterpret_cast<const uint4*>(krow));
-                const uint4 va = __ldcg(reinterpret_cast<const uint4*>(krow + cb));
-                kw[i][0] = ka.x; kw[i][1] = ka.y; kw[i][2] = ka.z; kw[i][3] = ka.w;
-                vw[i][0] = va.x; vw[i][1] = va.y; vw[i][2] = va.z; vw[i][3] = va.w;
-            } else {
-                const uint2 ka = __ldcg(reinterpret_cast<const uint2*>(krow));
-                const uint2 va = __ldcg(reinterpret_cast<const uint2*>(krow + cb));
-                kw[i][0] = ka.x; kw[i][1] = ka.y;
-                vw[i][0] = va.x; vw[i][1] = va.y;
-            }
-            sk[i] = __ldcg(sc + kh * kPage + slot);
-            sv[i] = __ldcg(sc + Hkv * kPage + kh * kPage + slot);
-        }
-    }
-    float q[CPL];
-    const float* qp = qkv + (size_t)b * ldq + h * DH + q4 * CPL;
-#pragma unroll
-    for (int i = 0; i < CPL; i += 4) {
-        float4 v = *reinterpret_cast<const float4*>(qp + i);
-        q[i] = v.x; q[i + 1] = v.y; q[i + 2] = v.z; q[i + 3] = v.w;
-    }
-    if (rope) {  // interleaved-pair RoPE of q in fp32 (q only feeds fp32 scores; K keeps the fp64 path)
-#pragma unroll
-        for (int i = 0; i < CPL; i += 2) {
-            const double2 cs = rt[(q4 * CPL + i) / 2];
-            const float c = (float)cs.x, sn = (float)cs.y, a = q[i], bb = q[i + 1];
-            q[i] = fmaf(a, c, -bb * sn);
-            q[i + 1] = fmaf(a, sn, bb * c);
-        }
-    }
-    float s[R];
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-        float d = 0.f;
-#pragma unroll
-        for (int w = 0; w < CPL / 8; ++w)
-#pragma unroll
-            for (int e = 0; e < 8; ++e) d = fmaf(q[w * 8 + e], (float)nib(kw[i][w], e), d);
-        d += __shfl_xor_sync(0xffffffffu, d, 1);
-        d += __shfl_xor_sync(0xffffffffu, d, 2);
-        s[i] = valid[i] ? d * sk[i] * inv_sqrt : -1e30f;
-    }
-    float m = fmaxf(s[0], s[1]);
-    float l = 0.f;
-    float acc[CPL];
-#pragma unroll
-    for (int c = 0; c < CPL; ++c) acc[c] = 0.f;
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-        if (!valid[i]) continue;
-        const float p = expf(s[i] - m);
-        l += p;
-        const float pv = p * sv[i];
-#pragma unroll
-        for (int w = 0; w < CPL / 8; ++w)
-#pragma unroll
-            for (int e = 0; e < 8; ++e) acc[w * 8 + e] = fmaf(pv, (float)nib(vw[i][w], e), acc[w * 8 + e]);
-    }
-    // merge the 8 quads of the warp (lanes with equal q4)
-#pragma unroll
-    for (int o = 4; o < 32; o <<= 1) {
-        const float mo = __shfl_xor_sync(0xffffffffu, m, o);
-        const float lo = __shfl_xor_sync(0xffffffffu, l, o);
-        const float mn = fmaxf(m, mo);
-        const float a1 = expf(m - mn), a2 = expf(mo - mn);
-        l = l * a1 + lo * a2;
-#pragma unroll
-        for (int c = 0; c < CPL; ++c) {
-            const float ao = __shfl_xor_sync(0xffffffffu, acc[c], o);
-            acc[c] = acc[c] * a1 + ao * a2;
-        }
-        m = mn;
-    }
-    __shared__ float smx[4][2];
-    __shared__ float so[4][DH];
-    if (quad == 0) {
-#pragma unroll
-        for (int c = 0; c < CPL; ++c) so[warp][q4 * CPL + c] = acc[c];
-        if (q4 == 0) {
-            smx[warp][0] = m;
-            smx[warp][1] = l;
-        }
-    }
-    __syncthreads();
-    if (threadIdx.x < DH) {
-        float mm = -1e30f;
-        for (int w = 0; w < 4; ++w) mm = fmaxf(mm, smx[w][0]);
-        float ll = 0.f, oo = 0.f;
-        for (int w = 0; w < 4; ++w) {
-            const float a = smx[w][1] > 0.f ? expf(smx[w][0] - mm) : 0.f;
-            ll += smx[w][1] * a;
-            oo += so[w][threadIdx.x] * a;
-        }
-        part_o[pidx * DH + threadIdx.x] = oo;
-        if (threadIdx.x == 0) {
-            part_ml[pidx * 2] = mm;
-            part_ml[pidx * 2 + 1] = ll;
-        }
-    }
-    if (cnt) attn_dec_arrive<DH>(b, h, H, npg, part_ml, part_o, cnt, row, hmax, codes, ld_codes, scales, qmode,
-                                 static_scale, d_pad, qmax);
-}
-
-// Two 64-row pages per CTA (4 rows per lane): half the CTAs and half the partials of
-// k_attn_decode.  Unfused path only (rope == nullptr).
-template <int DH, int PP = 2>
-__global__ void __launch_bounds__(128) k_attn_decode_pp2(const float* __restrict__ qkv, int ldq, int H, int Hkv,
-                                                     const int* __restrict__ kv_len, int len_add,
-                                                     uint8_t* __restrict__ pool, long long page_bytes,
-                                                     const int* __restrict__ pt, int max_pages, float inv_sqrt,
-                                                     float* __restrict__ part_ml, float* __restrict__ part_o,
-                                                     const double2* __restrict__ rope, const int* __restrict__ pos,
-                                                     unsigned* __restrict__ cnt, float* __restrict__ row,
-                                                     float* __restrict__ hmax, uint8_t* __restrict__ codes,
-                                                     int ld_codes, double* __restrict__ scales, int qmode,
-                                                     double static_scale, int d_pad, int qmax) {
-    constexpr int CPL = DH / 4;  // channels per lane
-    constexpr int R = 2 * PP;    // rows per lane: PP 64-row pages per CTA
-    constexpr int WR = 16 * PP;  // rows per warp (64 / WR warps per page)
-    pdl_launch_dependents();
-    // Without the fused append (rope == null) every cached row but the newest (len - 1, written
-    // by the K/V append kernel just before) is final since earlier steps, as are kv_len and the
-    // page table: those loads are issued before the dependency wait and overlap the upstream
-    // kernel; q and the newest row are read after it (the row through L2, not the .nc path,
-    // since its 128-byte line may have been cached with the row before it).
-    if (rope) pdl_wait();
-    const int b = blockIdx.z, h = blockIdx.y, pg = blockIdx.x, npg = gridDim.x;
-    const int kh = h / (H / Hkv);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int q4 = lane & 3, quad = lane >> 2;
-    const int len = kv_len[b] + len_add;
-    const int r0 = pg * PP * kPage;
-    const size_t pidx = ((size_t)b * H + h) * npg + pg;
-    const double2* rt = rope ? rope + (size_t)pos[b] * (DH / 2) : nullptr;
-    if (rope && pg == (len - 1) / kPage && warp < 2) {
-        // append the new token's K (warp 0, RoPE'd) or V (warp 1) of kv head kh at row len-1
-        constexpr int E = DH / 32;
-        const int r = len - 1;
-        const bool is_k = warp == 0;
-        const float* src = qkv + (size_t)b * ldq + (is_k ? H * DH : (H + Hkv) * DH) + kh * DH;
-        double val[E];
-#pragma unroll
-        for (int j = 0; j < E; ++j) val[j] = (double)src[lane * E + j];
-        if (is_k) {
-#pragma unroll
-            for (int j = 0; j < E; j += 2) {
-                const double2 cs = rt[(lane * E + j) / 2];
-                const double a = val[j], bb = val[j + 1];
-                val[j] = __dsub_rn(__dmul_rn(a, cs.x), __dmul_rn(bb, cs.y));
-                val[j + 1] = __dadd_rn(__dmul_rn(a, cs.y), __dmul_rn(bb, cs.x));
-            }
-        }
-        double mx = 0.0;
-#pragma unroll
-        for (int j = 0; j < E; ++j) mx = fmax(mx, fabs(val[j]));
-        mx = warp_max(mx);
-        const double s = q_scale(mx, 7), inv_s = 1.0 / s;
-        int c[4] = {0, 0, 0, 0};
-#pragma unroll
-        for (int j = 0; j < E; ++j) c[j] = q_code_r(val[j], s, inv_s, 7);
-        uint8_t* page = pool + (long long)pt[b * max_pages + r / kPage] * page_bytes;
-        const size_t cbn = (size_t)Hkv * kPage * (DH / 2);
-        uint8_t* dst = page + (is_k ? 0 : cbn) + ((size_t)kh * kPage + r % kPage) * (DH / 2) + lane * E / 2;
-        if (E == 4)
-            *reinterpret_cast<uint16_t*>(dst) =
-                (uint16_t)((c[0] & 0xF) | ((c[1] & 0xF) << 4) | ((c[2] & 0xF) << 8) | ((c[3] & 0xF) << 12));
-        else
-            *dst = (uint8_t)((c[0] & 0xF) | ((c[1] & 0xF) << 4));
-        if (lane == 0)
-            reinterpret_cast<float*>(page + 2 * cbn)[(is_k ? 0 : Hkv * kPage) + kh * kPage + r % kPage] = (float)s;
-    }
-    if (rope) __syncthreads();  // the appended row is visible to the block's loads below
-    if (r0 >= len) {
-        if (!rope) pdl_wait();  // part buffers are still read by the previous layer's merge
-        if (threadIdx.x < DH) part_o[pidx * DH + threadIdx.x] = 0.f;
-        if (threadIdx.x == 0) {
-            part_ml[pidx * 2] = -1e30f;
-            part_ml[pidx * 2 + 1] = 0.f;
-        }
-        if (cnt) attn_dec_arrive<DH>(b, h, H, npg, part_ml, part_o, cnt, row, hmax, codes, ld_codes, scales, qmode,
-                                     static_scale, d_pad, qmax);
-        return;
-    }
-    const int wrow0 = r0 + warp * WR;  // a warp's 32 rows lie in one page
-    // (clamped: a trailing odd page's partner may lie past the table; its rows are all invalid)
-    const uint8_t* page = pool + (long long)pt[b * max_pages + min(wrow0 / kPage, max_pages - 1)] * page_bytes;
-    const int pofs = wrow0 % kPage;
-    const size_t cb = (size_t)Hkv * kPage * (DH / 2);
-    const float* sc = reinterpret_cast<const float*>(page + 2 * cb);
-    uint32_t kw[R][CPL / 8], vw[R][CPL / 8];
-    float sk[R], sv[R];
-    bool valid[R];
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-        const int slot = warp * WR + quad + 8 * i;
-        valid[i] = r0 + slot < len;
-        const bool ld = valid[i] && (rope || r0 + slot != len - 1);  // the newest row: after the wait
-        const uint8_t* krow = page + ((size_t)kh * kPage + pofs + quad + 8 * i) * (DH / 2) + q4 * (CPL / 2);
-        if (CPL == 32) {
-            uint4 ka = ld ? ldg_nc_v4(krow) : make_uint4(0, 0, 0, 0);
-            uint4 va = ld ? ldg_nc_v4(krow + cb) : make_uint4(0, 0, 0, 0);
-            kw[i][0] = ka.x; kw[i][1] = ka.y; kw[i][2] = ka.z; kw[i][3] = ka.w;
-            vw[i][0] = va.x; vw[i][1] = va.y; vw[i][2] = va.z; vw[i][3] = va.w;
-        } else {
-            uint2 ka = ld ? *reinterpret_cast<const uint2*>(krow) : make_uint2(0, 0);
-            uint2 va = ld ? *reinterpret_cast<const uint2*>(krow + cb) : make_uint2(0, 0);
-            kw[i][0] = ka.x; kw[i][1] = ka.y;
-            vw[i][0] = va.x; vw[i][1] = va.y;
-        }
-        sk[i] = ld ? sc[kh * kPage + pofs + quad + 8 * i] : 0.f;
-        sv[i] = ld ? sc[Hkv * kPage + kh * kPage + pofs + quad + 8 * i] : 0.f;
-    }
-    if (!rope) {
-        pdl_wait();  // q and the newest row come from the upstream kernels
-#pragma unroll
-        for (int i = 0; i < R; ++i) {
-            const int slot = warp * WR + quad + 8 * i;
-            if (!(valid[i] && r0 + slot == len - 1)) continue;
-            const uint8_t* krow = page + ((size_t)kh * kPage + pofs + quad + 8 * i) * (DH / 2) + q4 * (CPL / 2);
-            if (CPL == 32) {
-                const uint4 ka = __ldcg(reinterpret_cast<const uint4*>(krow));
-                const uint4 va = __ldcg(reinterpret_cast<const uint4*>(krow + cb));
-                kw[i][0] = ka.x; kw[i][1] = ka.y; kw[i][2] = ka.z; kw[i][3] = ka.w;
-                vw[i][0] = va.x; vw[i][1] = va.y; vw[i][2] = va.z; vw[i][3] = va.w;
-            } else {
-                const uint2 ka = __ldcg(reinterpret_cast<const uint2*>(krow));
-                const uint2 va = __ldcg(reinterpret_cast<const uint2*>(krow + cb));
-                kw[i][0] = ka.x; kw[i][1] = ka.y;
-                vw[i][0] = va.x; vw[i][1] = va.y;
-            }
-            sk[i] = __ldcg(sc + kh * kPage + pofs + quad + 8 * i);
-            sv[i] = __ldcg(sc + Hkv * kPage + kh * kPage + pofs + quad + 8 * i);
-        }
-    }
-    float q[CPL];
-    const float* qp = qkv + (size_t)b * ldq + h * DH + q4 * CPL;
-#pragma unroll
-    for (int i = 0; i < CPL; i += 4) {
-        float4 v = *reinterpret_cast<const float4*>(qp + i);
-        q[i] = v.x; q[i + 1] = v.y; q[i + 2] = v.z; q[i + 3] = v.w;
-    }
-    if (rope) {  // interleaved-pair RoPE of q in fp32 (q only feeds fp32 scores; K keeps the fp64 path)
-#pragma unroll
-        for (int i = 0; i < CPL; i += 2) {
-            const double2 cs = rt[(q4 * CPL + i) / 2];
-            const float c = (float)cs.x, sn = (float)cs.y, a = q[i], bb = q[i + 1];
-            q[i] = fmaf(a, c, -bb * sn);
-            q[i + 1] = fmaf(a, sn, bb * c);
-        }
-    }
-    float s[R];
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-        float d = 0.f;
-#pragma unroll
-        for (int w = 0; w < CPL / 8; ++w)
-#pragma unroll
-            for (int e = 0; e < 8; ++e) d = fmaf(q[w * 8 + e], (float)nib(kw[i][w], e), d);
-        d += __shfl_xor_sync(0xffffffffu, d, 1);
-        d += __shfl_xor_sync(0xffffffffu, d, 2);
-        s[i] = valid[i] ? d * sk[i] * inv_sqrt : -1e30f;
-    }
-    float m = s[0];
-#pragma unroll
-    for (int i = 1; i < R; ++i) m = fmaxf(m, s[i]);
-    float l = 0.f;
-    float acc[CPL];
-#pragma unroll
-    for (int c = 0; c < CPL; ++c) acc[c] = 0.f;
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-        if (!valid[i]) continue;
-        const float p = expf(s[i] - m);
-        l += p;
-        const float pv = p * sv[i];
-#pragma unroll
-        for (int w = 0; w < CPL / 8; ++w)
-#pragma unroll
-            for (int e = 0; e < 8; ++e) acc[w * 8 + e] = fmaf(pv, (float)nib(vw[i][w], e), acc[w * 8 + e]);
-    }
-    // merge the 8 quads of the warp (lanes with equal q4)
-#pragma unroll
-    for (int o = 4; o < 32; o <<= 1) {
-        const float mo = __shfl_xor_sync(0xffffffffu, m, o);
-        const float lo = __shfl_xor_sync(0xffffffffu, l, o);
-        const float mn = fmaxf(m, mo);
-        const float a1 = expf(m - mn), a2 = expf(mo - mn);
-        l = l * a1 + lo * a2;
-#pragma unroll
-        for (int c = 0; c < CPL; ++c) {
-            const float ao = __shfl_xor_sync(0xffffffffu, acc[c], o);
-            acc[c] = acc[c] * a1 + ao * a2;
-        }
-        m = mn;
-    }
-    __shared__ float smx[4][2];
-    __shared__ float so[4][DH];
-    if (quad == 0) {
-#pragma unroll
-        for (int c = 0; c < CPL; ++c) so[warp][q4 * CPL + c] = acc[c];
-        if (q4 == 0) {
-            smx[warp][0] = m;
-            smx[warp][1] = l;
-        }
-    }
-    __syncthreads();
-    if (threadIdx.x < DH) {
-        float mm = -1e30f;
-        for (int w = 0; w < 4; ++w) mm = fmaxf(mm, smx[w][0]);
-        float ll = 0.f, oo = 0.f;
-        for (int w = 0; w < 4; ++w) {
-            const float a = smx[w][1] > 0.f ? expf(smx[w][0] - mm) : 0.f;
-            ll += smx[w][1] * a;
-            oo += so[w][threadIdx.x] * a;
-        }
-        part_o[pidx * DH + threadIdx.x] = oo;
-        if (threadIdx.x == 0) {
-            part_ml[pidx * 2] = mm;
-            part_ml[pidx * 2 + 1] = ll;
-        }
-    }
-    if (cnt) attn_dec_arrive<DH>(b, h, H, npg, part_ml, part_o, cnt, row, hmax, codes, ld_codes, scales, qmode,
-                                 static_scale, d_pad, qmax);
-}
-
-// Merge the page partials of every head of one sequence (fixed page order) and,
-// optionally, quantize the concatenated attention row (the attn_out site,
-// model.cpp:394/539) in the same kernel.  grid B, 1024 threads: warp w merges
-// heads w, w+32, ...; lane c holds channels c*CPL.. of that head.
-template <int DH, int MAXH>
-__global__ void __launch_bounds__(1024) k_attn_merge_quant(const float* __restrict__ part_ml,
-                                                           const float* __restrict__ part_o, int npg, int H,
-                                                           float* __restrict__ out, int ldo,
-                                                           uint8_t* __restrict__ codes, int ld_codes,
-                                                           double* __restrict__ scales, int mode, double static_scale,
-                                                           int d_pad, int qmax) {
-    constexpr int CPL = DH / 32;
-    __shared__ double red[32];
-    pdl_launch_dependents();
-    pdl_wait();
-    const int b = blockIdx.x;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    constexpr int HPW = (MAXH + 31) / 32;  // heads per warp
-    float o[HPW][CPL];
-    double mx = 0.0;
-#pragma unroll
-    for (int hh = 0; hh < HPW; ++hh) {
-        const int h = warp + 32 * hh;
-#pragma unroll
-        for (int c = 0; c < CPL; ++c) o[hh][c] = 0.f;
-        if (h >= H) continue;
-        const size_t base = ((size_t)b * H + h) * npg;
-        float M = -1e30f;
-        float L = 0.f;
-        if (npg <= 32) {
-            // lane p holds page p's (m, l): one load per lane, then the page loop only loads o
-            // (independent of M, so it pipelines) and takes (m, l) by shuffle -- same sums
-            float2 mlv = make_float2(-1e30f, 0.f);
-            if (lane < npg) mlv = *reinterpret_cast<const float2*>(part_ml + (base + lane) * 2);
-            M = warp_max(mlv.x);
-#pragma unroll 4
-            for (int p = 0; p < npg; ++p) {
-                float ov[CPL];
-#pragma unroll
-                for (int c = 0; c < CPL; ++c) ov[c] = part_o[(base + p) * DH + lane * CPL + c];
-                const float mp = __shfl_sync(0xffffffffu, mlv.x, p), lp = __shfl_sync(0xffffffffu, mlv.y, p);
-                const float a = lp == 0.f ? 0.f : expf(mp - M);
-                L += lp * a;
-#pragma unroll
-                for (int c = 0; c < CPL; ++c) o[hh][c] += ov[c] * a;
-            }
-        } else {
-            for (int p = lane; p < npg; p += 32) M = fmaxf(M, part_ml[(base + p) * 2]);
-            M = warp_max(M);
-            // branch-free so the loads of consecutive pages overlap; an empty page (l = 0,
-            // o = 0, m = -1e30) contributes exactly 0, as a skipped iteration would
-#pragma unroll 4
-            for (int p = 0; p < npg; ++p) {
-                const float2 mlp = *reinterpret_cast<const float2*>(part_ml + (base + p) * 2);
-                float ov[CPL];
-#pragma unroll
-                for (int c = 0; c < CPL; ++c) ov[c] = part_o[(base + p) * DH + lane * CPL + c];
-                const float a = mlp.y == 0.f ? 0.f : expf(mlp.x - M);
-                L += mlp.y * a;
-#pragma unroll
-                for (int c = 0; c < CPL; ++c) o[hh][c] += ov[c] * a;
-            }
-        }
-        const float il = 1.f / L;
-#pragma unroll
-        for (int c = 0; c < CPL; ++c) {
-            o[hh][c] *= il;
-            mx = fmax(mx, fabs((double)o[hh][c]));
-            if (out) out[(size_t)b * ldo + h * DH + lane * CPL + c] = o[hh][c];
-        }
-    }
-    if (!codes) return;
-    double s;
-    if (mode == 0) {
-        s = static_scale;
-    } else {
-        mx = block_max1(mx, red);
-        s = q_scale(mx, qmax);
-    }
-    const double inv_s = 1.0 / s;
-#pragma unroll
-    for (int hh = 0; hh < HPW; ++hh) {
-        const int h = warp + 32 * hh;
-        if (h >= H) continue;
-        int c[CPL];
-#pragma unroll
-        for (int e = 0; e < CPL; ++e) c[e] = q_code_r((double)o[hh][e], s, inv_s, qmax);
-        const int k0 = h * DH + lane * CPL;
-        if (CPL == 4) {
-            *reinterpret_cast<uint16_t*>(codes + w4t_offset(b, k0 / 2, ld_codes)) =
-                (uint16_t)((c[0] & 0xF) | ((c[1] & 0xF) << 4) | ((c[2] & 0xF) << 8) | ((c[3] & 0xF) << 12));
-        } else {
-            codes[w4t_offset(b, k0 / 2, ld_codes)] = (uint8_t)((c[0] & 0xF) | ((c[1] & 0xF) << 4));
-        }
-    }
-    // zero the K padding of this row
-    for (int k = H * DH + threadIdx.x * 2; k < d_pad; k += blockDim.x * 2) codes[w4t_offset(b, k / 2, ld_codes)] = 0;
-    if (threadIdx.x == 0) scales[b] = s;
-}
-
 }  // namespace qt
 
 using namespace qt;
@@ -1071,47 +437,6 @@ int qt_launch_attn_colsum(const float* qkv, int ldq, int H, int Hkv, int dh, con
     else
         return -1;
     return (int)cudaGetLastError();
-}
-
-int qt_launch_attn_decode(const float* qkv, int ldq, int H, int Hkv, int dh, const int* kv_len, int len_add, int B,
-                          uint8_t* pool, long long page_bytes, const int* pt, int max_pages, int n_pages,
-                          float* part_ml, float* part_o, float* out, int ldo, uint8_t* codes, int ld_codes,
-                          double* scales, int qmode, double static_scale, int d_pad, int bits, const double* rope,
-                          const int* pos, unsigned* counters, float* row, float* hmax, cudaStream_t st) {
-    const double2* rt = reinterpret_cast<const double2*>(rope);
-    if (counters && (!row || !hmax || !codes || (H * dh) % 8)) return -1;
-    if (B <= 0) return 0;
-    if (H > 64) return -1;
-    // two 64-row pages per CTA (unfused path, dh = 128): half the CTAs, half the partials
-    const int ppc = !rope && !counters && dh == 128 ? 2 : 1;
-    const bool pp2 = ppc > 1;
-    if (pp2) n_pages = (n_pages + ppc - 1) / ppc;
-    const dim3 grid(n_pages, H, B);
-    const float inv_sqrt = (float)(1.0 / sqrt((double)dh));
-    const int qmax = (1 << (bits - 1)) - 1;
-    int rc;
-    if (dh == 128) {
-        rc = pp2 ? launch_pdl(k_attn_decode_pp2<128, 2>, grid, dim3(128), 0, st, qkv, ldq, H, Hkv, kv_len, len_add, pool,
-                              page_bytes, pt, max_pages, inv_sqrt, part_ml, part_o, rt, pos, counters, row, hmax,
-                              codes, ld_codes, scales, qmode, static_scale, d_pad, qmax)
-                 : launch_pdl(k_attn_decode<128>, grid, dim3(128), 0, st, qkv, ldq, H, Hkv, kv_len, len_add, pool,
-                              page_bytes, pt, max_pages, inv_sqrt, part_ml, part_o, rt, pos, counters, row, hmax,
-                              codes, ld_codes, scales, qmode, static_scale, d_pad, qmax);
-        if (rc || counters) return rc;  // counters: merged + quantized by the last arrivals
-        auto mk = H > 32 ? k_attn_merge_quant<128, 64> : k_attn_merge_quant<128, 32>;
-        return launch_pdl(mk, dim3(B), dim3(1024), 0, st, (const float*)part_ml, (const float*)part_o, n_pages, H, out,
-                          ldo, codes, ld_codes, scales, qmode, static_scale, d_pad, qmax);
-    }
-    if (dh == 64) {
-        rc = launch_pdl(k_attn_decode<64>, grid, dim3(128), 0, st, qkv, ldq, H, Hkv, kv_len, len_add, pool,
-                        page_bytes, pt, max_pages, inv_sqrt, part_ml, part_o, rt, pos, counters, row, hmax, codes,
-                        ld_codes, scales, qmode, static_scale, d_pad, qmax);
-        if (rc || counters) return rc;  // counters: merged + quantized by the last arrivals
-        auto mk = H > 32 ? k_attn_merge_quant<64, 64> : k_attn_merge_quant<64, 32>;
-        return launch_pdl(mk, dim3(B), dim3(1024), 0, st, (const float*)part_ml, (const float*)part_o, n_pages, H, out,
-                          ldo, codes, ld_codes, scales, qmode, static_scale, d_pad, qmax);
-    }
-    return -1;
 }
 
 }  // extern "C"

@@ -75,15 +75,17 @@ int qt_launch_attn_colsum(const float* qkv, int ldq, int H, int Hkv, int dh, con
                           const int* seq_len, int B, int vmax, const uint8_t* pool, long long page_bytes,
                           const int* pt, int max_pages, const float* ml, int vstride, float* inter, float* intra,
                           cudaStream_t st);
-// rope/pos non-null: RoPE of q and the new token's K/V append fused in (decode step)
-// counters (B*H + B, zeroed once): merge + attn_out quantization by the last arrivals in the
-// same launch (row: fp32 [B x H*dh] scratch, hmax: [B*H]); null: separate merge launch
-int qt_launch_attn_decode(const float* qkv, int ldq, int H, int Hkv, int dh, const int* kv_len, int len_add, int B,
-                          uint8_t* pool, long long page_bytes, const int* pt, int max_pages, int n_pages,
-                          float* part_ml, float* part_o, float* out, int ldo, uint8_t* codes, int ld_codes,
-                          double* scales, int qmode, double static_scale, int d_pad, int bits, const double* rope,
-                          const int* pos, unsigned* counters, float* row, float* hmax,
-                          cudaStream_t st);
+// K6 decode attention (k_attn_decode.cu): grid (nsplit, Hkv, B), pps pages of 64 rows per
+// split (qt_attn_decode_plan); rope/pos non-null: the decode step -- q/k RoPE and the new
+// token's K/V quantize + append at row kv_len[b] fused in, attention over kv_len[b] + 1
+// rows; null: q post-RoPE, kv_len[b] rows.  Then the split merge (fixed order) writing the
+// fp32 rows to out (nullable) and/or the attn_out site codes (codes non-null).
+int qt_attn_decode_plan(int B, int Hkv, int pages, int sms, int* pps, int* nsplit);
+int qt_launch_attn_decode(const float* qkv, int ldq, int H, int Hkv, int dh, const int* kv_len, int B,
+                          uint8_t* pool, long long page_bytes, const int* pt, int max_pages, int pps, int nsplit,
+                          const double* rope, const int* pos, float* part_ml, float* part_o, float* out, int ldo,
+                          uint8_t* codes, int ld_codes, double* scales, int qmode, double static_scale, int d_pad,
+                          int bits, cudaStream_t st);
 int qt_launch_select_topk(const double* mag, const double* res, const float* inter, const float* intra, int H,
                           int vstride, const int* vis, const int* txt, const int* budget, const int* old_off,
                           const int* new_off, int B, int vmax, const double* w4, int* keep_src, int* keep_local,

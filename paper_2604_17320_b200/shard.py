@@ -38,6 +38,16 @@ def gather_rows(local: torch.Tensor, group=None):
     return torch.cat([p[:c] for p, c in zip(parts, counts)], dim=0)
 
 
+def gather_equal_rows(local: torch.Tensor, out: torch.Tensor, group=None):
+    """Every rank's [n x ...] rows (the same n on every rank -- the weak-scaling bench shards
+    an equal per-GPU batch) into out [world * n x ...] in rank order, with one
+    all_gather_into_tensor and no host synchronisation (it can sit inside a timed region
+    and a CUDA stream's order)."""
+    import torch.distributed as dist
+    dist.all_gather_into_tensor(out, local.contiguous(), group=group)
+    return out
+
+
 def max_over_ranks(value: float, device="cpu", group=None) -> float:
     """The job's time is the slowest rank's (bench.py contract)."""
     import torch.distributed as dist
