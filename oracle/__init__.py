@@ -346,6 +346,8 @@ def port_lib():
         lib.qo_run_rec.argtypes = [C.c_void_p, C.c_int, _ip, _i8p, _dp]
         lib.qo_run_clear_recs.argtypes = [C.c_void_p]
         lib.qo_run_clear_recs.restype = None
+        lib.qo_run_n_applied.argtypes = [C.c_void_p]
+        lib.qo_run_applied.argtypes = [C.c_void_p, u64p, _i8p, _dp]
         lib.qo_run_n_ties.argtypes = [C.c_void_p]
         lib.qo_run_ties.argtypes = [C.c_void_p, u64p, _i8p, _dp]
         _port_lib = lib
@@ -778,6 +780,17 @@ class PortRun:
         r = np.empty(n, dtype=np.float64)
         if n:
             self.lib.qo_run_ties(self.h, k.ctypes.data_as(C.POINTER(C.c_uint64)), _b(c), _d(r))
+        return k, c, r
+
+    def applied(self):
+        """Overrides that changed one of this run's decisions: (keys, the restatement's own
+        codes, their tie ratios)."""
+        n = self.lib.qo_run_n_applied(self.h)
+        k = np.empty(n, dtype=np.uint64)
+        c = np.empty(n, dtype=np.int8)
+        r = np.empty(n, dtype=np.float64)
+        if n:
+            self.lib.qo_run_applied(self.h, k.ctypes.data_as(C.POINTER(C.c_uint64)), _b(c), _d(r))
         return k, c, r
 
     def clear_records(self):

@@ -85,7 +85,9 @@ double scale_of(double max_abs, int bits) {
 thread_local double g_tie_margin = 1e300;
 thread_local bool g_track = false;
 thread_local double g_site_tol = 0.0;  // 0 = decision not tracked
-constexpr double kTolResidual = 1e-9, kTolAttn = 1e-4, kTolFp32 = 1e-5;
+// Residual-derived sites inherit the fp32 rounding of upstream site scales through the
+// int32-exact GEMMs (~1e-9 relative after a layer), hence 1e-6 code units, not fp64 ulps.
+constexpr double kTolResidual = 1e-6, kTolAttn = 1e-4, kTolFp32 = 1e-5;
 
 // Decision identity for the forced-replay parity tests (tests/replay.py): every
 // activation / KV quantization decision of a run has a key (phase = 0 prefill, 1 + t
@@ -109,6 +111,7 @@ struct DecRec {  // the codes and scales of one quantizer site
 struct DecCtx {
     bool record = false;
     std::vector<Decision> ties;
+    std::vector<Decision> applied;  // overrides that changed a decision: key, the natural code, ratio
     std::vector<DecRec> recs;
     std::unordered_map<uint64_t, int8_t> over;
 };
@@ -139,7 +142,10 @@ int8_t code_of(double x, double s, int bits) {
         if (ratio < 1.0) g_ctx->ties.push_back({key, c, ratio});
         if (!g_ctx->over.empty()) {
             auto it = g_ctx->over.find(key);
-            if (it != g_ctx->over.end()) c = it->second;
+            if (it != g_ctx->over.end() && it->second != c) {
+                g_ctx->applied.push_back({key, c, ratio});
+                c = it->second;
+            }
         }
     }
     return c;
@@ -1122,6 +1128,18 @@ void qo_run_clear_recs(void* r) {
     run->dec.recs.clear();
     run->dec.recs.shrink_to_fit();
     run->dec.ties.clear();
+    run->dec.applied.clear();
+}
+// overrides that changed a decision in this run: key, the restatement's own code, its tie ratio
+int qo_run_n_applied(void* r) { return static_cast<int>(static_cast<Run*>(r)->dec.applied.size()); }
+int qo_run_applied(void* r, uint64_t* keys, int8_t* codes, double* ratios) {
+    const auto& t = static_cast<Run*>(r)->dec.applied;
+    for (size_t i = 0; i < t.size(); ++i) {
+        keys[i] = t[i].key;
+        codes[i] = t[i].code;
+        ratios[i] = t[i].ratio;
+    }
+    return 0;
 }
 // decisions within the GPU error budget of a rounding tie: key, the restatement's code, ratio
 int qo_run_n_ties(void* r) { return static_cast<int>(static_cast<Run*>(r)->dec.ties.size()); }

@@ -12,10 +12,14 @@ comparable:
    decode steps;
 2. the restatement runs the same sequences, recording its codes and listing each decision
    within the GPU error budget of a tie (`ties`, keyed by (phase, layer, site, row, col));
-3. every GPU code must equal the restatement's, except at listed ties -- a difference
-   anywhere else is a genuine mismatch and fails;
-4. at the listed ties where the GPU rounded the other way, the restatement is re-run told
-   to take the GPU's code (`overrides`), and 2-4 repeat until no differences remain.
+3. sites are visited in execution order; at the first site where any code differs every
+   difference must be a listed tie (upstream of it everything agreed, so anything else is
+   a genuine mismatch and fails); listed differences anywhere are recorded as overrides
+   -- the restatement is re-run told to take the GPU's code there -- and 2-3 repeat until
+   no differences remain (later-site differences may be consequences of earlier flips);
+4. at convergence, every override that actually changed one of the restatement's own
+   decisions must be a listed tie of that final run (a forced non-tie would be a hidden
+   mismatch).
 
 After convergence every int4 decision (including all KV-cache codes) is identical, the
 retained token sets must match exactly, and logits are compared at north_star's 1e-2
@@ -26,9 +30,12 @@ import threading
 import numpy as np
 
 SITES = {0: "attn_in", 1: "attn_out", 2: "mlp_in", 3: "mlp_mid", 4: "head_in", 5: "K", 6: "V"}
-# scale agreement after convergence: residual-derived sites are fp64 end to end, the
-# fp32-buffered sites (attention output, MLP hidden, K/V) carry fp32 rounding
-SCALE_RTOL = {0: 1e-12, 2: 1e-12, 4: 1e-12, 1: 1e-5, 3: 1e-5, 5: 1e-6, 6: 1e-6}
+# scale agreement after convergence: the fp32-buffered sites (attention output, MLP hidden,
+# K/V) carry fp32 rounding; residual-derived sites inherit it through the upstream scales
+SCALE_RTOL = {0: 1e-6, 2: 1e-6, 4: 1e-6, 1: 1e-5, 3: 1e-5, 5: 1e-6, 6: 1e-6}
+# execution order of the sites within a layer: attn_in, K, V, attn_out, mlp_in, mlp_mid
+# (head_in has layer = n_layers, after every layer)
+ORDER = {0: 0, 5: 1, 6: 2, 1: 3, 2: 4, 3: 5, 4: 6}
 
 
 def dec_key(phase, layer, site, row, col):
@@ -63,12 +70,13 @@ def _split_gpu(gpu_recs, port_recs_per_seq):
 
 
 def compare_decisions(gpu_by_key, port_by_key, tie_keys):
-    """Codes equal except at listed ties.  Returns {key: gpu code} to force, and a summary."""
-    force, summary = {}, []
+    """Returns ({key: gpu code} for every listed difference, summary); raises Mismatch on a
+    non-listed difference at the first differing site in execution order."""
+    force, summary, first = {}, [], None
     if set(gpu_by_key) != set(port_by_key):
         raise Mismatch(f"site sets differ: {sorted(set(gpu_by_key) ^ set(port_by_key))[:5]}")
-    for k, g in gpu_by_key.items():
-        p = port_by_key[k]
+    for k in sorted(gpu_by_key, key=lambda k: (k[0], k[1], ORDER[k[2]])):
+        g, p = gpu_by_key[k], port_by_key[k]
         if g["codes"].shape != p["codes"].shape:
             raise Mismatch(f"shape mismatch at {k}: {g['codes'].shape} vs {p['codes'].shape}")
         rr, cc = np.nonzero(g["codes"] != p["codes"])
@@ -76,14 +84,18 @@ def compare_decisions(gpu_by_key, port_by_key, tie_keys):
             continue
         keys = dec_key(k[0], k[1], k[2], rr, cc)
         listed = np.isin(keys, tie_keys)
-        if not listed.all():
-            bad = np.nonzero(~listed)[0][:5]
-            raise Mismatch(f"{(~listed).sum()} code(s) differ outside the tie list at {SITES[k[2]]} phase {k[0]} "
-                           f"layer {k[1]}: (row, col, gpu, ref) = "
-                           f"{[(int(rr[i]), int(cc[i]), int(g['codes'][rr[i], cc[i]]), int(p['codes'][rr[i], cc[i]])) for i in bad]}")
-        for kk, r, c in zip(keys, rr, cc):
-            force[int(kk)] = int(g["codes"][r, c])
-        summary.append((SITES[k[2]], k[0], k[1], int(rr.size)))
+        if first is None:
+            first = k
+            if not listed.all():
+                bad = np.nonzero(~listed)[0][:5]
+                raise Mismatch(
+                    f"{(~listed).sum()} code(s) differ outside the tie list at {SITES[k[2]]} phase {k[0]} "
+                    f"layer {k[1]} (the first differing site): (row, col, gpu, ref) = "
+                    f"{[(int(rr[i]), int(cc[i]), int(g['codes'][rr[i], cc[i]]), int(p['codes'][rr[i], cc[i]])) for i in bad]}")
+        for kk, r, c, ok in zip(keys, rr, cc, listed):
+            if ok:
+                force[int(kk)] = int(g["codes"][r, c])
+        summary.append((SITES[k[2]], k[0], k[1], int(rr.size), int(listed.sum())))
     return force, summary
 
 
@@ -110,7 +122,8 @@ def run_port_seqs(port, seqs, recipe_for, dec_embs, overrides, threads=True):
                 lg.append(r.decode(de))
             recs = {(x["phase"], x["layer"], x["site"]): x for x in r.records()}
             tk, _, _ = r.ties()
-            res[b] = dict(run=r, logits=lg, recs=recs, ties=np.unique(tk))
+            ak, _, ar = r.applied()
+            res[b] = dict(run=r, logits=lg, recs=recs, ties=np.unique(tk), applied=(ak, ar))
             r.clear_records()
         except Exception as e:  # noqa: BLE001 - re-raised below
             errs.append(e)
@@ -127,7 +140,7 @@ def run_port_seqs(port, seqs, recipe_for, dec_embs, overrides, threads=True):
     return res
 
 
-def forced_replay(port, gpu_recs, seqs, recipe_for, dec_embs, max_iter=6, log=print):
+def forced_replay(port, gpu_recs, seqs, recipe_for, dec_embs, max_iter=10, log=print):
     """Iterate restatement runs until every GPU decision is reproduced.  Returns the final
     restatement results and the overrides per sequence."""
     overrides = [dict() for _ in seqs]
@@ -144,6 +157,10 @@ def forced_replay(port, gpu_recs, seqs, recipe_for, dec_embs, max_iter=6, log=pr
         if not changed:
             for b, r in enumerate(res):
                 check_scales(split[b], r["recs"])
+                ak, ar = r["applied"]
+                if ak.size and not np.all(ar < 1.0):
+                    raise Mismatch(f"seq {b}: {int((ar >= 1.0).sum())} override(s) changed a decision that is not "
+                                   f"within the GPU error budget of a tie (ratios {np.sort(ar)[-5:]})")
             log(f"replay converged after {it} iteration(s); forced per seq: {[len(o) for o in overrides]}; "
                 f"tie candidates per seq: {[int(r['ties'].size) for r in res]}")
             return res, overrides

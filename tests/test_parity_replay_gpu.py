@@ -54,11 +54,11 @@ def _run(cfg, w, acts, rec, seqs, n_decode, dec_seed, ref=None):
     lg = e.prefill(np.concatenate([s[0] for s in seqs]).astype(np.float32), [s[1] for s in seqs],
                    [s[2] for s in seqs], v0=[s[3] for s in seqs])
     lg = lg.copy()
-    layouts = [e.layout(b) for b in range(B)]
     traces = [e.trace(b) for b in range(B)]
     dec = [[O.synth_embeddings(1, cfg.d_model, seed=dec_seed + 100 * b + t)[0] for t in range(n_decode)]
            for b in range(B)]
     dlg = [e.decode(np.stack([dec[b][t] for b in range(B)]).astype(np.float32)).copy() for t in range(n_decode)]
+    layouts = [e.layout(b) for b in range(B)]  # after the decode steps, like the restatement's
     gpu_recs = e.captured()
     e.close()
 
@@ -74,7 +74,7 @@ def _run(cfg, w, acts, rec, seqs, n_decode, dec_seed, ref=None):
             assert np.array_equal(p1, p2), ("retained set differs", b)
         v, t, pos = layouts[b]
         assert (v, t) == (rr.visual, rr.text) and np.array_equal(pos, rr.positions)
-        n = v + t
+        n = rr.logits.shape[0]  # the prefill's final rows
         worst = max(worst, float(np.abs(lg[off:off + n].astype(np.float64) - rr.logits).max()))
         off += n
         for s in range(n_decode):
