@@ -205,6 +205,33 @@ int qt_engine_profile_read(qt_engine* e, double* out24);
  * (launch overheads and PDL overlap as in the real step).  Cache lengths and
  * positions are restored, so decoding continues unaffected. */
 int qt_engine_profile_chain(qt_engine* e, int skip_mask, int reps, double* ms_per_step);
+/* ForwardResult::records / block_outputs and arbitrary prune hooks for reference-API
+ * callers (model.hpp:74-80,155-156,164-171; model.cpp:380-406,439), one sequence per
+ * prefill (B = 1).  qt_engine_set_records(mode): bit 1 keeps every layer's post-block
+ * hidden states (qt_engine_block_output), bit 2 every layer's LayerActivationRecord
+ * (qt_engine_record_get): the post-attention-residual states of the visual and text rows
+ * (fp64) and the softmax probabilities of every query over the visual keys per head
+ * (fp32 on the device) -- attn_inter / attn_intra are its text / visual query rows.
+ * qt_engine_set_prune_hook: the engine calls hook(user, record, slots, n, budget) at every
+ * layer after the attention residual, as forward_prefill calls a PruneHook; return 1 with
+ * the retained visual slots (ascending, unique: apply_pruning's rules, violations fail with
+ * its messages) to prune on the device, 0 for no retained set (std::nullopt), < 0 to fail.
+ * Exclusive with a device recipe (qt_engine_set_recipe).  Both modes synchronise per layer. */
+typedef struct qt_layer_record {
+    int layer, visual, text, d_model, n_heads;
+    const int* positions;         /* [visual + text] original position ids */
+    const double* visual_states;  /* [visual x d_model] */
+    const double* text_states;    /* [text x d_model] */
+    const float* probs;           /* [n_heads x (visual + text) x visual] */
+} qt_layer_record;
+typedef int (*qt_prune_hook_fn)(void* user, const qt_layer_record* rec, int* slots, int* n_slots, int* budget);
+int qt_engine_set_records(qt_engine* e, int mode);
+int qt_engine_set_prune_hook(qt_engine* e, qt_prune_hook_fn hook, void* user);
+/* records of the last prefill: meta4 = {layer, visual, text, n_heads}; any output may be
+ * null (positions [v + t], states [(v + t) x d_model], probs [n_heads x (v + t) x v]) */
+int qt_engine_record_count(qt_engine* e);
+int qt_engine_record_get(qt_engine* e, int i, int* meta4, int* positions, double* states, float* probs);
+int qt_engine_block_output(qt_engine* e, int layer, double* out, long long cap, int* rows);
 /* Decision capture (parity / debugging only; never on the product path): with on != 0
  * the following prefill / decode calls read back, after every quantizer site, the int4
  * codes and scales it produced (synchronously; decode steps then run eagerly instead of

@@ -288,6 +288,21 @@ struct qt_engine {
     // full-precision calibration forward (k_fp.cu)
     bool keep_fp = false;
     std::vector<std::vector<double>>* rec_blocks = nullptr;  // block outputs of the next prefill (B = 1)
+    // ForwardResult::records / block_outputs (model.cpp:382-402,439) and arbitrary host prune
+    // hooks (model.cpp:404-405) for reference-API callers: B = 1, synchronous read-backs
+    int rec_mode = 0;  // bit 1: block outputs, bit 2: layer records
+    qt_prune_hook_fn host_hook = nullptr;
+    void* host_user = nullptr;
+    struct LayerRec {
+        int layer, V, T;
+        std::vector<int> pos;
+        std::vector<double> states;  // [(V + T) x d]
+        std::vector<float> probs;    // [H x (V + T) x V]
+    };
+    std::vector<LayerRec> lrecs;
+    std::vector<std::vector<double>> blocks;
+    float* probs_d = nullptr;
+    size_t probs_cap = 0;
     // QUOTA diagnostics of the next prefill (B = 1, calibration only): per layer the text
     // queries' top-10 visual attention mass [H x T] and the visual-state cosine Gram [V x V]
     struct DiagRec {
@@ -352,7 +367,7 @@ struct qt_engine {
             for (double* p : fl.w) f(p);
         f(fp_head);
         if (blas) cublasDestroy(blas);
-        f(splitk_ws); f(codes8); f(head8); f(pmax); f(gmax);
+        f(splitk_ws); f(codes8); f(head8); f(pmax); f(gmax); f(probs_d);
         if (pin) cudaFreeHost(pin);
         if (cst) {
             cudaStreamSynchronize(cst);
@@ -1153,6 +1168,12 @@ struct qt_engine {
             if (have_recipe && v0v[b] < 1) fail(QT_EINVAL, "v0 must be >= 1");
         }
         if (total > max_tokens) fail(QT_EINVAL, "batch tokens exceed engine capacity");
+        const bool want_rec = (rec_mode & 2) || host_hook;
+        if ((want_rec || (rec_mode & 1)) && B != 1)
+            fail(QT_EINVAL, "layer records, block outputs and host prune hooks need a batch of one sequence");
+        if (host_hook && have_recipe) fail(QT_EINVAL, "a host prune hook and a device recipe are exclusive");
+        lrecs.clear();
+        blocks.clear();
         // positions: strictly increasing per sequence (model.cpp:64-68)
         std::vector<int> hpos(total);
         {
@@ -1257,6 +1278,7 @@ struct qt_engine {
                 o += S;
             }
         }
+        std::vector<int> cur_pos0 = pos_host[0];  // sequence 0's current layout (records / host hooks)
 
         for (int l = 0; l < L; ++l) {
             const LayerW& w = lw[l];
@@ -1286,7 +1308,8 @@ struct qt_engine {
 
             pb(P_ATTN);
             ckl(qt_launch_attn_prefill(qkv, n_qkv, H, Hkv, dh, seq_off, seq_vis, seq_len, B, smax, pool, page_bytes,
-                                       ptl, max_pages, attn, d, prune_any ? ml : nullptr, pmax, kPmaxLd, st),
+                                       ptl, max_pages, attn, d, (prune_any || want_rec) ? ml : nullptr, pmax, kPmaxLd,
+                                       st),
                 "prefill attention");
             {  // mask-allowed (query, key) pairs x 4 dh flops per head
                 double pairs = 0;
@@ -1303,14 +1326,103 @@ struct qt_engine {
             cap_site(l, 1, M, d, kd_pad);
             gemm(QT_EPI_RESADD, w.o, nd_pad, w.s_o, M, d, kd_pad, xc, d, false, w.o8);
             if (rec_diag) diag_layer(l, ptl, cur_v[0], h_txt[0], xc);
+            // LayerActivationRecord (model.cpp:382-402) + a host prune hook (model.cpp:404-427)
+            std::vector<int> host_slots;
+            bool host_prune = false;
+            int host_budget = 0;
+            if (want_rec) {
+                const int V = cur_v[0], T = h_txt[0], S = V + T;
+                LayerRec r{l, V, T, cur_pos0, std::vector<double>((size_t)S * d),
+                           std::vector<float>((size_t)H * S * V)};
+                if (V > 0) {
+                    if (r.probs.size() > probs_cap) {
+                        ck(cudaStreamSynchronize(st), "sync");
+                        if (probs_d) cudaFree(probs_d);
+                        probs_d = dalloc<float>(r.probs.size());
+                        probs_cap = r.probs.size();
+                    }
+                    ckl(qt_launch_attn_colsum(qkv, n_qkv, H, Hkv, dh, seq_off, seq_vis, seq_len, 1, V, pool, page_bytes,
+                                              ptl, max_pages, ml, vstride, inter, intra, probs_d, S, V, st),
+                        "record attention probabilities");
+                    ck(cudaMemcpyAsync(r.probs.data(), probs_d, r.probs.size() * sizeof(float),
+                                       cudaMemcpyDeviceToHost, st),
+                       "record probabilities");
+                }
+                ck(cudaMemcpyAsync(r.states.data(), xc, r.states.size() * sizeof(double), cudaMemcpyDeviceToHost, st),
+                   "record states");
+                ck(cudaStreamSynchronize(st), "record");
+                if (host_hook) {
+                    qt_layer_record rec{l, V, T, d, H, r.pos.data(), r.states.data(), r.states.data() + (size_t)V * d,
+                                        r.probs.data()};
+                    std::vector<int> slots(std::max(V, 1));
+                    int n = 0;
+                    const int rc = host_hook(host_user, &rec, slots.data(), &n, &host_budget);
+                    if (rc < 0) fail(QT_ERUNTIME, "prune hook failed");
+                    if (rc == 1) {  // apply_pruning's validation (selector.cpp:140-148)
+                        if (n < 1) fail(QT_ERUNTIME, "pruning would remove every visual token");
+                        if (n > V) fail(QT_ERUNTIME, "pruning text or out-of-range token");
+                        int prev = -1;
+                        for (int i = 0; i < n; ++i) {
+                            if (slots[i] <= prev) fail(QT_ERUNTIME, "retained slots must be ascending and unique");
+                            if (slots[i] < 0 || slots[i] >= V) fail(QT_ERUNTIME, "pruning text or out-of-range token");
+                            prev = slots[i];
+                        }
+                        if (n < V) {  // retain-all is a strict no-op (selector.cpp:153-154)
+                            host_prune = true;
+                            host_slots.assign(slots.begin(), slots.begin() + n);
+                        }
+                    }
+                }
+                if (rec_mode & 2) lrecs.push_back(std::move(r));
+            }
             for (int b = 0; b < B; ++b) h_kvlen[(size_t)l * B + b] = cur_v[b] + h_txt[b];
 
+            if (host_prune) {  // the host hook's retained set: the device gather + KV filter
+                const int V = cur_v[0], T = h_txt[0], nv = (int)host_slots.size();
+                std::vector<int> ksrc, kloc((size_t)max_batch * vstride, 0), kp((size_t)max_batch * vstride, 0);
+                for (int j = 0; j < nv; ++j) {
+                    ksrc.push_back(host_slots[j]);
+                    kloc[j] = host_slots[j];
+                    kp[j] = cur_pos0[host_slots[j]];
+                }
+                for (int t = 0; t < T; ++t) {
+                    ksrc.push_back(V + t);
+                    kloc[nv + t] = V + t;
+                }
+                const size_t evi = trace_layers.size();
+                upload(keep_src, ksrc);
+                upload(keep_local, kloc);
+                ck(cudaMemcpyAsync(kept_pos + evi * max_batch * vstride, stage(kp.data(), kp.size()),
+                                   kp.size() * sizeof(int), cudaMemcpyHostToDevice, st),
+                   "kept positions");
+                std::vector<int> nlen{nv + T};
+                upload(new_len, nlen);
+                double* xn = x[xc == x[0] ? 1 : 0];
+                int* pn = pos[pc == pos[0] ? 1 : 0];
+                ckl(qt_launch_gather_rows(xc, xn, d, pc, pn, keep_src, nv + T, st), "compaction gather");
+                ckl(qt_launch_kv_compact(pool, page_bytes, ptl, max_pages, Hkv, dh, keep_local, vstride, new_len, 1, st),
+                    "kv compaction");
+                kbud[0][l] = host_budget;
+                trace_layers.push_back(l);
+                ev_prev_v.push_back(cur_v);
+                ev_new_v.push_back({nv});
+                h_kvlen[(size_t)l * B] = nv + T;
+                std::vector<int> npos;
+                for (int j = 0; j < nv; ++j) npos.push_back(cur_pos0[host_slots[j]]);
+                npos.insert(npos.end(), cur_pos0.begin() + V, cur_pos0.end());
+                cur_pos0 = std::move(npos);
+                cur_v[0] = nv;
+                xc = xn;
+                pc = pn;
+                off = upload_layout();
+                M = off[B];
+            }
             // recipe hook at candidate layers (selector.cpp:214-227, model.cpp:404-427)
             if (cand && prune_any) {
                 if (vmax > vstride) fail(QT_EINVAL, "visual prefix exceeds engine capacity");
                 pb(P_SELECT);
                 ckl(qt_launch_attn_colsum(qkv, n_qkv, H, Hkv, dh, seq_off, seq_vis, seq_len, B, vmax, pool, page_bytes,
-                                          ptl, max_pages, ml, vstride, inter, intra, st),
+                                          ptl, max_pages, ml, vstride, inter, intra, nullptr, 0, 0, st),
                     "quota attention metrics");
                 ckl(qt_launch_token_metrics(xc, d, seq_off, seq_vis, vmax, B, vstride, recipe.res_bits, mag, res, st),
                     "quota token metrics");
@@ -1339,6 +1451,13 @@ struct qt_engine {
                 ckl(qt_launch_kv_compact(pool, page_bytes, ptl, max_pages, Hkv, dh, keep_local, vstride, new_len, B, st),
                     "kv compaction");
                 pe((double)M * d * 8 * 2);
+                if (want_rec) {  // sequence 0's new layout, for the next layers' records
+                    std::vector<int> kp0(nv[0]);
+                    ck(cudaMemcpyAsync(kp0.data(), kp_ev, nv[0] * sizeof(int), cudaMemcpyDeviceToHost, st), "kept");
+                    ck(cudaStreamSynchronize(st), "kept");
+                    kp0.insert(kp0.end(), cur_pos0.begin() + cur_v[0], cur_pos0.end());
+                    cur_pos0 = std::move(kp0);
+                }
                 // trace: kept visual positions, read back once after the prefill
                 trace_layers.push_back(l);
                 ev_prev_v.push_back(cur_v);
@@ -1360,6 +1479,12 @@ struct qt_engine {
             norm_quant(mid, 0, dff, nullptr, M, dff, kff_pad, 4 * l + 3, true);
             cap_site(l, 3, M, dff, kff_pad);
             gemm(QT_EPI_RESADD, w.down, nd_pad, w.s_down, M, d, kff_pad, xc, d, false, w.down8);
+            if (rec_mode & 1) {  // ForwardResult::block_outputs (model.cpp:439)
+                blocks.resize(L);
+                blocks[l].resize((size_t)M * d);
+                ck(cudaMemcpyAsync(blocks[l].data(), xc, (size_t)M * d * sizeof(double), cudaMemcpyDeviceToHost, st),
+                   "block output");
+            }
             if (rec_blocks) {  // ForwardResult::block_outputs (model.cpp:439), calibration only
                 if (l == 0) rec_blocks->assign(L, {});
                 (*rec_blocks)[l].resize((size_t)M * d);
@@ -2212,6 +2337,49 @@ int qt_engine_profile_chain(qt_engine* e, int skip_mask, int reps, double* ms_pe
     });
 }
 
+int qt_engine_set_records(qt_engine* e, int mode) {
+    return guard([&] {
+        if (mode < 0 || mode > 3) fail(QT_EINVAL, "record mode must be 0..3");
+        e->rec_mode = mode;
+    });
+}
+
+int qt_engine_set_prune_hook(qt_engine* e, qt_prune_hook_fn hook, void* user) {
+    return guard([&] {
+        e->host_hook = hook;
+        e->host_user = user;
+    });
+}
+
+int qt_engine_record_count(qt_engine* e) { return (int)e->lrecs.size(); }
+
+int qt_engine_record_get(qt_engine* e, int i, int* meta, int* positions, double* states, float* probs) {
+    return guard([&] {
+        if (i < 0 || i >= (int)e->lrecs.size()) fail(QT_ERANGE, "record out of range");
+        const auto& r = e->lrecs[i];
+        if (meta) {
+            meta[0] = r.layer;
+            meta[1] = r.V;
+            meta[2] = r.T;
+            meta[3] = e->H;
+        }
+        if (positions) std::copy(r.pos.begin(), r.pos.end(), positions);
+        if (states) std::copy(r.states.begin(), r.states.end(), states);
+        if (probs) std::copy(r.probs.begin(), r.probs.end(), probs);
+    });
+}
+
+int qt_engine_block_output(qt_engine* e, int layer, double* out, long long cap, int* rows) {
+    return guard([&] {
+        if (layer < 0 || layer >= (int)e->blocks.size()) fail(QT_ERANGE, "no block output for this layer");
+        const auto& b = e->blocks[layer];
+        *rows = (int)(b.size() / e->d);
+        if (!out) return;
+        if ((long long)b.size() > cap) fail(QT_EINVAL, "buffer too small");
+        std::copy(b.begin(), b.end(), out);
+    });
+}
+
 int qt_engine_capture(qt_engine* e, int on) {
     return guard([&] {
         e->capture = on != 0;
@@ -2396,7 +2564,7 @@ int qt_quota_score(const double* x, int d_model, const float* q, int ldq, int B,
         double* mag = reinterpret_cast<double*>(intra + (size_t)B * H * vstride);
         double* res = mag + (size_t)B * vstride;
         ckl(qt_launch_attn_colsum(q, ldq, H, Hkv, d_head, seq_off, visual, seq_len, B, vmax, pool, page_bytes,
-                                  page_table, max_pages, row_stats, vstride, inter, intra, cs),
+                                  page_table, max_pages, row_stats, vstride, inter, intra, nullptr, 0, 0, cs),
             "quota attention metrics");
         ckl(qt_launch_token_metrics(x, d_model, seq_off, visual, vmax, B, vstride, res_bits < 0 ? 0 : res_bits, mag,
                                     res, cs),

@@ -321,7 +321,8 @@ __global__ void __launch_bounds__(128) k_attn_colsum(const float* __restrict__ q
                                                      const uint8_t* __restrict__ pool, long long page_bytes,
                                                      const int* __restrict__ pt, int max_pages, float inv_sqrt,
                                                      const float2* __restrict__ ml, int vstride,
-                                                     float* __restrict__ inter, float* __restrict__ intra) {
+                                                     float* __restrict__ inter, float* __restrict__ intra,
+                                                     float* __restrict__ probs, int p_rows, int p_ld) {
     constexpr int KLD = DH + 8;
     __shared__ __align__(16) __half Ks[AT_K * KLD];
     __shared__ float ks[AT_K], vs_unused[AT_K];
@@ -367,6 +368,9 @@ __global__ void __launch_bounds__(128) k_attn_colsum(const float* __restrict__ q
                 const float p = expf(s - mr[r]) * il[r];
                 if (isvis[r]) ca[t][c] += p;
                 else ci[t][c] += p;
+                // LayerActivationRecord blocks (model.cpp:382-384): p[h][query][visual key]
+                const int kk = k0 + t * 8 + 2 * tig + c;
+                if (probs && kk < V) probs[(((size_t)b * H + h) * p_rows + q0 + g + 8 * r) * p_ld + kk] = p;
             }
         }
     }
@@ -423,17 +427,17 @@ int qt_launch_attn_prefill(const float* qkv, int ldq, int H, int Hkv, int dh, co
 int qt_launch_attn_colsum(const float* qkv, int ldq, int H, int Hkv, int dh, const int* seq_off, const int* vis,
                           const int* seq_len, int B, int vmax, const uint8_t* pool, long long page_bytes,
                           const int* pt, int max_pages, const float* ml, int vstride, float* inter, float* intra,
-                          cudaStream_t st) {
+                          float* probs, int p_rows, int p_ld, cudaStream_t st) {
     if (B <= 0 || vmax <= 0) return 0;
     const dim3 grid((vmax + AT_K - 1) / AT_K, H, B);
     const float inv_sqrt = (float)(1.0 / sqrt((double)dh));
     const float2* m2 = reinterpret_cast<const float2*>(ml);
     if (dh == 128)
         k_attn_colsum<128><<<grid, 128, 0, st>>>(qkv, ldq, H, Hkv, seq_off, vis, seq_len, pool, page_bytes, pt,
-                                                 max_pages, inv_sqrt, m2, vstride, inter, intra);
+                                                 max_pages, inv_sqrt, m2, vstride, inter, intra, probs, p_rows, p_ld);
     else if (dh == 64)
         k_attn_colsum<64><<<grid, 128, 0, st>>>(qkv, ldq, H, Hkv, seq_off, vis, seq_len, pool, page_bytes, pt,
-                                                max_pages, inv_sqrt, m2, vstride, inter, intra);
+                                                max_pages, inv_sqrt, m2, vstride, inter, intra, probs, p_rows, p_ld);
     else
         return -1;
     return (int)cudaGetLastError();

@@ -74,7 +74,8 @@ int qt_launch_attn_prefill(const float* qkv, int ldq, int H, int Hkv, int dh, co
 int qt_launch_attn_colsum(const float* qkv, int ldq, int H, int Hkv, int dh, const int* seq_off, const int* vis,
                           const int* seq_len, int B, int vmax, const uint8_t* pool, long long page_bytes,
                           const int* pt, int max_pages, const float* ml, int vstride, float* inter, float* intra,
-                          cudaStream_t st);
+                          float* probs, int p_rows, int p_ld, cudaStream_t st);
+// probs (nullable): the softmax probabilities p[b][h][query < p_rows][visual key < p_ld]
 // K6 decode attention (k_attn_decode.cu): grid (nsplit, Hkv, B), pps pages of 64 rows per
 // split (qt_attn_decode_plan); rope/pos non-null: the decode step -- q/k RoPE and the new
 // token's K/V quantize + append at row kv_len[b] fused in, attention over kv_len[b] + 1
