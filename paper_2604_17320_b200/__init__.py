@@ -324,7 +324,9 @@ class Engine:
 
     def prefill(self, emb, visual, text, v0=None, positions=None, logits_out=None, logits_async=False):
         """emb: packed [sum(S) x d] fp32 -- numpy / CPU (pinned) torch on the host, or a
-        CUDA torch tensor.  Returns the logits rows (numpy, or a view of logits_out)."""
+        CUDA torch tensor.  Returns the logits rows (numpy, or a view of logits_out).
+        logits_async=True (host logits_out): the rows are copied back on the engine's copy
+        stream while later calls run and are valid only after synchronize()."""
         visual, text = _i32(visual), _i32(text)
         on_dev = _on_device(emb)
         if isinstance(emb, np.ndarray):

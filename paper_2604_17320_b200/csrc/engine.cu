@@ -348,6 +348,7 @@ struct qt_engine {
     int* splitk_ws = nullptr;     // int32 split-K partials of the tcgen05 GEMM at small M
 
     ~qt_engine() {
+        if (cst) cudaStreamSynchronize(cst);  // a pending async logits readback still reads `logits`
         cudaStreamSynchronize(st ? st : 0);
         if (graph) cudaGraphExecDestroy(graph);
         auto f = [](void* p) {

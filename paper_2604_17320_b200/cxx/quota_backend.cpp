@@ -19,16 +19,25 @@
 // Semantics kept from the reference: validation order and exception types /
 // messages, budget = ceil(r * v0) with the recipe's v0, pruning of the
 // candidate layer's own KV rows, next_position = last original position + 1,
-// decode appends one text token.  Differences (documented in INTEGRATION.md):
-//   * the QuantEnv's weights must be per OUTPUT channel (GroupAxis::PerColumn;
-//     quota_b200::prepare_quant_env_per_channel builds one) -- a per-input-
-//     channel scale cannot be applied after an int32 GEMM;
-//   * only hooks made by make_recipe_hook run on the device; records and
-//     block_outputs are not materialised;
-//   * KV scales come back as fp32 values (stored fp32 on the device).
+// decode appends one text token, ForwardResult::records and block_outputs
+// filled for every layer, any PruneHook honoured.  Differences:
+//   * weights are quantized per OUTPUT channel (GroupAxis::PerColumn): this
+//     library also serves quota::prepare_quant_env (model.cpp:212-237) with that
+//     axis, so stock callers (harness.cpp:113, calibrator.cpp:260) get an env the
+//     device runs -- a per-input-channel scale cannot be applied after an int32
+//     GEMM; a hand-built PerRow env is rejected;
+//   * make_recipe_hook hooks run on the device (scoring, top-k and compaction
+//     kernels); any other hook runs on the host once per layer on the
+//     materialised record, its retained set applied on the device;
+//   * record probabilities and KV scales come back from fp32 device values.
+// Engines are cached per model / env CONTENT (a fingerprint of every weight
+// code, scale, gain and activation scale), at most QUOTA_B200_MAX_ENGINES.
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <cstdint>
+#include <exception>
+#include <list>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -105,10 +114,11 @@ int env_int(const char* name, int dflt) {
     return v && *v ? std::atoi(v) : dflt;
 }
 
-// One device engine per (Model, QuantEnv) pair; one live prefill session per
+// One device engine per (Model, QuantEnv) content; one live prefill session per
 // engine (a new prefill invalidates the caches of earlier ones).
 struct Device {
     qt_engine* e = nullptr;
+    uint64_t fingerprint = 0;
     int max_tokens = 0, max_decode = 0;
     long long session = 0;  // id of the prefill whose KV the engine holds
     int steps = 0;
@@ -123,7 +133,7 @@ struct SessionRef {
 };
 
 std::mutex g_mu;
-std::map<std::pair<const Model*, const QuantEnv*>, std::unique_ptr<Device>> g_devices;
+std::list<std::unique_ptr<Device>> g_devices;  // most recently used first
 std::map<const int*, SessionRef> g_sessions;  // keyed by cache.layout.position_ids.data()
 long long g_next_session = 1;
 
@@ -138,8 +148,8 @@ void check_env(const Model& model, const QuantEnv& env) {
     auto chk = [&](const QuantizedWeight& w) {
         if (w.codes.params.axis != GroupAxis::PerColumn)
             throw std::invalid_argument(
-                "quota_b200: weights must be quantized per output channel (GroupAxis::PerColumn); "
-                "use quota_b200::prepare_quant_env_per_channel");
+                "quota_b200: weights must be quantized per output channel (GroupAxis::PerColumn), as this "
+                "library's quota::prepare_quant_env does");
         if (w.codes.params.bits != 4) throw std::invalid_argument("quota_b200: weights must be 4-bit");
     };
     for (const auto& l : env.layers) {
@@ -148,14 +158,82 @@ void check_env(const Model& model, const QuantEnv& env) {
     chk(env.w_head);
 }
 
+// 64-bit content hash, 8 bytes per step (FNV-1a style multiply on words)
+struct Fingerprint {
+    uint64_t h = 0xcbf29ce484222325ULL;
+    void bytes(const void* p, size_t n) {
+        const unsigned char* c = static_cast<const unsigned char*>(p);
+        size_t i = 0;
+        for (; i + 8 <= n; i += 8) {
+            uint64_t w;
+            std::memcpy(&w, c + i, 8);
+            h = (h ^ w) * 0x100000001b3ULL;
+            h ^= h >> 29;
+        }
+        for (; i < n; ++i) h = (h ^ c[i]) * 0x100000001b3ULL;
+        h ^= n;
+    }
+    template <class T>
+    void vec(const std::vector<T>& v) { bytes(v.data(), v.size() * sizeof(T)); }
+};
+
+uint64_t fingerprint(const Model& model, const QuantEnv& env) {
+    Fingerprint f;
+    const ModelConfig& c = model.config;
+    const int cfg[4] = {c.n_layers, c.d_model, c.n_heads, c.d_head};
+    f.bytes(cfg, sizeof(cfg));
+    const int qc[3] = {env.config.weight_bits, env.config.act_bits, env.config.kv_bits};
+    f.bytes(qc, sizeof(qc));
+    auto w = [&f](const QuantizedWeight& q) {
+        f.vec(q.codes.codes);
+        f.vec(q.codes.params.scales);
+    };
+    for (size_t l = 0; l < env.layers.size(); ++l) {
+        const auto& q = env.layers[l];
+        w(q.wq); w(q.wk); w(q.wv); w(q.wo); w(q.w1); w(q.w2);
+    }
+    w(env.w_head);
+    for (const auto& lw : model.layers) {
+        f.vec(lw.norm1_gain);
+        f.vec(lw.norm2_gain);
+    }
+    f.vec(model.final_norm_gain);
+    for (const auto& s : env.act.layers)
+        for (const QuantParams* p : {&s.attn_in, &s.attn_out, &s.mlp_in, &s.mlp_mid}) f.vec(p->scales);
+    f.vec(env.act.head_in.scales);
+    return f.h;
+}
+
+void drop_sessions(const Device* dev) {
+    for (auto it = g_sessions.begin(); it != g_sessions.end();)
+        it = it->second.dev == dev ? g_sessions.erase(it) : std::next(it);
+}
+
 Device* device_for(const Model& model, const QuantEnv& env, int tokens) {
-    auto key = std::make_pair(&model, &env);
-    auto& slot = g_devices[key];
-    const int max_decode = env_int("QUOTA_B200_MAX_DECODE", 512);
-    if (slot && slot->max_tokens >= tokens && slot->max_decode >= max_decode) return slot.get();
     check_env(model, env);
+    const uint64_t fp = fingerprint(model, env);
+    const int max_decode = env_int("QUOTA_B200_MAX_DECODE", 512);
+    std::unique_ptr<Device>* slotp = nullptr;
+    for (auto it = g_devices.begin(); it != g_devices.end(); ++it)
+        if ((*it)->fingerprint == fp) {
+            g_devices.splice(g_devices.begin(), g_devices, it);  // most recently used first
+            slotp = &g_devices.front();
+            break;
+        }
+    if (slotp && (*slotp)->max_tokens >= tokens && (*slotp)->max_decode >= max_decode) return slotp->get();
+    if (!slotp) {
+        g_devices.emplace_front();
+        slotp = &g_devices.front();
+        const size_t cap = (size_t)std::max(1, env_int("QUOTA_B200_MAX_ENGINES", 2));
+        while (g_devices.size() > cap) {  // evict the least recently used engine (and its sessions)
+            drop_sessions(g_devices.back().get());
+            g_devices.pop_back();
+        }
+    }
+    auto& slot = *slotp;
     const ModelConfig& c = model.config;
     auto dev = std::make_unique<Device>();
+    dev->fingerprint = fp;
     qt_config qc{};
     qc.n_layers = c.n_layers;
     qc.d_model = c.d_model;
@@ -191,10 +269,7 @@ Device* device_for(const Model& model, const QuantEnv& env, int tokens) {
     if (env.act.head_in.scales.size() != 1) throw std::invalid_argument("quota_b200: activation scales must be per-tensor");
     act.push_back(env.act.head_in.scales[0]);
     throw_status(qt_engine_set_act_scales(dev->e, act.data()));
-    // invalidate sessions of the engine being replaced
-    if (slot)
-        for (auto it = g_sessions.begin(); it != g_sessions.end();)
-            it = it->second.dev == slot.get() ? g_sessions.erase(it) : std::next(it);
+    if (slot) drop_sessions(slot.get());  // the engine being replaced (grown capacity)
     slot = std::move(dev);
     return slot.get();
 }
@@ -220,9 +295,82 @@ void read_layer_kv(Device* dev, const Model& model, int l, LayerKV& lk) {
         }
 }
 
+// An arbitrary PruneHook, called by the engine once per layer on the materialised record
+// (model.cpp:404-405); the retained set is validated as forward_prefill / apply_pruning
+// do (model.cpp:408-416, selector.cpp:140-148, same messages) before the device applies it.
+struct HostHook {
+    const PruneHook* hook;
+    std::exception_ptr err;
+};
+
+LayerActivationRecord to_record(const qt_layer_record& r) {
+    LayerActivationRecord rec;
+    rec.layer = r.layer;
+    const int V = r.visual, T = r.text, S = V + T, d = r.d_model;
+    rec.visual_states = Matrix(V, d);
+    std::copy(r.visual_states, r.visual_states + (size_t)V * d, rec.visual_states.data.begin());
+    rec.text_states = Matrix(T, d);
+    std::copy(r.text_states, r.text_states + (size_t)T * d, rec.text_states.data.begin());
+    for (int h = 0; h < r.n_heads; ++h) {
+        const float* p = r.probs + (size_t)h * S * V;
+        Matrix inter(T, V), intra(V, V);
+        for (int q = 0; q < V; ++q)
+            for (int k = 0; k < V; ++k) intra.at(q, k) = p[(size_t)q * V + k];
+        for (int q = 0; q < T; ++q)
+            for (int k = 0; k < V; ++k) inter.at(q, k) = p[(size_t)(V + q) * V + k];
+        rec.attn_inter.push_back(std::move(inter));
+        rec.attn_intra.push_back(std::move(intra));
+    }
+    return rec;
+}
+
+SequenceLayout layout_of(int V, int T, const int* pos) {
+    SequenceLayout l;
+    l.visual_count = V;
+    l.text_count = T;
+    l.position_ids.assign(pos, pos + V + T);
+    l.modality.assign(V, Modality::Visual);
+    l.modality.insert(l.modality.end(), T, Modality::Text);
+    return l;
+}
+
+int host_hook_tramp(void* user, const qt_layer_record* r, int* slots, int* n_slots, int* budget) {
+    HostHook* hh = static_cast<HostHook*>(user);
+    try {
+        const LayerActivationRecord rec = to_record(*r);
+        const SequenceLayout cur = layout_of(r->visual, r->text, r->positions);
+        std::optional<RetainedSet> rs = (*hh->hook)(rec, cur);
+        if (!rs) return 0;
+        const int V = r->visual;
+        if (static_cast<int>(rs->slots.size()) < V)
+            for (int s : rs->slots)
+                if (s < 0 || s >= V) throw std::runtime_error("pruning text or out-of-range token");
+        if (rs->slots.empty()) throw std::runtime_error("pruning would remove every visual token");
+        int prev = -1;
+        for (int s : rs->slots) {
+            if (s <= prev) throw std::runtime_error("retained slots must be ascending and unique");
+            if (s < 0 || s >= V) throw std::runtime_error("pruning text or out-of-range token");
+            prev = s;
+        }
+        std::copy(rs->slots.begin(), rs->slots.end(), slots);
+        *n_slots = static_cast<int>(rs->slots.size());
+        *budget = rs->budget;
+        return 1;
+    } catch (...) {
+        hh->err = std::current_exception();
+        return -1;
+    }
+}
+
 }  // namespace
 
 namespace quota {
+
+// prepare_quant_env (model.cpp:212-237) with per-OUTPUT-channel weights: the axis the
+// device's int32-accumulator GEMMs can scale; same validation.
+QuantEnv prepare_quant_env(const Model& model, const QuantConfig& config, const ActScales& act) {
+    return quota_b200::prepare_quant_env_per_channel(model, config, act);
+}
 
 PruneHook make_recipe_hook(const PruningRecipe& recipe, const MetricWeights& weights, std::optional<int> res_bits) {
     PruneHook host = ref_hook()(recipe, weights, res_bits);  // validates like selector.cpp:213
@@ -238,11 +386,8 @@ ForwardResult forward_prefill(const Model& model, const Matrix& embeddings, cons
     if (embeddings.rows != layout.total() || embeddings.cols != model.config.d_model)
         throw std::invalid_argument("embedding shape does not match layout");
     if (options.quant == nullptr) throw std::invalid_argument("quantized mode requires a QuantEnv");
-    const RecipeHook* rh = nullptr;
-    if (options.hook) {
-        rh = options.hook.target<RecipeHook>();
-        if (!rh) throw std::invalid_argument("quota_b200: only make_recipe_hook hooks run on the device");
-    }
+    const RecipeHook* rh = options.hook ? options.hook.target<RecipeHook>() : nullptr;
+    HostHook hh{options.hook ? &options.hook : nullptr, nullptr};
     const QuantEnv& env = *options.quant;
     const int L = model.config.n_layers, d = model.config.d_model;
 
@@ -254,13 +399,22 @@ ForwardResult forward_prefill(const Model& model, const Matrix& embeddings, cons
         const int n = static_cast<int>(r.candidate_layers.size());
         throw_status(qt_engine_set_recipe(dev->e, n, r.candidate_layers.data(), r.keep_ratios.data(), w4, r.v0,
                                           rh->res_bits ? *rh->res_bits : -1));
+        throw_status(qt_engine_set_prune_hook(dev->e, nullptr, nullptr));
     } else {
         throw_status(qt_engine_set_recipe(dev->e, 0, nullptr, nullptr, nullptr, 1, 4));
+        throw_status(qt_engine_set_prune_hook(dev->e, hh.hook ? host_hook_tramp : nullptr, &hh));
     }
+    // ForwardResult::records / block_outputs, as the reference always fills them
+    // (QUOTA_B200_RECORDS=0 skips both: a serving caller that never reads them)
+    const bool records = env_int("QUOTA_B200_RECORDS", 1) != 0;
+    throw_status(qt_engine_set_records(dev->e, records ? 3 : 0));
     const int vis = layout.visual_count, txt = layout.text_count;
     std::vector<float> logits(static_cast<size_t>(layout.total()) * d);
-    throw_status(qt_engine_prefill_f64(dev->e, 1, embeddings.data.data(), 0, &vis, &txt, nullptr,
-                                       layout.position_ids.data(), logits.data(), 0));
+    const int prc = qt_engine_prefill_f64(dev->e, 1, embeddings.data.data(), 0, &vis, &txt, nullptr,
+                                          layout.position_ids.data(), logits.data(), 0);
+    qt_engine_set_prune_hook(dev->e, nullptr, nullptr);
+    if (hh.err) std::rethrow_exception(hh.err);  // the hook's own exception, as the reference propagates it
+    throw_status(prc);
     const int rows = qt_engine_prefill_rows(dev->e);
 
     ForwardResult res;
@@ -292,6 +446,28 @@ ForwardResult forward_prefill(const Model& model, const Matrix& embeddings, cons
     }
     res.prune_trace = trace;
     res.final_layout = fl;
+    if (records) {
+        const int nr = qt_engine_record_count(dev->e);
+        for (int i = 0; i < nr; ++i) {
+            int meta[4];
+            throw_status(qt_engine_record_get(dev->e, i, meta, nullptr, nullptr, nullptr));
+            const int V = meta[1], T = meta[2], H = meta[3];
+            std::vector<int> pos(V + T);
+            std::vector<double> states((size_t)(V + T) * d);
+            std::vector<float> probs((size_t)H * (V + T) * V);
+            throw_status(qt_engine_record_get(dev->e, i, meta, pos.data(), states.data(), probs.data()));
+            qt_layer_record r{meta[0], V, T, d, H, pos.data(), states.data(), states.data() + (size_t)V * d,
+                              probs.data()};
+            res.records.push_back(to_record(r));
+        }
+        for (int l = 0; l < L; ++l) {
+            int br = 0;
+            throw_status(qt_engine_block_output(dev->e, l, nullptr, 0, &br));
+            Matrix b(br, d);
+            throw_status(qt_engine_block_output(dev->e, l, b.data.data(), (long long)b.data.size(), &br));
+            res.block_outputs.push_back(std::move(b));
+        }
+    }
     // KV cache state (model.cpp:447-451); layer l caches the token set entering it,
     // filtered by a prune at l itself (selector.cpp:168-206)
     res.cache.mode = ExecMode::Quantized;

@@ -9,6 +9,7 @@
 //
 // usage: dropin_main <out.txt> [n_decode]
 #include <cstdio>
+#include <optional>
 #include <cstdlib>
 #include <stdexcept>
 #include <string>
@@ -92,6 +93,24 @@ int main(int argc, char** argv) {
     std::fprintf(f, "logits %d %d", res.logits.rows, res.logits.cols);
     for (double v : res.logits.data) std::fprintf(f, " %.9g", v);
     std::fprintf(f, "\n");
+    // ForwardResult::records / block_outputs (model.cpp:382-402,439)
+    std::fprintf(f, "records %zu blocks %zu\n", res.records.size(), res.block_outputs.size());
+    for (const auto& r : res.records) {
+        double inter = 0, intra = 0, vs = 0, ts = 0;
+        for (const auto& m : r.attn_inter)
+            for (double v : m.data) inter += v;
+        for (const auto& m : r.attn_intra)
+            for (double v : m.data) intra += v;
+        for (double v : r.visual_states.data) vs += v * v;
+        for (double v : r.text_states.data) ts += v * v;
+        std::fprintf(f, "rec %d %d %d %zu %.9g %.9g %.9g %.9g\n", r.layer, r.visual_states.rows, r.text_states.rows,
+                     r.attn_inter.size(), inter, intra, vs, ts);
+    }
+    for (size_t l = 0; l < res.block_outputs.size(); ++l) {
+        double ss = 0;
+        for (double v : res.block_outputs[l].data) ss += v * v;
+        std::fprintf(f, "block %zu %d %.9g\n", l, res.block_outputs[l].rows, ss);
+    }
     KVCacheState cache = std::move(res.cache);
     for (int s = 0; s < n_decode; ++s) {
         Matrix e = embeddings(1, cfg.d_model, 900 + s);
@@ -101,9 +120,58 @@ int main(int argc, char** argv) {
         std::fprintf(f, "\n");
     }
     std::fprintf(f, "final %d %d next %d\n", cache.layout.visual_count, cache.layout.text_count, cache.next_position);
-    // error behaviour: a per-input-channel (reference default) env is rejected on the device path
+    // an arbitrary (non-recipe) PruneHook: keep the even visual slots at layer 1 and the
+    // first ceil(V/3) at layer 3 -- it runs on the host per layer over the record
+    {
+        ForwardOptions o3 = opts;
+        o3.hook = [](const LayerActivationRecord& rec, const SequenceLayout& cur) -> std::optional<RetainedSet> {
+            if (rec.layer != 1 && rec.layer != 3) return std::nullopt;
+            RetainedSet rs;
+            if (rec.layer == 1)
+                for (int i = 0; i < cur.visual_count; i += 2) rs.slots.push_back(i);
+            else
+                for (int i = 0; i < (cur.visual_count + 2) / 3; ++i) rs.slots.push_back(i);
+            rs.budget = static_cast<int>(rs.slots.size());
+            return rs;
+        };
+        ForwardResult hr = forward_prefill(model, embeddings(V + T, cfg.d_model, 8), layout, o3);
+        for (const auto& e : hr.prune_trace) {
+            std::fprintf(f, "hookprune %d %d", e.layer, e.budget);
+            for (int p : e.retained_positions) std::fprintf(f, " %d", p);
+            std::fprintf(f, "\n");
+        }
+        std::fprintf(f, "hooklogits %d %d", hr.logits.rows, hr.logits.cols);
+        for (double v : hr.logits.data) std::fprintf(f, " %.9g", v);
+        std::fprintf(f, "\n");
+        // a hook returning an invalid set fails with the reference's exception and message
+        ForwardOptions o4 = opts;
+        o4.hook = [](const LayerActivationRecord&, const SequenceLayout&) -> std::optional<RetainedSet> {
+            RetainedSet rs;
+            rs.slots = {3, 1};
+            return rs;
+        };
+        try {
+            forward_prefill(model, embeddings(V + T, cfg.d_model, 8), layout, o4);
+            std::fprintf(f, "badhook ok\n");
+        } catch (const std::runtime_error& e) {
+            std::fprintf(f, "badhook runtime_error %s\n", e.what());
+        }
+    }
+    // the stock prepare_quant_env (what harness.cpp:113 / calibrator.cpp:260 call): the device
+    // library serves it per output channel, which must equal per_channel_env bit for bit
+    {
+        QuantEnv stock = prepare_quant_env(model, QuantConfig{}, env.act);
+        bool same = stock.layers.size() == env.layers.size();
+        for (size_t l = 0; same && l < env.layers.size(); ++l)
+            same = stock.layers[l].w1.codes.codes == env.layers[l].w1.codes.codes &&
+                   stock.layers[l].w1.codes.params.scales == env.layers[l].w1.codes.params.scales;
+        std::fprintf(f, "stockenv axis %d same %d\n", static_cast<int>(stock.layers[0].wq.codes.params.axis),
+                     same ? 1 : 0);
+    }
+    // error behaviour: a hand-built per-input-channel env is rejected on the device path
     try {
-        QuantEnv row_env = prepare_quant_env(model, QuantConfig{}, env.act);
+        QuantEnv row_env = per_channel_env(model, env.act);
+        for (auto& l : row_env.layers) l.wq.codes = quantize(model.layers[0].wq, fit_params(model.layers[0].wq, 4, GroupAxis::PerRow));
         ForwardOptions o2 = opts;
         o2.quant = &row_env;
         forward_prefill(model, embeddings(V + T, cfg.d_model, 7), layout, o2);

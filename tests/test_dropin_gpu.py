@@ -20,11 +20,17 @@ CXX_SO = os.path.join(ROOT, "paper_2604_17320_b200", "_build", "libquota_b200_cx
 
 
 def _parse(path):
-    out = {"prune": [], "kv": [], "decode": []}
+    out = {"prune": [], "kv": [], "decode": [], "hookprune": [], "rec": [], "block": []}
     for line in open(path):
         t = line.split()
-        if t[0] == "prune":
-            out["prune"].append(list(map(int, t[1:])))
+        if t[0] in ("prune", "hookprune"):
+            out[t[0]].append(list(map(int, t[1:])))
+        elif t[0] == "rec":
+            out["rec"].append(list(map(int, t[1:5])) + list(map(float, t[5:])))
+        elif t[0] == "block":
+            out["block"].append((int(t[1]), int(t[2]), float(t[3])))
+        elif t[0] == "hooklogits":
+            out["hooklogits"] = np.array(list(map(float, t[3:]))).reshape(int(t[1]), int(t[2]))
         elif t[0] == "kv":
             out["kv"].append((int(t[1]), int(t[3]), int(t[5])))
         elif t[0] == "logits":
@@ -63,6 +69,21 @@ def test_reference_api_client_runs_on_b200(tmp_path):
     for x, y in zip(a["decode"], b["decode"]):
         assert np.abs(x - y).max() <= 1e-2
     assert a["final"] == b["final"]
+    # records / block outputs: the same layers and shapes; probability and state sums agree
+    assert a["records"] == b["records"] == "4 blocks 4"
+    for ra, rb in zip(a["rec"], b["rec"]):
+        assert ra[:4] == rb[:4]
+        np.testing.assert_allclose(rb[4:], ra[4:], rtol=1e-3)
+    for ba, bb in zip(a["block"], b["block"]):
+        assert ba[:2] == bb[:2]
+        np.testing.assert_allclose(bb[2], ba[2], rtol=1e-3)
+    # an arbitrary PruneHook (host-side, per layer) prunes identically and keeps the logits
+    assert a["hookprune"] == b["hookprune"] and len(a["hookprune"]) == 2
+    assert np.abs(a["hooklogits"] - b["hooklogits"]).max() <= 1e-2
+    assert a["badhook"] == b["badhook"] == "runtime_error retained slots must be ascending and unique"
+    # the stock prepare_quant_env: per row on the reference, per output channel (== the
+    # per-channel env, bitwise) under the device library
+    assert a["stockenv"] == "axis 1 same 0" and b["stockenv"] == "axis 2 same 1"
     assert a["perrow"] == "ok" and b["perrow"] == "invalid_argument"
 
 
@@ -71,7 +92,7 @@ def test_backend_exports_reference_entry_points():
         pytest.skip("libquota_b200_cxx.so not built")
     nm = subprocess.run(["nm", "-DC", "--defined-only", CXX_SO], capture_output=True, text=True).stdout
     for sym in ("quota::forward_prefill(", "quota::decode_step(", "quota::make_recipe_hook(",
-                "quota_b200::prepare_quant_env_per_channel("):
+                "quota::prepare_quant_env(", "quota_b200::prepare_quant_env_per_channel("):
         assert sym in nm, sym
 
 

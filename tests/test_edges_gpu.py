@@ -187,3 +187,16 @@ def test_async_logits_readback(pair):
     e.prefill(emb2, [30], [10], logits_out=out2, logits_async=True)  # joins the first copy
     e.synchronize()
     assert np.array_equal(out, ref) and np.array_equal(out2, ref2)
+    # pinned host buffers: the device->host copy is truly asynchronous, so the join that keeps
+    # the second prefill from overwriting the device logits mid-copy is exercised
+    import torch
+    p1 = torch.zeros(ref.shape, dtype=torch.float32).pin_memory()
+    p2 = torch.zeros(ref2.shape, dtype=torch.float32).pin_memory()
+    for _ in range(3):
+        p1.zero_()
+        p2.zero_()
+        e.prefill(torch.from_numpy(emb).pin_memory(), [30], [10], logits_out=p1, logits_async=True)
+        e.decode(O.synth_embeddings(1, 128, seed=31).astype(np.float32))
+        e.prefill(torch.from_numpy(emb2).pin_memory(), [30], [10], logits_out=p2, logits_async=True)
+        e.synchronize()  # the returned rows are valid only now
+        assert np.array_equal(p1.numpy(), ref) and np.array_equal(p2.numpy(), ref2)
