@@ -143,7 +143,7 @@ QT_DEV void t5_epilogue_g(int ew0, int warp, int lane, uint32_t tmem, int u0, in
                           int mtp, int cl, int rank, int M, int N, const double* __restrict__ sa,
                           const double* __restrict__ sw, double* sws, void* __restrict__ out, int ldo,
                           int* __restrict__ acc_dbg, int ksplit, int* __restrict__ ws, float* __restrict__ pmax,
-                          int pmax_ld, uint64_t* tfull, uint64_t* tempty) {
+                          int pmax_ld, uint64_t* tfull, uint64_t* tempty, bool pair = false) {
     // ---------------- epilogue: 8 warps; warp & 3 = TMEM lane quarter (32 rows), and
     // (warp - ew0) / 4 = column half -- the per-element fp64 scale math is split 2 ways
     pdl_wait();  // scales / residual come from upstream kernels
@@ -185,7 +185,10 @@ QT_DEV void t5_epilogue_g(int ew0, int warp, int lane, uint32_t tmem, int u0, in
                 // accumulator fully read: hand it back to the MMA issuer
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&tempty[acc]);
+                if (lane == 0) {
+                    if (pair) mbar_arrive_cluster(&tempty[acc], 0);  // the pair's MMA waits on the leader's
+                    else mbar_arrive(&tempty[acc]);
+                }
             }
             const int nb = n0 + j * 32;
             if (m >= M || nb >= N) continue;
@@ -226,15 +229,6 @@ QT_DEV void t5_epilogue(int ew0, int warp, int lane, uint32_t tmem, int units, i
                         float* __restrict__ pmax, int pmax_ld, uint64_t* tfull, uint64_t* tempty) {
     t5_epilogue_g<EPI>(ew0, warp, lane, tmem, blockIdx.x, gridDim.x, units, tiles, mt_n, 1, 0, M, N, sa, sw, sws, out,
                        ldo, acc_dbg, ksplit, ws, pmax, pmax_ld, tfull, tempty);
-}
-
-template <int EPI, int CL>
-QT_DEV void t5_epilogue_cl(int ew0, int warp, int lane, uint32_t tmem, int tiles, int mtp, int rank, int cid, int ncl,
-                           int mt_n, int M, int N, const double* __restrict__ sa, const double* __restrict__ sw,
-                           double* sws, void* __restrict__ out, int ldo, int* __restrict__ acc_dbg,
-                           float* __restrict__ pmax, int pmax_ld, uint64_t* tfull, uint64_t* tempty) {
-    t5_epilogue_g<EPI>(ew0, warp, lane, tmem, cid, ncl, tiles, tiles, mtp, CL, rank, M, N, sa, sw, sws, out, ldo,
-                       acc_dbg, 1, nullptr, pmax, pmax_ld, tfull, tempty);
 }
 
 template <int EPI>
@@ -427,23 +421,6 @@ QT_DEV void tma_load_2d(void* dst, const CUtensorMap* tm, int c0, int c1, uint64
         : "memory");
 }
 
-// TMA 2D load multicast to the CTAs of ctaMask (same smem offset and mbarrier offset in each)
-QT_DEV void tma_load_2d_mc(void* dst, const CUtensorMap* tm, int c0, int c1, uint64_t* bar, uint16_t mask) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster "
-        "[%0], [%1, {%2, %3}], [%4], %5;\n" ::"r"(smem_u32(dst)),
-        "l"(tm), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "h"(mask)
-        : "memory");
-}
-
-// tcgen05.commit arriving on the mbarrier at this smem offset in every CTA of ctaMask
-QT_DEV void mma_commit_mc(uint64_t* bar, uint16_t mask) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
-                     smem_u32(bar)),
-                 "h"(mask)
-                 : "memory");
-}
-
 QT_DEV uint32_t cluster_rank() {
     uint32_t r;
     asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
@@ -454,7 +431,7 @@ QT_DEV void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
 
-template <int EPI, int CL>
+template <int EPI>
 __global__ void __launch_bounds__(T8_THREADS, 1) k_gemm_tc05_i8(const __grid_constant__ CUtensorMap tmA,
                                                                  const __grid_constant__ CUtensorMap tmB,
                                                                  const double* __restrict__ sa,
@@ -472,16 +449,11 @@ __global__ void __launch_bounds__(T8_THREADS, 1) k_gemm_tc05_i8(const __grid_con
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int KB = K / 128;
     const int mt_n = (M + T5_BM - 1) / T5_BM, nt_n = (N + T5_BN - 1) / T5_BN;
-    // CL = 2: a cluster pair takes M tiles (2p, 2p + 1) of one N tile and shares its weight tile:
-    // each CTA loads half of it and multicasts that half to both (halves the per-SM weight ingress)
-    const int mtp = (mt_n + CL - 1) / CL;  // M-tile groups
-    const int tiles = mtp * nt_n;          // work units per cluster
-    const int rank = CL > 1 ? (int)cluster_rank() : 0;
-    const int cid = blockIdx.x / CL, ncl = gridDim.x / CL;
+    const int tiles = mt_n * nt_n;
     if (threadIdx.x == 0) {
         for (int s = 0; s < T8_S; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], CL);  // every CTA's MMA must release the stage (peer TMA writes into it)
+            mbar_init(&empty[s], 1);
         }
         for (int s = 0; s < T5_ACC; ++s) {
             mbar_init(&tfull[s], 1);
@@ -496,7 +468,6 @@ __global__ void __launch_bounds__(T8_THREADS, 1) k_gemm_tc05_i8(const __grid_con
     }
     tc_fence_before();
     __syncthreads();
-    if constexpr (CL > 1) cluster_sync_all();  // the peer's barriers exist before any multicast targets them
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     if (warp == 0) {
@@ -505,18 +476,14 @@ __global__ void __launch_bounds__(T8_THREADS, 1) k_gemm_tc05_i8(const __grid_con
             asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmB) : "memory");
             pdl_wait();  // activation codes come from the upstream kernel
             int it = 0;
-            for (int t = cid; t < tiles; t += ncl) {
-                const int m0 = ((t % mtp) * CL + rank) * T5_BM, n0 = (t / mtp) * T5_BN;
+            for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+                const int m0 = (t % mt_n) * T5_BM, n0 = (t / mt_n) * T5_BN;
                 for (int kb = 0; kb < KB; ++kb, ++it) {
                     const int s = it % T8_S;
                     if (it >= T8_S) mbar_wait(&empty[s], ((it / T8_S) - 1) & 1);
                     mbar_arrive_expect_tx(&full[s], (uint32_t)(T5_IA + T5_IB));
                     tma_load_2d(smem + T8Smem::ia + (size_t)s * T5_IA, &tmA, kb * 128, m0, &full[s]);
-                    if constexpr (CL > 1)
-                        tma_load_2d_mc(smem + T8Smem::ib + (size_t)s * T5_IB + (size_t)rank * (T5_IB / 2), &tmB,
-                                       kb * 128, n0 + rank * (T5_BN / 2), &full[s], (uint16_t)0x3);
-                    else
-                        tma_load_2d(smem + T8Smem::ib + (size_t)s * T5_IB, &tmB, kb * 128, n0, &full[s]);
+                    tma_load_2d(smem + T8Smem::ib + (size_t)s * T5_IB, &tmB, kb * 128, n0, &full[s]);
                 }
             }
         }
@@ -524,7 +491,7 @@ __global__ void __launch_bounds__(T8_THREADS, 1) k_gemm_tc05_i8(const __grid_con
         if (lane == 0) {
             const uint32_t idesc = t5_idesc();
             int it = 0, tl = 0;
-            for (int t = cid; t < tiles; t += ncl, ++tl) {
+            for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++tl) {
                 const int acc = tl % T5_ACC;
                 if (tl >= T5_ACC) mbar_wait(&tempty[acc], ((tl / T5_ACC) - 1) & 1);
                 tc_fence_after();
@@ -539,22 +506,176 @@ __global__ void __launch_bounds__(T8_THREADS, 1) k_gemm_tc05_i8(const __grid_con
                     for (int k = 0; k < 4; ++k)
                         mma_i8(tacc, umma_desc_sw128(a0 + 32 * k), umma_desc_sw128(b0 + 32 * k), idesc,
                                (kb != 0) || (k != 0));
-                    if constexpr (CL > 1) mma_commit_mc(&empty[s], (uint16_t)0x3);
-                    else mma_commit(&empty[s]);
+                    mma_commit(&empty[s]);
                 }
                 mma_commit(&tfull[acc]);
             }
         }
         __syncwarp();
     } else {
-        t5_epilogue_cl<EPI, CL>(T8_EW0, warp, lane, tmem, tiles, mtp, rank, cid, ncl, mt_n, M, N, sa, sw, sws, out,
-                                ldo, acc_dbg, pmax, pmax_ld, tfull, tempty);
+        t5_epilogue_g<EPI>(T8_EW0, warp, lane, tmem, blockIdx.x, gridDim.x, tiles, tiles, mt_n, 1, 0, M, N, sa, sw,
+                           sws, out, ldo, acc_dbg, 1, nullptr, pmax, pmax_ld, tfull, tempty);
     }
     tc_fence_before();
     __syncthreads();
-    if constexpr (CL > 1) cluster_sync_all();  // no CTA leaves while its peer may still multicast / commit into it
     if (warp == 1) {
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(T5_ACC * T5_BN));
+    }
+}
+
+// ============================================================== 2-SM (CTA pair) variant
+// A cluster of two CTAs on one TPC computes a 256 x 256 tile with tcgen05.mma.cta_group::2
+// (M = 256): each CTA stages its own 128 activation rows and HALF of the 256 weight rows, so
+// per SM the operand ingress -- TMA writes plus UMMA shared-memory reads -- is two thirds of
+// the single-CTA 128 x 256 tile's (which saturates shared-memory bandwidth, not the tensor
+// pipe).  Both CTAs' TMA loads complete on the leader's full barrier; the leader alone issues
+// the MMAs, whose commits arrive (multicast) on both CTAs' stage / accumulator barriers; each
+// CTA's epilogue reads its own 128 TMEM lanes and arrives on the leader's accumulator-empty
+// barrier.
+constexpr int T2_S = 6;                                   // stages (32 KB per CTA each)
+constexpr int T2_IA = 128 * 128, T2_IB = 128 * 128;       // per-CTA bytes per stage: A half, B half
+constexpr int T2_THREADS = (T8_EW0 + T5_EWN) * 32;
+
+struct T2Smem {
+    static constexpr size_t ia = 0;
+    static constexpr size_t ib = ia + (size_t)T2_S * T2_IA;
+    static constexpr size_t swb = ib + (size_t)T2_S * T2_IB;
+    static constexpr size_t bars = swb + (size_t)T5_ACC * T5_BN * 8;
+    static constexpr size_t total = bars + 256;
+};
+
+// InstrDescriptor for M = 256 (cta_group::2), N = 256, s8 x s8 -> s32, K-major
+constexpr uint32_t t2_idesc() {
+    return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(T5_BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+}
+
+QT_DEV uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+
+QT_DEV void tma_load_2d_pair(void* dst, const CUtensorMap* tm, int c0, int c1, uint32_t leader_bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%2, %3}], [%4];\n" ::"r"(smem_u32(dst)),
+        "l"(tm), "r"(c0), "r"(c1), "r"(leader_bar)
+        : "memory");
+}
+
+QT_DEV void mma_i8_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accum) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
+        : "memory");
+}
+
+QT_DEV void mma_commit_pair(uint64_t* bar) {  // arrive on the barrier at this offset in both CTAs
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+            smem_u32(bar)),
+        "h"((uint16_t)0x3)
+        : "memory");
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(T2_THREADS, 1) k_gemm_tc05_i8x2(const __grid_constant__ CUtensorMap tmA,
+                                                                   const __grid_constant__ CUtensorMap tmB,
+                                                                   const double* __restrict__ sa,
+                                                                   const double* __restrict__ sw, int M, int N,
+                                                                   int K, void* __restrict__ out, int ldo,
+                                                                   int* __restrict__ acc_dbg,
+                                                                   float* __restrict__ pmax, int pmax_ld) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + T2Smem::bars);
+    uint64_t* empty = full + T2_S;
+    uint64_t* tfull = empty + T2_S;
+    uint64_t* tempty = tfull + T5_ACC;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + T5_ACC);
+    double* sws = reinterpret_cast<double*>(smem + T2Smem::swb);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int rank = (int)cluster_rank();
+    const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+    const int KB = K / 128;
+    const int mtp = (M + 255) / 256, nt_n = (N + T5_BN - 1) / T5_BN;
+    const int tiles = mtp * nt_n;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < T2_S; ++s) {
+            mbar_init(&full[s], 1);   // the leader's arrive.expect_tx (both CTAs' bytes)
+            mbar_init(&empty[s], 1);  // the leader's multicast MMA commit
+        }
+        for (int s = 0; s < T5_ACC; ++s) {
+            mbar_init(&tfull[s], 1);
+            mbar_init(&tempty[s], 2 * T5_EWN);  // both CTAs' epilogue warps (leader's copy is used)
+        }
+        mbar_fence_init();
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                     "n"(T5_ACC * T5_BN));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
+    }
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync_all();  // both CTAs' barriers and TMEM exist before any cross-CTA signal
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    if (warp == 0) {
+        if (lane == 0) {
+            asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmA) : "memory");
+            asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmB) : "memory");
+            pdl_wait();  // activation codes come from the upstream kernel
+            int it = 0;
+            for (int t = cid; t < tiles; t += ncl) {
+                const int m0 = (t % mtp) * 256 + rank * 128, n0 = (t / mtp) * T5_BN + rank * 128;
+                for (int kb = 0; kb < KB; ++kb, ++it) {
+                    const int s = it % T2_S;
+                    if (it >= T2_S) mbar_wait(&empty[s], ((it / T2_S) - 1) & 1);
+                    if (rank == 0) mbar_arrive_expect_tx(&full[s], (uint32_t)(2 * (T2_IA + T2_IB)));
+                    const uint32_t lb = mapa_shared(smem_u32(&full[s]), 0);
+                    tma_load_2d_pair(smem + T2Smem::ia + (size_t)s * T2_IA, &tmA, kb * 128, m0, lb);
+                    tma_load_2d_pair(smem + T2Smem::ib + (size_t)s * T2_IB, &tmB, kb * 128, n0, lb);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && rank == 0) {
+            const uint32_t idesc = t2_idesc();
+            int it = 0, tl = 0;
+            for (int t = cid; t < tiles; t += ncl, ++tl) {
+                const int acc = tl % T5_ACC;
+                if (tl >= T5_ACC) mbar_wait(&tempty[acc], ((tl / T5_ACC) - 1) & 1);
+                tc_fence_after();
+                const uint32_t tacc = tmem + (uint32_t)(acc * T5_BN);
+                for (int kb = 0; kb < KB; ++kb, ++it) {
+                    const int s = it % T2_S;
+                    mbar_wait(&full[s], (it / T2_S) & 1);
+                    tc_fence_after();
+                    const uint32_t a0 = smem_u32(smem + T2Smem::ia + (size_t)s * T2_IA);
+                    const uint32_t b0 = smem_u32(smem + T2Smem::ib + (size_t)s * T2_IB);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        mma_i8_pair(tacc, umma_desc_sw128(a0 + 32 * k), umma_desc_sw128(b0 + 32 * k), idesc,
+                                    (kb != 0) || (k != 0));
+                    mma_commit_pair(&empty[s]);
+                }
+                mma_commit_pair(&tfull[acc]);
+            }
+        }
+        __syncwarp();
+    } else {
+        t5_epilogue_g<EPI>(T8_EW0, warp, lane, tmem, cid, ncl, tiles, tiles, mtp, 2, rank, M, N, sa, sw, sws, out,
+                           ldo, acc_dbg, 1, nullptr, pmax, pmax_ld, tfull, tempty, true);
+    }
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync_all();  // no CTA leaves while its peer may still signal into it
+    if (warp == 1) {
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(T5_ACC * T5_BN));
     }
 }
 
@@ -697,6 +818,7 @@ extern "C" int qt_launch_w4t_to_i8(const uint8_t* tiled, int rows_pad, int K, in
 }
 
 // A8: int8 activations [>= M rows x K], row stride lda8; W8: int8 weights [w_rows x K], stride ldw8.
+// M > 128: the 2-SM (CTA pair, cta_group::2) kernel on 256 x 256 tiles; else the single-CTA one.
 extern "C" int qt_launch_w4a4_tc05_i8(int epi, const int8_t* A8, int lda8, const double* sa, const int8_t* W8,
                                       int w_rows, int ldw8, const double* sw, int M, int N, int K, void* out, int ldo,
                                       int* acc_dbg, float* pmax, int pmax_ld, int* n_part, cudaStream_t st) {
@@ -704,23 +826,59 @@ extern "C" int qt_launch_w4a4_tc05_i8(int epi, const int8_t* A8, int lda8, const
     if (n_part) *n_part = 0;
     if (M <= 0) return 0;
     if (K % 128 || lda8 % 16 || ldw8 % 16 || N > w_rows) return -1;
-    CUtensorMap ta, tb;
-    if (qt_tmap_i8(&ta, A8, M, K, lda8, T5_BM) || qt_tmap_i8(&tb, W8, w_rows, K, ldw8, T5_BN)) return -2;
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    const int mt_n = (M + T5_BM - 1) / T5_BM, nt_n = (N + T5_BN - 1) / T5_BN;
-    const int units = mt_n * nt_n;
-    const dim3 grid(std::min(units, sms));
+    const int nt_n = (N + T5_BN - 1) / T5_BN;
     const int parts = 2 * nt_n;
     if (pmax && parts > pmax_ld) pmax = nullptr;
     if (pmax && n_part) *n_part = parts;
+    CUtensorMap ta, tb;
+    const bool pair = M > T5_BM;
+    if (qt_tmap_i8(&ta, A8, M, K, lda8, T5_BM) || qt_tmap_i8(&tb, W8, w_rows, K, ldw8, pair ? 128 : T5_BN))
+        return -2;
+    if (pair) {
+        const int tiles = ((M + 255) / 256) * nt_n;
+        const dim3 grid(2 * std::min(tiles, sms / 2));
+        const size_t smem = T2Smem::total;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = grid;
+        cfg.blockDim = dim3(T2_THREADS);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute at[2];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[1].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = g_pdl_block ? 1 : 2;
+        g_pdl_block = false;
+#define QT_T2(E)                                                                                                 \
+    do {                                                                                                         \
+        auto kfn = k_gemm_tc05_i8x2<E>;                                                                          \
+        cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                       \
+        return (int)cudaLaunchKernelEx(&cfg, kfn, ta, tb, sa, sw, M, N, K, out, ldo, acc_dbg, pmax, pmax_ld);    \
+    } while (0)
+        switch (epi) {
+            case QT_EPI_STORE: QT_T2(QT_EPI_STORE);
+            case QT_EPI_RESADD: QT_T2(QT_EPI_RESADD);
+            case QT_EPI_SILU: QT_T2(QT_EPI_SILU);
+            case QT_EPI_SWIGLU: QT_T2(QT_EPI_SWIGLU);
+        }
+#undef QT_T2
+        return -1;
+    }
+    const int units = ((M + T5_BM - 1) / T5_BM) * nt_n;
+    const dim3 grid(std::min(units, sms));
     const size_t smem = T8Smem::total;
-#define QT_T8(E)                                                                                                    \
-    do {                                                                                                            \
-        auto kfn = k_gemm_tc05_i8<E, 1>;                                                                            \
-        cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                          \
-        return launch_pdl(kfn, grid, dim3(T8_THREADS), smem, st, ta, tb, sa, sw, M, N, K, out, ldo, acc_dbg, pmax,  \
-                          pmax_ld);                                                                                 \
+#define QT_T8(E)                                                                                                 \
+    do {                                                                                                         \
+        auto kfn = k_gemm_tc05_i8<E>;                                                                            \
+        cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                       \
+        return launch_pdl(kfn, grid, dim3(T8_THREADS), smem, st, ta, tb, sa, sw, M, N, K, out, ldo, acc_dbg, pmax, \
+                          pmax_ld);                                                                              \
     } while (0)
     switch (epi) {
         case QT_EPI_STORE: QT_T8(QT_EPI_STORE);

@@ -217,10 +217,13 @@ def test_w4a4_gemm_splitk_epilogues(torch_cuda, epi):
 
 
 @pytest.mark.parametrize("epi", [Q.EPI_STORE, Q.EPI_RESADD, Q.EPI_SILU, Q.EPI_SWIGLU])
-@pytest.mark.parametrize("M,N,K", [(300, 640, 1024), (129, 256, 512), (1000, 1536, 384), (64, 4096, 256)])
+@pytest.mark.parametrize("M,N,K", [(300, 640, 1024), (129, 256, 512), (1000, 1536, 384), (64, 4096, 256),
+                                   (2048, 2560, 512), (520, 512, 4096), (1896, 4352, 256)])
 def test_w4a4_gemm_int8_operands(torch_cuda, epi, M, N, K):
     """impl 3: the int8-operand tcgen05 GEMM (TMA SWIZZLE_128B tensor loads, no converter warps):
-    int32 accumulators bit-exact, epilogues as the other paths; ragged M and N tiles."""
+    int32 accumulators bit-exact, epilogues as the other paths; ragged M and N tiles.  M > 128
+    runs the 2-SM kernel (cta_group::2, 256 x 256 tiles; more tiles than CTA pairs for the
+    larger shapes, so the pair's persistent loop and double-buffered accumulators cycle)."""
     torch = torch_cuda
     rng = np.random.default_rng(1000 * epi + M)
     a = rng.integers(-7, 8, size=(M, K))
