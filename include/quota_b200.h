@@ -258,9 +258,12 @@ int qt_rmsnorm_quant_i4(const void* x, int x_is_f64, int ld_x, const float* gain
                         float* normed, void* stream);
 /* K2: y = s_a[m] s_w[n] sum_k a[m][k] w[n][k]; out is double* for epilogue
  * 1 (residual add), float* otherwise; acc_out (nullable) receives the int32
- * accumulators; impl 0 = mma.sync path, 1 = tcgen05 path, 2 = tcgen05 with split-K
- * across CTAs when the output tiles would underfill the SMs (the engine's
- * decode path for 17..256 tokens). */
+ * accumulators.  impl 0 = mma.sync GEMM / weight-streaming GEMV (<= 64 tokens);
+ * 1 = tcgen05 on packed int4 (converter warps); 2 = the same with split-K across
+ * CTAs when its tiles would underfill the SMs (65..128 tokens); 3 = tcgen05 on
+ * int8 operands via TMA (2-SM cta_group::2 pairs for M > 128: the prefill GEMM);
+ * 4 = impl 3 with split-K across CTA pairs (129..256 tokens).  Impls 3 and 4
+ * widen the operands to int8 in temporary buffers first (the engine keeps them). */
 int qt_w4a4_gemm(int epilogue, const uint8_t* a_codes, int lda, const double* a_scales, const uint8_t* w_codes,
                  int ldw, const double* w_scales, int M, int N, int K, void* out, int ldo, int32_t* acc_out,
                  int impl, void* stream);

@@ -523,7 +523,7 @@ struct qt_engine {
             for (auto& sh : shapes)
                 for (int m = 17; m <= std::min(mt, 128 * 148); m = (m < 128 ? 128 : m + 128)) {
                     const int mm = std::min(m, mt);
-                    const int ks = qt_tc05_splitk(mm, sh[0], sh[1]);
+                    const int ks = std::max(qt_tc05_splitk(mm, sh[0], sh[1]), qt_tc05_i8_splitk(mm, sh[0], sh[1]));
                     if (ks > 1) need = std::max(need, (size_t)ks * mm * sh[0]);
                 }
             if (need) splitk_ws = dalloc<int>(need);
@@ -1117,11 +1117,12 @@ struct qt_engine {
         pm_parts = 0;
         pm_ptr = atomic_pm ? pm_atomic : pmax;
         pm_ld = atomic_pm ? 1 : kPmaxLd;
-        const bool split = splitk_ws && qt_tc05_splitk(M, N, K) > 1;
-        // tcgen05 for token-rich GEMMs; the weight-streaming GEMV up to 64 tokens (decode batches)
-        int rc = (use_tc05 && M > 64 && codes8 && w8 && !split)
+        // > 128 tokens: the 2-SM int8-operand tcgen05 GEMM (split-K when its tiles underfill the SM
+        // pairs: decode batches up to 256); 65..128: the packed-int4 tcgen05 GEMM with split-K; the
+        // weight-streaming GEMV up to 64 tokens (decode batches)
+        int rc = (use_tc05 && M > 128 && codes8 && w8)
                      ? qt_launch_w4a4_tc05_i8(epi, codes8, ld8, ascale, w8, wrows, K, sw, M, N, K, out, ldo, nullptr, pm,
-                                              kPmaxLd, &pm_parts, st)
+                                              kPmaxLd, &pm_parts, splitk_ws, st)
                  : (use_tc05 && M > 64)
                      ? qt_launch_w4a4_tc05_ex(epi, codes, codes_rows, ascale, w, wrows, sw, M, N, K, out, ldo, nullptr,
                                               splitk_ws, pm, kPmaxLd, &pm_parts, st)
@@ -1604,7 +1605,8 @@ struct qt_engine {
             int* lenl = kv_len + (size_t)l * max_batch;
             if (!(skip_mask & 4)) norm_quant(xcur, 1, d, w.g1, B, d, kd_pad, 4 * l + 0);
             cap_site(l, 0, B, d, kd_pad);
-            if (!(skip_mask & 1)) gemm(QT_EPI_STORE, w.qkv, n_qkv_pad, w.s_qkv, B, n_qkv, kd_pad, qkv, n_qkv);
+            if (!(skip_mask & 1))
+                gemm(QT_EPI_STORE, w.qkv, n_qkv_pad, w.s_qkv, B, n_qkv, kd_pad, qkv, n_qkv, false, w.qkv8);
             pb(P_ATTN);
             // decode attention over the int4 pages with the new token's RoPE + K/V quantize +
             // append fused in, then the split merge fused with the attn_out quantizer
@@ -1625,20 +1627,21 @@ struct qt_engine {
                 cap_kv(l, r0, nr);
             }
             cap_site(l, 1, B, d, kd_pad);
-            if (!(skip_mask & 1)) gemm(QT_EPI_RESADD, w.o, nd_pad, w.s_o, B, d, kd_pad, xcur, d);
+            if (!(skip_mask & 1)) gemm(QT_EPI_RESADD, w.o, nd_pad, w.s_o, B, d, kd_pad, xcur, d, false, w.o8);
             if (!(skip_mask & 4)) norm_quant(xcur, 1, d, w.g2, B, d, kd_pad, 4 * l + 2);
             cap_site(l, 2, B, d, kd_pad);
             float* gml = gmax ? gmax + (size_t)l * max_batch : nullptr;
             if (!(skip_mask & 1))
                 gemm(cfg.mlp == 1 ? QT_EPI_SWIGLU : QT_EPI_SILU, w.gu, n_gu_pad, w.s_gu, B, n_gu, kd_pad, mid, dff, true,
-                     nullptr, gml);
+                     w.gu8, gml);
             if (!(skip_mask & 4)) norm_quant(mid, 0, dff, nullptr, B, dff, kff_pad, 4 * l + 3, true);
             cap_site(l, 3, B, dff, kff_pad);
-            if (!(skip_mask & 1)) gemm(QT_EPI_RESADD, w.down, nd_pad, w.s_down, B, d, kff_pad, xcur, d);
+            if (!(skip_mask & 1))
+                gemm(QT_EPI_RESADD, w.down, nd_pad, w.s_down, B, d, kff_pad, xcur, d, false, w.down8);
         }
         norm_quant(xcur, 1, d, gf, B, d, kd_pad, 4 * L);
         cap_site(L, 4, B, d, kd_pad);
-        gemm(QT_EPI_STORE, head, nd_pad, s_head, B, d, kd_pad, dlogits, d);
+        gemm(QT_EPI_STORE, head, nd_pad, s_head, B, d, kd_pad, dlogits, d, false, head8);
         ckl(qt_launch_kv_len_bump(kv_len, L * max_batch, next_pos, B, st), "kv length / position bump");
         if (gmax) ck(cudaMemsetAsync(gmax, 0, (size_t)L * max_batch * sizeof(float), st), "row-max reset");
     }
@@ -2456,18 +2459,23 @@ int qt_w4a4_gemm(int epi, const uint8_t* a, int lda, const double* sa, const uin
                  int M, int N, int K, void* out, int ldo, int32_t* acc_out, int impl, void* stream) {
     return guard([&] {
         const cudaStream_t cs = (cudaStream_t)stream;
-        if (impl == 3) {  // int8-operand tcgen05 GEMM: both operands widened to int8 first (test / ABI path)
+        if (impl == 3 || impl == 4) {  // int8-operand tcgen05 GEMM: operands widened to int8 first (test / ABI
+                                       // path); impl 4 with the 2-SM kernel's split-K workspace
             int8_t *a8 = nullptr, *w8 = nullptr;
+            int* ws = nullptr;
             ck(cudaMalloc(&a8, (size_t)lda * K), "int8 activations");
             ck(cudaMalloc(&w8, (size_t)ldw * K), "int8 weights");
+            if (impl == 4)
+                ck(cudaMalloc(&ws, (size_t)std::max(1, qt_tc05_i8_splitk(M, N, K)) * M * N * sizeof(int)), "split-K ws");
             int rc = qt_launch_w4t_to_i8(a, lda, K, a8, cs);
             if (!rc) rc = qt_launch_w4t_to_i8(w, ldw, K, w8, cs);
             if (!rc)
                 rc = qt_launch_w4a4_tc05_i8(epi, a8, K, sa, w8, ldw, K, sw, M, N, K, out, ldo, acc_out, nullptr, 0,
-                                            nullptr, cs);
+                                            nullptr, ws, cs);
             cudaStreamSynchronize(cs);
             cudaFree(a8);
             cudaFree(w8);
+            if (ws) cudaFree(ws);
             ckl(rc, "w4a4 gemm (int8 operands)");
             return;
         }

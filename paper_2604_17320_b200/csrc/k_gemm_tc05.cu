@@ -589,7 +589,8 @@ __global__ void __launch_bounds__(T2_THREADS, 1) k_gemm_tc05_i8x2(const __grid_c
                                                                    const double* __restrict__ sw, int M, int N,
                                                                    int K, void* __restrict__ out, int ldo,
                                                                    int* __restrict__ acc_dbg,
-                                                                   float* __restrict__ pmax, int pmax_ld) {
+                                                                   float* __restrict__ pmax, int pmax_ld, int ksplit,
+                                                                   int* __restrict__ ws) {
     extern __shared__ __align__(1024) uint8_t smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + T2Smem::bars);
     uint64_t* empty = full + T2_S;
@@ -603,6 +604,9 @@ __global__ void __launch_bounds__(T2_THREADS, 1) k_gemm_tc05_i8x2(const __grid_c
     const int KB = K / 128;
     const int mtp = (M + 255) / 256, nt_n = (N + T5_BN - 1) / T5_BN;
     const int tiles = mtp * nt_n;
+    // work unit u: tile u % tiles, k slice u / tiles (split-K, ksplit > 1: int32 partials to ws,
+    // reduced in fixed order by k_splitk_epilogue)
+    const int units = tiles * ksplit, kbs = (KB + ksplit - 1) / ksplit;
     if (threadIdx.x == 0) {
         for (int s = 0; s < T2_S; ++s) {
             mbar_init(&full[s], 1);   // the leader's arrive.expect_tx (both CTAs' bytes)
@@ -630,9 +634,10 @@ __global__ void __launch_bounds__(T2_THREADS, 1) k_gemm_tc05_i8x2(const __grid_c
             asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmB) : "memory");
             pdl_wait();  // activation codes come from the upstream kernel
             int it = 0;
-            for (int t = cid; t < tiles; t += ncl) {
+            for (int u = cid; u < units; u += ncl) {
+                const int t = u % tiles, k0 = (u / tiles) * kbs, k1 = min(KB, k0 + kbs);
                 const int m0 = (t % mtp) * 256 + rank * 128, n0 = (t / mtp) * T5_BN + rank * 128;
-                for (int kb = 0; kb < KB; ++kb, ++it) {
+                for (int kb = k0; kb < k1; ++kb, ++it) {
                     const int s = it % T2_S;
                     if (it >= T2_S) mbar_wait(&empty[s], ((it / T2_S) - 1) & 1);
                     if (rank == 0) mbar_arrive_expect_tx(&full[s], (uint32_t)(2 * (T2_IA + T2_IB)));
@@ -646,12 +651,13 @@ __global__ void __launch_bounds__(T2_THREADS, 1) k_gemm_tc05_i8x2(const __grid_c
         if (lane == 0 && rank == 0) {
             const uint32_t idesc = t2_idesc();
             int it = 0, tl = 0;
-            for (int t = cid; t < tiles; t += ncl, ++tl) {
+            for (int u = cid; u < units; u += ncl, ++tl) {
+                const int k0 = (u / tiles) * kbs, k1 = min(KB, k0 + kbs);
                 const int acc = tl % T5_ACC;
                 if (tl >= T5_ACC) mbar_wait(&tempty[acc], ((tl / T5_ACC) - 1) & 1);
                 tc_fence_after();
                 const uint32_t tacc = tmem + (uint32_t)(acc * T5_BN);
-                for (int kb = 0; kb < KB; ++kb, ++it) {
+                for (int kb = k0; kb < k1; ++kb, ++it) {
                     const int s = it % T2_S;
                     mbar_wait(&full[s], (it / T2_S) & 1);
                     tc_fence_after();
@@ -660,7 +666,7 @@ __global__ void __launch_bounds__(T2_THREADS, 1) k_gemm_tc05_i8x2(const __grid_c
 #pragma unroll
                     for (int k = 0; k < 4; ++k)
                         mma_i8_pair(tacc, umma_desc_sw128(a0 + 32 * k), umma_desc_sw128(b0 + 32 * k), idesc,
-                                    (kb != 0) || (k != 0));
+                                    (kb != k0) || (k != 0));
                     mma_commit_pair(&empty[s]);
                 }
                 mma_commit_pair(&tfull[acc]);
@@ -668,8 +674,8 @@ __global__ void __launch_bounds__(T2_THREADS, 1) k_gemm_tc05_i8x2(const __grid_c
         }
         __syncwarp();
     } else {
-        t5_epilogue_g<EPI>(T8_EW0, warp, lane, tmem, cid, ncl, tiles, tiles, mtp, 2, rank, M, N, sa, sw, sws, out,
-                           ldo, acc_dbg, 1, nullptr, pmax, pmax_ld, tfull, tempty, true);
+        t5_epilogue_g<EPI>(T8_EW0, warp, lane, tmem, cid, ncl, units, tiles, mtp, 2, rank, M, N, sa, sw, sws, out,
+                           ldo, ksplit > 1 ? nullptr : acc_dbg, ksplit, ws, pmax, pmax_ld, tfull, tempty, true);
     }
     tc_fence_before();
     __syncthreads();
@@ -819,9 +825,22 @@ extern "C" int qt_launch_w4t_to_i8(const uint8_t* tiled, int rows_pad, int K, in
 
 // A8: int8 activations [>= M rows x K], row stride lda8; W8: int8 weights [w_rows x K], stride ldw8.
 // M > 128: the 2-SM (CTA pair, cta_group::2) kernel on 256 x 256 tiles; else the single-CTA one.
+int qt_tc05_i8_splitk(int M, int N, int K) {
+    // the 2-SM kernel's k slices: enough work units for every CTA pair, >= 4 k blocks per slice
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    if (M <= qt::T5_BM) return 1;
+    const int tiles = ((M + 255) / 256) * ((N + qt::T5_BN - 1) / qt::T5_BN);
+    const int pairs = sms / 2, KB = K / 128;
+    if (tiles >= pairs) return 1;
+    const int ks = std::max(1, std::min((pairs + tiles - 1) / tiles, KB / 4));
+    const int kbs = (KB + ks - 1) / ks;
+    return (KB + kbs - 1) / kbs;  // no empty slice
+}
+
 extern "C" int qt_launch_w4a4_tc05_i8(int epi, const int8_t* A8, int lda8, const double* sa, const int8_t* W8,
                                       int w_rows, int ldw8, const double* sw, int M, int N, int K, void* out, int ldo,
-                                      int* acc_dbg, float* pmax, int pmax_ld, int* n_part, cudaStream_t st) {
+                                      int* acc_dbg, float* pmax, int pmax_ld, int* n_part, int* ws, cudaStream_t st) {
     using namespace qt;
     if (n_part) *n_part = 0;
     if (M <= 0) return 0;
@@ -838,7 +857,12 @@ extern "C" int qt_launch_w4a4_tc05_i8(int epi, const int8_t* A8, int lda8, const
         return -2;
     if (pair) {
         const int tiles = ((M + 255) / 256) * nt_n;
-        const dim3 grid(2 * std::min(tiles, sms / 2));
+        const int ksplit = ws ? qt_tc05_i8_splitk(M, N, K) : 1;
+        if (ksplit > 1) {
+            pmax = nullptr;
+            if (n_part) *n_part = 0;
+        }
+        const dim3 grid(2 * std::min(tiles * ksplit, sms / 2));
         const size_t smem = T2Smem::total;
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = grid;
@@ -859,7 +883,12 @@ extern "C" int qt_launch_w4a4_tc05_i8(int epi, const int8_t* A8, int lda8, const
     do {                                                                                                         \
         auto kfn = k_gemm_tc05_i8x2<E>;                                                                          \
         cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                       \
-        return (int)cudaLaunchKernelEx(&cfg, kfn, ta, tb, sa, sw, M, N, K, out, ldo, acc_dbg, pmax, pmax_ld);    \
+        int rc = (int)cudaLaunchKernelEx(&cfg, kfn, ta, tb, sa, sw, M, N, K, out, ldo, acc_dbg, pmax, pmax_ld,   \
+                                         ksplit, ws);                                                            \
+        if (rc || ksplit == 1) return rc;                                                                        \
+        const long long pairs2 = ((long long)M * N + 1) / 2;                                                     \
+        return launch_pdl(k_splitk_epilogue<E>, dim3((unsigned)((pairs2 + 255) / 256)), dim3(256), 0, st,       \
+                          (const int*)ws, ksplit, M, N, sa, sw, out, ldo, acc_dbg);                               \
     } while (0)
         switch (epi) {
             case QT_EPI_STORE: QT_T2(QT_EPI_STORE);

@@ -45,7 +45,10 @@ int qt_launch_codes_pack(const int8_t* src, int K, int N, const double* s_in, in
 // int8-operand tcgen05 GEMM (operands 16 x code, k natural order, row-major; TMA SW128)
 int qt_launch_w4a4_tc05_i8(int epi, const int8_t* A8, int lda8, const double* sa, const int8_t* W8, int w_rows,
                            int ldw8, const double* sw, int M, int N, int K, void* out, int ldo, int* acc_dbg,
-                           float* pmax, int pmax_ld, int* n_part, cudaStream_t st);
+                           float* pmax, int pmax_ld, int* n_part, int* ws, cudaStream_t st);
+// ws (nullable): int32 split-K workspace of qt_tc05_i8_splitk(M, N, K) * M * N entries (the 2-SM kernel
+// splits K when its 256 x 256 tiles would leave CTA pairs idle: decode batches of 129..256 tokens)
+int qt_tc05_i8_splitk(int M, int N, int K);
 int qt_launch_w4t_to_i8(const uint8_t* tiled, int rows_pad, int K, int8_t* out, cudaStream_t st);
 int qt_launch_w4a4_mma_ex(int epi, const uint8_t* A, int lda, const double* sa, const uint8_t* W, int ldw,
                           const double* sw, int M, int N, int K, void* out, int ldo, int* acc_dbg, float* pmax,

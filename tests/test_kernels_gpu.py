@@ -218,12 +218,16 @@ def test_w4a4_gemm_splitk_epilogues(torch_cuda, epi):
 
 @pytest.mark.parametrize("epi", [Q.EPI_STORE, Q.EPI_RESADD, Q.EPI_SILU, Q.EPI_SWIGLU])
 @pytest.mark.parametrize("M,N,K", [(300, 640, 1024), (129, 256, 512), (1000, 1536, 384), (64, 4096, 256),
-                                   (2048, 2560, 512), (520, 512, 4096), (1896, 4352, 256)])
-def test_w4a4_gemm_int8_operands(torch_cuda, epi, M, N, K):
+                                   (2048, 2560, 512), (520, 512, 4096), (1896, 4352, 256), (256, 4096, 4096),
+                                   (200, 3072, 2048)])
+@pytest.mark.parametrize("impl", [3, 4])
+def test_w4a4_gemm_int8_operands(torch_cuda, epi, M, N, K, impl):
     """impl 3: the int8-operand tcgen05 GEMM (TMA SWIZZLE_128B tensor loads, no converter warps):
     int32 accumulators bit-exact, epilogues as the other paths; ragged M and N tiles.  M > 128
     runs the 2-SM kernel (cta_group::2, 256 x 256 tiles; more tiles than CTA pairs for the
-    larger shapes, so the pair's persistent loop and double-buffered accumulators cycle)."""
+    larger shapes, so the pair's persistent loop and double-buffered accumulators cycle).
+    impl 4: the same with the split-K workspace (decode batches of 129..256 tokens: k slices
+    across CTA pairs, int32 partials reduced in fixed order)."""
     torch = torch_cuda
     rng = np.random.default_rng(1000 * epi + M)
     a = rng.integers(-7, 8, size=(M, K))
@@ -248,7 +252,7 @@ def test_w4a4_gemm_int8_operands(torch_cuda, epi, M, N, K):
         exp, tol = y, dict(rtol=2e-7, atol=1e-7)
     acc = torch.zeros((M, N), dtype=torch.int32, device="cuda")
     Q.w4a4_gemm(epi, torch.from_numpy(_tiled(a)).cuda(), torch.from_numpy(sa).cuda(),
-                torch.from_numpy(_tiled(w, 128)).cuda(), torch.from_numpy(sw).cuda(), M, N, K, out, acc, impl=3)
+                torch.from_numpy(_tiled(w, 128)).cuda(), torch.from_numpy(sw).cuda(), M, N, K, out, acc, impl=impl)
     torch.cuda.synchronize()
     assert np.array_equal(acc.cpu().numpy(), acc_exp)
     np.testing.assert_allclose(out.cpu().numpy(), exp, **tol)
