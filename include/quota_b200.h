@@ -267,6 +267,14 @@ int qt_rmsnorm_quant_i4(const void* x, int x_is_f64, int ld_x, const float* gain
 int qt_w4a4_gemm(int epilogue, const uint8_t* a_codes, int lda, const double* a_scales, const uint8_t* w_codes,
                  int ldw, const double* w_scales, int M, int N, int K, void* out, int ldo, int32_t* acc_out,
                  int impl, void* stream);
+/* K2 on int8 operands (16 x code, k in natural order, row-major: the prefill layout, see
+ * qt_unpack_codes): a8 [>= M x lda8], w8 [w_rows x ldw8]; M > 128 runs the 2-SM
+ * (cta_group::2) kernel -- flags bit 0 forces the single-CTA one (A/B measurement) --
+ * with split-K when workspace (qt_w4a4_gemm_i8_workspace bytes, nullable) is given. */
+int qt_w4a4_gemm_i8(int epi, const int8_t* a8, int lda8, const double* sa, const int8_t* w8, int w_rows, int ldw8,
+                    const double* sw, int M, int N, int K, void* out, int ldo, int32_t* acc_out, int* workspace,
+                    int flags, void* stream);
+int64_t qt_w4a4_gemm_i8_workspace(int M, int N, int K);
 int qt_quant_weight_i4(const float* w, int K, int N, int row_mul, int row_add, uint8_t* codes, int ldc,
                        double* scales, double* scratch, void* stream);
 int qt_kv_quant_append_i4(float* qkv, int ld_qkv, int M, int H, int Hkv, int d_head, const int* positions,

@@ -102,6 +102,10 @@ def lib():
         L.qt_engine_load.argtypes = [vp, C.c_char_p]
         L.qt_engine_scores.argtypes = [vp, C.c_int, C.c_int, dp, dp, C.c_int, ip]
         L.qt_quota_topk.argtypes = [vp, C.c_int, C.c_int, vp, vp, dp, vp, vp, vp, vp]
+        L.qt_w4a4_gemm_i8.argtypes = [C.c_int, vp, C.c_int, vp, vp, C.c_int, C.c_int, vp, C.c_int, C.c_int,
+                                      C.c_int, vp, C.c_int, vp, vp, C.c_int, vp]
+        L.qt_w4a4_gemm_i8_workspace.restype = C.c_int64
+        L.qt_w4a4_gemm_i8_workspace.argtypes = [C.c_int, C.c_int, C.c_int]
         L.qt_engine_capture.argtypes = [vp, C.c_int]
         L.qt_engine_capture_count.argtypes = [vp]
         L.qt_engine_capture_get.argtypes = [vp, C.c_int, ip, vp, dp]
@@ -475,6 +479,14 @@ def w4a4_gemm(epi, a_codes, a_scales, w_codes, w_scales, M, N, K, out, acc_out=N
     check(lib().qt_w4a4_gemm(epi, _ptr(a_codes), a_codes.shape[0], _ptr(a_scales), _ptr(w_codes), w_codes.shape[0],
                              _ptr(w_scales), M, N, K, _ptr(out), out.stride(0), _ptr(acc_out), impl,
                              C.c_void_p(stream)))
+    return out
+
+
+def w4a4_gemm_i8(epi, a8, sa, w8, sw, M, N, K, out, acc_out=None, workspace=None, single=False, stream=0):
+    """qt_w4a4_gemm_i8 on int8 operand tensors (16 x code, row-major)."""
+    check(lib().qt_w4a4_gemm_i8(epi, _ptr(a8), a8.shape[1], _ptr(sa), _ptr(w8), w8.shape[0], w8.shape[1], _ptr(sw),
+                                M, N, K, _ptr(out), out.stride(0), _ptr(acc_out), _ptr(workspace), int(single),
+                                C.c_void_p(stream)))
     return out
 
 

@@ -14,8 +14,10 @@
 // since earlier steps, so the copies overlap the upstream QKV GEMV.  After the wait the
 // CTA whose split holds the new row RoPEs and quantizes that token's K / V (fp64, the
 // reference's arithmetic) and appends them to the cache and to its shared copy.  Scores
-// (4 lanes per row, fp32), a per-head softmax, then P . V (16 word columns x 16 row groups)
-// produce one (max, sum, unnormalised o) partial per (sequence, query head, split);
+// and probabilities are fp32, 4 lanes per row
+// (8-row chunks per warp: scores with every G head per converted K row, then P . V per head,
+// each warp on its own rows with no block barrier; the 8 warps' states are combined at the
+// end) produce one (max, sum, unnormalised o) partial per (sequence, query head, split);
 // k_attn_merge_quant merges the splits in fixed order and quantizes the attn_out site.
 // int4 -> fp32 without I2F: float(0x4B000000 | (nib ^ 8)) - (2^23 + 8) is exact.
 #include <algorithm>
@@ -40,6 +42,8 @@ template <int DH, int G>
 struct AdSmem {
     static constexpr int CB = kPage * (DH / 2);  // code bytes per (page, kv head, K|V)
     static constexpr int QLD = DH + 16;           // padded q row (the 4 quarter slices hit distinct banks)
+    // shared: the split's K / V codes and scales, q, scores [G][rows], per-warp partial o
+    // [8][G][DH] and (max, sum) [8][G], the pages' mbarrier
     QT_HD static size_t kc(int) { return 0; }
     QT_HD static size_t vc(int pps) { return (size_t)pps * CB; }
     QT_HD static size_t ks(int pps) { return (size_t)2 * pps * CB; }
@@ -48,7 +52,7 @@ struct AdSmem {
     QT_HD static size_t sc(int pps) { return q(pps) + (size_t)G * QLD * 4; }
     QT_HD static size_t red(int pps) { return sc(pps) + (size_t)G * pps * kPage * 4; }
     QT_HD static size_t stat(int pps) { return red(pps) + (size_t)8 * G * DH * 4; }
-    QT_HD static size_t bar(int pps) { return (stat(pps) + G * 8 + 15) / 16 * 16; }
+    QT_HD static size_t bar(int pps) { return (stat(pps) + 8 * G * 8 + G * 4 + 15) / 16 * 16; }
     QT_HD static size_t total(int pps) { return bar(pps) + 16; }
 };
 
@@ -61,7 +65,11 @@ __global__ void __launch_bounds__(AD_THREADS) k_attn_dec(const float* __restrict
                                                          long long page_bytes, const int* __restrict__ pt,
                                                          int max_pages, int pps, const double2* __restrict__ rope,
                                                          const int* __restrict__ pos, float inv_sqrt,
-                                                         float* __restrict__ part_ml, float* __restrict__ part_o) {
+                                                         float* __restrict__ part_ml, float* __restrict__ part_o,
+                                                         float* __restrict__ row, float* __restrict__ hmax,
+                                                         unsigned* __restrict__ cnt, uint8_t* __restrict__ codes,
+                                                         int ld_codes, double* __restrict__ scales, int qmode,
+                                                         double static_scale, int d_pad, int qmax) {
     using S = AdSmem<DH, G>;
     constexpr int CB = S::CB, QLD = S::QLD;
     constexpr int CPL = DH / 4;    // channels per lane in the score phase
@@ -89,7 +97,7 @@ __global__ void __launch_bounds__(AD_THREADS) k_attn_dec(const float* __restrict
     const int r0 = split * pps * kPage;
     const int n_rows = min(pps * kPage, len - r0);
     const size_t pidx0 = ((size_t)b * H + (size_t)kh * G) * nsplit + split;
-    if (n_rows <= 0) {  // nothing cached in this split: an empty partial per head
+    if (n_rows <= 0) {  // nothing cached in this split: an empty partial per head (never with row != null)
         pdl_wait();     // the partial buffers are still read by the previous layer's merge
         for (int i = tid; i < G * DH; i += AD_THREADS) part_o[(pidx0 + (size_t)(i / DH) * nsplit) * DH + i % DH] = 0.f;
         if (tid < G) {
@@ -115,6 +123,7 @@ __global__ void __launch_bounds__(AD_THREADS) k_attn_dec(const float* __restrict
             bulk_g2s(vsc + p * kPage, page + 2 * cbh + ((size_t)Hkv + kh) * kPage * 4, kPage * 4, bar);
         }
     }
+    if (tid < G) reinterpret_cast<int*>(stat)[16 * G + tid] = 0;  // per-head max |o| (fused quantizer)
     pdl_wait();  // q (and the new token's k / v) come from the upstream GEMV
 
     // q of the G heads -> smem (RoPE'd here in the decode step: fp64, rounded to fp32 like
@@ -136,159 +145,224 @@ __global__ void __launch_bounds__(AD_THREADS) k_attn_dec(const float* __restrict
         dst[0] = o.x;
         dst[1] = o.y;
     }
-    // the new row (decode step): warp 0 its K (RoPE'd), warp 1 its V -- kv_quantize in fp64
+    __syncthreads();  // the only block barrier before the final combine
+    // Rows are processed in 8-row chunks, each chunk owned by one warp (4 lanes per row, CPL
+    // channels per lane); the chunk holding the new row is warp 0's, so only warp 0 depends on
+    // the append it performs itself.
     const int new_r = old_len - r0;  // row within this split
     const bool has_new = fused && new_r >= 0 && new_r < n_rows;
-    constexpr int E = DH / 32;
-    uint32_t new_word = 0;
-    float new_scale = 0.f;
-    if (has_new && warp < 2) {
-        const bool is_k = warp == 0;
-        const float* src = qrow + (is_k ? H * DH : (H + Hkv) * DH) + kh * DH + lane * E;
-        double val[E];
+    const int n_chunks = npg * (kPage / 8);
+    const int c_rot = has_new ? new_r / 8 : 0;
+    if (has_new && warp == 0) {
+        // the new row: kv_quantize (quant.cpp:117-119) of the RoPE'd K and of V, fp64
+        constexpr int E = DH / 32;
+        uint32_t word[2] = {0, 0};
+        float scl[2] = {0.f, 0.f};
 #pragma unroll
-        for (int j = 0; j < E; ++j) val[j] = (double)src[j];
-        if (is_k) {
+        for (int w = 0; w < 2; ++w) {
+            const float* src = qrow + (w == 0 ? H * DH : (H + Hkv) * DH) + kh * DH + lane * E;
+            double val[E];
 #pragma unroll
-            for (int j = 0; j < E; j += 2) {
-                const double2 cs = rt[(lane * E + j) / 2];
-                const double a = val[j], bb = val[j + 1];
-                val[j] = __dsub_rn(__dmul_rn(a, cs.x), __dmul_rn(bb, cs.y));
-                val[j + 1] = __dadd_rn(__dmul_rn(a, cs.y), __dmul_rn(bb, cs.x));
+            for (int j = 0; j < E; ++j) val[j] = (double)src[j];
+            if (w == 0) {
+#pragma unroll
+                for (int j = 0; j < E; j += 2) {
+                    const double2 cs = rt[(lane * E + j) / 2];
+                    const double a = val[j], bb = val[j + 1];
+                    val[j] = __dsub_rn(__dmul_rn(a, cs.x), __dmul_rn(bb, cs.y));
+                    val[j + 1] = __dadd_rn(__dmul_rn(a, cs.y), __dmul_rn(bb, cs.x));
+                }
             }
+            double mx = 0.0;
+#pragma unroll
+            for (int j = 0; j < E; ++j) mx = fmax(mx, fabs(val[j]));
+            mx = warp_max(mx);
+            const double sq = q_scale(mx, 7), inv_s = 1.0 / sq;
+#pragma unroll
+            for (int j = 0; j < E; ++j) word[w] |= (uint32_t)(q_code_r(val[j], sq, inv_s, 7) & 0xF) << (4 * j);
+            scl[w] = (float)sq;
         }
-        double mx = 0.0;
-#pragma unroll
-        for (int j = 0; j < E; ++j) mx = fmax(mx, fabs(val[j]));
-        mx = warp_max(mx);
-        const double s = q_scale(mx, 7), inv_s = 1.0 / s;
-#pragma unroll
-        for (int j = 0; j < E; ++j) new_word |= (uint32_t)(q_code_r(val[j], s, inv_s, 7) & 0xF) << (4 * j);
-        new_scale = (float)s;
         // append to the cache (model.cpp:499-501)
         uint8_t* page = pool + (long long)pt[b * max_pages + old_len / kPage] * page_bytes;
         const int slot = old_len % kPage;
-        uint8_t* dst = page + (is_k ? 0 : cbh) + (size_t)kh * CB + (size_t)slot * (DH / 2) + lane * E / 2;
-        if (E == 4) *reinterpret_cast<uint16_t*>(dst) = (uint16_t)new_word;
-        else *dst = (uint8_t)new_word;
-        if (lane == 0)
-            reinterpret_cast<float*>(page + 2 * cbh)[(is_k ? 0 : Hkv * kPage) + kh * kPage + slot] = new_scale;
-    }
-    mbar_wait(bar, 0);  // the split's pages have landed
-    if (has_new && warp < 2) {  // ... and the new row replaces its (stale) shared copy
-        uint8_t* d = (warp == 0 ? kc : vc) + (size_t)new_r * (DH / 2) + lane * E / 2;
-        if (E == 4) *reinterpret_cast<uint16_t*>(d) = (uint16_t)new_word;
-        else *d = (uint8_t)new_word;
-        if (lane == 0) (warp == 0 ? ksc : vsc)[new_r] = new_scale;
-    }
-    __syncthreads();
-
-    // scores: 4 lanes per row, CPL channels each; all G heads per converted row
-    {
-        const int q4 = lane & 3;
-        for (int r = warp * 8 + (lane >> 2); r < npg * kPage; r += 64) {
-            float kf[CPL];
-            const uint8_t* kr = kc + (size_t)r * (DH / 2) + q4 * (CPL / 2);
-            if constexpr (CPL == 32) {
-                const uint4 w = *reinterpret_cast<const uint4*>(kr);
-                nib8_to_f32(w.x, kf); nib8_to_f32(w.y, kf + 8); nib8_to_f32(w.z, kf + 16); nib8_to_f32(w.w, kf + 24);
-            } else {
-                const uint2 w = *reinterpret_cast<const uint2*>(kr);
-                nib8_to_f32(w.x, kf); nib8_to_f32(w.y, kf + 8);
-            }
-            float d[G];
 #pragma unroll
-            for (int g = 0; g < G; ++g) {
-                const float4* qv = reinterpret_cast<const float4*>(qs + g * QLD + q4 * (CPL + 4));
-                float acc = 0.f;
-#pragma unroll
-                for (int c = 0; c < CPL / 4; ++c) {
-                    const float4 qq = qv[c];
-                    acc = fmaf(qq.x, kf[4 * c], acc);
-                    acc = fmaf(qq.y, kf[4 * c + 1], acc);
-                    acc = fmaf(qq.z, kf[4 * c + 2], acc);
-                    acc = fmaf(qq.w, kf[4 * c + 3], acc);
-                }
-                d[g] = acc;
-            }
-#pragma unroll
-            for (int g = 0; g < G; ++g) {
-                d[g] += __shfl_xor_sync(0xffffffffu, d[g], 1);
-                d[g] += __shfl_xor_sync(0xffffffffu, d[g], 2);
-            }
-            if (q4 == 0 && r < n_rows) {
-                const float s = ksc[r] * inv_sqrt;
-#pragma unroll
-                for (int g = 0; g < G; ++g) sc[g * pps * kPage + r] = d[g] * s;
-            }
+        for (int w = 0; w < 2; ++w) {
+            uint8_t* dst = page + (w == 0 ? 0 : cbh) + (size_t)kh * CB + (size_t)slot * (DH / 2) + lane * E / 2;
+            if (E == 4) *reinterpret_cast<uint16_t*>(dst) = (uint16_t)word[w];
+            else *dst = (uint8_t)word[w];
+            if (lane == 0)
+                reinterpret_cast<float*>(page + 2 * cbh)[(w == 0 ? 0 : Hkv * kPage) + kh * kPage + slot] = scl[w];
         }
-    }
-    __syncthreads();
-    // softmax per head (warp g): max, p = exp(s - max), sum
-    if (warp < G) {
-        float* sg = sc + warp * pps * kPage;
-        float m = -1e30f;
-        for (int r = lane; r < n_rows; r += 32) m = fmaxf(m, sg[r]);
-        m = warp_max(m);
-        float l = 0.f;
-        for (int r = lane; r < npg * kPage; r += 32) {
-            const float p = r < n_rows ? expf(sg[r] - m) : 0.f;
-            sg[r] = p * (r < n_rows ? vsc[r] : 0.f);  // p * s_v: the row's weight on its V codes
-            l += p;
+        mbar_wait(bar, 0);  // the pages have landed; the new row replaces its stale shared copy
+#pragma unroll
+        for (int w = 0; w < 2; ++w) {
+            uint8_t* d = (w == 0 ? kc : vc) + (size_t)new_r * (DH / 2) + lane * E / 2;
+            if (E == 4) *reinterpret_cast<uint16_t*>(d) = (uint16_t)word[w];
+            else *d = (uint8_t)word[w];
         }
-        l = warp_sum(l);
         if (lane == 0) {
-            stat[2 * warp] = m;
-            stat[2 * warp + 1] = l;
+            ksc[new_r] = scl[0];
+            vsc[new_r] = scl[1];
+        }
+        __syncwarp();
+    } else {
+        mbar_wait(bar, 0);  // the split's pages have landed
+    }
+
+    const int q4 = lane & 3, quad = lane >> 2;
+    // scores of this warp's rows (every G head per converted K row) and their running max
+    float mx[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) mx[g] = -1e30f;
+    for (int ci = warp; ci < n_chunks; ci += 8) {
+        const int r = ((ci + c_rot) % n_chunks) * 8 + quad;
+        float kf[CPL];
+        const uint8_t* kr = kc + (size_t)r * (DH / 2) + q4 * (CPL / 2);
+        if constexpr (CPL == 32) {
+            const uint4 w = *reinterpret_cast<const uint4*>(kr);
+            nib8_to_f32(w.x, kf); nib8_to_f32(w.y, kf + 8); nib8_to_f32(w.z, kf + 16); nib8_to_f32(w.w, kf + 24);
+        } else {
+            const uint2 w = *reinterpret_cast<const uint2*>(kr);
+            nib8_to_f32(w.x, kf); nib8_to_f32(w.y, kf + 8);
+        }
+        const bool ok = r < n_rows;
+        const float ksr = ok ? ksc[r] * inv_sqrt : 0.f;
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            const float4* qv = reinterpret_cast<const float4*>(qs + g * QLD + q4 * (CPL + 4));
+            float d = 0.f;
+#pragma unroll
+            for (int c = 0; c < CPL / 4; ++c) {
+                const float4 qq = qv[c];
+                d = fmaf(qq.x, kf[4 * c], d);
+                d = fmaf(qq.y, kf[4 * c + 1], d);
+                d = fmaf(qq.z, kf[4 * c + 2], d);
+                d = fmaf(qq.w, kf[4 * c + 3], d);
+            }
+            d += __shfl_xor_sync(0xffffffffu, d, 1);
+            d += __shfl_xor_sync(0xffffffffu, d, 2);
+            const float s = d * ksr;
+            if (ok) {
+                mx[g] = fmaxf(mx[g], s);
+                if (q4 == 0) sc[g * pps * kPage + r] = s;
+            }
+        }
+    }
+    __syncwarp();  // the warp's scores are in shared memory
+    // P . V over the warp's rows, one head at a time (acc: this lane's CPL channels)
+    for (int g = 0; g < G; ++g) {
+        const float m = warp_max(mx[g]);
+        const float* sg = sc + g * pps * kPage;
+        float acc[CPL];
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) acc[c] = 0.f;
+        float l = 0.f;
+        for (int ci = warp; ci < n_chunks; ci += 8) {
+            const int r = ((ci + c_rot) % n_chunks) * 8 + quad;
+            if (r >= n_rows) continue;
+            const float p = expf(sg[r] - m);
+            if (q4 == 0) l += p;
+            const float pv = p * vsc[r];
+            float vf[CPL];
+            const uint8_t* vr = vc + (size_t)r * (DH / 2) + q4 * (CPL / 2);
+            if constexpr (CPL == 32) {
+                const uint4 w = *reinterpret_cast<const uint4*>(vr);
+                nib8_to_f32(w.x, vf); nib8_to_f32(w.y, vf + 8); nib8_to_f32(w.z, vf + 16); nib8_to_f32(w.w, vf + 24);
+            } else {
+                const uint2 w = *reinterpret_cast<const uint2*>(vr);
+                nib8_to_f32(w.x, vf); nib8_to_f32(w.y, vf + 8);
+            }
+#pragma unroll
+            for (int c = 0; c < CPL; ++c) acc[c] = fmaf(pv, vf[c], acc[c]);
+        }
+        // the 8 quads of the warp hold partial sums of the same channels
+#pragma unroll
+        for (int o = 4; o < 32; o <<= 1)
+#pragma unroll
+            for (int c = 0; c < CPL; ++c) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o);
+        l = warp_sum(l);
+        if (quad == 0) {
+            float4* dst = reinterpret_cast<float4*>(red + ((size_t)warp * G + g) * DH + q4 * CPL);
+#pragma unroll
+            for (int c = 0; c < CPL / 4; ++c) dst[c] = make_float4(acc[4 * c], acc[4 * c + 1], acc[4 * c + 2], acc[4 * c + 3]);
+        }
+        if (lane == 0) {
+            stat[(warp * G + g) * 2] = m;
+            stat[(warp * G + g) * 2 + 1] = l;
         }
     }
     __syncthreads();
-    // P . V: thread (row group rg, word column wc) accumulates 8 channels x G heads
-    {
-        const int wc = tid % WC, rg = tid / WC;
-        float acc[G][8];
-#pragma unroll
-        for (int g = 0; g < G; ++g)
-#pragma unroll
-            for (int e = 0; e < 8; ++e) acc[g][e] = 0.f;
-        for (int r = rg; r < n_rows; r += NRG) {
-            float vf[8];
-            nib8_to_f32(*reinterpret_cast<const uint32_t*>(vc + (size_t)r * (DH / 2) + wc * 4), vf);
-#pragma unroll
-            for (int g = 0; g < G; ++g) {
-                const float pv = sc[g * pps * kPage + r];
-#pragma unroll
-                for (int e = 0; e < 8; ++e) acc[g][e] = fmaf(pv, vf[e], acc[g][e]);
-            }
-        }
-        // row groups within the warp (lanes differing above the word-column bits), then warps
-#pragma unroll
-        for (int o = WC; o < 32; o <<= 1)
-#pragma unroll
-            for (int g = 0; g < G; ++g)
-#pragma unroll
-                for (int e = 0; e < 8; ++e) acc[g][e] += __shfl_xor_sync(0xffffffffu, acc[g][e], o);
-        if (lane < WC) {
-#pragma unroll
-            for (int g = 0; g < G; ++g) {
-                float4* dst = reinterpret_cast<float4*>(red + ((size_t)warp * G + g) * DH + wc * 8);
-                dst[0] = make_float4(acc[g][0], acc[g][1], acc[g][2], acc[g][3]);
-                dst[1] = make_float4(acc[g][4], acc[g][5], acc[g][6], acc[g][7]);
-            }
-        }
-    }
-    __syncthreads();
+    // combine the 8 warps' (max, sum, o) per head, in fixed warp order
     for (int i = tid; i < G * DH; i += AD_THREADS) {
         const int g = i / DH, c = i % DH;
-        float o = 0.f;
+        float M = -1e30f;
 #pragma unroll
-        for (int w = 0; w < 8; ++w) o += red[((size_t)w * G + g) * DH + c];
-        part_o[(pidx0 + (size_t)g * nsplit) * DH + c] = o;
+        for (int w = 0; w < 8; ++w)
+            if (stat[(w * G + g) * 2 + 1] > 0.f) M = fmaxf(M, stat[(w * G + g) * 2]);
+        float o = 0.f, L = 0.f;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+            const float lw = stat[(w * G + g) * 2 + 1];
+            const float a = lw > 0.f ? expf(stat[(w * G + g) * 2] - M) : 0.f;
+            o += red[((size_t)w * G + g) * DH + c] * a;
+            L += lw * a;
+        }
+        if (row) {  // one split: the head's final output (o / L, as k_attn_merge_quant computes it)
+            const float ov = o * (1.f / L);
+            row[((size_t)b * H + kh * G + g) * DH + c] = ov;
+            atomicMax(reinterpret_cast<int*>(stat) + 16 * G + g, __float_as_int(fabsf(ov)));
+        } else {
+            part_o[(pidx0 + (size_t)g * nsplit) * DH + c] = o;
+            if (c == 0) {
+                part_ml[(pidx0 + (size_t)g * nsplit) * 2] = M;
+                part_ml[(pidx0 + (size_t)g * nsplit) * 2 + 1] = L;
+            }
+        }
     }
-    if (tid < G) {
-        part_ml[(pidx0 + (size_t)tid * nsplit) * 2] = stat[2 * tid];
-        part_ml[(pidx0 + (size_t)tid * nsplit) * 2 + 1] = stat[2 * tid + 1];
+    if (!row) return;
+    // The attn_out site quantizer (model.cpp:394,539) by the sequence's last kv-head CTA: every
+    // CTA publishes its heads' rows and max |o|; the last to arrive quantizes the whole row
+    // (k_attn_merge_quant's arithmetic), then resets the counter for the next graph replay.
+    __shared__ unsigned s_last;
+    __syncthreads();
+    if (tid < G) hmax[(size_t)b * H + kh * G + tid] = __int_as_float(reinterpret_cast<int*>(stat)[16 * G + tid]);
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = atomicAdd(&cnt[b], 1u) == (unsigned)Hkv - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (tid == 0) cnt[b] = 0;
+    double sq = static_scale;
+    if (qmode != 0) {
+        __shared__ float s_mx[8];
+        float m = 0.f;
+        for (int h = tid; h < H; h += AD_THREADS) m = fmaxf(m, __ldcg(hmax + (size_t)b * H + h));
+        m = warp_max(m);
+        if (lane == 0) s_mx[warp] = m;
+        __syncthreads();
+        m = s_mx[0];
+#pragma unroll
+        for (int w = 1; w < 8; ++w) m = fmaxf(m, s_mx[w]);
+        sq = q_scale((double)m, qmax);
     }
+    const double inv_s = 1.0 / sq;
+    const int HD = H * DH;
+    for (int w = tid; w < d_pad / 8; w += AD_THREADS) {
+        int cw[8];
+        if (w * 8 < HD) {
+            const float4 a = __ldcg(reinterpret_cast<const float4*>(row + (size_t)b * HD + w * 8));
+            const float4 bq = __ldcg(reinterpret_cast<const float4*>(row + (size_t)b * HD + w * 8 + 4));
+            const float f[8] = {a.x, a.y, a.z, a.w, bq.x, bq.y, bq.z, bq.w};
+#pragma unroll
+            for (int e = 0; e < 8; ++e) cw[e] = q_code_r((double)f[e], sq, inv_s, qmax);
+        } else {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) cw[e] = 0;
+        }
+        *reinterpret_cast<uint32_t*>(codes + w4t_offset(b, w * 4, ld_codes)) = pack8(cw);
+    }
+    if (tid == 0) scales[b] = sq;
 }
 
 // Merge the split partials of every head of one sequence (fixed split order) and,
@@ -392,12 +466,15 @@ __global__ void __launch_bounds__(1024) k_attn_merge_quant(const float* __restri
 template <int DH, int G>
 static int launch_dec(dim3 grid, int pps, cudaStream_t st, const float* qkv, int ldq, int H, int Hkv,
                       const int* kv_len, uint8_t* pool, long long page_bytes, const int* pt, int max_pages,
-                      const double2* rope, const int* pos, float inv_sqrt, float* part_ml, float* part_o) {
+                      const double2* rope, const int* pos, float inv_sqrt, float* part_ml, float* part_o,
+                      float* row, float* hmax, unsigned* cnt, uint8_t* codes, int ld_codes, double* scales,
+                      int qmode, double static_scale, int d_pad, int qmax) {
     const size_t smem = AdSmem<DH, G>::total(pps);
     auto kfn = k_attn_dec<DH, G>;
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     return launch_pdl(kfn, grid, dim3(AD_THREADS), smem, st, qkv, ldq, H, Hkv, kv_len, pool, page_bytes, pt,
-                      max_pages, pps, rope, pos, inv_sqrt, part_ml, part_o);
+                      max_pages, pps, rope, pos, inv_sqrt, part_ml, part_o, row, hmax, cnt, codes, ld_codes, scales,
+                      qmode, static_scale, d_pad, qmax);
 }
 
 }  // namespace qt
@@ -408,8 +485,8 @@ extern "C" {
 
 int qt_attn_decode_plan(int B, int Hkv, int pages, int sms, int* pps, int* nsplit) {
     if (pages < 1 || B < 1) return -1;
-    // enough CTAs for two per SM, at most AD_MAX_PPS pages each
-    int ns = std::max(1, std::min(pages, (2 * sms + B * Hkv - 1) / (B * Hkv)));
+    // enough CTAs for one per SM, at most AD_MAX_PPS pages each
+    int ns = std::max(1, std::min(pages, (sms + B * Hkv - 1) / (B * Hkv)));
     int p = (pages + ns - 1) / ns;
     if (p > AD_MAX_PPS) p = AD_MAX_PPS;
     ns = (pages + p - 1) / p;
@@ -422,7 +499,7 @@ int qt_launch_attn_decode(const float* qkv, int ldq, int H, int Hkv, int dh, con
                           uint8_t* pool, long long page_bytes, const int* pt, int max_pages, int pps, int nsplit,
                           const double* rope, const int* pos, float* part_ml, float* part_o, float* out, int ldo,
                           uint8_t* codes, int ld_codes, double* scales, int qmode, double static_scale, int d_pad,
-                          int bits, cudaStream_t st) {
+                          int bits, float* row, float* hmax, unsigned* counters, cudaStream_t st) {
     if (B <= 0) return 0;
     if (H > 64 || Hkv < 1 || H % Hkv || H / Hkv > AD_MAX_G || pps < 1 || pps > AD_MAX_PPS || nsplit < 1) return -1;
     // (the last split may extend past the page table: only pages holding cached rows are read)
@@ -430,16 +507,21 @@ int qt_launch_attn_decode(const float* qkv, int ldq, int H, int Hkv, int dh, con
     const dim3 grid(nsplit, Hkv, B);
     const float inv_sqrt = (float)(1.0 / sqrt((double)dh));
     const double2* rt = reinterpret_cast<const double2*>(rope);
+    const int qmax = (1 << (bits - 1)) - 1;
+    // one split + the attn_out codes wanted: the quantizer runs in the attention kernel's last
+    // kv-head CTA per sequence (no merge launch); scratch: row [B x H*dh], hmax [B x H], counters [B]
+    const bool fused_q = nsplit == 1 && codes && !out && row && hmax && counters;
+    float* rw = fused_q ? row : nullptr;
     int rc = -1;
 #define QT_AD(D, GG)                                                                                           \
     if (dh == D && G == GG)                                                                                    \
         rc = launch_dec<D, GG>(grid, pps, st, qkv, ldq, H, Hkv, kv_len, pool, page_bytes, pt, max_pages, rt, pos, \
-                               inv_sqrt, part_ml, part_o);
+                               inv_sqrt, part_ml, part_o, rw, hmax, counters, codes, ld_codes, scales, qmode,        \
+                               static_scale, d_pad, qmax);
     QT_AD(128, 1) QT_AD(128, 2) QT_AD(128, 4) QT_AD(128, 7) QT_AD(128, 8)
     QT_AD(64, 1) QT_AD(64, 2) QT_AD(64, 4) QT_AD(64, 7) QT_AD(64, 8)
 #undef QT_AD
-    if (rc) return rc;
-    const int qmax = (1 << (bits - 1)) - 1;
+    if (rc || fused_q) return rc;
     if (dh == 128) {
         auto mk = H > 32 ? k_attn_merge_quant<128, 64> : k_attn_merge_quant<128, 32>;
         return launch_pdl(mk, dim3(B), dim3(1024), 0, st, (const float*)part_ml, (const float*)part_o, nsplit, H,

@@ -838,9 +838,23 @@ int qt_tc05_i8_splitk(int M, int N, int K) {
     return (KB + kbs - 1) / kbs;  // no empty slice
 }
 
+extern "C" int qt_launch_w4a4_tc05_i8_ex(int epi, const int8_t* A8, int lda8, const double* sa, const int8_t* W8,
+                                         int w_rows, int ldw8, const double* sw, int M, int N, int K, void* out,
+                                         int ldo, int* acc_dbg, float* pmax, int pmax_ld, int* n_part, int* ws,
+                                         int force_single, cudaStream_t st);
+
 extern "C" int qt_launch_w4a4_tc05_i8(int epi, const int8_t* A8, int lda8, const double* sa, const int8_t* W8,
                                       int w_rows, int ldw8, const double* sw, int M, int N, int K, void* out, int ldo,
                                       int* acc_dbg, float* pmax, int pmax_ld, int* n_part, int* ws, cudaStream_t st) {
+    return qt_launch_w4a4_tc05_i8_ex(epi, A8, lda8, sa, W8, w_rows, ldw8, sw, M, N, K, out, ldo, acc_dbg, pmax,
+                                     pmax_ld, n_part, ws, 0, st);
+}
+
+// force_single: the single-CTA 128 x 256 kernel at any M (A/B measurements, qt_w4a4_gemm_i8)
+extern "C" int qt_launch_w4a4_tc05_i8_ex(int epi, const int8_t* A8, int lda8, const double* sa, const int8_t* W8,
+                                         int w_rows, int ldw8, const double* sw, int M, int N, int K, void* out,
+                                         int ldo, int* acc_dbg, float* pmax, int pmax_ld, int* n_part, int* ws,
+                                         int force_single, cudaStream_t st) {
     using namespace qt;
     if (n_part) *n_part = 0;
     if (M <= 0) return 0;
@@ -852,7 +866,7 @@ extern "C" int qt_launch_w4a4_tc05_i8(int epi, const int8_t* A8, int lda8, const
     if (pmax && parts > pmax_ld) pmax = nullptr;
     if (pmax && n_part) *n_part = parts;
     CUtensorMap ta, tb;
-    const bool pair = M > T5_BM;
+    const bool pair = M > T5_BM && !force_single;
     if (qt_tmap_i8(&ta, A8, M, K, lda8, T5_BM) || qt_tmap_i8(&tb, W8, w_rows, K, ldw8, pair ? 128 : T5_BN))
         return -2;
     if (pair) {

@@ -49,6 +49,9 @@ int qt_launch_w4a4_tc05_i8(int epi, const int8_t* A8, int lda8, const double* sa
 // ws (nullable): int32 split-K workspace of qt_tc05_i8_splitk(M, N, K) * M * N entries (the 2-SM kernel
 // splits K when its 256 x 256 tiles would leave CTA pairs idle: decode batches of 129..256 tokens)
 int qt_tc05_i8_splitk(int M, int N, int K);
+int qt_launch_w4a4_tc05_i8_ex(int epi, const int8_t* A8, int lda8, const double* sa, const int8_t* W8, int w_rows,
+                              int ldw8, const double* sw, int M, int N, int K, void* out, int ldo, int* acc_dbg,
+                              float* pmax, int pmax_ld, int* n_part, int* ws, int force_single, cudaStream_t st);
 int qt_launch_w4t_to_i8(const uint8_t* tiled, int rows_pad, int K, int8_t* out, cudaStream_t st);
 int qt_launch_w4a4_mma_ex(int epi, const uint8_t* A, int lda, const double* sa, const uint8_t* W, int ldw,
                           const double* sw, int M, int N, int K, void* out, int ldo, int* acc_dbg, float* pmax,
@@ -89,7 +92,9 @@ int qt_launch_attn_decode(const float* qkv, int ldq, int H, int Hkv, int dh, con
                           uint8_t* pool, long long page_bytes, const int* pt, int max_pages, int pps, int nsplit,
                           const double* rope, const int* pos, float* part_ml, float* part_o, float* out, int ldo,
                           uint8_t* codes, int ld_codes, double* scales, int qmode, double static_scale, int d_pad,
-                          int bits, cudaStream_t st);
+                          int bits, float* row, float* hmax, unsigned* counters, cudaStream_t st);
+// (nsplit == 1 with codes and row / hmax / counters (zeroed once) given: the attn_out quantizer
+// runs in the attention kernel itself, by the last kv-head CTA of each sequence)
 int qt_launch_select_topk(const double* mag, const double* res, const float* inter, const float* intra, int H,
                           int vstride, const int* vis, const int* txt, const int* budget, const int* old_off,
                           const int* new_off, int B, int vmax, const double* w4, int* keep_src, int* keep_local,
