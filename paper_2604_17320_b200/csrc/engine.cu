@@ -1121,10 +1121,11 @@ struct qt_engine {
         pm_parts = 0;
         pm_ptr = atomic_pm ? pm_atomic : pmax;
         pm_ld = atomic_pm ? 1 : kPmaxLd;
-        // > 128 tokens: the 2-SM int8-operand tcgen05 GEMM (split-K when its tiles underfill the SM
-        // pairs: decode batches up to 256); 65..128: the packed-int4 tcgen05 GEMM with split-K; the
-        // weight-streaming GEMV up to 64 tokens (decode batches)
-        int rc = (use_tc05 && M > 128 && codes8 && w8)
+        // > 256 tokens: the int8-operand tcgen05 GEMM (TMA); 65..256: the packed-int4 tcgen05 GEMM
+        // with split-K across CTAs (decode batches: streams the int4 weights, half the int8 copy's
+        // bytes; measured faster than the int8 kernel at 256 tokens); the weight-streaming GEMV up
+        // to 64 tokens (decode batches)
+        int rc = (use_tc05 && M > 256 && codes8 && w8)
                      ? qt_launch_w4a4_tc05_i8(epi, codes8, ld8, ascale, w8, wrows, K, sw, M, N, K, out, ldo, nullptr, pm,
                                               kPmaxLd, &pm_parts, splitk_ws, st)
                  : (use_tc05 && M > 64)

@@ -824,7 +824,7 @@ extern "C" int qt_launch_w4t_to_i8(const uint8_t* tiled, int rows_pad, int K, in
 }
 
 // A8: int8 activations [>= M rows x K], row stride lda8; W8: int8 weights [w_rows x K], stride ldw8.
-// M > 128: the 2-SM (CTA pair, cta_group::2) kernel on 256 x 256 tiles; else the single-CTA one.
+// M >= 8192: the 2-SM (CTA pair, cta_group::2) kernel on 256 x 256 tiles; else the single-CTA one.
 int qt_tc05_i8_splitk(int M, int N, int K) {
     // the 2-SM kernel's k slices: enough work units for every CTA pair, >= 4 k blocks per slice
     int sms = 148;
@@ -866,7 +866,9 @@ extern "C" int qt_launch_w4a4_tc05_i8_ex(int epi, const int8_t* A8, int lda8, co
     if (pmax && parts > pmax_ld) pmax = nullptr;
     if (pmax && n_part) *n_part = parts;
     CUtensorMap ta, tb;
-    const bool pair = M > T5_BM && !force_single;
+    // CTA pairs only pay for the largest token counts (measured, tools/bench_gemm.py: pair 2880 vs
+    // single 2774 TOPS at 8192^3, but 1582 vs 2004 on the 7B QKV GEMM at M = 1896)
+    const bool pair = M >= 8192 && !force_single;
     if (qt_tmap_i8(&ta, A8, M, K, lda8, T5_BM) || qt_tmap_i8(&tb, W8, w_rows, K, ldw8, pair ? 128 : T5_BN))
         return -2;
     if (pair) {
