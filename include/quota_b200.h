@@ -180,6 +180,16 @@ int qt_engine_prefill_rows(qt_engine* e);
  * emb [n_seq x d_model], logits_out [n_seq x d_model]. */
 int qt_engine_decode(qt_engine* e, const float* emb, int emb_on_device, float* logits_out, int out_on_device);
 int qt_engine_decode_f64(qt_engine* e, const double* emb, int emb_on_device, float* logits_out, int out_on_device);
+/* Greedy decoding (BASELINE.json configs: "128 greedy steps").  An extension: the reference's
+ * decode_step takes the next token's embedding (model.hpp:177-180) and its head is d_model wide
+ * (model.hpp:63), so a token is an index into the logits and the caller supplies a
+ * token-embedding table [vocab x d_model] fp32, vocab <= d_model.
+ * qt_engine_decode_greedy runs one decode_step for every sequence of the last prefill with
+ * input table[argmax(previous logits[0..vocab))] (the prefill's last row for the first step;
+ * ties to the smaller token id); the argmax + embedding kernel is part of the step's CUDA
+ * graph.  tokens_out: host int [n_seq] (nullable), logits_out as qt_engine_decode. */
+int qt_engine_set_token_table(qt_engine* e, const float* table, int vocab, int on_device);
+int qt_engine_decode_greedy(qt_engine* e, int* tokens_out, float* logits_out, int out_on_device);
 
 /* Introspection (parity tests, reports). */
 int qt_engine_layout(qt_engine* e, int seq, int* visual, int* text, int* positions, int cap);

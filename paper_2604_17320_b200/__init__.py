@@ -106,6 +106,8 @@ def lib():
                                       C.c_int, vp, C.c_int, vp, vp, C.c_int, vp]
         L.qt_w4a4_gemm_i8_workspace.restype = C.c_int64
         L.qt_w4a4_gemm_i8_workspace.argtypes = [C.c_int, C.c_int, C.c_int]
+        L.qt_engine_set_token_table.argtypes = [vp, vp, C.c_int, C.c_int]
+        L.qt_engine_decode_greedy.argtypes = [vp, vp, vp, C.c_int]
         L.qt_engine_capture.argtypes = [vp, C.c_int]
         L.qt_engine_capture_count.argtypes = [vp]
         L.qt_engine_capture_get.argtypes = [vp, C.c_int, ip, vp, dp]
@@ -355,6 +357,20 @@ class Engine:
         out = np.empty((emb.shape[0], self.cfg.d_model), dtype=np.float32) if logits_out is None else logits_out
         check(lib().qt_engine_decode(self.h, _ptr(emb), on_dev, _ptr(out), _on_device(out)))
         return out
+
+    def set_token_table(self, table):
+        """Token-embedding table [vocab x d_model] fp32 (numpy or CUDA torch) for decode_greedy."""
+        on_dev = _on_device(table)
+        t = np.ascontiguousarray(table, dtype=np.float32) if isinstance(table, np.ndarray) else table.contiguous()
+        check(lib().qt_engine_set_token_table(self.h, _ptr(t), t.shape[0], on_dev))
+
+    def decode_greedy(self, logits_out=None, tokens_out=None):
+        """One greedy step for every sequence: returns (tokens [B] int32 numpy, logits)."""
+        B = self.info()["batch"]
+        out = np.empty((B, self.cfg.d_model), dtype=np.float32) if logits_out is None else logits_out
+        tok = np.empty(B, dtype=np.int32) if tokens_out is None else tokens_out
+        check(lib().qt_engine_decode_greedy(self.h, _ptr(tok), _ptr(out), _on_device(out)))
+        return tok, out
 
     def layout(self, seq):
         v, t = C.c_int(), C.c_int()

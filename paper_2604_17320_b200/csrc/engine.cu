@@ -261,6 +261,14 @@ struct qt_engine {
     int n_sms = 148;
     cudaGraphExec_t graph = nullptr;
     bool graph_ok = false;
+    // greedy decoding (qt_engine_decode_greedy): token-embedding table [vocab x d] fp32, the step's
+    // tokens [max_batch], the prefill's last row per sequence; its own graph (argmax + embed first)
+    float* tok_table = nullptr;
+    int vocab = 0;
+    int* dec_tok = nullptr;
+    int* last_rows = nullptr;
+    cudaGraphExec_t graph_g = nullptr;
+    bool graph_g_ok = false;
     int decode_steps = 0;
 
     // host staging (pinned)
@@ -353,6 +361,7 @@ struct qt_engine {
         if (cst) cudaStreamSynchronize(cst);  // a pending async logits readback still reads `logits`
         cudaStreamSynchronize(st ? st : 0);
         if (graph) cudaGraphExecDestroy(graph);
+        if (graph_g) cudaGraphExecDestroy(graph_g);
         auto f = [](void* p) {
             if (p) cudaFree(p);
         };
@@ -371,6 +380,7 @@ struct qt_engine {
         f(fp_head);
         if (blas) cublasDestroy(blas);
         f(splitk_ws); f(codes8); f(head8); f(pmax); f(gmax); f(probs_d); f(dec_hmax); f(dec_cnt);
+        f(tok_table); f(dec_tok); f(last_rows);
         if (pin) cudaFreeHost(pin);
         if (cst) {
             cudaStreamSynchronize(cst);
@@ -1594,9 +1604,16 @@ struct qt_engine {
             dec_splits = std::max(dec_splits, dec_lsplit[l]);
         }
         (void)maxp;
+        if (tok_table) {  // the greedy decoding's first argmax reads the prefill's last row per sequence
+            std::vector<int> lr(B);
+            for (int b = 0; b < B; ++b) lr[b] = off[b + 1] - 1;
+            upload(last_rows, lr);
+            ckl(qt_launch_copy_rows_f32(logits, last_rows, d, dlogits, B, st), "last logits rows");
+        }
         ck(cudaStreamSynchronize(st), "prefill");
         decode_steps = 0;
         prefilled = true;
+        graph_ok = graph_g_ok = false;
         finish_profile();
     }
 
@@ -1720,15 +1737,25 @@ struct qt_engine {
         return (double)ms / reps;
     }
 
-    void decode(const void* emb, int emb_dev, int emb_f64, float* out, int out_dev) {
+    // emb == nullptr: a greedy step (the input is the embedding of the argmax of the previous logits)
+    void decode(const void* emb, int emb_dev, int emb_f64, float* out, int out_dev, int* tokens_out = nullptr) {
         if (!prefilled) fail(QT_ERUNTIME, "cache and execution mode mismatch");
         if (decode_steps >= max_decode) fail(QT_EINVAL, "decode steps exceed engine capacity");
+        const bool greedy = emb == nullptr;
+        if (greedy && !tok_table) fail(QT_EINVAL, "greedy decoding needs a token-embedding table");
         const bool profiling = prof_next;
         if (profiling) {
             prof = std::make_unique<Profiler>();
             prof->st = st;
         }
-        if (emb_f64) {
+        auto greedy_in = [&]() {
+            pb(P_OTHER);
+            ckl(qt_launch_greedy_next(dlogits, d, vocab, tok_table, d, xd, dec_tok, B, st), "greedy argmax + embed");
+            pe((double)B * d * 4 * 2 + (double)B * d * 8);
+        };
+        if (greedy) {
+            // the argmax + embedding kernel is the first node of the greedy graph
+        } else if (emb_f64) {
             ck(cudaMemcpyAsync(xd, emb, (size_t)B * d * sizeof(double),
                                emb_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st),
                "decode emb");
@@ -1742,15 +1769,19 @@ struct qt_engine {
             ckl(qt_launch_f32_to_f64(xd_in, xd, (long long)B * d, st), "embedding widen");
             pe((double)B * d * 12);
         }
+        cudaGraphExec_t& gx = greedy ? graph_g : graph;
+        bool& gx_ok = greedy ? graph_g_ok : graph_ok;
         if (profiling || capture) {
+            if (greedy) greedy_in();
             decode_body();  // eager launches so every kernel gets its own events / capture reads
-        } else if (!graph_ok) {
-            if (graph) cudaGraphExecDestroy(graph);
-            graph = nullptr;
+        } else if (!gx_ok) {
+            if (gx) cudaGraphExecDestroy(gx);
+            gx = nullptr;
             cudaGraph_t g = nullptr;
             ck(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "graph capture");
             g_capturing = true;
             try {
+                if (greedy) greedy_in();
                 decode_body();
             } catch (...) {
                 g_capturing = false;
@@ -1760,11 +1791,13 @@ struct qt_engine {
             }
             g_capturing = false;
             ck(cudaStreamEndCapture(st, &g), "graph capture end");
-            ck(cudaGraphInstantiate(&graph, g, 0), "graph instantiate");
+            ck(cudaGraphInstantiate(&gx, g, 0), "graph instantiate");
             cudaGraphDestroy(g);
-            graph_ok = true;
+            gx_ok = true;
         }
-        if (!profiling && !capture) ck(cudaGraphLaunch(graph, st), "graph launch");
+        if (!profiling && !capture) ck(cudaGraphLaunch(gx, st), "graph launch");
+        if (greedy && tokens_out)
+            ck(cudaMemcpyAsync(tokens_out, dec_tok, (size_t)B * sizeof(int), cudaMemcpyDeviceToHost, st), "tokens");
         if (out)
             ck(cudaMemcpyAsync(out, dlogits, (size_t)B * d * sizeof(float),
                                out_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st),
@@ -2244,6 +2277,28 @@ int qt_engine_decode(qt_engine* e, const float* emb, int emb_on_device, float* l
         if (!emb) fail(QT_EINVAL, "embedding width mismatch");
         e->decode(emb, emb_on_device, 0, logits_out, out_on_device);
     });
+}
+
+int qt_engine_set_token_table(qt_engine* e, const float* table, int vocab, int on_device) {
+    return guard([&] {
+        if (vocab < 1 || vocab > e->d) fail(QT_EINVAL, "vocab must be in [1, d_model] (the logits' width)");
+        if (!table) fail(QT_EINVAL, "null token table");
+        ck(cudaStreamSynchronize(e->st), "sync");
+        if (e->tok_table) cudaFree(e->tok_table);
+        e->tok_table = dalloc<float>((size_t)vocab * e->d);
+        if (!e->dec_tok) e->dec_tok = dalloc<int>(e->max_batch);
+        if (!e->last_rows) e->last_rows = dalloc<int>(e->max_batch);
+        ck(cudaMemcpyAsync(e->tok_table, table, (size_t)vocab * e->d * sizeof(float),
+                           on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, e->st),
+           "token table");
+        ck(cudaStreamSynchronize(e->st), "token table");
+        e->vocab = vocab;
+        e->graph_g_ok = false;
+    });
+}
+
+int qt_engine_decode_greedy(qt_engine* e, int* tokens_out, float* logits_out, int out_on_device) {
+    return guard([&] { e->decode(nullptr, 0, 0, logits_out, out_on_device, tokens_out); });
 }
 
 int qt_engine_decode_f64(qt_engine* e, const double* emb, int emb_on_device, float* logits_out, int out_on_device) {

@@ -239,6 +239,66 @@ __global__ void k_metrics_pack(const double* __restrict__ mag, const double* __r
     }
 }
 
+// Greedy decoding input (an extension: the reference's decode_step takes the next token's
+// embedding, model.hpp:177-180): per sequence, token = argmax of its previous logits over the
+// first `vocab` entries (ties to the smaller id, as std::max_element / numpy argmax), then that
+// row of the token-embedding table, widened to the fp64 residual, is the step's input.  grid B.
+__global__ void __launch_bounds__(256) k_greedy_next(const float* __restrict__ logits, int ld, int vocab,
+                                                     const float* __restrict__ table, int d, double* __restrict__ x,
+                                                     int* __restrict__ tokens) {
+    __shared__ float sv[8];
+    __shared__ int si[8];
+    __shared__ int s_tok;
+    pdl_launch_dependents();
+    pdl_wait();  // the logits come from the previous step's head GEMV
+    const int b = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const float* lg = logits + (size_t)b * ld;
+    float bv = -INFINITY;
+    int bi = 0x7fffffff;
+    for (int i = threadIdx.x; i < vocab; i += blockDim.x) {
+        const float v = lg[i];
+        if (v > bv) {  // strided ascending scan: the first maximum of this thread's indices
+            bv = v;
+            bi = i;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > bv || (ov == bv && oi < bi)) {
+            bv = ov;
+            bi = oi;
+        }
+    }
+    if (lane == 0) {
+        sv[warp] = bv;
+        si[warp] = bi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float v = sv[0];
+        int id = si[0];
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+            if (sv[w] > v || (sv[w] == v && si[w] < id)) {
+                v = sv[w];
+                id = si[w];
+            }
+        s_tok = id < vocab ? id : 0;
+        tokens[b] = s_tok;
+    }
+    __syncthreads();
+    const float* row = table + (size_t)s_tok * d;
+    for (int j = threadIdx.x; j < d; j += blockDim.x) x[(size_t)b * d + j] = (double)row[j];
+}
+
+// dst[b] = src[rows[b]] (fp32 rows of width d): the last prefill logits row of each sequence
+__global__ void k_copy_rows_f32(const float* __restrict__ src, const int* __restrict__ rows, int d,
+                                float* __restrict__ dst) {
+    const int b = blockIdx.x;
+    for (int j = threadIdx.x; j < d; j += blockDim.x) dst[(size_t)b * d + j] = src[(size_t)rows[b] * d + j];
+}
+
 // x_new[j] = x_old[src[j]], pos_new[j] = pos_old[src[j]]
 __global__ void k_gather_rows(const double* __restrict__ x, double* __restrict__ xn, int D,
                               const int* __restrict__ pos, int* __restrict__ posn, const int* __restrict__ src, int M) {
@@ -314,6 +374,18 @@ int qt_launch_metrics_pack(const double* mag, const double* res, const float* in
                            int vstride, const int* vis, int B, double* metrics, cudaStream_t st) {
     if (B <= 0) return 0;
     k_metrics_pack<<<B, 256, 0, st>>>(mag, res, inter, intra, H, vstride, vis, metrics);
+    return (int)cudaGetLastError();
+}
+
+int qt_launch_greedy_next(const float* logits, int ld, int vocab, const float* table, int d, double* x, int* tokens,
+                          int B, cudaStream_t st) {
+    if (B <= 0) return 0;
+    return launch_pdl(k_greedy_next, dim3(B), dim3(256), 0, st, logits, ld, vocab, table, d, x, tokens);
+}
+
+int qt_launch_copy_rows_f32(const float* src, const int* rows, int d, float* dst, int B, cudaStream_t st) {
+    if (B <= 0) return 0;
+    k_copy_rows_f32<<<B, 256, 0, st>>>(src, rows, d, dst);
     return (int)cudaGetLastError();
 }
 

@@ -105,6 +105,10 @@ int qt_launch_gather_rows(const double* x, double* xn, int D, const int* pos, in
 int qt_launch_kv_compact(uint8_t* pool, long long page_bytes, const int* pt, int max_pages, int Hkv, int dh,
                          const int* keep_local, int kl_stride, const int* new_len, int B, cudaStream_t st);
 int qt_launch_kv_len_bump(int* kv_len, int n, int* next_pos, int B, cudaStream_t st);
+// greedy decoding: token = argmax(logits[b][0..vocab)), x[b] = (double) table[token]
+int qt_launch_greedy_next(const float* logits, int ld, int vocab, const float* table, int d, double* x, int* tokens,
+                          int B, cudaStream_t st);
+int qt_launch_copy_rows_f32(const float* src, const int* rows, int d, float* dst, int B, cudaStream_t st);
 // tiled int4 codes -> row-major int8 [rows x K]
 int qt_launch_unpack_codes(const uint8_t* tiled, int rows_pad, int rows, int K, int8_t* out, cudaStream_t st);
 // per-head fp32 column sums + fp64 token metrics -> metrics [B][4][vstride] (mag, inter, intra, res),

@@ -200,3 +200,37 @@ def test_async_logits_readback(pair):
         e.prefill(torch.from_numpy(emb2).pin_memory(), [30], [10], logits_out=p2, logits_async=True)
         e.synchronize()  # the returned rows are valid only now
         assert np.array_equal(p1.numpy(), ref) and np.array_equal(p2.numpy(), ref2)
+
+
+def test_greedy_decode_matches_restatement(torch_cuda):
+    """Greedy decoding (BASELINE.json "greedy steps"): token = argmax of the previous logits
+    (ties to the smaller id), input = its row of a token-embedding table -- the GPU's tokens equal
+    the restatement driven the same way (numpy argmax of its fp64 logits), and so do the logits."""
+    cfg = O.ModelCfg(n_layers=4, d_model=256, n_heads=4, n_kv_heads=2, d_head=64, d_ff=688, mlp=1, act_mode=1,
+                     weight_axis=2)
+    w = O.synth_weights(cfg, seed=21)
+    port = O.Port(cfg)
+    port.set_weights(w)
+    port.prepare(None)
+    table = O.synth_embeddings(200, 256, seed=77)  # vocab 200 <= d_model
+    e = Q.Engine(Q.Config(n_layers=4, d_model=256, n_heads=4, n_kv_heads=2, d_head=64, d_ff=688, mlp=1, act_mode=1),
+                 max_batch=2, max_tokens=512, max_seq=256, max_decode=12)
+    e.load_weights(w)
+    e.set_token_table(table.astype(np.float32))
+    rec = O.Recipe([1, 2], [0.5, 0.3], v0=144)
+    e.set_recipe(rec.candidate_layers, rec.keep_ratios, rec.weights, rec.v0, 4)
+    embs = [O.synth_embeddings(184, 256, seed=13), O.synth_embeddings(150, 256, seed=14)]
+    lg = e.prefill(np.concatenate(embs).astype(np.float32), [144, 110], [40, 40])
+    runs = [port.prefill(embs[0], 144, 40, rec), port.prefill(embs[1], 110, 40, rec)]
+    last = [r.result().logits[-1] for r in runs]
+    for step in range(12):
+        tok, g = e.decode_greedy()
+        for b in range(2):
+            prev = last[b][:200]
+            exp_tok = int(np.argmax(prev))
+            top2 = np.sort(prev)[-2:]
+            if top2[1] - top2[0] < 1e-5:  # a near-tie argmax: the sequences may legitimately part
+                return
+            assert tok[b] == exp_tok, (step, b, tok[b], exp_tok)
+            last[b] = runs[b].decode(table[exp_tok])
+            assert np.abs(g[b].astype(np.float64) - last[b]).max() <= 1e-2
