@@ -332,6 +332,19 @@ def run_ours(args, cfg):
     emb_d, dec_d = emb_h.to(dev), dec_h.to(dev)
     logits_d = torch.empty(rows, d, device=dev)
     dlog_d = torch.empty(B, d, device=dev)
+    greedy = not args.teacher_forced
+    if greedy:  # the configs' "greedy steps": argmax token -> a seeded token-embedding table [d x d]
+        gt = torch.Generator(device="cpu").manual_seed(55)
+        table = torch.randn(d, d, generator=gt)
+        table[:, torch.randperm(d, generator=gt)[:max(1, int(round(cfg["outlier"] * d)))]] *= 20.0
+        eng.set_token_table(table.to(dev))
+    tok_d = torch.zeros(D, B, dtype=torch.int32, device=dev)
+
+    def decode_step(t, logits_out, tokens_out=None):
+        if greedy:
+            eng.decode_greedy(logits_out=logits_out, tokens_out=tokens_out if tokens_out is not None else tok_d[t])
+        else:
+            eng.decode(dec_d[t] if logits_out.is_cuda else dec_p[t], logits_out=logits_out)
     txt = [T] * B
     gathered = torch.empty(ws * B, d, device=dev) if ws > 1 else None
 
@@ -343,13 +356,14 @@ def run_ours(args, cfg):
     def step_device():
         eng.prefill(emb_d, vis, txt, v0=v0s, logits_out=logits_d)
         for t in range(D):
-            eng.decode(dec_d[t], logits_out=dlog_d)
+            decode_step(t, dlog_d)
         gather_outputs()
 
     # e2e: pinned host buffers through the public API, copies inside the timed region
     emb_p, dec_p = emb_h.pin_memory(), dec_h.pin_memory()
     logits_p = torch.empty(rows, d).pin_memory()
     dlog_p = torch.empty(D, B, d).pin_memory()
+    tok_p = torch.zeros(D, B, dtype=torch.int32).pin_memory()
     gathered_p = torch.empty(ws * B, d).pin_memory() if ws > 1 else None
 
     def step_e2e():
@@ -357,7 +371,10 @@ def run_ours(args, cfg):
         # join_copies() puts their completion back on the timed stream before the step ends
         eng.prefill(emb_p, vis, txt, v0=v0s, logits_out=logits_p, logits_async=True)
         for t in range(D):
-            eng.decode(dec_p[t], logits_out=dlog_p[t] if t < D - 1 else dlog_d)
+            if greedy:  # each step's tokens to the host; the logits stay on the device but the last
+                decode_step(t, dlog_d, tok_p[t])
+            else:
+                decode_step(t, dlog_p[t] if t < D - 1 else dlog_d)
         with torch.cuda.stream(stream):
             dlog_p[D - 1].copy_(dlog_d, non_blocking=True)
             if dist is not None:  # the gathered final logits land in rank 0's host memory
@@ -402,7 +419,7 @@ def run_ours(args, cfg):
     eng.prefill(emb_d, vis, txt, v0=v0s, logits_out=logits_d)
     ev[1].record(stream)
     for t in range(D):
-        eng.decode(dec_d[t], logits_out=dlog_d)
+        decode_step(t, dlog_d)
     ev[2].record(stream)
     stream.synchronize()
     prefill_ms = ev[0].elapsed_time(ev[1])
@@ -417,7 +434,7 @@ def run_ours(args, cfg):
     eng.prefill(emb_d, vis, txt, v0=v0s, logits_out=logits_d)
     prof_pre = eng.profile_read()
     eng.profile_next()
-    eng.decode(dec_d[0], logits_out=dlog_d)
+    decode_step(0, dlog_d)
     prof_dec = eng.profile_read()
     # per-class decode time inside the CUDA graph (PDL overlap, real launch overheads): the
     # step replayed with only one kernel class left in (per-launch events break both)
@@ -503,7 +520,11 @@ def run_ours(args, cfg):
             "config": {"workload": cfg["workload"], "batch_per_gpu": B, "global_batch": ws * B,
                        "visual": V if len(set(vis)) == 1 else {"ragged": list(cfg["visual"]), "mean": float(np.mean(vis))},
                        "text": T,
-                       "decode_steps": D, "recipe": {"candidate_layers": cfg["layers"], "keep_ratios": cfg["keeps"],
+                       "decode_steps": D,
+                       "decode": "teacher-forced (seeded step embeddings)" if not greedy else
+                       "greedy: argmax over the d_model-wide logits -> row of a seeded token-embedding table "
+                       "[d x d] (SURVEY.md 0.1; the argmax + embedding kernel is in the step's CUDA graph)",
+                       "recipe": {"candidate_layers": cfg["layers"], "keep_ratios": cfg["keeps"],
                                                      "v0": cfg["v0"]},
                        "layers": cfg["n_layers"], "d_model": d, "heads": cfg["n_heads"], "d_ff": cfg["d_ff"],
                        "parallelism": f"dp{ws} (batch sharded, NCCL gather of outputs only)",
@@ -515,9 +536,9 @@ def run_ours(args, cfg):
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_val, "unit": UNIT, "ms_per_step": ms_e2e,
-                    "h2d_bytes_per_step": int(emb_p.numel() * 4 + dec_p.numel() * 4),
-                    "d2h_bytes_per_step": int(final_rows * d * 4 + D * B * d * 4 +
-                                              (ws * B * d * 4 if ws > 1 else 0)),
+                    "h2d_bytes_per_step": int(emb_p.numel() * 4 + (0 if greedy else dec_p.numel() * 4)),
+                    "d2h_bytes_per_step": int(final_rows * d * 4 + (D * B * 4 + B * d * 4 if greedy else D * B * d * 4)
+                                              + (ws * B * d * 4 if ws > 1 else 0)),
                     "per_rank": True, "gather": "final decode logits of all ws x B sequences to rank 0 host"
                     if ws > 1 else None},
             "gpu_launches": int(sum(v["launches"] for v in prof_pre.values())
@@ -585,6 +606,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference", "stub"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--teacher-forced", action="store_true",
+                    help="decode with seeded step embeddings instead of greedy argmax tokens")
     ap.add_argument("--batch", type=int, default=None, help="override the config's per-GPU batch (c5 sweep)")
     ap.add_argument("--decode", type=int, default=None, help="override the config's decode steps (c5 sweep)")
     args = ap.parse_args()

@@ -187,7 +187,7 @@ int qt_engine_decode_f64(qt_engine* e, const double* emb, int emb_on_device, flo
  * qt_engine_decode_greedy runs one decode_step for every sequence of the last prefill with
  * input table[argmax(previous logits[0..vocab))] (the prefill's last row for the first step;
  * ties to the smaller token id); the argmax + embedding kernel is part of the step's CUDA
- * graph.  tokens_out: host int [n_seq] (nullable), logits_out as qt_engine_decode. */
+ * graph.  tokens_out: int [n_seq], host or device (nullable); logits_out as qt_engine_decode. */
 int qt_engine_set_token_table(qt_engine* e, const float* table, int vocab, int on_device);
 int qt_engine_decode_greedy(qt_engine* e, int* tokens_out, float* logits_out, int out_on_device);
 

@@ -1797,7 +1797,7 @@ struct qt_engine {
         }
         if (!profiling && !capture) ck(cudaGraphLaunch(gx, st), "graph launch");
         if (greedy && tokens_out)
-            ck(cudaMemcpyAsync(tokens_out, dec_tok, (size_t)B * sizeof(int), cudaMemcpyDeviceToHost, st), "tokens");
+            ck(cudaMemcpyAsync(tokens_out, dec_tok, (size_t)B * sizeof(int), cudaMemcpyDefault, st), "tokens");
         if (out)
             ck(cudaMemcpyAsync(out, dlogits, (size_t)B * d * sizeof(float),
                                out_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st),
