@@ -27,6 +27,19 @@
 
 namespace qt {
 
+// Build-time alternatives, fixed by measurement (tools/gpu_attn_ab.sh):
+//   QT_AD_KERNEL   1: per-warp chunks for G == 1, two-phase for G > 1; 2: two-phase always
+//   QT_AD_CTAS     CTAs per SM the split plan aims for
+//   QT_AD_FUSEQ    1: the attn_out quantizer in the attention kernel when one split suffices
+#ifndef QT_AD_KERNEL
+#define QT_AD_KERNEL 1
+#endif
+#ifndef QT_AD_CTAS
+#define QT_AD_CTAS 1
+#endif
+#ifndef QT_AD_FUSEQ
+#define QT_AD_FUSEQ 1
+#endif
 constexpr int AD_THREADS = 256;
 constexpr int AD_MAX_PPS = 8;  // pages per split (smem: 8.5 KB each at d_head 128)
 constexpr int AD_MAX_G = 8;    // query heads per kv head (one softmax warp each)
@@ -365,6 +378,245 @@ __global__ void __launch_bounds__(AD_THREADS) k_attn_dec(const float* __restrict
     if (tid == 0) scales[b] = sq;
 }
 
+template <int DH, int G>
+__global__ void __launch_bounds__(AD_THREADS) k_attn_dec_2p(const float* __restrict__ qkv, int ldq, int H, int Hkv,
+                                                         const int* __restrict__ kv_len, uint8_t* __restrict__ pool,
+                                                         long long page_bytes, const int* __restrict__ pt,
+                                                         int max_pages, int pps, const double2* __restrict__ rope,
+                                                         const int* __restrict__ pos, float inv_sqrt,
+                                                         float* __restrict__ part_ml, float* __restrict__ part_o,
+                                                         float* __restrict__, float* __restrict__, unsigned* __restrict__,
+                                                         uint8_t* __restrict__, int, double* __restrict__, int, double,
+                                                         int, int) {
+    using S = AdSmem<DH, G>;
+    constexpr int CB = S::CB, QLD = S::QLD;
+    constexpr int CPL = DH / 4;    // channels per lane in the score phase
+    constexpr int WC = DH / 8;     // 32-bit words (8 codes) per row
+    constexpr int NRG = AD_THREADS / WC;  // row groups in the PV phase
+    extern __shared__ __align__(128) uint8_t sm[];
+    uint8_t* kc = sm + S::kc(pps);
+    uint8_t* vc = sm + S::vc(pps);
+    float* ksc = reinterpret_cast<float*>(sm + S::ks(pps));
+    float* vsc = reinterpret_cast<float*>(sm + S::vs(pps));
+    float* qs = reinterpret_cast<float*>(sm + S::q(pps));
+    float* sc = reinterpret_cast<float*>(sm + S::sc(pps));
+    float* red = reinterpret_cast<float*>(sm + S::red(pps));
+    float* stat = reinterpret_cast<float*>(sm + S::stat(pps));
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + S::bar(pps));
+
+    pdl_launch_dependents();
+    const int split = blockIdx.x, nsplit = gridDim.x, kh = blockIdx.y, b = blockIdx.z;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const bool fused = rope != nullptr;
+    // kv_len and the page table are final since the previous step (or the host upload):
+    // read before the dependency wait, like the cached rows themselves
+    const int old_len = kv_len[b];
+    const int len = old_len + (fused ? 1 : 0);
+    const int r0 = split * pps * kPage;
+    const int n_rows = min(pps * kPage, len - r0);
+    const size_t pidx0 = ((size_t)b * H + (size_t)kh * G) * nsplit + split;
+    if (n_rows <= 0) {  // nothing cached in this split: an empty partial per head
+        pdl_wait();     // the partial buffers are still read by the previous layer's merge
+        for (int i = tid; i < G * DH; i += AD_THREADS) part_o[(pidx0 + (size_t)(i / DH) * nsplit) * DH + i % DH] = 0.f;
+        if (tid < G) {
+            part_ml[(pidx0 + (size_t)tid * nsplit) * 2] = -1e30f;
+            part_ml[(pidx0 + (size_t)tid * nsplit) * 2 + 1] = 0.f;
+        }
+        return;
+    }
+    const int npg = (n_rows + kPage - 1) / kPage;
+    const size_t cbh = (size_t)Hkv * CB;  // K codes of all kv heads in a page
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    if (tid == 0) {
+        mbar_arrive_expect_tx(bar, (uint32_t)npg * (2 * CB + 2 * kPage * 4));
+        for (int p = 0; p < npg; ++p) {
+            const uint8_t* page = pool + (long long)pt[b * max_pages + split * pps + p] * page_bytes;
+            bulk_g2s(kc + (size_t)p * CB, page + (size_t)kh * CB, CB, bar);
+            bulk_g2s(vc + (size_t)p * CB, page + cbh + (size_t)kh * CB, CB, bar);
+            bulk_g2s(ksc + p * kPage, page + 2 * cbh + (size_t)kh * kPage * 4, kPage * 4, bar);
+            bulk_g2s(vsc + p * kPage, page + 2 * cbh + ((size_t)Hkv + kh) * kPage * 4, kPage * 4, bar);
+        }
+    }
+    pdl_wait();  // q (and the new token's k / v) come from the upstream GEMV
+
+    // q of the G heads -> smem (RoPE'd here in the decode step: fp64, rounded to fp32 like
+    // the prefill's k_rope_kv_append)
+    const float* qrow = qkv + (size_t)b * ldq;
+    const double2* rt = fused ? rope + (size_t)pos[b] * (DH / 2) : nullptr;
+    for (int i = tid; i < G * DH / 2; i += AD_THREADS) {
+        const int g = i / (DH / 2), pr = i % (DH / 2);
+        const float2 v = *reinterpret_cast<const float2*>(qrow + (size_t)(kh * G + g) * DH + 2 * pr);
+        float2 o = v;
+        if (fused) {
+            const double2 cs = rt[pr];
+            const double a = v.x, bb = v.y;
+            o.x = (float)__dsub_rn(__dmul_rn(a, cs.x), __dmul_rn(bb, cs.y));
+            o.y = (float)__dadd_rn(__dmul_rn(a, cs.y), __dmul_rn(bb, cs.x));
+        }
+        const int c = 2 * pr;
+        float* dst = qs + g * QLD + (c / CPL) * (CPL + 4) + c % CPL;
+        dst[0] = o.x;
+        dst[1] = o.y;
+    }
+    // the new row (decode step): warp 0 its K (RoPE'd), warp 1 its V -- kv_quantize in fp64
+    const int new_r = old_len - r0;  // row within this split
+    const bool has_new = fused && new_r >= 0 && new_r < n_rows;
+    constexpr int E = DH / 32;
+    uint32_t new_word = 0;
+    float new_scale = 0.f;
+    if (has_new && warp < 2) {
+        const bool is_k = warp == 0;
+        const float* src = qrow + (is_k ? H * DH : (H + Hkv) * DH) + kh * DH + lane * E;
+        double val[E];
+#pragma unroll
+        for (int j = 0; j < E; ++j) val[j] = (double)src[j];
+        if (is_k) {
+#pragma unroll
+            for (int j = 0; j < E; j += 2) {
+                const double2 cs = rt[(lane * E + j) / 2];
+                const double a = val[j], bb = val[j + 1];
+                val[j] = __dsub_rn(__dmul_rn(a, cs.x), __dmul_rn(bb, cs.y));
+                val[j + 1] = __dadd_rn(__dmul_rn(a, cs.y), __dmul_rn(bb, cs.x));
+            }
+        }
+        double mx = 0.0;
+#pragma unroll
+        for (int j = 0; j < E; ++j) mx = fmax(mx, fabs(val[j]));
+        mx = warp_max(mx);
+        const double s = q_scale(mx, 7), inv_s = 1.0 / s;
+#pragma unroll
+        for (int j = 0; j < E; ++j) new_word |= (uint32_t)(q_code_r(val[j], s, inv_s, 7) & 0xF) << (4 * j);
+        new_scale = (float)s;
+        // append to the cache (model.cpp:499-501)
+        uint8_t* page = pool + (long long)pt[b * max_pages + old_len / kPage] * page_bytes;
+        const int slot = old_len % kPage;
+        uint8_t* dst = page + (is_k ? 0 : cbh) + (size_t)kh * CB + (size_t)slot * (DH / 2) + lane * E / 2;
+        if (E == 4) *reinterpret_cast<uint16_t*>(dst) = (uint16_t)new_word;
+        else *dst = (uint8_t)new_word;
+        if (lane == 0)
+            reinterpret_cast<float*>(page + 2 * cbh)[(is_k ? 0 : Hkv * kPage) + kh * kPage + slot] = new_scale;
+    }
+    mbar_wait(bar, 0);  // the split's pages have landed
+    if (has_new && warp < 2) {  // ... and the new row replaces its (stale) shared copy
+        uint8_t* d = (warp == 0 ? kc : vc) + (size_t)new_r * (DH / 2) + lane * E / 2;
+        if (E == 4) *reinterpret_cast<uint16_t*>(d) = (uint16_t)new_word;
+        else *d = (uint8_t)new_word;
+        if (lane == 0) (warp == 0 ? ksc : vsc)[new_r] = new_scale;
+    }
+    __syncthreads();
+
+    // scores: 4 lanes per row, CPL channels each; all G heads per converted row
+    {
+        const int q4 = lane & 3;
+        for (int r = warp * 8 + (lane >> 2); r < npg * kPage; r += 64) {
+            float kf[CPL];
+            const uint8_t* kr = kc + (size_t)r * (DH / 2) + q4 * (CPL / 2);
+            if constexpr (CPL == 32) {
+                const uint4 w = *reinterpret_cast<const uint4*>(kr);
+                nib8_to_f32(w.x, kf); nib8_to_f32(w.y, kf + 8); nib8_to_f32(w.z, kf + 16); nib8_to_f32(w.w, kf + 24);
+            } else {
+                const uint2 w = *reinterpret_cast<const uint2*>(kr);
+                nib8_to_f32(w.x, kf); nib8_to_f32(w.y, kf + 8);
+            }
+            float d[G];
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                const float4* qv = reinterpret_cast<const float4*>(qs + g * QLD + q4 * (CPL + 4));
+                float acc = 0.f;
+#pragma unroll
+                for (int c = 0; c < CPL / 4; ++c) {
+                    const float4 qq = qv[c];
+                    acc = fmaf(qq.x, kf[4 * c], acc);
+                    acc = fmaf(qq.y, kf[4 * c + 1], acc);
+                    acc = fmaf(qq.z, kf[4 * c + 2], acc);
+                    acc = fmaf(qq.w, kf[4 * c + 3], acc);
+                }
+                d[g] = acc;
+            }
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                d[g] += __shfl_xor_sync(0xffffffffu, d[g], 1);
+                d[g] += __shfl_xor_sync(0xffffffffu, d[g], 2);
+            }
+            if (q4 == 0 && r < n_rows) {
+                const float s = ksc[r] * inv_sqrt;
+#pragma unroll
+                for (int g = 0; g < G; ++g) sc[g * pps * kPage + r] = d[g] * s;
+            }
+        }
+    }
+    __syncthreads();
+    // softmax per head (warp g): max, p = exp(s - max), sum
+    if (warp < G) {
+        float* sg = sc + warp * pps * kPage;
+        float m = -1e30f;
+        for (int r = lane; r < n_rows; r += 32) m = fmaxf(m, sg[r]);
+        m = warp_max(m);
+        float l = 0.f;
+        for (int r = lane; r < npg * kPage; r += 32) {
+            const float p = r < n_rows ? expf(sg[r] - m) : 0.f;
+            sg[r] = p * (r < n_rows ? vsc[r] : 0.f);  // p * s_v: the row's weight on its V codes
+            l += p;
+        }
+        l = warp_sum(l);
+        if (lane == 0) {
+            stat[2 * warp] = m;
+            stat[2 * warp + 1] = l;
+        }
+    }
+    __syncthreads();
+    // P . V: thread (row group rg, word column wc) accumulates 8 channels x G heads
+    {
+        const int wc = tid % WC, rg = tid / WC;
+        float acc[G][8];
+#pragma unroll
+        for (int g = 0; g < G; ++g)
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc[g][e] = 0.f;
+        for (int r = rg; r < n_rows; r += NRG) {
+            float vf[8];
+            nib8_to_f32(*reinterpret_cast<const uint32_t*>(vc + (size_t)r * (DH / 2) + wc * 4), vf);
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                const float pv = sc[g * pps * kPage + r];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) acc[g][e] = fmaf(pv, vf[e], acc[g][e]);
+            }
+        }
+        // row groups within the warp (lanes differing above the word-column bits), then warps
+#pragma unroll
+        for (int o = WC; o < 32; o <<= 1)
+#pragma unroll
+            for (int g = 0; g < G; ++g)
+#pragma unroll
+                for (int e = 0; e < 8; ++e) acc[g][e] += __shfl_xor_sync(0xffffffffu, acc[g][e], o);
+        if (lane < WC) {
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                float4* dst = reinterpret_cast<float4*>(red + ((size_t)warp * G + g) * DH + wc * 8);
+                dst[0] = make_float4(acc[g][0], acc[g][1], acc[g][2], acc[g][3]);
+                dst[1] = make_float4(acc[g][4], acc[g][5], acc[g][6], acc[g][7]);
+            }
+        }
+    }
+    __syncthreads();
+    for (int i = tid; i < G * DH; i += AD_THREADS) {
+        const int g = i / DH, c = i % DH;
+        float o = 0.f;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) o += red[((size_t)w * G + g) * DH + c];
+        part_o[(pidx0 + (size_t)g * nsplit) * DH + c] = o;
+    }
+    if (tid < G) {
+        part_ml[(pidx0 + (size_t)tid * nsplit) * 2] = stat[2 * tid];
+        part_ml[(pidx0 + (size_t)tid * nsplit) * 2 + 1] = stat[2 * tid + 1];
+    }
+}
+
 // Merge the split partials of every head of one sequence (fixed split order) and,
 // optionally, quantize the concatenated attention row (the attn_out site,
 // model.cpp:394/539) in the same kernel.  grid B, 1024 threads: warp w merges heads
@@ -470,7 +722,7 @@ static int launch_dec(dim3 grid, int pps, cudaStream_t st, const float* qkv, int
                       float* row, float* hmax, unsigned* cnt, uint8_t* codes, int ld_codes, double* scales,
                       int qmode, double static_scale, int d_pad, int qmax) {
     const size_t smem = AdSmem<DH, G>::total(pps);
-    auto kfn = k_attn_dec<DH, G>;
+    auto kfn = (QT_AD_KERNEL == 1 && G == 1) ? k_attn_dec<DH, G> : k_attn_dec_2p<DH, G>;
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     return launch_pdl(kfn, grid, dim3(AD_THREADS), smem, st, qkv, ldq, H, Hkv, kv_len, pool, page_bytes, pt,
                       max_pages, pps, rope, pos, inv_sqrt, part_ml, part_o, row, hmax, cnt, codes, ld_codes, scales,
@@ -486,7 +738,7 @@ extern "C" {
 int qt_attn_decode_plan(int B, int Hkv, int pages, int sms, int* pps, int* nsplit) {
     if (pages < 1 || B < 1) return -1;
     // enough CTAs for one per SM, at most AD_MAX_PPS pages each
-    int ns = std::max(1, std::min(pages, (sms + B * Hkv - 1) / (B * Hkv)));
+    int ns = std::max(1, std::min(pages, (QT_AD_CTAS * sms + B * Hkv - 1) / (B * Hkv)));
     int p = (pages + ns - 1) / ns;
     if (p > AD_MAX_PPS) p = AD_MAX_PPS;
     ns = (pages + p - 1) / p;
@@ -510,7 +762,8 @@ int qt_launch_attn_decode(const float* qkv, int ldq, int H, int Hkv, int dh, con
     const int qmax = (1 << (bits - 1)) - 1;
     // one split + the attn_out codes wanted: the quantizer runs in the attention kernel's last
     // kv-head CTA per sequence (no merge launch); scratch: row [B x H*dh], hmax [B x H], counters [B]
-    const bool fused_q = nsplit == 1 && codes && !out && row && hmax && counters;
+    const bool fused_q = QT_AD_FUSEQ && (QT_AD_KERNEL == 1 && Hkv == H) && nsplit == 1 && codes && !out && row &&
+                         hmax && counters;
     float* rw = fused_q ? row : nullptr;
     int rc = -1;
 #define QT_AD(D, GG)                                                                                           \
