@@ -14,10 +14,8 @@
 // since earlier steps, so the copies overlap the upstream QKV GEMV.  After the wait the
 // CTA whose split holds the new row RoPEs and quantizes that token's K / V (fp64, the
 // reference's arithmetic) and appends them to the cache and to its shared copy.  Scores
-// and probabilities are fp32, 4 lanes per row
-// (8-row chunks per warp: scores with every G head per converted K row, then P . V per head,
-// each warp on its own rows with no block barrier; the 8 warps' states are combined at the
-// end) produce one (max, sum, unnormalised o) partial per (sequence, query head, split);
+// (4 lanes per row, fp32), a per-head softmax, then P . V (16 word columns x 16 row groups)
+// produce one (max, sum, unnormalised o) partial per (sequence, query head, split);
 // k_attn_merge_quant merges the splits in fixed order and quantizes the attn_out site.
 // int4 -> fp32 without I2F: float(0x4B000000 | (nib ^ 8)) - (2^23 + 8) is exact.
 #include <algorithm>
@@ -27,19 +25,6 @@
 
 namespace qt {
 
-// Build-time alternatives, fixed by measurement (tools/gpu_attn_ab.sh):
-//   QT_AD_KERNEL   1: per-warp chunks for G == 1, two-phase for G > 1; 2: two-phase always
-//   QT_AD_CTAS     CTAs per SM the split plan aims for
-//   QT_AD_FUSEQ    1: the attn_out quantizer in the attention kernel when one split suffices
-#ifndef QT_AD_KERNEL
-#define QT_AD_KERNEL 1
-#endif
-#ifndef QT_AD_CTAS
-#define QT_AD_CTAS 1
-#endif
-#ifndef QT_AD_FUSEQ
-#define QT_AD_FUSEQ 1
-#endif
 constexpr int AD_THREADS = 256;
 constexpr int AD_MAX_PPS = 8;  // pages per split (smem: 8.5 KB each at d_head 128)
 constexpr int AD_MAX_G = 8;    // query heads per kv head (one softmax warp each)
@@ -55,8 +40,6 @@ template <int DH, int G>
 struct AdSmem {
     static constexpr int CB = kPage * (DH / 2);  // code bytes per (page, kv head, K|V)
     static constexpr int QLD = DH + 16;           // padded q row (the 4 quarter slices hit distinct banks)
-    // shared: the split's K / V codes and scales, q, scores [G][rows], per-warp partial o
-    // [8][G][DH] and (max, sum) [8][G], the pages' mbarrier
     QT_HD static size_t kc(int) { return 0; }
     QT_HD static size_t vc(int pps) { return (size_t)pps * CB; }
     QT_HD static size_t ks(int pps) { return (size_t)2 * pps * CB; }
@@ -65,7 +48,7 @@ struct AdSmem {
     QT_HD static size_t sc(int pps) { return q(pps) + (size_t)G * QLD * 4; }
     QT_HD static size_t red(int pps) { return sc(pps) + (size_t)G * pps * kPage * 4; }
     QT_HD static size_t stat(int pps) { return red(pps) + (size_t)8 * G * DH * 4; }
-    QT_HD static size_t bar(int pps) { return (stat(pps) + 8 * G * 8 + G * 4 + 15) / 16 * 16; }
+    QT_HD static size_t bar(int pps) { return (stat(pps) + G * 8 + 15) / 16 * 16; }
     QT_HD static size_t total(int pps) { return bar(pps) + 16; }
 };
 
@@ -78,316 +61,7 @@ __global__ void __launch_bounds__(AD_THREADS) k_attn_dec(const float* __restrict
                                                          long long page_bytes, const int* __restrict__ pt,
                                                          int max_pages, int pps, const double2* __restrict__ rope,
                                                          const int* __restrict__ pos, float inv_sqrt,
-                                                         float* __restrict__ part_ml, float* __restrict__ part_o,
-                                                         float* __restrict__ row, float* __restrict__ hmax,
-                                                         unsigned* __restrict__ cnt, uint8_t* __restrict__ codes,
-                                                         int ld_codes, double* __restrict__ scales, int qmode,
-                                                         double static_scale, int d_pad, int qmax) {
-    using S = AdSmem<DH, G>;
-    constexpr int CB = S::CB, QLD = S::QLD;
-    constexpr int CPL = DH / 4;    // channels per lane in the score phase
-    constexpr int WC = DH / 8;     // 32-bit words (8 codes) per row
-    constexpr int NRG = AD_THREADS / WC;  // row groups in the PV phase
-    extern __shared__ __align__(128) uint8_t sm[];
-    uint8_t* kc = sm + S::kc(pps);
-    uint8_t* vc = sm + S::vc(pps);
-    float* ksc = reinterpret_cast<float*>(sm + S::ks(pps));
-    float* vsc = reinterpret_cast<float*>(sm + S::vs(pps));
-    float* qs = reinterpret_cast<float*>(sm + S::q(pps));
-    float* sc = reinterpret_cast<float*>(sm + S::sc(pps));
-    float* red = reinterpret_cast<float*>(sm + S::red(pps));
-    float* stat = reinterpret_cast<float*>(sm + S::stat(pps));
-    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + S::bar(pps));
-
-    pdl_launch_dependents();
-    const int split = blockIdx.x, nsplit = gridDim.x, kh = blockIdx.y, b = blockIdx.z;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const bool fused = rope != nullptr;
-    // kv_len and the page table are final since the previous step (or the host upload):
-    // read before the dependency wait, like the cached rows themselves
-    const int old_len = kv_len[b];
-    const int len = old_len + (fused ? 1 : 0);
-    const int r0 = split * pps * kPage;
-    const int n_rows = min(pps * kPage, len - r0);
-    const size_t pidx0 = ((size_t)b * H + (size_t)kh * G) * nsplit + split;
-    if (n_rows <= 0) {  // nothing cached in this split: an empty partial per head (never with row != null)
-        pdl_wait();     // the partial buffers are still read by the previous layer's merge
-        for (int i = tid; i < G * DH; i += AD_THREADS) part_o[(pidx0 + (size_t)(i / DH) * nsplit) * DH + i % DH] = 0.f;
-        if (tid < G) {
-            part_ml[(pidx0 + (size_t)tid * nsplit) * 2] = -1e30f;
-            part_ml[(pidx0 + (size_t)tid * nsplit) * 2 + 1] = 0.f;
-        }
-        return;
-    }
-    const int npg = (n_rows + kPage - 1) / kPage;
-    const size_t cbh = (size_t)Hkv * CB;  // K codes of all kv heads in a page
-    if (tid == 0) {
-        mbar_init(bar, 1);
-        mbar_fence_init();
-    }
-    __syncthreads();
-    if (tid == 0) {
-        mbar_arrive_expect_tx(bar, (uint32_t)npg * (2 * CB + 2 * kPage * 4));
-        for (int p = 0; p < npg; ++p) {
-            const uint8_t* page = pool + (long long)pt[b * max_pages + split * pps + p] * page_bytes;
-            bulk_g2s(kc + (size_t)p * CB, page + (size_t)kh * CB, CB, bar);
-            bulk_g2s(vc + (size_t)p * CB, page + cbh + (size_t)kh * CB, CB, bar);
-            bulk_g2s(ksc + p * kPage, page + 2 * cbh + (size_t)kh * kPage * 4, kPage * 4, bar);
-            bulk_g2s(vsc + p * kPage, page + 2 * cbh + ((size_t)Hkv + kh) * kPage * 4, kPage * 4, bar);
-        }
-    }
-    if (tid < G) reinterpret_cast<int*>(stat)[16 * G + tid] = 0;  // per-head max |o| (fused quantizer)
-    pdl_wait();  // q (and the new token's k / v) come from the upstream GEMV
-
-    // q of the G heads -> smem (RoPE'd here in the decode step: fp64, rounded to fp32 like
-    // the prefill's k_rope_kv_append)
-    const float* qrow = qkv + (size_t)b * ldq;
-    const double2* rt = fused ? rope + (size_t)pos[b] * (DH / 2) : nullptr;
-    for (int i = tid; i < G * DH / 2; i += AD_THREADS) {
-        const int g = i / (DH / 2), pr = i % (DH / 2);
-        const float2 v = *reinterpret_cast<const float2*>(qrow + (size_t)(kh * G + g) * DH + 2 * pr);
-        float2 o = v;
-        if (fused) {
-            const double2 cs = rt[pr];
-            const double a = v.x, bb = v.y;
-            o.x = (float)__dsub_rn(__dmul_rn(a, cs.x), __dmul_rn(bb, cs.y));
-            o.y = (float)__dadd_rn(__dmul_rn(a, cs.y), __dmul_rn(bb, cs.x));
-        }
-        const int c = 2 * pr;
-        float* dst = qs + g * QLD + (c / CPL) * (CPL + 4) + c % CPL;
-        dst[0] = o.x;
-        dst[1] = o.y;
-    }
-    __syncthreads();  // the only block barrier before the final combine
-    // Rows are processed in 8-row chunks, each chunk owned by one warp (4 lanes per row, CPL
-    // channels per lane); the chunk holding the new row is warp 0's, so only warp 0 depends on
-    // the append it performs itself.
-    const int new_r = old_len - r0;  // row within this split
-    const bool has_new = fused && new_r >= 0 && new_r < n_rows;
-    const int n_chunks = npg * (kPage / 8);
-    const int c_rot = has_new ? new_r / 8 : 0;
-    if (has_new && warp == 0) {
-        // the new row: kv_quantize (quant.cpp:117-119) of the RoPE'd K and of V, fp64
-        constexpr int E = DH / 32;
-        uint32_t word[2] = {0, 0};
-        float scl[2] = {0.f, 0.f};
-#pragma unroll
-        for (int w = 0; w < 2; ++w) {
-            const float* src = qrow + (w == 0 ? H * DH : (H + Hkv) * DH) + kh * DH + lane * E;
-            double val[E];
-#pragma unroll
-            for (int j = 0; j < E; ++j) val[j] = (double)src[j];
-            if (w == 0) {
-#pragma unroll
-                for (int j = 0; j < E; j += 2) {
-                    const double2 cs = rt[(lane * E + j) / 2];
-                    const double a = val[j], bb = val[j + 1];
-                    val[j] = __dsub_rn(__dmul_rn(a, cs.x), __dmul_rn(bb, cs.y));
-                    val[j + 1] = __dadd_rn(__dmul_rn(a, cs.y), __dmul_rn(bb, cs.x));
-                }
-            }
-            double mx = 0.0;
-#pragma unroll
-            for (int j = 0; j < E; ++j) mx = fmax(mx, fabs(val[j]));
-            mx = warp_max(mx);
-            const double sq = q_scale(mx, 7), inv_s = 1.0 / sq;
-#pragma unroll
-            for (int j = 0; j < E; ++j) word[w] |= (uint32_t)(q_code_r(val[j], sq, inv_s, 7) & 0xF) << (4 * j);
-            scl[w] = (float)sq;
-        }
-        // append to the cache (model.cpp:499-501)
-        uint8_t* page = pool + (long long)pt[b * max_pages + old_len / kPage] * page_bytes;
-        const int slot = old_len % kPage;
-#pragma unroll
-        for (int w = 0; w < 2; ++w) {
-            uint8_t* dst = page + (w == 0 ? 0 : cbh) + (size_t)kh * CB + (size_t)slot * (DH / 2) + lane * E / 2;
-            if (E == 4) *reinterpret_cast<uint16_t*>(dst) = (uint16_t)word[w];
-            else *dst = (uint8_t)word[w];
-            if (lane == 0)
-                reinterpret_cast<float*>(page + 2 * cbh)[(w == 0 ? 0 : Hkv * kPage) + kh * kPage + slot] = scl[w];
-        }
-        mbar_wait(bar, 0);  // the pages have landed; the new row replaces its stale shared copy
-#pragma unroll
-        for (int w = 0; w < 2; ++w) {
-            uint8_t* d = (w == 0 ? kc : vc) + (size_t)new_r * (DH / 2) + lane * E / 2;
-            if (E == 4) *reinterpret_cast<uint16_t*>(d) = (uint16_t)word[w];
-            else *d = (uint8_t)word[w];
-        }
-        if (lane == 0) {
-            ksc[new_r] = scl[0];
-            vsc[new_r] = scl[1];
-        }
-        __syncwarp();
-    } else {
-        mbar_wait(bar, 0);  // the split's pages have landed
-    }
-
-    const int q4 = lane & 3, quad = lane >> 2;
-    // scores of this warp's rows (every G head per converted K row) and their running max
-    float mx[G];
-#pragma unroll
-    for (int g = 0; g < G; ++g) mx[g] = -1e30f;
-    for (int ci = warp; ci < n_chunks; ci += 8) {
-        const int r = ((ci + c_rot) % n_chunks) * 8 + quad;
-        float kf[CPL];
-        const uint8_t* kr = kc + (size_t)r * (DH / 2) + q4 * (CPL / 2);
-        if constexpr (CPL == 32) {
-            const uint4 w = *reinterpret_cast<const uint4*>(kr);
-            nib8_to_f32(w.x, kf); nib8_to_f32(w.y, kf + 8); nib8_to_f32(w.z, kf + 16); nib8_to_f32(w.w, kf + 24);
-        } else {
-            const uint2 w = *reinterpret_cast<const uint2*>(kr);
-            nib8_to_f32(w.x, kf); nib8_to_f32(w.y, kf + 8);
-        }
-        const bool ok = r < n_rows;
-        const float ksr = ok ? ksc[r] * inv_sqrt : 0.f;
-#pragma unroll
-        for (int g = 0; g < G; ++g) {
-            const float4* qv = reinterpret_cast<const float4*>(qs + g * QLD + q4 * (CPL + 4));
-            float d = 0.f;
-#pragma unroll
-            for (int c = 0; c < CPL / 4; ++c) {
-                const float4 qq = qv[c];
-                d = fmaf(qq.x, kf[4 * c], d);
-                d = fmaf(qq.y, kf[4 * c + 1], d);
-                d = fmaf(qq.z, kf[4 * c + 2], d);
-                d = fmaf(qq.w, kf[4 * c + 3], d);
-            }
-            d += __shfl_xor_sync(0xffffffffu, d, 1);
-            d += __shfl_xor_sync(0xffffffffu, d, 2);
-            const float s = d * ksr;
-            if (ok) {
-                mx[g] = fmaxf(mx[g], s);
-                if (q4 == 0) sc[g * pps * kPage + r] = s;
-            }
-        }
-    }
-    __syncwarp();  // the warp's scores are in shared memory
-    // P . V over the warp's rows, one head at a time (acc: this lane's CPL channels)
-    for (int g = 0; g < G; ++g) {
-        const float m = warp_max(mx[g]);
-        const float* sg = sc + g * pps * kPage;
-        float acc[CPL];
-#pragma unroll
-        for (int c = 0; c < CPL; ++c) acc[c] = 0.f;
-        float l = 0.f;
-        for (int ci = warp; ci < n_chunks; ci += 8) {
-            const int r = ((ci + c_rot) % n_chunks) * 8 + quad;
-            if (r >= n_rows) continue;
-            const float p = expf(sg[r] - m);
-            if (q4 == 0) l += p;
-            const float pv = p * vsc[r];
-            float vf[CPL];
-            const uint8_t* vr = vc + (size_t)r * (DH / 2) + q4 * (CPL / 2);
-            if constexpr (CPL == 32) {
-                const uint4 w = *reinterpret_cast<const uint4*>(vr);
-                nib8_to_f32(w.x, vf); nib8_to_f32(w.y, vf + 8); nib8_to_f32(w.z, vf + 16); nib8_to_f32(w.w, vf + 24);
-            } else {
-                const uint2 w = *reinterpret_cast<const uint2*>(vr);
-                nib8_to_f32(w.x, vf); nib8_to_f32(w.y, vf + 8);
-            }
-#pragma unroll
-            for (int c = 0; c < CPL; ++c) acc[c] = fmaf(pv, vf[c], acc[c]);
-        }
-        // the 8 quads of the warp hold partial sums of the same channels
-#pragma unroll
-        for (int o = 4; o < 32; o <<= 1)
-#pragma unroll
-            for (int c = 0; c < CPL; ++c) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o);
-        l = warp_sum(l);
-        if (quad == 0) {
-            float4* dst = reinterpret_cast<float4*>(red + ((size_t)warp * G + g) * DH + q4 * CPL);
-#pragma unroll
-            for (int c = 0; c < CPL / 4; ++c) dst[c] = make_float4(acc[4 * c], acc[4 * c + 1], acc[4 * c + 2], acc[4 * c + 3]);
-        }
-        if (lane == 0) {
-            stat[(warp * G + g) * 2] = m;
-            stat[(warp * G + g) * 2 + 1] = l;
-        }
-    }
-    __syncthreads();
-    // combine the 8 warps' (max, sum, o) per head, in fixed warp order
-    for (int i = tid; i < G * DH; i += AD_THREADS) {
-        const int g = i / DH, c = i % DH;
-        float M = -1e30f;
-#pragma unroll
-        for (int w = 0; w < 8; ++w)
-            if (stat[(w * G + g) * 2 + 1] > 0.f) M = fmaxf(M, stat[(w * G + g) * 2]);
-        float o = 0.f, L = 0.f;
-#pragma unroll
-        for (int w = 0; w < 8; ++w) {
-            const float lw = stat[(w * G + g) * 2 + 1];
-            const float a = lw > 0.f ? expf(stat[(w * G + g) * 2] - M) : 0.f;
-            o += red[((size_t)w * G + g) * DH + c] * a;
-            L += lw * a;
-        }
-        if (row) {  // one split: the head's final output (o / L, as k_attn_merge_quant computes it)
-            const float ov = o * (1.f / L);
-            row[((size_t)b * H + kh * G + g) * DH + c] = ov;
-            atomicMax(reinterpret_cast<int*>(stat) + 16 * G + g, __float_as_int(fabsf(ov)));
-        } else {
-            part_o[(pidx0 + (size_t)g * nsplit) * DH + c] = o;
-            if (c == 0) {
-                part_ml[(pidx0 + (size_t)g * nsplit) * 2] = M;
-                part_ml[(pidx0 + (size_t)g * nsplit) * 2 + 1] = L;
-            }
-        }
-    }
-    if (!row) return;
-    // The attn_out site quantizer (model.cpp:394,539) by the sequence's last kv-head CTA: every
-    // CTA publishes its heads' rows and max |o|; the last to arrive quantizes the whole row
-    // (k_attn_merge_quant's arithmetic), then resets the counter for the next graph replay.
-    __shared__ unsigned s_last;
-    __syncthreads();
-    if (tid < G) hmax[(size_t)b * H + kh * G + tid] = __int_as_float(reinterpret_cast<int*>(stat)[16 * G + tid]);
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) s_last = atomicAdd(&cnt[b], 1u) == (unsigned)Hkv - 1;
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    if (tid == 0) cnt[b] = 0;
-    double sq = static_scale;
-    if (qmode != 0) {
-        __shared__ float s_mx[8];
-        float m = 0.f;
-        for (int h = tid; h < H; h += AD_THREADS) m = fmaxf(m, __ldcg(hmax + (size_t)b * H + h));
-        m = warp_max(m);
-        if (lane == 0) s_mx[warp] = m;
-        __syncthreads();
-        m = s_mx[0];
-#pragma unroll
-        for (int w = 1; w < 8; ++w) m = fmaxf(m, s_mx[w]);
-        sq = q_scale((double)m, qmax);
-    }
-    const double inv_s = 1.0 / sq;
-    const int HD = H * DH;
-    for (int w = tid; w < d_pad / 8; w += AD_THREADS) {
-        int cw[8];
-        if (w * 8 < HD) {
-            const float4 a = __ldcg(reinterpret_cast<const float4*>(row + (size_t)b * HD + w * 8));
-            const float4 bq = __ldcg(reinterpret_cast<const float4*>(row + (size_t)b * HD + w * 8 + 4));
-            const float f[8] = {a.x, a.y, a.z, a.w, bq.x, bq.y, bq.z, bq.w};
-#pragma unroll
-            for (int e = 0; e < 8; ++e) cw[e] = q_code_r((double)f[e], sq, inv_s, qmax);
-        } else {
-#pragma unroll
-            for (int e = 0; e < 8; ++e) cw[e] = 0;
-        }
-        *reinterpret_cast<uint32_t*>(codes + w4t_offset(b, w * 4, ld_codes)) = pack8(cw);
-    }
-    if (tid == 0) scales[b] = sq;
-}
-
-template <int DH, int G>
-__global__ void __launch_bounds__(AD_THREADS) k_attn_dec_2p(const float* __restrict__ qkv, int ldq, int H, int Hkv,
-                                                         const int* __restrict__ kv_len, uint8_t* __restrict__ pool,
-                                                         long long page_bytes, const int* __restrict__ pt,
-                                                         int max_pages, int pps, const double2* __restrict__ rope,
-                                                         const int* __restrict__ pos, float inv_sqrt,
-                                                         float* __restrict__ part_ml, float* __restrict__ part_o,
-                                                         float* __restrict__, float* __restrict__, unsigned* __restrict__,
-                                                         uint8_t* __restrict__, int, double* __restrict__, int, double,
-                                                         int, int) {
+                                                         float* __restrict__ part_ml, float* __restrict__ part_o) {
     using S = AdSmem<DH, G>;
     constexpr int CB = S::CB, QLD = S::QLD;
     constexpr int CPL = DH / 4;    // channels per lane in the score phase
@@ -718,15 +392,12 @@ __global__ void __launch_bounds__(1024) k_attn_merge_quant(const float* __restri
 template <int DH, int G>
 static int launch_dec(dim3 grid, int pps, cudaStream_t st, const float* qkv, int ldq, int H, int Hkv,
                       const int* kv_len, uint8_t* pool, long long page_bytes, const int* pt, int max_pages,
-                      const double2* rope, const int* pos, float inv_sqrt, float* part_ml, float* part_o,
-                      float* row, float* hmax, unsigned* cnt, uint8_t* codes, int ld_codes, double* scales,
-                      int qmode, double static_scale, int d_pad, int qmax) {
+                      const double2* rope, const int* pos, float inv_sqrt, float* part_ml, float* part_o) {
     const size_t smem = AdSmem<DH, G>::total(pps);
-    auto kfn = (QT_AD_KERNEL == 1 && G == 1) ? k_attn_dec<DH, G> : k_attn_dec_2p<DH, G>;
+    auto kfn = k_attn_dec<DH, G>;
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     return launch_pdl(kfn, grid, dim3(AD_THREADS), smem, st, qkv, ldq, H, Hkv, kv_len, pool, page_bytes, pt,
-                      max_pages, pps, rope, pos, inv_sqrt, part_ml, part_o, row, hmax, cnt, codes, ld_codes, scales,
-                      qmode, static_scale, d_pad, qmax);
+                      max_pages, pps, rope, pos, inv_sqrt, part_ml, part_o);
 }
 
 }  // namespace qt
@@ -737,8 +408,8 @@ extern "C" {
 
 int qt_attn_decode_plan(int B, int Hkv, int pages, int sms, int* pps, int* nsplit) {
     if (pages < 1 || B < 1) return -1;
-    // enough CTAs for one per SM, at most AD_MAX_PPS pages each
-    int ns = std::max(1, std::min(pages, (QT_AD_CTAS * sms + B * Hkv - 1) / (B * Hkv)));
+    // enough CTAs for two per SM, at most AD_MAX_PPS pages each
+    int ns = std::max(1, std::min(pages, (2 * sms + B * Hkv - 1) / (B * Hkv)));
     int p = (pages + ns - 1) / ns;
     if (p > AD_MAX_PPS) p = AD_MAX_PPS;
     ns = (pages + p - 1) / p;
@@ -751,7 +422,7 @@ int qt_launch_attn_decode(const float* qkv, int ldq, int H, int Hkv, int dh, con
                           uint8_t* pool, long long page_bytes, const int* pt, int max_pages, int pps, int nsplit,
                           const double* rope, const int* pos, float* part_ml, float* part_o, float* out, int ldo,
                           uint8_t* codes, int ld_codes, double* scales, int qmode, double static_scale, int d_pad,
-                          int bits, float* row, float* hmax, unsigned* counters, cudaStream_t st) {
+                          int bits, cudaStream_t st) {
     if (B <= 0) return 0;
     if (H > 64 || Hkv < 1 || H % Hkv || H / Hkv > AD_MAX_G || pps < 1 || pps > AD_MAX_PPS || nsplit < 1) return -1;
     // (the last split may extend past the page table: only pages holding cached rows are read)
@@ -759,22 +430,16 @@ int qt_launch_attn_decode(const float* qkv, int ldq, int H, int Hkv, int dh, con
     const dim3 grid(nsplit, Hkv, B);
     const float inv_sqrt = (float)(1.0 / sqrt((double)dh));
     const double2* rt = reinterpret_cast<const double2*>(rope);
-    const int qmax = (1 << (bits - 1)) - 1;
-    // one split + the attn_out codes wanted: the quantizer runs in the attention kernel's last
-    // kv-head CTA per sequence (no merge launch); scratch: row [B x H*dh], hmax [B x H], counters [B]
-    const bool fused_q = QT_AD_FUSEQ && (QT_AD_KERNEL == 1 && Hkv == H) && nsplit == 1 && codes && !out && row &&
-                         hmax && counters;
-    float* rw = fused_q ? row : nullptr;
     int rc = -1;
 #define QT_AD(D, GG)                                                                                           \
     if (dh == D && G == GG)                                                                                    \
         rc = launch_dec<D, GG>(grid, pps, st, qkv, ldq, H, Hkv, kv_len, pool, page_bytes, pt, max_pages, rt, pos, \
-                               inv_sqrt, part_ml, part_o, rw, hmax, counters, codes, ld_codes, scales, qmode,        \
-                               static_scale, d_pad, qmax);
+                               inv_sqrt, part_ml, part_o);
     QT_AD(128, 1) QT_AD(128, 2) QT_AD(128, 4) QT_AD(128, 7) QT_AD(128, 8)
     QT_AD(64, 1) QT_AD(64, 2) QT_AD(64, 4) QT_AD(64, 7) QT_AD(64, 8)
 #undef QT_AD
-    if (rc || fused_q) return rc;
+    if (rc) return rc;
+    const int qmax = (1 << (bits - 1)) - 1;
     if (dh == 128) {
         auto mk = H > 32 ? k_attn_merge_quant<128, 64> : k_attn_merge_quant<128, 32>;
         return launch_pdl(mk, dim3(B), dim3(1024), 0, st, (const float*)part_ml, (const float*)part_o, nsplit, H,
