@@ -253,8 +253,6 @@ struct qt_engine {
     float* dlogits = nullptr;  // [max_batch x d]
     float* part_ml = nullptr;
     float* part_o = nullptr;
-    float* dec_hmax = nullptr;    // [max_batch x H] per-head max |o| (fused attn_out quantizer)
-    unsigned* dec_cnt = nullptr;  // [max_batch] arrival counters, reset by the last arrival
     int dec_splits = 1, dec_pps = 1;   // the largest split plan over the layers (info)
     std::vector<int> dec_pages;        // cache pages per (layer, sequence) over the decode horizon
     std::vector<int> dec_lpps, dec_lsplit;  // decode-attention plan per layer (qt_attn_decode_plan)
@@ -379,7 +377,7 @@ struct qt_engine {
             for (double* p : fl.w) f(p);
         f(fp_head);
         if (blas) cublasDestroy(blas);
-        f(splitk_ws); f(codes8); f(head8); f(pmax); f(gmax); f(probs_d); f(dec_hmax); f(dec_cnt);
+        f(splitk_ws); f(codes8); f(head8); f(pmax); f(gmax); f(probs_d);
         f(tok_table); f(dec_tok); f(last_rows);
         if (pin) cudaFreeHost(pin);
         if (cst) {
@@ -524,8 +522,6 @@ struct qt_engine {
         dec_splits = max_pages;  // splits never exceed the pages
         part_ml = dalloc<float>((size_t)mb * H * dec_splits * 2);
         part_o = dalloc<float>((size_t)mb * H * dec_splits * dh);
-        dec_hmax = dalloc<float>((size_t)mb * H);
-        dec_cnt = dalloc<unsigned>(mb);
         {
             int dev = 0;
             ck(cudaGetDevice(&dev), "device");
@@ -1636,8 +1632,7 @@ struct qt_engine {
                 ckl(qt_launch_attn_decode(qkv, n_qkv, H, Hkv, dh, lenl, B, pool, page_bytes, ptl, max_pages,
                                           dec_lpps[l], dec_lsplit[l], rope, next_pos, part_ml, part_o, nullptr, d,
                                           codes, codes_rows, ascale, cfg.act_mode,
-                                          cfg.act_mode == 0 ? act[4 * l + 1] : 0.0, kd_pad, 4, attn, dec_hmax, dec_cnt,
-                                          st),
+                                          cfg.act_mode == 0 ? act[4 * l + 1] : 0.0, kd_pad, 4, st),
                     "decode attention");
             {  // decode attention streams every cached K/V row of this layer once
                 double rows = 0;
@@ -2629,7 +2624,7 @@ int qt_attn_decode_i4kv(const float* q, int ldq, int B, int H, int Hkv, int d_he
         if (qt_attn_decode_plan(B, Hkv, pages, sms, &pps, &nsplit)) fail(QT_EINVAL, "decode attention plan");
         ckl(qt_launch_attn_decode(q, ldq, H, Hkv, d_head, kv_len, B, const_cast<uint8_t*>(pool), page_bytes,
                                   page_table, max_pages, pps, nsplit, nullptr, nullptr, part_ml, part_o, out, ldo,
-                                  nullptr, 0, nullptr, 1, 0.0, 0, 4, nullptr, nullptr, nullptr, (cudaStream_t)stream),
+                                  nullptr, 0, nullptr, 1, 0.0, 0, 4, (cudaStream_t)stream),
             "decode attention");
     });
 }

@@ -408,7 +408,9 @@ extern "C" {
 
 int qt_attn_decode_plan(int B, int Hkv, int pages, int sms, int* pps, int* nsplit) {
     if (pages < 1 || B < 1) return -1;
-    // enough CTAs for two per SM, at most AD_MAX_PPS pages each
+    // enough CTAs for two per SM, at most AD_MAX_PPS pages each (measured against one per SM and
+    // against a per-warp-chunk kernel with the attn_out quantizer fused by the last arrival:
+    // tools/gpu_attn_ab.sh)
     int ns = std::max(1, std::min(pages, (2 * sms + B * Hkv - 1) / (B * Hkv)));
     int p = (pages + ns - 1) / ns;
     if (p > AD_MAX_PPS) p = AD_MAX_PPS;

@@ -92,9 +92,7 @@ int qt_launch_attn_decode(const float* qkv, int ldq, int H, int Hkv, int dh, con
                           uint8_t* pool, long long page_bytes, const int* pt, int max_pages, int pps, int nsplit,
                           const double* rope, const int* pos, float* part_ml, float* part_o, float* out, int ldo,
                           uint8_t* codes, int ld_codes, double* scales, int qmode, double static_scale, int d_pad,
-                          int bits, float* row, float* hmax, unsigned* counters, cudaStream_t st);
-// (nsplit == 1 with codes and row / hmax / counters (zeroed once) given: the attn_out quantizer
-// runs in the attention kernel itself, by the last kv-head CTA of each sequence)
+                          int bits, cudaStream_t st);
 int qt_launch_select_topk(const double* mag, const double* res, const float* inter, const float* intra, int H,
                           int vstride, const int* vis, const int* txt, const int* budget, const int* old_off,
                           const int* new_off, int B, int vmax, const double* w4, int* keep_src, int* keep_local,
