@@ -20,6 +20,7 @@
 #include <stdexcept>
 #include <string>
 #include <vector>
+#include <mutex>
 
 #include "../../include/quota_b200.h"
 #include "qt_common.cuh"
@@ -346,6 +347,7 @@ struct qt_engine {
     }
     // per-row partial max |x| of the mlp_mid site left by the gate|up GEMM epilogue (act_mode 1)
     static constexpr int kPmaxLd = 512;
+    static constexpr int kGemvMaxRows = 32;  // decode batches up to this many tokens: the int4 GEMV
     float* pmax = nullptr;
     int pm_parts = 0;
     float* pm_ptr = nullptr;  // where the last producer left them, row stride pm_ld
@@ -474,7 +476,7 @@ struct qt_engine {
         mid = dalloc<float>(T * dff);
         codes_rows = round_up(std::max((int)T, mb), 16);
         codes = dalloc<uint8_t>((size_t)codes_rows * std::max(kd_pad, kff_pad) / 2);  // tiled rows
-        if ((int)T > 64) {
+        if (std::max((int)T, mb) > kGemvMaxRows) {  // int8 activation copy for the tcgen05 GEMM
             ld8 = std::max(kd_pad, kff_pad);
             codes8 = dalloc<int8_t>((size_t)codes_rows * ld8);
         }
@@ -531,7 +533,7 @@ struct qt_engine {
             const int shapes[5][2] = {{n_qkv, kd_pad}, {d, kd_pad}, {n_gu, kd_pad}, {d, kff_pad}, {d, kd_pad}};
             size_t need = 0;
             for (auto& sh : shapes)
-                for (int m = 17; m <= std::min(mt, 128 * 148); m = (m < 128 ? 128 : m + 128)) {
+                for (int m = 1; m <= std::min(mt, 128 * 148); m = (m < 1024 ? m + 1 : m + 128)) {
                     const int mm = std::min(m, mt);
                     const int ks = std::max(qt_tc05_splitk(mm, sh[0], sh[1]), qt_tc05_i8_splitk(mm, sh[0], sh[1]));
                     if (ks > 1) need = std::max(need, (size_t)ks * mm * sh[0]);
@@ -1105,7 +1107,7 @@ struct qt_engine {
         const int mode = cfg.act_mode;
         const double s = mode == 0 ? act[site_idx] : 0.0;
         pb(P_QUANT);
-        int8_t* c8 = codes8 && M > 64 ? codes8 : nullptr;  // the next GEMM runs on int8 operands
+        int8_t* c8 = i8_rows(M) ? codes8 : nullptr;  // the next GEMM runs on int8 operands
         if (from_pmax && pm_parts > 0 && !is_f64 && !gain && mode == 1)
             ckl(qt_launch_quant_pmax(static_cast<const float*>(xin), ldx, pm_ptr, pm_parts, pm_ld, M, D, dpad, 7, mode,
                                      s, codes, codes_rows, ascale, c8, ld8, st),
@@ -1116,24 +1118,26 @@ struct qt_engine {
                 "rmsnorm+quant");
         pe((double)M * D * (is_f64 ? 8 : 4) + (double)M * dpad / 2 + 8.0 * M);
     }
+    // the int8-operand tcgen05 GEMM serves this many token rows (activation codes8 written)
+    bool i8_rows(int M) const { return use_tc05 && codes8 && M > kGemvMaxRows; }
     // w: tiled int4 weights with wrows padded rows; activation codes: tiled with codes_rows rows
     // want_pm: also leave the per-row partial max |out| in pmax (pm_parts slots; 0 = not produced)
     void gemm(int epi, const uint8_t* w, int wrows, const double* sw, int M, int N, int K, void* out, int ldo,
               bool want_pm = false, const int8_t* w8 = nullptr, float* pm_atomic = nullptr) {
         pb(P_GEMM);
-        const bool atomic_pm = want_pm && pm_atomic && M <= 64;  // GEMV: one reduced max per row
+        const bool i8 = i8_rows(M) && w8;
+        const bool atomic_pm = want_pm && pm_atomic && !i8 && M <= 64;  // GEMV: one reduced max per row
         float* pm = want_pm ? (atomic_pm ? pm_atomic : pmax) : nullptr;
         const int pld = atomic_pm ? 0 : kPmaxLd;
         pm_parts = 0;
         pm_ptr = atomic_pm ? pm_atomic : pmax;
         pm_ld = atomic_pm ? 1 : kPmaxLd;
-        // > 256 tokens: the int8-operand tcgen05 GEMM (TMA); 65..256: the packed-int4 tcgen05 GEMM
-        // with split-K across CTAs (decode batches: streams the int4 weights, half the int8 copy's
-        // bytes; measured faster than the int8 kernel at 256 tokens); the weight-streaming GEMV up
-        // to 64 tokens (decode batches)
-        int rc = (use_tc05 && M > 256 && codes8 && w8)
-                     ? qt_launch_w4a4_tc05_i8(epi, codes8, ld8, ascale, w8, wrows, K, sw, M, N, K, out, ldo, nullptr, pm,
-                                              kPmaxLd, &pm_parts, splitk_ws, st)
+        // > 32 tokens: the int8-operand tcgen05 GEMM (TMA), with k slices for the decode batches'
+        // narrow projections (qt_tc05_i8_single_splitk); up to 32 tokens the weight-streaming GEMV
+        // on the int4 tiles (half the int8 copy's bytes).  Measured per shape at 32..256 tokens
+        // against the GEMV and the packed-int4 tcgen05 kernel: tools/bench_decode_gemm.py
+        int rc = i8 ? qt_launch_w4a4_tc05_i8(epi, codes8, ld8, ascale, w8, wrows, K, sw, M, N, K, out, ldo, nullptr, pm,
+                                             kPmaxLd, &pm_parts, splitk_ws, st)
                  : (use_tc05 && M > 64)
                      ? qt_launch_w4a4_tc05_ex(epi, codes, codes_rows, ascale, w, wrows, sw, M, N, K, out, ldo, nullptr,
                                               splitk_ws, pm, kPmaxLd, &pm_parts, st)
@@ -1632,7 +1636,8 @@ struct qt_engine {
                 ckl(qt_launch_attn_decode(qkv, n_qkv, H, Hkv, dh, lenl, B, pool, page_bytes, ptl, max_pages,
                                           dec_lpps[l], dec_lsplit[l], rope, next_pos, part_ml, part_o, nullptr, d,
                                           codes, codes_rows, ascale, cfg.act_mode,
-                                          cfg.act_mode == 0 ? act[4 * l + 1] : 0.0, kd_pad, 4, st),
+                                          cfg.act_mode == 0 ? act[4 * l + 1] : 0.0, kd_pad, 4,
+                                          i8_rows(B) ? codes8 : nullptr, ld8, st),
                     "decode attention");
             {  // decode attention streams every cached K/V row of this layer once
                 double rows = 0;
@@ -2535,17 +2540,35 @@ int qt_w4a4_gemm(int epi, const uint8_t* a, int lda, const double* sa, const uin
             ckl(rc, "w4a4 gemm (int8 operands)");
             return;
         }
-        int* ws = nullptr;  // impl 2: tcgen05 with split-K (temporary workspace; test / ABI path)
+        if (impl == 5) {  // decode GEMV on weights in the row-block-major tile order (qt_w4t_to_rbm)
+            ckl(qt_launch_w4a4_gemv_rbm(epi, a, lda, sa, w, ldw, sw, M, N, K, out, ldo, acc_out, nullptr, 0, nullptr,
+                                        cs),
+                "w4a4 gemv (row-block-major)");
+            return;
+        }
+        int* ws = nullptr;  // impl 2: tcgen05 with split-K (a grow-only ABI-level workspace, so a
+                            // timing loop over one shape allocates once)
         if (impl == 2) {
-            const int ks = qt_tc05_splitk(M, N, K);
-            ck(cudaMalloc(&ws, (size_t)std::max(ks, 1) * M * N * sizeof(int)), "split-K workspace");
+            static std::mutex mu;
+            static int* g_ws = nullptr;
+            static size_t g_bytes = 0;
+            std::lock_guard<std::mutex> lk(mu);
+            const size_t need = (size_t)std::max(qt_tc05_splitk(M, N, K), 1) * M * N * sizeof(int);
+            if (need > g_bytes) {
+                cudaStreamSynchronize(cs);
+                if (g_ws) cudaFree(g_ws);
+                g_ws = nullptr;
+                g_bytes = 0;
+                ck(cudaMalloc(&g_ws, need), "split-K workspace");
+                g_bytes = need;
+            }
+            ws = g_ws;
+            ckl(impl >= 1 ? qt_launch_w4a4_tc05(epi, a, lda, sa, w, ldw, sw, M, N, K, out, ldo, acc_out, ws, cs) : 0,
+                "w4a4 gemm");
+            return;
         }
         int rc = impl >= 1 ? qt_launch_w4a4_tc05(epi, a, lda, sa, w, ldw, sw, M, N, K, out, ldo, acc_out, ws, cs)
                            : qt_launch_w4a4_mma(epi, a, lda, sa, w, ldw, sw, M, N, K, out, ldo, acc_out, cs);
-        if (ws) {
-            cudaStreamSynchronize(cs);
-            cudaFree(ws);
-        }
         ckl(rc, "w4a4 gemm");
     });
 }
@@ -2555,7 +2578,7 @@ int qt_w4a4_gemm_i8(int epi, const int8_t* a8, int lda8, const double* sa, const
                     int flags, void* stream) {
     return guard([&] {
         ckl(qt_launch_w4a4_tc05_i8_ex(epi, a8, lda8, sa, w8, w_rows, ldw8, sw, M, N, K, out, ldo, acc_out, nullptr, 0,
-                                      nullptr, workspace, flags & 1, (cudaStream_t)stream),
+                                      nullptr, workspace, flags, (cudaStream_t)stream),
             "w4a4 gemm (int8 operands)");
     });
 }
@@ -2563,6 +2586,10 @@ int qt_w4a4_gemm_i8(int epi, const int8_t* a8, int lda8, const double* sa, const
 int64_t qt_w4a4_gemm_i8_workspace(int M, int N, int K) {
     const int ks = qt_tc05_i8_splitk(M, N, K);
     return ks > 1 ? (int64_t)ks * M * N * (int64_t)sizeof(int) : 0;
+}
+
+int qt_w4t_to_rbm(const uint8_t* tiled, int rows_pad, int K, uint8_t* out, void* stream) {
+    return guard([&] { ckl(qt_launch_w4t_to_rbm(tiled, rows_pad, K, out, (cudaStream_t)stream), "tile reorder"); });
 }
 
 int qt_quant_weight_i4(const float* w, int K, int N, int row_mul, int row_add, uint8_t* codes, int ldc,
@@ -2624,7 +2651,7 @@ int qt_attn_decode_i4kv(const float* q, int ldq, int B, int H, int Hkv, int d_he
         if (qt_attn_decode_plan(B, Hkv, pages, sms, &pps, &nsplit)) fail(QT_EINVAL, "decode attention plan");
         ckl(qt_launch_attn_decode(q, ldq, H, Hkv, d_head, kv_len, B, const_cast<uint8_t*>(pool), page_bytes,
                                   page_table, max_pages, pps, nsplit, nullptr, nullptr, part_ml, part_o, out, ldo,
-                                  nullptr, 0, nullptr, 1, 0.0, 0, 4, (cudaStream_t)stream),
+                                  nullptr, 0, nullptr, 1, 0.0, 0, 4, nullptr, 0, (cudaStream_t)stream),
             "decode attention");
     });
 }

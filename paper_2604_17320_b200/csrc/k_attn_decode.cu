@@ -301,7 +301,7 @@ __global__ void __launch_bounds__(1024) k_attn_merge_quant(const float* __restri
                                                            float* __restrict__ out, int ldo,
                                                            uint8_t* __restrict__ codes, int ld_codes,
                                                            double* __restrict__ scales, int mode, double static_scale,
-                                                           int d_pad, int qmax) {
+                                                           int d_pad, int qmax, int8_t* __restrict__ codes8, int ld8) {
     constexpr int CPL = DH / 32;
     __shared__ double red[32];
     pdl_launch_dependents();
@@ -380,12 +380,22 @@ __global__ void __launch_bounds__(1024) k_attn_merge_quant(const float* __restri
         if (CPL == 4) {
             *reinterpret_cast<uint16_t*>(codes + w4t_offset(b, k0 / 2, ld_codes)) =
                 (uint16_t)((c[0] & 0xF) | ((c[1] & 0xF) << 4) | ((c[2] & 0xF) << 8) | ((c[3] & 0xF) << 12));
+            if (codes8)  // the int8-operand GEMM's copy: 16 x code, row-major
+                *reinterpret_cast<uint32_t*>(codes8 + (size_t)b * ld8 + k0) =
+                    (uint32_t)((c[0] << 4) & 0xFF) | ((uint32_t)((c[1] << 4) & 0xFF) << 8) |
+                    ((uint32_t)((c[2] << 4) & 0xFF) << 16) | ((uint32_t)((c[3] << 4) & 0xFF) << 24);
         } else {
             codes[w4t_offset(b, k0 / 2, ld_codes)] = (uint8_t)((c[0] & 0xF) | ((c[1] & 0xF) << 4));
+            if (codes8)
+                *reinterpret_cast<uint16_t*>(codes8 + (size_t)b * ld8 + k0) =
+                    (uint16_t)(((c[0] << 4) & 0xFF) | (((c[1] << 4) & 0xFF) << 8));
         }
     }
     // zero the K padding of this row
-    for (int k = H * DH + threadIdx.x * 2; k < d_pad; k += blockDim.x * 2) codes[w4t_offset(b, k / 2, ld_codes)] = 0;
+    for (int k = H * DH + threadIdx.x * 2; k < d_pad; k += blockDim.x * 2) {
+        codes[w4t_offset(b, k / 2, ld_codes)] = 0;
+        if (codes8) *reinterpret_cast<uint16_t*>(codes8 + (size_t)b * ld8 + k) = 0;
+    }
     if (threadIdx.x == 0) scales[b] = s;
 }
 
@@ -424,7 +434,7 @@ int qt_launch_attn_decode(const float* qkv, int ldq, int H, int Hkv, int dh, con
                           uint8_t* pool, long long page_bytes, const int* pt, int max_pages, int pps, int nsplit,
                           const double* rope, const int* pos, float* part_ml, float* part_o, float* out, int ldo,
                           uint8_t* codes, int ld_codes, double* scales, int qmode, double static_scale, int d_pad,
-                          int bits, cudaStream_t st) {
+                          int bits, int8_t* codes8, int ld8, cudaStream_t st) {
     if (B <= 0) return 0;
     if (H > 64 || Hkv < 1 || H % Hkv || H / Hkv > AD_MAX_G || pps < 1 || pps > AD_MAX_PPS || nsplit < 1) return -1;
     // (the last split may extend past the page table: only pages holding cached rows are read)
@@ -445,11 +455,11 @@ int qt_launch_attn_decode(const float* qkv, int ldq, int H, int Hkv, int dh, con
     if (dh == 128) {
         auto mk = H > 32 ? k_attn_merge_quant<128, 64> : k_attn_merge_quant<128, 32>;
         return launch_pdl(mk, dim3(B), dim3(1024), 0, st, (const float*)part_ml, (const float*)part_o, nsplit, H,
-                          out, ldo, codes, ld_codes, scales, qmode, static_scale, d_pad, qmax);
+                          out, ldo, codes, ld_codes, scales, qmode, static_scale, d_pad, qmax, codes8, ld8);
     }
     auto mk = H > 32 ? k_attn_merge_quant<64, 64> : k_attn_merge_quant<64, 32>;
     return launch_pdl(mk, dim3(B), dim3(1024), 0, st, (const float*)part_ml, (const float*)part_o, nsplit, H, out,
-                      ldo, codes, ld_codes, scales, qmode, static_scale, d_pad, qmax);
+                      ldo, codes, ld_codes, scales, qmode, static_scale, d_pad, qmax, codes8, ld8);
 }
 
 }  // extern "C"

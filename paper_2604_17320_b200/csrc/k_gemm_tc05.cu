@@ -194,9 +194,16 @@ QT_DEV void t5_epilogue_g(int ew0, int warp, int lane, uint32_t tmem, int u0, in
             if (m >= M || nb >= N) continue;
             if (ksplit > 1) {  // raw partial sums of this k slice
                 int* wr = ws + ((size_t)sl * M + m) * N + nb;
+                if (nb + 32 <= N && (N & 3) == 0) {  // the row's 128 B as 16-B stores (full sectors)
+                    int4* w4 = reinterpret_cast<int4*>(wr);
 #pragma unroll
-                for (int e = 0; e < 32; ++e)
-                    if (nb + e < N) wr[e] = (int)r[e] >> 8;
+                    for (int e = 0; e < 32; e += 4)
+                        w4[e / 4] = make_int4((int)r[e] >> 8, (int)r[e + 1] >> 8, (int)r[e + 2] >> 8, (int)r[e + 3] >> 8);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 32; ++e)
+                        if (nb + e < N) wr[e] = (int)r[e] >> 8;
+                }
                 continue;
             }
             if (acc_dbg) {
@@ -438,7 +445,7 @@ __global__ void __launch_bounds__(T8_THREADS, 1) k_gemm_tc05_i8(const __grid_con
                                                                  const double* __restrict__ sw, int M, int N, int K,
                                                                  void* __restrict__ out, int ldo,
                                                                  int* __restrict__ acc_dbg, float* __restrict__ pmax,
-                                                                 int pmax_ld) {
+                                                                 int pmax_ld, int ksplit, int* __restrict__ ws) {
     extern __shared__ __align__(1024) uint8_t smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + T8Smem::bars);
     uint64_t* empty = full + T8_S;
@@ -450,6 +457,9 @@ __global__ void __launch_bounds__(T8_THREADS, 1) k_gemm_tc05_i8(const __grid_con
     const int KB = K / 128;
     const int mt_n = (M + T5_BM - 1) / T5_BM, nt_n = (N + T5_BN - 1) / T5_BN;
     const int tiles = mt_n * nt_n;
+    // work unit u: tile u % tiles, k slice u / tiles (split-K for decode batches, ksplit > 1:
+    // int32 partials to ws, reduced in fixed order by k_splitk_epilogue)
+    const int units = tiles * ksplit, kbs = (KB + ksplit - 1) / ksplit;
     if (threadIdx.x == 0) {
         for (int s = 0; s < T8_S; ++s) {
             mbar_init(&full[s], 1);
@@ -476,9 +486,10 @@ __global__ void __launch_bounds__(T8_THREADS, 1) k_gemm_tc05_i8(const __grid_con
             asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmB) : "memory");
             pdl_wait();  // activation codes come from the upstream kernel
             int it = 0;
-            for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+            for (int u = blockIdx.x; u < units; u += gridDim.x) {
+                const int t = u % tiles, k0 = (u / tiles) * kbs, k1 = min(KB, k0 + kbs);
                 const int m0 = (t % mt_n) * T5_BM, n0 = (t / mt_n) * T5_BN;
-                for (int kb = 0; kb < KB; ++kb, ++it) {
+                for (int kb = k0; kb < k1; ++kb, ++it) {
                     const int s = it % T8_S;
                     if (it >= T8_S) mbar_wait(&empty[s], ((it / T8_S) - 1) & 1);
                     mbar_arrive_expect_tx(&full[s], (uint32_t)(T5_IA + T5_IB));
@@ -491,12 +502,13 @@ __global__ void __launch_bounds__(T8_THREADS, 1) k_gemm_tc05_i8(const __grid_con
         if (lane == 0) {
             const uint32_t idesc = t5_idesc();
             int it = 0, tl = 0;
-            for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++tl) {
+            for (int u = blockIdx.x; u < units; u += gridDim.x, ++tl) {
+                const int k0 = (u / tiles) * kbs, k1 = min(KB, k0 + kbs);
                 const int acc = tl % T5_ACC;
                 if (tl >= T5_ACC) mbar_wait(&tempty[acc], ((tl / T5_ACC) - 1) & 1);
                 tc_fence_after();
                 const uint32_t tacc = tmem + (uint32_t)(acc * T5_BN);
-                for (int kb = 0; kb < KB; ++kb, ++it) {
+                for (int kb = k0; kb < k1; ++kb, ++it) {
                     const int s = it % T8_S;
                     mbar_wait(&full[s], (it / T8_S) & 1);
                     tc_fence_after();
@@ -505,7 +517,7 @@ __global__ void __launch_bounds__(T8_THREADS, 1) k_gemm_tc05_i8(const __grid_con
 #pragma unroll
                     for (int k = 0; k < 4; ++k)
                         mma_i8(tacc, umma_desc_sw128(a0 + 32 * k), umma_desc_sw128(b0 + 32 * k), idesc,
-                               (kb != 0) || (k != 0));
+                               (kb != k0) || (k != 0));
                     mma_commit(&empty[s]);
                 }
                 mma_commit(&tfull[acc]);
@@ -513,8 +525,8 @@ __global__ void __launch_bounds__(T8_THREADS, 1) k_gemm_tc05_i8(const __grid_con
         }
         __syncwarp();
     } else {
-        t5_epilogue_g<EPI>(T8_EW0, warp, lane, tmem, blockIdx.x, gridDim.x, tiles, tiles, mt_n, 1, 0, M, N, sa, sw,
-                           sws, out, ldo, acc_dbg, 1, nullptr, pmax, pmax_ld, tfull, tempty);
+        t5_epilogue_g<EPI>(T8_EW0, warp, lane, tmem, blockIdx.x, gridDim.x, units, tiles, mt_n, 1, 0, M, N, sa, sw,
+                           sws, out, ldo, ksplit > 1 ? nullptr : acc_dbg, ksplit, ws, pmax, pmax_ld, tfull, tempty);
     }
     tc_fence_before();
     __syncthreads();
@@ -825,11 +837,31 @@ extern "C" int qt_launch_w4t_to_i8(const uint8_t* tiled, int rows_pad, int K, in
 
 // A8: int8 activations [>= M rows x K], row stride lda8; W8: int8 weights [w_rows x K], stride ldw8.
 // M >= 8192: the 2-SM (CTA pair, cta_group::2) kernel on 256 x 256 tiles; else the single-CTA one.
+// k slices of the single-CTA kernel (decode batches, M <= 512): only when the tiles fill
+// less than half the SMs (the N = d_model projections), as many slices as keep one wave,
+// at most 6 and >= 4 k blocks each -- measured per shape and slice count at M = 32..256
+// (tools/bench_decode_gemm.py): splitting the wide projections only added the int32
+// partials' round trip.  ks_force > 0 overrides (measurement).
+static int qt_tc05_i8_single_splitk(int M, int N, int K, int ks_force = 0) {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const int KB = K / 128;
+    const int tiles = ((M + qt::T5_BM - 1) / qt::T5_BM) * ((N + qt::T5_BN - 1) / qt::T5_BN);
+    auto eff = [&](int ks) {  // slices actually formed (no empty slice)
+        ks = std::max(1, std::min(ks, KB));
+        const int kbs = (KB + ks - 1) / ks;
+        return (KB + kbs - 1) / kbs;
+    };
+    if (ks_force > 0) return eff(ks_force);
+    if (M > 512 || 2 * tiles > sms) return 1;
+    return eff(std::min({6, sms / tiles, KB / 4}));
+}
+
 int qt_tc05_i8_splitk(int M, int N, int K) {
     // the 2-SM kernel's k slices: enough work units for every CTA pair, >= 4 k blocks per slice
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    if (M <= qt::T5_BM) return 1;
+    if (M < 8192) return qt_tc05_i8_single_splitk(M, N, K);
     const int tiles = ((M + 255) / 256) * ((N + qt::T5_BN - 1) / qt::T5_BN);
     const int pairs = sms / 2, KB = K / 128;
     if (tiles >= pairs) return 1;
@@ -841,7 +873,7 @@ int qt_tc05_i8_splitk(int M, int N, int K) {
 extern "C" int qt_launch_w4a4_tc05_i8_ex(int epi, const int8_t* A8, int lda8, const double* sa, const int8_t* W8,
                                          int w_rows, int ldw8, const double* sw, int M, int N, int K, void* out,
                                          int ldo, int* acc_dbg, float* pmax, int pmax_ld, int* n_part, int* ws,
-                                         int force_single, cudaStream_t st);
+                                         int flags, cudaStream_t st);
 
 extern "C" int qt_launch_w4a4_tc05_i8(int epi, const int8_t* A8, int lda8, const double* sa, const int8_t* W8,
                                       int w_rows, int ldw8, const double* sw, int M, int N, int K, void* out, int ldo,
@@ -850,12 +882,15 @@ extern "C" int qt_launch_w4a4_tc05_i8(int epi, const int8_t* A8, int lda8, const
                                      pmax_ld, n_part, ws, 0, st);
 }
 
-// force_single: the single-CTA 128 x 256 kernel at any M (A/B measurements, qt_w4a4_gemm_i8)
+// flags bit 0: the single-CTA 128 x 256 kernel at any M (A/B measurements, qt_w4a4_gemm_i8);
+// bits 8..15: k-slice count override of the single-CTA kernel (needs ws; measurement)
 extern "C" int qt_launch_w4a4_tc05_i8_ex(int epi, const int8_t* A8, int lda8, const double* sa, const int8_t* W8,
                                          int w_rows, int ldw8, const double* sw, int M, int N, int K, void* out,
                                          int ldo, int* acc_dbg, float* pmax, int pmax_ld, int* n_part, int* ws,
-                                         int force_single, cudaStream_t st) {
+                                         int flags, cudaStream_t st) {
     using namespace qt;
+    const bool force_single = flags & 1;
+    const int ks_force = (flags >> 8) & 0xFF;
     if (n_part) *n_part = 0;
     if (M <= 0) return 0;
     if (K % 128 || lda8 % 16 || ldw8 % 16 || N > w_rows) return -1;
@@ -868,7 +903,7 @@ extern "C" int qt_launch_w4a4_tc05_i8_ex(int epi, const int8_t* A8, int lda8, co
     CUtensorMap ta, tb;
     // CTA pairs only pay for the largest token counts (measured, tools/bench_gemm.py: pair 2880 vs
     // single 2774 TOPS at 8192^3, but 1582 vs 2004 on the 7B QKV GEMM at M = 1896)
-    const bool pair = M >= 8192 && !force_single;
+    const bool pair = M >= 8192 && !force_single && ks_force == 0;
     if (qt_tmap_i8(&ta, A8, M, K, lda8, T5_BM) || qt_tmap_i8(&tb, W8, w_rows, K, ldw8, pair ? 128 : T5_BN))
         return -2;
     if (pair) {
@@ -915,15 +950,24 @@ extern "C" int qt_launch_w4a4_tc05_i8_ex(int epi, const int8_t* A8, int lda8, co
 #undef QT_T2
         return -1;
     }
-    const int units = ((M + T5_BM - 1) / T5_BM) * nt_n;
+    const int ksplit = ws ? qt_tc05_i8_single_splitk(M, N, K, ks_force) : 1;
+    if (ksplit > 1) {
+        pmax = nullptr;
+        if (n_part) *n_part = 0;
+    }
+    const int units = ((M + T5_BM - 1) / T5_BM) * nt_n * ksplit;
     const dim3 grid(std::min(units, sms));
     const size_t smem = T8Smem::total;
 #define QT_T8(E)                                                                                                 \
     do {                                                                                                         \
         auto kfn = k_gemm_tc05_i8<E>;                                                                            \
         cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                       \
-        return launch_pdl(kfn, grid, dim3(T8_THREADS), smem, st, ta, tb, sa, sw, M, N, K, out, ldo, acc_dbg, pmax, \
-                          pmax_ld);                                                                              \
+        int rc = launch_pdl(kfn, grid, dim3(T8_THREADS), smem, st, ta, tb, sa, sw, M, N, K, out, ldo, acc_dbg,    \
+                            pmax, pmax_ld, ksplit, ws);                                                          \
+        if (rc || ksplit == 1) return rc;                                                                        \
+        const long long pairs1 = ((long long)M * N + 1) / 2;                                                     \
+        return launch_pdl(k_splitk_epilogue<E>, dim3((unsigned)((pairs1 + 255) / 256)), dim3(256), 0, st,       \
+                          (const int*)ws, ksplit, M, N, sa, sw, out, ldo, acc_dbg);                               \
     } while (0)
     switch (epi) {
         case QT_EPI_STORE: QT_T8(QT_EPI_STORE);

@@ -12,7 +12,15 @@ namespace qt {
 // bottleneck of the gate|up GEMM.  The row-wise epi_store (decode GEMV) keeps fp64.
 QT_DEV float silu_f32(double g) {
     const float gf = (float)g;
-    return gf / (1.0f + expf(-gf));
+    // approximate divide (2 ulp; 0 once 1 + e^-g > 2^126, where silu underflows anyway): the
+    // IEEE division's subroutine call dominated the gate|up epilogue (ncu source page);
+    // expf stays the accurate one (the mlp_mid quantizer's tie budget, tests/replay.py)
+    return __fdividef(gf, 1.0f + expf(-gf));
+}
+
+// int32 -> fp64 without the F64 conversion unit: (2^52 + 2^31 + a) as bits, minus the offset (exact)
+QT_DEV double i2d_exact(int a) {
+    return __hiloint2double(0x43300000, (unsigned)a ^ 0x80000000u) - 4503601774854144.0;
 }
 
 // y = (acc / 256) * s_a[m] * s_w[n] in fp64 (scales are the reference's fp64
@@ -78,8 +86,8 @@ QT_DEV void epi_row32(void* __restrict__ outv, int ldo, int m, int n, const uint
             for (int u = 0; u < 4; ++u) v[u] = p[e / 2 + u];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                v[u].x += (double)((int)r[e + 2 * u] >> 8) * (a_s * swt[e + 2 * u]);
-                v[u].y += (double)((int)r[e + 2 * u + 1] >> 8) * (a_s * swt[e + 2 * u + 1]);
+                v[u].x += i2d_exact((int)r[e + 2 * u] >> 8) * (a_s * swt[e + 2 * u]);
+                v[u].y += i2d_exact((int)r[e + 2 * u + 1] >> 8) * (a_s * swt[e + 2 * u + 1]);
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u) p[e / 2 + u] = v[u];
@@ -94,8 +102,8 @@ QT_DEV void epi_row32(void* __restrict__ outv, int ldo, int m, int n, const uint
             float v[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const double g = (double)((int)r[e + 2 * u] >> 8) * (a_s * swt[e + 2 * u]);
-                const double up = (double)((int)r[e + 2 * u + 1] >> 8) * (a_s * swt[e + 2 * u + 1]);
+                const double g = i2d_exact((int)r[e + 2 * u] >> 8) * (a_s * swt[e + 2 * u]);
+                const double up = i2d_exact((int)r[e + 2 * u + 1] >> 8) * (a_s * swt[e + 2 * u + 1]);
                 v[u] = silu_f32(g) * (float)up;
                 mx = fmaxf(mx, fabsf(v[u]));
             }
@@ -109,7 +117,7 @@ QT_DEV void epi_row32(void* __restrict__ outv, int ldo, int m, int n, const uint
         float v[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-            const double y = (double)((int)r[e + u] >> 8) * (a_s * swt[e + u]);
+            const double y = i2d_exact((int)r[e + u] >> 8) * (a_s * swt[e + u]);
             v[u] = EPI == QT_EPI_SILU ? silu_f32(y) : (float)y;
             mx = fmaxf(mx, fabsf(v[u]));
         }

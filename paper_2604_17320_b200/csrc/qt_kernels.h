@@ -51,7 +51,7 @@ int qt_launch_w4a4_tc05_i8(int epi, const int8_t* A8, int lda8, const double* sa
 int qt_tc05_i8_splitk(int M, int N, int K);
 int qt_launch_w4a4_tc05_i8_ex(int epi, const int8_t* A8, int lda8, const double* sa, const int8_t* W8, int w_rows,
                               int ldw8, const double* sw, int M, int N, int K, void* out, int ldo, int* acc_dbg,
-                              float* pmax, int pmax_ld, int* n_part, int* ws, int force_single, cudaStream_t st);
+                              float* pmax, int pmax_ld, int* n_part, int* ws, int flags, cudaStream_t st);
 int qt_launch_w4t_to_i8(const uint8_t* tiled, int rows_pad, int K, int8_t* out, cudaStream_t st);
 int qt_launch_w4a4_mma_ex(int epi, const uint8_t* A, int lda, const double* sa, const uint8_t* W, int ldw,
                           const double* sw, int M, int N, int K, void* out, int ldo, int* acc_dbg, float* pmax,
@@ -64,6 +64,11 @@ int qt_launch_w4a4_tc05_ex(int epi, const uint8_t* A, int lda, const double* sa,
 int qt_launch_quant_pmax(const float* x, int ld_x, const float* pmax, int n_part, int pmax_ld, int M, int D,
                          int d_pad, int qmax, int mode, double static_scale, uint8_t* codes, int ld_codes,
                          double* scales, int8_t* codes8, int ld8, cudaStream_t st);
+// decode GEMV on a row-block-major weight copy (made by qt_launch_w4t_to_rbm)
+int qt_launch_w4a4_gemv_rbm(int epi, const uint8_t* A, int lda, const double* sa, const uint8_t* W, int ldw,
+                            const double* sw, int M, int N, int K, void* out, int ldo, int* acc_dbg, float* pmax,
+                            int pmax_ld, int* n_part, cudaStream_t st);
+int qt_launch_w4t_to_rbm(const uint8_t* in, int rows_pad, int K, uint8_t* out, cudaStream_t st);
 int qt_launch_w4a4_mma(int epi, const uint8_t* A, int lda, const double* sa, const uint8_t* W, int ldw,
                        const double* sw, int M, int N, int K, void* out, int ldo, int* acc_dbg, cudaStream_t st);
 // ws (nullable): int32 split-K workspace of qt_tc05_splitk(M, N, K) * M * N entries; with ws the
@@ -92,7 +97,7 @@ int qt_launch_attn_decode(const float* qkv, int ldq, int H, int Hkv, int dh, con
                           uint8_t* pool, long long page_bytes, const int* pt, int max_pages, int pps, int nsplit,
                           const double* rope, const int* pos, float* part_ml, float* part_o, float* out, int ldo,
                           uint8_t* codes, int ld_codes, double* scales, int qmode, double static_scale, int d_pad,
-                          int bits, cudaStream_t st);
+                          int bits, int8_t* codes8, int ld8, cudaStream_t st);
 int qt_launch_select_topk(const double* mag, const double* res, const float* inter, const float* intra, int H,
                           int vstride, const int* vis, const int* txt, const int* budget, const int* old_off,
                           const int* new_off, int B, int vmax, const double* w4, int* keep_src, int* keep_local,

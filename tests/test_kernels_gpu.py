@@ -278,3 +278,45 @@ def test_w4a4_gemv_wide_batches_int32_exact(torch_cuda, M):
     exp = a.astype(np.int64) @ w.T.astype(np.int64)
     assert np.array_equal(acc.cpu().numpy(), exp)
     np.testing.assert_allclose(out.cpu().numpy(), exp * sa[:, None] * sw[None, :], rtol=2e-7, atol=1e-7)
+
+
+@pytest.mark.parametrize("epi", [Q.EPI_STORE, Q.EPI_RESADD, Q.EPI_SWIGLU])
+@pytest.mark.parametrize("M,N,K,ks", [(64, 4096, 4096, 4), (256, 12288, 1024, 3), (200, 1536, 11008, 5),
+                                      (8, 512, 512, 2), (256, 4096, 4096, 0)])
+def test_w4a4_gemm_i8_single_splitk(torch_cuda, epi, M, N, K, ks):
+    """The single-CTA int8 tcgen05 kernel with k slices (decode batches): int32 partials per slice
+    in the workspace, reduced in fixed order -- bit-exact accumulators, the same epilogues.
+    ks = 0: the automatic slice choice (qt_w4a4_gemm_i8_workspace)."""
+    torch = torch_cuda
+    rng = np.random.default_rng(31 * M + ks + epi)
+    a = rng.integers(-7, 8, size=(M, K))
+    w = rng.integers(-7, 8, size=(N, K))
+    sa = rng.uniform(0.01, 0.5, M)
+    sw = rng.uniform(0.001, 0.01, N)
+    acc_exp = a.astype(np.int64) @ w.T.astype(np.int64)
+    y = acc_exp * (sa[:, None] * sw[None, :])
+    if epi == Q.EPI_SWIGLU:
+        out = torch.zeros((M, N // 2), dtype=torch.float32, device="cuda")
+        g, u = y[:, 0::2], y[:, 1::2]
+        exp, tol = g / (1 + np.exp(-g)) * u, dict(rtol=1e-5, atol=1e-6)
+    elif epi == Q.EPI_RESADD:
+        base = rng.standard_normal((M, N))
+        out = torch.from_numpy(base.copy()).cuda()
+        exp, tol = base + y, dict(rtol=1e-14, atol=1e-14)
+    else:
+        out = torch.zeros((M, N), dtype=torch.float32, device="cuda")
+        exp, tol = y, dict(rtol=2e-7, atol=1e-7)
+    a8 = torch.from_numpy((a * 16).astype(np.int8)).cuda()
+    w8 = torch.from_numpy((w * 16).astype(np.int8)).cuda()
+    if ks:
+        wsp = torch.empty(ks * M * N, dtype=torch.int32, device="cuda")
+    else:
+        nb = Q.lib().qt_w4a4_gemm_i8_workspace(M, N, K)
+        assert nb > 0  # the automatic choice splits this decode shape
+        wsp = torch.empty(nb // 4, dtype=torch.int32, device="cuda")
+    acc = torch.zeros((M, N), dtype=torch.int32, device="cuda")
+    Q.w4a4_gemm_i8(epi, a8, torch.from_numpy(sa).cuda(), w8, torch.from_numpy(sw).cuda(), M, N, K, out, acc,
+                   workspace=wsp, ksplit=ks)
+    torch.cuda.synchronize()
+    assert np.array_equal(acc.cpu().numpy(), acc_exp)
+    np.testing.assert_allclose(out.cpu().numpy(), exp, **tol)

@@ -129,6 +129,18 @@ def test_replay_c1_r1_dynamic_swiglu_gqa(torch_cuda):
     _run(cfg, w, None, rec, [(emb, 144, 40, 144)], 16, 700)
 
 
+def test_replay_c1_r1_decode_batch_40(torch_cuda):
+    """A decode batch above the GEMV's 32 tokens: every decode GEMM runs on the int8-operand
+    tcgen05 kernel (the narrow projections with k slices, tools/bench_decode_gemm.py), the
+    attention merge writes the int8 activation copy; 40 ragged sequences, 3 decode steps."""
+    cfg = O.ModelCfg(n_layers=4, d_model=256, n_heads=4, n_kv_heads=2, d_head=64, d_ff=688, mlp=1, act_mode=1,
+                     weight_axis=2)
+    w = O.synth_weights(cfg, seed=23)
+    rec = O.Recipe([1, 2], [0.5, 0.3], v0=48)
+    seqs = [(O.synth_embeddings(48 + 8 + i % 5, 256, seed=300 + i), 48, 8 + i % 5, 48) for i in range(40)]
+    _run(cfg, w, None, rec, seqs, 3, 1700)
+
+
 def _c2_weights(mlp, act_mode):
     cfg = O.ModelCfg(n_layers=3, d_model=4096, n_heads=32, n_kv_heads=32, d_head=128,
                      d_ff=11008 if mlp == 1 else 16384, mlp=mlp, act_mode=act_mode, weight_axis=2)
