@@ -25,6 +25,10 @@
 
 namespace qt {
 
+#ifndef QT_AD_CTA_MULT
+#define QT_AD_CTA_MULT 8  // decode attention CTAs per SM the split plan aims for (A/B: 2 / 4 / 8,
+                          // tools/gpu_attn_ab.sh -- C2 decode 1.719 / 1.652 / 1.647 ms per step)
+#endif
 constexpr int AD_THREADS = 256;
 constexpr int AD_MAX_PPS = 8;  // pages per split (smem: 8.5 KB each at d_head 128)
 constexpr int AD_MAX_G = 8;    // query heads per kv head (one softmax warp each)
@@ -418,10 +422,10 @@ extern "C" {
 
 int qt_attn_decode_plan(int B, int Hkv, int pages, int sms, int* pps, int* nsplit) {
     if (pages < 1 || B < 1) return -1;
-    // enough CTAs for two per SM, at most AD_MAX_PPS pages each (measured against one per SM and
-    // against a per-warp-chunk kernel with the attn_out quantizer fused by the last arrival:
-    // tools/gpu_attn_ab.sh)
-    int ns = std::max(1, std::min(pages, (2 * sms + B * Hkv - 1) / (B * Hkv)));
+    // enough CTAs for QT_AD_CTA_MULT per SM, at most AD_MAX_PPS pages each (measured against
+    // fewer CTAs and against a per-warp-chunk kernel with the attn_out quantizer fused by the last
+    // arrival: tools/gpu_attn_ab.sh)
+    int ns = std::max(1, std::min(pages, (QT_AD_CTA_MULT * sms + B * Hkv - 1) / (B * Hkv)));
     int p = (pages + ns - 1) / ns;
     if (p > AD_MAX_PPS) p = AD_MAX_PPS;
     ns = (pages + p - 1) / p;

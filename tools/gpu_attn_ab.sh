@@ -2,7 +2,7 @@
 # decode-attention A/B: the bench's per-class decode chain for each build variant
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-for v in ${VARIANTS:-pw1fq pw1 pw2 tp2 tp1}; do
+for v in ${VARIANTS:-m2 m4 m8}; do
   for c in "c2" "c4" "c5 --batch 256 --decode 128"; do
     QT_LIB_PATH=$PWD/paper_2604_17320_b200/_build_var/$v/libquota_b200.so timeout 600 python bench.py --config $c \
       --steps 2 --warmup 2 --no-cpu-baseline > gpurun_out/ab.log 2>&1
