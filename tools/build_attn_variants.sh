@@ -8,7 +8,9 @@ B=paper_2604_17320_b200/_build
 FLAGS="-std=c++17 -O3 -lineinfo -gencode arch=compute_100a,code=sm_100a -Xcompiler -fPIC --expt-relaxed-constexpr -Iinclude"
 make -C paper_2604_17320_b200/csrc -j8 > /dev/null
 OTHERS=$(ls $B/*.o | grep -v k_attn_decode.o)
-for v in ${VARIANTS:-"m2:-DQT_AD_CTA_MULT=2" "m4:-DQT_AD_CTA_MULT=4" "m8:-DQT_AD_CTA_MULT=8"}; do
+# VARIANTS: ';'-separated name:defines list
+IFS=';' read -ra VL <<< "${VARIANTS:-m2:-DQT_AD_CTA_MULT=2;m4:-DQT_AD_CTA_MULT=4;m8:-DQT_AD_CTA_MULT=8}"
+for v in "${VL[@]}"; do
   name=${v%%:*}; defs=${v#*:}
   out=paper_2604_17320_b200/_build_var/$name; mkdir -p $out
   /usr/local/cuda/bin/nvcc $FLAGS $defs -c paper_2604_17320_b200/csrc/k_attn_decode.cu -o $out/k_attn_decode.o
