@@ -326,6 +326,8 @@ def run_ours(args, cfg):
     rows = sum(vis) + B * T  # prefill tokens of the batch
     v0s = vis if cfg["v0"] is None else None  # ragged: each sequence's own v0
     eng = build_engine(cfg, torch, Q, vis)
+    if args.eager_decode:  # per-kernel tools (ncu launch lists): no graph replays
+        eng.set_graphs(False)
     stream = torch.cuda.Stream(device=dev)
     eng.set_stream(stream)
     emb_h, dec_h = synth_inputs(cfg, torch, seqs, vis)
@@ -610,6 +612,8 @@ def main():
                     help="decode with seeded step embeddings instead of greedy argmax tokens")
     ap.add_argument("--batch", type=int, default=None, help="override the config's per-GPU batch (c5 sweep)")
     ap.add_argument("--decode", type=int, default=None, help="override the config's decode steps (c5 sweep)")
+    ap.add_argument("--eager-decode", action="store_true",
+                    help="decode steps as eager launches, not CUDA graph replays (for ncu launch lists)")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.batch:

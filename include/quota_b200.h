@@ -189,6 +189,10 @@ int qt_engine_decode_f64(qt_engine* e, const double* emb, int emb_on_device, flo
  * ties to the smaller token id); the argmax + embedding kernel is part of the step's CUDA
  * graph.  tokens_out: int [n_seq], host or device (nullable); logits_out as qt_engine_decode. */
 int qt_engine_set_token_table(qt_engine* e, const float* table, int vocab, int on_device);
+/* Decode steps replay a captured CUDA graph (on, the default) or launch their kernels eagerly
+ * (off; the same kernels and programmatic-dependent launches -- for per-kernel tools such as
+ * an ncu launch list, whose graph-node replay of the page-streaming attention kernel fails). */
+int qt_engine_set_graphs(qt_engine* e, int on);
 int qt_engine_decode_greedy(qt_engine* e, int* tokens_out, float* logits_out, int out_on_device);
 
 /* Introspection (parity tests, reports). */

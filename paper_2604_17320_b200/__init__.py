@@ -107,6 +107,7 @@ def lib():
         L.qt_w4a4_gemm_i8_workspace.restype = C.c_int64
         L.qt_w4a4_gemm_i8_workspace.argtypes = [C.c_int, C.c_int, C.c_int]
         L.qt_engine_set_token_table.argtypes = [vp, vp, C.c_int, C.c_int]
+        L.qt_engine_set_graphs.argtypes = [vp, C.c_int]
         L.qt_engine_decode_greedy.argtypes = [vp, vp, vp, C.c_int]
         L.qt_w4t_to_rbm.argtypes = [vp, C.c_int, C.c_int, vp, vp]
         L.qt_engine_capture.argtypes = [vp, C.c_int]
@@ -358,6 +359,10 @@ class Engine:
         out = np.empty((emb.shape[0], self.cfg.d_model), dtype=np.float32) if logits_out is None else logits_out
         check(lib().qt_engine_decode(self.h, _ptr(emb), on_dev, _ptr(out), _on_device(out)))
         return out
+
+    def set_graphs(self, on):
+        """Decode steps as CUDA graph replays (True, default) or eager launches (False)."""
+        check(lib().qt_engine_set_graphs(self.h, int(bool(on))))
 
     def set_token_table(self, table):
         """Token-embedding table [vocab x d_model] fp32 (numpy or CUDA torch) for decode_greedy."""

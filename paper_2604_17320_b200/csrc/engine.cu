@@ -1618,6 +1618,7 @@ struct qt_engine {
     }
 
     // ------------------------------------------------------------ decode
+    bool use_graphs = true;  // qt_engine_set_graphs: decode steps as CUDA graph replays (else eager)
     int skip_mask = 0;  // kernel classes left out of decode_body (profile_chain: 1 GEMM, 2 attention, 4 quant, 8 kv)
     void decode_body() {
         double* xcur = xd;  // the step's input was written (widened) into xd before the graph
@@ -1771,7 +1772,7 @@ struct qt_engine {
         }
         cudaGraphExec_t& gx = greedy ? graph_g : graph;
         bool& gx_ok = greedy ? graph_g_ok : graph_ok;
-        if (profiling || capture) {
+        if (profiling || capture || !use_graphs) {
             if (greedy) greedy_in();
             decode_body();  // eager launches so every kernel gets its own events / capture reads
         } else if (!gx_ok) {
@@ -1795,7 +1796,7 @@ struct qt_engine {
             cudaGraphDestroy(g);
             gx_ok = true;
         }
-        if (!profiling && !capture) ck(cudaGraphLaunch(gx, st), "graph launch");
+        if (!profiling && !capture && use_graphs) ck(cudaGraphLaunch(gx, st), "graph launch");
         if (greedy && tokens_out)
             ck(cudaMemcpyAsync(tokens_out, dec_tok, (size_t)B * sizeof(int), cudaMemcpyDefault, st), "tokens");
         if (out)
@@ -2277,6 +2278,10 @@ int qt_engine_decode(qt_engine* e, const float* emb, int emb_on_device, float* l
         if (!emb) fail(QT_EINVAL, "embedding width mismatch");
         e->decode(emb, emb_on_device, 0, logits_out, out_on_device);
     });
+}
+
+int qt_engine_set_graphs(qt_engine* e, int on) {
+    return guard([&] { e->use_graphs = on != 0; });
 }
 
 int qt_engine_set_token_table(qt_engine* e, const float* table, int vocab, int on_device) {

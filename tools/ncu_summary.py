@@ -37,12 +37,15 @@ def summarize(seq, title=""):
 
 if __name__ == "__main__":
     seq = load(sys.argv[1])
-    marks = [i for i, s in enumerate(seq) if "k_f32_to_f64" in s[0]]
-    # first widen = prefill start; later ones = decode steps
-    if marks:
-        pre = seq[marks[0]:marks[1]] if len(marks) > 1 else seq[marks[0]:]
-        summarize(pre, "prefill")
-        if len(marks) > 1:
-            summarize(seq[marks[1]:marks[2]] if len(marks) > 2 else seq[marks[1]:], "decode step")
+    # prefill: from the first embedding widen (k_f32_to_f64); decode steps start at the greedy
+    # argmax + embed kernel (k_greedy_next) or, teacher-forced, at the later widens
+    widen = [i for i, s in enumerate(seq) if "k_f32_to_f64" in s[0]]
+    greedy = [i for i, s in enumerate(seq) if "k_greedy_next" in s[0]]
+    if widen:
+        steps = greedy if greedy else widen[1:]
+        steps = [i for i in steps if i > widen[0]]
+        summarize(seq[widen[0]:steps[0]] if steps else seq[widen[0]:], "prefill")
+        if steps:
+            summarize(seq[steps[0]:steps[1]] if len(steps) > 1 else seq[steps[0]:], "decode step")
     else:
         summarize(seq, "all")
