@@ -278,9 +278,7 @@ int qt_rmsnorm_quant_i4(const void* x, int x_is_f64, int ld_x, const float* gain
  * int8 operands via TMA (2-SM cta_group::2 pairs for M >= 8192; the prefill GEMM);
  * 4 = impl 3 with split-K (decode batches up to 512 tokens: k slices across CTAs, int32
  * partials reduced in fixed order).  Impls 3 and 4
- * widen the operands to int8 in temporary buffers first (the engine keeps them).
- * 5 = the decode GEMV (<= 64 tokens) on weights already in the row-block-major tile
- * order (qt_w4t_to_rbm: a row block's K range contiguous). */
+ * widen the operands to int8 in temporary buffers first (the engine keeps them). */
 int qt_w4a4_gemm(int epilogue, const uint8_t* a_codes, int lda, const double* a_scales, const uint8_t* w_codes,
                  int ldw, const double* w_scales, int M, int N, int K, void* out, int ldo, int32_t* acc_out,
                  int impl, void* stream);
@@ -294,9 +292,6 @@ int qt_w4a4_gemm_i8(int epi, const int8_t* a8, int lda8, const double* sa, const
                     const double* sw, int M, int N, int K, void* out, int ldo, int32_t* acc_out, int* workspace,
                     int flags, void* stream);
 int64_t qt_w4a4_gemm_i8_workspace(int M, int N, int K);
-/* tiled int4 weights [rows_pad x K] -> row-block-major tile order (tile (rb, kt) at
- * (rb * K/128 + kt) * 1 KB), the decode GEMV's weight stream */
-int qt_w4t_to_rbm(const uint8_t* tiled, int rows_pad, int K, uint8_t* out, void* stream);
 int qt_quant_weight_i4(const float* w, int K, int N, int row_mul, int row_add, uint8_t* codes, int ldc,
                        double* scales, double* scratch, void* stream);
 int qt_kv_quant_append_i4(float* qkv, int ld_qkv, int M, int H, int Hkv, int d_head, const int* positions,

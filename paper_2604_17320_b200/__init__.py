@@ -109,7 +109,6 @@ def lib():
         L.qt_engine_set_token_table.argtypes = [vp, vp, C.c_int, C.c_int]
         L.qt_engine_set_graphs.argtypes = [vp, C.c_int]
         L.qt_engine_decode_greedy.argtypes = [vp, vp, vp, C.c_int]
-        L.qt_w4t_to_rbm.argtypes = [vp, C.c_int, C.c_int, vp, vp]
         L.qt_engine_capture.argtypes = [vp, C.c_int]
         L.qt_engine_capture_count.argtypes = [vp]
         L.qt_engine_capture_get.argtypes = [vp, C.c_int, ip, vp, dp]
@@ -509,14 +508,6 @@ def w4a4_gemm_i8(epi, a8, sa, w8, sw, M, N, K, out, acc_out=None, workspace=None
     check(lib().qt_w4a4_gemm_i8(epi, _ptr(a8), a8.shape[1], _ptr(sa), _ptr(w8), w8.shape[0], w8.shape[1], _ptr(sw),
                                 M, N, K, _ptr(out), out.stride(0), _ptr(acc_out), _ptr(workspace),
                                 int(single) | (int(ksplit) << 8), C.c_void_p(stream)))
-    return out
-
-
-def w4t_to_rbm(tiled, K, stream=0):
-    """qt_w4t_to_rbm: tiled int4 weights (k-block-major) -> row-block-major tile order."""
-    import torch
-    out = torch.empty_like(tiled)
-    check(lib().qt_w4t_to_rbm(_ptr(tiled), tiled.shape[0], K, _ptr(out), C.c_void_p(stream)))
     return out
 
 

@@ -2545,12 +2545,6 @@ int qt_w4a4_gemm(int epi, const uint8_t* a, int lda, const double* sa, const uin
             ckl(rc, "w4a4 gemm (int8 operands)");
             return;
         }
-        if (impl == 5) {  // decode GEMV on weights in the row-block-major tile order (qt_w4t_to_rbm)
-            ckl(qt_launch_w4a4_gemv_rbm(epi, a, lda, sa, w, ldw, sw, M, N, K, out, ldo, acc_out, nullptr, 0, nullptr,
-                                        cs),
-                "w4a4 gemv (row-block-major)");
-            return;
-        }
         int* ws = nullptr;  // impl 2: tcgen05 with split-K (a grow-only ABI-level workspace, so a
                             // timing loop over one shape allocates once)
         if (impl == 2) {
@@ -2593,9 +2587,6 @@ int64_t qt_w4a4_gemm_i8_workspace(int M, int N, int K) {
     return ks > 1 ? (int64_t)ks * M * N * (int64_t)sizeof(int) : 0;
 }
 
-int qt_w4t_to_rbm(const uint8_t* tiled, int rows_pad, int K, uint8_t* out, void* stream) {
-    return guard([&] { ckl(qt_launch_w4t_to_rbm(tiled, rows_pad, K, out, (cudaStream_t)stream), "tile reorder"); });
-}
 
 int qt_quant_weight_i4(const float* w, int K, int N, int row_mul, int row_add, uint8_t* codes, int ldc,
                        double* scales, double* scratch, void* stream) {

@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(256, NT <= 2 ? QT_GEMV_MINB : 1) k_gemv_reg(co
                                                   const uint8_t* __restrict__ W, int ldw, const double* __restrict__ sw,
                                                   int M, int N, int K, void* __restrict__ out, int ldo,
                                                   int* __restrict__ acc_dbg, int l2rows,
-                                                  float* __restrict__ pmax, int pmax_ld, int rbm) {
+                                                  float* __restrict__ pmax, int pmax_ld) {
     constexpr int TOK = 8 * NT;
     constexpr bool ASM = NT <= 2 && !AREG;  // activation codes staged in smem
     constexpr int U = NT <= 2 ? 4 : 2;
@@ -202,8 +202,7 @@ __global__ void __launch_bounds__(256, NT <= 2 ? QT_GEMV_MINB : 1) k_gemv_reg(co
         for (int u = 0; u < U; ++u) {
             const int c = ch0 + bat * U + u;
             const bool ok = rb < n_rb && c < ch1;
-            // rbm: row-block-major weight tiles (a row block's K range contiguous), else k-block-major
-            const uint8_t* tile = W + (rbm ? (size_t)rb * KT + c : (size_t)c * (ldw >> 4) + rb) * 1024 + g * 64 + tig * 16;
+            const uint8_t* tile = W + ((size_t)c * (ldw >> 4) + rb) * 1024 + g * 64 + tig * 16;
             xa[u] = ok ? ldg_nc_v4(tile) : make_uint4(0, 0, 0, 0);
             xb[u] = ok ? ldg_nc_v4(tile + 512) : make_uint4(0, 0, 0, 0);
         }
@@ -217,12 +216,12 @@ __global__ void __launch_bounds__(256, NT <= 2 ? QT_GEMV_MINB : 1) k_gemv_reg(co
             const int r2 = blockIdx.x + j * gridDim.x;
             if (r2 >= n_rb) break;
             for (int c = ch0 + (lane >> 3); c < ch1; c += 4)  // 8 lanes x 128 B per 1 KB tile
-                asm volatile("prefetch.global.L2 [%0];\n" ::"l"(W + (rbm ? (size_t)r2 * KT + c : (size_t)c * (ldw >> 4) + r2) * 1024 +
+                asm volatile("prefetch.global.L2 [%0];\n" ::"l"(W + ((size_t)c * (ldw >> 4) + r2) * 1024 +
                                                                (lane & 7) * 128));
         }
         if (nbat > 1)  // and the rest of the first row block beyond the register batch
             for (int c = ch0 + U + (lane >> 3); c < ch1; c += 4)
-                asm volatile("prefetch.global.L2 [%0];\n" ::"l"(W + (rbm ? (size_t)rb * KT + c : (size_t)c * (ldw >> 4) + rb) * 1024 +
+                asm volatile("prefetch.global.L2 [%0];\n" ::"l"(W + ((size_t)c * (ldw >> 4) + rb) * 1024 +
                                                                (lane & 7) * 128));
     }
     pdl_wait();
@@ -374,7 +373,7 @@ __global__ void __launch_bounds__(256, NT <= 2 ? QT_GEMV_MINB : 1) k_gemv_reg(co
 template <int EPI>
 int launch_gemm(const uint8_t* A, int lda, const double* sa, const uint8_t* W, int ldw, const double* sw, int M,
                 int N, int K, void* out, int ldo, int* acc_dbg, cudaStream_t st, float* pmax = nullptr,
-                int pmax_ld = 0, int* n_part = nullptr, int rbm = 0) {
+                int pmax_ld = 0, int* n_part = nullptr) {
     if (n_part) *n_part = 0;
     if (M <= 0) return 0;
     if (K % 128 || lda % 16 || ldw % 16 || M > lda || N > ldw) return -1;  // lda/ldw = padded rows
@@ -398,7 +397,7 @@ int launch_gemm(const uint8_t* A, int lda, const double* sa, const uint8_t* W, i
             auto kfn = k_gemv_reg<4, EPI>;
             cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             return launch_pdl(kfn, grid, dim3(256), smem, st, A, lda, sa, W, ldw, sw, M, N, K, out, ldo, acc_dbg,
-                              kGemvL2Rows, pm, pmax_ld, rbm);
+                              kGemvL2Rows, pm, pmax_ld);
         }
         if (lda >= 64) {
             want_pmax((int)grid.x);
@@ -406,7 +405,7 @@ int launch_gemm(const uint8_t* A, int lda, const double* sa, const uint8_t* W, i
             auto kfn = k_gemv_reg<8, EPI>;
             cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             return launch_pdl(kfn, grid, dim3(256), smem, st, A, lda, sa, W, ldw, sw, M, N, K, out, ldo, acc_dbg,
-                              kGemvL2Rows, pm, pmax_ld, rbm);
+                              kGemvL2Rows, pm, pmax_ld);
         }
     }
     if (M <= 16) {
@@ -424,20 +423,19 @@ int launch_gemm(const uint8_t* A, int lda, const double* sa, const uint8_t* W, i
             auto kfn = k_gemv_reg<1, EPI, true>;
             cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
             return launch_pdl(kfn, grid, dim3(256), smem2, st, A, lda, sa, W, ldw, sw, M, N, K, out, ldo, acc_dbg,
-                              kGemvL2Rows, pm, pmax_ld, rbm);
+                              kGemvL2Rows, pm, pmax_ld);
         }
         if (TOK == 8) {
             auto kfn = k_gemv_reg<1, EPI>;
             cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             return launch_pdl(kfn, grid, dim3(256), smem, st, A, lda, sa, W, ldw, sw, M, N, K, out, ldo, acc_dbg,
-                              kGemvL2Rows, pm, pmax_ld, rbm);
+                              kGemvL2Rows, pm, pmax_ld);
         }
         auto kfn = k_gemv_reg<2, EPI>;
         cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         return launch_pdl(kfn, grid, dim3(256), smem, st, A, lda, sa, W, ldw, sw, M, N, K, out, ldo, acc_dbg,
-                              kGemvL2Rows, pm, pmax_ld, rbm);
+                              kGemvL2Rows, pm, pmax_ld);
     }
-    if (rbm) return -1;  // the row-block-major copy serves the GEMV only
     if (M <= 512 || (long long)((M + 127) / 128) * nb < 148) {
         constexpr int BM = 64;
         const size_t smem = (size_t)G_STAGES * (BM + GB_N) * G_ROWB;
@@ -477,46 +475,6 @@ extern "C" int qt_launch_w4a4_mma_ex(int epi, const uint8_t* A, int lda, const d
                                               n_part);
     }
     return -1;
-}
-
-// the decode GEMV (M <= 64) on a row-block-major weight copy (qt_launch_w4t_to_rbm)
-extern "C" int qt_launch_w4a4_gemv_rbm(int epi, const uint8_t* A, int lda, const double* sa, const uint8_t* W,
-                                       int ldw, const double* sw, int M, int N, int K, void* out, int ldo,
-                                       int* acc_dbg, float* pmax, int pmax_ld, int* n_part, cudaStream_t st) {
-    using namespace qt;
-    if (M > 64) return -1;
-    switch (epi) {
-        case QT_EPI_STORE:
-            return launch_gemm<QT_EPI_STORE>(A, lda, sa, W, ldw, sw, M, N, K, out, ldo, acc_dbg, st, pmax, pmax_ld,
-                                             n_part, 1);
-        case QT_EPI_RESADD:
-            return launch_gemm<QT_EPI_RESADD>(A, lda, sa, W, ldw, sw, M, N, K, out, ldo, acc_dbg, st, nullptr, 0,
-                                              n_part, 1);
-        case QT_EPI_SILU:
-            return launch_gemm<QT_EPI_SILU>(A, lda, sa, W, ldw, sw, M, N, K, out, ldo, acc_dbg, st, pmax, pmax_ld,
-                                            n_part, 1);
-        case QT_EPI_SWIGLU:
-            return launch_gemm<QT_EPI_SWIGLU>(A, lda, sa, W, ldw, sw, M, N, K, out, ldo, acc_dbg, st, pmax, pmax_ld,
-                                              n_part, 1);
-    }
-    return -1;
-}
-
-// k-block-major tiled int4 weights -> row-block-major (tile (rb, kt) at (rb * KT + kt) * 1 KB)
-__global__ void k_w4t_to_rbm(const uint8_t* __restrict__ in, int rows_pad, int K, uint8_t* __restrict__ out) {
-    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // one 16-byte chunk
-    const int KT = K / 128, RB = rows_pad / 16;
-    if (i >= (long long)RB * KT * 64) return;
-    const long long t = i / 64;  // destination tile
-    const int rb = (int)(t / KT), kt = (int)(t % KT);
-    reinterpret_cast<uint4*>(out)[i] = reinterpret_cast<const uint4*>(in)[((long long)kt * RB + rb) * 64 + i % 64];
-}
-
-extern "C" int qt_launch_w4t_to_rbm(const uint8_t* in, int rows_pad, int K, uint8_t* out, cudaStream_t st) {
-    const long long n = (long long)(rows_pad / 16) * (K / 128) * 64;
-    if (n <= 0) return 0;
-    k_w4t_to_rbm<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(in, rows_pad, K, out);
-    return (int)cudaGetLastError();
 }
 
 extern "C" int qt_launch_w4a4_mma(int epi, const uint8_t* A, int lda, const double* sa, const uint8_t* W, int ldw,

@@ -64,11 +64,6 @@ int qt_launch_w4a4_tc05_ex(int epi, const uint8_t* A, int lda, const double* sa,
 int qt_launch_quant_pmax(const float* x, int ld_x, const float* pmax, int n_part, int pmax_ld, int M, int D,
                          int d_pad, int qmax, int mode, double static_scale, uint8_t* codes, int ld_codes,
                          double* scales, int8_t* codes8, int ld8, cudaStream_t st);
-// decode GEMV on a row-block-major weight copy (made by qt_launch_w4t_to_rbm)
-int qt_launch_w4a4_gemv_rbm(int epi, const uint8_t* A, int lda, const double* sa, const uint8_t* W, int ldw,
-                            const double* sw, int M, int N, int K, void* out, int ldo, int* acc_dbg, float* pmax,
-                            int pmax_ld, int* n_part, cudaStream_t st);
-int qt_launch_w4t_to_rbm(const uint8_t* in, int rows_pad, int K, uint8_t* out, cudaStream_t st);
 int qt_launch_w4a4_mma(int epi, const uint8_t* A, int lda, const double* sa, const uint8_t* W, int ldw,
                        const double* sw, int M, int N, int K, void* out, int ldo, int* acc_dbg, cudaStream_t st);
 // ws (nullable): int32 split-K workspace of qt_tc05_splitk(M, N, K) * M * N entries; with ws the

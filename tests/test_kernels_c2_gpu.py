@@ -317,29 +317,3 @@ def test_unpack_codes_roundtrip(torch_cuda):
     got = Q.unpack_codes(t, 37, 640)
     torch.cuda.synchronize()
     assert np.array_equal(got.cpu().numpy(), c)
-
-
-@pytest.mark.parametrize("M,K,N,epi", [(8, 4096, 12288, Q.EPI_STORE), (8, 11008, 4096, Q.EPI_RESADD),
-                                       (5, 4096, 22016, Q.EPI_SWIGLU), (40, 4096, 4096, Q.EPI_STORE)])
-def test_decode_gemv_row_block_major_matches(torch_cuda, M, K, N, epi):
-    """The GEMV on the row-block-major tile order (qt_w4t_to_rbm, impl 5) is bit-identical to the
-    k-block-major one (impl 0): int32 accumulators and outputs."""
-    torch = torch_cuda
-    from tests.test_kernels_gpu import _tiled
-    rng = np.random.default_rng(K + N + M)
-    a = rng.integers(-7, 8, size=(M, K))
-    w = rng.integers(-7, 8, size=(N, K))
-    sa = torch.from_numpy(rng.uniform(0.01, 0.5, M)).cuda()
-    sw = torch.from_numpy(rng.uniform(0.001, 0.01, N)).cuda()
-    ad = torch.from_numpy(_tiled(a, pad=64)).cuda()
-    wd = torch.from_numpy(_tiled(w, 128)).cuda()
-    outs = []
-    for impl, wt in ((0, wd), (5, Q.w4t_to_rbm(wd, K))):
-        shape = (M, N // 2) if epi == Q.EPI_SWIGLU else (M, N)
-        out = torch.ones(shape, dtype=torch.float64 if epi == Q.EPI_RESADD else torch.float32, device="cuda")
-        acc = torch.zeros((M, N), dtype=torch.int32, device="cuda")
-        Q.w4a4_gemm(epi, ad, sa, wt, sw, M, N, K, out, acc, impl=impl)
-        torch.cuda.synchronize()
-        outs.append((acc.cpu().numpy(), out.cpu().numpy()))
-    assert np.array_equal(outs[0][0], a.astype(np.int64) @ w.T.astype(np.int64))
-    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])

@@ -13,8 +13,6 @@ def run(N, K, epi, copies, iters=64, impl=0):
     a = (torch.randint(0, 256, (rows, K // 2), dtype=torch.uint8, device="cuda") & 0x77)
     ws = [(torch.randint(0, 256, ((N + 127) // 128 * 128, K // 2), dtype=torch.uint8, device="cuda") & 0x77)
           for _ in range(copies)]
-    if impl == 5:
-        ws = [Q.w4t_to_rbm(w, K) for w in ws]
     sa = torch.rand(M, dtype=torch.float64, device="cuda")
     sw = torch.rand(ws[0].shape[0], dtype=torch.float64, device="cuda")
     if epi == Q.EPI_RESADD:
@@ -48,8 +46,8 @@ for N, K, epi, name in [(12288, 4096, Q.EPI_STORE, "qkv"), (4096, 4096, Q.EPI_RE
                         (22016, 4096, Q.EPI_SWIGLU, "gu"), (4096, 11008, Q.EPI_RESADD, "down")]:
     wb = (N + 127) // 128 * 128 * K // 2
     cold = max(2, int(400e6 // wb) + 1)
-    for impl in (0, 5):
+    for impl in (0,):
         uw, gw = run(N, K, epi, 1, impl=impl)
         uc, gc = run(N, K, epi, cold, impl=impl)
-        print(f"{name:5s} {'kbm' if impl == 0 else 'rbm'} M={M} N={N} K={K} {wb/1e6:6.1f} MB  warm {uw:7.2f} us "
+        print(f"{name:5s} M={M} N={N} K={K} {wb/1e6:6.1f} MB  warm {uw:7.2f} us "
               f"{gw:7.0f} GB/s   cold {uc:7.2f} us {gc:7.0f} GB/s", flush=True)
