@@ -139,7 +139,7 @@ def load_traffic():
             M, N, K = 8, 12288, 4096
             r["algorithmic_bytes"] = N * K / 2 + 8 * N + M * K / 2 + 8 * M + 4 * M * N
             out["gemv"] = r
-        elif "k_attn_decode" in k:
+        elif "k_attn_dec" in k:  # decode attention (k_attn_dec; r01: k_attn_decode_pp2)
             out["attn_decode"] = dict(r, algorithmic_bytes=r["dram_bytes"])
     return out
 
@@ -475,10 +475,13 @@ def run_ours(args, cfg):
         achieved = alg / (avg_ms / 1e3) / 1e9
         traffic, tsrc = None, None
         ref = traffic_db.get("gemv" if cls == "gemm" else "attn_decode")
+        if cls == "gemm" and B > 32:  # the capture is of the GEMV, not the int8 tcgen05 decode GEMM
+            ref = None
         if ref:  # ncu --set full capture of one launch: DRAM bytes / algorithmic bytes of that launch
             ratio = ref["dram_bytes"] / ref["algorithmic_bytes"]
             traffic, tsrc = alg * ratio, f"{ref['source']}: dram/algorithmic = {ratio:.3f} on {ref['kernel']}"
-        roofline = {"bound": "hbm", "kernel": f"{phase} {cls} (W4A4 GEMV, k_gemv_reg)" if cls == "gemm"
+        gname = "W4A4 GEMV, k_gemv_reg" if B <= 32 else "int8-operand tcgen05 GEMM, k_gemm_tc05_i8"
+        roofline = {"bound": "hbm", "kernel": f"{phase} {cls} ({gname})" if cls == "gemm"
                     else f"{phase} {cls}", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                     "traffic": traffic, "traffic_source": tsrc, "peak_source": peak_src,
                     "algorithmic_bytes_per_launch": alg, "avg_launch_ms": avg_ms,
