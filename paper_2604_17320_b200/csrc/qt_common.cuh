@@ -248,6 +248,23 @@ QT_DEV uint4 ldg_nc_v4(const void* p) {
     return r;
 }
 
+// 256-bit global accesses (sm_100: LDG/STG.E.ENL2.256): one full 32-byte sector per thread
+// and instruction -- the row-per-thread GEMM epilogues touch 32 rows per warp instruction
+QT_DEV double4 ld_v4f64(const double* p) {
+    double4 r;
+    asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];\n" : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w) : "l"(p));
+    return r;
+}
+QT_DEV void st_v4f64(double* p, double4 v) {
+    asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};\n" ::"l"(p), "d"(v.x), "d"(v.y), "d"(v.z), "d"(v.w)
+                 : "memory");
+}
+QT_DEV void st_v8f32(float* p, const float* v) {
+    asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n" ::"l"(p), "f"(v[0]), "f"(v[1]), "f"(v[2]),
+                 "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+                 : "memory");
+}
+
 QT_DEV float silu_f(float x) { return x / (1.0f + expf(-x)); }
 
 // ---------------------------------------------------------------- PDL

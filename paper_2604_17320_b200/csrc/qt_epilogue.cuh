@@ -78,50 +78,79 @@ template <int EPI>
 QT_DEV void epi_row32(void* __restrict__ outv, int ldo, int m, int n, const uint32_t* r, double a_s,
                       const double* swt, float& mx) {
     if (EPI == QT_EPI_RESADD) {
-        double2* p = reinterpret_cast<double2*>(static_cast<double*>(outv) + (size_t)m * ldo + n);
+        double* p = static_cast<double*>(outv) + (size_t)m * ldo + n;
+        if ((reinterpret_cast<uintptr_t>(p) & 31) == 0) {  // 256-bit row accesses: full sectors
+#pragma unroll
+            for (int e = 0; e < 32; e += 8) {
+                double4 v0 = ld_v4f64(p + e), v1 = ld_v4f64(p + e + 4);
+                double* w0 = &v0.x;
+                double* w1 = &v1.x;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    w0[u] += i2d_exact((int)r[e + u] >> 8) * (a_s * swt[e + u]);
+                    w1[u] += i2d_exact((int)r[e + 4 + u] >> 8) * (a_s * swt[e + 4 + u]);
+                }
+                st_v4f64(p + e, v0);
+                st_v4f64(p + e + 4, v1);
+            }
+            return;
+        }
+        double2* p2 = reinterpret_cast<double2*>(p);
 #pragma unroll
         for (int e = 0; e < 32; e += 8) {
             double2 v[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) v[u] = p[e / 2 + u];
+            for (int u = 0; u < 4; ++u) v[u] = p2[e / 2 + u];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 v[u].x += i2d_exact((int)r[e + 2 * u] >> 8) * (a_s * swt[e + 2 * u]);
                 v[u].y += i2d_exact((int)r[e + 2 * u + 1] >> 8) * (a_s * swt[e + 2 * u + 1]);
             }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) p[e / 2 + u] = v[u];
+            for (int u = 0; u < 4; ++u) p2[e / 2 + u] = v[u];
         }
         return;
     }
     float* out = static_cast<float*>(outv);
     if (EPI == QT_EPI_SWIGLU) {
-        float4* p = reinterpret_cast<float4*>(out + (size_t)m * ldo + n / 2);
+        float* pf = out + (size_t)m * ldo + n / 2;
+        const bool wide = (reinterpret_cast<uintptr_t>(pf) & 31) == 0;
 #pragma unroll
-        for (int e = 0; e < 32; e += 8) {
-            float v[4];
+        for (int e = 0; e < 32; e += 16) {
+            float v[8];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < 8; ++u) {
                 const double g = i2d_exact((int)r[e + 2 * u] >> 8) * (a_s * swt[e + 2 * u]);
                 const double up = i2d_exact((int)r[e + 2 * u + 1] >> 8) * (a_s * swt[e + 2 * u + 1]);
                 v[u] = silu_f32(g) * (float)up;
                 mx = fmaxf(mx, fabsf(v[u]));
             }
-            p[e / 8] = make_float4(v[0], v[1], v[2], v[3]);
+            if (wide) {
+                st_v8f32(pf + e / 2, v);
+            } else {
+                reinterpret_cast<float4*>(pf + e / 2)[0] = make_float4(v[0], v[1], v[2], v[3]);
+                reinterpret_cast<float4*>(pf + e / 2)[1] = make_float4(v[4], v[5], v[6], v[7]);
+            }
         }
         return;
     }
-    float4* p = reinterpret_cast<float4*>(out + (size_t)m * ldo + n);
+    float* pf = out + (size_t)m * ldo + n;
+    const bool wide = (reinterpret_cast<uintptr_t>(pf) & 31) == 0;
 #pragma unroll
-    for (int e = 0; e < 32; e += 4) {
-        float v[4];
+    for (int e = 0; e < 32; e += 8) {
+        float v[8];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < 8; ++u) {
             const double y = i2d_exact((int)r[e + u] >> 8) * (a_s * swt[e + u]);
             v[u] = EPI == QT_EPI_SILU ? silu_f32(y) : (float)y;
             mx = fmaxf(mx, fabsf(v[u]));
         }
-        p[e / 4] = make_float4(v[0], v[1], v[2], v[3]);
+        if (wide) {
+            st_v8f32(pf + e, v);
+        } else {
+            reinterpret_cast<float4*>(pf + e)[0] = make_float4(v[0], v[1], v[2], v[3]);
+            reinterpret_cast<float4*>(pf + e)[1] = make_float4(v[4], v[5], v[6], v[7]);
+        }
     }
 }
 
