@@ -89,13 +89,17 @@ QT_DEV int q_code(double x, double s, int qmax) {
 // lies within 1e-4 of a .5 tie, rint() of both agrees; |q| >= 8 clamps either
 // way.  Near-ties take the fp64 path: x * (1/s), and the correctly rounded
 // x / s when even that sits within 1e-9 of the tie.
+// The fp32 rounding is the 1.5 * 2^23 magic add (round half to even, exact for |q| < 2^22 --
+// the quotient is first clamped to [-(qmax + 1), qmax + 1]); the integer is read from the
+// sum's mantissa and the distance to the rounded value (exact) is the tie test: no F2I or
+// FRND in the fast path.
 QT_DEV int q_code_r(double x, double s, double inv_s, int qmax) {
     const float qf = (float)x * (float)inv_s;
-    const float af = fabsf(qf);
-    if (af >= (float)qmax + 1.0f) return qf > 0.f ? qmax : -qmax;
-    const float ff = af - floorf(af);
-    if (fabsf(ff - 0.5f) > 1e-4f) {
-        const int c = (int)rintf(qf);
+    const float lim = (float)qmax + 1.0f;
+    const float qc = fminf(fmaxf(qf, -lim), lim);
+    const float t = qc + 12582912.0f;
+    if (fabsf(qc - (t - 12582912.0f)) < 0.4999f) {
+        const int c = __float_as_int(t) - 0x4B400000;
         return c > qmax ? qmax : (c < -qmax ? -qmax : c);
     }
     double q = x * inv_s;
