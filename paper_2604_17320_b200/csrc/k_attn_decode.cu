@@ -31,6 +31,10 @@ namespace qt {
 #endif
 constexpr int AD_THREADS = 256;
 constexpr int AD_MAX_PPS = 8;  // pages per split (smem: 8.5 KB each at d_head 128)
+#ifndef QT_AD_PLAN_PPS
+#define QT_AD_PLAN_PPS 2  // the split plan's page cap (A/B 8 / 2 / 1 pages: C5 B = 256 decode chain
+                          // 9.76 / 9.32 / 10.68 ms per step; C2, C4 equal within noise)
+#endif
 constexpr int AD_MAX_G = 8;    // query heads per kv head (one softmax warp each)
 
 // 8 signed nibbles of w -> 8 exact floats
@@ -427,7 +431,7 @@ int qt_attn_decode_plan(int B, int Hkv, int pages, int sms, int* pps, int* nspli
     // arrival: tools/gpu_attn_ab.sh)
     int ns = std::max(1, std::min(pages, (QT_AD_CTA_MULT * sms + B * Hkv - 1) / (B * Hkv)));
     int p = (pages + ns - 1) / ns;
-    if (p > AD_MAX_PPS) p = AD_MAX_PPS;
+    if (p > QT_AD_PLAN_PPS) p = QT_AD_PLAN_PPS;
     ns = (pages + p - 1) / p;
     *pps = p;
     *nsplit = ns;
