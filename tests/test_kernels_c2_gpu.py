@@ -194,6 +194,9 @@ DECODE_SHAPES = [  # (H, Hkv, dh, lens): C2 (237 + t), C5 long context, C4 GQA, 
     (32, 32, 128, [2285, 1000]),
     (28, 4, 128, [300, 1344, 77, 64]),
     (4, 2, 64, [84, 150, 1, 63]),
+    # enough work units for the persistent, double-buffered grid (units > 2 waves of CTAs)
+    (32, 32, 128, [300, 64, 1, 129, 511, 257] * 8),
+    (28, 4, 128, [700, 65, 1290, 3] * 16),
 ]
 
 
