@@ -52,20 +52,12 @@ QT_DEV void load_kv_tile(const uint8_t* page, int Hkv, int kh, int nkeys, __half
         uint4 w = row < nkeys ? *reinterpret_cast<const uint4*>(kc + (size_t)c * 16) : make_uint4(0, 0, 0, 0);
         uint32_t* dst = reinterpret_cast<uint32_t*>(Ks + row * KLD + col);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            uint32_t word = (&w.x)[q];
-#pragma unroll
-            for (int bb = 0; bb < 4; ++bb) dst[q * 4 + bb] = nib2_to_h2((word >> (8 * bb)) & 0xFF);
-        }
+        for (int q = 0; q < 4; ++q) word_to_h2_pairs((&w.x)[q], dst + q * 4);
         if (need_v) {  // row-major like K; the PV MMA reads it transposed with ldmatrix.trans
             uint4 v = row < nkeys ? *reinterpret_cast<const uint4*>(vc + (size_t)c * 16) : make_uint4(0, 0, 0, 0);
             uint32_t* vd = reinterpret_cast<uint32_t*>(Vt + row * KLD + col);
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                uint32_t word = (&v.x)[q];
-#pragma unroll
-                for (int bb = 0; bb < 4; ++bb) vd[q * 4 + bb] = nib2_to_h2((word >> (8 * bb)) & 0xFF);
-            }
+            for (int q = 0; q < 4; ++q) word_to_h2_pairs((&v.x)[q], vd + q * 4);
         }
     }
     for (int r = threadIdx.x; r < AT_K; r += blockDim.x) {
@@ -109,11 +101,8 @@ QT_DEV void dequant_kv_raw(const uint8_t* raw, int nkeys, __half* Ks, __half* Vt
         uint32_t* vd = reinterpret_cast<uint32_t*>(Vt + row * KLD + col);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-#pragma unroll
-            for (int bb = 0; bb < 4; ++bb) {
-                kd[q * 4 + bb] = nib2_to_h2(((&w.x)[q] >> (8 * bb)) & 0xFF);
-                vd[q * 4 + bb] = nib2_to_h2(((&v.x)[q] >> (8 * bb)) & 0xFF);
-            }
+            word_to_h2_pairs((&w.x)[q], kd + q * 4);
+            word_to_h2_pairs((&v.x)[q], vd + q * 4);
         }
     }
     const float* sc = reinterpret_cast<const float*>(raw + 2 * CB);

@@ -225,6 +225,24 @@ QT_DEV void split_h2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
     lo = h2_as_u32(l);
 }
 
+// 8 nibbles of one word (channel e at bits 4e) -> 4 exact half2 of consecutive channel pairs
+// (2j, 2j + 1): byte j of w and of w >> 4 go to the two halves (PRMT), their low nibbles
+// offset by 8 into the mantissas of fp16 1024 (LOP3 0x6A: b ? a ^ c : c), and the magic
+// 1032 is subtracted (HSUB2) -- 3 instructions per pair, no I2F
+QT_DEV void word_to_h2_pairs(uint32_t w, uint32_t* h) {  // h: 16-byte aligned (one uint4 store)
+    const uint32_t w4 = w >> 4;
+    uint32_t o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const uint32_t z = __byte_perm(w, w4, (uint32_t)(j | ((4 + j) << 8)));
+        uint32_t m;
+        asm("lop3.b32 %0, %1, %2, %3, 0x6A;\n" : "=r"(m) : "r"(z), "r"(0x000F000Fu), "r"(0x64086408u));
+        const __half2 r = __hsub2(*reinterpret_cast<const __half2*>(&m), __half2half2(__ushort_as_half(0x6408)));
+        o[j] = *reinterpret_cast<const uint32_t*>(&r);
+    }
+    *reinterpret_cast<uint4*>(h) = make_uint4(o[0], o[1], o[2], o[3]);
+}
+
 // int4 nibble pair (one byte: even k low, odd k high) -> half2(code_even, code_odd)
 QT_DEV uint32_t nib2_to_h2(uint32_t byte) {
     int lo = ((int)(byte << 28)) >> 28;
