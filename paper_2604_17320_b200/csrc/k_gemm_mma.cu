@@ -174,7 +174,7 @@ constexpr int kGemvL2Rows = 1;
 // k slice are loaded once into registers after the dependency wait -- no smem staging, no
 // block barrier before the first MMA.
 template <int NT, int EPI, bool AREG = false>
-__global__ void __launch_bounds__(256, NT <= 2 ? QT_GEMV_MINB : 1) k_gemv_reg(const uint8_t* __restrict__ A, int lda, const double* __restrict__ sa,
+__global__ void __launch_bounds__(256, (NT <= 2 && !(AREG && NT == 2)) ? QT_GEMV_MINB : 1) k_gemv_reg(const uint8_t* __restrict__ A, int lda, const double* __restrict__ sa,
                                                   const uint8_t* __restrict__ W, int ldw, const double* __restrict__ sw,
                                                   int M, int N, int K, void* __restrict__ out, int ldo,
                                                   int* __restrict__ acc_dbg, int l2rows,
@@ -417,7 +417,20 @@ int launch_gemm(const uint8_t* A, int lda, const double* sa, const uint8_t* W, i
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
         const dim3 grid(std::min(n_rb, QT_GEMV_MINB * sms));
         want_pmax((int)grid.x);
-        // AREG: K <= 4096 is one register batch per warp (the 9..16-token variant spills)
+#ifndef QT_GEMV_AREG2
+#define QT_GEMV_AREG2 1  // CTAs per SM of the 9..16-token AREG GEMV (0: the smem-staged one).
+                         // A/B (tools/gpu_attn_ab.sh): C4 decode 2.10 -> 2.04 ms/step, C5 B = 16
+                         // 2.19 -> 2.05 ms/step at 1; 2 (two waves) 2.17 / 2.17
+#endif
+        // AREG: K <= 4096 is one register batch per warp (the 9..16-token variant spills at 2
+        // CTAs per SM -- 183 registers -- so it runs one CTA per SM)
+        if (QT_GEMV_AREG2 && TOK == 16 && (K / 128 + 7) / 8 <= 4) {
+            const size_t smem2 = (size_t)2 * 8 * 16 * TOK * 4;
+            auto kfn = k_gemv_reg<2, EPI, true>;
+            cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
+            return launch_pdl(kfn, dim3(std::min(n_rb, QT_GEMV_AREG2 * sms)), dim3(256), smem2, st, A, lda, sa, W,
+                              ldw, sw, M, N, K, out, ldo, acc_dbg, kGemvL2Rows, pm, pmax_ld);
+        }
         if (TOK == 8 && (K / 128 + 7) / 8 <= 4) {
             const size_t smem2 = (size_t)2 * 8 * 16 * TOK * 4;  // split-K reduction buffers only
             auto kfn = k_gemv_reg<1, EPI, true>;

@@ -276,7 +276,7 @@ def _ref_fused(m4, w):
     return w[0] * norm[0] + w[1] * norm[1] + w[2] * norm[2] + w[3] * norm[3]
 
 
-@pytest.mark.parametrize("M", [1, 5, 8])
+@pytest.mark.parametrize("M", [1, 5, 8, 12, 16])
 @pytest.mark.parametrize("K,N,epi", [(4096, 4096, Q.EPI_RESADD), (11008, 4096, Q.EPI_RESADD),
                                      (4096, 12288, Q.EPI_STORE), (4096, 22016, Q.EPI_SWIGLU)])
 def test_decode_gemv_7b_shapes_int32_exact(torch_cuda, M, K, N, epi):

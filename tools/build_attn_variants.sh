@@ -7,13 +7,14 @@ cd "$(dirname "$0")/.."
 B=paper_2604_17320_b200/_build
 FLAGS="-std=c++17 -O3 -lineinfo -gencode arch=compute_100a,code=sm_100a -Xcompiler -fPIC --expt-relaxed-constexpr -Iinclude"
 make -C paper_2604_17320_b200/csrc -j8 > /dev/null
-OTHERS=$(ls $B/*.o | grep -v k_attn_decode.o)
+SRC=${VARIANT_SRC:-k_attn_decode}   # the csrc/<SRC>.cu file the variants rebuild
+OTHERS=$(ls $B/*.o | grep -v "/$SRC.o")
 # VARIANTS: ';'-separated name:defines list
 IFS=';' read -ra VL <<< "${VARIANTS:-m2:-DQT_AD_CTA_MULT=2;m4:-DQT_AD_CTA_MULT=4;m8:-DQT_AD_CTA_MULT=8}"
 for v in "${VL[@]}"; do
   name=${v%%:*}; defs=${v#*:}
   out=paper_2604_17320_b200/_build_var/$name; mkdir -p $out
-  /usr/local/cuda/bin/nvcc $FLAGS $defs -c paper_2604_17320_b200/csrc/k_attn_decode.cu -o $out/k_attn_decode.o
-  /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared $OTHERS $out/k_attn_decode.o -o $out/libquota_b200.so -lcudart -lcublas -Xlinker -rpath,/usr/local/cuda/lib64
+  /usr/local/cuda/bin/nvcc $FLAGS $defs -c paper_2604_17320_b200/csrc/$SRC.cu -o $out/$SRC.o
+  /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared $OTHERS $out/$SRC.o -o $out/libquota_b200.so -lcudart -lcublas -Xlinker -rpath,/usr/local/cuda/lib64
   echo built $name
 done
