@@ -305,313 +305,6 @@ __global__ void __launch_bounds__(32 * AT_QW, AT_QW > 4 ? 1 : QT_ATTN_MINB) k_at
     }
 }
 
-// ============================================================== K7 on tcgen05 (d_head 128)
-// One CTA per (128-query tile, head, sequence); thread i owns query row i = TMEM lane i.
-// Per 64-key tile: the int4 K / V codes (cp.async, one tile ahead) are dequantised to fp16
-// (exact) into UMMA K-major SWIZZLE_128B tiles -- K as [key][dh], V transposed as [dh][key];
-// S = Q K^T by tcgen05.mma kind::f16 with Q split hi + lo fp16 (two MMAs, fp32 accumulate
-// in TMEM); each thread reads its S row (tcgen05.ld), applies the reference mask and the
-// online softmax in log2 units, writes p * s_v split hi + lo as the A operand of
-// O += P V (TMEM, 128 fp32 columns).  The running max is only raised when a tile's max
-// exceeds it by 8 (log2): O and l are rescaled then (tcgen05.ld / st of the row), so p <= 256.
-constexpr int TA_Q = 128, TA_K = 64, TA_THREADS = 128;
-struct TaSmem {
-    static constexpr size_t qh = 0;                    // [2 sub-tiles][128 rows][128 B]
-    static constexpr size_t ql = qh + 32768;
-    static constexpr size_t kt = ql + 32768;           // [2][64 keys][128 B]
-    static constexpr size_t vt = kt + 16384;           // [128 dh][128 B = 64 keys]
-    static constexpr size_t ph = vt + 16384;           // [128 q][128 B = 64 keys]
-    static constexpr size_t pl = ph + 16384;
-    static constexpr size_t raw = pl + 16384;          // 2 x (K codes 4 KB, V codes 4 KB, scales 512 B)
-    static constexpr size_t raw_sz = 2 * 4096 + 512;
-    static constexpr size_t kvs = raw + 2 * raw_sz;    // ks[64], vs[64]
-    static constexpr size_t bars = kvs + 512;
-    static constexpr size_t total = bars + 64;
-};
-
-QT_DEV uint64_t ta_desc(uint32_t saddr) {  // K-major SWIZZLE_128B smem descriptor (SBO 1024)
-    uint64_t d = 0;
-    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
-    d |= (uint64_t)1 << 16;
-    d |= (uint64_t)(1024 >> 4) << 32;
-    d |= (uint64_t)1 << 46;
-    d |= (uint64_t)2 << 61;
-    return d;
-}
-// kind::f16 instruction descriptor: F32 accumulate, F16 A / B, K-major, N, M = 128
-constexpr uint32_t ta_idesc(int n) { return (1u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(TA_Q >> 4) << 24); }
-QT_DEV void ta_mma(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-    asm volatile(
-        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
-        "l"(a), "l"(b), "r"(idesc), "r"(acc)
-        : "memory");
-}
-QT_DEV void ta_commit(uint64_t* bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
-                 : "memory");
-}
-QT_DEV void ta_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
-QT_DEV void ta_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
-QT_DEV void ta_fence_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
-QT_DEV void ta_ld32(uint32_t taddr, float* v) {
-    uint32_t r[32];
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-#pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-}
-QT_DEV void ta_st32(uint32_t taddr, const float* v) {
-    asm volatile(
-        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
-        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
-        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};\n" ::"r"(taddr),
-        "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]),
-        "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]), "f"(v[16]),
-        "f"(v[17]), "f"(v[18]), "f"(v[19]), "f"(v[20]), "f"(v[21]), "f"(v[22]), "f"(v[23]), "f"(v[24]),
-        "f"(v[25]), "f"(v[26]), "f"(v[27]), "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31])
-        : "memory");
-}
-// byte offset of 16-byte chunk c of row r in a [rows][128 B] SWIZZLE_128B tile
-QT_DEV uint32_t ta_sw(int r, int c) { return (uint32_t)(r * 128 + ((c ^ (r & 7)) << 4)); }
-
-__global__ void __launch_bounds__(TA_THREADS, 1) k_attn_prefill_tc(const float* __restrict__ qkv, int ldq, int H,
-                                                                    int Hkv, const int* __restrict__ seq_off,
-                                                                    const int* __restrict__ vis,
-                                                                    const int* __restrict__ seq_len,
-                                                                    const uint8_t* __restrict__ pool,
-                                                                    long long page_bytes, const int* __restrict__ pt,
-                                                                    int max_pages, float inv_sqrt,
-                                                                    float* __restrict__ out, int ldo,
-                                                                    float2* __restrict__ ml, float* __restrict__ pmax,
-                                                                    int pmax_ld) {
-    constexpr int DH = 128;
-    extern __shared__ __align__(1024) uint8_t sm[];
-    const int b = blockIdx.z, h = blockIdx.y;
-    const int S = seq_len[b], V = vis[b];
-    const int q0 = blockIdx.x * TA_Q;
-    if (q0 >= S) return;
-    const int kh = h / (H / Hkv);
-    const int tid = threadIdx.x, warp = tid >> 5;
-    const int tok0 = seq_off[b];
-    const int q = q0 + tid;  // this thread's query row (index in the sequence)
-    const float sl2 = inv_sqrt * 1.4426950408889634f;
-    float* ks = reinterpret_cast<float*>(sm + TaSmem::kvs);
-    float* vs = ks + TA_K;
-    uint64_t* barS = reinterpret_cast<uint64_t*>(sm + TaSmem::bars);
-    uint64_t* barO = barS + 1;
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(barO + 1);
-    const int kend = max(V, min(S, q0 + TA_Q));
-    const int ntiles = (kend + TA_K - 1) / TA_K;
-
-    // first tile's codes in flight while Q is staged
-    load_kv_raw_async<DH>(page_base(pool, page_bytes, pt, max_pages, b, 0), Hkv, kh, min(TA_K, S),
-                          sm + TaSmem::raw);
-    if (tid == 0) {
-        mbar_init(barS, 1);
-        mbar_init(barO, 1);
-        mbar_fence_init();
-    }
-    if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;\n" ::"r"(smem_u32(tslot)));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
-    }
-    // Q row -> hi / lo fp16 (rows past S are zero)
-    {
-        const float* qr = qkv + (size_t)(tok0 + min(q, S - 1)) * ldq + h * DH;
-        const bool ok = q < S;
-#pragma unroll 4
-        for (int c = 0; c < 16; ++c) {  // 16-byte chunks of 8 dh
-            const float4 a = ok ? *reinterpret_cast<const float4*>(qr + c * 8) : make_float4(0.f, 0.f, 0.f, 0.f);
-            const float4 bb = ok ? *reinterpret_cast<const float4*>(qr + c * 8 + 4) : make_float4(0.f, 0.f, 0.f, 0.f);
-            uint32_t hi[4], lo[4];
-            split_h2(a.x, a.y, hi[0], lo[0]);
-            split_h2(a.z, a.w, hi[1], lo[1]);
-            split_h2(bb.x, bb.y, hi[2], lo[2]);
-            split_h2(bb.z, bb.w, hi[3], lo[3]);
-            const uint32_t off = (uint32_t)(c >> 3) * 16384 + ta_sw(tid, c & 7);
-            *reinterpret_cast<uint4*>(sm + TaSmem::qh + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-            *reinterpret_cast<uint4*>(sm + TaSmem::ql + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-        }
-    }
-    ta_fence_before();
-    __syncthreads();
-    ta_fence_after();
-    const uint32_t tmem = *tslot;
-    const uint32_t tS = tmem, tO = tmem + 64;
-    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
-
-    float m_used = -1e30f, l = 0.f;
-    int npv = 0;  // PV MMAs issued
-    for (int t = 0; t < ntiles; ++t) {
-        const int k0 = t * TA_K;
-        const int nk = min(TA_K, S - k0);
-        uint8_t* raw = sm + TaSmem::raw + (size_t)(t & 1) * TaSmem::raw_sz;
-        if (npv) {  // the previous PV MMA has read P and V^T
-            mbar_wait(barO, (uint32_t)(npv - 1) & 1u);
-            ta_fence_after();
-        }
-        cp_async_wait<0>();
-        __syncthreads();  // raw[t] landed for every thread's copies
-        if (t + 1 < ntiles)
-            load_kv_raw_async<DH>(page_base(pool, page_bytes, pt, max_pages, b, k0 + TA_K), Hkv, kh,
-                                  min(TA_K, S - k0 - TA_K), sm + TaSmem::raw + (size_t)((t + 1) & 1) * TaSmem::raw_sz);
-        // dequant: K [key][dh] (word = 8 dh = one 16-byte chunk), V^T [dh][key]
-        {
-            const uint32_t* kw = reinterpret_cast<const uint32_t*>(raw);
-            const uint32_t* vw = reinterpret_cast<const uint32_t*>(raw + 4096);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const int wi = tid + TA_THREADS * i;   // K: word (key, w) in row order
-                const int key = wi >> 4, w = wi & 15;
-                uint32_t hp[4];
-                word_to_h2_pairs(kw[wi], hp);  // one uint4 store below
-                *reinterpret_cast<uint4*>(sm + TaSmem::kt + (size_t)(w >> 3) * 8192 + ta_sw(key, w & 7)) =
-                    *reinterpret_cast<const uint4*>(hp);
-            }
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const int key = tid & 63, w = (tid >> 6) + 2 * i;  // V: a warp covers 32 keys of one word
-                uint32_t hp[4];
-                word_to_h2_pairs(vw[key * 16 + w], hp);
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const int c = 8 * w + 2 * j;
-                    const uint32_t base = TaSmem::vt + (uint32_t)((key & 7) * 2);
-                    *reinterpret_cast<uint16_t*>(sm + base + ta_sw(c, key >> 3)) = (uint16_t)(hp[j] & 0xFFFF);
-                    *reinterpret_cast<uint16_t*>(sm + base + ta_sw(c + 1, key >> 3)) = (uint16_t)(hp[j] >> 16);
-                }
-            }
-            if (tid < TA_K) {
-                const float* sc = reinterpret_cast<const float*>(raw + 8192);
-                ks[tid] = tid < nk ? sc[tid] : 0.f;
-                vs[tid] = tid < nk ? sc[TA_K + tid] : 0.f;
-            }
-        }
-        ta_fence_async();
-        ta_fence_before();
-        __syncthreads();
-        if (tid == 0) {  // S = Qhi K^T + Qlo K^T
-            ta_fence_after();
-            const uint32_t qh = smem_u32(sm + TaSmem::qh), ql = smem_u32(sm + TaSmem::ql);
-            const uint32_t kt = smem_u32(sm + TaSmem::kt);
-#pragma unroll
-            for (int k = 0; k < 8; ++k)
-                ta_mma(tS, ta_desc(qh + (k >> 2) * 16384 + (k & 3) * 32), ta_desc(kt + (k >> 2) * 8192 + (k & 3) * 32),
-                       ta_idesc(TA_K), k != 0);
-#pragma unroll
-            for (int k = 0; k < 8; ++k)
-                ta_mma(tS, ta_desc(ql + (k >> 2) * 16384 + (k & 3) * 32), ta_desc(kt + (k >> 2) * 8192 + (k & 3) * 32),
-                       ta_idesc(TA_K), 1);
-            ta_commit(barS);
-        }
-        mbar_wait(barS, (uint32_t)t & 1u);
-        ta_fence_after();
-        float s[TA_K];
-        ta_ld32(tS + lane_off, s);
-        ta_ld32(tS + lane_off + 32, s + 32);
-        // scale + reference mask (model.cpp:35-44) in log2 units; tile max
-        float tmax = -1e30f;
-#pragma unroll
-        for (int j = 0; j < TA_K; ++j) {
-            const int kj = k0 + j;
-            const bool ok = q < S && kj < S && (q < V ? kj < V : (kj < V || kj <= q));
-            s[j] = ok ? s[j] * (ks[j] * sl2) : -1e30f;
-            tmax = fmaxf(tmax, s[j]);
-        }
-        // lazy rescale: raise the running max only past +8 (p <= 256); warp-uniform O update
-        const bool raise = tmax > m_used + 8.f;
-        const float fac = raise ? exp2f(m_used - tmax) : 1.f;  // 0 while nothing accumulated
-        if (raise) {
-            l *= fac;
-            m_used = tmax;
-        }
-        if (__any_sync(0xffffffffu, raise) && npv) {
-#pragma unroll 1
-            for (int c = 0; c < DH; c += 32) {
-                float o[32];
-                ta_ld32(tO + lane_off + c, o);
-#pragma unroll
-                for (int i = 0; i < 32; ++i) o[i] *= fac;
-                ta_st32(tO + lane_off + c, o);
-            }
-            asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
-        }
-        float psum = 0.f;
-#pragma unroll
-        for (int c = 0; c < TA_K / 8; ++c) {
-            uint32_t hi[4], lo[4];
-#pragma unroll
-            for (int e = 0; e < 8; e += 2) {
-                const int j = 8 * c + e;
-                const float p0 = s[j] <= -1e30f ? 0.f : exp2f(s[j] - m_used);
-                const float p1 = s[j + 1] <= -1e30f ? 0.f : exp2f(s[j + 1] - m_used);
-                psum += p0 + p1;
-                split_h2(p0 * vs[j], p1 * vs[j + 1], hi[e / 2], lo[e / 2]);
-            }
-            *reinterpret_cast<uint4*>(sm + TaSmem::ph + ta_sw(tid, c)) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-            *reinterpret_cast<uint4*>(sm + TaSmem::pl + ta_sw(tid, c)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-        }
-        l += psum;
-        ta_fence_async();
-        ta_fence_before();
-        __syncthreads();
-        if (tid == 0) {  // O += Phi V + Plo V
-            ta_fence_after();
-            const uint32_t ph = smem_u32(sm + TaSmem::ph), pl = smem_u32(sm + TaSmem::pl);
-            const uint32_t vt = smem_u32(sm + TaSmem::vt);
-#pragma unroll
-            for (int k = 0; k < TA_K / 16; ++k)
-                ta_mma(tO, ta_desc(ph + k * 32), ta_desc(vt + k * 32), ta_idesc(DH), (npv != 0) || (k != 0));
-#pragma unroll
-            for (int k = 0; k < TA_K / 16; ++k)
-                ta_mma(tO, ta_desc(pl + k * 32), ta_desc(vt + k * 32), ta_idesc(DH), 1);
-            ta_commit(barO);
-        }
-        ++npv;
-    }
-    // finalize: O / l, the attn_out quantizer's partial row max, (m, l) for the QUOTA sums
-    float mx = 0.f;
-    if (npv) {
-        mbar_wait(barO, (uint32_t)(npv - 1) & 1u);
-        ta_fence_after();
-    }
-    const bool ok = q < S;
-    const float inv_l = l > 0.f ? 1.f / l : 0.f;
-    float* orow = out + (size_t)(tok0 + min(q, S - 1)) * ldo + h * DH;
-#pragma unroll 1
-    for (int c = 0; c < DH; c += 32) {
-        float o[32];
-        if (npv) ta_ld32(tO + lane_off + c, o);
-        else
-#pragma unroll
-            for (int i = 0; i < 32; ++i) o[i] = 0.f;
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-            o[i] *= inv_l;
-            mx = fmaxf(mx, fabsf(o[i]));
-        }
-        if (ok)
-#pragma unroll
-            for (int i = 0; i < 32; i += 8) st_v8f32(orow + c + i, o + i);
-    }
-    if (ok) {
-        if (ml) ml[(size_t)(tok0 + q) * H + h] = make_float2(m_used * 0.69314718055994531f, l);
-        if (pmax) pmax[(size_t)(tok0 + q) * pmax_ld + h] = mx;
-    }
-    ta_fence_before();
-    __syncthreads();
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;\n" ::"r"(tmem));
-}
-
 // ============================================================== K3a
 // grid (ceil(Vmax/64), H, B).  colsum[(b*H + h)*vstride + i] for i < V.
 template <int DH>
@@ -712,17 +405,6 @@ int qt_launch_attn_prefill(const float* qkv, int ldq, int H, int Hkv, int dh, co
     if (B <= 0 || smax <= 0) return 0;
     if (pmax && H > pmax_ld) return -1;
     const float inv_sqrt = (float)(1.0 / sqrt((double)dh));
-#ifndef QT_ATTN_TC
-#define QT_ATTN_TC 0  // 1: d_head 128 on the tcgen05 kernel (measured slower)
-#endif
-    if (dh == 128 && QT_ATTN_TC) {
-        const dim3 gtc((smax + TA_Q - 1) / TA_Q, H, B);
-        cudaFuncSetAttribute(k_attn_prefill_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TaSmem::total);
-        k_attn_prefill_tc<<<gtc, TA_THREADS, TaSmem::total, st>>>(qkv, ldq, H, Hkv, seq_off, vis, seq_len, pool,
-                                                                 page_bytes, pt, max_pages, inv_sqrt, out, ldo,
-                                                                 reinterpret_cast<float2*>(ml), pmax, pmax_ld);
-        return (int)cudaGetLastError();
-    }
     const dim3 grid((smax + AT_Q - 1) / AT_Q, H, B);
     if (dh == 128)
         k_attn_prefill<128><<<grid, 32 * AT_QW, 0, st>>>(qkv, ldq, H, Hkv, seq_off, vis, seq_len, pool, page_bytes, pt,
