@@ -10,6 +10,6 @@ for v in ${VARIANTS:-m2 m4 m8}; do
     echo "$v | $c | rc $? | $(grep '"metric"' gpurun_out/ab.log | python -c "
 import json,sys
 d=json.loads(sys.stdin.read()); c=d['profile']['decode_chain_ms']
-print('decode %.3f ms/step  chain gemm %.3f attn %.3f full %.3f' % (d['decode_ms_per_step'], c['gemm'], c['attention'], c['full']))")"
+print('prefill %.2f ms (attn %.2f)  decode %.3f ms/step  chain gemm %.3f attn %.3f full %.3f' % (d['prefill_ms'], d['profile']['prefill']['attention']['ms'], d['decode_ms_per_step'], c['gemm'], c['attention'], c['full']))")"
   done
 done
