@@ -175,3 +175,16 @@ def test_replay_c2_7b_width_r0(torch_cuda):
                              for i in range(2)])
     e.close()
     _run(cfg, w, acts, O.Recipe([2], [0.3], v0=576), _c2_seqs(), 2, 1500)
+
+
+def test_replay_c4_qwen2vl_width_gqa(torch_cuda):
+    """configs[3] C4 width (Qwen2-VL-7B shape: d 3584, 28 query / 4 kv heads x 128 -- GQA 7,
+    SwiGLU 18944) at reduced depth (2 layers), a ragged pair of sequences with their own
+    visual lengths, 30 % retention at layer 1, 3 decode steps (the 9..16-token decode GEMV
+    does not apply at B = 2; the GQA-7 decode attention and the d = 3584 GEMVs do)."""
+    cfg = O.ModelCfg(n_layers=2, d_model=3584, n_heads=28, n_kv_heads=4, d_head=128, d_ff=18944, mlp=1,
+                     act_mode=1, weight_axis=2)
+    w = O.synth_weights(cfg, seed=37)
+    seqs = [(O.synth_embeddings(420 + 64, 3584, seed=43, outlier_frac=0.01), 420, 64, 420),
+            (O.synth_embeddings(256 + 64, 3584, seed=44, outlier_frac=0.01), 256, 64, 256)]
+    _run(cfg, w, None, O.Recipe([1], [0.3], v0=420), seqs, 3, 1900)
