@@ -138,7 +138,7 @@ QT_DEV void store_converted(const uint4 w, uint8_t* i8, int row, int q) {
 // (warp - ew0) / 4 = column half.  Shared by the packed-int4 and the int8-operand kernels.
 // Work unit u (u0, u0 + ustep, ... < units): tile t = u % tiles, k slice u / tiles; the
 // tile's M tile is (t % mtp) * cl + rank (cl = cluster size along M) and its N tile t / mtp.
-template <int EPI>
+template <int EPI, int BN = T5_BN>
 QT_DEV void t5_epilogue_g(int ew0, int warp, int lane, uint32_t tmem, int u0, int ustep, int units, int tiles,
                           int mtp, int cl, int rank, int M, int N, const double* __restrict__ sa,
                           const double* __restrict__ sw, double* sws, void* __restrict__ out, int ldo,
@@ -150,14 +150,14 @@ QT_DEV void t5_epilogue_g(int ew0, int warp, int lane, uint32_t tmem, int u0, in
     pdl_launch_dependents();
     const int q = warp & 3;
     const int et = threadIdx.x - ew0 * 32;
-    const int jh = ((warp - ew0) >> 2) * (T5_BN / 64);  // first 32-column chunk of this half
+    const int jh = ((warp - ew0) >> 2) * (BN / 64);  // first 32-column chunk of this half
     int tl = 0;
     for (int u = u0; u < units; u += ustep, ++tl) {
         const int t = u % tiles, sl = u / tiles;
         const int acc = tl % T5_ACC;
-        const int m0 = ((t % mtp) * cl + rank) * T5_BM, n0 = (t / mtp) * T5_BN;
-        double* swt = sws + acc * T5_BN;
-        for (int i = et; i < T5_BN; i += T5_ET) swt[i] = n0 + i < N ? sw[n0 + i] : 0.0;
+        const int m0 = ((t % mtp) * cl + rank) * T5_BM, n0 = (t / mtp) * BN;
+        double* swt = sws + acc * BN;
+        for (int i = et; i < BN; i += T5_ET) swt[i] = n0 + i < N ? sw[n0 + i] : 0.0;
         if (EPI == QT_EPI_RESADD && ksplit == 1) {
             // pull this thread's residual row segment (256 fp64) toward L2 while the
             // tile's MMAs run: the read-modify-write below then hits L2, not HBM
@@ -166,7 +166,7 @@ QT_DEV void t5_epilogue_g(int ew0, int warp, int lane, uint32_t tmem, int u0, in
             if (mr < M && n0 + c0 < N) {
                 const char* rp =
                     reinterpret_cast<const char*>(static_cast<const double*>(out) + (size_t)mr * ldo + n0 + c0);
-                const int nb = min(T5_BN / 2, N - n0 - c0) * 8;
+                const int nb = min(BN / 2, N - n0 - c0) * 8;
                 for (int c = 0; c < nb; c += 128) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(rp + c));
             }
         }
@@ -175,13 +175,13 @@ QT_DEV void t5_epilogue_g(int ew0, int warp, int lane, uint32_t tmem, int u0, in
         tc_fence_after();
         const int m = m0 + q * 32 + lane;
         const double a_s = m < M ? sa[m] : 0.0;
-        const uint32_t tacc = tmem + (uint32_t)(acc * T5_BN) + ((uint32_t)(q * 32) << 16);
+        const uint32_t tacc = tmem + (uint32_t)(acc * BN) + ((uint32_t)(q * 32) << 16);
         float mx = 0.f;  // max |v| over this thread's (row, column half) of the tile
 #pragma unroll 1
-        for (int j = jh; j < jh + T5_BN / 64; ++j) {
+        for (int j = jh; j < jh + BN / 64; ++j) {
             uint32_t r[32];
             tmem_ld32(tacc + (uint32_t)(j * 32), r);
-            if (j == jh + T5_BN / 64 - 1) {
+            if (j == jh + BN / 64 - 1) {
                 // accumulator fully read: hand it back to the MMA issuer
                 tc_fence_before();
                 __syncwarp();
@@ -224,7 +224,7 @@ QT_DEV void t5_epilogue_g(int ew0, int warp, int lane, uint32_t tmem, int u0, in
             }
         }
         // partial row max for the next site's dynamic quantizer: slot (n tile, column half)
-        if (pmax && ksplit == 1 && m < M) pmax[(size_t)m * pmax_ld + (t / mtp) * 2 + jh / (T5_BN / 64)] = mx;
+        if (pmax && ksplit == 1 && m < M) pmax[(size_t)m * pmax_ld + (t / mtp) * 2 + jh / (BN / 64)] = mx;
         asm volatile("bar.sync 2, %0;\n" ::"n"(T5_ET) : "memory");  // swt reuse
     }
 }
@@ -408,17 +408,26 @@ __global__ void __launch_bounds__(T5_THREADS, 1) k_gemm_tc05(const uint8_t* __re
 //   warp 0      TMA producer (2D tensor loads, 4-stage 48 KB ring)
 //   warp 1      TMEM allocator + MMA issuer (same UMMA as k_gemm_tc05)
 //   warps 2..9  epilogue (t5_epilogue)
-constexpr int T8_S = 4;
+// stages of the int8 TMA ring: 4 x 48 KB at N = 256; 6 x 32 KB at N = 128 (decode batches: more
+// CTAs, each with as many bytes in flight)
+template <int BN>
+constexpr int t8_stages() { return BN == 256 ? 4 : 6; }
 constexpr int T8_EW0 = 2;
 constexpr int T8_THREADS = (T8_EW0 + T5_EWN) * 32;
 
+template <int BN>
 struct T8Smem {
+    static constexpr int S = t8_stages<BN>();
     static constexpr size_t ia = 0;
-    static constexpr size_t ib = ia + (size_t)T8_S * T5_IA;
-    static constexpr size_t swb = ib + (size_t)T8_S * T5_IB;
-    static constexpr size_t bars = swb + (size_t)T5_ACC * T5_BN * 8;
+    static constexpr size_t ib = ia + (size_t)S * T5_IA;
+    static constexpr size_t swb = ib + (size_t)S * BN * 128;
+    static constexpr size_t bars = swb + (size_t)T5_ACC * BN * 8;
     static constexpr size_t total = bars + 256;
 };
+template <int BN>
+constexpr uint32_t t8_idesc() {
+    return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(T5_BM >> 4) << 24);
+}
 
 QT_DEV void tma_load_2d(void* dst, const CUtensorMap* tm, int c0, int c1, uint64_t* bar) {
     asm volatile(
@@ -438,7 +447,7 @@ QT_DEV void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
 
-template <int EPI>
+template <int EPI, int BN = T5_BN>
 __global__ void __launch_bounds__(T8_THREADS, 1) k_gemm_tc05_i8(const __grid_constant__ CUtensorMap tmA,
                                                                  const __grid_constant__ CUtensorMap tmB,
                                                                  const double* __restrict__ sa,
@@ -447,21 +456,21 @@ __global__ void __launch_bounds__(T8_THREADS, 1) k_gemm_tc05_i8(const __grid_con
                                                                  int* __restrict__ acc_dbg, float* __restrict__ pmax,
                                                                  int pmax_ld, int ksplit, int* __restrict__ ws) {
     extern __shared__ __align__(1024) uint8_t smem[];
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + T8Smem::bars);
-    uint64_t* empty = full + T8_S;
-    uint64_t* tfull = empty + T8_S;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + T8Smem<BN>::bars);
+    uint64_t* empty = full + T8Smem<BN>::S;
+    uint64_t* tfull = empty + T8Smem<BN>::S;
     uint64_t* tempty = tfull + T5_ACC;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + T5_ACC);
-    double* sws = reinterpret_cast<double*>(smem + T8Smem::swb);
+    double* sws = reinterpret_cast<double*>(smem + T8Smem<BN>::swb);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int KB = K / 128;
-    const int mt_n = (M + T5_BM - 1) / T5_BM, nt_n = (N + T5_BN - 1) / T5_BN;
+    const int mt_n = (M + T5_BM - 1) / T5_BM, nt_n = (N + BN - 1) / BN;
     const int tiles = mt_n * nt_n;
     // work unit u: tile u % tiles, k slice u / tiles (split-K for decode batches, ksplit > 1:
     // int32 partials to ws, reduced in fixed order by k_splitk_epilogue)
     const int units = tiles * ksplit, kbs = (KB + ksplit - 1) / ksplit;
     if (threadIdx.x == 0) {
-        for (int s = 0; s < T8_S; ++s) {
+        for (int s = 0; s < T8Smem<BN>::S; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
@@ -473,7 +482,7 @@ __global__ void __launch_bounds__(T8_THREADS, 1) k_gemm_tc05_i8(const __grid_con
     }
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
-                     "n"(T5_ACC * T5_BN));
+                     "n"(T5_ACC * BN));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
     }
     tc_fence_before();
@@ -488,32 +497,32 @@ __global__ void __launch_bounds__(T8_THREADS, 1) k_gemm_tc05_i8(const __grid_con
             int it = 0;
             for (int u = blockIdx.x; u < units; u += gridDim.x) {
                 const int t = u % tiles, k0 = (u / tiles) * kbs, k1 = min(KB, k0 + kbs);
-                const int m0 = (t % mt_n) * T5_BM, n0 = (t / mt_n) * T5_BN;
+                const int m0 = (t % mt_n) * T5_BM, n0 = (t / mt_n) * BN;
                 for (int kb = k0; kb < k1; ++kb, ++it) {
-                    const int s = it % T8_S;
-                    if (it >= T8_S) mbar_wait(&empty[s], ((it / T8_S) - 1) & 1);
-                    mbar_arrive_expect_tx(&full[s], (uint32_t)(T5_IA + T5_IB));
-                    tma_load_2d(smem + T8Smem::ia + (size_t)s * T5_IA, &tmA, kb * 128, m0, &full[s]);
-                    tma_load_2d(smem + T8Smem::ib + (size_t)s * T5_IB, &tmB, kb * 128, n0, &full[s]);
+                    const int s = it % T8Smem<BN>::S;
+                    if (it >= T8Smem<BN>::S) mbar_wait(&empty[s], ((it / T8Smem<BN>::S) - 1) & 1);
+                    mbar_arrive_expect_tx(&full[s], (uint32_t)(T5_IA + (BN * 128)));
+                    tma_load_2d(smem + T8Smem<BN>::ia + (size_t)s * T5_IA, &tmA, kb * 128, m0, &full[s]);
+                    tma_load_2d(smem + T8Smem<BN>::ib + (size_t)s * (BN * 128), &tmB, kb * 128, n0, &full[s]);
                 }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {
-            const uint32_t idesc = t5_idesc();
+            const uint32_t idesc = t8_idesc<BN>();
             int it = 0, tl = 0;
             for (int u = blockIdx.x; u < units; u += gridDim.x, ++tl) {
                 const int k0 = (u / tiles) * kbs, k1 = min(KB, k0 + kbs);
                 const int acc = tl % T5_ACC;
                 if (tl >= T5_ACC) mbar_wait(&tempty[acc], ((tl / T5_ACC) - 1) & 1);
                 tc_fence_after();
-                const uint32_t tacc = tmem + (uint32_t)(acc * T5_BN);
+                const uint32_t tacc = tmem + (uint32_t)(acc * BN);
                 for (int kb = k0; kb < k1; ++kb, ++it) {
-                    const int s = it % T8_S;
-                    mbar_wait(&full[s], (it / T8_S) & 1);
+                    const int s = it % T8Smem<BN>::S;
+                    mbar_wait(&full[s], (it / T8Smem<BN>::S) & 1);
                     tc_fence_after();
-                    const uint32_t a0 = smem_u32(smem + T8Smem::ia + (size_t)s * T5_IA);
-                    const uint32_t b0 = smem_u32(smem + T8Smem::ib + (size_t)s * T5_IB);
+                    const uint32_t a0 = smem_u32(smem + T8Smem<BN>::ia + (size_t)s * T5_IA);
+                    const uint32_t b0 = smem_u32(smem + T8Smem<BN>::ib + (size_t)s * (BN * 128));
 #pragma unroll
                     for (int k = 0; k < 4; ++k)
                         mma_i8(tacc, umma_desc_sw128(a0 + 32 * k), umma_desc_sw128(b0 + 32 * k), idesc,
@@ -525,13 +534,13 @@ __global__ void __launch_bounds__(T8_THREADS, 1) k_gemm_tc05_i8(const __grid_con
         }
         __syncwarp();
     } else {
-        t5_epilogue_g<EPI>(T8_EW0, warp, lane, tmem, blockIdx.x, gridDim.x, units, tiles, mt_n, 1, 0, M, N, sa, sw,
+        t5_epilogue_g<EPI, BN>(T8_EW0, warp, lane, tmem, blockIdx.x, gridDim.x, units, tiles, mt_n, 1, 0, M, N, sa, sw,
                            sws, out, ldo, ksplit > 1 ? nullptr : acc_dbg, ksplit, ws, pmax, pmax_ld, tfull, tempty);
     }
     tc_fence_before();
     __syncthreads();
     if (warp == 1) {
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(T5_ACC * T5_BN));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(T5_ACC * BN));
     }
 }
 
@@ -842,11 +851,19 @@ extern "C" int qt_launch_w4t_to_i8(const uint8_t* tiled, int rows_pad, int K, in
 // at most 6 and >= 4 k blocks each -- measured per shape and slice count at M = 32..256
 // (tools/bench_decode_gemm.py): splitting the wide projections only added the int32
 // partials' round trip.  ks_force > 0 overrides (measurement).
+#ifndef QT_I8_NARROW_M
+#define QT_I8_NARROW_M 256  // up to this many tokens the single-CTA kernel uses N = 128 tiles (A/B:
+                           // C5 decode GEMM class 2.29 -> 2.04 ms/step at B = 64, 3.28 -> 2.94 at 256)
+#endif
+// tile width of the single-CTA int8 kernel: 128 for decode batches (twice the CTAs streaming
+// the weights, 6 stages in flight each), 256 for prefill
+static int qt_i8_bn(int M) { return M <= QT_I8_NARROW_M ? 128 : qt::T5_BN; }
+
 static int qt_tc05_i8_single_splitk(int M, int N, int K, int ks_force = 0) {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    const int KB = K / 128;
-    const int tiles = ((M + qt::T5_BM - 1) / qt::T5_BM) * ((N + qt::T5_BN - 1) / qt::T5_BN);
+    const int KB = K / 128, bn = qt_i8_bn(M);
+    const int tiles = ((M + qt::T5_BM - 1) / qt::T5_BM) * ((N + bn - 1) / bn);
     auto eff = [&](int ks) {  // slices actually formed (no empty slice)
         ks = std::max(1, std::min(ks, KB));
         const int kbs = (KB + ks - 1) / ks;
@@ -896,15 +913,16 @@ extern "C" int qt_launch_w4a4_tc05_i8_ex(int epi, const int8_t* A8, int lda8, co
     if (K % 128 || lda8 % 16 || ldw8 % 16 || N > w_rows) return -1;
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    const int nt_n = (N + T5_BN - 1) / T5_BN;
+    // CTA pairs only pay for the largest token counts (measured, tools/bench_gemm.py: pair 2880 vs
+    // single 2774 TOPS at 8192^3, but 1582 vs 2004 on the 7B QKV GEMM at M = 1896)
+    const bool pair = M >= 8192 && !force_single && ks_force == 0;
+    const int bn = pair ? T5_BN : qt_i8_bn(M);
+    const int nt_n = (N + bn - 1) / bn;
     const int parts = 2 * nt_n;
     if (pmax && parts > pmax_ld) pmax = nullptr;
     if (pmax && n_part) *n_part = parts;
     CUtensorMap ta, tb;
-    // CTA pairs only pay for the largest token counts (measured, tools/bench_gemm.py: pair 2880 vs
-    // single 2774 TOPS at 8192^3, but 1582 vs 2004 on the 7B QKV GEMM at M = 1896)
-    const bool pair = M >= 8192 && !force_single && ks_force == 0;
-    if (qt_tmap_i8(&ta, A8, M, K, lda8, T5_BM) || qt_tmap_i8(&tb, W8, w_rows, K, ldw8, pair ? 128 : T5_BN))
+    if (qt_tmap_i8(&ta, A8, M, K, lda8, T5_BM) || qt_tmap_i8(&tb, W8, w_rows, K, ldw8, pair ? 128 : bn))
         return -2;
     if (pair) {
         const int tiles = ((M + 255) / 256) * nt_n;
@@ -957,10 +975,10 @@ extern "C" int qt_launch_w4a4_tc05_i8_ex(int epi, const int8_t* A8, int lda8, co
     }
     const int units = ((M + T5_BM - 1) / T5_BM) * nt_n * ksplit;
     const dim3 grid(std::min(units, sms));
-    const size_t smem = T8Smem::total;
+    const size_t smem = bn == 128 ? T8Smem<128>::total : T8Smem<T5_BN>::total;
 #define QT_T8(E)                                                                                                 \
     do {                                                                                                         \
-        auto kfn = k_gemm_tc05_i8<E>;                                                                            \
+        auto kfn = bn == 128 ? k_gemm_tc05_i8<E, 128> : k_gemm_tc05_i8<E, T5_BN>;                                \
         cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                       \
         int rc = launch_pdl(kfn, grid, dim3(T8_THREADS), smem, st, ta, tb, sa, sw, M, N, K, out, ldo, acc_dbg,    \
                             pmax, pmax_ld, ksplit, ws);                                                          \
