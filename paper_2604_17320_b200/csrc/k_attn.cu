@@ -305,6 +305,379 @@ __global__ void __launch_bounds__(32 * AT_QW, AT_QW > 4 ? 1 : QT_ATTN_MINB) k_at
     }
 }
 
+// ---------------------------------------------------------------- tcgen05 helpers (kind::f16)
+QT_DEV uint64_t ta_desc(uint32_t saddr) {  // K-major SWIZZLE_128B smem descriptor (SBO 1024)
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)1 << 16;
+    d |= (uint64_t)(1024 >> 4) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)2 << 61;
+    return d;
+}
+// kind::f16 instruction descriptor: F32 accumulate, F16 A / B, K-major, N, M = 128
+constexpr uint32_t ta_idesc(int n) { return (1u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24); }  // M = 128
+QT_DEV void ta_mma(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+QT_DEV void ta_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+QT_DEV void ta_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+QT_DEV void ta_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+QT_DEV void ta_fence_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+QT_DEV void ta_ld32(uint32_t taddr, float* v) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+QT_DEV void ta_st32(uint32_t taddr, const float* v) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};\n" ::"r"(taddr),
+        "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]),
+        "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]), "f"(v[16]),
+        "f"(v[17]), "f"(v[18]), "f"(v[19]), "f"(v[20]), "f"(v[21]), "f"(v[22]), "f"(v[23]), "f"(v[24]),
+        "f"(v[25]), "f"(v[26]), "f"(v[27]), "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31])
+        : "memory");
+}
+// byte offset of 16-byte chunk c of row r in a [rows][128 B] SWIZZLE_128B tile
+QT_DEV uint32_t ta_sw(int r, int c) { return (uint32_t)(r * 128 + ((c ^ (r & 7)) << 4)); }
+
+// ============================================================== K7 on tcgen05, warp-specialised (d_head 128)
+// One CTA per (128-query tile, head, sequence), 9 warps:
+//   warps 0-3  softmax: thread i owns query row i = TMEM lane i (tcgen05.ld of S, the
+//              reference mask, online softmax in log2 units with a lazy max, P = p * s_v
+//              split hi + lo fp16 into the UMMA A tile, O rescale when the max rises by > 8)
+//   warps 4-7  producer: the int4 K / V codes of the next tiles by cp.async, dequantised to
+//              fp16 (exact) into double-buffered K [key][dh] and V^T [dh][key] UMMA tiles
+//   warp 8     TMEM owner + MMA issuer: S(t) = Q K^T (Q hi + lo) into a double-buffered S,
+//              then O += P(t-1) V(t-1) -- tile t's S product runs while tile t-1's softmax does
+// mbarriers: kv_full / kv_empty (producer <-> MMA), s_full (MMA -> softmax), p_full (softmax ->
+// MMA), pv_done (MMA -> softmax: P buffer free, O updated).
+constexpr int TW_Q = 128, TW_K = 64;
+constexpr int TW_THREADS = 9 * 32;
+struct TwSmem {
+    static constexpr size_t qh = 0;                 // [2 sub-tiles][128 rows][128 B]
+    static constexpr size_t ql = qh + 32768;
+    static constexpr size_t kt = ql + 32768;        // [2 bufs][2 sub-tiles][64 keys][128 B]
+    static constexpr size_t vt = kt + 2 * 16384;    // [2 bufs][128 dh][128 B]
+    static constexpr size_t ph = vt + 2 * 16384;    // [2 bufs][128 q][128 B]
+    static constexpr size_t pl = ph + 2 * 16384;
+    static constexpr size_t raw = pl + 2 * 16384;   // [2] x (K codes 4 KB, V codes 4 KB, scales 512 B)
+    static constexpr size_t raw_sz = 2 * 4096 + 512;
+    static constexpr size_t kvs = raw + 2 * raw_sz; // [2 bufs] ks[64], then [2 bufs] vs[64]
+    static constexpr size_t bars = kvs + 1024;
+    static constexpr size_t total = bars + 128;
+};
+
+template <int DH>
+QT_DEV void tw_load_raw(const uint8_t* page, int Hkv, int kh, int nkeys, uint8_t* raw, int p, int np) {
+    constexpr int CB = TW_K * (DH / 2);
+    const size_t cb = (size_t)Hkv * kPage * (DH / 2);
+    const uint8_t* kc = page + (size_t)kh * kPage * (DH / 2);
+    const uint8_t* vc = page + cb + (size_t)kh * kPage * (DH / 2);
+    const uint8_t* ksc = page + 2 * cb + (size_t)kh * kPage * 4;
+    const uint8_t* vsc = page + 2 * cb + ((size_t)Hkv * kPage + kh * kPage) * 4;
+    for (int c = p; c < CB / 16; c += np) {
+        const bool ok = c / (DH / 32) < nkeys;
+        cp_async16(raw + c * 16, kc + (size_t)c * 16, ok);
+        cp_async16(raw + CB + c * 16, vc + (size_t)c * 16, ok);
+    }
+    for (int c = p; c < 2 * (TW_K * 4 / 16); c += np) {
+        const int m = c / (TW_K * 4 / 16), q = c % (TW_K * 4 / 16);
+        cp_async16(raw + 2 * CB + c * 16, (m ? vsc : ksc) + q * 16, q * 4 < nkeys);
+    }
+    cp_async_commit();
+}
+
+__global__ void __launch_bounds__(TW_THREADS, 1) k_attn_prefill_ws(const float* __restrict__ qkv, int ldq, int H,
+                                                                    int Hkv, const int* __restrict__ seq_off,
+                                                                    const int* __restrict__ vis,
+                                                                    const int* __restrict__ seq_len,
+                                                                    const uint8_t* __restrict__ pool,
+                                                                    long long page_bytes, const int* __restrict__ pt,
+                                                                    int max_pages, float inv_sqrt,
+                                                                    float* __restrict__ out, int ldo,
+                                                                    float2* __restrict__ ml, float* __restrict__ pmax,
+                                                                    int pmax_ld) {
+    constexpr int DH = 128;
+    extern __shared__ __align__(1024) uint8_t sm[];
+    const int b = blockIdx.z, h = blockIdx.y;
+    const int S = seq_len[b], V = vis[b];
+    const int q0 = blockIdx.x * TW_Q;
+    if (q0 >= S) return;
+    const int kh = h / (H / Hkv);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int tok0 = seq_off[b];
+    const int kend = max(V, min(S, q0 + TW_Q));
+    const int T = (kend + TW_K - 1) / TW_K;
+    uint64_t* kv_full = reinterpret_cast<uint64_t*>(sm + TwSmem::bars);
+    uint64_t* kv_empty = kv_full + 2;
+    uint64_t* s_full = kv_empty + 2;
+    uint64_t* p_full = s_full + 2;
+    uint64_t* pv_done = p_full + 2;
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(pv_done + 2);
+    float* ksb = reinterpret_cast<float*>(sm + TwSmem::kvs);  // [2][64] K scales, then [2][64] V scales
+    float* vsb = ksb + 2 * TW_K;
+
+    if (tid == 0) {
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&kv_full[i], 128);
+            mbar_init(&kv_empty[i], 1);
+            mbar_init(&s_full[i], 1);
+            mbar_init(&p_full[i], 128);
+            mbar_init(&pv_done[i], 1);
+        }
+        mbar_fence_init();
+    }
+    if (warp == 8) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;\n" ::"r"(smem_u32(tslot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    if (warp >= 4 && warp < 8)  // the first tile's codes in flight while Q is staged
+        tw_load_raw<DH>(page_base(pool, page_bytes, pt, max_pages, b, 0), Hkv, kh, min(TW_K, S),
+                        sm + TwSmem::raw, tid - 128, 128);
+    if (warp < 4) {  // Q row -> hi / lo fp16 (rows past S are zero)
+        const int q = q0 + tid;
+        const float* qr = qkv + (size_t)(tok0 + min(q, S - 1)) * ldq + h * DH;
+        const bool ok = q < S;
+#pragma unroll 4
+        for (int c = 0; c < 16; ++c) {
+            const float4 a = ok ? *reinterpret_cast<const float4*>(qr + c * 8) : make_float4(0.f, 0.f, 0.f, 0.f);
+            const float4 bb = ok ? *reinterpret_cast<const float4*>(qr + c * 8 + 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+            uint32_t hi[4], lo[4];
+            split_h2(a.x, a.y, hi[0], lo[0]);
+            split_h2(a.z, a.w, hi[1], lo[1]);
+            split_h2(bb.x, bb.y, hi[2], lo[2]);
+            split_h2(bb.z, bb.w, hi[3], lo[3]);
+            const uint32_t off = (uint32_t)(c >> 3) * 16384 + ta_sw(tid, c & 7);
+            *reinterpret_cast<uint4*>(sm + TwSmem::qh + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+            *reinterpret_cast<uint4*>(sm + TwSmem::ql + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+        }
+        ta_fence_async();
+    }
+    ta_fence_before();
+    __syncthreads();
+    ta_fence_after();
+    const uint32_t tmem = *tslot;
+    const uint32_t tO = tmem + 128;  // S buffers at columns 0 and 64
+
+    if (warp == 8) {
+        // ---------------- MMA issuer
+        if (lane == 0) {
+            const uint32_t qh = smem_u32(sm + TwSmem::qh), ql = smem_u32(sm + TwSmem::ql);
+            for (int t = 0; t <= T; ++t) {
+                if (t < T) {  // S(t) = Qhi K^T + Qlo K^T into S[t & 1]
+                    const int bf = t & 1;
+                    mbar_wait(&kv_full[bf], (uint32_t)(t >> 1) & 1u);
+                    ta_fence_after();
+                    const uint32_t kt = smem_u32(sm + TwSmem::kt + (size_t)bf * 16384);
+                    const uint32_t tS = tmem + (uint32_t)(bf * 64);
+#pragma unroll
+                    for (int k = 0; k < 8; ++k)
+                        ta_mma(tS, ta_desc(qh + (k >> 2) * 16384 + (k & 3) * 32),
+                               ta_desc(kt + (k >> 2) * 8192 + (k & 3) * 32), ta_idesc(TW_K), k != 0);
+#pragma unroll
+                    for (int k = 0; k < 8; ++k)
+                        ta_mma(tS, ta_desc(ql + (k >> 2) * 16384 + (k & 3) * 32),
+                               ta_desc(kt + (k >> 2) * 8192 + (k & 3) * 32), ta_idesc(TW_K), 1);
+                    ta_commit(&s_full[bf]);
+                }
+                if (t >= 1) {  // O += Phi V + Plo V of tile t - 1
+                    const int u = t - 1, c = u & 1;
+                    mbar_wait(&p_full[c], (uint32_t)(u >> 1) & 1u);
+                    ta_fence_after();
+                    const uint32_t ph = smem_u32(sm + TwSmem::ph + (size_t)c * 16384);
+                    const uint32_t pl = smem_u32(sm + TwSmem::pl + (size_t)c * 16384);
+                    const uint32_t vt = smem_u32(sm + TwSmem::vt + (size_t)c * 16384);
+#pragma unroll
+                    for (int k = 0; k < TW_K / 16; ++k)
+                        ta_mma(tO, ta_desc(ph + k * 32), ta_desc(vt + k * 32), ta_idesc(DH), (u != 0) || (k != 0));
+#pragma unroll
+                    for (int k = 0; k < TW_K / 16; ++k)
+                        ta_mma(tO, ta_desc(pl + k * 32), ta_desc(vt + k * 32), ta_idesc(DH), 1);
+                    ta_commit(&pv_done[c]);
+                    ta_commit(&kv_empty[c]);
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp >= 4) {
+        // ---------------- producer
+        const int p = tid - 128;
+        for (int t = 0; t < T; ++t) {
+            const int bf = t & 1;
+            const int k0 = t * TW_K;
+            const int nk = min(TW_K, S - k0);
+            cp_async_wait<0>();
+            asm volatile("bar.sync 1, 128;\n" ::: "memory");  // raw(t) landed; dequant(t-1) done by all
+            if (t + 1 < T)
+                tw_load_raw<DH>(page_base(pool, page_bytes, pt, max_pages, b, k0 + TW_K), Hkv, kh,
+                                min(TW_K, S - k0 - TW_K), sm + TwSmem::raw + (size_t)((t + 1) & 1) * TwSmem::raw_sz,
+                                p, 128);
+            if (t >= 2) mbar_wait(&kv_empty[bf], (uint32_t)((t - 2) >> 1) & 1u);
+            const uint8_t* raw = sm + TwSmem::raw + (size_t)bf * TwSmem::raw_sz;
+            const uint32_t* kw = reinterpret_cast<const uint32_t*>(raw);
+            const uint32_t* vw = reinterpret_cast<const uint32_t*>(raw + 4096);
+            uint8_t* ktb = sm + TwSmem::kt + (size_t)bf * 16384;
+            uint8_t* vtb = sm + TwSmem::vt + (size_t)bf * 16384;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int wi = p + 128 * i;  // K: word (key, w) in row order
+                const int key = wi >> 4, w = wi & 15;
+                uint32_t hp[4];
+                word_to_h2_pairs(kw[wi], hp);
+                *reinterpret_cast<uint4*>(ktb + (size_t)(w >> 3) * 8192 + ta_sw(key, w & 7)) =
+                    *reinterpret_cast<const uint4*>(hp);
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int key = p & 63, w = (p >> 6) + 2 * i;  // V: a warp covers 32 keys of one word
+                uint32_t hp[4];
+                word_to_h2_pairs(vw[key * 16 + w], hp);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int c = 8 * w + 2 * j;
+                    uint8_t* base = vtb + (key & 7) * 2;
+                    *reinterpret_cast<uint16_t*>(base + ta_sw(c, key >> 3)) = (uint16_t)(hp[j] & 0xFFFF);
+                    *reinterpret_cast<uint16_t*>(base + ta_sw(c + 1, key >> 3)) = (uint16_t)(hp[j] >> 16);
+                }
+            }
+            if (p < TW_K) {
+                const float* sc = reinterpret_cast<const float*>(raw + 8192);
+                ksb[bf * TW_K + p] = p < nk ? sc[p] : 0.f;
+                vsb[bf * TW_K + p] = p < nk ? sc[TW_K + p] : 0.f;
+            }
+            ta_fence_async();
+            mbar_arrive(&kv_full[bf]);
+        }
+    } else {
+        // ---------------- softmax (thread tid = query row q0 + tid = TMEM lane tid)
+        const int q = q0 + tid;
+        const float sl2 = inv_sqrt * 1.4426950408889634f;
+        const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+        float m_used = -1e30f, l = 0.f;
+        for (int t = 0; t < T; ++t) {
+            const int bf = t & 1;
+            const uint32_t ph = (uint32_t)(t >> 1) & 1u;
+            const int k0 = t * TW_K;
+            mbar_wait(&s_full[bf], ph);
+            mbar_wait(&kv_full[bf], ph);  // this tile's scales
+            ta_fence_after();
+            float s[TW_K];
+            ta_ld32(tmem + (uint32_t)(bf * 64) + lane_off, s);
+            ta_ld32(tmem + (uint32_t)(bf * 64 + 32) + lane_off, s + 32);
+            const float* ks = ksb + bf * TW_K;
+            const float* vs = vsb + bf * TW_K;
+            // every (query, key) pair of the tile allowed and in range: no per-element mask
+            const int klast = k0 + TW_K - 1, qlast = q0 + TW_Q - 1;
+            const bool full = qlast < S && klast < S &&
+                              (qlast < V ? klast < V : (q0 >= V && (klast < V || klast <= q0)));
+            float tmax = -1e30f;
+            if (full) {
+#pragma unroll
+                for (int j = 0; j < TW_K; ++j) {
+                    s[j] *= ks[j] * sl2;
+                    tmax = fmaxf(tmax, s[j]);
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < TW_K; ++j) {
+                    const int kj = k0 + j;
+                    const bool ok = q < S && kj < S && (q < V ? kj < V : (kj < V || kj <= q));
+                    s[j] = ok ? s[j] * (ks[j] * sl2) : -1e30f;
+                    tmax = fmaxf(tmax, s[j]);
+                }
+            }
+            const bool raise = tmax > m_used + 8.f;
+            const float fac = raise ? exp2f(m_used - tmax) : 1.f;
+            if (raise) {
+                l *= fac;
+                m_used = tmax;
+            }
+            if (t >= 1 && __any_sync(0xffffffffu, raise)) {  // O holds tiles < t: rescale after PV(t-1)
+                mbar_wait(&pv_done[(t - 1) & 1], (uint32_t)((t - 1) >> 1) & 1u);
+                ta_fence_after();
+#pragma unroll 1
+                for (int c = 0; c < DH; c += 32) {
+                    float o[32];
+                    ta_ld32(tO + lane_off + c, o);
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) o[i] *= fac;
+                    ta_st32(tO + lane_off + c, o);
+                }
+                asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+            }
+            if (t >= 2) mbar_wait(&pv_done[bf], (uint32_t)((t - 2) >> 1) & 1u);  // P buffer free
+            uint8_t* phb = sm + TwSmem::ph + (size_t)bf * 16384;
+            uint8_t* plb = sm + TwSmem::pl + (size_t)bf * 16384;
+            float psum = 0.f;
+#pragma unroll
+            for (int c = 0; c < TW_K / 8; ++c) {
+                uint32_t hi[4], lo[4];
+#pragma unroll
+                for (int e = 0; e < 8; e += 2) {
+                    const int j = 8 * c + e;
+                    const float p0 = s[j] <= -1e30f ? 0.f : exp2f(s[j] - m_used);
+                    const float p1 = s[j + 1] <= -1e30f ? 0.f : exp2f(s[j + 1] - m_used);
+                    psum += p0 + p1;
+                    split_h2(p0 * vs[j], p1 * vs[j + 1], hi[e / 2], lo[e / 2]);
+                }
+                *reinterpret_cast<uint4*>(phb + ta_sw(tid, c)) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+                *reinterpret_cast<uint4*>(plb + ta_sw(tid, c)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+            }
+            l += psum;
+            ta_fence_async();
+            ta_fence_before();
+            mbar_arrive(&p_full[bf]);
+        }
+        // finalize: O / l, the attn_out quantizer's partial row max, (m, l) for the QUOTA sums
+        mbar_wait(&pv_done[(T - 1) & 1], (uint32_t)((T - 1) >> 1) & 1u);
+        ta_fence_after();
+        const bool ok = q < S;
+        const float inv_l = l > 0.f ? 1.f / l : 0.f;
+        float* orow = out + (size_t)(tok0 + min(q, S - 1)) * ldo + h * DH;
+        float mx = 0.f;
+#pragma unroll 1
+        for (int c = 0; c < DH; c += 32) {
+            float o[32];
+            ta_ld32(tO + lane_off + c, o);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                o[i] *= inv_l;
+                mx = fmaxf(mx, fabsf(o[i]));
+            }
+            if (ok)
+#pragma unroll
+                for (int i = 0; i < 32; i += 8) st_v8f32(orow + c + i, o + i);
+        }
+        if (ok) {
+            if (ml) ml[(size_t)(tok0 + q) * H + h] = make_float2(m_used * 0.69314718055994531f, l);
+            if (pmax) pmax[(size_t)(tok0 + q) * pmax_ld + h] = mx;
+        }
+    }
+    ta_fence_before();
+    __syncthreads();
+    if (warp == 8) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;\n" ::"r"(tmem));
+}
+
 // ============================================================== K3a
 // grid (ceil(Vmax/64), H, B).  colsum[(b*H + h)*vstride + i] for i < V.
 template <int DH>
@@ -405,6 +778,19 @@ int qt_launch_attn_prefill(const float* qkv, int ldq, int H, int Hkv, int dh, co
     if (B <= 0 || smax <= 0) return 0;
     if (pmax && H > pmax_ld) return -1;
     const float inv_sqrt = (float)(1.0 / sqrt((double)dh));
+#ifndef QT_ATTN_WS_MIN_S
+#define QT_ATTN_WS_MIN_S 512  // longest sequence from which d_head 128 runs the tcgen05 kernel
+                              // (A/B: C3 attention 24.9 -> 20.6 ms, C2 4.50 -> 4.37; below 512 tokens
+                              // the 128-query tiles are mostly empty and the mma.sync kernel wins)
+#endif
+    if (dh == 128 && smax >= QT_ATTN_WS_MIN_S) {
+        const dim3 gws((smax + TW_Q - 1) / TW_Q, H, B);
+        cudaFuncSetAttribute(k_attn_prefill_ws, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TwSmem::total);
+        k_attn_prefill_ws<<<gws, TW_THREADS, TwSmem::total, st>>>(qkv, ldq, H, Hkv, seq_off, vis, seq_len, pool,
+                                                                 page_bytes, pt, max_pages, inv_sqrt, out, ldo,
+                                                                 reinterpret_cast<float2*>(ml), pmax, pmax_ld);
+        return (int)cudaGetLastError();
+    }
     const dim3 grid((smax + AT_Q - 1) / AT_Q, H, B);
     if (dh == 128)
         k_attn_prefill<128><<<grid, 32 * AT_QW, 0, st>>>(qkv, ldq, H, Hkv, seq_off, vis, seq_len, pool, page_bytes, pt,
