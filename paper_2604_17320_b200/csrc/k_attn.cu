@@ -372,7 +372,9 @@ QT_DEV uint32_t ta_sw(int r, int c) { return (uint32_t)(r * 128 + ((c ^ (r & 7))
 // mbarriers: kv_full / kv_empty (producer <-> MMA), s_full (MMA -> softmax), p_full (softmax ->
 // MMA), pv_done (MMA -> softmax: P buffer free, O updated).
 constexpr int TW_Q = 128, TW_K = 64;
-constexpr int TW_THREADS = 9 * 32;
+constexpr int TW_SW = 8, TW_PW = 4;                // softmax warps (2 threads per query row), producer warps
+constexpr int TW_MW = TW_SW + TW_PW;              // the MMA warp
+constexpr int TW_THREADS = (TW_MW + 1) * 32;
 struct TwSmem {
     static constexpr size_t qh = 0;                 // [2 sub-tiles][128 rows][128 B]
     static constexpr size_t ql = qh + 32768;
@@ -383,7 +385,8 @@ struct TwSmem {
     static constexpr size_t raw = pl + 2 * 16384;   // [2] x (K codes 4 KB, V codes 4 KB, scales 512 B)
     static constexpr size_t raw_sz = 2 * 4096 + 512;
     static constexpr size_t kvs = raw + 2 * raw_sz; // [2 bufs] ks[64], then [2 bufs] vs[64]
-    static constexpr size_t bars = kvs + 1024;
+    static constexpr size_t xch = kvs + 1024;       // [2 tiles][2 halves][128] tile max, then [2][128] l, [2][128] max |o|
+    static constexpr size_t bars = xch + 4096;
     static constexpr size_t total = bars + 128;
 };
 
@@ -439,21 +442,21 @@ __global__ void __launch_bounds__(TW_THREADS, 1) k_attn_prefill_ws(const float* 
 
     if (tid == 0) {
         for (int i = 0; i < 2; ++i) {
-            mbar_init(&kv_full[i], 128);
+            mbar_init(&kv_full[i], TW_PW * 32);
             mbar_init(&kv_empty[i], 1);
             mbar_init(&s_full[i], 1);
-            mbar_init(&p_full[i], 128);
+            mbar_init(&p_full[i], TW_SW * 32);
             mbar_init(&pv_done[i], 1);
         }
         mbar_fence_init();
     }
-    if (warp == 8) {
+    if (warp == TW_MW) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;\n" ::"r"(smem_u32(tslot)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
     }
-    if (warp >= 4 && warp < 8)  // the first tile's codes in flight while Q is staged
+    if (warp >= TW_SW && warp < TW_MW)  // the first tile's codes in flight while Q is staged
         tw_load_raw<DH>(page_base(pool, page_bytes, pt, max_pages, b, 0), Hkv, kh, min(TW_K, S),
-                        sm + TwSmem::raw, tid - 128, 128);
+                        sm + TwSmem::raw, tid - TW_SW * 32, TW_PW * 32);
     if (warp < 4) {  // Q row -> hi / lo fp16 (rows past S are zero)
         const int q = q0 + tid;
         const float* qr = qkv + (size_t)(tok0 + min(q, S - 1)) * ldq + h * DH;
@@ -479,7 +482,7 @@ __global__ void __launch_bounds__(TW_THREADS, 1) k_attn_prefill_ws(const float* 
     const uint32_t tmem = *tslot;
     const uint32_t tO = tmem + 128;  // S buffers at columns 0 and 64
 
-    if (warp == 8) {
+    if (warp == TW_MW) {
         // ---------------- MMA issuer
         if (lane == 0) {
             const uint32_t qh = smem_u32(sm + TwSmem::qh), ql = smem_u32(sm + TwSmem::ql);
@@ -519,15 +522,15 @@ __global__ void __launch_bounds__(TW_THREADS, 1) k_attn_prefill_ws(const float* 
             }
         }
         __syncwarp();
-    } else if (warp >= 4) {
+    } else if (warp >= TW_SW) {
         // ---------------- producer
-        const int p = tid - 128;
+        const int p = tid - TW_SW * 32;
         for (int t = 0; t < T; ++t) {
             const int bf = t & 1;
             const int k0 = t * TW_K;
             const int nk = min(TW_K, S - k0);
             cp_async_wait<0>();
-            asm volatile("bar.sync 1, 128;\n" ::: "memory");  // raw(t) landed; dequant(t-1) done by all
+            asm volatile("bar.sync 1, %0;\n" ::"n"(TW_PW * 32) : "memory");  // raw(t) landed; dequant(t-1) done
             if (t + 1 < T)
                 tw_load_raw<DH>(page_base(pool, page_bytes, pt, max_pages, b, k0 + TW_K), Hkv, kh,
                                 min(TW_K, S - k0 - TW_K), sm + TwSmem::raw + (size_t)((t + 1) & 1) * TwSmem::raw_sz,
@@ -569,43 +572,50 @@ __global__ void __launch_bounds__(TW_THREADS, 1) k_attn_prefill_ws(const float* 
             mbar_arrive(&kv_full[bf]);
         }
     } else {
-        // ---------------- softmax (thread tid = query row q0 + tid = TMEM lane tid)
-        const int q = q0 + tid;
+        // ---------------- softmax: query row r = TMEM lane r (warps w and w + 4 share lane quarter
+        // w), half hf of the tile's 64 keys and of O's 128 columns per thread
+        const int r = tid & 127, hf = tid >> 7;
+        const int q = q0 + r;
         const float sl2 = inv_sqrt * 1.4426950408889634f;
-        const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+        const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+        float* xch = reinterpret_cast<float*>(sm + TwSmem::xch);  // [2][2][128]
+        constexpr int HK = TW_K / 2;  // keys per thread
         float m_used = -1e30f, l = 0.f;
         for (int t = 0; t < T; ++t) {
             const int bf = t & 1;
             const uint32_t ph = (uint32_t)(t >> 1) & 1u;
-            const int k0 = t * TW_K;
+            const int k0 = t * TW_K + hf * HK;
             mbar_wait(&s_full[bf], ph);
             mbar_wait(&kv_full[bf], ph);  // this tile's scales
             ta_fence_after();
-            float s[TW_K];
-            ta_ld32(tmem + (uint32_t)(bf * 64) + lane_off, s);
-            ta_ld32(tmem + (uint32_t)(bf * 64 + 32) + lane_off, s + 32);
-            const float* ks = ksb + bf * TW_K;
-            const float* vs = vsb + bf * TW_K;
+            float s[HK];
+            ta_ld32(tmem + (uint32_t)(bf * 64 + hf * HK) + lane_off, s);
+            const float* ks = ksb + bf * TW_K + hf * HK;
+            const float* vs = vsb + bf * TW_K + hf * HK;
             // every (query, key) pair of the tile allowed and in range: no per-element mask
-            const int klast = k0 + TW_K - 1, qlast = q0 + TW_Q - 1;
+            const int klast = t * TW_K + TW_K - 1, qlast = q0 + TW_Q - 1;
             const bool full = qlast < S && klast < S &&
                               (qlast < V ? klast < V : (q0 >= V && (klast < V || klast <= q0)));
             float tmax = -1e30f;
             if (full) {
 #pragma unroll
-                for (int j = 0; j < TW_K; ++j) {
+                for (int j = 0; j < HK; ++j) {
                     s[j] *= ks[j] * sl2;
                     tmax = fmaxf(tmax, s[j]);
                 }
             } else {
 #pragma unroll
-                for (int j = 0; j < TW_K; ++j) {
+                for (int j = 0; j < HK; ++j) {
                     const int kj = k0 + j;
                     const bool ok = q < S && kj < S && (q < V ? kj < V : (kj < V || kj <= q));
                     s[j] = ok ? s[j] * (ks[j] * sl2) : -1e30f;
                     tmax = fmaxf(tmax, s[j]);
                 }
             }
+            // the row's tile max from both halves (the two threads then decide identically)
+            xch[(bf * 2 + hf) * 128 + r] = tmax;
+            asm volatile("bar.sync 2, %0;\n" ::"n"(TW_SW * 32) : "memory");
+            tmax = fmaxf(tmax, xch[(bf * 2 + (hf ^ 1)) * 128 + r]);
             const bool raise = tmax > m_used + 8.f;
             const float fac = raise ? exp2f(m_used - tmax) : 1.f;
             if (raise) {
@@ -616,7 +626,7 @@ __global__ void __launch_bounds__(TW_THREADS, 1) k_attn_prefill_ws(const float* 
                 mbar_wait(&pv_done[(t - 1) & 1], (uint32_t)((t - 1) >> 1) & 1u);
                 ta_fence_after();
 #pragma unroll 1
-                for (int c = 0; c < DH; c += 32) {
+                for (int c = hf * 64; c < hf * 64 + 64; c += 32) {
                     float o[32];
                     ta_ld32(tO + lane_off + c, o);
 #pragma unroll
@@ -630,7 +640,7 @@ __global__ void __launch_bounds__(TW_THREADS, 1) k_attn_prefill_ws(const float* 
             uint8_t* plb = sm + TwSmem::pl + (size_t)bf * 16384;
             float psum = 0.f;
 #pragma unroll
-            for (int c = 0; c < TW_K / 8; ++c) {
+            for (int c = 0; c < HK / 8; ++c) {
                 uint32_t hi[4], lo[4];
 #pragma unroll
                 for (int e = 0; e < 8; e += 2) {
@@ -640,23 +650,28 @@ __global__ void __launch_bounds__(TW_THREADS, 1) k_attn_prefill_ws(const float* 
                     psum += p0 + p1;
                     split_h2(p0 * vs[j], p1 * vs[j + 1], hi[e / 2], lo[e / 2]);
                 }
-                *reinterpret_cast<uint4*>(phb + ta_sw(tid, c)) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-                *reinterpret_cast<uint4*>(plb + ta_sw(tid, c)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+                const int chunk = hf * (HK / 8) + c;
+                *reinterpret_cast<uint4*>(phb + ta_sw(r, chunk)) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+                *reinterpret_cast<uint4*>(plb + ta_sw(r, chunk)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
             }
             l += psum;
             ta_fence_async();
             ta_fence_before();
             mbar_arrive(&p_full[bf]);
         }
-        // finalize: O / l, the attn_out quantizer's partial row max, (m, l) for the QUOTA sums
+        // finalize: O / l over this half's 64 columns; l and the row max |out| combined across the
+        // two halves; (m, l) for the QUOTA sums
+        xch[512 + hf * 128 + r] = l;
         mbar_wait(&pv_done[(T - 1) & 1], (uint32_t)((T - 1) >> 1) & 1u);
         ta_fence_after();
+        asm volatile("bar.sync 2, %0;\n" ::"n"(TW_SW * 32) : "memory");
+        const float lt = xch[512 + r] + xch[512 + 128 + r];  // half 0 + half 1, fixed order
         const bool ok = q < S;
-        const float inv_l = l > 0.f ? 1.f / l : 0.f;
+        const float inv_l = lt > 0.f ? 1.f / lt : 0.f;
         float* orow = out + (size_t)(tok0 + min(q, S - 1)) * ldo + h * DH;
         float mx = 0.f;
 #pragma unroll 1
-        for (int c = 0; c < DH; c += 32) {
+        for (int c = hf * 64; c < hf * 64 + 64; c += 32) {
             float o[32];
             ta_ld32(tO + lane_off + c, o);
 #pragma unroll
@@ -668,14 +683,16 @@ __global__ void __launch_bounds__(TW_THREADS, 1) k_attn_prefill_ws(const float* 
 #pragma unroll
                 for (int i = 0; i < 32; i += 8) st_v8f32(orow + c + i, o + i);
         }
-        if (ok) {
-            if (ml) ml[(size_t)(tok0 + q) * H + h] = make_float2(m_used * 0.69314718055994531f, l);
-            if (pmax) pmax[(size_t)(tok0 + q) * pmax_ld + h] = mx;
+        xch[768 + hf * 128 + r] = mx;
+        asm volatile("bar.sync 2, %0;\n" ::"n"(TW_SW * 32) : "memory");
+        if (ok && hf == 0) {
+            if (ml) ml[(size_t)(tok0 + q) * H + h] = make_float2(m_used * 0.69314718055994531f, lt);
+            if (pmax) pmax[(size_t)(tok0 + q) * pmax_ld + h] = fmaxf(mx, xch[768 + 128 + r]);
         }
     }
     ta_fence_before();
     __syncthreads();
-    if (warp == 8) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;\n" ::"r"(tmem));
+    if (warp == TW_MW) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;\n" ::"r"(tmem));
 }
 
 // ============================================================== K3a
