@@ -795,12 +795,10 @@ int qt_launch_attn_prefill(const float* qkv, int ldq, int H, int Hkv, int dh, co
     if (B <= 0 || smax <= 0) return 0;
     if (pmax && H > pmax_ld) return -1;
     const float inv_sqrt = (float)(1.0 / sqrt((double)dh));
-#ifndef QT_ATTN_WS_MIN_S
-#define QT_ATTN_WS_MIN_S 512  // longest sequence from which d_head 128 runs the tcgen05 kernel
-                              // (A/B: C3 attention 24.9 -> 20.6 ms, C2 4.50 -> 4.37; below 512 tokens
-                              // the 128-query tiles are mostly empty and the mma.sync kernel wins)
-#endif
-    if (dh == 128 && smax >= QT_ATTN_WS_MIN_S) {
+    // d_head 128: the warp-specialised tcgen05 kernel at every batch length (A/B against the
+    // mma.sync kernel from 0 / 256 / 512 tokens: equal within noise below 512, faster above);
+    // d_head 64 (configs[0]): the mma.sync kernel
+    if (dh == 128) {
         const dim3 gws((smax + TW_Q - 1) / TW_Q, H, B);
         cudaFuncSetAttribute(k_attn_prefill_ws, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TwSmem::total);
         k_attn_prefill_ws<<<gws, TW_THREADS, TwSmem::total, st>>>(qkv, ldq, H, Hkv, seq_off, vis, seq_len, pool,
@@ -809,10 +807,7 @@ int qt_launch_attn_prefill(const float* qkv, int ldq, int H, int Hkv, int dh, co
         return (int)cudaGetLastError();
     }
     const dim3 grid((smax + AT_Q - 1) / AT_Q, H, B);
-    if (dh == 128)
-        k_attn_prefill<128><<<grid, 32 * AT_QW, 0, st>>>(qkv, ldq, H, Hkv, seq_off, vis, seq_len, pool, page_bytes, pt,
-                                                  max_pages, inv_sqrt, out, ldo, reinterpret_cast<float2*>(ml), pmax, pmax_ld);
-    else if (dh == 64)
+    if (dh == 64)
         k_attn_prefill<64><<<grid, 32 * AT_QW, 0, st>>>(qkv, ldq, H, Hkv, seq_off, vis, seq_len, pool, page_bytes, pt,
                                                  max_pages, inv_sqrt, out, ldo, reinterpret_cast<float2*>(ml), pmax, pmax_ld);
     else

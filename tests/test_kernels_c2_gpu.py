@@ -78,8 +78,8 @@ def _layout(lens, seed):
     return pos, np.array(ts, np.int32), np.array(tr, np.int32), np.array(off, np.int32)
 
 
-SHAPES = [  # (H, Hkv, dh, lens): C2 MHA 7B, C4 GQA 7B, the tiny GQA config; smax >= 512 runs the
-    # tcgen05 prefill attention (k_attn_prefill_ws), shorter batches the mma.sync one
+SHAPES = [  # (H, Hkv, dh, lens): C2 MHA 7B, C4 GQA 7B, the tiny GQA config; d_head 128 runs the
+    # tcgen05 prefill attention (k_attn_prefill_ws), d_head 64 the mma.sync one
     (32, 32, 128, [640, 237]),
     (28, 4, 128, [300, 77]),
     (28, 4, 128, [700, 515, 77]),
