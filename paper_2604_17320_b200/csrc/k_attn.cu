@@ -306,6 +306,11 @@ __global__ void __launch_bounds__(32 * AT_QW, AT_QW > 4 ? 1 : QT_ATTN_MINB) k_at
 }
 
 // ---------------------------------------------------------------- tcgen05 helpers (kind::f16)
+QT_DEV float ex2_approx(float x) {  // 2^x, flush-to-zero (x < -126 -> 0)
+    float r;
+    asm("ex2.approx.ftz.f32 %0, %1;\n" : "=f"(r) : "f"(x));
+    return r;
+}
 QT_DEV uint64_t ta_desc(uint32_t saddr) {  // K-major SWIZZLE_128B smem descriptor (SBO 1024)
     uint64_t d = 0;
     d |= (uint64_t)((saddr >> 4) & 0x3FFF);
@@ -565,7 +570,7 @@ __global__ void __launch_bounds__(TW_THREADS, 1) k_attn_prefill_ws(const float* 
             }
             if (p < TW_K) {
                 const float* sc = reinterpret_cast<const float*>(raw + 8192);
-                ksb[bf * TW_K + p] = p < nk ? sc[p] : 0.f;
+                ksb[bf * TW_K + p] = p < nk ? sc[p] * (inv_sqrt * 1.4426950408889634f) : 0.f;  // s_k / sqrt(dh) * log2 e
                 vsb[bf * TW_K + p] = p < nk ? sc[TW_K + p] : 0.f;
             }
             ta_fence_async();
@@ -576,7 +581,6 @@ __global__ void __launch_bounds__(TW_THREADS, 1) k_attn_prefill_ws(const float* 
         // w), half hf of the tile's 64 keys and of O's 128 columns per thread
         const int r = tid & 127, hf = tid >> 7;
         const int q = q0 + r;
-        const float sl2 = inv_sqrt * 1.4426950408889634f;
         const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
         float* xch = reinterpret_cast<float*>(sm + TwSmem::xch);  // [2][2][128]
         constexpr int HK = TW_K / 2;  // keys per thread
@@ -600,7 +604,7 @@ __global__ void __launch_bounds__(TW_THREADS, 1) k_attn_prefill_ws(const float* 
             if (full) {
 #pragma unroll
                 for (int j = 0; j < HK; ++j) {
-                    s[j] *= ks[j] * sl2;
+                    s[j] *= ks[j];
                     tmax = fmaxf(tmax, s[j]);
                 }
             } else {
@@ -608,7 +612,7 @@ __global__ void __launch_bounds__(TW_THREADS, 1) k_attn_prefill_ws(const float* 
                 for (int j = 0; j < HK; ++j) {
                     const int kj = k0 + j;
                     const bool ok = q < S && kj < S && (q < V ? kj < V : (kj < V || kj <= q));
-                    s[j] = ok ? s[j] * (ks[j] * sl2) : -1e30f;
+                    s[j] = ok ? s[j] * ks[j] : -1e30f;
                     tmax = fmaxf(tmax, s[j]);
                 }
             }
@@ -645,8 +649,9 @@ __global__ void __launch_bounds__(TW_THREADS, 1) k_attn_prefill_ws(const float* 
 #pragma unroll
                 for (int e = 0; e < 8; e += 2) {
                     const int j = 8 * c + e;
-                    const float p0 = s[j] <= -1e30f ? 0.f : exp2f(s[j] - m_used);
-                    const float p1 = s[j + 1] <= -1e30f ? 0.f : exp2f(s[j + 1] - m_used);
+                    // masked scores (-1e30) underflow to exactly 0 (ex2.approx of < -126 flushes)
+                    const float p0 = ex2_approx(s[j] - m_used);
+                    const float p1 = ex2_approx(s[j + 1] - m_used);
                     psum += p0 + p1;
                     split_h2(p0 * vs[j], p1 * vs[j + 1], hi[e / 2], lo[e / 2]);
                 }
