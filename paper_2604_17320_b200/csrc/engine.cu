@@ -1598,7 +1598,7 @@ struct qt_engine {
         dec_lsplit.assign(L, 1);
         dec_pps = dec_splits = 1;
         for (int l = 0; l < L; ++l) {
-            if (qt_attn_decode_plan(B, Hkv, dec_pages[l], n_sms, &dec_lpps[l], &dec_lsplit[l]))
+            if (qt_attn_decode_plan(B, H, Hkv, dec_pages[l], n_sms, &dec_lpps[l], &dec_lsplit[l]))
                 fail(QT_EINVAL, "decode attention plan");
             dec_pps = std::max(dec_pps, dec_lpps[l]);
             dec_splits = std::max(dec_splits, dec_lsplit[l]);
@@ -2644,7 +2644,7 @@ int qt_attn_decode_i4kv(const float* q, int ldq, int B, int H, int Hkv, int d_he
         int dev = 0, sms = 148, pps = 1, nsplit = 1;
         ck(cudaGetDevice(&dev), "device");
         ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "sm count");
-        if (qt_attn_decode_plan(B, Hkv, pages, sms, &pps, &nsplit)) fail(QT_EINVAL, "decode attention plan");
+        if (qt_attn_decode_plan(B, H, Hkv, pages, sms, &pps, &nsplit)) fail(QT_EINVAL, "decode attention plan");
         ckl(qt_launch_attn_decode(q, ldq, H, Hkv, d_head, kv_len, B, const_cast<uint8_t*>(pool), page_bytes,
                                   page_table, max_pages, pps, nsplit, nullptr, nullptr, part_ml, part_o, out, ldo,
                                   nullptr, 0, nullptr, 1, 0.0, 0, 4, nullptr, 0, (cudaStream_t)stream),

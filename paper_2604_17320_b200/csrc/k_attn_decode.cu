@@ -6,7 +6,10 @@
 // quant.cpp:117-119), then per query head an unmasked max-subtracted softmax of
 // q . k^ / sqrt(d_head) over every cached row and out = sum_j p_j v^_j (model.cpp:515-535).
 //
-// B200 layout of the work: one CTA per (page split, kv head, sequence) serves all
+// Two kernels.  MHA and G = 2 (C1, C2, C3, C5): k_attn_dec_w below -- one warp per (page,
+// kv head, sequence), both products as exact integer MMAs on the stored codes.  GQA with
+// G >= 4 (C4): k_attn_dec --
+// one CTA per (page split, kv head, sequence) serves all
 // G = H / Hkv query heads of its kv head, so every cached K/V byte is read from HBM once
 // (GQA included).  The split's pages -- per (page, kv head) one contiguous 4 KB K block,
 // one V block and two 256 B scale vectors -- arrive by cp.async.bulk (TMA 1D) into shared
@@ -34,6 +37,9 @@ constexpr int AD_MAX_PPS = 8;  // pages per split (smem: 8.5 KB each at d_head 1
 #ifndef QT_AD_PLAN_PPS
 #define QT_AD_PLAN_PPS 2  // the split plan's page cap (A/B 8 / 2 / 1 pages: C5 B = 256 decode chain
                           // 9.76 / 9.32 / 10.68 ms per step; C2, C4 equal within noise)
+#endif
+#ifndef QT_AD_WARP
+#define QT_AD_WARP 1  // 1: k_attn_dec_w (integer tensor cores, one warp per page); 0: k_attn_dec
 #endif
 constexpr int AD_MAX_G = 8;    // query heads per kv head (one softmax warp each)
 
@@ -299,6 +305,369 @@ __global__ void __launch_bounds__(AD_THREADS) k_attn_dec(const float* __restrict
     }
 }
 
+// ---------------------------------------------------------------- K6 on integer tensor cores
+// One WARP per (page, kv head, sequence), serving the G query heads of its kv head; a CTA is
+// up to 4 warps (4 kv heads of the same page) with no block barrier.  The page's K / V code
+// blocks and scales arrive by cp.async.bulk into the warp's own smem slice.
+//
+// Both products run as exact integer MMAs (mma.sync m16n8k32 s8.s8.s32) on the codes as
+// stored: the fp32 operand (q, then p * s_v) is written as a fixed-point integer Q =
+// rint(x * 2^F) (|Q| < 2^30, F from the head's max |x|) in four balanced base-256 digits, one
+// MMA column per digit: S = sum_d Q_d * c_d is exact in int32 per digit and recombined exactly
+// in fp64, so a score's only roundings are the fixed-point step (2^-31 of the head's max |q|)
+// and one fp32 rounding -- tighter than the fp32 dot product of k_attn_dec.
+//   QK: A = K codes (16 keys x 32 dims, 16 * code in s8 as unpack_x16 gives), B = q digits.
+//   PV: A = V^T (16 channels x 32 keys), built by a 4 x 4 byte transpose of 4 keys' code
+//       words (PRMT) then unpack_x16; B = (p * s_v) digits.
+// Balanced digits of Q: U = Q + 0x80808080 has bytes d_j + 128, so (U ^ 0x80808080) holds
+// the four signed digits d_j directly.
+constexpr int AW_MAXW = 4;  // warps (kv heads) per CTA
+// query heads per kv head served by k_attn_dec_w: its one warp runs every head's softmax and
+// (G + 1) / 2 MMA column tiles serially, which at G = 7 (C4) measured slower than k_attn_dec
+// (decode attention chain 0.613 vs 0.487 ms/step; MHA at C5 B = 256: 2.64 vs 5.32 ms)
+constexpr int AW_MAX_G = 2;
+template <int DH, int G>
+struct AwSmem {  // one warp's slice
+    static constexpr int CB = kPage * (DH / 2);
+    static constexpr size_t kc = 0, vc = CB, ks = 2 * CB, vs = ks + kPage * 4;
+    static constexpr size_t sc = vs + kPage * 4;        // [G][64] scores
+    static constexpr size_t ql = sc + G * kPage * 4;     // [G][4 digits][DH] q digits, MMA-B order
+    static constexpr size_t wl = ql + G * 4 * DH;        // [G][4 digits][64] (p * s_v) digits
+    static constexpr size_t bar = (wl + G * 4 * kPage + 15) / 16 * 16;
+    static constexpr size_t total = (bar + 8 + 127) / 128 * 128;
+};
+QT_DEV uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+    uint32_t r;
+    asm("prmt.b32 %0, %1, %2, %3;\n" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+    return r;
+}
+// position of dim d (word d / 8, nibble d % 8) in a digit row: the MMA-B fragment's bytes
+// (even nibbles of a word, then odd ones) contiguous
+QT_DEV int aw_qpos(int d) { return (d & ~7) | ((d & 1) << 2) | ((d >> 1) & 3); }
+// position of key k = 32 s + 16 h + t + 4 i in a digit row: 32 s + 16 h + 4 t + i
+QT_DEV int aw_kpos(int k) { return (k & 48) | ((k & 3) << 2) | ((k >> 2) & 3); }
+// fixed-point exponent: |x| * 2^F < 2^30 for every |x| <= mx
+QT_DEV int aw_fexp(float mx) {
+    if (!(mx > 0.f)) return 0;
+    int e;
+    frexpf(mx, &e);
+    return 30 - e;
+}
+QT_DEV uint32_t aw_digits(float x, int F) {  // the four signed digits of rint(x * 2^F)
+    const int Q = __double2int_rn((double)x * ldexp(1.0, F));
+    return ((uint32_t)Q + 0x80808080u) ^ 0x80808080u;
+}
+
+template <int DH, int G>
+__global__ void __launch_bounds__(AW_MAXW * 32) k_attn_dec_w(const float* __restrict__ qkv, int ldq, int H, int Hkv,
+                                                             const int* __restrict__ kv_len, uint8_t* __restrict__ pool,
+                                                             long long page_bytes, const int* __restrict__ pt,
+                                                             int max_pages, const double2* __restrict__ rope,
+                                                             const int* __restrict__ pos, float inv_sqrt,
+                                                             float* __restrict__ part_ml, float* __restrict__ part_o) {
+    using S = AwSmem<DH, G>;
+    constexpr int CB = S::CB;
+    constexpr int NT = (G + 1) / 2;  // n8 tiles: two heads x four digits each
+    constexpr int KS = DH / 32;      // QK k-steps; also the 32-bit code words a lane reads per key
+    constexpr int MT = DH / 16;      // PV m-tiles (channels)
+    constexpr int WPG = DH / 64;     // code words per key a lane transposes in PV
+    extern __shared__ __align__(128) uint8_t sm_all[];
+    pdl_launch_dependents();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane >> 2, t = lane & 3;
+    const int kh = blockIdx.y * (blockDim.x >> 5) + warp;
+    if (kh >= Hkv) {
+        pdl_wait();
+        return;
+    }
+    uint8_t* sm = sm_all + (size_t)warp * S::total;
+    const int p = blockIdx.x, nsplit = gridDim.x, b = blockIdx.z;
+    const bool fused = rope != nullptr;
+    const int old_len = kv_len[b];
+    const int len = old_len + (fused ? 1 : 0);
+    const int r0 = p * kPage;
+    const int n_rows = min(kPage, len - r0);
+    const size_t pidx0 = ((size_t)b * H + (size_t)kh * G) * nsplit + p;
+    if (n_rows <= 0) {  // nothing cached in this page: an empty partial per head
+        pdl_wait();     // the partial buffers are still read by the previous layer's merge
+#pragma unroll
+        for (int gh = 0; gh < G; ++gh)
+            for (int c = lane; c < DH; c += 32) part_o[(pidx0 + (size_t)gh * nsplit) * DH + c] = 0.f;
+        if (lane < G) {
+            part_ml[(pidx0 + (size_t)lane * nsplit) * 2] = -1e30f;
+            part_ml[(pidx0 + (size_t)lane * nsplit) * 2 + 1] = 0.f;
+        }
+        return;
+    }
+    uint8_t* kc = sm + S::kc;
+    uint8_t* vc = sm + S::vc;
+    float* ksc = reinterpret_cast<float*>(sm + S::ks);
+    float* vsc = reinterpret_cast<float*>(sm + S::vs);
+    float* sc = reinterpret_cast<float*>(sm + S::sc);
+    uint8_t* ql = sm + S::ql;
+    uint8_t* wl = sm + S::wl;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + S::bar);
+    const size_t cbh = (size_t)Hkv * CB;
+    if (lane == 0) {
+        mbar_init(bar, 1);
+        mbar_fence_init();
+        mbar_arrive_expect_tx(bar, (uint32_t)(2 * CB + 2 * kPage * 4));
+        const uint8_t* page = pool + (long long)pt[b * max_pages + p] * page_bytes;
+        bulk_g2s(kc, page + (size_t)kh * CB, CB, bar);
+        bulk_g2s(vc, page + cbh + (size_t)kh * CB, CB, bar);
+        bulk_g2s(ksc, page + 2 * cbh + (size_t)kh * kPage * 4, kPage * 4, bar);
+        bulk_g2s(vsc, page + 2 * cbh + ((size_t)Hkv + kh) * kPage * 4, kPage * 4, bar);
+    }
+    pdl_wait();  // q (and the new token's k / v) come from the upstream GEMV
+
+    // q of the G heads (RoPE'd here in the decode step: fp64, rounded to fp32 like the
+    // prefill's k_rope_kv_append) -> fixed-point digits in MMA-B order
+    const float* qrow = qkv + (size_t)b * ldq;
+    const double2* rt = fused ? rope + (size_t)pos[b] * (DH / 2) : nullptr;
+    constexpr int PPL = DH / 64;  // dim pairs per lane per head
+    int F[G];
+#pragma unroll
+    for (int gh = 0; gh < G; ++gh) {
+        float2 v[PPL];
+        float mx = 0.f;
+#pragma unroll
+        for (int j = 0; j < PPL; ++j) {
+            const int pr = lane + 32 * j;
+            v[j] = *reinterpret_cast<const float2*>(qrow + (size_t)(kh * G + gh) * DH + 2 * pr);
+            if (fused) {
+                const double2 cs = rt[pr];
+                const double a = v[j].x, bb = v[j].y;
+                v[j].x = (float)__dsub_rn(__dmul_rn(a, cs.x), __dmul_rn(bb, cs.y));
+                v[j].y = (float)__dadd_rn(__dmul_rn(a, cs.y), __dmul_rn(bb, cs.x));
+            }
+            mx = fmaxf(mx, fmaxf(fabsf(v[j].x), fabsf(v[j].y)));
+        }
+        F[gh] = aw_fexp(warp_max(mx));
+#pragma unroll
+        for (int j = 0; j < PPL; ++j) {
+            const int d = 2 * (lane + 32 * j);
+            const uint32_t L0 = aw_digits(v[j].x, F[gh]), L1 = aw_digits(v[j].y, F[gh]);
+            uint8_t* row = ql + (size_t)gh * 4 * DH;
+#pragma unroll
+            for (int dg = 0; dg < 4; ++dg) {
+                row[dg * DH + aw_qpos(d)] = (uint8_t)(L0 >> (8 * dg));
+                row[dg * DH + aw_qpos(d + 1)] = (uint8_t)(L1 >> (8 * dg));
+            }
+        }
+    }
+    // the new row (decode step): its K (RoPE'd) then its V -- kv_quantize in fp64, appended
+    const int new_r = old_len - r0;  // row within this page
+    const bool has_new = fused && new_r >= 0 && new_r < n_rows;
+    constexpr int E = DH / 32;
+    uint32_t new_word[2] = {0u, 0u};
+    float new_scale[2] = {0.f, 0.f};
+    if (has_new) {
+        uint8_t* page = pool + (long long)pt[b * max_pages + p] * page_bytes;
+#pragma unroll
+        for (int kv = 0; kv < 2; ++kv) {
+            const float* src = qrow + (kv == 0 ? H * DH : (H + Hkv) * DH) + kh * DH + lane * E;
+            double val[E];
+#pragma unroll
+            for (int j = 0; j < E; ++j) val[j] = (double)src[j];
+            if (kv == 0) {
+#pragma unroll
+                for (int j = 0; j < E; j += 2) {
+                    const double2 cs = rt[(lane * E + j) / 2];
+                    const double a = val[j], bb = val[j + 1];
+                    val[j] = __dsub_rn(__dmul_rn(a, cs.x), __dmul_rn(bb, cs.y));
+                    val[j + 1] = __dadd_rn(__dmul_rn(a, cs.y), __dmul_rn(bb, cs.x));
+                }
+            }
+            double mx = 0.0;
+#pragma unroll
+            for (int j = 0; j < E; ++j) mx = fmax(mx, fabs(val[j]));
+            mx = warp_max(mx);
+            const double s = q_scale(mx, 7), inv_s = 1.0 / s;
+            uint32_t w = 0;
+#pragma unroll
+            for (int j = 0; j < E; ++j) w |= (uint32_t)(q_code_r(val[j], s, inv_s, 7) & 0xF) << (4 * j);
+            new_word[kv] = w;
+            new_scale[kv] = (float)s;
+            // append to the cache (model.cpp:499-501)
+            uint8_t* dst = page + (kv == 0 ? 0 : cbh) + (size_t)kh * CB + (size_t)new_r * (DH / 2) + lane * E / 2;
+            if (E == 4) *reinterpret_cast<uint16_t*>(dst) = (uint16_t)w;
+            else *dst = (uint8_t)w;
+            if (lane == 0)
+                reinterpret_cast<float*>(page + 2 * cbh)[(kv == 0 ? 0 : Hkv * kPage) + kh * kPage + new_r] =
+                    (float)s;
+        }
+    }
+    mbar_wait(bar, 0);  // the page has landed
+    if (has_new) {      // ... and the new row replaces its (stale) shared copy
+#pragma unroll
+        for (int kv = 0; kv < 2; ++kv) {
+            uint8_t* d = (kv == 0 ? kc : vc) + (size_t)new_r * (DH / 2) + lane * E / 2;
+            if (E == 4) *reinterpret_cast<uint16_t*>(d) = (uint16_t)new_word[kv];
+            else *d = (uint8_t)new_word[kv];
+        }
+        if (lane == 0) {
+            ksc[new_r] = new_scale[0];
+            vsc[new_r] = new_scale[1];
+        }
+    }
+    __syncwarp();
+
+    // ---- scores: S[key][head] for the 64 keys (4 m-tiles of 16 keys)
+    {
+        uint32_t kw[4][2][KS];  // lane's code words: keys 16 mt + g (+ 8), words KS * t ..
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+                const uint8_t* src = kc + (size_t)(16 * mt + g + 8 * hf) * (DH / 2) + t * KS * 4;
+                if constexpr (KS == 4) {
+                    const uint4 w4 = *reinterpret_cast<const uint4*>(src);
+                    kw[mt][hf][0] = w4.x; kw[mt][hf][1] = w4.y; kw[mt][hf][2] = w4.z; kw[mt][hf][3] = w4.w;
+                } else {
+                    const uint2 w2 = *reinterpret_cast<const uint2*>(src);
+                    kw[mt][hf][0] = w2.x; kw[mt][hf][1] = w2.y;
+                }
+            }
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+            const int hq = 2 * nt + (g >> 2);  // the B column's head and digit
+            uint32_t bq[KS][2];
+#pragma unroll
+            for (int s = 0; s < KS; ++s) {
+                const uint2 v = hq < G ? *reinterpret_cast<const uint2*>(ql + (size_t)(hq * 4 + (g & 3)) * DH +
+                                                                         8 * (KS * t + s))
+                                       : make_uint2(0u, 0u);
+                bq[s][0] = v.x;
+                bq[s][1] = v.y;
+            }
+            const int ho = 2 * nt + (t >> 1);  // the accumulator columns' head
+            const int Fo = (2 * nt + 1 < G && (t >> 1)) ? F[(2 * nt + 1) % G] : F[2 * nt];
+            const double qsc = ldexp(1.0, -(Fo + 4)) * (double)inv_sqrt;
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt) {
+                int acc[4] = {0, 0, 0, 0};
+#pragma unroll
+                for (int s = 0; s < KS; ++s) {
+                    uint32_t a[4];
+                    unpack_x16(kw[mt][0][s], a[0], a[2]);
+                    unpack_x16(kw[mt][1][s], a[1], a[3]);
+                    mma_s8_16832(acc, a, bq[s]);
+                }
+                const int P0 = acc[0] + (acc[1] << 8), P1 = acc[2] + (acc[3] << 8);  // digits 2(t&1), +1
+                const int U0 = __shfl_xor_sync(0xffffffffu, P0, 1), U1 = __shfl_xor_sync(0xffffffffu, P1, 1);
+                if (!(t & 1) && ho < G) {
+                    const int k0 = 16 * mt + g;
+                    sc[ho * kPage + k0] =
+                        (float)(((double)P0 + (double)U0 * 65536.0) * qsc) * ksc[k0];
+                    sc[ho * kPage + k0 + 8] =
+                        (float)(((double)P1 + (double)U1 * 65536.0) * qsc) * ksc[k0 + 8];
+                }
+            }
+        }
+    }
+    __syncwarp();
+    // ---- softmax per head over the page's rows; p * s_v -> fixed-point digits
+    float m_h[G], l_h[G];
+    double osc[G];
+#pragma unroll
+    for (int gh = 0; gh < G; ++gh) {
+        const bool ok0 = lane < n_rows, ok1 = lane + 32 < n_rows;
+        const float s0 = ok0 ? sc[gh * kPage + lane] : -1e30f, s1 = ok1 ? sc[gh * kPage + lane + 32] : -1e30f;
+        const float m = warp_max(fmaxf(s0, s1));
+        const float p0 = ok0 ? expf(s0 - m) : 0.f, p1 = ok1 ? expf(s1 - m) : 0.f;
+        const float w0 = p0 * (ok0 ? vsc[lane] : 0.f), w1 = p1 * (ok1 ? vsc[lane + 32] : 0.f);
+        m_h[gh] = m;
+        l_h[gh] = warp_sum(p0 + p1);
+        const int Fw = aw_fexp(warp_max(fmaxf(w0, w1)));
+        osc[gh] = ldexp(1.0, -(Fw + 4));
+        const uint32_t L0 = aw_digits(w0, Fw), L1 = aw_digits(w1, Fw);
+        uint8_t* row = wl + (size_t)gh * 4 * kPage;
+#pragma unroll
+        for (int dg = 0; dg < 4; ++dg) {
+            row[dg * kPage + aw_kpos(lane)] = (uint8_t)(L0 >> (8 * dg));
+            row[dg * kPage + aw_kpos(lane + 32)] = (uint8_t)(L1 >> (8 * dg));
+        }
+    }
+    __syncwarp();
+    // ---- P . V: o[channel][head]; A = V^T by 4 x 4 byte transposes of 4 keys' code words
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+        const int hq = 2 * nt + (g >> 2);
+        int acc[MT][4];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) acc[mt][0] = acc[mt][1] = acc[mt][2] = acc[mt][3] = 0;
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+            uint32_t bw[2];
+            bw[0] = hq < G ? *reinterpret_cast<const uint32_t*>(wl + (size_t)(hq * 4 + (g & 3)) * kPage + 32 * s + 4 * t) : 0u;
+            bw[1] = hq < G ? *reinterpret_cast<const uint32_t*>(wl + (size_t)(hq * 4 + (g & 3)) * kPage + 32 * s + 16 + 4 * t) : 0u;
+            // R[hf][ww][e]: channel (word WPG * g + ww, nibble e) of keys 32 s + 16 hf + t + 4 i
+            uint32_t R[2][WPG][8];
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+                uint32_t w[4][WPG];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const uint8_t* src = vc + (size_t)(32 * s + 16 * hf + t + 4 * i) * (DH / 2) + g * WPG * 4;
+                    if constexpr (WPG == 2) {
+                        const uint2 v2 = *reinterpret_cast<const uint2*>(src);
+                        w[i][0] = v2.x;
+                        w[i][1] = v2.y;
+                    } else {
+                        w[i][0] = *reinterpret_cast<const uint32_t*>(src);
+                    }
+                }
+#pragma unroll
+                for (int ww = 0; ww < WPG; ++ww) {
+                    const uint32_t t0 = prmt(w[0][ww], w[1][ww], 0x5140), t1 = prmt(w[0][ww], w[1][ww], 0x7362);
+                    const uint32_t t2 = prmt(w[2][ww], w[3][ww], 0x5140), t3 = prmt(w[2][ww], w[3][ww], 0x7362);
+                    const uint32_t T[4] = {prmt(t0, t2, 0x5410), prmt(t0, t2, 0x7632), prmt(t1, t3, 0x5410),
+                                           prmt(t1, t3, 0x7632)};  // T[c] = byte c of the 4 keys
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) unpack_x16(T[c], R[hf][ww][2 * c], R[hf][ww][2 * c + 1]);
+                }
+            }
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) {
+                // rows g / g + 8 of m-tile mt: channel 8 WPG g + mt / 8 WPG g + DH / 16 + mt
+                constexpr int HALF = DH / 16;  // == 8 WPG / 2 ... channel offset of row g + 8
+                const int e0 = mt, e1 = HALF + mt;  // nibble index within the lane's 8 * WPG channels
+                uint32_t a[4];
+                a[0] = R[0][e0 >> 3][e0 & 7];
+                a[1] = R[0][e1 >> 3][e1 & 7];
+                a[2] = R[1][e0 >> 3][e0 & 7];
+                a[3] = R[1][e1 >> 3][e1 & 7];
+                mma_s8_16832(acc[mt], a, bw);
+            }
+        }
+        const int ho = 2 * nt + (t >> 1);
+        const double oscale = (2 * nt + 1 < G && (t >> 1)) ? osc[(2 * nt + 1) % G] : osc[2 * nt];
+        float o[2][MT];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+            const int P0 = acc[mt][0] + (acc[mt][1] << 8), P1 = acc[mt][2] + (acc[mt][3] << 8);
+            const int U0 = __shfl_xor_sync(0xffffffffu, P0, 1), U1 = __shfl_xor_sync(0xffffffffu, P1, 1);
+            o[0][mt] = (float)(((double)P0 + (double)U0 * 65536.0) * oscale);
+            o[1][mt] = (float)(((double)P1 + (double)U1 * 65536.0) * oscale);
+        }
+        if (!(t & 1) && ho < G) {  // channels 8 WPG g .. 8 WPG g + 8 WPG - 1 (rows g, then g + 8)
+            float* dst = part_o + (pidx0 + (size_t)ho * nsplit) * DH + 8 * WPG * g;
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf)
+#pragma unroll
+                for (int c = 0; c < MT; c += 4)
+                    *reinterpret_cast<float4*>(dst + hf * MT + c) =
+                        make_float4(o[hf][c], o[hf][c + 1], o[hf][c + 2], o[hf][c + 3]);
+        }
+    }
+#pragma unroll
+    for (int gh = 0; gh < G; ++gh)
+        if (lane == gh) {
+            part_ml[(pidx0 + (size_t)gh * nsplit) * 2] = m_h[gh];
+            part_ml[(pidx0 + (size_t)gh * nsplit) * 2 + 1] = l_h[gh];
+        }
+}
+
 // Merge the split partials of every head of one sequence (fixed split order) and,
 // optionally, quantize the concatenated attention row (the attn_out site,
 // model.cpp:394/539) in the same kernel.  grid B, 1024 threads: warp w merges heads
@@ -408,6 +777,18 @@ __global__ void __launch_bounds__(1024) k_attn_merge_quant(const float* __restri
 }
 
 template <int DH, int G>
+static int launch_dec_w(int nsplit, int Hkv, int B, cudaStream_t st, const float* qkv, int ldq, int H,
+                        const int* kv_len, uint8_t* pool, long long page_bytes, const int* pt, int max_pages,
+                        const double2* rope, const int* pos, float inv_sqrt, float* part_ml, float* part_o) {
+    const int wpc = std::min(AW_MAXW, Hkv);
+    const size_t smem = (size_t)wpc * AwSmem<DH, G>::total;
+    auto kfn = k_attn_dec_w<DH, G>;
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    return launch_pdl(kfn, dim3(nsplit, (Hkv + wpc - 1) / wpc, B), dim3(32 * wpc), smem, st, qkv, ldq, H, Hkv,
+                      kv_len, pool, page_bytes, pt, max_pages, rope, pos, inv_sqrt, part_ml, part_o);
+}
+
+template <int DH, int G>
 static int launch_dec(dim3 grid, int pps, cudaStream_t st, const float* qkv, int ldq, int H, int Hkv,
                       const int* kv_len, uint8_t* pool, long long page_bytes, const int* pt, int max_pages,
                       const double2* rope, const int* pos, float inv_sqrt, float* part_ml, float* part_o) {
@@ -418,17 +799,37 @@ static int launch_dec(dim3 grid, int pps, cudaStream_t st, const float* qkv, int
                       max_pages, pps, rope, pos, inv_sqrt, part_ml, part_o);
 }
 
+// k_attn_dec_w for G <= AW_MAX_G (the plan then gives one page per split), else k_attn_dec
+template <int DH, int G>
+static int launch_any(dim3 grid, int pps, cudaStream_t st, const float* qkv, int ldq, int H, int Hkv,
+                      const int* kv_len, uint8_t* pool, long long page_bytes, const int* pt, int max_pages,
+                      const double2* rope, const int* pos, float inv_sqrt, float* part_ml, float* part_o) {
+    if constexpr (QT_AD_WARP && G <= AW_MAX_G) {
+        if (pps != 1) return -1;
+        return launch_dec_w<DH, G>((int)grid.x, Hkv, (int)grid.z, st, qkv, ldq, H, kv_len, pool, page_bytes, pt,
+                                   max_pages, rope, pos, inv_sqrt, part_ml, part_o);
+    } else {
+        return launch_dec<DH, G>(grid, pps, st, qkv, ldq, H, Hkv, kv_len, pool, page_bytes, pt, max_pages, rope, pos,
+                                 inv_sqrt, part_ml, part_o);
+    }
+}
+
 }  // namespace qt
 
 using namespace qt;
 
 extern "C" {
 
-int qt_attn_decode_plan(int B, int Hkv, int pages, int sms, int* pps, int* nsplit) {
-    if (pages < 1 || B < 1) return -1;
+int qt_attn_decode_plan(int B, int H, int Hkv, int pages, int sms, int* pps, int* nsplit) {
+    if (pages < 1 || B < 1 || Hkv < 1 || H % Hkv) return -1;
     // enough CTAs for QT_AD_CTA_MULT per SM, at most AD_MAX_PPS pages each (measured against
     // fewer CTAs and against a per-warp-chunk kernel with the attn_out quantizer fused by the last
     // arrival: tools/gpu_attn_ab.sh)
+    if (QT_AD_WARP && H / Hkv <= AW_MAX_G) {  // k_attn_dec_w: one warp per (page, kv head, sequence)
+        *pps = 1;
+        *nsplit = pages;
+        return 0;
+    }
     int ns = std::max(1, std::min(pages, (QT_AD_CTA_MULT * sms + B * Hkv - 1) / (B * Hkv)));
     int p = (pages + ns - 1) / ns;
     if (p > QT_AD_PLAN_PPS) p = QT_AD_PLAN_PPS;
@@ -451,10 +852,8 @@ int qt_launch_attn_decode(const float* qkv, int ldq, int H, int Hkv, int dh, con
     const float inv_sqrt = (float)(1.0 / sqrt((double)dh));
     const double2* rt = reinterpret_cast<const double2*>(rope);
     int rc = -1;
-#define QT_AD(D, GG)                                                                                           \
-    if (dh == D && G == GG)                                                                                    \
-        rc = launch_dec<D, GG>(grid, pps, st, qkv, ldq, H, Hkv, kv_len, pool, page_bytes, pt, max_pages, rt, pos, \
-                               inv_sqrt, part_ml, part_o);
+#define QT_AD(D, GG) \
+    if (dh == D && G == GG) rc = launch_any<D, GG>(grid, pps, st, qkv, ldq, H, Hkv, kv_len, pool, page_bytes, pt, max_pages, rt, pos, inv_sqrt, part_ml, part_o);
     QT_AD(128, 1) QT_AD(128, 2) QT_AD(128, 4) QT_AD(128, 7) QT_AD(128, 8)
     QT_AD(64, 1) QT_AD(64, 2) QT_AD(64, 4) QT_AD(64, 7) QT_AD(64, 8)
 #undef QT_AD

@@ -87,7 +87,7 @@ int qt_launch_attn_colsum(const float* qkv, int ldq, int H, int Hkv, int dh, con
 // token's K/V quantize + append at row kv_len[b] fused in, attention over kv_len[b] + 1
 // rows; null: q post-RoPE, kv_len[b] rows.  Then the split merge (fixed order) writing the
 // fp32 rows to out (nullable) and/or the attn_out site codes (codes non-null).
-int qt_attn_decode_plan(int B, int Hkv, int pages, int sms, int* pps, int* nsplit);
+int qt_attn_decode_plan(int B, int H, int Hkv, int pages, int sms, int* pps, int* nsplit);
 int qt_launch_attn_decode(const float* qkv, int ldq, int H, int Hkv, int dh, const int* kv_len, int B,
                           uint8_t* pool, long long page_bytes, const int* pt, int max_pages, int pps, int nsplit,
                           const double* rope, const int* pos, float* part_ml, float* part_o, float* out, int ldo,
