@@ -370,12 +370,15 @@ QT_DEV uint32_t ta_sw(int r, int c) { return (uint32_t)(r * 128 + ((c ^ (r & 7))
 //   warps 0-3  softmax: thread i owns query row i = TMEM lane i (tcgen05.ld of S, the
 //              reference mask, online softmax in log2 units with a lazy max, P = p * s_v
 //              split hi + lo fp16 into the UMMA A tile, O rescale when the max rises by > 8)
-//   warps 4-7  producer: the int4 K / V codes of the next tiles by cp.async, dequantised to
-//              fp16 (exact) into double-buffered K [key][dh] and V^T [dh][key] UMMA tiles
+//   warps 4-7  producer: the int4 K / V codes of the next tiles by cp.async into a 3-deep raw
+//              ring, dequantised to fp16 (exact) into double-buffered K [key][dh] and V^T
+//              [dh][key] UMMA tiles -- K one tile ahead of V: K(t) then V(t - 1)
 //   warp 8     TMEM owner + MMA issuer: S(t) = Q K^T (Q hi + lo) into a double-buffered S,
 //              then O += P(t-1) V(t-1) -- tile t's S product runs while tile t-1's softmax does
-// mbarriers: kv_full / kv_empty (producer <-> MMA), s_full (MMA -> softmax), p_full (softmax ->
-// MMA), pv_done (MMA -> softmax: P buffer free, O updated).
+// mbarriers: k_full / k_empty and v_full / v_empty (producer <-> MMA; a K buffer is free once
+// its S product is done, a V buffer once its P.V is -- so the next K tile never waits for a
+// P.V), ks_full (producer -> softmax: the tile's K / V scales, a 4-deep ring), s_full (MMA ->
+// softmax), p_full (softmax -> MMA), pv_done (MMA -> softmax: P buffer free, O updated).
 constexpr int TW_Q = 128, TW_K = 64;
 constexpr int TW_SW = 8, TW_PW = 4;                // softmax warps (2 threads per query row), producer warps
 constexpr int TW_MW = TW_SW + TW_PW;              // the MMA warp
@@ -387,12 +390,12 @@ struct TwSmem {
     static constexpr size_t vt = kt + 2 * 16384;    // [2 bufs][128 dh][128 B]
     static constexpr size_t ph = vt + 2 * 16384;    // [2 bufs][128 q][128 B]
     static constexpr size_t pl = ph + 2 * 16384;
-    static constexpr size_t raw = pl + 2 * 16384;   // [2] x (K codes 4 KB, V codes 4 KB, scales 512 B)
+    static constexpr size_t raw = pl + 2 * 16384;   // [3] x (K codes 4 KB, V codes 4 KB, scales 512 B)
     static constexpr size_t raw_sz = 2 * 4096 + 512;
-    static constexpr size_t kvs = raw + 2 * raw_sz; // [2 bufs] ks[64], then [2 bufs] vs[64]
-    static constexpr size_t xch = kvs + 1024;       // [2 tiles][2 halves][128] tile max, then [2][128] l, [2][128] max |o|
+    static constexpr size_t kvs = raw + 3 * raw_sz; // [4 tiles] ks[64], then [4 tiles] vs[64]
+    static constexpr size_t xch = kvs + 2048;       // [2 tiles][2 halves][128] tile max, then [2][128] l, [2][128] max |o|
     static constexpr size_t bars = xch + 4096;
-    static constexpr size_t total = bars + 128;
+    static constexpr size_t total = bars + 256;
 };
 
 template <int DH>
@@ -436,32 +439,44 @@ __global__ void __launch_bounds__(TW_THREADS, 1) k_attn_prefill_ws(const float* 
     const int tok0 = seq_off[b];
     const int kend = max(V, min(S, q0 + TW_Q));
     const int T = (kend + TW_K - 1) / TW_K;
-    uint64_t* kv_full = reinterpret_cast<uint64_t*>(sm + TwSmem::bars);
-    uint64_t* kv_empty = kv_full + 2;
-    uint64_t* s_full = kv_empty + 2;
+    uint64_t* k_full = reinterpret_cast<uint64_t*>(sm + TwSmem::bars);
+    uint64_t* k_empty = k_full + 2;
+    uint64_t* v_full = k_empty + 2;
+    uint64_t* v_empty = v_full + 2;
+    uint64_t* s_full = v_empty + 2;
     uint64_t* p_full = s_full + 2;
     uint64_t* pv_done = p_full + 2;
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(pv_done + 2);
-    float* ksb = reinterpret_cast<float*>(sm + TwSmem::kvs);  // [2][64] K scales, then [2][64] V scales
-    float* vsb = ksb + 2 * TW_K;
+    uint64_t* ks_full = pv_done + 2;  // [4]
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(ks_full + 4);
+    float* ksb = reinterpret_cast<float*>(sm + TwSmem::kvs);  // [4][64] K scales, then [4][64] V scales
+    float* vsb = ksb + 4 * TW_K;
 
     if (tid == 0) {
         for (int i = 0; i < 2; ++i) {
-            mbar_init(&kv_full[i], TW_PW * 32);
-            mbar_init(&kv_empty[i], 1);
+            mbar_init(&k_full[i], TW_PW * 32);
+            mbar_init(&k_empty[i], 1);
+            mbar_init(&v_full[i], TW_PW * 32);
+            mbar_init(&v_empty[i], 1);
             mbar_init(&s_full[i], 1);
             mbar_init(&p_full[i], TW_SW * 32);
             mbar_init(&pv_done[i], 1);
         }
+        for (int i = 0; i < 4; ++i) mbar_init(&ks_full[i], TW_PW * 32);
         mbar_fence_init();
     }
     if (warp == TW_MW) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;\n" ::"r"(smem_u32(tslot)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
     }
-    if (warp >= TW_SW && warp < TW_MW)  // the first tile's codes in flight while Q is staged
-        tw_load_raw<DH>(page_base(pool, page_bytes, pt, max_pages, b, 0), Hkv, kh, min(TW_K, S),
-                        sm + TwSmem::raw, tid - TW_SW * 32, TW_PW * 32);
+    if (warp >= TW_SW && warp < TW_MW)  // the first three tiles' codes in flight while Q is staged
+        for (int j = 0; j < 3; ++j) {
+            if (j < T)
+                tw_load_raw<DH>(page_base(pool, page_bytes, pt, max_pages, b, j * TW_K), Hkv, kh,
+                                min(TW_K, S - j * TW_K), sm + TwSmem::raw + (size_t)j * TwSmem::raw_sz,
+                                tid - TW_SW * 32, TW_PW * 32);
+            else
+                cp_async_commit();  // (empty group: the wait counts below stay regular)
+        }
     if (warp < 4) {  // Q row -> hi / lo fp16 (rows past S are zero)
         const int q = q0 + tid;
         const float* qr = qkv + (size_t)(tok0 + min(q, S - 1)) * ldq + h * DH;
@@ -494,7 +509,7 @@ __global__ void __launch_bounds__(TW_THREADS, 1) k_attn_prefill_ws(const float* 
             for (int t = 0; t <= T; ++t) {
                 if (t < T) {  // S(t) = Qhi K^T + Qlo K^T into S[t & 1]
                     const int bf = t & 1;
-                    mbar_wait(&kv_full[bf], (uint32_t)(t >> 1) & 1u);
+                    mbar_wait(&k_full[bf], (uint32_t)(t >> 1) & 1u);
                     ta_fence_after();
                     const uint32_t kt = smem_u32(sm + TwSmem::kt + (size_t)bf * 16384);
                     const uint32_t tS = tmem + (uint32_t)(bf * 64);
@@ -507,9 +522,11 @@ __global__ void __launch_bounds__(TW_THREADS, 1) k_attn_prefill_ws(const float* 
                         ta_mma(tS, ta_desc(ql + (k >> 2) * 16384 + (k & 3) * 32),
                                ta_desc(kt + (k >> 2) * 8192 + (k & 3) * 32), ta_idesc(TW_K), 1);
                     ta_commit(&s_full[bf]);
+                    ta_commit(&k_empty[bf]);
                 }
                 if (t >= 1) {  // O += Phi V + Plo V of tile t - 1
                     const int u = t - 1, c = u & 1;
+                    mbar_wait(&v_full[c], (uint32_t)(u >> 1) & 1u);
                     mbar_wait(&p_full[c], (uint32_t)(u >> 1) & 1u);
                     ta_fence_after();
                     const uint32_t ph = smem_u32(sm + TwSmem::ph + (size_t)c * 16384);
@@ -522,59 +539,74 @@ __global__ void __launch_bounds__(TW_THREADS, 1) k_attn_prefill_ws(const float* 
                     for (int k = 0; k < TW_K / 16; ++k)
                         ta_mma(tO, ta_desc(pl + k * 32), ta_desc(vt + k * 32), ta_idesc(DH), 1);
                     ta_commit(&pv_done[c]);
-                    ta_commit(&kv_empty[c]);
+                    ta_commit(&v_empty[c]);
                 }
             }
         }
         __syncwarp();
     } else if (warp >= TW_SW) {
-        // ---------------- producer
+        // ---------------- producer: K(t) then V(t - 1) per step
         const int p = tid - TW_SW * 32;
-        for (int t = 0; t < T; ++t) {
-            const int bf = t & 1;
-            const int k0 = t * TW_K;
-            const int nk = min(TW_K, S - k0);
-            cp_async_wait<0>();
-            asm volatile("bar.sync 1, %0;\n" ::"n"(TW_PW * 32) : "memory");  // raw(t) landed; dequant(t-1) done
-            if (t + 1 < T)
-                tw_load_raw<DH>(page_base(pool, page_bytes, pt, max_pages, b, k0 + TW_K), Hkv, kh,
-                                min(TW_K, S - k0 - TW_K), sm + TwSmem::raw + (size_t)((t + 1) & 1) * TwSmem::raw_sz,
-                                p, 128);
-            if (t >= 2) mbar_wait(&kv_empty[bf], (uint32_t)((t - 2) >> 1) & 1u);
-            const uint8_t* raw = sm + TwSmem::raw + (size_t)bf * TwSmem::raw_sz;
-            const uint32_t* kw = reinterpret_cast<const uint32_t*>(raw);
-            const uint32_t* vw = reinterpret_cast<const uint32_t*>(raw + 4096);
-            uint8_t* ktb = sm + TwSmem::kt + (size_t)bf * 16384;
-            uint8_t* vtb = sm + TwSmem::vt + (size_t)bf * 16384;
+        for (int it = 0; it <= T; ++it) {
+            if (it < T) {  // K(it): raw(it) has landed (groups raw(0 .. it + 1) issued so far)
+                const int j = it, bf = j & 1;
+                if (j == 0) cp_async_wait<2>();
+                else cp_async_wait<1>();
+                asm volatile("bar.sync 1, %0;\n" ::"n"(TW_PW * 32) : "memory");
+                if (j >= 2) mbar_wait(&k_empty[bf], (uint32_t)((j - 2) >> 1) & 1u);
+                const uint8_t* raw = sm + TwSmem::raw + (size_t)(j % 3) * TwSmem::raw_sz;
+                const uint32_t* kw = reinterpret_cast<const uint32_t*>(raw);
+                uint8_t* ktb = sm + TwSmem::kt + (size_t)bf * 16384;
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const int wi = p + 128 * i;  // K: word (key, w) in row order
-                const int key = wi >> 4, w = wi & 15;
-                uint32_t hp[4];
-                word_to_h2_pairs(kw[wi], hp);
-                *reinterpret_cast<uint4*>(ktb + (size_t)(w >> 3) * 8192 + ta_sw(key, w & 7)) =
-                    *reinterpret_cast<const uint4*>(hp);
-            }
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const int key = p & 63, w = (p >> 6) + 2 * i;  // V: a warp covers 32 keys of one word
-                uint32_t hp[4];
-                word_to_h2_pairs(vw[key * 16 + w], hp);
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const int c = 8 * w + 2 * j;
-                    uint8_t* base = vtb + (key & 7) * 2;
-                    *reinterpret_cast<uint16_t*>(base + ta_sw(c, key >> 3)) = (uint16_t)(hp[j] & 0xFFFF);
-                    *reinterpret_cast<uint16_t*>(base + ta_sw(c + 1, key >> 3)) = (uint16_t)(hp[j] >> 16);
+                for (int i = 0; i < 8; ++i) {
+                    const int wi = p + 128 * i;  // K: word (key, w) in row order
+                    const int key = wi >> 4, w = wi & 15;
+                    uint32_t hp[4];
+                    word_to_h2_pairs(kw[wi], hp);
+                    *reinterpret_cast<uint4*>(ktb + (size_t)(w >> 3) * 8192 + ta_sw(key, w & 7)) =
+                        *reinterpret_cast<const uint4*>(hp);
                 }
+                if (p < TW_K) {  // the tile's scales, a 4-deep ring (overwritten at K(j + 4), after S(j + 2),
+                                 // so after softmax(j))
+                    const int nk = min(TW_K, S - j * TW_K);
+                    const float* sc = reinterpret_cast<const float*>(raw + 8192);
+                    ksb[(j & 3) * TW_K + p] = p < nk ? sc[p] * (inv_sqrt * 1.4426950408889634f) : 0.f;  // s_k / sqrt(dh) * log2 e
+                    vsb[(j & 3) * TW_K + p] = p < nk ? sc[TW_K + p] : 0.f;
+                }
+                ta_fence_async();
+                mbar_arrive(&k_full[bf]);
+                mbar_arrive(&ks_full[j & 3]);
             }
-            if (p < TW_K) {
-                const float* sc = reinterpret_cast<const float*>(raw + 8192);
-                ksb[bf * TW_K + p] = p < nk ? sc[p] * (inv_sqrt * 1.4426950408889634f) : 0.f;  // s_k / sqrt(dh) * log2 e
-                vsb[bf * TW_K + p] = p < nk ? sc[TW_K + p] : 0.f;
+            if (it >= 1) {  // V(it - 1)
+                const int j = it - 1, bf = j & 1;
+                if (j >= 2) mbar_wait(&v_empty[bf], (uint32_t)((j - 2) >> 1) & 1u);
+                const uint8_t* raw = sm + TwSmem::raw + (size_t)(j % 3) * TwSmem::raw_sz;
+                const uint32_t* vw = reinterpret_cast<const uint32_t*>(raw + 4096);
+                uint8_t* vtb = sm + TwSmem::vt + (size_t)bf * 16384;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int key = p & 63, w = (p >> 6) + 2 * i;  // V: a warp covers 32 keys of one word
+                    uint32_t hp[4];
+                    word_to_h2_pairs(vw[key * 16 + w], hp);
+#pragma unroll
+                    for (int jj = 0; jj < 4; ++jj) {
+                        const int c = 8 * w + 2 * jj;
+                        uint8_t* base = vtb + (key & 7) * 2;
+                        *reinterpret_cast<uint16_t*>(base + ta_sw(c, key >> 3)) = (uint16_t)(hp[jj] & 0xFFFF);
+                        *reinterpret_cast<uint16_t*>(base + ta_sw(c + 1, key >> 3)) = (uint16_t)(hp[jj] >> 16);
+                    }
+                }
+                ta_fence_async();
+                mbar_arrive(&v_full[bf]);
+                // raw(j) fully read by every producer thread: its slot takes raw(j + 3)
+                asm volatile("bar.sync 1, %0;\n" ::"n"(TW_PW * 32) : "memory");
+                if (j + 3 < T)
+                    tw_load_raw<DH>(page_base(pool, page_bytes, pt, max_pages, b, (j + 3) * TW_K), Hkv, kh,
+                                    min(TW_K, S - (j + 3) * TW_K), sm + TwSmem::raw + (size_t)(j % 3) * TwSmem::raw_sz,
+                                    p, 128);
+                else
+                    cp_async_commit();
             }
-            ta_fence_async();
-            mbar_arrive(&kv_full[bf]);
         }
     } else {
         // ---------------- softmax: query row r = TMEM lane r (warps w and w + 4 share lane quarter
@@ -590,12 +622,12 @@ __global__ void __launch_bounds__(TW_THREADS, 1) k_attn_prefill_ws(const float* 
             const uint32_t ph = (uint32_t)(t >> 1) & 1u;
             const int k0 = t * TW_K + hf * HK;
             mbar_wait(&s_full[bf], ph);
-            mbar_wait(&kv_full[bf], ph);  // this tile's scales
+            mbar_wait(&ks_full[t & 3], (uint32_t)(t >> 2) & 1u);  // this tile's scales
             ta_fence_after();
             float s[HK];
             ta_ld32(tmem + (uint32_t)(bf * 64 + hf * HK) + lane_off, s);
-            const float* ks = ksb + bf * TW_K + hf * HK;
-            const float* vs = vsb + bf * TW_K + hf * HK;
+            const float* ks = ksb + (t & 3) * TW_K + hf * HK;
+            const float* vs = vsb + (t & 3) * TW_K + hf * HK;
             // every (query, key) pair of the tile allowed and in range: no per-element mask
             const int klast = t * TW_K + TW_K - 1, qlast = q0 + TW_Q - 1;
             const bool full = qlast < S && klast < S &&
