@@ -130,6 +130,7 @@ __global__ void __launch_bounds__(AD_THREADS) k_attn_dec(const float* __restrict
         }
     }
     pdl_wait();  // q (and the new token's k / v) come from the upstream GEMV
+    qkv = pdl_fresh(qkv);
 
     // q of the G heads -> smem (RoPE'd here in the decode step: fp64, rounded to fp32 like
     // the prefill's k_rope_kv_append)
@@ -307,29 +308,37 @@ __global__ void __launch_bounds__(AD_THREADS) k_attn_dec(const float* __restrict
 
 // ---------------------------------------------------------------- K6 on integer tensor cores
 // One WARP per (page, kv head, sequence), serving the G query heads of its kv head; a CTA is
-// up to 4 warps (4 kv heads of the same page) with no block barrier.  The page's K / V code
-// blocks and scales arrive by cp.async.bulk into the warp's own smem slice.
+// up to 4 warps (4 kv heads of the same page) with no block barrier.  The page's V code block
+// and scales arrive by cp.async.bulk into the warp's own smem slice; its K codes go straight
+// into the MMA lanes' registers (each warp load instruction covers 8 whole 64 B rows).  Both
+// are issued before the programmatic-dependency wait.
 //
 // Both products run as exact integer MMAs (mma.sync m16n8k32 s8.s8.s32) on the codes as
 // stored: the fp32 operand (q, then p * s_v) is written as a fixed-point integer Q =
 // rint(x * 2^F) (|Q| < 2^30, F from the head's max |x|) in four balanced base-256 digits, one
-// MMA column per digit: S = sum_d Q_d * c_d is exact in int32 per digit and recombined exactly
-// in fp64, so a score's only roundings are the fixed-point step (2^-31 of the head's max |q|)
-// and one fp32 rounding -- tighter than the fp32 dot product of k_attn_dec.
+// MMA column per digit: S = sum_d Q_d * c_d is exact in int32 per digit, and a score's only
+// roundings are the fixed-point step (2^-31 of the head's max |q|) and the final fp32 one --
+// tighter than the fp32 dot product of k_attn_dec.
 //   QK: A = K codes (16 keys x 32 dims, 16 * code in s8 as unpack_x16 gives), B = q digits.
 //   PV: A = V^T (16 channels x 32 keys), built by a 4 x 4 byte transpose of 4 keys' code
 //       words (PRMT) then unpack_x16; B = (p * s_v) digits.
 // Balanced digits of Q: U = Q + 0x80808080 has bytes d_j + 128, so (U ^ 0x80808080) holds
-// the four signed digits d_j directly.
+// the four signed digits d_j directly.  The exact integer digit-pair sums are recombined and
+// rounded once in fp32 (hi * 2^16 + lo by one FMA).
 constexpr int AW_MAXW = 4;  // warps (kv heads) per CTA
+// Two register budgets (A/B at C2 / C5 B = 64 / C5 B = 256, decode attention chain ms per
+// step): 96 registers, 5 CTAs per SM by shared memory -- 0.361 / 0.859 / 2.797; capped at 80
+// for 6 CTAs per SM -- 0.387 / 0.842 / 2.537 (7: 0.412 / 0.873 / 2.535).  Latency decides a
+// grid of less than one full wave, residency a larger one.
+constexpr int AW_MINB_WIDE = 6;
 // query heads per kv head served by k_attn_dec_w: its one warp runs every head's softmax and
 // (G + 1) / 2 MMA column tiles serially, which at G = 7 (C4) measured slower than k_attn_dec
 // (decode attention chain 0.613 vs 0.487 ms/step; MHA at C5 B = 256: 2.64 vs 5.32 ms)
 constexpr int AW_MAX_G = 2;
 template <int DH, int G>
-struct AwSmem {  // one warp's slice
+struct AwSmem {  // one warp's slice (the K codes go straight to registers)
     static constexpr int CB = kPage * (DH / 2);
-    static constexpr size_t kc = 0, vc = CB, ks = 2 * CB, vs = ks + kPage * 4;
+    static constexpr size_t vc = 0, ks = CB, vs = ks + kPage * 4;
     static constexpr size_t sc = vs + kPage * 4;        // [G][64] scores
     static constexpr size_t ql = sc + G * kPage * 4;     // [G][4 digits][DH] q digits, MMA-B order
     static constexpr size_t wl = ql + G * 4 * DH;        // [G][4 digits][64] (p * s_v) digits
@@ -346,20 +355,25 @@ QT_DEV uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
 QT_DEV int aw_qpos(int d) { return (d & ~7) | ((d & 1) << 2) | ((d >> 1) & 3); }
 // position of key k = 32 s + 16 h + t + 4 i in a digit row: 32 s + 16 h + 4 t + i
 QT_DEV int aw_kpos(int k) { return (k & 48) | ((k & 3) << 2) | ((k >> 2) & 3); }
-// fixed-point exponent: |x| * 2^F < 2^30 for every |x| <= mx
+// fixed-point exponent: |x| * 2^F < 2^30 for every |x| <= mx (F <= 100: 2^F and the
+// recombination factor 2^-(F + 4) stay normal fp32 numbers)
 QT_DEV int aw_fexp(float mx) {
     if (!(mx > 0.f)) return 0;
     int e;
     frexpf(mx, &e);
-    return 30 - e;
+    return min(30 - e, 100);
 }
-QT_DEV uint32_t aw_digits(float x, int F) {  // the four signed digits of rint(x * 2^F)
-    const int Q = __double2int_rn((double)x * ldexp(1.0, F));
+QT_DEV float aw_pow2(int e) { return __int_as_float((127 + e) << 23); }  // 2^e, -126 <= e <= 127
+// the four signed digits of rint(x * 2^F) (x * 2^F is exact: a power-of-two scaling)
+QT_DEV uint32_t aw_digits(float x, float two_f) {
+    const int Q = __float2int_rn(x * two_f);
     return ((uint32_t)Q + 0x80808080u) ^ 0x80808080u;
 }
+// hi * 2^16 + lo (the digit pairs' partial sums, exact ints) rounded once to fp32, scaled
+QT_DEV float aw_comb(int lo, int hi, float scale) { return fmaf((float)hi, 65536.f, (float)lo) * scale; }
 
-template <int DH, int G>
-__global__ void __launch_bounds__(AW_MAXW * 32) k_attn_dec_w(const float* __restrict__ qkv, int ldq, int H, int Hkv,
+template <int DH, int G, int MINB>
+__global__ void __launch_bounds__(AW_MAXW * 32, MINB) k_attn_dec_w(const float* __restrict__ qkv, int ldq, int H, int Hkv,
                                                              const int* __restrict__ kv_len, uint8_t* __restrict__ pool,
                                                              long long page_bytes, const int* __restrict__ pt,
                                                              int max_pages, const double2* __restrict__ rope,
@@ -399,7 +413,6 @@ __global__ void __launch_bounds__(AW_MAXW * 32) k_attn_dec_w(const float* __rest
         }
         return;
     }
-    uint8_t* kc = sm + S::kc;
     uint8_t* vc = sm + S::vc;
     float* ksc = reinterpret_cast<float*>(sm + S::ks);
     float* vsc = reinterpret_cast<float*>(sm + S::vs);
@@ -408,17 +421,35 @@ __global__ void __launch_bounds__(AW_MAXW * 32) k_attn_dec_w(const float* __rest
     uint8_t* wl = sm + S::wl;
     uint64_t* bar = reinterpret_cast<uint64_t*>(sm + S::bar);
     const size_t cbh = (size_t)Hkv * CB;
+    const uint8_t* page_c = pool + (long long)pt[b * max_pages + p] * page_bytes;
     if (lane == 0) {
         mbar_init(bar, 1);
         mbar_fence_init();
-        mbar_arrive_expect_tx(bar, (uint32_t)(2 * CB + 2 * kPage * 4));
-        const uint8_t* page = pool + (long long)pt[b * max_pages + p] * page_bytes;
-        bulk_g2s(kc, page + (size_t)kh * CB, CB, bar);
+        mbar_arrive_expect_tx(bar, (uint32_t)(CB + 2 * kPage * 4));
+        const uint8_t* page = page_c;
         bulk_g2s(vc, page + cbh + (size_t)kh * CB, CB, bar);
         bulk_g2s(ksc, page + 2 * cbh + (size_t)kh * kPage * 4, kPage * 4, bar);
         bulk_g2s(vsc, page + 2 * cbh + ((size_t)Hkv + kh) * kPage * 4, kPage * 4, bar);
     }
+    // the lane's K code words (keys 16 mt + g (+ 8), words KS * t ..), straight from the cache:
+    // one warp instruction reads 8 whole 64 B rows
+    uint32_t kw[4][2][KS];
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+            const uint8_t* src = page_c + (size_t)kh * CB + (size_t)(16 * mt + g + 8 * hf) * (DH / 2) + t * KS * 4;
+            // (ld.global.cg: the rows are read once, no L1 allocation)
+            if constexpr (KS == 4) {
+                const uint4 w4 = __ldcg(reinterpret_cast<const uint4*>(src));
+                kw[mt][hf][0] = w4.x; kw[mt][hf][1] = w4.y; kw[mt][hf][2] = w4.z; kw[mt][hf][3] = w4.w;
+            } else {
+                const uint2 w2 = __ldcg(reinterpret_cast<const uint2*>(src));
+                kw[mt][hf][0] = w2.x; kw[mt][hf][1] = w2.y;
+            }
+        }
     pdl_wait();  // q (and the new token's k / v) come from the upstream GEMV
+    qkv = pdl_fresh(qkv);
 
     // q of the G heads (RoPE'd here in the decode step: fp64, rounded to fp32 like the
     // prefill's k_rope_kv_append) -> fixed-point digits in MMA-B order
@@ -443,10 +474,11 @@ __global__ void __launch_bounds__(AW_MAXW * 32) k_attn_dec_w(const float* __rest
             mx = fmaxf(mx, fmaxf(fabsf(v[j].x), fabsf(v[j].y)));
         }
         F[gh] = aw_fexp(warp_max(mx));
+        const float two_f = aw_pow2(F[gh]);
 #pragma unroll
         for (int j = 0; j < PPL; ++j) {
             const int d = 2 * (lane + 32 * j);
-            const uint32_t L0 = aw_digits(v[j].x, F[gh]), L1 = aw_digits(v[j].y, F[gh]);
+            const uint32_t L0 = aw_digits(v[j].x, two_f), L1 = aw_digits(v[j].y, two_f);
             uint8_t* row = ql + (size_t)gh * 4 * DH;
 #pragma unroll
             for (int dg = 0; dg < 4; ++dg) {
@@ -497,13 +529,28 @@ __global__ void __launch_bounds__(AW_MAXW * 32) k_attn_dec_w(const float* __rest
                     (float)s;
         }
     }
-    mbar_wait(bar, 0);  // the page has landed
-    if (has_new) {      // ... and the new row replaces its (stale) shared copy
+    if (has_new) {  // the new K row replaces its stale register copy: word w of the row is the
+                    // 8 / E lanes' pieces from lane w * 8 / E on
 #pragma unroll
-        for (int kv = 0; kv < 2; ++kv) {
-            uint8_t* d = (kv == 0 ? kc : vc) + (size_t)new_r * (DH / 2) + lane * E / 2;
-            if (E == 4) *reinterpret_cast<uint16_t*>(d) = (uint16_t)new_word[kv];
-            else *d = (uint8_t)new_word[kv];
+        for (int s2 = 0; s2 < KS; ++s2) {
+            const int w = KS * t + s2;
+            uint32_t word = 0;
+#pragma unroll
+            for (int q = 0; q < 8 / E; ++q)
+                word |= (__shfl_sync(0xffffffffu, new_word[0], w * (8 / E) + q) & ((1u << (4 * E)) - 1u)) << (4 * E * q);
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+                for (int hf = 0; hf < 2; ++hf)
+                    if (new_r == 16 * mt + 8 * hf + g) kw[mt][hf][s2] = word;
+        }
+    }
+    mbar_wait(bar, 0);  // the page's V codes and scales have landed
+    if (has_new) {      // ... and the new row replaces its (stale) shared copy
+        {
+            uint8_t* d = vc + (size_t)new_r * (DH / 2) + lane * E / 2;
+            if (E == 4) *reinterpret_cast<uint16_t*>(d) = (uint16_t)new_word[1];
+            else *d = (uint8_t)new_word[1];
         }
         if (lane == 0) {
             ksc[new_r] = new_scale[0];
@@ -514,20 +561,6 @@ __global__ void __launch_bounds__(AW_MAXW * 32) k_attn_dec_w(const float* __rest
 
     // ---- scores: S[key][head] for the 64 keys (4 m-tiles of 16 keys)
     {
-        uint32_t kw[4][2][KS];  // lane's code words: keys 16 mt + g (+ 8), words KS * t ..
-#pragma unroll
-        for (int mt = 0; mt < 4; ++mt)
-#pragma unroll
-            for (int hf = 0; hf < 2; ++hf) {
-                const uint8_t* src = kc + (size_t)(16 * mt + g + 8 * hf) * (DH / 2) + t * KS * 4;
-                if constexpr (KS == 4) {
-                    const uint4 w4 = *reinterpret_cast<const uint4*>(src);
-                    kw[mt][hf][0] = w4.x; kw[mt][hf][1] = w4.y; kw[mt][hf][2] = w4.z; kw[mt][hf][3] = w4.w;
-                } else {
-                    const uint2 w2 = *reinterpret_cast<const uint2*>(src);
-                    kw[mt][hf][0] = w2.x; kw[mt][hf][1] = w2.y;
-                }
-            }
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
             const int hq = 2 * nt + (g >> 2);  // the B column's head and digit
@@ -542,7 +575,7 @@ __global__ void __launch_bounds__(AW_MAXW * 32) k_attn_dec_w(const float* __rest
             }
             const int ho = 2 * nt + (t >> 1);  // the accumulator columns' head
             const int Fo = (2 * nt + 1 < G && (t >> 1)) ? F[(2 * nt + 1) % G] : F[2 * nt];
-            const double qsc = ldexp(1.0, -(Fo + 4)) * (double)inv_sqrt;
+            const float qsc = aw_pow2(-(Fo + 4)) * inv_sqrt;
 #pragma unroll
             for (int mt = 0; mt < 4; ++mt) {
                 int acc[4] = {0, 0, 0, 0};
@@ -557,18 +590,15 @@ __global__ void __launch_bounds__(AW_MAXW * 32) k_attn_dec_w(const float* __rest
                 const int U0 = __shfl_xor_sync(0xffffffffu, P0, 1), U1 = __shfl_xor_sync(0xffffffffu, P1, 1);
                 if (!(t & 1) && ho < G) {
                     const int k0 = 16 * mt + g;
-                    sc[ho * kPage + k0] =
-                        (float)(((double)P0 + (double)U0 * 65536.0) * qsc) * ksc[k0];
-                    sc[ho * kPage + k0 + 8] =
-                        (float)(((double)P1 + (double)U1 * 65536.0) * qsc) * ksc[k0 + 8];
+                    sc[ho * kPage + k0] = aw_comb(P0, U0, qsc) * ksc[k0];
+                    sc[ho * kPage + k0 + 8] = aw_comb(P1, U1, qsc) * ksc[k0 + 8];
                 }
             }
         }
     }
     __syncwarp();
     // ---- softmax per head over the page's rows; p * s_v -> fixed-point digits
-    float m_h[G], l_h[G];
-    double osc[G];
+    float m_h[G], l_h[G], osc[G];
 #pragma unroll
     for (int gh = 0; gh < G; ++gh) {
         const bool ok0 = lane < n_rows, ok1 = lane + 32 < n_rows;
@@ -579,8 +609,9 @@ __global__ void __launch_bounds__(AW_MAXW * 32) k_attn_dec_w(const float* __rest
         m_h[gh] = m;
         l_h[gh] = warp_sum(p0 + p1);
         const int Fw = aw_fexp(warp_max(fmaxf(w0, w1)));
-        osc[gh] = ldexp(1.0, -(Fw + 4));
-        const uint32_t L0 = aw_digits(w0, Fw), L1 = aw_digits(w1, Fw);
+        osc[gh] = aw_pow2(-(Fw + 4));
+        const float two_w = aw_pow2(Fw);
+        const uint32_t L0 = aw_digits(w0, two_w), L1 = aw_digits(w1, two_w);
         uint8_t* row = wl + (size_t)gh * 4 * kPage;
 #pragma unroll
         for (int dg = 0; dg < 4; ++dg) {
@@ -641,14 +672,14 @@ __global__ void __launch_bounds__(AW_MAXW * 32) k_attn_dec_w(const float* __rest
             }
         }
         const int ho = 2 * nt + (t >> 1);
-        const double oscale = (2 * nt + 1 < G && (t >> 1)) ? osc[(2 * nt + 1) % G] : osc[2 * nt];
+        const float oscale = (2 * nt + 1 < G && (t >> 1)) ? osc[(2 * nt + 1) % G] : osc[2 * nt];
         float o[2][MT];
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
             const int P0 = acc[mt][0] + (acc[mt][1] << 8), P1 = acc[mt][2] + (acc[mt][3] << 8);
             const int U0 = __shfl_xor_sync(0xffffffffu, P0, 1), U1 = __shfl_xor_sync(0xffffffffu, P1, 1);
-            o[0][mt] = (float)(((double)P0 + (double)U0 * 65536.0) * oscale);
-            o[1][mt] = (float)(((double)P1 + (double)U1 * 65536.0) * oscale);
+            o[0][mt] = aw_comb(P0, U0, oscale);
+            o[1][mt] = aw_comb(P1, U1, oscale);
         }
         if (!(t & 1) && ho < G) {  // channels 8 WPG g .. 8 WPG g + 8 WPG - 1 (rows g, then g + 8)
             float* dst = part_o + (pidx0 + (size_t)ho * nsplit) * DH + 8 * WPG * g;
@@ -782,7 +813,11 @@ static int launch_dec_w(int nsplit, int Hkv, int B, cudaStream_t st, const float
                         const double2* rope, const int* pos, float inv_sqrt, float* part_ml, float* part_o) {
     const int wpc = std::min(AW_MAXW, Hkv);
     const size_t smem = (size_t)wpc * AwSmem<DH, G>::total;
-    auto kfn = k_attn_dec_w<DH, G>;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const long long ctas = (long long)nsplit * ((Hkv + wpc - 1) / wpc) * B;
+    auto kfn = ctas > (long long)5 * sms ? k_attn_dec_w<DH, G, AW_MINB_WIDE> : k_attn_dec_w<DH, G, 1>;
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     return launch_pdl(kfn, dim3(nsplit, (Hkv + wpc - 1) / wpc, B), dim3(32 * wpc), smem, st, qkv, ldq, H, Hkv,
                       kv_len, pool, page_bytes, pt, max_pages, rope, pos, inv_sqrt, part_ml, part_o);

@@ -296,6 +296,16 @@ QT_DEV float silu_f(float x) { return x / (1.0f + expf(-x)); }
 // and its writes are visible.  Every kernel calls pdl_wait() before touching
 // data produced upstream (and before exiting), so completion stays transitive.
 QT_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+// A pointer to upstream-produced data, opaque to the compiler from this point on.  Loads
+// through `const T* __restrict__` are invariant to the compiler, which may hoist them above
+// the (memory-clobbering) griddepcontrol.wait -- measured in k_attn_dec_w: the q loads moved
+// before the wait and read the upstream GEMV's output before it was written.  Passing the
+// pointer through an empty volatile asm after pdl_wait() pins those loads below the wait.
+template <typename T>
+QT_DEV T* pdl_fresh(T* p) {
+    asm volatile("" : "+l"(p));
+    return p;
+}
 QT_DEV void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
 
 }  // namespace qt
