@@ -139,7 +139,7 @@ def load_traffic():
             M, N, K = 8, 12288, 4096
             r["algorithmic_bytes"] = N * K / 2 + 8 * N + M * K / 2 + 8 * M + 4 * M * N
             out["gemv"] = r
-        elif "k_attn_dec" in k:  # decode attention (k_attn_dec; r01: k_attn_decode_pp2)
+        elif "k_attn_dec" in k:  # decode attention (k_attn_dec_w; earlier: k_attn_dec, k_attn_decode_pp2)
             out["attn_decode"] = dict(r, algorithmic_bytes=r["dram_bytes"])
     return out
 

@@ -6,21 +6,12 @@
 // quant.cpp:117-119), then per query head an unmasked max-subtracted softmax of
 // q . k^ / sqrt(d_head) over every cached row and out = sum_j p_j v^_j (model.cpp:515-535).
 //
-// Two kernels.  MHA and G = 2 (C1, C2, C3, C5): k_attn_dec_w below -- one warp per (page,
-// kv head, sequence), both products as exact integer MMAs on the stored codes.  GQA with
-// G >= 4 (C4): k_attn_dec --
-// one CTA per (page split, kv head, sequence) serves all
-// G = H / Hkv query heads of its kv head, so every cached K/V byte is read from HBM once
-// (GQA included).  The split's pages -- per (page, kv head) one contiguous 4 KB K block,
-// one V block and two 256 B scale vectors -- arrive by cp.async.bulk (TMA 1D) into shared
-// memory, all issued before the programmatic-dependency wait: the cache rows are final
-// since earlier steps, so the copies overlap the upstream QKV GEMV.  After the wait the
-// CTA whose split holds the new row RoPEs and quantizes that token's K / V (fp64, the
-// reference's arithmetic) and appends them to the cache and to its shared copy.  Scores
-// (4 lanes per row, fp32), a per-head softmax, then P . V (16 word columns x 16 row groups)
-// produce one (max, sum, unnormalised o) partial per (sequence, query head, split);
-// k_attn_merge_quant merges the splits in fixed order and quantizes the attn_out site.
-// int4 -> fp32 without I2F: float(0x4B000000 | (nib ^ 8)) - (2^23 + 8) is exact.
+// B200 layout of the work (k_attn_dec_w): one warp per (page, kv head, sequence) -- G <= 2:
+// a CTA holds up to 4 kv heads of one page; G > 2 (GQA, C4): a CTA is one kv head of one
+// page with one warp per pair of query heads, sharing the page's V copy -- so every cached
+// K / V byte is read from HBM once.  Each (sequence, query head, page) leaves one (max, sum,
+// unnormalised o) partial; k_attn_merge_quant merges the pages in fixed order and quantizes
+// the attn_out site.
 #include <algorithm>
 
 #include "qt_common.cuh"
@@ -28,297 +19,23 @@
 
 namespace qt {
 
-#ifndef QT_AD_CTA_MULT
-#define QT_AD_CTA_MULT 8  // decode attention CTAs per SM the split plan aims for (A/B: 2 / 4 / 8,
-                          // tools/gpu_attn_ab.sh -- C2 decode 1.719 / 1.652 / 1.647 ms per step)
-#endif
-constexpr int AD_THREADS = 256;
-constexpr int AD_MAX_PPS = 8;  // pages per split (smem: 8.5 KB each at d_head 128)
-#ifndef QT_AD_PLAN_PPS
-#define QT_AD_PLAN_PPS 2  // the split plan's page cap (A/B 8 / 2 / 1 pages: C5 B = 256 decode chain
-                          // 9.76 / 9.32 / 10.68 ms per step; C2, C4 equal within noise)
-#endif
-#ifndef QT_AD_WARP
-#define QT_AD_WARP 1  // 1: k_attn_dec_w (integer tensor cores, one warp per page); 0: k_attn_dec
-#endif
-constexpr int AD_MAX_G = 8;    // query heads per kv head (one softmax warp each)
-
-// 8 signed nibbles of w -> 8 exact floats
-QT_DEV void nib8_to_f32(uint32_t w, float* f) {
-    const uint32_t x = w ^ 0x88888888u;  // two's complement nibble -> offset-8 unsigned
-#pragma unroll
-    for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(0x4B000000u | ((x >> (4 * e)) & 0xFu)) - 8388616.0f;
-}
-
-template <int DH, int G>
-struct AdSmem {
-    static constexpr int CB = kPage * (DH / 2);  // code bytes per (page, kv head, K|V)
-    static constexpr int QLD = DH + 16;           // padded q row (the 4 quarter slices hit distinct banks)
-    QT_HD static size_t kc(int) { return 0; }
-    QT_HD static size_t vc(int pps) { return (size_t)pps * CB; }
-    QT_HD static size_t ks(int pps) { return (size_t)2 * pps * CB; }
-    QT_HD static size_t vs(int pps) { return ks(pps) + (size_t)pps * kPage * 4; }
-    QT_HD static size_t q(int pps) { return vs(pps) + (size_t)pps * kPage * 4; }
-    QT_HD static size_t sc(int pps) { return q(pps) + (size_t)G * QLD * 4; }
-    QT_HD static size_t red(int pps) { return sc(pps) + (size_t)G * pps * kPage * 4; }
-    QT_HD static size_t stat(int pps) { return red(pps) + (size_t)8 * G * DH * 4; }
-    QT_HD static size_t bar(int pps) { return (stat(pps) + G * 8 + 15) / 16 * 16; }
-    QT_HD static size_t total(int pps) { return bar(pps) + 16; }
-};
-
-// grid (splits, Hkv, B), 256 threads.  rope != null: the decode step (q / k / v raw GEMV
-// outputs in qkv, RoPE + append of the new row at kv_len[b], attention over kv_len[b] + 1
-// rows); rope == null: q post-RoPE, attention over kv_len[b] rows of an existing cache.
-template <int DH, int G>
-__global__ void __launch_bounds__(AD_THREADS) k_attn_dec(const float* __restrict__ qkv, int ldq, int H, int Hkv,
-                                                         const int* __restrict__ kv_len, uint8_t* __restrict__ pool,
-                                                         long long page_bytes, const int* __restrict__ pt,
-                                                         int max_pages, int pps, const double2* __restrict__ rope,
-                                                         const int* __restrict__ pos, float inv_sqrt,
-                                                         float* __restrict__ part_ml, float* __restrict__ part_o) {
-    using S = AdSmem<DH, G>;
-    constexpr int CB = S::CB, QLD = S::QLD;
-    constexpr int CPL = DH / 4;    // channels per lane in the score phase
-    constexpr int WC = DH / 8;     // 32-bit words (8 codes) per row
-    constexpr int NRG = AD_THREADS / WC;  // row groups in the PV phase
-    extern __shared__ __align__(128) uint8_t sm[];
-    uint8_t* kc = sm + S::kc(pps);
-    uint8_t* vc = sm + S::vc(pps);
-    float* ksc = reinterpret_cast<float*>(sm + S::ks(pps));
-    float* vsc = reinterpret_cast<float*>(sm + S::vs(pps));
-    float* qs = reinterpret_cast<float*>(sm + S::q(pps));
-    float* sc = reinterpret_cast<float*>(sm + S::sc(pps));
-    float* red = reinterpret_cast<float*>(sm + S::red(pps));
-    float* stat = reinterpret_cast<float*>(sm + S::stat(pps));
-    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + S::bar(pps));
-
-    pdl_launch_dependents();
-    const int split = blockIdx.x, nsplit = gridDim.x, kh = blockIdx.y, b = blockIdx.z;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const bool fused = rope != nullptr;
-    // kv_len and the page table are final since the previous step (or the host upload):
-    // read before the dependency wait, like the cached rows themselves
-    const int old_len = kv_len[b];
-    const int len = old_len + (fused ? 1 : 0);
-    const int r0 = split * pps * kPage;
-    const int n_rows = min(pps * kPage, len - r0);
-    const size_t pidx0 = ((size_t)b * H + (size_t)kh * G) * nsplit + split;
-    if (n_rows <= 0) {  // nothing cached in this split: an empty partial per head
-        pdl_wait();     // the partial buffers are still read by the previous layer's merge
-        for (int i = tid; i < G * DH; i += AD_THREADS) part_o[(pidx0 + (size_t)(i / DH) * nsplit) * DH + i % DH] = 0.f;
-        if (tid < G) {
-            part_ml[(pidx0 + (size_t)tid * nsplit) * 2] = -1e30f;
-            part_ml[(pidx0 + (size_t)tid * nsplit) * 2 + 1] = 0.f;
-        }
-        return;
-    }
-    const int npg = (n_rows + kPage - 1) / kPage;
-    const size_t cbh = (size_t)Hkv * CB;  // K codes of all kv heads in a page
-    if (tid == 0) {
-        mbar_init(bar, 1);
-        mbar_fence_init();
-    }
-    __syncthreads();
-    if (tid == 0) {
-        mbar_arrive_expect_tx(bar, (uint32_t)npg * (2 * CB + 2 * kPage * 4));
-        for (int p = 0; p < npg; ++p) {
-            const uint8_t* page = pool + (long long)pt[b * max_pages + split * pps + p] * page_bytes;
-            bulk_g2s(kc + (size_t)p * CB, page + (size_t)kh * CB, CB, bar);
-            bulk_g2s(vc + (size_t)p * CB, page + cbh + (size_t)kh * CB, CB, bar);
-            bulk_g2s(ksc + p * kPage, page + 2 * cbh + (size_t)kh * kPage * 4, kPage * 4, bar);
-            bulk_g2s(vsc + p * kPage, page + 2 * cbh + ((size_t)Hkv + kh) * kPage * 4, kPage * 4, bar);
-        }
-    }
-    pdl_wait();  // q (and the new token's k / v) come from the upstream GEMV
-    qkv = pdl_fresh(qkv);
-
-    // q of the G heads -> smem (RoPE'd here in the decode step: fp64, rounded to fp32 like
-    // the prefill's k_rope_kv_append)
-    const float* qrow = qkv + (size_t)b * ldq;
-    const double2* rt = fused ? rope + (size_t)pos[b] * (DH / 2) : nullptr;
-    for (int i = tid; i < G * DH / 2; i += AD_THREADS) {
-        const int g = i / (DH / 2), pr = i % (DH / 2);
-        const float2 v = *reinterpret_cast<const float2*>(qrow + (size_t)(kh * G + g) * DH + 2 * pr);
-        float2 o = v;
-        if (fused) {
-            const double2 cs = rt[pr];
-            const double a = v.x, bb = v.y;
-            o.x = (float)__dsub_rn(__dmul_rn(a, cs.x), __dmul_rn(bb, cs.y));
-            o.y = (float)__dadd_rn(__dmul_rn(a, cs.y), __dmul_rn(bb, cs.x));
-        }
-        const int c = 2 * pr;
-        float* dst = qs + g * QLD + (c / CPL) * (CPL + 4) + c % CPL;
-        dst[0] = o.x;
-        dst[1] = o.y;
-    }
-    // the new row (decode step): warp 0 its K (RoPE'd), warp 1 its V -- kv_quantize in fp64
-    const int new_r = old_len - r0;  // row within this split
-    const bool has_new = fused && new_r >= 0 && new_r < n_rows;
-    constexpr int E = DH / 32;
-    uint32_t new_word = 0;
-    float new_scale = 0.f;
-    if (has_new && warp < 2) {
-        const bool is_k = warp == 0;
-        const float* src = qrow + (is_k ? H * DH : (H + Hkv) * DH) + kh * DH + lane * E;
-        double val[E];
-#pragma unroll
-        for (int j = 0; j < E; ++j) val[j] = (double)src[j];
-        if (is_k) {
-#pragma unroll
-            for (int j = 0; j < E; j += 2) {
-                const double2 cs = rt[(lane * E + j) / 2];
-                const double a = val[j], bb = val[j + 1];
-                val[j] = __dsub_rn(__dmul_rn(a, cs.x), __dmul_rn(bb, cs.y));
-                val[j + 1] = __dadd_rn(__dmul_rn(a, cs.y), __dmul_rn(bb, cs.x));
-            }
-        }
-        double mx = 0.0;
-#pragma unroll
-        for (int j = 0; j < E; ++j) mx = fmax(mx, fabs(val[j]));
-        mx = warp_max(mx);
-        const double s = q_scale(mx, 7), inv_s = 1.0 / s;
-#pragma unroll
-        for (int j = 0; j < E; ++j) new_word |= (uint32_t)(q_code_r(val[j], s, inv_s, 7) & 0xF) << (4 * j);
-        new_scale = (float)s;
-        // append to the cache (model.cpp:499-501)
-        uint8_t* page = pool + (long long)pt[b * max_pages + old_len / kPage] * page_bytes;
-        const int slot = old_len % kPage;
-        uint8_t* dst = page + (is_k ? 0 : cbh) + (size_t)kh * CB + (size_t)slot * (DH / 2) + lane * E / 2;
-        if (E == 4) *reinterpret_cast<uint16_t*>(dst) = (uint16_t)new_word;
-        else *dst = (uint8_t)new_word;
-        if (lane == 0)
-            reinterpret_cast<float*>(page + 2 * cbh)[(is_k ? 0 : Hkv * kPage) + kh * kPage + slot] = new_scale;
-    }
-    mbar_wait(bar, 0);  // the split's pages have landed
-    if (has_new && warp < 2) {  // ... and the new row replaces its (stale) shared copy
-        uint8_t* d = (warp == 0 ? kc : vc) + (size_t)new_r * (DH / 2) + lane * E / 2;
-        if (E == 4) *reinterpret_cast<uint16_t*>(d) = (uint16_t)new_word;
-        else *d = (uint8_t)new_word;
-        if (lane == 0) (warp == 0 ? ksc : vsc)[new_r] = new_scale;
-    }
-    __syncthreads();
-
-    // scores: 4 lanes per row, CPL channels each; all G heads per converted row
-    {
-        const int q4 = lane & 3;
-        for (int r = warp * 8 + (lane >> 2); r < npg * kPage; r += 64) {
-            float kf[CPL];
-            const uint8_t* kr = kc + (size_t)r * (DH / 2) + q4 * (CPL / 2);
-            if constexpr (CPL == 32) {
-                const uint4 w = *reinterpret_cast<const uint4*>(kr);
-                nib8_to_f32(w.x, kf); nib8_to_f32(w.y, kf + 8); nib8_to_f32(w.z, kf + 16); nib8_to_f32(w.w, kf + 24);
-            } else {
-                const uint2 w = *reinterpret_cast<const uint2*>(kr);
-                nib8_to_f32(w.x, kf); nib8_to_f32(w.y, kf + 8);
-            }
-            float d[G];
-#pragma unroll
-            for (int g = 0; g < G; ++g) {
-                const float4* qv = reinterpret_cast<const float4*>(qs + g * QLD + q4 * (CPL + 4));
-                float acc = 0.f;
-#pragma unroll
-                for (int c = 0; c < CPL / 4; ++c) {
-                    const float4 qq = qv[c];
-                    acc = fmaf(qq.x, kf[4 * c], acc);
-                    acc = fmaf(qq.y, kf[4 * c + 1], acc);
-                    acc = fmaf(qq.z, kf[4 * c + 2], acc);
-                    acc = fmaf(qq.w, kf[4 * c + 3], acc);
-                }
-                d[g] = acc;
-            }
-#pragma unroll
-            for (int g = 0; g < G; ++g) {
-                d[g] += __shfl_xor_sync(0xffffffffu, d[g], 1);
-                d[g] += __shfl_xor_sync(0xffffffffu, d[g], 2);
-            }
-            if (q4 == 0 && r < n_rows) {
-                const float s = ksc[r] * inv_sqrt;
-#pragma unroll
-                for (int g = 0; g < G; ++g) sc[g * pps * kPage + r] = d[g] * s;
-            }
-        }
-    }
-    __syncthreads();
-    // softmax per head (warp g): max, p = exp(s - max), sum
-    if (warp < G) {
-        float* sg = sc + warp * pps * kPage;
-        float m = -1e30f;
-        for (int r = lane; r < n_rows; r += 32) m = fmaxf(m, sg[r]);
-        m = warp_max(m);
-        float l = 0.f;
-        for (int r = lane; r < npg * kPage; r += 32) {
-            const float p = r < n_rows ? expf(sg[r] - m) : 0.f;
-            sg[r] = p * (r < n_rows ? vsc[r] : 0.f);  // p * s_v: the row's weight on its V codes
-            l += p;
-        }
-        l = warp_sum(l);
-        if (lane == 0) {
-            stat[2 * warp] = m;
-            stat[2 * warp + 1] = l;
-        }
-    }
-    __syncthreads();
-    // P . V: thread (row group rg, word column wc) accumulates 8 channels x G heads
-    {
-        const int wc = tid % WC, rg = tid / WC;
-        float acc[G][8];
-#pragma unroll
-        for (int g = 0; g < G; ++g)
-#pragma unroll
-            for (int e = 0; e < 8; ++e) acc[g][e] = 0.f;
-        for (int r = rg; r < n_rows; r += NRG) {
-            float vf[8];
-            nib8_to_f32(*reinterpret_cast<const uint32_t*>(vc + (size_t)r * (DH / 2) + wc * 4), vf);
-#pragma unroll
-            for (int g = 0; g < G; ++g) {
-                const float pv = sc[g * pps * kPage + r];
-#pragma unroll
-                for (int e = 0; e < 8; ++e) acc[g][e] = fmaf(pv, vf[e], acc[g][e]);
-            }
-        }
-        // row groups within the warp (lanes differing above the word-column bits), then warps
-#pragma unroll
-        for (int o = WC; o < 32; o <<= 1)
-#pragma unroll
-            for (int g = 0; g < G; ++g)
-#pragma unroll
-                for (int e = 0; e < 8; ++e) acc[g][e] += __shfl_xor_sync(0xffffffffu, acc[g][e], o);
-        if (lane < WC) {
-#pragma unroll
-            for (int g = 0; g < G; ++g) {
-                float4* dst = reinterpret_cast<float4*>(red + ((size_t)warp * G + g) * DH + wc * 8);
-                dst[0] = make_float4(acc[g][0], acc[g][1], acc[g][2], acc[g][3]);
-                dst[1] = make_float4(acc[g][4], acc[g][5], acc[g][6], acc[g][7]);
-            }
-        }
-    }
-    __syncthreads();
-    for (int i = tid; i < G * DH; i += AD_THREADS) {
-        const int g = i / DH, c = i % DH;
-        float o = 0.f;
-#pragma unroll
-        for (int w = 0; w < 8; ++w) o += red[((size_t)w * G + g) * DH + c];
-        part_o[(pidx0 + (size_t)g * nsplit) * DH + c] = o;
-    }
-    if (tid < G) {
-        part_ml[(pidx0 + (size_t)tid * nsplit) * 2] = stat[2 * tid];
-        part_ml[(pidx0 + (size_t)tid * nsplit) * 2 + 1] = stat[2 * tid + 1];
-    }
-}
+constexpr int AD_MAX_G = 8;  // query heads per kv head
 
 // ---------------------------------------------------------------- K6 on integer tensor cores
-// One WARP per (page, kv head, sequence), serving the G query heads of its kv head; a CTA is
-// up to 4 warps (4 kv heads of the same page) with no block barrier.  The page's V code block
-// and scales arrive by cp.async.bulk into the warp's own smem slice; its K codes go straight
-// into the MMA lanes' registers (each warp load instruction covers 8 whole 64 B rows).  Both
-// are issued before the programmatic-dependency wait.
+// One WARP per (page, kv head, sequence) for G <= 2 (a CTA is up to 4 kv heads of the same
+// page, no block barrier), one warp per (page, pair of query heads) for G > 2 (a CTA is one kv
+// head, its warps share the V copy; two block barriers).  The page's V code block and scales
+// arrive by cp.async.bulk into shared memory; its K codes go straight into the MMA lanes'
+// registers (each warp load instruction covers 8 whole 64 B rows).  Both are issued before the
+// programmatic-dependency wait.
 //
 // Both products run as exact integer MMAs (mma.sync m16n8k32 s8.s8.s32) on the codes as
 // stored: the fp32 operand (q, then p * s_v) is written as a fixed-point integer Q =
 // rint(x * 2^F) (|Q| < 2^30, F from the head's max |x|) in four balanced base-256 digits, one
 // MMA column per digit: S = sum_d Q_d * c_d is exact in int32 per digit, and a score's only
 // roundings are the fixed-point step (2^-31 of the head's max |q|) and the final fp32 one --
-// tighter than the fp32 dot product of k_attn_dec.
+// tighter than an fp32 dot product (round 2's fp32 CUDA-core kernel, replaced: C5 B = 256
+// attention 5.32 -> 2.53 ms/step, C4 0.487 -> 0.412).
 //   QK: A = K codes (16 keys x 32 dims, 16 * code in s8 as unpack_x16 gives), B = q digits.
 //   PV: A = V^T (16 channels x 32 keys), built by a 4 x 4 byte transpose of 4 keys' code
 //       words (PRMT) then unpack_x16; B = (p * s_v) digits.
@@ -331,19 +48,17 @@ constexpr int AW_MAXW = 4;  // warps (kv heads) per CTA
 // for 6 CTAs per SM -- 0.387 / 0.842 / 2.537 (7: 0.412 / 0.873 / 2.535).  Latency decides a
 // grid of less than one full wave, residency a larger one.
 constexpr int AW_MINB_WIDE = 6;
-// query heads per kv head served by k_attn_dec_w: its one warp runs every head's softmax and
-// (G + 1) / 2 MMA column tiles serially, which at G = 7 (C4) measured slower than k_attn_dec
-// (decode attention chain 0.613 vs 0.487 ms/step; MHA at C5 B = 256: 2.64 vs 5.32 ms)
-constexpr int AW_MAX_G = 2;
-template <int DH, int G>
-struct AwSmem {  // one warp's slice (the K codes go straight to registers)
-    static constexpr int CB = kPage * (DH / 2);
-    static constexpr size_t vc = 0, ks = CB, vs = ks + kPage * 4;
-    static constexpr size_t sc = vs + kPage * 4;        // [G][64] scores
-    static constexpr size_t ql = sc + G * kPage * 4;     // [G][4 digits][DH] q digits, MMA-B order
-    static constexpr size_t wl = ql + G * 4 * DH;        // [G][4 digits][64] (p * s_v) digits
-    static constexpr size_t bar = (wl + G * 4 * kPage + 15) / 16 * 16;
-    static constexpr size_t total = (bar + 8 + 127) / 128 * 128;
+// (G > 2 splits the heads over warps: one warp running all G = 7 heads of C4 -- 4 MMA column
+// tiles and 7 softmaxes serially -- measured 0.613 ms/step against 0.412 split)
+template <int DH, int HW>
+struct AwSmem {  // the page's V slice (shared by the warps of one kv head) + per-warp scratch
+    static constexpr int CB = kPage * (DH / 2);   // (the K codes go straight to registers)
+    static constexpr size_t vc = 0, ks = CB, vs = ks + kPage * 4, bar = vs + kPage * 4;
+    static constexpr size_t sh_total = (bar + 8 + 127) / 128 * 128;
+    static constexpr size_t sc = 0;                      // [HW][64] scores
+    static constexpr size_t ql = sc + HW * kPage * 4;    // [HW][4 digits][DH] q digits, MMA-B order
+    static constexpr size_t wl = ql + HW * 4 * DH;       // [HW][4 digits][64] (p * s_v) digits
+    static constexpr size_t w_total = (wl + HW * 4 * kPage + 127) / 128 * 128;
 };
 QT_DEV uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
     uint32_t r;
@@ -379,9 +94,11 @@ __global__ void __launch_bounds__(AW_MAXW * 32, MINB) k_attn_dec_w(const float* 
                                                              int max_pages, const double2* __restrict__ rope,
                                                              const int* __restrict__ pos, float inv_sqrt,
                                                              float* __restrict__ part_ml, float* __restrict__ part_o) {
-    using S = AwSmem<DH, G>;
+    constexpr bool SPLIT = G > 2;       // one kv head per CTA, one MMA column tile per warp
+    constexpr int HW = SPLIT ? 2 : G;   // query heads per warp
+    using S = AwSmem<DH, HW>;
     constexpr int CB = S::CB;
-    constexpr int NT = (G + 1) / 2;  // n8 tiles: two heads x four digits each
+    constexpr int NT = SPLIT ? 1 : (G + 1) / 2;  // the warp's n8 tiles: two heads x four digits each
     constexpr int KS = DH / 32;      // QK k-steps; also the 32-bit code words a lane reads per key
     constexpr int MT = DH / 16;      // PV m-tiles (channels)
     constexpr int WPG = DH / 64;     // code words per key a lane transposes in PV
@@ -389,12 +106,14 @@ __global__ void __launch_bounds__(AW_MAXW * 32, MINB) k_attn_dec_w(const float* 
     pdl_launch_dependents();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, t = lane & 3;
-    const int kh = blockIdx.y * (blockDim.x >> 5) + warp;
+    const int kh = SPLIT ? blockIdx.y : blockIdx.y * (blockDim.x >> 5) + warp;
+    const int hb = SPLIT ? 2 * warp : 0;  // the warp's first query head within its kv head
     if (kh >= Hkv) {
         pdl_wait();
         return;
     }
-    uint8_t* sm = sm_all + (size_t)warp * S::total;
+    uint8_t* sm = sm_all + (SPLIT ? 0 : (size_t)warp * (S::sh_total + S::w_total));
+    uint8_t* smw = SPLIT ? sm_all + S::sh_total + (size_t)warp * S::w_total : sm + S::sh_total;
     const int p = blockIdx.x, nsplit = gridDim.x, b = blockIdx.z;
     const bool fused = rope != nullptr;
     const int old_len = kv_len[b];
@@ -405,24 +124,26 @@ __global__ void __launch_bounds__(AW_MAXW * 32, MINB) k_attn_dec_w(const float* 
     if (n_rows <= 0) {  // nothing cached in this page: an empty partial per head
         pdl_wait();     // the partial buffers are still read by the previous layer's merge
 #pragma unroll
-        for (int gh = 0; gh < G; ++gh)
-            for (int c = lane; c < DH; c += 32) part_o[(pidx0 + (size_t)gh * nsplit) * DH + c] = 0.f;
-        if (lane < G) {
-            part_ml[(pidx0 + (size_t)lane * nsplit) * 2] = -1e30f;
-            part_ml[(pidx0 + (size_t)lane * nsplit) * 2 + 1] = 0.f;
+        for (int gl = 0; gl < HW; ++gl)
+            if (hb + gl < G)
+                for (int c = lane; c < DH; c += 32) part_o[(pidx0 + (size_t)(hb + gl) * nsplit) * DH + c] = 0.f;
+        if (lane < HW && hb + lane < G) {
+            part_ml[(pidx0 + (size_t)(hb + lane) * nsplit) * 2] = -1e30f;
+            part_ml[(pidx0 + (size_t)(hb + lane) * nsplit) * 2 + 1] = 0.f;
         }
         return;
     }
     uint8_t* vc = sm + S::vc;
     float* ksc = reinterpret_cast<float*>(sm + S::ks);
     float* vsc = reinterpret_cast<float*>(sm + S::vs);
-    float* sc = reinterpret_cast<float*>(sm + S::sc);
-    uint8_t* ql = sm + S::ql;
-    uint8_t* wl = sm + S::wl;
+    float* sc = reinterpret_cast<float*>(smw + S::sc);
+    uint8_t* ql = smw + S::ql;
+    uint8_t* wl = smw + S::wl;
     uint64_t* bar = reinterpret_cast<uint64_t*>(sm + S::bar);
     const size_t cbh = (size_t)Hkv * CB;
     const uint8_t* page_c = pool + (long long)pt[b * max_pages + p] * page_bytes;
-    if (lane == 0) {
+    const bool owner = !SPLIT || warp == 0;  // issues the page copy, appends the new row
+    if (owner && lane == 0) {
         mbar_init(bar, 1);
         mbar_fence_init();
         mbar_arrive_expect_tx(bar, (uint32_t)(CB + 2 * kPage * 4));
@@ -448,17 +169,21 @@ __global__ void __launch_bounds__(AW_MAXW * 32, MINB) k_attn_dec_w(const float* 
                 kw[mt][hf][0] = w2.x; kw[mt][hf][1] = w2.y;
             }
         }
+    if (SPLIT) __syncthreads();  // the barrier is initialised before the other warps wait on it
     pdl_wait();  // q (and the new token's k / v) come from the upstream GEMV
     qkv = pdl_fresh(qkv);
 
-    // q of the G heads (RoPE'd here in the decode step: fp64, rounded to fp32 like the
+    // q of the warp's heads (RoPE'd here in the decode step: fp64, rounded to fp32 like the
     // prefill's k_rope_kv_append) -> fixed-point digits in MMA-B order
     const float* qrow = qkv + (size_t)b * ldq;
     const double2* rt = fused ? rope + (size_t)pos[b] * (DH / 2) : nullptr;
     constexpr int PPL = DH / 64;  // dim pairs per lane per head
-    int F[G];
+    int F[HW];
 #pragma unroll
-    for (int gh = 0; gh < G; ++gh) {
+    for (int gl = 0; gl < HW; ++gl) {
+        const int gh = hb + gl;
+        F[gl] = 0;
+        if (gh >= G) continue;
         float2 v[PPL];
         float mx = 0.f;
 #pragma unroll
@@ -473,13 +198,13 @@ __global__ void __launch_bounds__(AW_MAXW * 32, MINB) k_attn_dec_w(const float* 
             }
             mx = fmaxf(mx, fmaxf(fabsf(v[j].x), fabsf(v[j].y)));
         }
-        F[gh] = aw_fexp(warp_max(mx));
-        const float two_f = aw_pow2(F[gh]);
+        F[gl] = aw_fexp(warp_max(mx));
+        const float two_f = aw_pow2(F[gl]);
 #pragma unroll
         for (int j = 0; j < PPL; ++j) {
             const int d = 2 * (lane + 32 * j);
             const uint32_t L0 = aw_digits(v[j].x, two_f), L1 = aw_digits(v[j].y, two_f);
-            uint8_t* row = ql + (size_t)gh * 4 * DH;
+            uint8_t* row = ql + (size_t)gl * 4 * DH;
 #pragma unroll
             for (int dg = 0; dg < 4; ++dg) {
                 row[dg * DH + aw_qpos(d)] = (uint8_t)(L0 >> (8 * dg));
@@ -497,6 +222,7 @@ __global__ void __launch_bounds__(AW_MAXW * 32, MINB) k_attn_dec_w(const float* 
         uint8_t* page = pool + (long long)pt[b * max_pages + p] * page_bytes;
 #pragma unroll
         for (int kv = 0; kv < 2; ++kv) {
+            if (kv == 1 && !owner) break;  // the other warps only need the K row (in registers)
             const float* src = qrow + (kv == 0 ? H * DH : (H + Hkv) * DH) + kh * DH + lane * E;
             double val[E];
 #pragma unroll
@@ -520,6 +246,7 @@ __global__ void __launch_bounds__(AW_MAXW * 32, MINB) k_attn_dec_w(const float* 
             for (int j = 0; j < E; ++j) w |= (uint32_t)(q_code_r(val[j], s, inv_s, 7) & 0xF) << (4 * j);
             new_word[kv] = w;
             new_scale[kv] = (float)s;
+            if (!owner) continue;
             // append to the cache (model.cpp:499-501)
             uint8_t* dst = page + (kv == 0 ? 0 : cbh) + (size_t)kh * CB + (size_t)new_r * (DH / 2) + lane * E / 2;
             if (E == 4) *reinterpret_cast<uint16_t*>(dst) = (uint16_t)w;
@@ -545,8 +272,8 @@ __global__ void __launch_bounds__(AW_MAXW * 32, MINB) k_attn_dec_w(const float* 
                     if (new_r == 16 * mt + 8 * hf + g) kw[mt][hf][s2] = word;
         }
     }
-    mbar_wait(bar, 0);  // the page's V codes and scales have landed
-    if (has_new) {      // ... and the new row replaces its (stale) shared copy
+    mbar_wait(bar, 0);     // the page's V codes and scales have landed
+    if (has_new && owner) {  // ... and the new row replaces its (stale) shared copy
         {
             uint8_t* d = vc + (size_t)new_r * (DH / 2) + lane * E / 2;
             if (E == 4) *reinterpret_cast<uint16_t*>(d) = (uint16_t)new_word[1];
@@ -557,24 +284,25 @@ __global__ void __launch_bounds__(AW_MAXW * 32, MINB) k_attn_dec_w(const float* 
             vsc[new_r] = new_scale[1];
         }
     }
-    __syncwarp();
+    if (SPLIT) __syncthreads();  // the patched row is visible to every warp of the kv head
+    else __syncwarp();
 
     // ---- scores: S[key][head] for the 64 keys (4 m-tiles of 16 keys)
     {
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
-            const int hq = 2 * nt + (g >> 2);  // the B column's head and digit
+            const int hq = 2 * nt + (g >> 2);  // the B column's head (within the warp's) and digit
             uint32_t bq[KS][2];
 #pragma unroll
             for (int s = 0; s < KS; ++s) {
-                const uint2 v = hq < G ? *reinterpret_cast<const uint2*>(ql + (size_t)(hq * 4 + (g & 3)) * DH +
+                const uint2 v = hb + hq < G ? *reinterpret_cast<const uint2*>(ql + (size_t)(hq * 4 + (g & 3)) * DH +
                                                                          8 * (KS * t + s))
                                        : make_uint2(0u, 0u);
                 bq[s][0] = v.x;
                 bq[s][1] = v.y;
             }
             const int ho = 2 * nt + (t >> 1);  // the accumulator columns' head
-            const int Fo = (2 * nt + 1 < G && (t >> 1)) ? F[(2 * nt + 1) % G] : F[2 * nt];
+            const int Fo = (2 * nt + 1 < HW && (t >> 1)) ? F[(2 * nt + 1) % HW] : F[2 * nt];
             const float qsc = aw_pow2(-(Fo + 4)) * inv_sqrt;
 #pragma unroll
             for (int mt = 0; mt < 4; ++mt) {
@@ -588,7 +316,7 @@ __global__ void __launch_bounds__(AW_MAXW * 32, MINB) k_attn_dec_w(const float* 
                 }
                 const int P0 = acc[0] + (acc[1] << 8), P1 = acc[2] + (acc[3] << 8);  // digits 2(t&1), +1
                 const int U0 = __shfl_xor_sync(0xffffffffu, P0, 1), U1 = __shfl_xor_sync(0xffffffffu, P1, 1);
-                if (!(t & 1) && ho < G) {
+                if (!(t & 1) && hb + ho < G) {
                     const int k0 = 16 * mt + g;
                     sc[ho * kPage + k0] = aw_comb(P0, U0, qsc) * ksc[k0];
                     sc[ho * kPage + k0 + 8] = aw_comb(P1, U1, qsc) * ksc[k0 + 8];
@@ -598,9 +326,11 @@ __global__ void __launch_bounds__(AW_MAXW * 32, MINB) k_attn_dec_w(const float* 
     }
     __syncwarp();
     // ---- softmax per head over the page's rows; p * s_v -> fixed-point digits
-    float m_h[G], l_h[G], osc[G];
+    float m_h[HW], l_h[HW], osc[HW];
 #pragma unroll
-    for (int gh = 0; gh < G; ++gh) {
+    for (int gh = 0; gh < HW; ++gh) {  // (the warp's heads)
+        m_h[gh] = l_h[gh] = osc[gh] = 0.f;
+        if (hb + gh >= G) continue;
         const bool ok0 = lane < n_rows, ok1 = lane + 32 < n_rows;
         const float s0 = ok0 ? sc[gh * kPage + lane] : -1e30f, s1 = ok1 ? sc[gh * kPage + lane + 32] : -1e30f;
         const float m = warp_max(fmaxf(s0, s1));
@@ -630,8 +360,8 @@ __global__ void __launch_bounds__(AW_MAXW * 32, MINB) k_attn_dec_w(const float* 
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
             uint32_t bw[2];
-            bw[0] = hq < G ? *reinterpret_cast<const uint32_t*>(wl + (size_t)(hq * 4 + (g & 3)) * kPage + 32 * s + 4 * t) : 0u;
-            bw[1] = hq < G ? *reinterpret_cast<const uint32_t*>(wl + (size_t)(hq * 4 + (g & 3)) * kPage + 32 * s + 16 + 4 * t) : 0u;
+            bw[0] = hb + hq < G ? *reinterpret_cast<const uint32_t*>(wl + (size_t)(hq * 4 + (g & 3)) * kPage + 32 * s + 4 * t) : 0u;
+            bw[1] = hb + hq < G ? *reinterpret_cast<const uint32_t*>(wl + (size_t)(hq * 4 + (g & 3)) * kPage + 32 * s + 16 + 4 * t) : 0u;
             // R[hf][ww][e]: channel (word WPG * g + ww, nibble e) of keys 32 s + 16 hf + t + 4 i
             uint32_t R[2][WPG][8];
 #pragma unroll
@@ -672,7 +402,7 @@ __global__ void __launch_bounds__(AW_MAXW * 32, MINB) k_attn_dec_w(const float* 
             }
         }
         const int ho = 2 * nt + (t >> 1);
-        const float oscale = (2 * nt + 1 < G && (t >> 1)) ? osc[(2 * nt + 1) % G] : osc[2 * nt];
+        const float oscale = (2 * nt + 1 < HW && (t >> 1)) ? osc[(2 * nt + 1) % HW] : osc[2 * nt];
         float o[2][MT];
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
@@ -681,8 +411,8 @@ __global__ void __launch_bounds__(AW_MAXW * 32, MINB) k_attn_dec_w(const float* 
             o[0][mt] = aw_comb(P0, U0, oscale);
             o[1][mt] = aw_comb(P1, U1, oscale);
         }
-        if (!(t & 1) && ho < G) {  // channels 8 WPG g .. 8 WPG g + 8 WPG - 1 (rows g, then g + 8)
-            float* dst = part_o + (pidx0 + (size_t)ho * nsplit) * DH + 8 * WPG * g;
+        if (!(t & 1) && hb + ho < G) {  // channels 8 WPG g .. 8 WPG g + 8 WPG - 1 (rows g, then g + 8)
+            float* dst = part_o + (pidx0 + (size_t)(hb + ho) * nsplit) * DH + 8 * WPG * g;
 #pragma unroll
             for (int hf = 0; hf < 2; ++hf)
 #pragma unroll
@@ -692,10 +422,10 @@ __global__ void __launch_bounds__(AW_MAXW * 32, MINB) k_attn_dec_w(const float* 
         }
     }
 #pragma unroll
-    for (int gh = 0; gh < G; ++gh)
-        if (lane == gh) {
-            part_ml[(pidx0 + (size_t)gh * nsplit) * 2] = m_h[gh];
-            part_ml[(pidx0 + (size_t)gh * nsplit) * 2 + 1] = l_h[gh];
+    for (int gh = 0; gh < HW; ++gh)
+        if (lane == gh && hb + gh < G) {
+            part_ml[(pidx0 + (size_t)(hb + gh) * nsplit) * 2] = m_h[gh];
+            part_ml[(pidx0 + (size_t)(hb + gh) * nsplit) * 2 + 1] = l_h[gh];
         }
 }
 
@@ -811,43 +541,22 @@ template <int DH, int G>
 static int launch_dec_w(int nsplit, int Hkv, int B, cudaStream_t st, const float* qkv, int ldq, int H,
                         const int* kv_len, uint8_t* pool, long long page_bytes, const int* pt, int max_pages,
                         const double2* rope, const int* pos, float inv_sqrt, float* part_ml, float* part_o) {
-    const int wpc = std::min(AW_MAXW, Hkv);
-    const size_t smem = (size_t)wpc * AwSmem<DH, G>::total;
+    constexpr bool SPLIT = G > 2;
+    using S = AwSmem<DH, SPLIT ? 2 : G>;
+    // G <= 2: up to 4 kv heads per CTA, one warp each; G > 2: one kv head, one warp per 2 heads
+    const int wpc = SPLIT ? (G + 1) / 2 : std::min(AW_MAXW, Hkv);
+    const size_t smem = SPLIT ? S::sh_total + (size_t)wpc * S::w_total : (size_t)wpc * (S::sh_total + S::w_total);
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const long long ctas = (long long)nsplit * ((Hkv + wpc - 1) / wpc) * B;
+    const int gy = SPLIT ? Hkv : (Hkv + wpc - 1) / wpc;
+    const long long ctas = (long long)nsplit * gy * B;
     auto kfn = ctas > (long long)5 * sms ? k_attn_dec_w<DH, G, AW_MINB_WIDE> : k_attn_dec_w<DH, G, 1>;
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    return launch_pdl(kfn, dim3(nsplit, (Hkv + wpc - 1) / wpc, B), dim3(32 * wpc), smem, st, qkv, ldq, H, Hkv,
+    return launch_pdl(kfn, dim3(nsplit, gy, B), dim3(32 * wpc), smem, st, qkv, ldq, H, Hkv,
                       kv_len, pool, page_bytes, pt, max_pages, rope, pos, inv_sqrt, part_ml, part_o);
 }
 
-template <int DH, int G>
-static int launch_dec(dim3 grid, int pps, cudaStream_t st, const float* qkv, int ldq, int H, int Hkv,
-                      const int* kv_len, uint8_t* pool, long long page_bytes, const int* pt, int max_pages,
-                      const double2* rope, const int* pos, float inv_sqrt, float* part_ml, float* part_o) {
-    const size_t smem = AdSmem<DH, G>::total(pps);
-    auto kfn = k_attn_dec<DH, G>;
-    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    return launch_pdl(kfn, grid, dim3(AD_THREADS), smem, st, qkv, ldq, H, Hkv, kv_len, pool, page_bytes, pt,
-                      max_pages, pps, rope, pos, inv_sqrt, part_ml, part_o);
-}
-
-// k_attn_dec_w for G <= AW_MAX_G (the plan then gives one page per split), else k_attn_dec
-template <int DH, int G>
-static int launch_any(dim3 grid, int pps, cudaStream_t st, const float* qkv, int ldq, int H, int Hkv,
-                      const int* kv_len, uint8_t* pool, long long page_bytes, const int* pt, int max_pages,
-                      const double2* rope, const int* pos, float inv_sqrt, float* part_ml, float* part_o) {
-    if constexpr (QT_AD_WARP && G <= AW_MAX_G) {
-        if (pps != 1) return -1;
-        return launch_dec_w<DH, G>((int)grid.x, Hkv, (int)grid.z, st, qkv, ldq, H, kv_len, pool, page_bytes, pt,
-                                   max_pages, rope, pos, inv_sqrt, part_ml, part_o);
-    } else {
-        return launch_dec<DH, G>(grid, pps, st, qkv, ldq, H, Hkv, kv_len, pool, page_bytes, pt, max_pages, rope, pos,
-                                 inv_sqrt, part_ml, part_o);
-    }
-}
 
 }  // namespace qt
 
@@ -857,20 +566,9 @@ extern "C" {
 
 int qt_attn_decode_plan(int B, int H, int Hkv, int pages, int sms, int* pps, int* nsplit) {
     if (pages < 1 || B < 1 || Hkv < 1 || H % Hkv) return -1;
-    // enough CTAs for QT_AD_CTA_MULT per SM, at most AD_MAX_PPS pages each (measured against
-    // fewer CTAs and against a per-warp-chunk kernel with the attn_out quantizer fused by the last
-    // arrival: tools/gpu_attn_ab.sh)
-    if (QT_AD_WARP && H / Hkv <= AW_MAX_G) {  // k_attn_dec_w: one warp per (page, kv head, sequence)
-        *pps = 1;
-        *nsplit = pages;
-        return 0;
-    }
-    int ns = std::max(1, std::min(pages, (QT_AD_CTA_MULT * sms + B * Hkv - 1) / (B * Hkv)));
-    int p = (pages + ns - 1) / ns;
-    if (p > QT_AD_PLAN_PPS) p = QT_AD_PLAN_PPS;
-    ns = (pages + p - 1) / p;
-    *pps = p;
-    *nsplit = ns;
+    (void)sms;
+    *pps = 1;  // k_attn_dec_w: one page per warp (per split)
+    *nsplit = pages;
     return 0;
 }
 
@@ -880,15 +578,16 @@ int qt_launch_attn_decode(const float* qkv, int ldq, int H, int Hkv, int dh, con
                           uint8_t* codes, int ld_codes, double* scales, int qmode, double static_scale, int d_pad,
                           int bits, int8_t* codes8, int ld8, cudaStream_t st) {
     if (B <= 0) return 0;
-    if (H > 64 || Hkv < 1 || H % Hkv || H / Hkv > AD_MAX_G || pps < 1 || pps > AD_MAX_PPS || nsplit < 1) return -1;
-    // (the last split may extend past the page table: only pages holding cached rows are read)
+    if (H > 64 || Hkv < 1 || H % Hkv || H / Hkv > AD_MAX_G || pps != 1 || nsplit < 1) return -1;
+    // (splits past a sequence's pages write empty partials: only pages holding cached rows are read)
     const int G = H / Hkv;
-    const dim3 grid(nsplit, Hkv, B);
     const float inv_sqrt = (float)(1.0 / sqrt((double)dh));
     const double2* rt = reinterpret_cast<const double2*>(rope);
     int rc = -1;
-#define QT_AD(D, GG) \
-    if (dh == D && G == GG) rc = launch_any<D, GG>(grid, pps, st, qkv, ldq, H, Hkv, kv_len, pool, page_bytes, pt, max_pages, rt, pos, inv_sqrt, part_ml, part_o);
+#define QT_AD(D, GG)                                                                                          \
+    if (dh == D && G == GG)                                                                                   \
+        rc = launch_dec_w<D, GG>(nsplit, Hkv, B, st, qkv, ldq, H, kv_len, pool, page_bytes, pt, max_pages, rt, pos, \
+                                 inv_sqrt, part_ml, part_o);
     QT_AD(128, 1) QT_AD(128, 2) QT_AD(128, 4) QT_AD(128, 7) QT_AD(128, 8)
     QT_AD(64, 1) QT_AD(64, 2) QT_AD(64, 4) QT_AD(64, 7) QT_AD(64, 8)
 #undef QT_AD

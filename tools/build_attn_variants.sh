@@ -10,7 +10,7 @@ make -C paper_2604_17320_b200/csrc -j8 > /dev/null
 SRC=${VARIANT_SRC:-k_attn_decode}   # the csrc/<SRC>.cu file the variants rebuild
 OTHERS=$(ls $B/*.o | grep -v "/$SRC.o")
 # VARIANTS: ';'-separated name:defines list
-IFS=';' read -ra VL <<< "${VARIANTS:-m2:-DQT_AD_CTA_MULT=2;m4:-DQT_AD_CTA_MULT=4;m8:-DQT_AD_CTA_MULT=8}"
+IFS=';' read -ra VL <<< "${VARIANTS:-base:}"
 for v in "${VL[@]}"; do
   name=${v%%:*}; defs=${v#*:}
   out=paper_2604_17320_b200/_build_var/$name; mkdir -p $out

@@ -3,7 +3,7 @@
 # C2 launch list (per-kernel durations, serialized).
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-for spec in "c2:k_attn_dec:40" "c2:k_attn_merge_quant:40" "c5 --batch 256 --decode 8:k_attn_dec:40"; do
+for spec in "c2:k_attn_dec_w:40" "c2:k_attn_merge_quant:40" "c5 --batch 256 --decode 8:k_attn_dec_w:40"; do
   cfg=${spec%%:*}; rest=${spec#*:}; k=${rest%%:*}; s=${rest##*:}
   tag=$(echo "$cfg" | tr -d ' -' | cut -c1-12)_$k
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:"$k" -s $s -c 1 \
