@@ -21,7 +21,7 @@ done
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file gpurun_out/${T}_launches_c2.csv \
   python bench.py --steps 1 --warmup 0 --no-cpu-baseline --eager-decode > /dev/null 2>&1; echo "launch list rc $?"
 python tools/ncu_summary.py gpurun_out/${T}_launches_c2.csv > gpurun_out/${T}_launch_summary.txt; head -40 gpurun_out/${T}_launch_summary.txt
-for spec in "c2:k_gemv_reg:65:gemv" "c2:k_attn_dec_w:40:attn_dec" "c2:k_gemm_tc05_i8:2:gemm_i8" "c2:k_attn_prefill_ws:3:attn_prefill" "c2:k_norm_quant_st:70:norm_quant_st" "c2:k_attn_merge_quant:40:attn_merge" "c5 --batch 256 --decode 8:k_attn_dec_w:40:attn_dec_b256"; do
+for spec in "c2:k_gemv_reg:65:gemv" "c2:k_attn_dec_w:40:attn_dec" "c2:k_gemm_tc05_i8:2:gemm_i8" "c2:k_attn_prefill_ws:3:attn_prefill" "c2:k_norm_quant4:70:norm_quant4" "c2:k_attn_merge_quant:40:attn_merge" "c5 --batch 256 --decode 8:k_attn_dec_w:40:attn_dec_b256"; do
   IFS=':' read -r cfg k s name <<< "$spec"
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:"$k" -s $s -c 1 \
     -o gpurun_out/${T}_ncu_$name -f python bench.py --config $cfg --steps 1 --warmup 0 --no-cpu-baseline --eager-decode > gpurun_out/${T}_ncu_$name.log 2>&1
