@@ -169,6 +169,19 @@ __global__ void __launch_bounds__(AW_MAXW * 32, MINB) k_attn_dec_w(const float* 
                 kw[mt][hf][0] = w2.x; kw[mt][hf][1] = w2.y;
             }
         }
+    // the RoPE cos / sin of the lane's q pairs and new-K pairs (the table and the position are
+    // final before the upstream chain): loaded before the wait, off the q -> RoPE path
+    constexpr int PPL = DH / 64;  // dim pairs per lane per head
+    constexpr int E = DH / 32;
+    // (ld.global.cg: an invariant .nc load is scheduled below the wait by the compiler / ptxas)
+    double2 cq[PPL], ckr[E / 2];
+    if (fused) {
+        const double2* rt = rope + (size_t)pos[b] * (DH / 2);
+#pragma unroll
+        for (int j = 0; j < PPL; ++j) cq[j] = __ldcg(rt + lane + 32 * j);
+#pragma unroll
+        for (int j = 0; j < E / 2; ++j) ckr[j] = __ldcg(rt + lane * E / 2 + j);
+    }
     if (SPLIT) __syncthreads();  // the barrier is initialised before the other warps wait on it
     pdl_wait();  // q (and the new token's k / v) come from the upstream GEMV
     qkv = pdl_fresh(qkv);
@@ -176,8 +189,6 @@ __global__ void __launch_bounds__(AW_MAXW * 32, MINB) k_attn_dec_w(const float* 
     // q of the warp's heads (RoPE'd here in the decode step: fp64, rounded to fp32 like the
     // prefill's k_rope_kv_append) -> fixed-point digits in MMA-B order
     const float* qrow = qkv + (size_t)b * ldq;
-    const double2* rt = fused ? rope + (size_t)pos[b] * (DH / 2) : nullptr;
-    constexpr int PPL = DH / 64;  // dim pairs per lane per head
     int F[HW];
 #pragma unroll
     for (int gl = 0; gl < HW; ++gl) {
@@ -191,7 +202,7 @@ __global__ void __launch_bounds__(AW_MAXW * 32, MINB) k_attn_dec_w(const float* 
             const int pr = lane + 32 * j;
             v[j] = *reinterpret_cast<const float2*>(qrow + (size_t)(kh * G + gh) * DH + 2 * pr);
             if (fused) {
-                const double2 cs = rt[pr];
+                const double2 cs = cq[j];
                 const double a = v[j].x, bb = v[j].y;
                 v[j].x = (float)__dsub_rn(__dmul_rn(a, cs.x), __dmul_rn(bb, cs.y));
                 v[j].y = (float)__dadd_rn(__dmul_rn(a, cs.y), __dmul_rn(bb, cs.x));
@@ -215,7 +226,6 @@ __global__ void __launch_bounds__(AW_MAXW * 32, MINB) k_attn_dec_w(const float* 
     // the new row (decode step): its K (RoPE'd) then its V -- kv_quantize in fp64, appended
     const int new_r = old_len - r0;  // row within this page
     const bool has_new = fused && new_r >= 0 && new_r < n_rows;
-    constexpr int E = DH / 32;
     uint32_t new_word[2] = {0u, 0u};
     float new_scale[2] = {0.f, 0.f};
     if (has_new) {
@@ -230,7 +240,7 @@ __global__ void __launch_bounds__(AW_MAXW * 32, MINB) k_attn_dec_w(const float* 
             if (kv == 0) {
 #pragma unroll
                 for (int j = 0; j < E; j += 2) {
-                    const double2 cs = rt[(lane * E + j) / 2];
+                    const double2 cs = ckr[j / 2];
                     const double a = val[j], bb = val[j + 1];
                     val[j] = __dsub_rn(__dmul_rn(a, cs.x), __dmul_rn(bb, cs.y));
                     val[j + 1] = __dadd_rn(__dmul_rn(a, cs.y), __dmul_rn(bb, cs.x));

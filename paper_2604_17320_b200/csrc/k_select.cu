@@ -251,15 +251,30 @@ __global__ void __launch_bounds__(256) k_greedy_next(const float* __restrict__ l
     __shared__ int s_tok;
     pdl_launch_dependents();
     pdl_wait();  // the logits come from the previous step's head GEMV
+    logits = pdl_fresh(logits);
     const int b = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const float* lg = logits + (size_t)b * ld;
     float bv = -INFINITY;
     int bi = 0x7fffffff;
-    for (int i = threadIdx.x; i < vocab; i += blockDim.x) {
-        const float v = lg[i];
-        if (v > bv) {  // strided ascending scan: the first maximum of this thread's indices
-            bv = v;
-            bi = i;
+    if ((vocab & 3) == 0 && (ld & 3) == 0) {
+        // 4 consecutive logits per load, 4 loads in flight per thread before the compares (the
+        // scalar loop waited one L2 round trip per element); ascending indices per thread, so
+        // the strict > keeps the first maximum
+#pragma unroll 4
+        for (int i = threadIdx.x * 4; i < vocab; i += blockDim.x * 4) {
+            const float4 v = *reinterpret_cast<const float4*>(lg + i);
+            if (v.x > bv) { bv = v.x; bi = i; }
+            if (v.y > bv) { bv = v.y; bi = i + 1; }
+            if (v.z > bv) { bv = v.z; bi = i + 2; }
+            if (v.w > bv) { bv = v.w; bi = i + 3; }
+        }
+    } else {
+        for (int i = threadIdx.x; i < vocab; i += blockDim.x) {
+            const float v = lg[i];
+            if (v > bv) {  // strided ascending scan: the first maximum of this thread's indices
+                bv = v;
+                bi = i;
+            }
         }
     }
 #pragma unroll
