@@ -13,6 +13,7 @@
 // unnormalised o) partial; k_attn_merge_quant merges the pages in fixed order and quantizes
 // the attn_out site.
 #include <algorithm>
+#include <type_traits>
 
 #include "qt_common.cuh"
 #include "qt_kernels.h"
@@ -471,19 +472,32 @@ __global__ void __launch_bounds__(1024) k_attn_merge_quant(const float* __restri
         if (npg <= 32) {
             // lane p holds split p's (m, l): one load per lane, then the loop only loads o
             // (independent of M, so it pipelines) and takes (m, l) by shuffle
+            // (o of up to 8 pages per batch as one vector load each, all issued together with
+            // the (m, l) load: one L2 round trip per 8 pages instead of one per 4 pages and
+            // channel; the accumulation order is unchanged)
+            using VecT = typename std::conditional<CPL == 4, float4, float2>::type;
             float2 mlv = make_float2(-1e30f, 0.f);
-            if (lane < npg) mlv = *reinterpret_cast<const float2*>(part_ml + (base + lane) * 2);
+            if (lane < npg) mlv = __ldcg(reinterpret_cast<const float2*>(part_ml + (base + lane) * 2));
+            constexpr int PB = 8;
+            VecT ov[PB];
+#pragma unroll
+            for (int j = 0; j < PB; ++j)
+                if (j < npg) ov[j] = __ldcg(reinterpret_cast<const VecT*>(part_o + (base + j) * DH + lane * CPL));
             M = warp_max(mlv.x);
-#pragma unroll 4
-            for (int p = 0; p < npg; ++p) {
-                float ov[CPL];
+            for (int p0 = 0; p0 < npg; p0 += PB) {
 #pragma unroll
-                for (int c = 0; c < CPL; ++c) ov[c] = part_o[(base + p) * DH + lane * CPL + c];
-                const float mp = __shfl_sync(0xffffffffu, mlv.x, p), lp = __shfl_sync(0xffffffffu, mlv.y, p);
-                const float a = lp == 0.f ? 0.f : expf(mp - M);
-                L += lp * a;
+                for (int j = 0; j < PB; ++j) {
+                    const int p = p0 + j;
+                    if (p >= npg) break;
+                    const float mp = __shfl_sync(0xffffffffu, mlv.x, p), lp = __shfl_sync(0xffffffffu, mlv.y, p);
+                    const float a = lp == 0.f ? 0.f : expf(mp - M);
+                    L += lp * a;
+                    const float* v = reinterpret_cast<const float*>(&ov[j]);
 #pragma unroll
-                for (int c = 0; c < CPL; ++c) o[hh][c] += ov[c] * a;
+                    for (int c = 0; c < CPL; ++c) o[hh][c] += v[c] * a;
+                    if (p + PB < npg)  // the next batch's page, into the slot just consumed
+                        ov[j] = __ldcg(reinterpret_cast<const VecT*>(part_o + (base + p + PB) * DH + lane * CPL));
+                }
             }
         } else {
             for (int p = lane; p < npg; p += 32) M = fmaxf(M, part_ml[(base + p) * 2]);
